@@ -1,0 +1,436 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product library.
+//
+// C-ABI shim over the UNMODIFIED reference library (header-only C++20,
+// /root/reference/proj/include/pact/*.hpp), compiled in place by
+// oracle/Makefile into oracle/_ref/libpact_ref.so.  It exists so that
+//   * the CPU restatement in oracle/pact_oracle.c can be pinned against the
+//     reference itself (tests/golden/ fixtures are generated through it), and
+//   * bench.py --impl reference can time the reference's own CPU path.
+// Every function forwards to the reference entry point named in its comment;
+// the only code here is argument marshalling (flat fp64 arrays <-> pact types).
+#include <chrono>
+#include <complex>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "pact/aberration.hpp"
+#include "pact/beamform.hpp"
+#include "pact/core.hpp"
+#include "pact/deconv.hpp"
+#include "pact/nfield.hpp"
+#include "pact/optimize.hpp"
+#include "pact/phantom.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const pact::ValidationError& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const pact::NumericalError& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+pact::GridSpec grid_of(int w, int h, double pitch, double ox, double oy) {
+  pact::GridSpec g;
+  g.width = w;
+  g.height = h;
+  g.pitch = pitch;
+  g.origin = {ox, oy};
+  return g;
+}
+
+pact::RasterGrid raster_of(const pact::GridSpec& g, const double* v) {
+  pact::RasterGrid r = pact::RasterGrid::zeros(g);
+  std::memcpy(r.values.data(), v, sizeof(double) * r.values.size());
+  return r;
+}
+
+pact::SignalSet signals_of(int n, double radius, double offset, int T, double dt, double t0,
+                           double v0, const double* data) {
+  pact::SignalSet s;
+  s.geom = {n, radius, offset};
+  s.n_samples = T;
+  s.dt = dt;
+  s.t0 = t0;
+  s.background_sos = v0;
+  s.data.assign(data, data + static_cast<size_t>(n) * T);
+  return s;
+}
+
+pact::SirenParams siren_of(int hidden, int layers, double omega0, double out_scale, double v0,
+                           const double* theta) {
+  pact::SirenParams p;
+  p.hidden = hidden;
+  p.n_hidden_layers = layers;
+  p.omega0 = omega0;
+  p.out_scale = out_scale;
+  p.v0 = v0;
+  p.theta.assign(theta, theta + p.param_count());
+  return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// das_stack, beamform.hpp:77-110
+int ref_das_stack(int n_tx, double radius, double offset, int T, double dt, double t0,
+                  const double* sig, int W, int H, double pitch, double ox, double oy, double v0,
+                  int K, const double* delays, int workers, double* out) {
+  return guarded([&] {
+    auto s = signals_of(n_tx, radius, offset, T, dt, t0, v0, sig);
+    auto st = pact::das_stack(s, grid_of(W, H, pitch, ox, oy), v0,
+                              std::vector<double>(delays, delays + K), workers);
+    size_t plane = static_cast<size_t>(W) * H;
+    for (int j = 0; j < K; ++j)
+      std::memcpy(out + j * plane, st.images[j].values.data(), sizeof(double) * plane);
+  });
+}
+
+// das, beamform.hpp:56-75
+int ref_das(int n_tx, double radius, double offset, int T, double dt, double t0,
+            const double* sig, int W, int H, double pitch, double ox, double oy, double v0,
+            double d, int workers, double* out) {
+  return guarded([&] {
+    auto s = signals_of(n_tx, radius, offset, T, dt, t0, v0, sig);
+    auto img = pact::das(s, grid_of(W, H, pitch, ox, oy), v0, d, workers);
+    std::memcpy(out, img.values.data(), sizeof(double) * img.values.size());
+  });
+}
+
+// init_siren, nfield.hpp:83-107
+int ref_init_siren(uint64_t seed, int hidden, int layers, double omega0, double out_scale,
+                   double v0, double* theta) {
+  return guarded([&] {
+    auto p = pact::init_siren(seed, hidden, layers, omega0, out_scale, v0);
+    std::memcpy(theta, p.theta.data(), sizeof(double) * p.theta.size());
+  });
+}
+
+long ref_siren_param_count(int hidden, int layers) {
+  return static_cast<long>(pact::siren_param_count(2, hidden, layers));
+}
+
+// render_sos, nfield.hpp:145-162 ; returns the masked-pixel count
+int ref_render_sos(int hidden, int layers, double omega0, double out_scale, double v0,
+                   const double* theta, int W, int H, double pitch, double ox, double oy,
+                   double mcx, double mcy, double mr, double* raster, int* n_masked) {
+  return guarded([&] {
+    auto p = siren_of(hidden, layers, omega0, out_scale, v0, theta);
+    auto f = pact::render_sos(p, grid_of(W, H, pitch, ox, oy), {{mcx, mcy}, mr});
+    std::memcpy(raster, f.raster.values.data(), sizeof(double) * f.raster.values.size());
+    if (n_masked) *n_masked = static_cast<int>(f.masked_indices.size());
+  });
+}
+
+// backprop_sos, nfield.hpp:166-233 ; grad_v is per masked pixel (row-major order)
+int ref_backprop_sos(int hidden, int layers, double omega0, double out_scale, double v0,
+                     const double* theta, int W, int H, double pitch, double ox, double oy,
+                     double mcx, double mcy, double mr, const double* grad_v, double* grad) {
+  return guarded([&] {
+    auto p = siren_of(hidden, layers, omega0, out_scale, v0, theta);
+    auto f = pact::render_sos(p, grid_of(W, H, pitch, ox, oy), {{mcx, mcy}, mr});
+    std::vector<double> g(grad_v, grad_v + f.masked_indices.size());
+    auto out = pact::backprop_sos(p, f, g);
+    std::memcpy(grad, out.data(), sizeof(double) * out.size());
+  });
+}
+
+// wavefront_profile, aberration.hpp:134-186 (for n_centers centres)
+int ref_wavefront_profile(int n_centers, const double* centers, int n_tx, double radius,
+                          double offset, int W, int H, double pitch, double ox, double oy,
+                          const double* sos, double v0, double mcx, double mcy, double mr,
+                          int n_angles, double step, double* w) {
+  return guarded([&] {
+    auto g = grid_of(W, H, pitch, ox, oy);
+    auto r = raster_of(g, sos);
+    for (int i = 0; i < n_centers; ++i) {
+      auto prof = pact::wavefront_profile({centers[2 * i], centers[2 * i + 1]},
+                                          {n_tx, radius, offset}, r, v0, {{mcx, mcy}, mr},
+                                          n_angles, step, false);
+      std::memcpy(w + static_cast<size_t>(i) * n_angles, prof.w.data(),
+                  sizeof(double) * n_angles);
+    }
+  });
+}
+
+// transfer_stack, aberration.hpp:236-265 ; H is interleaved complex [K][P][P]
+int ref_transfer_stack(int n_angles, const double* w, int K, const double* delays, int P,
+                       double pitch, double* H) {
+  return guarded([&] {
+    pact::WavefrontProfile prof;
+    prof.n_angles = n_angles;
+    prof.w.assign(w, w + n_angles);
+    auto ts = pact::transfer_stack(prof, std::vector<double>(delays, delays + K), P, pitch);
+    for (int j = 0; j < K; ++j)
+      std::memcpy(H + 2 * static_cast<size_t>(j) * P * P, ts.spectra[j].data(),
+                  sizeof(double) * 2 * P * P);
+  });
+}
+
+// make_patch_layout, core.hpp:252-281 ; returns P, stride, nx, ny, offsets, centres
+int ref_patch_layout(int W, int H, double pitch, double ox, double oy, double patch_mm,
+                     double overlap, int* info, int* offsets, double* centers) {
+  return guarded([&] {
+    auto lay = pact::make_patch_layout(grid_of(W, H, pitch, ox, oy), patch_mm, overlap);
+    info[0] = lay.patch_pixels;
+    info[1] = lay.stride_pixels;
+    info[2] = lay.nx;
+    info[3] = lay.ny;
+    if (offsets)
+      for (int i = 0; i < lay.n_patches(); ++i) {
+        offsets[2 * i] = lay.offsets[i].first;
+        offsets[2 * i + 1] = lay.offsets[i].second;
+      }
+    if (centers)
+      for (int i = 0; i < lay.n_patches(); ++i) {
+        centers[2 * i] = lay.centers[i].x;
+        centers[2 * i + 1] = lay.centers[i].y;
+      }
+  });
+}
+
+static pact::DasStack stack_of(int K, const double* delays, double v0, const pact::GridSpec& g,
+                               const double* stack) {
+  pact::DasStack st;
+  st.delays.assign(delays, delays + K);
+  st.v0 = v0;
+  size_t plane = static_cast<size_t>(g.width) * g.height;
+  for (int j = 0; j < K; ++j) st.images.push_back(raster_of(g, stack + j * plane));
+  return st;
+}
+
+// extract_patch_spectra, deconv.hpp:64-74 ; Y interleaved complex [patch][K][P][P]
+int ref_patch_spectra(int K, const double* delays, double v0, int W, int H, double pitch,
+                      double ox, double oy, const double* stack, double patch_mm,
+                      double overlap, int workers, double* Y) {
+  return guarded([&] {
+    auto g = grid_of(W, H, pitch, ox, oy);
+    auto st = stack_of(K, delays, v0, g, stack);
+    auto lay = pact::make_patch_layout(g, patch_mm, overlap);
+    auto ps = pact::extract_patch_spectra(st, lay, workers);
+    size_t P2 = static_cast<size_t>(lay.patch_pixels) * lay.patch_pixels;
+    for (size_t i = 0; i < ps.size(); ++i)
+      for (int j = 0; j < K; ++j)
+        std::memcpy(Y + 2 * (i * K + j) * P2, ps[i].Y[j].data(), sizeof(double) * 2 * P2);
+  });
+}
+
+// deconvolve_image, deconv.hpp:176-198
+int ref_deconvolve_image(int K, const double* delays, double v0, int W, int H, double pitch,
+                         double ox, double oy, const double* stack, const double* sos,
+                         int n_tx, double radius, double offset, double mcx, double mcy,
+                         double mr, double patch_mm, double overlap, double eps, int n_angles,
+                         double ray_step, double merge_fwhm, int workers, double* image) {
+  return guarded([&] {
+    auto g = grid_of(W, H, pitch, ox, oy);
+    auto st = stack_of(K, delays, v0, g, stack);
+    auto lay = pact::make_patch_layout(g, patch_mm, overlap);
+    pact::DeconvolveOptions opt;
+    opt.eps = eps;
+    opt.n_angles = n_angles;
+    opt.ray_step = ray_step;
+    opt.merge_fwhm = merge_fwhm;
+    opt.workers = workers;
+    auto img = pact::deconvolve_image(st, raster_of(g, sos), {n_tx, radius, offset},
+                                      {{mcx, mcy}, mr}, lay, opt);
+    std::memcpy(image, img.values.data(), sizeof(double) * img.values.size());
+  });
+}
+
+// detail::fused_patch_loss_grad, optimize.hpp:234-325, with the training-path
+// complex<float> spectra cache (optimize.hpp:382-392).  Yf: float pairs [K][P][P].
+int ref_fused_patch_loss_grad(int K, const float* Yf, const double* w, int P, double pitch,
+                              int n_angles, const double* delays, double eps, double scale,
+                              int implicit, double* loss, double* dw) {
+  return guarded([&] {
+    size_t P2 = static_cast<size_t>(P) * P;
+    std::vector<std::vector<std::complex<float>>> ys(K, std::vector<std::complex<float>>(P2));
+    for (int j = 0; j < K; ++j)
+      for (size_t b = 0; b < P2; ++b)
+        ys[j][b] = {Yf[2 * (j * P2 + b)], Yf[2 * (j * P2 + b) + 1]};
+    auto table = pact::PatchBinTable::make(P, pitch, n_angles);
+    auto phases =
+        pact::detail::make_delay_phases(table, std::vector<double>(delays, delays + K));
+    pact::detail::FusedScratch scratch;
+    std::vector<double> dwv;
+    *loss = pact::detail::fused_patch_loss_grad(ys, std::vector<double>(w, w + n_angles), table,
+                                                phases, eps, scale, implicit != 0, scratch,
+                                                dwv);
+    std::memcpy(dw, dwv.data(), sizeof(double) * n_angles);
+  });
+}
+
+// wavefront_grad_trace, aberration.hpp:333-361 (accumulates into grad_v, W*H)
+int ref_wavefront_grad_trace(double cx, double cy, int n_tx, double radius, double offset,
+                             int W, int H, double pitch, double ox, double oy, const double* sos,
+                             double v0, double mcx, double mcy, double mr, int n_angles,
+                             double step, const double* dw, double* grad_v) {
+  return guarded([&] {
+    auto g = grid_of(W, H, pitch, ox, oy);
+    auto r = raster_of(g, sos);
+    std::vector<double> gv(grad_v, grad_v + static_cast<size_t>(W) * H);
+    pact::wavefront_grad_trace({cx, cy}, {n_tx, radius, offset}, r, v0, {{mcx, mcy}, mr},
+                               n_angles, step, std::vector<double>(dw, dw + n_angles), gv);
+    std::memcpy(grad_v, gv.data(), sizeof(double) * gv.size());
+  });
+}
+
+// tv_loss, optimize.hpp:120-153 on the field render_sos would produce for
+// the given raster (masked pixels = mask.contains(world(ix, iy))).
+int ref_tv_loss(int W, int H, double pitch, double ox, double oy, const double* raster,
+                double mcx, double mcy, double mr, double lambda, double* value,
+                double* grad_masked) {
+  return guarded([&] {
+    auto g = grid_of(W, H, pitch, ox, oy);
+    pact::SosField f;
+    f.mask = {{mcx, mcy}, mr};
+    f.raster = raster_of(g, raster);
+    for (int iy = 0; iy < H; ++iy)
+      for (int ix = 0; ix < W; ++ix) {
+        pact::Vec2 p = g.world(ix, iy);
+        if (!f.mask.contains(p)) continue;
+        f.masked_indices.push_back(iy * W + ix);
+        f.coords.push_back({(p.x - mcx) / mr, (p.y - mcy) / mr});
+      }
+    auto tv = pact::tv_loss(f, lambda);
+    *value = tv.value;
+    std::memcpy(grad_masked, tv.grad.data(), sizeof(double) * tv.grad.size());
+  });
+}
+
+// adam_step, optimize.hpp:87-110 ; state = (m, v, t)
+int ref_adam_step(int n, double* params, const double* grads, double* m, double* v, long* t,
+                  double lr, double b1, double b2, double eps) {
+  return guarded([&] {
+    std::vector<double> p(params, params + n), g(grads, grads + n);
+    pact::AdamState st;
+    if (*t > 0) {
+      st.m.assign(m, m + n);
+      st.v.assign(v, v + n);
+    }
+    st.t = *t;
+    pact::adam_step(p, g, st, lr, b1, b2, eps);
+    std::memcpy(params, p.data(), sizeof(double) * n);
+    std::memcpy(m, st.m.data(), sizeof(double) * n);
+    std::memcpy(v, st.v.data(), sizeof(double) * n);
+    *t = st.t;
+  });
+}
+
+struct RefTrainCfg {
+  int epochs, steps_per_epoch;
+  double lr, beta1, beta2, adam_eps, lambda_tv;
+  int n_delays;
+  const double* delays;
+  double eps_deconv;
+  int n_angles;
+  double ray_step;
+  uint64_t seed;
+  int hidden, sine_layers;
+  double omega0, out_scale, patch_mm, overlap, merge_fwhm;
+  int implicit_xhat_grad, workers;
+};
+
+// joint_reconstruct, optimize.hpp:367-494.  reports: [epochs][4] = data, tv,
+// total, wall_time.  image/sos: W*H.  theta: final parameters.
+int ref_joint_reconstruct(int n_tx, double radius, double offset, int T, double dt, double t0,
+                          double v0, const double* sig, int W, int H, double pitch, double ox,
+                          double oy, double mcx, double mcy, double mr, const RefTrainCfg* c,
+                          double* reports, double* image, double* sos, double* theta) {
+  return guarded([&] {
+    auto s = signals_of(n_tx, radius, offset, T, dt, t0, v0, sig);
+    pact::TrainConfig cfg;
+    cfg.epochs = c->epochs;
+    cfg.steps_per_epoch = c->steps_per_epoch;
+    cfg.learning_rate = c->lr;
+    cfg.beta1 = c->beta1;
+    cfg.beta2 = c->beta2;
+    cfg.adam_eps = c->adam_eps;
+    cfg.lambda_tv = c->lambda_tv;
+    cfg.delays.assign(c->delays, c->delays + c->n_delays);
+    cfg.eps_deconv = c->eps_deconv;
+    cfg.n_angles = c->n_angles;
+    cfg.ray_step = c->ray_step;
+    cfg.seed = c->seed;
+    cfg.hidden = c->hidden;
+    cfg.sine_layers = c->sine_layers;
+    cfg.omega0 = c->omega0;
+    cfg.out_scale = c->out_scale;
+    cfg.patch_mm = c->patch_mm;
+    cfg.overlap = c->overlap;
+    cfg.merge_fwhm = c->merge_fwhm;
+    cfg.implicit_xhat_grad = c->implicit_xhat_grad != 0;
+    cfg.workers = c->workers;
+    auto jr = pact::joint_reconstruct(s, grid_of(W, H, pitch, ox, oy), {{mcx, mcy}, mr}, cfg);
+    for (size_t e = 0; e < jr.reports.size(); ++e) {
+      reports[4 * e + 0] = jr.reports[e].data_term;
+      reports[4 * e + 1] = jr.reports[e].tv_term;
+      reports[4 * e + 2] = jr.reports[e].total;
+      reports[4 * e + 3] = jr.reports[e].wall_time;
+    }
+    if (image) std::memcpy(image, jr.image.values.data(), sizeof(double) * W * H);
+    if (sos) std::memcpy(sos, jr.sos.values.data(), sizeof(double) * W * H);
+    if (theta) std::memcpy(theta, jr.params.theta.data(), sizeof(double) * jr.params.theta.size());
+  });
+}
+
+// simulate_signals, phantom.hpp:282-362, on a phantom given as rasters.
+// t0 / n_samples fixed by the caller (SimulateOptions.t0 / n_samples).
+int ref_simulate_signals(int W, int H, double pitch, double ox, double oy,
+                         const double* pressure, const double* sos, double mcx, double mcy,
+                         double mr, double background_sos, int n_tx, double radius,
+                         double offset, double pulse_sigma, double dt, double t0, int T,
+                         double ray_step, int workers, double* out) {
+  return guarded([&] {
+    auto g = grid_of(W, H, pitch, ox, oy);
+    pact::Phantom ph;
+    ph.pressure = raster_of(g, pressure);
+    ph.sos = raster_of(g, sos);
+    ph.mask = {{mcx, mcy}, mr};
+    ph.background_sos = background_sos;
+    pact::SimulateOptions opt;
+    opt.pulse_sigma = pulse_sigma;
+    opt.dt = dt;
+    opt.t0 = t0;
+    opt.n_samples = T;
+    opt.ray_step = ray_step;
+    opt.workers = workers;
+    auto s = pact::simulate_signals(ph, {n_tx, radius, offset}, opt);
+    std::memcpy(out, s.data.data(), sizeof(double) * s.data.size());
+  });
+}
+
+// Wall-clock of `reps` calls of das_stack (the CPU baseline of bench.py).
+double ref_time_das_stack(int reps, int n_tx, double radius, double offset, int T, double dt,
+                          double t0, const double* sig, int W, int H, double pitch, double ox,
+                          double oy, double v0, int K, const double* delays, int workers) {
+  auto s = signals_of(n_tx, radius, offset, T, dt, t0, v0, sig);
+  auto g = grid_of(W, H, pitch, ox, oy);
+  std::vector<double> d(delays, delays + K);
+  auto t_start = std::chrono::steady_clock::now();
+  for (int r = 0; r < reps; ++r) {
+    auto st = pact::das_stack(s, g, v0, d, workers);
+    (void)st;
+  }
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+}
+
+}  // extern "C"

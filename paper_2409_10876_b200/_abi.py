@@ -1,0 +1,127 @@
+"""ctypes binding of the C-ABI in include/pact_cuda.h.
+
+This is the Python view of the drop-in boundary: the same entry points the C++
+host API (paper_2409_10876_b200/include/pact/*.hpp) calls.  Device buffers are
+passed as raw pointers (torch CUDA tensors' data_ptr(), or pact_device_alloc).
+There is no fallback: if libpact_cuda.so is missing the import fails.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libpact_cuda.so")
+
+PACT_OK = 0
+PACT_E_VALIDATION = 2
+PACT_E_NUMERICAL = 3
+PACT_E_CUDA = 4
+PACT_E_UNSUPPORTED = 5
+
+
+class PactError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[pact {code}] {msg}")
+        self.code = code
+
+
+class ValidationError(PactError):
+    """The reference's pact::ValidationError (core.hpp:35-38)."""
+
+
+class NumericalError(PactError):
+    """The reference's pact::NumericalError (core.hpp:41-44)."""
+
+
+class Ring(C.Structure):
+    _fields_ = [("n_transducers", C.c_int32), ("radius", C.c_double),
+                ("angle_offset", C.c_double)]
+
+
+class Grid(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("pitch", C.c_double),
+                ("origin_x", C.c_double), ("origin_y", C.c_double)]
+
+
+class SignalMeta(C.Structure):
+    _fields_ = [("n_samples", C.c_int32), ("dt", C.c_double), ("t0", C.c_double),
+                ("background_sos", C.c_double)]
+
+
+class Mask(C.Structure):
+    _fields_ = [("center_x", C.c_double), ("center_y", C.c_double), ("radius", C.c_double)]
+
+
+class Layout(C.Structure):
+    _fields_ = [("grid", Grid), ("patch_pixels", C.c_int32), ("stride_pixels", C.c_int32),
+                ("nx", C.c_int32), ("ny", C.c_int32), ("last_x", C.c_int32),
+                ("last_y", C.c_int32)]
+
+
+_P = C.c_void_p
+_D = C.c_double
+_I = C.c_int32
+_DP = C.POINTER(C.c_double)
+
+# name -> (restype, argtypes); every symbol declared in include/pact_cuda.h.
+SIGNATURES = {
+    "pact_abi_version": (C.c_int, []),
+    "pact_last_error": (C.c_char_p, []),
+    "pact_ctx_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
+    "pact_ctx_destroy": (C.c_int, [_P]),
+    "pact_ctx_stream": (_P, [_P]),
+    "pact_ctx_set_stream": (C.c_int, [_P, _P]),
+    "pact_ctx_synchronize": (C.c_int, [_P]),
+    "pact_ctx_launch_count": (C.c_int64, [_P]),
+    "pact_device_alloc": (C.c_int, [_P, C.c_size_t, C.POINTER(_P)]),
+    "pact_device_free": (C.c_int, [_P, _P]),
+    "pact_host_alloc_pinned": (C.c_int, [C.c_size_t, C.POINTER(_P)]),
+    "pact_host_free_pinned": (C.c_int, [_P]),
+    "pact_upload": (C.c_int, [_P, _P, _P, C.c_size_t]),
+    "pact_download": (C.c_int, [_P, _P, _P, C.c_size_t]),
+    "pact_memset": (C.c_int, [_P, _P, C.c_int, C.c_size_t]),
+    "pact_make_delays": (C.c_int, [_D, _D, _I, _DP]),
+    "pact_das_stack": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(SignalMeta), _P,
+                                 C.POINTER(Grid), _D, _DP, _I, _P]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libpact_cuda.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `make lib` (or __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(code: int) -> None:
+    if code == PACT_OK:
+        return
+    msg = lib().pact_last_error().decode(errors="replace")
+    if code == PACT_E_VALIDATION:
+        raise ValidationError(code, msg)
+    if code == PACT_E_NUMERICAL:
+        raise NumericalError(code, msg)
+    raise PactError(code, msg)
+
+
+def dptr(x) -> C.c_void_p:
+    """Raw device pointer of a torch tensor (or an int address)."""
+    if isinstance(x, int):
+        return C.c_void_p(x)
+    return C.c_void_p(x.data_ptr())
+
+
+def darr(values) -> C.Array:
+    vals = [float(v) for v in values]
+    return (C.c_double * max(1, len(vals)))(*vals)
