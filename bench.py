@@ -54,7 +54,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -195,8 +195,14 @@ def run_ours(args):
     def step():
         ctx.das_stack(sig, w.ring, w.meta, w.grid, w.v0, w.delays, out=out)
 
-    for _ in range(max(3, args.warmup)):
+    clk = Clocks(local).__enter__()  # sampling starts with the warm-up load
+    t_w = time.time()
+    n_warm = 0
+    while n_warm < max(3, args.warmup) or time.time() - t_w < 0.5:
         step()
+        n_warm += 1
+        if n_warm % 8 == 0:
+            torch.cuda.synchronize()
     torch.cuda.synchronize()
 
     # ---- device-resident timed region ----
@@ -206,13 +212,13 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     n0 = ctx.launch_count()
-    with Clocks(local) as clk:
-        for i in range(args.steps):
-            flush.zero_()  # L2 flush (256 MB > 126 MB L2) outside the event pair
-            ev[i][0].record(stream)
-            step()
-            ev[i][1].record(stream)
-        torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()  # L2 flush (256 MB > 126 MB L2) outside the event pair
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    clk.__exit__()
     launches = ctx.launch_count() - n0
     if world > 1:
         dist.barrier()

@@ -94,8 +94,11 @@ int pact_ctx_create(int device, pact_ctx** out);
 int pact_ctx_destroy(pact_ctx* ctx);
 /* Returns the cudaStream_t the context launches on (as void*). */
 void* pact_ctx_stream(pact_ctx* ctx);
-/* Makes the context launch on a caller-owned stream (NULL = its own). */
+/* Makes the context launch on a caller-owned stream.  NULL is the legacy
+ * default stream (e.g. torch's default stream); pact_ctx_use_own_stream
+ * switches back to the context's private non-blocking stream. */
 int pact_ctx_set_stream(pact_ctx* ctx, void* stream);
+int pact_ctx_use_own_stream(pact_ctx* ctx);
 int pact_ctx_synchronize(pact_ctx* ctx);
 /* Number of kernels this library launched on the context so far. */
 int64_t pact_ctx_launch_count(pact_ctx* ctx);

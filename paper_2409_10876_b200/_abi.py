@@ -72,6 +72,7 @@ SIGNATURES = {
     "pact_ctx_destroy": (C.c_int, [_P]),
     "pact_ctx_stream": (_P, [_P]),
     "pact_ctx_set_stream": (C.c_int, [_P, _P]),
+    "pact_ctx_use_own_stream": (C.c_int, [_P]),
     "pact_ctx_synchronize": (C.c_int, [_P]),
     "pact_ctx_launch_count": (C.c_int64, [_P]),
     "pact_device_alloc": (C.c_int, [_P, C.c_size_t, C.POINTER(_P)]),

@@ -85,7 +85,13 @@ void* pact_ctx_stream(pact_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr
 
 int pact_ctx_set_stream(pact_ctx* ctx, void* stream) {
   if (!ctx) return validation("pact_ctx_set_stream: null context").code;
-  ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+  ctx->stream = (cudaStream_t)stream;
+  return PACT_OK;
+}
+
+int pact_ctx_use_own_stream(pact_ctx* ctx) {
+  if (!ctx) return validation("pact_ctx_use_own_stream: null context").code;
+  ctx->stream = ctx->own_stream;
   return PACT_OK;
 }
 

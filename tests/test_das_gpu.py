@@ -142,3 +142,13 @@ def test_validation_errors_match_reference(ctx):
         ctx.das_stack(sig, w.ring, w.meta, w.grid, 1500.0, [0.1, 0.1])
     with pytest.raises(_abi.ValidationError, match="v0 must be > 0"):
         ctx.das_stack(sig, w.ring, w.meta, w.grid, -1.0, [0.0])
+
+
+def test_context_launches_on_torchs_current_stream(ctx):
+    """No explicit synchronize: torch's D2H copy must observe the kernel."""
+    w = wl.cfg1()
+    sig = torch.as_tensor(wl.iid_signals(w, 5)).cuda()
+    a = ctx.das_stack(sig, w.ring, w.meta, w.grid, w.v0, w.delays).cpu()
+    s2 = torch.stack([sig, sig]).sum(0) * 0.5  # same values, new buffer
+    b = ctx.das_stack(s2, w.ring, w.meta, w.grid, w.v0, w.delays).cpu()
+    assert torch.equal(a, b) and a.abs().max() > 0
