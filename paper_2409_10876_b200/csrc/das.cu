@@ -26,20 +26,21 @@
 #include <vector>
 
 #include "common.cuh"
+#include "simd.cuh"
 
 namespace pactgpu {
 namespace {
 
 constexpr int kTile = 16;
 constexpr int kThreads = kTile * kTile;
-constexpr uint32_t kMagicBits = 0x4B000000u;   // bits of 2^23
-constexpr float kMagic = 12582912.0f;           // 1.5 * 2^23
+constexpr uint32_t kMagicIndexBias = 0x4B400000u;  // bits(2^23) + 2^22
+constexpr float kMagic = 12582912.0f;                // 1.5 * 2^23
 
 template <int KB>
 struct DelayConsts {
-  float g[KB];   // 0.5 - frac(c_j)
-  float m[KB];   // 1.5*2^23 - floor(c_j)   (exact in fp32)
-  int ci[KB];    // floor(c_j)
+  float g[KB];  // -frac(c_j)
+  float m[KB];  // 1.5*2^23 - floor(c_j)   (integer-valued, exact in fp32)
+  int ci[KB];   // floor(c_j)
 };
 
 struct DasArgs {
@@ -52,19 +53,15 @@ struct DasArgs {
   double s_off;   // t0 / dt
   double cmin, cmax;
   int n_delays;   // delays in this block (<= KB)
-  int cap;        // staged samples per transducer (multiple of 4)
+  int cap;        // staged entries per transducer
   int chunk;      // transducers per staging round
   int tx_per_split;
-  float* out;     // [split][K_total][H][W] block-offset applied by host
+  // 8 * (bits(2^23) + 2^22): runtime value so ptxas keeps one LEA per tap
+  uint32_t bias8;
+  float* out;     // [split][K_block][H][W]
   size_t split_stride;
   size_t plane;   // H*W
 };
-
-__device__ __forceinline__ float lds_f32(uint32_t addr) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-  return v;
-}
 
 __device__ __forceinline__ double rect_min_dist(double px, double py, double x0, double x1,
                                                 double y0, double y1) {
@@ -81,14 +78,20 @@ __device__ __forceinline__ double rect_max_dist(double px, double py, double x0,
   return sqrt(dx * dx + dy * dy);
 }
 
+// Shared-memory window entry i holds (x[i], x[i+1] - x[i]) so one LDS.64 and
+// one FFMA produce the interpolated tap a + f*d.  Each warp covers an 8x4
+// pixel block, which keeps the sample spread of a warp small (few smem
+// wavefronts per LDS.64).  Index math runs two delays at a time in FADD2.
 template <int KB>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, (KB <= 32 ? 3 : 2))
 das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
-  extern __shared__ float s_win[];  // [chunk][cap]
+  extern __shared__ float2 s_win[];  // [chunk][cap]
   __shared__ int s_lo[128];
 
   const int tid = threadIdx.x;
-  const int lx = tid % kTile, ly = tid / kTile;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int lx = (warp & 1) * 8 + (lane & 7);
+  const int ly = (warp >> 1) * 4 + (lane >> 3);
   const int x0 = blockIdx.x * kTile, y0 = blockIdx.y * kTile;
   const int px = x0 + lx, py = y0 + ly;
   const bool active = px < a.width && py < a.height;
@@ -104,9 +107,9 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
   const int T = a.n_samples;
   const uint32_t smem_base = static_cast<uint32_t>(__cvta_generic_to_shared(s_win));
 
-  float acc[KB];
+  f32x2 acc[KB / 2];
 #pragma unroll
-  for (int j = 0; j < KB; ++j) acc[j] = 0.f;
+  for (int j = 0; j < KB / 2; ++j) acc[j] = 0ull;
 
   for (int n0 = n_begin; n0 < n_end; n0 += a.chunk) {
     const int cnt = min(a.chunk, n_end - n0);
@@ -118,26 +121,26 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
       double smax = dmax * a.k_dist - a.s_off - a.cmin;
       long lo = static_cast<long>(floor(smin)) - 2;
       long hi = static_cast<long>(floor(smax)) + 2;
-      if (hi < 0 || lo > T - 1) {
+      if (hi < 0 || lo > T - 1)
         s_lo[tid] = INT_MIN;  // every tap of the tile is out of window
-      } else {
-        lo = lo < 0 ? 0 : lo;
-        s_lo[tid] = static_cast<int>(lo & ~3L);
-      }
+      else
+        s_lo[tid] = static_cast<int>(lo < 0 ? 0 : lo);
     }
     __syncthreads();
-    // Stage the windows: contiguous per transducer, coalesced.
+    // Stage the windows: contiguous per transducer, coalesced, zero outside [0, T-1].
     const int total = cnt * a.cap;
     for (int e = tid; e < total; e += kThreads) {
       int nl = e / a.cap;
       int off = e - nl * a.cap;
       int lo = s_lo[nl];
-      float v = 0.f;
+      float v0 = 0.f, v1 = 0.f;
       if (lo != INT_MIN) {
         int idx = lo + off;
-        if (idx < T) v = __ldg(&a.sig[static_cast<size_t>(n0 + nl) * T + idx]);
+        const float* row = a.sig + static_cast<size_t>(n0 + nl) * T;
+        if (idx < T) v0 = __ldg(row + idx);
+        if (idx + 1 < T) v1 = __ldg(row + idx + 1);
       }
-      s_win[e] = v;
+      s_win[e] = make_float2(v0, v1 - v0);
     }
     __syncthreads();
 
@@ -152,37 +155,50 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
         double ibd = floor(sb);
         int ib = static_cast<int>(ibd);
         float fb = static_cast<float>(sb - ibd);
-        // smem byte address of tap j = 4*bits(t_j) + cbase  (uint32 wrap-around)
-        uint32_t cidx = static_cast<uint32_t>(ib - 1 - lo + nl * a.cap) - kMagicBits - 4194304u;
-        uint32_t cbase = smem_base + 4u * cidx;
-        bool fast = (sb - a.cmax >= 0.0) && (sb - a.cmin <= static_cast<double>(T - 1));
+        const f32x2 fb2 = pack2(fb, fb);
+        // byte address of tap j: 8*bits(t_j) + cbase (uint32 wrap-around)
+        const uint32_t cbase =
+            smem_base + 8u * static_cast<uint32_t>(ib - lo + nl * a.cap) - a.bias8;
+        const bool fast = (sb - a.cmax >= 0.0) && (sb - a.cmin <= static_cast<double>(T - 1));
         if (fast) {
 #pragma unroll
-          for (int j = 0; j < KB; ++j) {
-            float y = fb + dc.g[j];
-            float t = y + dc.m[j];
-            float r = t - dc.m[j];
-            float f = (y - r) + 0.5f;
-            uint32_t addr = 4u * __float_as_uint(t) + cbase;
-            float va = lds_f32(addr);
-            float vb = lds_f32(addr + 4u);
-            acc[j] += fmaf(f, vb - va, va);
+          for (int j = 0; j < KB; j += 2) {
+            f32x2 m2 = pack2(dc.m[j], dc.m[j + 1]);
+            f32x2 x2 = add2(fb2, pack2(dc.g[j], dc.g[j + 1]));
+            f32x2 t2 = add2_rm(x2, m2);           // m_j + floor(x_j)
+            f32x2 f2 = sub2(x2, sub2(t2, m2));    // frac
+            float t0, t1, f0, f1;
+            unpack2(t2, t0, t1);
+            unpack2(f2, f0, f1);
+            float2 v0 = lds_f32x2(mad_u32(__float_as_uint(t0), 8u, cbase));
+            float2 v1 = lds_f32x2(mad_u32(__float_as_uint(t1), 8u, cbase));
+            acc[j / 2] = add2(acc[j / 2], pack2(fmaf(f0, v0.y, v0.x), fmaf(f1, v1.y, v1.x)));
           }
         } else {
+          // Exact SignalSet::sample edge semantics (core.hpp:296-304).
 #pragma unroll
-          for (int j = 0; j < KB; ++j) {
-            float y = fb + dc.g[j];
-            float t = y + dc.m[j];
-            float r = t - dc.m[j];
-            float f = (y - r) + 0.5f;
-            int i = ib - dc.ci[j] - 1 + static_cast<int>(r);
-            bool valid = (i >= 0) && (i < T - 1 || (i == T - 1 && f == 0.f));
-            if (valid) {
-              uint32_t addr = 4u * __float_as_uint(t) + cbase;
-              float va = lds_f32(addr);
-              float vb = lds_f32(addr + 4u);
-              acc[j] += fmaf(f, vb - va, va);
+          for (int j = 0; j < KB; j += 2) {
+            f32x2 m2 = pack2(dc.m[j], dc.m[j + 1]);
+            f32x2 x2 = add2(fb2, pack2(dc.g[j], dc.g[j + 1]));
+            f32x2 t2 = add2_rm(x2, m2);
+            f32x2 r2 = sub2(t2, m2);
+            f32x2 f2 = sub2(x2, r2);
+            float t[2], f[2], r[2];
+            unpack2(t2, t[0], t[1]);
+            unpack2(f2, f[0], f[1]);
+            unpack2(r2, r[0], r[1]);
+            float val[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              int i = ib - dc.ci[j + h] + static_cast<int>(r[h]);
+              bool valid = (i >= 0) && (i < T - 1 || (i == T - 1 && f[h] == 0.f));
+              val[h] = 0.f;
+              if (valid) {
+                float2 v = lds_f32x2(mad_u32(__float_as_uint(t[h]), 8u, cbase));
+                val[h] = fmaf(f[h], v.y, v.x);
+              }
             }
+            acc[j / 2] = add2(acc[j / 2], pack2(val[0], val[1]));
           }
         }
       }
@@ -193,8 +209,12 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
   if (active) {
     float* o = a.out + blockIdx.z * a.split_stride + static_cast<size_t>(py) * a.width + px;
 #pragma unroll
-    for (int j = 0; j < KB; ++j)
-      if (j < a.n_delays) o[j * a.plane] = acc[j];
+    for (int j = 0; j < KB; j += 2) {
+      float v0, v1;
+      unpack2(acc[j / 2], v0, v1);
+      if (j < a.n_delays) o[j * a.plane] = v0;
+      if (j + 1 < a.n_delays) o[(j + 1) * a.plane] = v1;
+    }
   }
 }
 
@@ -218,7 +238,7 @@ Status launch_block(pact_ctx* ctx, DasArgs a, const double* c, int nsplit, dim3 
     double cj = c[j < a.n_delays ? j : a.n_delays - 1];
     double fl = std::floor(cj);
     dc.ci[j] = static_cast<int>(fl);
-    dc.g[j] = static_cast<float>(0.5 - (cj - fl));
+    dc.g[j] = static_cast<float>(-(cj - fl));
     dc.m[j] = kMagic - static_cast<float>(fl);
   }
   if (smem > 48 * 1024)
@@ -281,6 +301,7 @@ Status das_stack_device(pact_ctx* ctx, const pact_ring& ring, const pact_signal_
   a.k_dist = k_dist;
   a.s_off = meta.t0 / meta.dt;
   a.plane = plane;
+  a.bias8 = 8u * kMagicIndexBias;
 
   const double diag = std::hypot((double)(kTile - 1), (double)(kTile - 1)) * grid.pitch;
 
@@ -292,9 +313,9 @@ Status das_stack_device(pact_ctx* ctx, const pact_ring& ring, const pact_signal_
     a.cmin = c[jb];
     a.cmax = c[jb + kb - 1];
     int span = static_cast<int>(std::ceil(diag * k_dist + (a.cmax - a.cmin))) + 12;
-    int cap = (span + 3) & ~3;
-    int chunk = std::max(1, std::min(64, static_cast<int>((40 * 1024) / (cap * 4))));
-    size_t smem = static_cast<size_t>(chunk) * cap * sizeof(float);
+    int cap = span;
+    int chunk = std::max(1, std::min(64, static_cast<int>((48 * 1024) / (cap * 8))));
+    size_t smem = static_cast<size_t>(chunk) * cap * sizeof(float2);
     if (smem > 200 * 1024) {
       return validation("das_stack: per-tile time window exceeds shared memory "
                         "(pitch x tile diagonal + delay span too large)");
