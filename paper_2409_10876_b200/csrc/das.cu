@@ -35,6 +35,20 @@ constexpr int kTile = 16;
 constexpr int kThreads = kTile * kTile;
 constexpr uint32_t kMagicIndexBias = 0x4B400000u;  // bits(2^23) + 2^22
 constexpr float kMagic = 12582912.0f;                // 1.5 * 2^23
+// Shared-memory window: sample plane X then difference plane D at a fixed
+// offset, so the D load is the X address plus an LDS immediate.
+constexpr int kPlaneFloats = 6144;
+constexpr int kPlaneBytes = kPlaneFloats * 4;
+constexpr size_t kWindowSmem = 2 * kPlaneBytes;
+
+// (x[i], x[i+1] - x[i]) from the two planes: two conflict-free LDS.32 when the
+// warp's samples span < 32 words.
+__device__ __forceinline__ float2 lds_xd(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+24576];"
+               : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
+}
 
 template <int KB>
 struct DelayConsts {
@@ -56,8 +70,8 @@ struct DasArgs {
   int cap;        // staged entries per transducer
   int chunk;      // transducers per staging round
   int tx_per_split;
-  // 8 * (bits(2^23) + 2^22): runtime value so ptxas keeps one LEA per tap
-  uint32_t bias8;
+  // 4 * (bits(2^23) + 2^22): runtime value so ptxas keeps one LEA per tap
+  uint32_t bias4;
   float* out;     // [split][K_block][H][W]
   size_t split_stride;
   size_t plane;   // H*W
@@ -78,14 +92,14 @@ __device__ __forceinline__ double rect_max_dist(double px, double py, double x0,
   return sqrt(dx * dx + dy * dy);
 }
 
-// Shared-memory window entry i holds (x[i], x[i+1] - x[i]) so one LDS.64 and
-// one FFMA produce the interpolated tap a + f*d.  Each warp covers an 8x4
-// pixel block, which keeps the sample spread of a warp small (few smem
-// wavefronts per LDS.64).  Index math runs two delays at a time in FADD2.
+// Window entry i is (x[i], x[i+1] - x[i]) so two LDS.32 and one FFMA produce
+// the interpolated tap a + f*d.  Each warp covers an 8x4 pixel block, which
+// keeps the sample spread of a warp under 32 words (one smem wavefront per
+// LDS).  Index math runs two delays at a time in FADD2.
 template <int KB>
 __global__ void __launch_bounds__(kThreads, (KB <= 32 ? 3 : 2))
 das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
-  extern __shared__ float2 s_win[];  // [chunk][cap]
+  extern __shared__ float s_win[];  // X plane [chunk][cap], D plane at +kPlaneBytes
   __shared__ int s_lo[128];
 
   const int tid = threadIdx.x;
@@ -140,7 +154,8 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
         if (idx < T) v0 = __ldg(row + idx);
         if (idx + 1 < T) v1 = __ldg(row + idx + 1);
       }
-      s_win[e] = make_float2(v0, v1 - v0);
+      s_win[e] = v0;
+      s_win[e + kPlaneFloats] = v1 - v0;
     }
     __syncthreads();
 
@@ -158,7 +173,7 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
         const f32x2 fb2 = pack2(fb, fb);
         // byte address of tap j: 8*bits(t_j) + cbase (uint32 wrap-around)
         const uint32_t cbase =
-            smem_base + 8u * static_cast<uint32_t>(ib - lo + nl * a.cap) - a.bias8;
+            smem_base + 4u * static_cast<uint32_t>(ib - lo + nl * a.cap) - a.bias4;
         const bool fast = (sb - a.cmax >= 0.0) && (sb - a.cmin <= static_cast<double>(T - 1));
         if (fast) {
 #pragma unroll
@@ -170,8 +185,8 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
             float t0, t1, f0, f1;
             unpack2(t2, t0, t1);
             unpack2(f2, f0, f1);
-            float2 v0 = lds_f32x2(mad_u32(__float_as_uint(t0), 8u, cbase));
-            float2 v1 = lds_f32x2(mad_u32(__float_as_uint(t1), 8u, cbase));
+            float2 v0 = lds_xd(mad_u32(__float_as_uint(t0), 4u, cbase));
+            float2 v1 = lds_xd(mad_u32(__float_as_uint(t1), 4u, cbase));
             acc[j / 2] = add2(acc[j / 2], pack2(fmaf(f0, v0.y, v0.x), fmaf(f1, v1.y, v1.x)));
           }
         } else {
@@ -194,7 +209,7 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
               bool valid = (i >= 0) && (i < T - 1 || (i == T - 1 && f[h] == 0.f));
               val[h] = 0.f;
               if (valid) {
-                float2 v = lds_f32x2(mad_u32(__float_as_uint(t[h]), 8u, cbase));
+                float2 v = lds_xd(mad_u32(__float_as_uint(t[h]), 4u, cbase));
                 val[h] = fmaf(f[h], v.y, v.x);
               }
             }
@@ -241,9 +256,13 @@ Status launch_block(pact_ctx* ctx, DasArgs a, const double* c, int nsplit, dim3 
     dc.g[j] = static_cast<float>(-(cj - fl));
     dc.m[j] = kMagic - static_cast<float>(fl);
   }
-  if (smem > 48 * 1024)
+  static bool configured = false;  // per instantiation
+  if (!configured) {
     PACT_CUDA_S(cudaFuncSetAttribute(das_stack_kernel<KB>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kWindowSmem));
+    configured = true;
+  }
   grid.z = nsplit;
   das_stack_kernel<KB><<<grid, kThreads, smem, ctx->stream>>>(a, dc);
   return after_launch(ctx, "das_stack_kernel");
@@ -301,7 +320,7 @@ Status das_stack_device(pact_ctx* ctx, const pact_ring& ring, const pact_signal_
   a.k_dist = k_dist;
   a.s_off = meta.t0 / meta.dt;
   a.plane = plane;
-  a.bias8 = 8u * kMagicIndexBias;
+  a.bias4 = 4u * kMagicIndexBias;
 
   const double diag = std::hypot((double)(kTile - 1), (double)(kTile - 1)) * grid.pitch;
 
@@ -314,9 +333,9 @@ Status das_stack_device(pact_ctx* ctx, const pact_ring& ring, const pact_signal_
     a.cmax = c[jb + kb - 1];
     int span = static_cast<int>(std::ceil(diag * k_dist + (a.cmax - a.cmin))) + 12;
     int cap = span;
-    int chunk = std::max(1, std::min(64, static_cast<int>((48 * 1024) / (cap * 8))));
-    size_t smem = static_cast<size_t>(chunk) * cap * sizeof(float2);
-    if (smem > 200 * 1024) {
+    int chunk = std::min(64, kPlaneFloats / cap);
+    size_t smem = kWindowSmem;
+    if (chunk < 1) {
       return validation("das_stack: per-tile time window exceeds shared memory "
                         "(pitch x tile diagonal + delay span too large)");
     }
