@@ -126,6 +126,190 @@ int pact_das_stack(pact_ctx* ctx, const pact_ring* ring, const pact_signal_meta*
                    const float* signals, const pact_grid* grid, double v0,
                    const double* delays, int32_t n_delays, float* out);
 
+/* ---- patch layout (host) ---- */
+
+/* make_patch_layout, core.hpp:252-281 (same validation and messages). */
+int pact_make_patch_layout(const pact_grid* grid, double patch_mm, double overlap,
+                           pact_layout* out);
+int32_t pact_layout_n_patches(const pact_layout* layout);
+/* PatchLayout::offsets / centers (row-major patch order): offsets[2i] = ox,
+ * offsets[2i+1] = oy (pixels); centers[2i], centers[2i+1] world mm.  Either may be NULL. */
+int pact_layout_patches(const pact_layout* layout, int32_t* offsets, double* centers);
+
+/* ---- part 2: SOS field, wavefronts, transfer stacks ---- */
+
+/* SirenParams scalars, nfield.hpp:37-71; theta layout is the reference's
+ * (per layer: W row-major [rows][cols], then b). */
+typedef struct pact_siren {
+  int32_t in_dim; /* must be 2 */
+  int32_t hidden;
+  int32_t n_hidden_layers;
+  double omega0;
+  double out_scale; /* m/s per unit output */
+  double v0;        /* background SOS, m/s */
+} pact_siren;
+
+/* siren_param_count, nfield.hpp:73-78. */
+int64_t pact_siren_param_count(const pact_siren* siren);
+/* init_siren, nfield.hpp:83-107 (host; mt19937_64 + uniform_real_distribution,
+ * bit-identical to the reference).  theta: HOST double[param_count]. */
+int pact_init_siren(uint64_t seed, const pact_siren* siren, double* theta);
+/* Masked pixels of render_sos (nfield.hpp:152-160): row-major flat indices and
+ * normalised coordinates (HOST arrays; either may be NULL). */
+int32_t pact_masked_count(const pact_grid* grid, const pact_mask* mask);
+int pact_masked_pixels(const pact_grid* grid, const pact_mask* mask, int32_t* idx,
+                       float* coords);
+
+/* render_sos, nfield.hpp:145-162.  theta: device fp32.  raster: device fp32
+ * [H][W], v0 outside the mask.  sos_dev (optional): device fp32 [H][W] holding
+ * v - v0 (the full-precision form the ray kernels consume). */
+int pact_render_sos(pact_ctx* ctx, const pact_siren* siren, const float* theta,
+                    const pact_grid* grid, const pact_mask* mask, float* raster, float* sos_dev);
+
+/* backprop_sos, nfield.hpp:166-233: gradient of sum_m g_m v(m).
+ *   grad_masked : device fp32 [n_masked] (render_sos masked order)
+ *   grad_theta  : device fp64 [param_count] (overwritten) */
+int pact_siren_backward(pact_ctx* ctx, const pact_siren* siren, const float* theta,
+                        const pact_grid* grid, const pact_mask* mask, const float* grad_masked,
+                        double* grad_theta);
+
+/* wavefront_profile, aberration.hpp:134-186, for n_centers patch centres.
+ *   sos_dev : device fp32 [H][W] = v - v0 on `grid`
+ *   centers : HOST double[2 n_centers] (mm)
+ *   w       : device fp32 [n_centers][n_angles] (mm) */
+int pact_wavefront(pact_ctx* ctx, const pact_ring* ring, const pact_grid* grid,
+                   const float* sos_dev, double v0, const pact_mask* mask, int32_t n_centers,
+                   const double* centers, int32_t n_angles, double step, float* w);
+
+/* transfer_stack, aberration.hpp:236-265, batched over patches.
+ *   w      : device fp32 [n_patches][n_angles]
+ *   delays : HOST double[K]
+ *   H      : device complex64 [n_patches][K][P][P] (interleaved re, im) */
+int pact_transfer_stack(pact_ctx* ctx, int32_t n_patches, const float* w, int32_t n_angles,
+                        const double* delays, int32_t K, int32_t P, double pitch, float* H);
+
+/* ---- part 3: spectra, deconvolution, loss and gradients ---- */
+
+/* extract_patch_spectra, deconv.hpp:64-74.
+ *   stack : device fp32 [K][H][W];  Y : device complex64 [n_patches][K][P][P] */
+int pact_patch_spectra(pact_ctx* ctx, const pact_layout* layout, const float* stack, int32_t K,
+                       float* Y);
+
+/* DeconvolveOptions, deconv.hpp:166-172 (workers has no meaning here). */
+typedef struct pact_deconv_options {
+  double eps;
+  int32_t n_angles;
+  double ray_step;
+  double merge_fwhm;
+} pact_deconv_options;
+
+/* deconvolve_image, deconv.hpp:176-198.  stack device fp32 [K][H][W];
+ * sos_dev device fp32 [H][W] = v - v0 with v0 = the stack's v0; image device fp32 [H][W]. */
+int pact_deconvolve_image(pact_ctx* ctx, const float* stack, int32_t K, const double* delays,
+                          double v0, const float* sos_dev, const pact_ring* ring,
+                          const pact_mask* mask, const pact_layout* layout,
+                          const pact_deconv_options* options, float* image);
+
+/* detail::fused_patch_loss_grad, optimize.hpp:234-325, batched over patches:
+ *   Y      : device complex64 [n_patches][K][P][P] (the training-path fp32 cache)
+ *   w      : device fp32 [n_patches][n_angles]
+ *   loss   : device fp64 [n_patches]   (sum_j sum_k |k| scale |Y_j - H_j X|^2)
+ *   dw     : device fp32 [n_patches][n_angles]  (dL/dw) */
+int pact_loss_grad(pact_ctx* ctx, int32_t n_patches, const float* Y, const float* w,
+                   int32_t n_angles, const double* delays, int32_t K, int32_t P, double pitch,
+                   double eps, double scale, int32_t implicit, double* loss_per_patch, float* dw);
+
+/* wavefront_grad_trace, aberration.hpp:333-361, batched: grad_v (device fp64
+ * [H][W]) += sum over rays of dL/dw * dl * v0 / v^2 * bilinear weight. */
+int pact_ray_backward(pact_ctx* ctx, const pact_ring* ring, const pact_grid* grid,
+                      const float* sos_dev, double v0, const pact_mask* mask, int32_t n_centers,
+                      const double* centers, int32_t n_angles, double step, const float* dw,
+                      double* grad_v);
+
+/* tv_loss, optimize.hpp:120-153 on the masked pixels of (grid, mask).
+ *   raster      : device fp32 [H][W] (v, or v - v0: differences agree)
+ *   value       : HOST double (synchronous)
+ *   grad_masked : device fp32 [n_masked] */
+int pact_tv_loss(pact_ctx* ctx, const pact_grid* grid, const pact_mask* mask, const float* raster,
+                 double lambda, double* value, float* grad_masked);
+
+/* adam_step, optimize.hpp:87-110, on device fp64 buffers; `t` is the step
+ * count AFTER this update (AdamState::t).  Non-finite gradients ->
+ * PACT_E_NUMERICAL and no update (synchronous check). */
+int pact_adam_step(pact_ctx* ctx, int64_t n, double* theta, const double* grad, double* m,
+                   double* v, int64_t t, double lr, double beta1, double beta2, double eps);
+
+/* ---- the NF-APACT iteration engine: joint_reconstruct, optimize.hpp:367-494 ---- */
+
+/* TrainConfig, optimize.hpp:48-78 (workers is accepted and ignored). */
+typedef struct pact_train_config {
+  int32_t epochs;
+  int32_t steps_per_epoch;
+  double learning_rate;
+  double beta1;
+  double beta2;
+  double adam_eps;
+  double lambda_tv;
+  int32_t n_delays;
+  const double* delays; /* HOST */
+  double eps_deconv;
+  int32_t n_angles;
+  double ray_step;
+  uint64_t seed;
+  int32_t hidden;
+  int32_t sine_layers;
+  double omega0;
+  double out_scale;
+  double patch_mm;
+  double overlap;
+  double merge_fwhm;
+  int32_t implicit_xhat_grad;
+  int32_t workers;
+  int32_t use_cuda_graph; /* capture one step as a CUDA graph (1 = yes) */
+} pact_train_config;
+
+typedef struct pact_trainer pact_trainer;
+
+/* Fills `cfg` with the reference defaults (TrainConfig, optimize.hpp:48-69);
+ * cfg->delays points to a static make_delays(-0.8, 0.8, 32) array. */
+int pact_train_config_default(pact_train_config* cfg);
+
+/* One-time part of joint_reconstruct (optimize.hpp:369-405): layout, DAS
+ * stack, fp32 patch spectra, SIREN init, tables.  signals: device fp32 [N][T]. */
+int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_meta* meta,
+                        const float* signals, const pact_grid* grid, const pact_mask* mask,
+                        const pact_train_config* cfg, pact_trainer** out);
+/* Enqueue n_steps full iterations (render -> wavefront -> fused loss ->
+ * ray backward -> TV -> SIREN backward -> Adam); asynchronous. */
+int pact_trainer_step(pact_trainer* tr, int32_t n_steps);
+/* Last step's LossReport terms {data, tv, total} (host) and the NumericalError
+ * check of joint_reconstruct; synchronises.  `epoch` is used in the message. */
+int pact_trainer_report(pact_trainer* tr, int32_t epoch, double* report3);
+/* One reported epoch (steps_per_epoch steps): report4 = {data, tv, total, wall_s}. */
+int pact_trainer_run_epoch(pact_trainer* tr, int32_t epoch, double* report4);
+/* Final render + deconvolution (optimize.hpp:478-486): device fp32 [H][W]
+ * image and SOS (either may be NULL). */
+int pact_trainer_finish(pact_trainer* tr, float* image, float* sos);
+/* Current parameters (HOST fp64) / overwrite them (resets nothing else). */
+int pact_trainer_get_theta(pact_trainer* tr, double* theta);
+int pact_trainer_set_theta(pact_trainer* tr, const double* theta);
+/* Device pointers of the engine's state for inspection:
+ * what: 0 stack fp32 [K][H][W], 1 spectra c64 [n][K][P][P], 2 sos_dev fp32 [H][W],
+ * 3 wavefronts fp32 [n][A], 4 dw fp32 [n][A], 5 grad_v fp64 [H][W],
+ * 6 grad_theta fp64 [P], 7 theta fp64 [P]. */
+void* pact_trainer_buffer(pact_trainer* tr, int32_t what);
+int pact_trainer_destroy(pact_trainer* tr);
+/* Kernels the engine launched so far (graph replays counted per kernel). */
+int64_t pact_trainer_launch_count(pact_trainer* tr);
+
+/* joint_reconstruct, optimize.hpp:367-494, end to end.  reports: HOST
+ * double[epochs][4] {data, tv, total, wall_s}; image, sos: device fp32
+ * [H][W] (may be NULL); theta: HOST fp64 (may be NULL). */
+int pact_joint_reconstruct(pact_ctx* ctx, const pact_ring* ring, const pact_signal_meta* meta,
+                           const float* signals, const pact_grid* grid, const pact_mask* mask,
+                           const pact_train_config* cfg, double* reports, float* image,
+                           float* sos, double* theta);
+
 #ifdef __cplusplus
 }
 #endif

@@ -418,6 +418,148 @@ int ref_simulate_signals(int W, int H, double pitch, double ox, double oy,
   });
 }
 
+// testsupport::make_small_instance (tests/test_support.hpp:43-75): the
+// reference's shared 64x64 fixture.  Call with sig == nullptr to get T.
+int ref_small_instance_signals(double* sig, int* T, double* t0) {
+  return guarded([&] {
+    pact::GridSpec grid = pact::GridSpec::centered(64, 64, 0.1);
+    pact::CircularMask mask{{0.0, 0.0}, 2.6};
+    pact::RingGeometry ring{64, 50.0, 0.0};
+    pact::PhantomSpec spec = pact::builtin_phantom_spec("empty", 1500.0);
+    spec.mask = mask;
+    spec.discs.push_back({{0.4, -0.3}, 1.2, 1560.0, 0.0});
+    spec.points.push_back({{0.0, 0.0}, 1.0});
+    spec.points.push_back({{1.0, 0.8}, 0.8});
+    spec.points.push_back({{-1.2, 0.4}, 0.9});
+    pact::Phantom ph = pact::generate_phantom(grid, spec, 0);
+    pact::SignalSet s = pact::simulate_signals(ph, ring);
+    *T = s.n_samples;
+    *t0 = s.t0;
+    if (sig) std::memcpy(sig, s.data.data(), sizeof(double) * s.data.size());
+  });
+}
+
+static pact::TrainConfig train_config_of(const RefTrainCfg* c) {
+  pact::TrainConfig cfg;
+  cfg.epochs = c->epochs;
+  cfg.steps_per_epoch = c->steps_per_epoch;
+  cfg.learning_rate = c->lr;
+  cfg.beta1 = c->beta1;
+  cfg.beta2 = c->beta2;
+  cfg.adam_eps = c->adam_eps;
+  cfg.lambda_tv = c->lambda_tv;
+  cfg.delays.assign(c->delays, c->delays + c->n_delays);
+  cfg.eps_deconv = c->eps_deconv;
+  cfg.n_angles = c->n_angles;
+  cfg.ray_step = c->ray_step;
+  cfg.seed = c->seed;
+  cfg.hidden = c->hidden;
+  cfg.sine_layers = c->sine_layers;
+  cfg.omega0 = c->omega0;
+  cfg.out_scale = c->out_scale;
+  cfg.patch_mm = c->patch_mm;
+  cfg.overlap = c->overlap;
+  cfg.merge_fwhm = c->merge_fwhm;
+  cfg.implicit_xhat_grad = c->implicit_xhat_grad != 0;
+  cfg.workers = c->workers;
+  return cfg;
+}
+
+// One NF-APACT iteration at parameters `theta` without the Adam update: the
+// body of joint_reconstruct's step loop (optimize.hpp:413-461) composed from
+// the reference entry points, plus deconvolve_image under theta's SOS
+// (optimize.hpp:478-486).  Any output pointer may be null.  patch_lo/hi
+// restrict the per-patch work to a sample (bench CPU baseline); pass 0/-1 for all.
+int ref_nf_step(int n_tx, double radius, double offset, int T, double dt, double t0, double v0,
+                const double* sig, int W, int H, double pitch, double ox, double oy, double mcx,
+                double mcy, double mr, const RefTrainCfg* c, const double* theta, int patch_lo,
+                int patch_hi, double* data_term, double* tv_term, double* loss_patch,
+                double* w_out, double* dw_out, double* sos_out, double* grad_v_masked,
+                double* grad_theta, double* image, double* seconds) {
+  return guarded([&] {
+    auto s = signals_of(n_tx, radius, offset, T, dt, t0, v0, sig);
+    pact::TrainConfig cfg = train_config_of(c);
+    auto grid = grid_of(W, H, pitch, ox, oy);
+    pact::CircularMask mask{{mcx, mcy}, mr};
+    auto layout = pact::make_patch_layout(grid, cfg.patch_mm, cfg.overlap);
+    const int P = layout.patch_pixels, N = layout.n_patches();
+    const size_t M = cfg.delays.size();
+    const double loss_scale = 1.0 / (static_cast<double>(N) * M * P * P);
+    auto stack = pact::das_stack(s, grid, v0, cfg.delays, cfg.workers);
+    std::vector<std::vector<std::vector<std::complex<float>>>> ycache(N);
+    pact::parallel_for(N, cfg.workers, [&](int i) {
+      pact::PatchSpectra ps = pact::extract_patch_spectra_one(stack, layout, i);
+      ycache[i].resize(M);
+      for (size_t j = 0; j < M; ++j) {
+        ycache[i][j].resize(ps.Y[j].size());
+        for (size_t b = 0; b < ps.Y[j].size(); ++b)
+          ycache[i][j][b] = std::complex<float>(ps.Y[j][b]);
+      }
+    });
+    auto params = siren_of(cfg.hidden, cfg.sine_layers, cfg.omega0, cfg.out_scale, v0, theta);
+    const auto table = pact::PatchBinTable::make(P, grid.pitch, cfg.n_angles);
+    const auto phases = pact::detail::make_delay_phases(table, cfg.delays);
+    int lo = patch_lo, hi = patch_hi < 0 ? N : std::min(N, patch_hi);
+    auto t_start = std::chrono::steady_clock::now();
+    auto field = pact::render_sos(params, grid, mask);
+    std::vector<double> gv(field.raster.values.size(), 0.0);
+    std::vector<double> lp(N, 0.0);
+    const int nw = pact::resolve_workers(cfg.workers);
+    const int span = hi - lo;
+    const int n_chunks = std::max(1, std::min(span, nw * 4));
+    const int chunk_len = (span + n_chunks - 1) / n_chunks;
+    std::vector<std::vector<double>> chunk_gv(n_chunks);
+    pact::parallel_for(n_chunks, cfg.workers, [&](int ck) {
+      int a = lo + ck * chunk_len, b = std::min(hi, a + chunk_len);
+      if (a >= b) return;
+      auto& g = chunk_gv[ck];
+      g.assign(gv.size(), 0.0);
+      pact::detail::FusedScratch scratch;
+      std::vector<double> dw;
+      for (int i = a; i < b; ++i) {
+        auto prof = pact::wavefront_profile(layout.centers[i], s.geom, field.raster, v0, mask,
+                                            cfg.n_angles, cfg.ray_step, false);
+        lp[i] = pact::detail::fused_patch_loss_grad(ycache[i], prof.w, table, phases,
+                                                    cfg.eps_deconv, loss_scale,
+                                                    cfg.implicit_xhat_grad, scratch, dw);
+        if (w_out) std::memcpy(w_out + static_cast<size_t>(i) * cfg.n_angles, prof.w.data(),
+                               sizeof(double) * cfg.n_angles);
+        if (dw_out) std::memcpy(dw_out + static_cast<size_t>(i) * cfg.n_angles, dw.data(),
+                                sizeof(double) * cfg.n_angles);
+        pact::wavefront_grad_trace(layout.centers[i], s.geom, field.raster, v0, mask,
+                                   cfg.n_angles, cfg.ray_step, dw, g);
+      }
+    });
+    for (const auto& g : chunk_gv)
+      if (!g.empty())
+        for (size_t k = 0; k < gv.size(); ++k) gv[k] += g[k];
+    double data = 0.0;
+    for (int i = 0; i < N; ++i) data += lp[i];
+    auto tv = pact::tv_loss(field, cfg.lambda_tv);
+    std::vector<double> gm(field.masked_indices.size());
+    for (size_t i = 0; i < gm.size(); ++i) gm[i] = gv[field.masked_indices[i]] + tv.grad[i];
+    auto grads = pact::backprop_sos(params, field, gm);
+    if (seconds)
+      *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    if (data_term) *data_term = data;
+    if (tv_term) *tv_term = tv.value;
+    if (loss_patch) std::memcpy(loss_patch, lp.data(), sizeof(double) * N);
+    if (sos_out) std::memcpy(sos_out, field.raster.values.data(), sizeof(double) * W * H);
+    if (grad_v_masked) std::memcpy(grad_v_masked, gm.data(), sizeof(double) * gm.size());
+    if (grad_theta) std::memcpy(grad_theta, grads.data(), sizeof(double) * grads.size());
+    if (image) {
+      pact::DeconvolveOptions dopt;
+      dopt.eps = cfg.eps_deconv;
+      dopt.n_angles = cfg.n_angles;
+      dopt.ray_step = cfg.ray_step;
+      dopt.merge_fwhm = cfg.merge_fwhm;
+      dopt.workers = cfg.workers;
+      auto img = pact::deconvolve_image(stack, field.raster, s.geom, mask, layout, dopt);
+      std::memcpy(image, img.values.data(), sizeof(double) * W * H);
+    }
+  });
+}
+
 // Wall-clock of `reps` calls of das_stack (the CPU baseline of bench.py).
 double ref_time_das_stack(int reps, int n_tx, double radius, double offset, int T, double dt,
                           double t0, const double* sig, int W, int H, double pitch, double ox,

@@ -59,10 +59,34 @@ class Layout(C.Structure):
                 ("last_y", C.c_int32)]
 
 
+class Siren(C.Structure):
+    _fields_ = [("in_dim", C.c_int32), ("hidden", C.c_int32), ("n_hidden_layers", C.c_int32),
+                ("omega0", C.c_double), ("out_scale", C.c_double), ("v0", C.c_double)]
+
+
+class DeconvOptions(C.Structure):
+    _fields_ = [("eps", C.c_double), ("n_angles", C.c_int32), ("ray_step", C.c_double),
+                ("merge_fwhm", C.c_double)]
+
+
+class TrainConfig(C.Structure):
+    _fields_ = [("epochs", C.c_int32), ("steps_per_epoch", C.c_int32),
+                ("learning_rate", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
+                ("adam_eps", C.c_double), ("lambda_tv", C.c_double), ("n_delays", C.c_int32),
+                ("delays", C.POINTER(C.c_double)), ("eps_deconv", C.c_double),
+                ("n_angles", C.c_int32), ("ray_step", C.c_double), ("seed", C.c_uint64),
+                ("hidden", C.c_int32), ("sine_layers", C.c_int32), ("omega0", C.c_double),
+                ("out_scale", C.c_double), ("patch_mm", C.c_double), ("overlap", C.c_double),
+                ("merge_fwhm", C.c_double), ("implicit_xhat_grad", C.c_int32),
+                ("workers", C.c_int32), ("use_cuda_graph", C.c_int32)]
+
+
 _P = C.c_void_p
 _D = C.c_double
 _I = C.c_int32
 _DP = C.POINTER(C.c_double)
+_IP = C.POINTER(C.c_int32)
+_FP = C.POINTER(C.c_float)
 
 # name -> (restype, argtypes); every symbol declared in include/pact_cuda.h.
 SIGNATURES = {
@@ -85,6 +109,45 @@ SIGNATURES = {
     "pact_make_delays": (C.c_int, [_D, _D, _I, _DP]),
     "pact_das_stack": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(SignalMeta), _P,
                                  C.POINTER(Grid), _D, _DP, _I, _P]),
+    "pact_make_patch_layout": (C.c_int, [C.POINTER(Grid), _D, _D, C.POINTER(Layout)]),
+    "pact_layout_n_patches": (C.c_int32, [C.POINTER(Layout)]),
+    "pact_layout_patches": (C.c_int, [C.POINTER(Layout), _IP, _DP]),
+    "pact_siren_param_count": (C.c_int64, [C.POINTER(Siren)]),
+    "pact_init_siren": (C.c_int, [C.c_uint64, C.POINTER(Siren), _DP]),
+    "pact_masked_count": (C.c_int32, [C.POINTER(Grid), C.POINTER(Mask)]),
+    "pact_masked_pixels": (C.c_int, [C.POINTER(Grid), C.POINTER(Mask), _IP, _FP]),
+    "pact_render_sos": (C.c_int, [_P, C.POINTER(Siren), _P, C.POINTER(Grid), C.POINTER(Mask),
+                                  _P, _P]),
+    "pact_siren_backward": (C.c_int, [_P, C.POINTER(Siren), _P, C.POINTER(Grid),
+                                      C.POINTER(Mask), _P, _P]),
+    "pact_wavefront": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(Grid), _P, _D, C.POINTER(Mask),
+                                 _I, _DP, _I, _D, _P]),
+    "pact_transfer_stack": (C.c_int, [_P, _I, _P, _I, _DP, _I, _I, _D, _P]),
+    "pact_patch_spectra": (C.c_int, [_P, C.POINTER(Layout), _P, _I, _P]),
+    "pact_deconvolve_image": (C.c_int, [_P, _P, _I, _DP, _D, _P, C.POINTER(Ring),
+                                        C.POINTER(Mask), C.POINTER(Layout),
+                                        C.POINTER(DeconvOptions), _P]),
+    "pact_loss_grad": (C.c_int, [_P, _I, _P, _P, _I, _DP, _I, _I, _D, _D, _D, _I, _P, _P]),
+    "pact_ray_backward": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(Grid), _P, _D,
+                                    C.POINTER(Mask), _I, _DP, _I, _D, _P, _P]),
+    "pact_tv_loss": (C.c_int, [_P, C.POINTER(Grid), C.POINTER(Mask), _P, _D, _DP, _P]),
+    "pact_adam_step": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, C.c_int64, _D, _D, _D, _D]),
+    "pact_train_config_default": (C.c_int, [C.POINTER(TrainConfig)]),
+    "pact_trainer_create": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(SignalMeta), _P,
+                                      C.POINTER(Grid), C.POINTER(Mask), C.POINTER(TrainConfig),
+                                      C.POINTER(_P)]),
+    "pact_trainer_step": (C.c_int, [_P, _I]),
+    "pact_trainer_report": (C.c_int, [_P, _I, _DP]),
+    "pact_trainer_run_epoch": (C.c_int, [_P, _I, _DP]),
+    "pact_trainer_finish": (C.c_int, [_P, _P, _P]),
+    "pact_trainer_get_theta": (C.c_int, [_P, _DP]),
+    "pact_trainer_set_theta": (C.c_int, [_P, _DP]),
+    "pact_trainer_buffer": (_P, [_P, _I]),
+    "pact_trainer_destroy": (C.c_int, [_P]),
+    "pact_trainer_launch_count": (C.c_int64, [_P]),
+    "pact_joint_reconstruct": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(SignalMeta), _P,
+                                         C.POINTER(Grid), C.POINTER(Mask),
+                                         C.POINTER(TrainConfig), _DP, _P, _P, _DP]),
 }
 
 _lib = None

@@ -135,3 +135,347 @@ class Context:
     def das(self, signals, ring, meta, grid, v0, d):
         """das, beamform.hpp:56-75 (the K = 1 stack)."""
         return self.das_stack(signals, ring, meta, grid, v0, [d])[0]
+
+
+# --------------------------------------------------------------------------- #
+# patch layout, SIREN, PSF, deconvolution, loss and gradients
+# --------------------------------------------------------------------------- #
+
+@dataclass(frozen=True)
+class PatchLayout:
+    """PatchLayout, core.hpp:222-281 (built by make_patch_layout)."""
+    raw: object
+    offsets: np.ndarray  # [n, 2] (ox, oy)
+    centers: np.ndarray  # [n, 2] world mm
+
+    @property
+    def patch_pixels(self) -> int:
+        return self.raw.patch_pixels
+
+    @property
+    def n_patches(self) -> int:
+        return self.raw.nx * self.raw.ny
+
+    def c(self):
+        return self.raw
+
+
+def make_patch_layout(grid: GridSpec, patch_mm: float, overlap: float) -> PatchLayout:
+    """make_patch_layout, core.hpp:252-281."""
+    L = _abi.lib()
+    lay = _abi.Layout()
+    g = grid.c()
+    check(L.pact_make_patch_layout(C.byref(g), patch_mm, overlap, C.byref(lay)))
+    n = lay.nx * lay.ny
+    off = np.zeros((n, 2), np.int32)
+    cen = np.zeros((n, 2), np.float64)
+    check(L.pact_layout_patches(C.byref(lay), off.ctypes.data_as(C.POINTER(C.c_int32)),
+                                cen.ctypes.data_as(C.POINTER(C.c_double))))
+    return PatchLayout(lay, off, cen)
+
+
+@dataclass(frozen=True)
+class SirenSpec:
+    """SirenParams scalars, nfield.hpp:37-71."""
+    hidden: int = 64
+    n_hidden_layers: int = 2
+    omega0: float = 30.0
+    out_scale: float = 100.0
+    v0: float = 1500.0
+
+    def c(self):
+        return _abi.Siren(2, self.hidden, self.n_hidden_layers, self.omega0, self.out_scale,
+                          self.v0)
+
+    def param_count(self) -> int:
+        s = self.c()
+        return int(_abi.lib().pact_siren_param_count(C.byref(s)))
+
+
+def init_siren(seed: int, spec: SirenSpec) -> np.ndarray:
+    """init_siren, nfield.hpp:83-107 (fp64, bit-identical to the reference)."""
+    th = np.zeros(spec.param_count(), np.float64)
+    s = spec.c()
+    check(_abi.lib().pact_init_siren(seed, C.byref(s), th.ctypes.data_as(C.POINTER(C.c_double))))
+    return th
+
+
+def masked_pixels(grid: GridSpec, mask: CircularMask):
+    """render_sos's masked pixel list: (flat indices, normalised coords)."""
+    L = _abi.lib()
+    g, m = grid.c(), mask.c()
+    n = L.pact_masked_count(C.byref(g), C.byref(m))
+    idx = np.zeros(max(n, 1), np.int32)
+    co = np.zeros((max(n, 1), 2), np.float32)
+    check(L.pact_masked_pixels(C.byref(g), C.byref(m), idx.ctypes.data_as(C.POINTER(C.c_int32)),
+                               co.ctypes.data_as(C.POINTER(C.c_float))))
+    return idx[:n], co[:n]
+
+
+@dataclass(frozen=True)
+class DeconvolveOptions:
+    """DeconvolveOptions, deconv.hpp:166-172."""
+    eps: float = 1e-3
+    n_angles: int = 512
+    ray_step: float = 0.05
+    merge_fwhm: float = 1.5
+
+    def c(self):
+        return _abi.DeconvOptions(self.eps, self.n_angles, self.ray_step, self.merge_fwhm)
+
+
+def _cplx(t: torch.Tensor) -> torch.Tensor:
+    return t if t.dtype == torch.complex64 else t.to(torch.complex64)
+
+
+def _ctx_methods():
+    def render_sos(self, spec: SirenSpec, theta: torch.Tensor, grid: GridSpec,
+                   mask: CircularMask):
+        """render_sos, nfield.hpp:145-162 -> (raster v, deviation v - v0), fp32 [H, W]."""
+        theta = theta.to(device="cuda", dtype=torch.float32).contiguous()
+        raster = torch.empty((grid.height, grid.width), device="cuda", dtype=torch.float32)
+        dev = torch.empty_like(raster)
+        s, g, m = spec.c(), grid.c(), mask.c()
+        check(_abi.lib().pact_render_sos(self._h, C.byref(s), dptr(theta), C.byref(g), C.byref(m),
+                                         dptr(raster), dptr(dev)))
+        return raster, dev
+
+    def siren_backward(self, spec: SirenSpec, theta: torch.Tensor, grid: GridSpec,
+                       mask: CircularMask, grad_masked: torch.Tensor) -> torch.Tensor:
+        """backprop_sos, nfield.hpp:166-233 -> fp64 [param_count]."""
+        theta = theta.to(device="cuda", dtype=torch.float32).contiguous()
+        gm = grad_masked.to(device="cuda", dtype=torch.float32).contiguous()
+        out = torch.empty(spec.param_count(), device="cuda", dtype=torch.float64)
+        s, g, m = spec.c(), grid.c(), mask.c()
+        check(_abi.lib().pact_siren_backward(self._h, C.byref(s), dptr(theta), C.byref(g),
+                                             C.byref(m), dptr(gm), dptr(out)))
+        return out
+
+    def wavefront(self, ring: RingGeometry, grid: GridSpec, sos_dev: torch.Tensor, v0: float,
+                  mask: CircularMask, centers, n_angles: int, step: float) -> torch.Tensor:
+        """wavefront_profile, aberration.hpp:134-186 for every centre -> fp32 [n, A]."""
+        cen = np.ascontiguousarray(np.asarray(centers, np.float64).reshape(-1, 2))
+        n = cen.shape[0]
+        w = torch.empty((n, n_angles), device="cuda", dtype=torch.float32)
+        r, g, m = ring.c(), grid.c(), mask.c()
+        check(_abi.lib().pact_wavefront(self._h, C.byref(r), C.byref(g), dptr(sos_dev.contiguous()),
+                                        v0, C.byref(m), n,
+                                        cen.ctypes.data_as(C.POINTER(C.c_double)), n_angles, step,
+                                        dptr(w)))
+        return w
+
+    def transfer_stack(self, w: torch.Tensor, delays, P: int, pitch: float) -> torch.Tensor:
+        """transfer_stack, aberration.hpp:236-265 -> complex64 [n, K, P, P]."""
+        w = w.contiguous()
+        n, A = w.shape
+        K = len(delays)
+        H = torch.empty((n, K, P, P), device="cuda", dtype=torch.complex64)
+        check(_abi.lib().pact_transfer_stack(self._h, n, dptr(w), A, darr(delays), K, P, pitch,
+                                             dptr(H)))
+        return H
+
+    def patch_spectra(self, layout: PatchLayout, stack: torch.Tensor) -> torch.Tensor:
+        """extract_patch_spectra, deconv.hpp:64-74 -> complex64 [n, K, P, P]."""
+        K = stack.shape[0]
+        P = layout.patch_pixels
+        Y = torch.empty((layout.n_patches, K, P, P), device="cuda", dtype=torch.complex64)
+        lay = layout.c()
+        check(_abi.lib().pact_patch_spectra(self._h, C.byref(lay), dptr(stack.contiguous()), K,
+                                            dptr(Y)))
+        return Y
+
+    def deconvolve_image(self, stack: torch.Tensor, delays, v0: float, sos_dev: torch.Tensor,
+                         ring: RingGeometry, mask: CircularMask, layout: PatchLayout,
+                         opt: DeconvolveOptions) -> torch.Tensor:
+        """deconvolve_image, deconv.hpp:176-198 -> fp32 [H, W]."""
+        g = layout.raw.grid
+        img = torch.empty((g.height, g.width), device="cuda", dtype=torch.float32)
+        r, m, lay, o = ring.c(), mask.c(), layout.c(), opt.c()
+        check(_abi.lib().pact_deconvolve_image(self._h, dptr(stack.contiguous()), len(delays),
+                                               darr(delays), v0, dptr(sos_dev.contiguous()),
+                                               C.byref(r), C.byref(m), C.byref(lay), C.byref(o),
+                                               dptr(img)))
+        return img
+
+    def loss_grad(self, Y: torch.Tensor, w: torch.Tensor, delays, P: int, pitch: float,
+                  eps: float, scale: float, implicit: bool = True):
+        """fused_patch_loss_grad, optimize.hpp:234-325, batched -> (loss fp64 [n], dw fp32 [n, A])."""
+        Y = _cplx(Y).contiguous()
+        w = w.contiguous()
+        n, A = w.shape
+        loss = torch.empty(n, device="cuda", dtype=torch.float64)
+        dw = torch.empty_like(w)
+        check(_abi.lib().pact_loss_grad(self._h, n, dptr(Y), dptr(w), A, darr(delays), len(delays),
+                                        P, pitch, eps, scale, 1 if implicit else 0, dptr(loss),
+                                        dptr(dw)))
+        return loss, dw
+
+    def ray_backward(self, ring: RingGeometry, grid: GridSpec, sos_dev: torch.Tensor, v0: float,
+                     mask: CircularMask, centers, n_angles: int, step: float, dw: torch.Tensor,
+                     grad_v: torch.Tensor | None = None) -> torch.Tensor:
+        """wavefront_grad_trace, aberration.hpp:333-361, batched: grad_v (fp64 [H, W]) +=."""
+        cen = np.ascontiguousarray(np.asarray(centers, np.float64).reshape(-1, 2))
+        if grad_v is None:
+            grad_v = torch.zeros((grid.height, grid.width), device="cuda", dtype=torch.float64)
+        r, g, m = ring.c(), grid.c(), mask.c()
+        check(_abi.lib().pact_ray_backward(self._h, C.byref(r), C.byref(g),
+                                           dptr(sos_dev.contiguous()), v0, C.byref(m),
+                                           cen.shape[0], cen.ctypes.data_as(C.POINTER(C.c_double)),
+                                           n_angles, step, dptr(dw.contiguous()), dptr(grad_v)))
+        return grad_v
+
+    def tv_loss(self, grid: GridSpec, mask: CircularMask, raster: torch.Tensor, lam: float):
+        """tv_loss, optimize.hpp:120-153 -> (value, grad per masked pixel fp32)."""
+        g, m = grid.c(), mask.c()
+        n = _abi.lib().pact_masked_count(C.byref(g), C.byref(m))
+        grad = torch.empty(max(n, 1), device="cuda", dtype=torch.float32)
+        val = C.c_double()
+        check(_abi.lib().pact_tv_loss(self._h, C.byref(g), C.byref(m), dptr(raster.contiguous()),
+                                      lam, C.byref(val), dptr(grad)))
+        return val.value, grad[:n]
+
+    def adam_step(self, theta, grad, m, v, t, lr, beta1, beta2, eps):
+        """adam_step, optimize.hpp:87-110 on fp64 device tensors (t after the update)."""
+        check(_abi.lib().pact_adam_step(self._h, theta.numel(), dptr(theta), dptr(grad), dptr(m),
+                                        dptr(v), t, lr, beta1, beta2, eps))
+
+    for f in (render_sos, siren_backward, wavefront, transfer_stack, patch_spectra,
+              deconvolve_image, loss_grad, ray_backward, tv_loss, adam_step):
+        setattr(Context, f.__name__, f)
+
+
+_ctx_methods()
+
+
+# --------------------------------------------------------------------------- #
+# joint_reconstruct engine
+# --------------------------------------------------------------------------- #
+
+@dataclass
+class TrainConfig:
+    """TrainConfig, optimize.hpp:48-78 (reference defaults)."""
+    epochs: int = 10
+    steps_per_epoch: int = 30
+    learning_rate: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    adam_eps: float = 1e-8
+    lambda_tv: float = 3e9
+    delays: tuple = tuple(-0.8 + 1.6 * j / 31 for j in range(32))
+    eps_deconv: float = 1e-3
+    n_angles: int = 512
+    ray_step: float = 0.05
+    seed: int = 0
+    hidden: int = 64
+    sine_layers: int = 2
+    omega0: float = 30.0
+    out_scale: float = 100.0
+    patch_mm: float = 3.2
+    overlap: float = 0.75
+    merge_fwhm: float = 1.5
+    implicit_xhat_grad: bool = True
+    workers: int = 0
+    use_cuda_graph: bool = True
+
+    def c(self):
+        arr = (C.c_double * len(self.delays))(*[float(d) for d in self.delays])
+        cfg = _abi.TrainConfig(self.epochs, self.steps_per_epoch, self.learning_rate, self.beta1,
+                               self.beta2, self.adam_eps, self.lambda_tv, len(self.delays),
+                               C.cast(arr, C.POINTER(C.c_double)), self.eps_deconv, self.n_angles,
+                               self.ray_step, self.seed, self.hidden, self.sine_layers,
+                               self.omega0, self.out_scale, self.patch_mm, self.overlap,
+                               self.merge_fwhm, 1 if self.implicit_xhat_grad else 0, self.workers,
+                               1 if self.use_cuda_graph else 0)
+        return cfg, arr
+
+
+class Trainer:
+    """pact_trainer: joint_reconstruct (optimize.hpp:367-494) split into
+    create / step / report / finish so the iteration can be timed."""
+
+    def __init__(self, ctx: Context, signals: torch.Tensor, ring: RingGeometry,
+                 meta: SignalMetaInfo, grid: GridSpec, mask: CircularMask, cfg: TrainConfig):
+        self.ctx, self.grid, self.cfg = ctx, grid, cfg
+        self._signals = signals.contiguous()
+        c, self._arr = cfg.c()
+        r, m, g, mk = ring.c(), meta.c(), grid.c(), mask.c()
+        h = C.c_void_p()
+        check(_abi.lib().pact_trainer_create(ctx.handle, C.byref(r), C.byref(m),
+                                             dptr(self._signals), C.byref(g), C.byref(mk),
+                                             C.byref(c), C.byref(h)))
+        self._h = h
+        self.n_params = SirenSpec(cfg.hidden, cfg.sine_layers, cfg.omega0, cfg.out_scale,
+                                  meta.background_sos).param_count()
+
+    def step(self, n: int = 1):
+        check(_abi.lib().pact_trainer_step(self._h, n))
+
+    def report(self, epoch: int = 1):
+        rep = (C.c_double * 3)()
+        check(_abi.lib().pact_trainer_report(self._h, epoch, rep))
+        return list(rep)
+
+    def run_epoch(self, epoch: int):
+        rep = (C.c_double * 4)()
+        check(_abi.lib().pact_trainer_run_epoch(self._h, epoch, rep))
+        return list(rep)
+
+    def finish(self):
+        img = torch.empty((self.grid.height, self.grid.width), device="cuda", dtype=torch.float32)
+        sos = torch.empty_like(img)
+        check(_abi.lib().pact_trainer_finish(self._h, dptr(img), dptr(sos)))
+        return img, sos
+
+    def theta(self) -> np.ndarray:
+        th = np.zeros(self.n_params, np.float64)
+        check(_abi.lib().pact_trainer_get_theta(self._h, th.ctypes.data_as(C.POINTER(C.c_double))))
+        return th
+
+    def set_theta(self, th: np.ndarray):
+        th = np.ascontiguousarray(th, np.float64)
+        check(_abi.lib().pact_trainer_set_theta(self._h, th.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def buffer(self, what: int) -> int:
+        return int(_abi.lib().pact_trainer_buffer(self._h, what) or 0)
+
+    def read(self, what: int, shape, dtype) -> np.ndarray:
+        """Copy an engine buffer (see pact_trainer_buffer) to the host."""
+        out = np.zeros(shape, dtype)
+        check(_abi.lib().pact_trainer_step(self._h, 0))
+        torch.cuda.synchronize()
+        check(_abi.lib().pact_download(self.ctx.handle, C.c_void_p(out.ctypes.data),
+                                       C.c_void_p(self.buffer(what)), out.nbytes))
+        return out
+
+    def launch_count(self) -> int:
+        return int(_abi.lib().pact_trainer_launch_count(self._h))
+
+    def close(self):
+        if self._h:
+            _abi.lib().pact_trainer_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def joint_reconstruct(ctx: Context, signals: torch.Tensor, ring: RingGeometry,
+                      meta: SignalMetaInfo, grid: GridSpec, mask: CircularMask, cfg: TrainConfig):
+    """joint_reconstruct, optimize.hpp:367-494 -> (reports [epochs, 4], image, sos, theta)."""
+    c, arr = cfg.c()
+    reps = np.zeros((cfg.epochs, 4))
+    img = torch.empty((grid.height, grid.width), device="cuda", dtype=torch.float32)
+    sos = torch.empty_like(img)
+    n = SirenSpec(cfg.hidden, cfg.sine_layers, cfg.omega0, cfg.out_scale,
+                  meta.background_sos).param_count()
+    th = np.zeros(n, np.float64)
+    r, m, g, mk = ring.c(), meta.c(), grid.c(), mask.c()
+    check(_abi.lib().pact_joint_reconstruct(ctx.handle, C.byref(r), C.byref(m),
+                                            dptr(signals.contiguous()), C.byref(g), C.byref(mk),
+                                            C.byref(c), reps.ctypes.data_as(C.POINTER(C.c_double)),
+                                            dptr(img), dptr(sos),
+                                            th.ctypes.data_as(C.POINTER(C.c_double))))
+    return reps, img, sos, th

@@ -53,6 +53,9 @@ struct pact_ctx {
   std::atomic<int64_t> launches{0};
   // Named scratch slots so independent entry points do not alias.
   pact_scratch scratch[16];
+  // Per-context caches of the standalone entry points (api.cu).
+  void* api = nullptr;
+  void (*api_free)(void*) = nullptr;
 };
 
 namespace pactgpu {

@@ -74,6 +74,7 @@ int pact_ctx_destroy(pact_ctx* ctx) {
   if (!ctx) return PACT_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->api && ctx->api_free) ctx->api_free(ctx->api);
   for (auto& s : ctx->scratch)
     if (s.ptr) cudaFree(s.ptr);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

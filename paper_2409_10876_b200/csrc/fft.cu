@@ -1,0 +1,245 @@
+// Patch FFTs (part 3): forward 2-D FFT of every (patch, delay) window of the
+// DAS stack (extract_patch_spectra, deconv.hpp:45-74) and inverse 2-D FFT of
+// the deconvolved patch spectra (deconvolve_image, deconv.hpp:193-196), with
+// the reference conventions (fft.hpp:86-115): forward e^{-i}, unscaled;
+// inverse e^{+i}, scaled by 1/(w h); rows first, then columns.
+//
+// One CTA per transform; the P x P complex tile lives in shared memory
+// (32 KB at P = 64, 128 KB at P = 128).  Power-of-two P uses an in-place
+// radix-2 Cooley-Tukey with fp64-accurate fp32 twiddles; other sizes use the
+// direct DFT like the reference.  The patch gather is fused into the load
+// (no separate crop pass) and the inverse keeps only the real part.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace pactgpu {
+namespace {
+
+__device__ __forceinline__ int bitrev(int x, int logn) { return __brev(x) >> (32 - logn); }
+
+__device__ __forceinline__ float2 cm(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// In-place 2-D transform of buf[P][P] (row-major). sign = -1 forward, +1 inverse.
+// tw[q] = exp(sign * 2 pi i q / P) for q < P.  scratch: P*P float2 (DFT path only).
+__device__ void fft2d(float2* buf, float2* scratch, const float2* tw, int P, int logP) {
+  const int P2 = P * P;
+  const int nt = blockDim.x;
+  if (logP >= 0) {
+    // rows: bit-reverse within each row, then butterflies
+    for (int pass = 0; pass < 2; ++pass) {
+      // pass 0: rows (stride 1 within row, rows at stride P); pass 1: columns
+      const int es = pass == 0 ? 1 : P, ls = pass == 0 ? P : 1;
+      for (int e = threadIdx.x; e < P2; e += nt) {
+        // consecutive threads -> consecutive addresses in both passes
+        int line = pass == 0 ? e / P : e % P, i = pass == 0 ? e % P : e / P;
+        int j = bitrev(i, logP);
+        if (i < j) {
+          float2* a = buf + line * ls + i * es;
+          float2* b = buf + line * ls + j * es;
+          float2 t = *a;
+          *a = *b;
+          *b = t;
+        }
+      }
+      __syncthreads();
+      for (int len = 2; len <= P; len <<= 1) {
+        const int half = len >> 1, tstep = P / len;
+        for (int e = threadIdx.x; e < P2 / 2; e += nt) {
+          int line = pass == 0 ? e / (P / 2) : e % P;
+          int bf = pass == 0 ? e % (P / 2) : e / P;
+          int grp = bf / half, k = bf - grp * half;
+          int i0 = grp * len + k;
+          float2* base = buf + line * ls;
+          float2 u = base[i0 * es];
+          float2 v = cm(base[(i0 + half) * es], tw[k * tstep]);
+          base[i0 * es] = make_float2(u.x + v.x, u.y + v.y);
+          base[(i0 + half) * es] = make_float2(u.x - v.x, u.y - v.y);
+        }
+        __syncthreads();
+      }
+    }
+  } else {
+    // direct DFT (fft.hpp:60-71), rows then columns
+    for (int pass = 0; pass < 2; ++pass) {
+      const int es = pass == 0 ? 1 : P, ls = pass == 0 ? P : 1;
+      for (int e = threadIdx.x; e < P2; e += nt) {
+        int line = pass == 0 ? e / P : e % P, k = pass == 0 ? e % P : e / P;
+        const float2* src = buf + line * ls;
+        float2 acc = make_float2(0.f, 0.f);
+        for (int m = 0; m < P; ++m) {
+          float2 p = cm(src[m * es], tw[(k * m) % P]);
+          acc.x += p.x;
+          acc.y += p.y;
+        }
+        scratch[line * ls + k * es] = acc;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < P2; e += nt) buf[e] = scratch[e];
+      __syncthreads();
+    }
+  }
+}
+
+__device__ void make_twiddles(float2* tw, int P, double sign) {
+  for (int q = threadIdx.x; q < P; q += blockDim.x) {
+    double s, c;
+    sincospi(sign * 2.0 * q / P, &s, &c);
+    tw[q] = make_float2(static_cast<float>(c), static_cast<float>(s));
+  }
+}
+
+struct LayoutDev {
+  int P, nx, ny, stride, last_x, last_y, W, H;
+};
+
+// patch_offsets_1d (core.hpp:232-241): offsets 0, s, 2s, ... then the clamped last
+__device__ __forceinline__ int patch_offset(int i, int n, int stride, int last) {
+  return i == n - 1 ? last : i * stride;
+}
+
+// Y[patch][j] = FFT2(stack[j][oy:oy+P, ox:ox+P])       grid (n_patches, K)
+__global__ void patch_fft_kernel(LayoutDev L, const float* __restrict__ stack, int K, int logP,
+                                 float2* __restrict__ Y) {
+  extern __shared__ float2 sm[];
+  const int P = L.P, P2 = P * P;
+  float2* buf = sm;
+  float2* tw = sm + P2;
+  float2* scratch = tw + P;
+  const int patch = blockIdx.x, j = blockIdx.y;
+  const int px = patch % L.nx, py = patch / L.nx;
+  const int ox = patch_offset(px, L.nx, L.stride, L.last_x);
+  const int oy = patch_offset(py, L.ny, L.stride, L.last_y);
+  make_twiddles(tw, P, -1.0);
+  const float* img = stack + static_cast<size_t>(j) * L.W * L.H;
+  for (int e = threadIdx.x; e < P2; e += blockDim.x) {
+    int y = e / P, x = e - y * P;
+    buf[e] = make_float2(img[static_cast<size_t>(oy + y) * L.W + ox + x], 0.f);
+  }
+  __syncthreads();
+  fft2d(buf, scratch, tw, P, logP);
+  float2* out = Y + (static_cast<size_t>(patch) * K + j) * P2;
+  for (int e = threadIdx.x; e < P2; e += blockDim.x) out[e] = buf[e];
+}
+
+// out[patch][P2] = Re(IFFT2(X[patch])) / (P*P)           grid (n_patches)
+__global__ void patch_ifft_real_kernel(int P, int logP, const float2* __restrict__ X,
+                                       float* __restrict__ out) {
+  extern __shared__ float2 sm[];
+  const int P2 = P * P;
+  float2* buf = sm;
+  float2* tw = sm + P2;
+  float2* scratch = tw + P;
+  make_twiddles(tw, P, +1.0);
+  const float2* src = X + static_cast<size_t>(blockIdx.x) * P2;
+  for (int e = threadIdx.x; e < P2; e += blockDim.x) buf[e] = src[e];
+  __syncthreads();
+  fft2d(buf, scratch, tw, P, logP);
+  const float inv = 1.f / static_cast<float>(P2);
+  float* o = out + static_cast<size_t>(blockIdx.x) * P2;
+  for (int e = threadIdx.x; e < P2; e += blockDim.x) o[e] = buf[e].x * inv;
+}
+
+// merge_patches (deconv.hpp:142-164) in gather form: every pixel sums the
+// windowed values of the (<= 3x3) patches covering it in layout order.
+__global__ void merge_kernel(LayoutDev L, const float* __restrict__ patches,
+                             const float* __restrict__ win, float* __restrict__ img) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L.W * L.H) return;
+  int y = i / L.W, x = i - y * L.W;
+  const int P = L.P;
+  float acc = 0.f, ws = 0.f;
+  // Patches covering (x, y), ascending index per axis (= the reference's
+  // row-major accumulation order): offsets i*s for i < n-1, then the last.
+  const int ylo = y - P + 1 <= 0 ? 0 : (y - P + 1 + L.stride - 1) / L.stride;
+  const int yhi = min(y / L.stride, L.ny - 2);
+  const int xlo = x - P + 1 <= 0 ? 0 : (x - P + 1 + L.stride - 1) / L.stride;
+  const int xhi = min(x / L.stride, L.nx - 2);
+  const bool ylast = L.last_y <= y && y < L.last_y + P;
+  const bool xlast = L.last_x <= x && x < L.last_x + P;
+  for (int py = min(ylo, yhi + 1); py <= yhi + 1; ++py) {
+    if (py == yhi + 1) {
+      if (!ylast) break;
+      py = L.ny - 1;
+    }
+    const int oy = patch_offset(py, L.ny, L.stride, L.last_y);
+    for (int px = min(xlo, xhi + 1); px <= xhi + 1; ++px) {
+      if (px == xhi + 1) {
+        if (!xlast) break;
+        px = L.nx - 1;
+      }
+      const int ox = patch_offset(px, L.nx, L.stride, L.last_x);
+      const int q = (y - oy) * P + (x - ox);
+      const float w = win[q];
+      acc += w * patches[static_cast<size_t>(py * L.nx + px) * P * P + q];
+      ws += w;
+    }
+  }
+  img[i] = ws > 0.f ? acc / ws : 0.f;
+}
+
+int ilog2_exact(int P) {
+  int l = 0;
+  while ((1 << l) < P) ++l;
+  return (1 << l) == P ? l : -1;
+}
+
+size_t fft_smem(int P, int logP) {
+  size_t P2 = static_cast<size_t>(P) * P;
+  return sizeof(float2) * (P2 + P + (logP >= 0 ? 0 : P2));
+}
+
+LayoutDev layout_dev(const pact_layout& l) {
+  LayoutDev d;
+  d.P = l.patch_pixels;
+  d.nx = l.nx;
+  d.ny = l.ny;
+  d.stride = l.stride_pixels;
+  d.last_x = l.last_x;
+  d.last_y = l.last_y;
+  d.W = l.grid.width;
+  d.H = l.grid.height;
+  return d;
+}
+
+}  // namespace
+
+Status launch_patch_fft(pact_ctx* ctx, const pact_layout& lay, const float* stack, int K,
+                        float2* Y) {
+  const int P = lay.patch_pixels, logP = ilog2_exact(P);
+  size_t smem = fft_smem(P, logP);
+  if (smem > 220 * 1024) return validation("extract_patch_spectra: patch too large for the device FFT");
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    PACT_CUDA_S(cudaFuncSetAttribute(patch_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    configured = smem;
+  }
+  dim3 g(lay.nx * lay.ny, K);
+  patch_fft_kernel<<<g, 512, smem, ctx->stream>>>(layout_dev(lay), stack, K, logP, Y);
+  return after_launch(ctx, "patch_fft_kernel");
+}
+
+Status launch_patch_ifft_real(pact_ctx* ctx, int P, int n_patches, const float2* X, float* out) {
+  const int logP = ilog2_exact(P);
+  size_t smem = fft_smem(P, logP);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    PACT_CUDA_S(cudaFuncSetAttribute(patch_ifft_real_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  patch_ifft_real_kernel<<<n_patches, 512, smem, ctx->stream>>>(P, logP, X, out);
+  return after_launch(ctx, "patch_ifft_real_kernel");
+}
+
+Status launch_merge(pact_ctx* ctx, const pact_layout& lay, const float* patches, const float* win,
+                    float* img) {
+  int n = lay.grid.width * lay.grid.height;
+  merge_kernel<<<div_up(n, 256), 256, 0, ctx->stream>>>(layout_dev(lay), patches, win, img);
+  return after_launch(ctx, "merge_kernel");
+}
+
+}  // namespace pactgpu

@@ -1,0 +1,430 @@
+// Part 2/3 Fourier-domain kernels: transfer stacks H_j(k) from the wavefront
+// profiles, the fused |k|-weighted multichannel loss with its gradient pulled
+// back to dL/dw, and the Wiener (pseudo-inverse) deconvolution epilogue.
+//
+//   transfer_stack                aberration.hpp:236-265
+//   conj_symmetrize_nyquist       aberration.hpp:203-218
+//   detail::fused_patch_loss_grad optimize.hpp:234-325
+//   multichannel_deconvolve       deconv.hpp:78-96
+//
+// One thread owns one frequency bin of one patch and walks the M delay
+// channels (coalesced over bins: Y is [patch][M][P][P]).  Bins on the Nyquist
+// row/column (even P) also evaluate their conjugate partner so the reference's
+// symmetrisation of H and of dL/dH is reproduced without a second pass.
+// dL/dw is accumulated per bin, then gathered per angle through a static CSR
+// table (deterministic; no atomics).  The loss is reduced per patch in fp64.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "fourier.cuh"
+
+namespace pactgpu {
+
+void fourier_table_free(FourierTable& t) {
+  if (t.dev) cudaFree(t.dev);
+  t.dev = nullptr;
+  t.bytes = 0;
+  t.P = 0;
+}
+
+Status fourier_table(pact_ctx* ctx, FourierTable& t, int P, double pitch, int A,
+                     const double* delays, int K) {
+  if (t.dev && t.P == P && t.pitch == pitch && t.A == A && t.K == K &&
+      std::equal(t.delays.begin(), t.delays.end(), delays))
+    return {};
+  const int P2 = P * P;
+  const double tau = 2.0 * M_PI;
+  std::vector<float> kmag(P2);
+  std::vector<int4> idx(P2);
+  std::vector<float2> frac(P2);
+  std::vector<int> mirror(P2, -1);
+  std::vector<float2> dp(static_cast<size_t>(K) * P2);
+  // PatchBinTable::make, aberration.hpp:373-401
+  auto interp = [&](double theta, int& i0, int& i1, double& f) {
+    double pos = std::fmod(theta, tau);
+    if (pos < 0) pos += tau;
+    pos = pos / tau * A;
+    i0 = static_cast<int>(pos) % A;
+    f = pos - std::floor(pos);
+    i1 = (i0 + 1) % A;
+  };
+  const double scale = 2.0 * M_PI / (P * pitch);
+  const int half = P / 2;
+  for (int by = 0; by < P; ++by)
+    for (int bx = 0; bx < P; ++bx) {
+      int b = by * P + bx;
+      double kx = scale * (bx <= P / 2 ? bx : bx - P);
+      double ky = scale * (by <= P / 2 ? by : by - P);
+      double k = std::hypot(kx, ky), ang = std::atan2(ky, kx);
+      int a0, a1, b0, b1;
+      double f1, f2;
+      interp(ang, a0, a1, f1);
+      interp(ang + M_PI, b0, b1, f2);
+      kmag[b] = static_cast<float>(k);
+      idx[b] = make_int4(a0, a1, b0, b1);
+      frac[b] = make_float2(static_cast<float>(f1), static_cast<float>(f2));
+      if (P % 2 == 0 && (bx == half || by == half))
+        mirror[b] = ((P - by) % P) * P + (P - bx) % P;
+      for (int j = 0; j < K; ++j) {
+        // make_delay_phases, optimize.hpp:229: polar(1, -|k| d_j)
+        double ph = -k * delays[j];
+        dp[static_cast<size_t>(j) * P2 + b] =
+            make_float2(static_cast<float>(std::cos(ph)), static_cast<float>(std::sin(ph)));
+      }
+    }
+  // angle -> (bin, branch, weight): the scatter of fused_patch_loss_grad
+  // (optimize.hpp:318-321) as a gather.
+  std::vector<int> start(A + 1, 0);
+  for (int b = 0; b < P2; ++b) {
+    start[idx[b].x + 1]++;
+    start[idx[b].y + 1]++;
+    start[idx[b].z + 1]++;
+    start[idx[b].w + 1]++;
+  }
+  for (int a = 0; a < A; ++a) start[a + 1] += start[a];
+  std::vector<int> key(4 * P2);
+  std::vector<float> wt(4 * P2);
+  std::vector<int> fill(start.begin(), start.end() - 1);
+  for (int b = 0; b < P2; ++b) {
+    double f1 = frac[b].x, f2 = frac[b].y;
+    key[fill[idx[b].x]] = (b << 1);
+    wt[fill[idx[b].x]++] = static_cast<float>(1.0 - f1);
+    key[fill[idx[b].y]] = (b << 1);
+    wt[fill[idx[b].y]++] = static_cast<float>(f1);
+    key[fill[idx[b].z]] = (b << 1) | 1;
+    wt[fill[idx[b].z]++] = static_cast<float>(1.0 - f2);
+    key[fill[idx[b].w]] = (b << 1) | 1;
+    wt[fill[idx[b].w]++] = static_cast<float>(f2);
+  }
+  // one device allocation, 16-byte aligned sections
+  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+  size_t o_kmag = 0, o_idx = al(o_kmag + 4 * P2), o_frac = al(o_idx + 16 * P2),
+         o_mirror = al(o_frac + 8 * P2), o_dp = al(o_mirror + 4 * P2),
+         o_start = al(o_dp + 8 * static_cast<size_t>(K) * P2), o_key = al(o_start + 4 * (A + 1)),
+         o_wt = al(o_key + 16 * P2), total = al(o_wt + 16 * P2);
+  std::vector<char> host(total, 0);
+  std::memcpy(host.data() + o_kmag, kmag.data(), 4 * P2);
+  std::memcpy(host.data() + o_idx, idx.data(), 16 * P2);
+  std::memcpy(host.data() + o_frac, frac.data(), 8 * P2);
+  std::memcpy(host.data() + o_mirror, mirror.data(), 4 * P2);
+  std::memcpy(host.data() + o_dp, dp.data(), 8 * dp.size());
+  std::memcpy(host.data() + o_start, start.data(), 4 * (A + 1));
+  std::memcpy(host.data() + o_key, key.data(), 16 * P2);
+  std::memcpy(host.data() + o_wt, wt.data(), 16 * P2);
+  if (t.dev && t.bytes < total) {
+    PACT_CUDA_S(cudaStreamSynchronize(ctx->stream));
+    fourier_table_free(t);
+  }
+  if (!t.dev) {
+    PACT_CUDA_S(cudaMalloc(&t.dev, total));
+    t.bytes = total;
+  }
+  PACT_CUDA_S(cudaMemcpyAsync(t.dev, host.data(), total, cudaMemcpyHostToDevice, ctx->stream));
+  PACT_CUDA_S(cudaStreamSynchronize(ctx->stream));  // `host` goes out of scope
+  char* d = static_cast<char*>(t.dev);
+  t.P = P;
+  t.A = A;
+  t.K = K;
+  t.pitch = pitch;
+  t.delays.assign(delays, delays + K);
+  t.tab.P = P;
+  t.tab.P2 = P2;
+  t.tab.A = A;
+  t.tab.K = K;
+  t.tab.kmag = reinterpret_cast<const float*>(d + o_kmag);
+  t.tab.idx = reinterpret_cast<const int4*>(d + o_idx);
+  t.tab.frac = reinterpret_cast<const float2*>(d + o_frac);
+  t.tab.mirror = reinterpret_cast<const int*>(d + o_mirror);
+  t.tab.dp = reinterpret_cast<const float2*>(d + o_dp);
+  t.tab.csr_start = reinterpret_cast<const int*>(d + o_start);
+  t.tab.csr_key = reinterpret_cast<const int*>(d + o_key);
+  t.tab.csr_wt = reinterpret_cast<const float*>(d + o_wt);
+  return {};
+}
+
+namespace {
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // conj(a) * b
+  return make_float2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
+
+// e1 = exp(+i|k| w(angle)), e2 = exp(-i|k| w(angle + pi)) for bin b
+// (optimize.hpp:261-265), w interpolated from the patch profile in smem.
+__device__ __forceinline__ void bin_phases(const FourierTab& t, const float* __restrict__ w, int b,
+                                           float2& e1, float2& e2) {
+  float k = t.kmag[b];
+  int4 ix = t.idx[b];
+  float2 fr = t.frac[b];
+  float w1 = (1.f - fr.x) * w[ix.x] + fr.x * w[ix.y];
+  float w2 = (1.f - fr.y) * w[ix.z] + fr.y * w[ix.w];
+  float s, c;
+  sincosf(k * w1, &s, &c);
+  e1 = make_float2(c, s);
+  sincosf(k * w2, &s, &c);
+  e2 = make_float2(c, -s);
+}
+
+// h_j = 1/2 (dp_j e1 + conj(dp_j) e2)   (optimize.hpp:270-271)
+__device__ __forceinline__ float2 h_of(float2 dp, float2 e1, float2 e2) {
+  float2 a = cmul(dp, e1), b = cmul(conjf2(dp), e2);
+  return make_float2(0.5f * (a.x + b.x), 0.5f * (a.y + b.y));
+}
+
+// Symmetrised H_j at bin b (partner m = -1 for ordinary bins).
+__device__ __forceinline__ float2 h_sym(const FourierTab& t, int j, int b, int m, float2 e1b,
+                                        float2 e2b, float2 e1m, float2 e2m) {
+  float2 hb = h_of(t.dp[j * t.P2 + b], e1b, e2b);
+  if (m < 0) return hb;
+  float2 hm = h_of(t.dp[j * t.P2 + m], e1m, e2m);
+  return make_float2(0.5f * (hb.x + hm.x), 0.5f * (hb.y - hm.y));  // (h_b + conj h_m)/2
+}
+
+__global__ void transfer_stack_kernel(FourierTab t, const float* __restrict__ w_all, int n_patches,
+                                      float2* __restrict__ H) {
+  extern __shared__ float s_w[];
+  const int patch = blockIdx.y;
+  for (int a = threadIdx.x; a < t.A; a += blockDim.x) s_w[a] = w_all[patch * t.A + a];
+  __syncthreads();
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= t.P2) return;
+  float2 e1b, e2b, e1m = {}, e2m = {};
+  bin_phases(t, s_w, b, e1b, e2b);
+  int m = t.mirror[b];
+  if (m >= 0) bin_phases(t, s_w, m, e1m, e2m);
+  float2* out = H + static_cast<size_t>(patch) * t.K * t.P2 + b;
+  for (int j = 0; j < t.K; ++j) out[j * t.P2] = h_sym(t, j, b, m, e1b, e2b, e1m, e2m);
+}
+
+// Per-bin state of the loss chain (optimize.hpp:275-311).
+struct BinLoss {
+  float2 x;    // X-hat
+  float den;   // sum |h|^2 + eps M
+  float2 G;    // sum conj(r_j) h_j
+  float gx;    // Re(G X)
+  float wk;    // |k| * scale
+};
+
+// Pass 1 + 2 for one bin whose symmetrised H is h_sym(...) (or its conjugate
+// when `conj_h` — the partner of a Nyquist bin).
+__device__ __forceinline__ BinLoss bin_loss(const FourierTab& t, const float2* __restrict__ Y,
+                                            int b, int hb, int hm, float2 e1b, float2 e2b,
+                                            float2 e1m, float2 e2m, bool conj_h, float eps_m,
+                                            float scale, double& value) {
+  BinLoss L;
+  L.wk = t.kmag[b] * scale;
+  float2 num = make_float2(0.f, 0.f);
+  float den = eps_m;
+  for (int j = 0; j < t.K; ++j) {
+    float2 h = h_sym(t, j, hb, hm, e1b, e2b, e1m, e2m);
+    if (conj_h) h.y = -h.y;
+    float2 y = Y[j * t.P2 + b];
+    float2 c = cmulc(h, y);
+    num.x += c.x;
+    num.y += c.y;
+    den += h.x * h.x + h.y * h.y;
+  }
+  L.den = den;
+  L.x = den > 0.f ? make_float2(num.x / den, num.y / den) : make_float2(0.f, 0.f);
+  float2 G = make_float2(0.f, 0.f);
+  float acc = 0.f;
+  for (int j = 0; j < t.K; ++j) {
+    float2 h = h_sym(t, j, hb, hm, e1b, e2b, e1m, e2m);
+    if (conj_h) h.y = -h.y;
+    float2 y = Y[j * t.P2 + b];
+    float2 hx = cmul(h, L.x);
+    float2 r = make_float2(y.x - hx.x, y.y - hx.y);
+    acc += r.x * r.x + r.y * r.y;
+    float2 c = cmulc(r, h);
+    G.x += c.x;
+    G.y += c.y;
+  }
+  value += static_cast<double>(L.wk) * acc;
+  L.G = G;
+  L.gx = G.x * L.x.x - G.y * L.x.y;
+  return L;
+}
+
+// dL/dH_j at bin b (explicit + implicit terms, optimize.hpp:290-311).
+__device__ __forceinline__ float2 bin_grad(const BinLoss& L, float2 h, float2 y, bool implicit) {
+  float2 hx = cmul(h, L.x);
+  float2 r = make_float2(y.x - hx.x, y.y - hx.y);
+  float2 z = cmulc(r, L.x);
+  float2 g = make_float2(-2.f * L.wk * z.x, 2.f * L.wk * z.y);
+  if (implicit && L.den > 0.f) {
+    float2 gy = cmul(L.G, y);
+    float inv = 1.f / L.den;
+    g.x += (-2.f * L.wk * gy.x + 4.f * L.wk * L.gx * h.x) * inv;
+    g.y += (-2.f * L.wk * gy.y + 4.f * L.wk * L.gx * h.y) * inv;
+  }
+  return g;
+}
+
+__global__ void __launch_bounds__(512) loss_grad_kernel(FourierTab t, const float2* __restrict__ Y_all,
+                                                        const float* __restrict__ w_all, float eps_m,
+                                                        float scale, int implicit,
+                                                        double* __restrict__ loss_out,
+                                                        float* __restrict__ dw_out) {
+  extern __shared__ float smem[];
+  float* s_w = smem;               // [A]
+  float* s_g1 = smem + t.A;        // [P2]
+  float* s_g2 = s_g1 + t.P2;       // [P2]
+  __shared__ double s_red[32];
+  const int patch = blockIdx.x;
+  for (int a = threadIdx.x; a < t.A; a += blockDim.x) s_w[a] = w_all[patch * t.A + a];
+  __syncthreads();
+  const float2* Y = Y_all + static_cast<size_t>(patch) * t.K * t.P2;
+  double value = 0.0;
+  for (int b = threadIdx.x; b < t.P2; b += blockDim.x) {
+    float G1 = 0.f, G2 = 0.f;
+    if (t.kmag[b] * scale != 0.f) {
+      float2 e1b, e2b, e1m = {}, e2m = {};
+      bin_phases(t, s_w, b, e1b, e2b);
+      const int m = t.mirror[b];
+      if (m >= 0) bin_phases(t, s_w, m, e1m, e2m);
+      BinLoss Lb = bin_loss(t, Y, b, b, m, e1b, e2b, e1m, e2m, false, eps_m, scale, value);
+      BinLoss Lm;
+      if (m >= 0) {
+        double dummy = 0.0;  // the partner's own thread adds its loss
+        Lm = bin_loss(t, Y, m, b, m, e1b, e2b, e1m, e2m, true, eps_m, scale, dummy);
+      }
+      const float k = t.kmag[b];
+      for (int j = 0; j < t.K; ++j) {
+        float2 h = h_sym(t, j, b, m, e1b, e2b, e1m, e2m);
+        float2 g = bin_grad(Lb, h, Y[j * t.P2 + b], implicit != 0);
+        if (m >= 0) {  // self-adjoint symmetrisation of dL/dH (optimize.hpp:306-308)
+          float2 gm = bin_grad(Lm, conjf2(h), Y[j * t.P2 + m], implicit != 0);
+          g = make_float2(0.5f * (g.x + gm.x), 0.5f * (g.y - gm.y));
+        }
+        // pullback through t1 = dp e1 / 2, t2 = conj(dp) e2 / 2 (optimize.hpp:314-317)
+        float2 dp = t.dp[j * t.P2 + b];
+        float2 t1 = cmul(dp, e1b), t2 = cmul(conjf2(dp), e2b);
+        G1 += 0.5f * k * (g.x * -t1.y + g.y * t1.x);
+        G2 += 0.5f * k * (g.x * t2.y - g.y * t2.x);
+      }
+    }
+    s_g1[b] = G1;
+    s_g2[b] = G2;
+  }
+  // deterministic block reduction of the patch loss
+  for (int o = 16; o > 0; o >>= 1) value += __shfl_xor_sync(0xffffffffu, value, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = value;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int nw = blockDim.x >> 5;
+    double v = threadIdx.x < nw ? s_red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) loss_out[patch] = v;
+  }
+  // dL/dw gather per angle
+  for (int a = threadIdx.x; a < t.A; a += blockDim.x) {
+    float acc = 0.f;
+    for (int e = t.csr_start[a]; e < t.csr_start[a + 1]; ++e) {
+      int key = t.csr_key[e];
+      acc += t.csr_wt[e] * ((key & 1) ? s_g2[key >> 1] : s_g1[key >> 1]);
+    }
+    dw_out[patch * t.A + a] = acc;
+  }
+}
+
+// X = sum_j conj(H_j) Y_j / (sum_j |H_j|^2 + eps M), 0 where den == 0
+// (multichannel_deconvolve, deconv.hpp:78-96), H from the wavefront profile.
+__global__ void wiener_kernel(FourierTab t, const float2* __restrict__ Y_all,
+                              const float* __restrict__ w_all, float eps_m,
+                              float2* __restrict__ X_all) {
+  extern __shared__ float s_w[];
+  const int patch = blockIdx.y;
+  for (int a = threadIdx.x; a < t.A; a += blockDim.x) s_w[a] = w_all[patch * t.A + a];
+  __syncthreads();
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= t.P2) return;
+  float2 e1b, e2b, e1m = {}, e2m = {};
+  bin_phases(t, s_w, b, e1b, e2b);
+  int m = t.mirror[b];
+  if (m >= 0) bin_phases(t, s_w, m, e1m, e2m);
+  const float2* Y = Y_all + static_cast<size_t>(patch) * t.K * t.P2;
+  float2 num = make_float2(0.f, 0.f);
+  float den = eps_m;
+  for (int j = 0; j < t.K; ++j) {
+    float2 h = h_sym(t, j, b, m, e1b, e2b, e1m, e2m);
+    float2 c = cmulc(h, Y[j * t.P2 + b]);
+    num.x += c.x;
+    num.y += c.y;
+    den += h.x * h.x + h.y * h.y;
+  }
+  X_all[static_cast<size_t>(patch) * t.P2 + b] =
+      den > 0.f ? make_float2(num.x / den, num.y / den) : make_float2(0.f, 0.f);
+}
+
+}  // namespace
+
+Status launch_transfer_stack(pact_ctx* ctx, const FourierTab& t, const float* w, int n_patches,
+                             float2* H) {
+  dim3 g(div_up(t.P2, 256), n_patches);
+  transfer_stack_kernel<<<g, 256, t.A * sizeof(float), ctx->stream>>>(t, w, n_patches, H);
+  return after_launch(ctx, "transfer_stack_kernel");
+}
+
+Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, const float* w,
+                        int n_patches, double eps, double scale, bool implicit, double* loss,
+                        float* dw) {
+  size_t smem = sizeof(float) * (t.A + 2 * t.P2);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    PACT_CUDA_S(cudaFuncSetAttribute(loss_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    configured = smem;
+  }
+  loss_grad_kernel<<<n_patches, 512, smem, ctx->stream>>>(
+      t, Y, w, static_cast<float>(eps * t.K), static_cast<float>(scale), implicit ? 1 : 0, loss,
+      dw);
+  return after_launch(ctx, "loss_grad_kernel");
+}
+
+Status launch_wiener(pact_ctx* ctx, const FourierTab& t, const float2* Y, const float* w,
+                     int n_patches, double eps, float2* X) {
+  dim3 g(div_up(t.P2, 256), n_patches);
+  wiener_kernel<<<g, 256, t.A * sizeof(float), ctx->stream>>>(t, Y, w,
+                                                              static_cast<float>(eps * t.K), X);
+  return after_launch(ctx, "wiener_kernel");
+}
+
+}  // namespace pactgpu
+
+using namespace pactgpu;
+
+namespace {
+FourierTable g_tab_api;  // table cache for the standalone entry points
+}
+
+extern "C" int pact_transfer_stack(pact_ctx* ctx, int32_t n_patches, const float* w,
+                                   int32_t n_angles, const double* delays, int32_t K, int32_t P,
+                                   double pitch, float* H) {
+  if (!ctx || !w || !H || (!delays && K > 0))
+    return validation("pact_transfer_stack: null argument").code;
+  if (P < 1) return validation("transfer_stack: patch_pixels must be >= 1").code;
+  if (!(pitch > 0.0)) return validation("transfer_stack: pitch must be > 0").code;
+  if (n_angles < 1 || K < 1 || n_patches < 1) return validation("transfer_stack: empty input").code;
+  PACT_TRY(fourier_table(ctx, g_tab_api, P, pitch, n_angles, delays, K));
+  PACT_TRY(launch_transfer_stack(ctx, g_tab_api.tab, w, n_patches, reinterpret_cast<float2*>(H)));
+  return PACT_OK;
+}
+
+extern "C" int pact_loss_grad(pact_ctx* ctx, int32_t n_patches, const float* Y, const float* w,
+                              int32_t n_angles, const double* delays, int32_t K, int32_t P,
+                              double pitch, double eps, double scale, int32_t implicit,
+                              double* loss_per_patch, float* dw) {
+  if (!ctx || !Y || !w || !loss_per_patch || !dw || (!delays && K > 0))
+    return validation("pact_loss_grad: null argument").code;
+  if (K < 1) return validation("data_loss: no channels").code;
+  if (n_patches < 1) return validation("data_loss: no patches").code;
+  if (P < 1 || !(pitch > 0.0) || n_angles < 1) return validation("pact_loss_grad: bad geometry").code;
+  PACT_TRY(fourier_table(ctx, g_tab_api, P, pitch, n_angles, delays, K));
+  PACT_TRY(launch_loss_grad(ctx, g_tab_api.tab, reinterpret_cast<const float2*>(Y), w, n_patches,
+                            eps, scale, implicit != 0, loss_per_patch, dw));
+  return PACT_OK;
+}

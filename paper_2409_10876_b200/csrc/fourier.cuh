@@ -1,0 +1,40 @@
+// Frequency-grid tables shared by the transfer-stack, fused loss/gradient and
+// Wiener-deconvolution kernels (one set per patch layout, like the
+// reference's PatchBinTable, aberration.hpp:365-402, and delay phase table,
+// optimize.hpp:223-232).
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace pactgpu {
+
+struct FourierTab {
+  int P = 0, P2 = 0, A = 0, K = 0;
+  const float* kmag = nullptr;    // [P2] |k| rad/mm
+  const int4* idx = nullptr;      // [P2] (a0, a1, b0, b1) interpolation indices
+  const float2* frac = nullptr;   // [P2] (f1, f2)
+  const int* mirror = nullptr;    // [P2] conjugate partner for Nyquist bins, -1 otherwise
+  const float2* dp = nullptr;     // [K][P2] exp(-i |k| d_j)
+  const int* csr_start = nullptr; // [A+1] angle -> contributions
+  const int* csr_key = nullptr;   // [4 P2] (bin << 1) | (0: via w1, 1: via w2)
+  const float* csr_wt = nullptr;  // [4 P2] interpolation weight
+};
+
+// Host-built table (fp64 reference formulas, stored fp32) + its device copy.
+struct FourierTable {
+  int P = 0, A = 0, K = 0;
+  double pitch = 0.0;
+  std::vector<double> delays;
+  void* dev = nullptr;
+  size_t bytes = 0;
+  FourierTab tab;
+};
+
+// Builds (or reuses, if parameters match) the table on the device.
+Status fourier_table(pact_ctx* ctx, FourierTable& t, int P, double pitch, int n_angles,
+                     const double* delays, int K);
+void fourier_table_free(FourierTable& t);
+
+}  // namespace pactgpu

@@ -1,0 +1,126 @@
+// Device/host geometry shared by the ray-march, PSF and TV kernels.  Each
+// helper restates one reference routine (file:line) with identical
+// branch structure; ray setup stays in fp64 like the reference so step counts
+// n = max(1, ceil((t1 - t0)/step)) match exactly.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "pact_cuda.h"
+
+namespace pactgpu {
+
+#define PACT_HD __host__ __device__ __forceinline__
+
+// segment_circle_intersection, core.hpp:184-204.  Returns false for an empty
+// interval (the reference's {1, 0}).
+PACT_HD bool seg_circle(double ax, double ay, double bx, double by, double cx, double cy,
+                        double r, double& t0, double& t1) {
+  double dx = bx - ax, dy = by - ay;
+  double len = hypot(dx, dy);
+  if (len == 0.0) {
+    bool inside = hypot(ax - cx, ay - cy) <= r;
+    t0 = inside ? 0.0 : 1.0;
+    t1 = 0.0;
+    return t0 <= t1 && inside;
+  }
+  double ux = dx * (1.0 / len), uy = dy * (1.0 / len);
+  double mx = ax - cx, my = ay - cy;
+  double bq = mx * ux + my * uy;
+  double cq = (mx * mx + my * my) - r * r;
+  double disc = bq * bq - cq;
+  if (disc < 0.0) {
+    t0 = 1.0;
+    t1 = 0.0;
+    return false;
+  }
+  double s = sqrt(disc);
+  t0 = fmax(-bq - s, 0.0);
+  t1 = fmin(-bq + s, len);
+  if (t0 > t1) {
+    t0 = 1.0;
+    t1 = 0.0;
+    return false;
+  }
+  return true;
+}
+
+// Ray of wavefront_profile / wavefront_grad_trace (aberration.hpp:153-171):
+// direction theta = 2 pi a / n_angles from `center` to the ring, clipped to
+// the mask disc.  Marching positions are p_i = center + u (t0 + (i + 0.5) dl).
+struct Ray {
+  double ux, uy;  // direction
+  double t0;      // first arclength of the clipped segment
+  double dl;      // step
+  int n;          // number of midpoint steps (0 = no contribution)
+};
+
+PACT_HD Ray make_ray(double cx, double cy, int a, int n_angles, double ring_r, double mcx,
+                     double mcy, double mr, double step) {
+  Ray ray;
+  double theta = 2.0 * M_PI * a / n_angles;  // WavefrontProfile::angle, aberration.hpp:116
+  ray.ux = cos(theta);
+  ray.uy = sin(theta);
+  double b = cx * ray.ux + cy * ray.uy;
+  double c = (cx * cx + cy * cy) - ring_r * ring_r;
+  double t_ring = -b + sqrt(b * b - c);
+  double ex = cx + ray.ux * t_ring, ey = cy + ray.uy * t_ring;
+  double t0, t1;
+  seg_circle(cx, cy, ex, ey, mcx, mcy, mr, t0, t1);
+  ray.n = 0;
+  ray.t0 = 0.0;
+  ray.dl = 0.0;
+  if (t0 >= t1) return ray;  // aberration.hpp:163
+  int n = static_cast<int>(ceil((t1 - t0) / step));
+  ray.n = n < 1 ? 1 : n;
+  ray.dl = (t1 - t0) / ray.n;
+  ray.t0 = t0;
+  return ray;
+}
+
+// Clamped bilinear stencil, detail::bilinear_stencil (aberration.hpp:41-72),
+// in fp32 relative to the grid origin (fx, fy are pixel coordinates).
+struct Stencil {
+  int i00, i01, i10, i11;  // idx[0..3]
+  float w00, w01, w10, w11;
+};
+
+__device__ __forceinline__ Stencil stencil_at(float fx, float fy, int W, int H) {
+  fx = fminf(fmaxf(fx, 0.f), static_cast<float>(W - 1));
+  fy = fminf(fmaxf(fy, 0.f), static_cast<float>(H - 1));
+  int ix = min(static_cast<int>(fx), max(W - 2, 0));
+  int iy = min(static_cast<int>(fy), max(H - 2, 0));
+  float ax = fx - ix, ay = fy - iy;
+  int ix1 = min(ix + 1, W - 1), iy1 = min(iy + 1, H - 1);
+  Stencil s;
+  s.i00 = iy * W + ix;
+  s.i01 = iy * W + ix1;
+  s.i10 = iy1 * W + ix;
+  s.i11 = iy1 * W + ix1;
+  s.w00 = (1.f - ax) * (1.f - ay);
+  s.w01 = ax * (1.f - ay);
+  s.w10 = (1.f - ax) * ay;
+  s.w11 = ax * ay;
+  return s;
+}
+
+// Arguments of the ray-march kernels (raymarch.cu).
+struct RayArgs {
+  const float* dv;  // SOS deviation raster v - v0, [H][W]
+  int W, H;
+  double ox, oy, inv_pitch;
+  double v0;
+  double ring_r;
+  double mcx, mcy, mr;
+  double step;
+  int n_angles;
+  int n_rays;
+  const double2* centers;  // [n_centers]
+};
+
+// freq_index, fft.hpp:35
+PACT_HD int freq_index(int i, int n) { return i <= n / 2 ? i : i - n; }
+
+}  // namespace pactgpu

@@ -1,0 +1,625 @@
+// SIREN coordinate network (part 2's SOS field and part 3's last gradient
+// link), nfield.hpp:110-233:
+//   forward   a_0 = W_0 c + b_0,  a_l = W_l sin(w0 a_{l-1}) + b_l,
+//             v = v0 + out_scale (w_L . sin(w0 a_{L-1}) + b_L)
+//   backward  reverse mode of sum_m g_m v(m) (backprop_sos, nfield.hpp:166-233)
+//
+// B200 design: per-layer fp32 SIMT GEMMs (128-pixel x 128-unit tiles, 8x8
+// register micro-tiles, 256 threads) with the sine / cosine folded into the
+// operand loaders and epilogues, so no z_l = sin(w0 a_l) tensor is ever
+// stored: only the pre-activations a_l (needed for the cosine of the
+// backward) are written.  Weight gradients are split over pixel chunks and
+// reduced in a fixed order in fp64 (bitwise deterministic).  TF32/BF16 tensor
+// cores fail the 1e-4 PSF tolerance for this network, so the
+// dense layers stay on the FP32 pipe here.  Hidden widths that are not a
+// multiple of 64 (unit-test networks) take a per-pixel path.
+#include <cmath>
+#include <random>
+
+#include "siren.cuh"
+
+namespace pactgpu {
+
+MaskedPixels masked_pixels(const pact_grid& g, const pact_mask& m) {
+  MaskedPixels mp;
+  for (int iy = 0; iy < g.height; ++iy)
+    for (int ix = 0; ix < g.width; ++ix) {
+      double px = g.origin_x + ix * g.pitch, py = g.origin_y + iy * g.pitch;
+      if (!(std::hypot(px - m.center_x, py - m.center_y) <= m.radius)) continue;
+      mp.idx.push_back(iy * g.width + ix);
+      mp.coords.push_back(static_cast<float>((px - m.center_x) / m.radius));
+      mp.coords.push_back(static_cast<float>((py - m.center_y) / m.radius));
+    }
+  mp.n = static_cast<int>(mp.idx.size());
+  return mp;
+}
+
+namespace {
+
+constexpr int BM = 128, BK = 16, NT = 256;
+
+__device__ __forceinline__ float sinw(float a, float w0) { return sinf(w0 * a); }
+__device__ __forceinline__ float dsinw(float a, float w0) { return w0 * cosf(w0 * a); }
+
+// ---- tiled GEMM core: acc[8 rows][TN cols] += As[kk][rows] * Bs[kk][cols] ----
+template <int BN>
+struct TileShape {
+  static constexpr int TN = BN / 16;  // 8 (BN=128) or 4 (BN=64)
+};
+
+// column owned by thread tx, slot j (interleaved so a warp's LDS.128 are contiguous)
+template <int BN>
+__device__ __forceinline__ int tcol(int tx, int j) {
+  return BN == 128 ? ((j < 4) ? tx * 4 + j : 64 + tx * 4 + (j - 4)) : tx * 4 + j;
+}
+
+template <int BN>
+__device__ __forceinline__ void mma_tile(const float* __restrict__ As, const float* __restrict__ Bs,
+                                         float (&acc)[8][TileShape<BN>::TN], int ty, int tx) {
+  constexpr int TN = TileShape<BN>::TN;
+#pragma unroll
+  for (int kk = 0; kk < BK; ++kk) {
+    float a[8], b[TN];
+    float4 a0 = *reinterpret_cast<const float4*>(As + kk * BM + ty * 8);
+    float4 a1 = *reinterpret_cast<const float4*>(As + kk * BM + ty * 8 + 4);
+    a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+    a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+    float4 b0 = *reinterpret_cast<const float4*>(Bs + kk * BN + tx * 4);
+    b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+    if constexpr (TN == 8) {
+      float4 b1 = *reinterpret_cast<const float4*>(Bs + kk * BN + 64 + tx * 4);
+      b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+  }
+}
+
+// Load R rows x 16 cols of row-major X (leading dim ld) starting at
+// (r0, c0) into smem transposed: S[kk][r].  Rows >= rmax are zero.  TR: sine.
+template <int R, bool SIN>
+__device__ __forceinline__ void load_T(float* __restrict__ S, const float* __restrict__ X, int ld,
+                                       int r0, int c0, int rmax, float w0) {
+  // R*16 elements, 8 consecutive per thread (R = 128) or 4 (R = 64)
+  constexpr int PER = R * BK / NT;
+  const int t = threadIdx.x;
+  const int r = t / (BK / PER);
+  const int kk0 = (t % (BK / PER)) * PER;
+  float v[PER];
+  if (r0 + r < rmax) {
+    const float* src = X + static_cast<size_t>(r0 + r) * ld + c0 + kk0;
+#pragma unroll
+    for (int q = 0; q < PER; q += 4) {
+      float4 x = *reinterpret_cast<const float4*>(src + q);
+      v[q] = x.x; v[q + 1] = x.y; v[q + 2] = x.z; v[q + 3] = x.w;
+    }
+    if (SIN) {
+#pragma unroll
+      for (int q = 0; q < PER; ++q) v[q] = sinw(v[q], w0);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) v[q] = 0.f;
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) S[(kk0 + q) * R + r] = v[q];
+}
+
+// Load 16 rows x C cols of row-major X at (r0, c0) directly: S[kk][c].
+template <int C, bool SIN>
+__device__ __forceinline__ void load_D(float* __restrict__ S, const float* __restrict__ X, int ld,
+                                       int r0, int c0, int rmax, float w0) {
+  constexpr int PER = C * BK / NT;  // 8 or 4
+  const int t = threadIdx.x;
+  const int kk = t / (C / PER);
+  const int cc = (t % (C / PER)) * PER;
+  float v[PER];
+  if (r0 + kk < rmax) {
+    const float* src = X + static_cast<size_t>(r0 + kk) * ld + c0 + cc;
+#pragma unroll
+    for (int q = 0; q < PER; q += 4) {
+      float4 x = *reinterpret_cast<const float4*>(src + q);
+      v[q] = x.x; v[q + 1] = x.y; v[q + 2] = x.z; v[q + 3] = x.w;
+    }
+    if (SIN) {
+#pragma unroll
+      for (int q = 0; q < PER; ++q) v[q] = sinw(v[q], w0);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) v[q] = 0.f;
+  }
+#pragma unroll
+  for (int q = 0; q < PER; q += 4)
+    *reinterpret_cast<float4*>(S + kk * C + cc + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+}
+
+// a_0[m][n] = b_0[n] + W_0[n][0] c_x + W_0[n][1] c_y     (nfield.hpp:117-121, l = 0)
+__global__ void siren_first_kernel(const float2* __restrict__ coords, const float* __restrict__ W0,
+                                   const float* __restrict__ b0, int n, int H,
+                                   float* __restrict__ A0) {
+  size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<size_t>(n) * H) return;
+  int m = static_cast<int>(i / H), k = static_cast<int>(i - static_cast<size_t>(m) * H);
+  float2 c = coords[m];
+  A0[i] = fmaf(W0[2 * k + 1], c.y, fmaf(W0[2 * k], c.x, b0[k]));
+}
+
+// a_l = W_l sin(w0 a_{l-1}) + b_l        grid (ceil(n/128), H/BN)
+template <int BN>
+__global__ void __launch_bounds__(NT, 2)
+siren_fwd_kernel(const float* __restrict__ Ain, const float* __restrict__ W,
+                 const float* __restrict__ b, int n, int H, float w0, float* __restrict__ Aout) {
+  constexpr int TN = TileShape<BN>::TN;
+  __shared__ __align__(16) float As[BK * BM];
+  __shared__ __align__(16) float Bs[BK * BN];
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+  float acc[8][TN] = {};
+  for (int k0 = 0; k0 < H; k0 += BK) {
+    load_T<BM, true>(As, Ain, H, m0, k0, n, w0);
+    load_T<BN, false>(Bs, W, H, n0, k0, H, w0);  // Bs[kk][n] = W[n0+n][k0+kk]
+    __syncthreads();
+    mma_tile<BN>(As, Bs, acc, ty, tx);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int m = m0 + ty * 8 + i;
+    if (m >= n) break;
+#pragma unroll
+    for (int j = 0; j < TN; j += 4) {
+      int c = n0 + tcol<BN>(tx, j);
+      float4 o = make_float4(acc[i][j] + b[c], acc[i][j + 1] + b[c + 1], acc[i][j + 2] + b[c + 2],
+                             acc[i][j + 3] + b[c + 3]);
+      *reinterpret_cast<float4*>(Aout + static_cast<size_t>(m) * H + c) = o;
+    }
+  }
+}
+
+// dv[idx[m]] = out_scale (b_L + sum_k w_L[k] sin(w0 a_{L-1}[m][k]))   one warp per pixel group
+__global__ void siren_out_kernel(const float* __restrict__ A, const float* __restrict__ wL,
+                                 const float* __restrict__ bL, const int* __restrict__ idx, int n,
+                                 int H, float w0, float out_scale, float* __restrict__ dv) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int m0 = warp * 32;
+  for (int q = 0; q < 32; ++q) {
+    int m = m0 + q;
+    if (m >= n) break;
+    const float* row = A + static_cast<size_t>(m) * H;
+    float s = 0.f;
+    for (int k = lane; k < H; k += 32) s = fmaf(wL[k], sinw(row[k], w0), s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) dv[idx[m]] = out_scale * (bL[0] + s);
+  }
+}
+
+// Top of the backward: g_m = out_scale (gv[idx m] + gmask[m]);
+//   dA_{L-1}[m][k] = g_m w_L[k] w0 cos(w0 a)      (nfield.hpp:198-200)
+//   partial gW_L[k] += g_m sin(w0 a), gb_L += g_m (nfield.hpp:194-197)
+// grid.x = pixel chunks of `rows` pixels; 256 threads = H columns x (256/H) row lanes.
+__global__ void siren_top_kernel(const float* __restrict__ A, const float* __restrict__ wL,
+                                 const double* __restrict__ gv, const float* __restrict__ gmask,
+                                 const int* __restrict__ idx, int n, int H, int rows, float w0,
+                                 float out_scale, float* __restrict__ dA,
+                                 float* __restrict__ partial) {
+  __shared__ float s_part[NT + 32];
+  const int lanes = NT / H;  // H in {64, 128, 256}
+  const int k = threadIdx.x % H, rl = threadIdx.x / H;
+  const int m_begin = blockIdx.x * rows, m_end = min(n, m_begin + rows);
+  float gw = 0.f, gb = 0.f;
+  const float wk = wL[k];
+  for (int m = m_begin + rl; m < m_end; m += lanes) {
+    float g = 0.f;
+    if (gv) g += static_cast<float>(gv[idx[m]]);
+    if (gmask) g += gmask[m];
+    g *= out_scale;
+    float a = A[static_cast<size_t>(m) * H + k];
+    float s, c;
+    sincosf(w0 * a, &s, &c);
+    dA[static_cast<size_t>(m) * H + k] = g * wk * w0 * c;
+    gw = fmaf(g, s, gw);
+    gb += g;
+  }
+  s_part[threadIdx.x] = gw;
+  __syncthreads();
+  float* out = partial + static_cast<size_t>(blockIdx.x) * (H + 1);
+  if (threadIdx.x < H) {
+    float t = 0.f;
+    for (int q = 0; q < lanes; ++q) t += s_part[q * H + threadIdx.x];
+    out[threadIdx.x] = t;
+  }
+  __syncthreads();
+  s_part[threadIdx.x] = (k == 0) ? gb : 0.f;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int q = 0; q < lanes; ++q) t += s_part[q * H];
+    out[H] = t;
+  }
+}
+
+// dA_{l-1}[m][k] = (sum_r dA_l[m][r] W_l[r][k]) w0 cos(w0 a_{l-1}[m][k])   (nfield.hpp:207-227)
+template <int BN>
+__global__ void __launch_bounds__(NT, 2)
+siren_dgrad_kernel(const float* __restrict__ dAl, const float* __restrict__ W,
+                   const float* __restrict__ Aprev, int n, int H, float w0,
+                   float* __restrict__ dAprev) {
+  constexpr int TN = TileShape<BN>::TN;
+  __shared__ __align__(16) float As[BK * BM];
+  __shared__ __align__(16) float Bs[BK * BN];
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+  float acc[8][TN] = {};
+  for (int r0 = 0; r0 < H; r0 += BK) {
+    load_T<BM, false>(As, dAl, H, m0, r0, n, w0);   // As[rr][m] = dA_l[m][r0+rr]
+    load_D<BN, false>(Bs, W, H, r0, n0, H, w0);     // Bs[rr][k] = W[r0+rr][n0+k]
+    __syncthreads();
+    mma_tile<BN>(As, Bs, acc, ty, tx);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int m = m0 + ty * 8 + i;
+    if (m >= n) break;
+#pragma unroll
+    for (int j = 0; j < TN; j += 4) {
+      int c = n0 + tcol<BN>(tx, j);
+      size_t off = static_cast<size_t>(m) * H + c;
+      float4 a = *reinterpret_cast<const float4*>(Aprev + off);
+      float4 o = make_float4(acc[i][j] * dsinw(a.x, w0), acc[i][j + 1] * dsinw(a.y, w0),
+                             acc[i][j + 2] * dsinw(a.z, w0), acc[i][j + 3] * dsinw(a.w, w0));
+      *reinterpret_cast<float4*>(dAprev + off) = o;
+    }
+  }
+}
+
+// Split-M weight gradient of a hidden layer l >= 1:
+//   partial[chunk][r][k] = sum_{m in chunk} dA_l[m][r] sin(w0 a_{l-1}[m][k]),
+//   partial bias[chunk][r] = sum_m dA_l[m][r]
+// grid (n_chunks, H/BN (rows r), H/BN (cols k)); the tile is BN x BN with
+// BN/16 x BN/16 outputs per thread.
+template <int BN>
+__global__ void __launch_bounds__(NT, 2)
+siren_wgrad_kernel(const float* __restrict__ dAl, const float* __restrict__ Aprev, int n, int H,
+                   int rows, float w0, float* __restrict__ partial) {
+  constexpr int T = BN / 16;  // outputs per thread along each axis (8 or 4)
+  __shared__ __align__(16) float As[BK * BN];
+  __shared__ __align__(16) float Bs[BK * BN];
+  const int chunk = blockIdx.x;
+  const int r0 = blockIdx.y * BN, k0 = blockIdx.z * BN;
+  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+  const int m_begin = chunk * rows, m_end = min(n, m_begin + rows);
+  float acc[T][T] = {};
+  float bias[T] = {};
+  const bool do_bias = (blockIdx.z == 0 && tx == 0);
+  for (int mb = m_begin; mb < m_end; mb += BK) {
+    load_D<BN, false>(As, dAl, H, mb, r0, m_end, w0);   // As[mm][r] = dA[mb+mm][r0+r]
+    load_D<BN, true>(Bs, Aprev, H, mb, k0, m_end, w0);  // Bs[mm][k] = sin(w0 a_{l-1}[mb+mm][k0+k])
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[T], b[T];
+#pragma unroll
+      for (int q = 0; q < T; q += 4) {
+        float4 x = *reinterpret_cast<const float4*>(As + kk * BN + ty * T + q);
+        a[q] = x.x; a[q + 1] = x.y; a[q + 2] = x.z; a[q + 3] = x.w;
+        float4 y = *reinterpret_cast<const float4*>(Bs + kk * BN + (q == 0 ? tx * 4 : 64 + tx * 4));
+        b[q] = y.x; b[q + 1] = y.y; b[q + 2] = y.z; b[q + 3] = y.w;
+      }
+#pragma unroll
+      for (int i = 0; i < T; ++i)
+#pragma unroll
+        for (int j = 0; j < T; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      if (do_bias) {
+#pragma unroll
+        for (int i = 0; i < T; ++i) bias[i] += a[i];
+      }
+    }
+    __syncthreads();
+  }
+  // partial layout per chunk: [H rows][H cols] weights then [H] bias
+  float* out = partial + static_cast<size_t>(chunk) * (static_cast<size_t>(H) * H + H);
+#pragma unroll
+  for (int i = 0; i < T; ++i) {
+    int r = r0 + ty * T + i;
+#pragma unroll
+    for (int j = 0; j < T; ++j) out[static_cast<size_t>(r) * H + k0 + tcol<BN>(tx, j)] = acc[i][j];
+    if (do_bias) out[static_cast<size_t>(H) * H + r] = bias[i];
+  }
+}
+
+// Layer-0 gradient partials: gW_0[r][c] += dA_0[m][r] c_m[c], gb_0[r] += dA_0[m][r].
+__global__ void siren_wgrad0_kernel(const float* __restrict__ dA0, const float2* __restrict__ coords,
+                                    int n, int H, int rows, float* __restrict__ partial) {
+  __shared__ float s_part[3 * NT];
+  const int lanes = NT / H;
+  const int r = threadIdx.x % H, rl = threadIdx.x / H;
+  const int m_begin = blockIdx.x * rows, m_end = min(n, m_begin + rows);
+  float gx = 0.f, gy = 0.f, gb = 0.f;
+  for (int m = m_begin + rl; m < m_end; m += lanes) {
+    float d = dA0[static_cast<size_t>(m) * H + r];
+    float2 c = coords[m];
+    gx = fmaf(d, c.x, gx);
+    gy = fmaf(d, c.y, gy);
+    gb += d;
+  }
+  s_part[threadIdx.x] = gx;
+  s_part[NT + threadIdx.x] = gy;
+  s_part[2 * NT + threadIdx.x] = gb;
+  __syncthreads();
+  if (threadIdx.x < H) {
+    float tx = 0.f, ty = 0.f, tb = 0.f;
+    for (int q = 0; q < lanes; ++q) {
+      tx += s_part[q * H + threadIdx.x];
+      ty += s_part[NT + q * H + threadIdx.x];
+      tb += s_part[2 * NT + q * H + threadIdx.x];
+    }
+    float* out = partial + static_cast<size_t>(blockIdx.x) * (3 * H);
+    out[2 * threadIdx.x] = tx;  // W_0 row-major [r][c]
+    out[2 * threadIdx.x + 1] = ty;
+    out[2 * H + threadIdx.x] = tb;
+  }
+}
+
+// grad[off + p] = sum_chunk partial[chunk][p]   (fixed order, fp64)
+__global__ void reduce_partials_kernel(const float* __restrict__ partial, int n_chunks,
+                                       int per_chunk, double* __restrict__ grad) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= per_chunk) return;
+  double s = 0.0;
+  for (int c = 0; c < n_chunks; ++c) s += partial[static_cast<size_t>(c) * per_chunk + p];
+  grad[p] = s;
+}
+
+// ---- per-pixel path for small / odd hidden widths (unit-test networks) ----
+// Forward: a_l stored as in the tiled path; output written into dv.
+__global__ void siren_fwd_small_kernel(const float* __restrict__ th, const float2* __restrict__ coords,
+                                       const int* __restrict__ idx, int n, int H, int L, float w0,
+                                       float out_scale, float* __restrict__ acts,
+                                       float* __restrict__ dv, size_t layer_stride) {
+  int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  float2 c = coords[m];
+  const float* W0 = th;
+  const float* b0 = th + 2 * H;
+  float* a0 = acts + static_cast<size_t>(m) * H;
+  for (int k = 0; k < H; ++k) a0[k] = fmaf(W0[2 * k + 1], c.y, fmaf(W0[2 * k], c.x, b0[k]));
+  size_t off = 3 * H;
+  for (int l = 1; l < L; ++l) {
+    const float* W = th + off;
+    const float* b = W + static_cast<size_t>(H) * H;
+    const float* ap = acts + (l - 1) * layer_stride + static_cast<size_t>(m) * H;
+    float* ao = acts + l * layer_stride + static_cast<size_t>(m) * H;
+    for (int r = 0; r < H; ++r) {
+      float s = b[r];
+      for (int k = 0; k < H; ++k) s = fmaf(W[r * H + k], sinw(ap[k], w0), s);
+      ao[r] = s;
+    }
+    off += static_cast<size_t>(H) * H + H;
+  }
+  const float* wL = th + off;
+  const float* ap = acts + (L - 1) * layer_stride + static_cast<size_t>(m) * H;
+  float s = 0.f;
+  for (int k = 0; k < H; ++k) s = fmaf(wL[k], sinw(ap[k], w0), s);
+  dv[idx[m]] = out_scale * (wL[H] + s);
+}
+
+// Backward per pixel into contrib[m][param] (reduced afterwards in fixed order).
+__global__ void siren_bwd_small_kernel(const float* __restrict__ th, const float2* __restrict__ coords,
+                                       const int* __restrict__ idx, int n, int H, int L, float w0,
+                                       float out_scale, const float* __restrict__ acts,
+                                       size_t layer_stride, const double* __restrict__ gv,
+                                       const float* __restrict__ gmask, float* __restrict__ delta,
+                                       float* __restrict__ contrib, int n_params) {
+  int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  float* cg = contrib + static_cast<size_t>(m) * n_params;
+  float g = 0.f;
+  if (gv) g += static_cast<float>(gv[idx[m]]);
+  if (gmask) g += gmask[m];
+  g *= out_scale;
+  float* d = delta + static_cast<size_t>(m) * 2 * H;  // [delta | delta_prev]
+  float* dp = d + H;
+  size_t offL = 3 * H + static_cast<size_t>(L - 1) * (static_cast<size_t>(H) * H + H);
+  const float* wL = th + offL;
+  const float* aL = acts + (L - 1) * layer_stride + static_cast<size_t>(m) * H;
+  for (int k = 0; k < H; ++k) {
+    cg[offL + k] = g * sinw(aL[k], w0);
+    d[k] = g * wL[k];
+  }
+  cg[offL + H] = g;
+  for (int l = L - 1; l >= 0; --l) {
+    size_t off = l == 0 ? 0 : 3 * H + static_cast<size_t>(l - 1) * (static_cast<size_t>(H) * H + H);
+    int cols = l == 0 ? 2 : H;
+    const float* W = th + off;
+    const float* al = acts + l * layer_stride + static_cast<size_t>(m) * H;
+    const float* ap = l > 0 ? acts + (l - 1) * layer_stride + static_cast<size_t>(m) * H : nullptr;
+    float2 c = coords[m];
+    for (int k = 0; k < H; ++k) dp[k] = 0.f;
+    for (int r = 0; r < H; ++r) {
+      float da = d[r] * dsinw(al[r], w0);
+      cg[off + static_cast<size_t>(H) * cols + r] = da;
+      for (int q = 0; q < cols; ++q) {
+        float zin = l == 0 ? (q == 0 ? c.x : c.y) : sinw(ap[q], w0);
+        cg[off + static_cast<size_t>(r) * cols + q] = da * zin;
+        if (l > 0) dp[q] = fmaf(da, W[r * cols + q], dp[q]);
+      }
+    }
+    for (int k = 0; k < H; ++k) d[k] = dp[k];
+  }
+}
+
+__global__ void reduce_rows_kernel(const float* __restrict__ contrib, int n, int n_params,
+                                   double* __restrict__ grad) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_params) return;
+  double s = 0.0;
+  for (int m = 0; m < n; ++m) s += contrib[static_cast<size_t>(m) * n_params + p];
+  grad[p] = s;
+}
+
+bool tiled(const SirenShape& s) { return s.hidden % 64 == 0 && s.hidden <= 256 && s.in_dim == 2; }
+
+int chunk_rows(int n, int tiles, int num_sms) {
+  int chunks = std::max(1, (2 * num_sms) / std::max(1, tiles));
+  int rows = div_up(n, chunks);
+  rows = div_up(rows, BK) * BK;
+  return std::max(rows, BK);
+}
+
+}  // namespace
+
+Status siren_work_alloc(SirenWork& w, const MaskedPixels& mp, const SirenShape& s,
+                        cudaStream_t stream) {
+  siren_work_free(w);
+  w.n = mp.n;
+  w.hidden = s.hidden;
+  w.layers = s.layers;
+  size_t nh = static_cast<size_t>(std::max(1, mp.n)) * s.hidden;
+  PACT_CUDA_S(cudaMalloc(&w.idx, sizeof(int) * std::max(1, mp.n)));
+  PACT_CUDA_S(cudaMalloc(&w.coords, sizeof(float2) * std::max(1, mp.n)));
+  PACT_CUDA_S(cudaMalloc(&w.acts, sizeof(float) * nh * s.layers));
+  PACT_CUDA_S(cudaMalloc(&w.dA, sizeof(float) * nh * 2));
+  PACT_CUDA_S(cudaMalloc(&w.dB, sizeof(float) * nh));
+  if (mp.n > 0) {
+    PACT_CUDA_S(cudaMemcpyAsync(w.idx, mp.idx.data(), sizeof(int) * mp.n, cudaMemcpyHostToDevice,
+                                stream));
+    PACT_CUDA_S(cudaMemcpyAsync(w.coords, mp.coords.data(), sizeof(float2) * mp.n,
+                                cudaMemcpyHostToDevice, stream));
+    PACT_CUDA_S(cudaStreamSynchronize(stream));
+  }
+  return {};
+}
+
+void siren_work_free(SirenWork& w) {
+  if (w.idx) cudaFree(w.idx);
+  if (w.coords) cudaFree(w.coords);
+  if (w.acts) cudaFree(w.acts);
+  if (w.dA) cudaFree(w.dA);
+  if (w.dB) cudaFree(w.dB);
+  if (w.partial) cudaFree(w.partial);
+  w = SirenWork{};
+}
+
+static Status ensure_partial(SirenWork& w, size_t floats, cudaStream_t stream) {
+  if (w.partial_floats >= floats) return {};
+  if (w.partial) {
+    PACT_CUDA_S(cudaStreamSynchronize(stream));
+    cudaFree(w.partial);
+  }
+  PACT_CUDA_S(cudaMalloc(&w.partial, sizeof(float) * floats));
+  w.partial_floats = floats;
+  return {};
+}
+
+Status siren_forward(pact_ctx* ctx, const SirenShape& s, const float* theta, SirenWork& w,
+                     float* dv) {
+  const int n = w.n, H = s.hidden, L = s.layers;
+  if (n == 0) return {};
+  const float w0 = static_cast<float>(s.omega0);
+  const size_t stride = static_cast<size_t>(n) * H;
+  cudaStream_t st = ctx->stream;
+  if (!tiled(s)) {
+    siren_fwd_small_kernel<<<div_up(n, 128), 128, 0, st>>>(theta, w.coords, w.idx, n, H, L, w0,
+                                                           static_cast<float>(s.out_scale), w.acts,
+                                                           dv, stride);
+    return after_launch(ctx, "siren_fwd_small_kernel");
+  }
+  size_t total = stride;
+  siren_first_kernel<<<static_cast<int>((total + 255) / 256), 256, 0, st>>>(
+      w.coords, theta + s.offset(0), theta + s.offset(0) + 2 * H, n, H, w.acts);
+  PACT_TRY_S(after_launch(ctx, "siren_first_kernel"));
+  for (int l = 1; l < L; ++l) {
+    const float* W = theta + s.offset(l);
+    const float* b = W + static_cast<size_t>(H) * H;
+    const float* Ain = w.acts + (l - 1) * stride;
+    float* Aout = w.acts + l * stride;
+    if (H == 64) {
+      siren_fwd_kernel<64><<<dim3(div_up(n, BM), 1), NT, 0, st>>>(Ain, W, b, n, H, w0, Aout);
+    } else {
+      siren_fwd_kernel<128><<<dim3(div_up(n, BM), H / 128), NT, 0, st>>>(Ain, W, b, n, H, w0, Aout);
+    }
+    PACT_TRY_S(after_launch(ctx, "siren_fwd_kernel"));
+  }
+  const float* wL = theta + s.offset(L);
+  siren_out_kernel<<<div_up(div_up(n, 32), 8), 256, 0, st>>>(w.acts + (L - 1) * stride, wL, wL + H,
+                                                             w.idx, n, H, w0,
+                                                             static_cast<float>(s.out_scale), dv);
+  return after_launch(ctx, "siren_out_kernel");
+}
+
+Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, SirenWork& w,
+                      const double* gv, const float* gmask, double* grad) {
+  const int n = w.n, H = s.hidden, L = s.layers;
+  const int P = static_cast<int>(s.count());
+  cudaStream_t st = ctx->stream;
+  if (n == 0) {
+    PACT_CUDA_S(cudaMemsetAsync(grad, 0, sizeof(double) * P, st));
+    return {};
+  }
+  const float w0 = static_cast<float>(s.omega0);
+  const float osc = static_cast<float>(s.out_scale);
+  const size_t stride = static_cast<size_t>(n) * H;
+  if (!tiled(s)) {
+    PACT_TRY_S(ensure_partial(w, static_cast<size_t>(n) * P, st));
+    siren_bwd_small_kernel<<<div_up(n, 128), 128, 0, st>>>(theta, w.coords, w.idx, n, H, L, w0, osc,
+                                                           w.acts, stride, gv, gmask, w.dA,
+                                                           w.partial, P);
+    PACT_TRY_S(after_launch(ctx, "siren_bwd_small_kernel"));
+    reduce_rows_kernel<<<div_up(P, 128), 128, 0, st>>>(w.partial, n, P, grad);
+    return after_launch(ctx, "reduce_rows_kernel");
+  }
+  // chunking for the split-M reductions
+  const int tilesW = (H / 128 > 0 ? H / 128 : 1) * (H / 128 > 0 ? H / 128 : 1);
+  const int rows_top = chunk_rows(n, 1, ctx->num_sms);
+  const int n_top = div_up(n, rows_top);
+  const int rows_w = chunk_rows(n, tilesW, ctx->num_sms);
+  const int n_w = div_up(n, rows_w);
+  size_t need = std::max(static_cast<size_t>(n_top) * (H + 1),
+                         static_cast<size_t>(n_w) * (static_cast<size_t>(H) * H + H));
+  need = std::max(need, static_cast<size_t>(n_top) * 3 * H);
+  PACT_TRY_S(ensure_partial(w, need, st));
+
+  float* cur = w.dA;   // dA_l
+  float* nxt = w.dB;   // dA_{l-1}
+  // output layer
+  const float* wL = theta + s.offset(L);
+  siren_top_kernel<<<n_top, NT, 0, st>>>(w.acts + (L - 1) * stride, wL, gv, gmask, w.idx, n, H,
+                                         rows_top, w0, osc, cur, w.partial);
+  PACT_TRY_S(after_launch(ctx, "siren_top_kernel"));
+  reduce_partials_kernel<<<div_up(H + 1, 128), 128, 0, st>>>(w.partial, n_top, H + 1,
+                                                             grad + s.offset(L));
+  PACT_TRY_S(after_launch(ctx, "reduce_partials_kernel"));
+  for (int l = L - 1; l >= 1; --l) {
+    const float* W = theta + s.offset(l);
+    const float* Aprev = w.acts + (l - 1) * stride;
+    // weight gradient of layer l
+    if (H == 64)
+      siren_wgrad_kernel<64><<<dim3(n_w, 1, 1), NT, 0, st>>>(cur, Aprev, n, H, rows_w, w0, w.partial);
+    else
+      siren_wgrad_kernel<128><<<dim3(n_w, H / 128, H / 128), NT, 0, st>>>(cur, Aprev, n, H, rows_w,
+                                                                         w0, w.partial);
+    PACT_TRY_S(after_launch(ctx, "siren_wgrad_kernel"));
+    int per = H * H + H;
+    reduce_partials_kernel<<<div_up(per, 256), 256, 0, st>>>(w.partial, n_w, per, grad + s.offset(l));
+    PACT_TRY_S(after_launch(ctx, "reduce_partials_kernel"));
+    // delta to layer l-1
+    if (H == 64)
+      siren_dgrad_kernel<64><<<dim3(div_up(n, BM), 1), NT, 0, st>>>(cur, W, Aprev, n, H, w0, nxt);
+    else
+      siren_dgrad_kernel<128><<<dim3(div_up(n, BM), H / 128), NT, 0, st>>>(cur, W, Aprev, n, H, w0,
+                                                                          nxt);
+    PACT_TRY_S(after_launch(ctx, "siren_dgrad_kernel"));
+    std::swap(cur, nxt);
+  }
+  siren_wgrad0_kernel<<<n_top, NT, 0, st>>>(cur, w.coords, n, H, rows_top, w.partial);
+  PACT_TRY_S(after_launch(ctx, "siren_wgrad0_kernel"));
+  reduce_partials_kernel<<<div_up(3 * H, 128), 128, 0, st>>>(w.partial, n_top, 3 * H,
+                                                             grad + s.offset(0));
+  return after_launch(ctx, "reduce_partials_kernel");
+}
+
+}  // namespace pactgpu

@@ -1,0 +1,66 @@
+// SIREN coordinate network on the device (nfield.hpp).  Activations are kept
+// per masked pixel, row-major [n_masked][hidden] fp32.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace pactgpu {
+
+struct SirenShape {
+  int in_dim = 2;
+  int hidden = 64;
+  int layers = 2;  // n_hidden_layers (sine layers)
+  double omega0 = 30.0;
+  double out_scale = 100.0;
+  double v0 = 1500.0;
+
+  // SirenParams::layer_shape / layer_offset / param_count, nfield.hpp:45-63
+  int rows(int l) const { return l == layers ? 1 : hidden; }
+  int cols(int l) const { return l == 0 ? in_dim : hidden; }
+  size_t offset(int l) const {
+    size_t o = 0;
+    for (int k = 0; k < l; ++k) o += static_cast<size_t>(rows(k)) * cols(k) + rows(k);
+    return o;
+  }
+  size_t count() const { return offset(layers + 1); }
+};
+
+// Masked pixels of (grid, mask) in row-major order with their normalised
+// coordinates (render_sos, nfield.hpp:152-160), computed in fp64 on the host.
+struct MaskedPixels {
+  int n = 0;
+  std::vector<int> idx;
+  std::vector<float> coords;  // [n][2]
+};
+MaskedPixels masked_pixels(const pact_grid& g, const pact_mask& m);
+
+// Device workspace for one SIREN evaluation over n masked pixels.
+struct SirenWork {
+  int n = 0, hidden = 0, layers = 0;
+  int* idx = nullptr;        // [n]
+  float2* coords = nullptr;  // [n]
+  float* acts = nullptr;     // [layers][n][hidden] pre-activations a_l
+  float* dA = nullptr;       // [n][hidden]  backward ping
+  float* dB = nullptr;       // [n][hidden]  backward pong
+  float* partial = nullptr;  // split-M weight-gradient partials
+  size_t partial_floats = 0;
+};
+
+Status siren_work_alloc(SirenWork& w, const MaskedPixels& mp, const SirenShape& s,
+                        cudaStream_t stream);
+void siren_work_free(SirenWork& w);
+
+// Forward over the masked pixels: a_l for every sine layer, and
+// dv[idx[m]] = out_scale * MLP(c_m) written into the deviation raster.
+Status siren_forward(pact_ctx* ctx, const SirenShape& s, const float* theta, SirenWork& w,
+                     float* dv_raster);
+
+// Reverse mode of sum_m g_m v(m), g_m = gv_raster[idx[m]] (fp64 raster, may
+// be null) + g_masked[m] (may be null); grad (fp64, reference layout) is
+// overwritten.  Requires siren_forward on the same theta first.
+Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, SirenWork& w,
+                      const double* gv_raster, const float* g_masked, double* grad);
+
+}  // namespace pactgpu

@@ -1,0 +1,500 @@
+// The NF-APACT iteration engine: joint_reconstruct (optimize.hpp:367-494) on
+// one B200.
+//
+// One-time (optimize.hpp:369-405): patch layout, DAS stack, fp32 patch
+// spectra (the reference also caches them as complex<float>), SIREN init,
+// Fourier tables.  Each iteration (optimize.hpp:412-471) is one sequence on
+// the engine's stream, captured once as a CUDA graph:
+//   siren_forward -> finite(SOS) -> wavefront -> fused loss/dL/dw ->
+//   ray backward (dL/dv) -> TV -> report -> siren_backward -> finite(grad) ->
+//   Adam (fp64 master parameters, fp32 working copy)
+// The host reads back only the three loss terms and the NumericalError flags
+// once per reported epoch.  Results are deterministic: every reduction has a
+// fixed order except the dL/dv scatter, which accumulates in fp64.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "geom.cuh"
+#include "siren.cuh"
+#include "train_ops.cuh"
+
+namespace pactgpu {
+Status merge_window(double fwhm, int P, double pitch, std::vector<float>& w);
+Status launch_sos_from_dev(pact_ctx* ctx, const float* dv, size_t n, double v0, float* out);
+}  // namespace pactgpu
+
+using namespace pactgpu;
+
+struct pact_trainer {
+  pact_ctx* user = nullptr;  // caller's context (its stream orders inputs/outputs)
+  pact_ctx eng;              // engine context: private stream
+  pact_ring ring{};
+  pact_signal_meta meta{};
+  pact_grid grid{};
+  pact_mask mask{};
+  pact_train_config cfg{};
+  std::vector<double> delays;
+  double v0 = 0.0;
+  pact_layout lay{};
+  int n_patches = 0, P = 0, K = 0, A = 0, n_params = 0;
+  double loss_scale = 0.0;
+  SirenShape shape;
+  MaskedPixels mp;
+  SirenWork sw;
+  FourierTable ftab;
+  RayArgs ray{};
+  int n_tv = 0;
+  // device state
+  void* arena = nullptr;
+  float* stack = nullptr;
+  float2* Y = nullptr;
+  float* dv = nullptr;
+  float* w = nullptr;
+  float* dw = nullptr;
+  double* loss_patch = nullptr;
+  double* gv = nullptr;
+  float* gtv = nullptr;
+  double* tv_partial = nullptr;
+  unsigned char* inmask = nullptr;
+  double* theta = nullptr;
+  double* m = nullptr;
+  double* v = nullptr;
+  float* theta32 = nullptr;
+  double* grad = nullptr;
+  unsigned* flags = nullptr;
+  double* report = nullptr;
+  long long* t = nullptr;
+  double2* centers = nullptr;
+  float* win = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int64_t graph_kernels = 0;
+  int steps_done = 0;
+};
+
+namespace {
+
+Status enqueue_step(pact_trainer* tr) {
+  pact_ctx* ctx = &tr->eng;
+  const size_t npx = static_cast<size_t>(tr->grid.width) * tr->grid.height;
+  // render_sos (optimize.hpp:413) + finiteness (414-417)
+  PACT_TRY_S(siren_forward(ctx, tr->shape, tr->theta32, tr->sw, tr->dv));
+  PACT_TRY_S(launch_check_finite_f32(ctx, tr->dv, tr->sw.idx, tr->mp.n, kFlagSos, tr->flags));
+  // wavefront_profile for every patch (431-433)
+  PACT_TRY_S(launch_wavefront(ctx, tr->ray, tr->w));
+  // fused_patch_loss_grad (434-436)
+  PACT_TRY_S(launch_loss_grad(ctx, tr->ftab.tab, tr->Y, tr->w, tr->n_patches, tr->cfg.eps_deconv,
+                              tr->loss_scale, tr->cfg.implicit_xhat_grad != 0, tr->loss_patch,
+                              tr->dw));
+  // wavefront_grad_trace into dL/dv (437-438)
+  PACT_CUDA_S(cudaMemsetAsync(tr->gv, 0, sizeof(double) * npx, ctx->stream));
+  PACT_TRY_S(launch_ray_backward(ctx, tr->ray, tr->dw, tr->gv));
+  // tv_loss (448) and the loss report / checks (442-451)
+  PACT_TRY_S(launch_tv(ctx, tr->dv, tr->inmask, tr->sw.idx, tr->mp.n, tr->grid.width,
+                       tr->grid.height, tr->cfg.lambda_tv, tr->gtv, tr->tv_partial, tr->n_tv));
+  PACT_TRY_S(launch_step_report(ctx, tr->loss_patch, tr->n_patches, tr->tv_partial, tr->n_tv,
+                                tr->cfg.lambda_tv, tr->report, tr->flags));
+  // backprop_sos of (dL/dv at masked pixels + TV gradient) (453-461)
+  PACT_TRY_S(siren_backward(ctx, tr->shape, tr->theta32, tr->sw, tr->gv, tr->gtv, tr->grad));
+  PACT_TRY_S(launch_check_finite_f64(ctx, tr->grad, tr->n_params, kFlagGrad, tr->flags));
+  // adam_step (466-467)
+  PACT_TRY_S(launch_adam(ctx, tr->n_params, tr->theta, tr->grad, tr->m, tr->v, tr->t,
+                         tr->cfg.learning_rate, tr->cfg.beta1, tr->cfg.beta2, tr->cfg.adam_eps,
+                         tr->flags, tr->theta32, true));
+  return {};
+}
+
+Status capture_graph(pact_trainer* tr) {
+  cudaStream_t s = tr->eng.stream;
+  PACT_CUDA_S(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  int64_t before = tr->eng.launches.load();
+  Status st = enqueue_step(tr);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &g);
+  if (!st.ok()) {
+    if (g) cudaGraphDestroy(g);
+    return st;
+  }
+  PACT_CUDA_S(e);
+  // kernels inside the graph are counted per replay, not per capture
+  tr->eng.launches.store(before);
+  e = cudaGraphInstantiate(&tr->graph, g, 0);
+  cudaGraphDestroy(g);
+  return cuda_status(e, "cudaGraphInstantiate");
+}
+
+template <typename T>
+T* carve(char*& p, size_t count) {
+  T* r = reinterpret_cast<T*>(p);
+  p += (sizeof(T) * count + 255) & ~size_t(255);
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pact_train_config_default(pact_train_config* c) {
+  // TrainConfig defaults, optimize.hpp:48-69
+  static double delays[32];
+  for (int j = 0; j < 32; ++j) delays[j] = -0.8 + (0.8 - -0.8) * j / 31;
+  if (!c) return validation("pact_train_config_default: null").code;
+  std::memset(c, 0, sizeof(*c));
+  c->epochs = 10;
+  c->steps_per_epoch = 30;
+  c->learning_rate = 1e-3;
+  c->beta1 = 0.9;
+  c->beta2 = 0.999;
+  c->adam_eps = 1e-8;
+  c->lambda_tv = 3e9;
+  c->n_delays = 32;
+  c->delays = delays;
+  c->eps_deconv = 1e-3;
+  c->n_angles = 512;
+  c->ray_step = 0.05;
+  c->seed = 0;
+  c->hidden = 64;
+  c->sine_layers = 2;
+  c->omega0 = 30.0;
+  c->out_scale = 100.0;
+  c->patch_mm = 3.2;
+  c->overlap = 0.75;
+  c->merge_fwhm = 1.5;
+  c->implicit_xhat_grad = 1;
+  c->workers = 0;
+  c->use_cuda_graph = 1;
+  return PACT_OK;
+}
+
+int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_meta* meta,
+                        const float* signals, const pact_grid* grid, const pact_mask* mask,
+                        const pact_train_config* cfg, pact_trainer** out) {
+  if (!ctx || !ring || !meta || !signals || !grid || !mask || !cfg || !out)
+    return validation("pact_trainer_create: null argument").code;
+  *out = nullptr;
+  // TrainConfig::validate (optimize.hpp:71-77), SignalSet::validate, v0 (369-371)
+  if (cfg->epochs < 1) return validation("train: epochs must be >= 1").code;
+  if (cfg->steps_per_epoch < 1) return validation("train: steps_per_epoch must be >= 1").code;
+  if (!(cfg->learning_rate > 0.0)) return validation("train: learning rate must be > 0").code;
+  if (!(cfg->lambda_tv >= 0.0)) return validation("train: lambda_tv must be >= 0").code;
+  if (cfg->n_delays < 1 || !cfg->delays) return validation("train: need at least one delay").code;
+  if (ring->n_transducers < 3) return validation("ring: need at least 3 transducers").code;
+  if (!(ring->radius > 0.0)) return validation("ring: radius must be > 0").code;
+  if (meta->n_samples < 2) return validation("signals: need at least 2 samples").code;
+  if (!(meta->dt > 0.0)) return validation("signals: dt must be > 0").code;
+  const double v0 = meta->background_sos;
+  if (!(v0 > 0.0)) return validation("joint_reconstruct: non-positive background SOS").code;
+
+  auto* tr = new pact_trainer();
+  tr->user = ctx;
+  tr->eng.device = ctx->device;
+  tr->eng.num_sms = ctx->num_sms;
+  cudaError_t ce = cudaStreamCreateWithFlags(&tr->eng.own_stream, cudaStreamNonBlocking);
+  if (ce != cudaSuccess) {
+    delete tr;
+    return cuda_status(ce, "cudaStreamCreateWithFlags").code;
+  }
+  tr->eng.stream = tr->eng.own_stream;
+  auto fail = [&](int code) {
+    pact_trainer_destroy(tr);
+    return code;
+  };
+  tr->ring = *ring;
+  tr->meta = *meta;
+  tr->grid = *grid;
+  tr->mask = *mask;
+  tr->cfg = *cfg;
+  tr->delays.assign(cfg->delays, cfg->delays + cfg->n_delays);
+  tr->cfg.delays = tr->delays.data();
+  tr->v0 = v0;
+  Status st = make_layout(*grid, cfg->patch_mm, cfg->overlap, tr->lay);
+  if (!st.ok()) return fail(st.code);
+  tr->n_patches = tr->lay.nx * tr->lay.ny;
+  tr->P = tr->lay.patch_pixels;
+  tr->K = cfg->n_delays;
+  tr->A = cfg->n_angles;
+  tr->loss_scale = 1.0 / (static_cast<double>(tr->n_patches) * tr->K * tr->P * tr->P);
+  tr->shape.hidden = cfg->hidden;
+  tr->shape.layers = cfg->sine_layers;
+  tr->shape.omega0 = cfg->omega0;
+  tr->shape.out_scale = cfg->out_scale;
+  tr->shape.v0 = v0;
+  tr->n_params = static_cast<int>(tr->shape.count());
+  std::vector<double> centers(2 * tr->n_patches);
+  layout_centers(tr->lay, centers.data());
+  st = ray_args(*ring, *grid, v0, *mask, cfg->n_angles, cfg->ray_step, tr->ray);
+  if (!st.ok()) return fail(st.code);
+  st = validate_centers(*ring, tr->n_patches, centers.data());
+  if (!st.ok()) return fail(st.code);
+  std::vector<float> win;
+  st = merge_window(cfg->merge_fwhm, tr->P, grid->pitch, win);
+  if (!st.ok()) return fail(st.code);
+  tr->mp = masked_pixels(*grid, *mask);
+
+  // ---- device arena ----
+  const size_t npx = static_cast<size_t>(grid->width) * grid->height;
+  const size_t P2 = static_cast<size_t>(tr->P) * tr->P;
+  tr->n_tv = std::max(1, std::min(div_up(std::max(tr->mp.n, 1), 256), ctx->num_sms * 4));
+  size_t bytes = 0;
+  auto add = [&](size_t b) { bytes += (b + 255) & ~size_t(255); };
+  add(sizeof(float) * tr->K * npx);                              // stack
+  add(sizeof(float2) * tr->n_patches * tr->K * P2);              // Y
+  add(sizeof(float) * npx);                                      // dv
+  add(sizeof(float) * tr->n_patches * tr->A);                    // w
+  add(sizeof(float) * tr->n_patches * tr->A);                    // dw
+  add(sizeof(double) * tr->n_patches);                           // loss_patch
+  add(sizeof(double) * npx);                                     // gv
+  add(sizeof(float) * std::max(tr->mp.n, 1));                    // gtv
+  add(sizeof(double) * tr->n_tv);                                // tv_partial
+  add(npx);                                                      // inmask
+  add(sizeof(double) * tr->n_params * 4);                        // theta m v grad
+  add(sizeof(float) * tr->n_params);                             // theta32
+  add(64);                                                       // flags
+  add(sizeof(double) * 4);                                       // report
+  add(sizeof(long long));                                        // t
+  add(sizeof(double2) * tr->n_patches);                          // centers
+  add(sizeof(float) * P2);                                       // window
+  bytes += 64 * 256;  // per-carve alignment slack
+  ce = cudaMalloc(&tr->arena, bytes);
+  if (ce != cudaSuccess) return fail(cuda_status(ce, "trainer arena").code);
+  char* p = static_cast<char*>(tr->arena);
+  tr->stack = carve<float>(p, tr->K * npx);
+  tr->Y = carve<float2>(p, tr->n_patches * tr->K * P2);
+  tr->dv = carve<float>(p, npx);
+  tr->w = carve<float>(p, tr->n_patches * tr->A);
+  tr->dw = carve<float>(p, tr->n_patches * tr->A);
+  tr->loss_patch = carve<double>(p, tr->n_patches);
+  tr->gv = carve<double>(p, npx);
+  tr->gtv = carve<float>(p, std::max(tr->mp.n, 1));
+  tr->tv_partial = carve<double>(p, tr->n_tv);
+  tr->inmask = carve<unsigned char>(p, npx);
+  tr->theta = carve<double>(p, tr->n_params);
+  tr->m = carve<double>(p, tr->n_params);
+  tr->v = carve<double>(p, tr->n_params);
+  tr->grad = carve<double>(p, tr->n_params);
+  tr->theta32 = carve<float>(p, tr->n_params);
+  tr->flags = carve<unsigned>(p, 16);
+  tr->report = carve<double>(p, 4);
+  tr->t = carve<long long>(p, 1);
+  tr->centers = carve<double2>(p, tr->n_patches);
+  tr->win = carve<float>(p, P2);
+
+  pact_ctx* e = &tr->eng;
+  cudaStream_t s = e->stream;
+  // inputs produced on the caller's stream must be visible to the engine
+  cudaEvent_t ev;
+  cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  cudaEventRecord(ev, ctx->stream);
+  cudaStreamWaitEvent(s, ev, 0);
+  cudaEventDestroy(ev);
+
+  std::vector<unsigned char> flag(npx, 0);
+  for (int i : tr->mp.idx) flag[i] = 1;
+  std::vector<double> theta(tr->n_params);
+  pact_siren sp{2, cfg->hidden, cfg->sine_layers, cfg->omega0, cfg->out_scale, v0};
+  int rc = pact_init_siren(cfg->seed, &sp, theta.data());
+  if (rc) return fail(rc);
+  std::vector<float> theta32(theta.begin(), theta.end());
+#define TRY_CU(x)                                        \
+  do {                                                   \
+    cudaError_t _e = (x);                                \
+    if (_e != cudaSuccess) return fail(cuda_status(_e, #x).code); \
+  } while (0)
+#define TRY_ST(x)                                        \
+  do {                                                   \
+    Status _s = (x);                                     \
+    if (!_s.ok()) return fail(_s.code);                  \
+  } while (0)
+  TRY_CU(cudaMemcpyAsync(tr->inmask, flag.data(), npx, cudaMemcpyHostToDevice, s));
+  TRY_CU(cudaMemcpyAsync(tr->theta, theta.data(), sizeof(double) * tr->n_params,
+                         cudaMemcpyHostToDevice, s));
+  TRY_CU(cudaMemcpyAsync(tr->theta32, theta32.data(), sizeof(float) * tr->n_params,
+                         cudaMemcpyHostToDevice, s));
+  TRY_CU(cudaMemcpyAsync(tr->centers, centers.data(), sizeof(double2) * tr->n_patches,
+                         cudaMemcpyHostToDevice, s));
+  TRY_CU(cudaMemcpyAsync(tr->win, win.data(), sizeof(float) * P2, cudaMemcpyHostToDevice, s));
+  TRY_CU(cudaMemsetAsync(tr->m, 0, sizeof(double) * tr->n_params, s));
+  TRY_CU(cudaMemsetAsync(tr->v, 0, sizeof(double) * tr->n_params, s));
+  TRY_CU(cudaMemsetAsync(tr->flags, 0, 64, s));
+  TRY_CU(cudaMemsetAsync(tr->t, 0, sizeof(long long), s));
+  TRY_CU(cudaMemsetAsync(tr->dv, 0, sizeof(float) * npx, s));
+  tr->ray.dv = tr->dv;
+  tr->ray.centers = tr->centers;
+  tr->ray.n_rays = tr->n_patches * tr->A;
+  // DAS stack + spectra, once (optimize.hpp:380-392)
+  TRY_ST(das_stack_device(e, *ring, *meta, signals, *grid, v0, tr->delays.data(), tr->K,
+                          tr->stack));
+  TRY_ST(launch_patch_fft(e, tr->lay, tr->stack, tr->K, tr->Y));
+  TRY_ST(siren_work_alloc(tr->sw, tr->mp, tr->shape, s));
+  TRY_ST(fourier_table(e, tr->ftab, tr->P, grid->pitch, tr->A, tr->delays.data(), tr->K));
+  TRY_CU(cudaStreamSynchronize(s));
+  *out = tr;
+  return PACT_OK;
+#undef TRY_CU
+#undef TRY_ST
+}
+
+int pact_trainer_step(pact_trainer* tr, int32_t n_steps) {
+  if (!tr) return validation("pact_trainer_step: null trainer").code;
+  for (int i = 0; i < n_steps; ++i) {
+    if (tr->graph) {
+      PACT_CUDA(cudaGraphLaunch(tr->graph, tr->eng.stream));
+      tr->eng.launches.fetch_add(tr->graph_kernels);
+    } else {
+      int64_t before = tr->eng.launches.load();
+      PACT_TRY(enqueue_step(tr));
+      // the first (eager) step configures kernel attributes and scratch; later
+      // steps replay it as one graph
+      if (tr->cfg.use_cuda_graph && tr->steps_done == 0) {
+        tr->graph_kernels = tr->eng.launches.load() - before;
+        PACT_TRY(capture_graph(tr));
+      }
+    }
+    ++tr->steps_done;
+  }
+  return PACT_OK;
+}
+
+int pact_trainer_report(pact_trainer* tr, int32_t epoch, double* report3) {
+  if (!tr) return validation("pact_trainer_report: null trainer").code;
+  double rep[4];
+  unsigned flags = 0;
+  PACT_CUDA(cudaMemcpyAsync(rep, tr->report, sizeof(double) * 3, cudaMemcpyDeviceToHost,
+                            tr->eng.stream));
+  PACT_CUDA(cudaMemcpyAsync(&flags, tr->flags, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                            tr->eng.stream));
+  PACT_CUDA(cudaStreamSynchronize(tr->eng.stream));
+  if (flags) {
+    const char* what = (flags & kFlagSos)    ? "non-finite rendered SOS"
+                       : (flags & kFlagLoss) ? "non-finite data loss"
+                       : (flags & kFlagTv)   ? "non-finite TV loss"
+                                             : "non-finite parameter gradient";
+    set_error("joint_reconstruct: %s at epoch %d", what, epoch);
+    return PACT_E_NUMERICAL;
+  }
+  if (report3) std::memcpy(report3, rep, sizeof(double) * 3);
+  return PACT_OK;
+}
+
+int pact_trainer_run_epoch(pact_trainer* tr, int32_t epoch, double* report4) {
+  if (!tr) return validation("pact_trainer_run_epoch: null trainer").code;
+  auto t0 = std::chrono::steady_clock::now();
+  int rc = pact_trainer_step(tr, tr->cfg.steps_per_epoch);
+  if (rc) return rc;
+  double rep[3];
+  rc = pact_trainer_report(tr, epoch, rep);
+  if (rc) return rc;
+  double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (report4) {
+    report4[0] = rep[0];
+    report4[1] = rep[1];
+    report4[2] = rep[2];
+    report4[3] = wall;
+  }
+  return PACT_OK;
+}
+
+int pact_trainer_finish(pact_trainer* tr, float* image, float* sos) {
+  if (!tr) return validation("pact_trainer_finish: null trainer").code;
+  pact_ctx* e = &tr->eng;
+  const size_t npx = static_cast<size_t>(tr->grid.width) * tr->grid.height;
+  const size_t P2 = static_cast<size_t>(tr->P) * tr->P;
+  // render_sos + deconvolve_image with the learned field (optimize.hpp:478-486)
+  PACT_TRY(siren_forward(e, tr->shape, tr->theta32, tr->sw, tr->dv));
+  PACT_TRY(launch_wavefront(e, tr->ray, tr->w));
+  void* tmp = nullptr;
+  PACT_TRY(scratch_get(e, kScratchGeneric1, sizeof(float2) * tr->n_patches * P2 +
+                                                sizeof(float) * tr->n_patches * P2 + 256,
+                       &tmp));
+  float2* X = static_cast<float2*>(tmp);
+  float* patches = reinterpret_cast<float*>(X + tr->n_patches * P2);
+  if (image) {
+    PACT_TRY(launch_wiener(e, tr->ftab.tab, tr->Y, tr->w, tr->n_patches, tr->cfg.eps_deconv, X));
+    PACT_TRY(launch_patch_ifft_real(e, tr->P, tr->n_patches, X, patches));
+    PACT_TRY(launch_merge(e, tr->lay, patches, tr->win, image));
+  }
+  if (sos) PACT_TRY(launch_sos_from_dev(e, tr->dv, npx, tr->v0, sos));
+  // outputs visible on the caller's stream
+  cudaEvent_t ev;
+  cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  cudaEventRecord(ev, e->stream);
+  cudaStreamWaitEvent(tr->user->stream, ev, 0);
+  cudaEventDestroy(ev);
+  tr->user->launches.fetch_add(e->launches.exchange(0));
+  return PACT_OK;
+}
+
+int pact_trainer_get_theta(pact_trainer* tr, double* theta) {
+  if (!tr || !theta) return validation("pact_trainer_get_theta: null argument").code;
+  PACT_CUDA(cudaMemcpyAsync(theta, tr->theta, sizeof(double) * tr->n_params,
+                            cudaMemcpyDeviceToHost, tr->eng.stream));
+  PACT_CUDA(cudaStreamSynchronize(tr->eng.stream));
+  return PACT_OK;
+}
+
+int pact_trainer_set_theta(pact_trainer* tr, const double* theta) {
+  if (!tr || !theta) return validation("pact_trainer_set_theta: null argument").code;
+  std::vector<float> t32(theta, theta + tr->n_params);
+  PACT_CUDA(cudaMemcpyAsync(tr->theta, theta, sizeof(double) * tr->n_params,
+                            cudaMemcpyHostToDevice, tr->eng.stream));
+  PACT_CUDA(cudaMemcpyAsync(tr->theta32, t32.data(), sizeof(float) * tr->n_params,
+                            cudaMemcpyHostToDevice, tr->eng.stream));
+  PACT_CUDA(cudaStreamSynchronize(tr->eng.stream));
+  return PACT_OK;
+}
+
+void* pact_trainer_buffer(pact_trainer* tr, int32_t what) {
+  if (!tr) return nullptr;
+  switch (what) {
+    case 0: return tr->stack;
+    case 1: return tr->Y;
+    case 2: return tr->dv;
+    case 3: return tr->w;
+    case 4: return tr->dw;
+    case 5: return tr->gv;
+    case 6: return tr->grad;
+    case 7: return tr->theta;
+    default: return nullptr;
+  }
+}
+
+int pact_trainer_destroy(pact_trainer* tr) {
+  if (!tr) return PACT_OK;
+  if (tr->eng.stream) cudaStreamSynchronize(tr->eng.stream);
+  if (tr->user) tr->user->launches.fetch_add(tr->eng.launches.exchange(0));
+  if (tr->graph) cudaGraphExecDestroy(tr->graph);
+  siren_work_free(tr->sw);
+  fourier_table_free(tr->ftab);
+  for (auto& sc : tr->eng.scratch)
+    if (sc.ptr) cudaFree(sc.ptr);
+  if (tr->arena) cudaFree(tr->arena);
+  if (tr->eng.own_stream) cudaStreamDestroy(tr->eng.own_stream);
+  delete tr;
+  return PACT_OK;
+}
+
+int64_t pact_trainer_launch_count(pact_trainer* tr) { return tr ? tr->eng.launches.load() : -1; }
+
+int pact_joint_reconstruct(pact_ctx* ctx, const pact_ring* ring, const pact_signal_meta* meta,
+                           const float* signals, const pact_grid* grid, const pact_mask* mask,
+                           const pact_train_config* cfg, double* reports, float* image,
+                           float* sos, double* theta) {
+  pact_trainer* tr = nullptr;
+  int rc0 = pact_trainer_create(ctx, ring, meta, signals, grid, mask, cfg, &tr);
+  if (rc0) return rc0;
+  for (int e = 1; e <= cfg->epochs; ++e) {
+    int rc = pact_trainer_run_epoch(tr, e, reports ? reports + 4 * (e - 1) : nullptr);
+    if (rc) {
+      pact_trainer_destroy(tr);
+      return rc;
+    }
+  }
+  int rc = pact_trainer_finish(tr, image, sos);
+  if (!rc && theta) rc = pact_trainer_get_theta(tr, theta);
+  pact_trainer_destroy(tr);
+  return rc;
+}
+
+}  // extern "C"

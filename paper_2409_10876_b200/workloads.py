@@ -140,3 +140,16 @@ def phantom_rasters(w: Workload, seed: int = 0):
         blob[r2 > (3 * sg) ** 2] = 0.0
         p += blob
     return p, sos
+
+
+def train_config(w: Workload, **kw):
+    """TrainConfig for a workload (Appendix A; reference defaults elsewhere)."""
+    from .api import TrainConfig
+
+    c = TrainConfig(delays=tuple(w.delays), eps_deconv=w.eps_deconv, n_angles=w.n_angles,
+                    ray_step=w.ray_step, hidden=w.hidden, sine_layers=w.sine_layers,
+                    omega0=w.omega0, out_scale=w.out_scale, patch_mm=w.patch_mm,
+                    overlap=w.overlap, merge_fwhm=w.merge_fwhm, lambda_tv=w.lambda_tv)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c

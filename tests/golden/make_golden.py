@@ -65,11 +65,105 @@ def das_cases(R):
          sig=sig1.astype(np.float32), delays=np.array(w.delays), v0=np.array(w.v0), out=out1)
 
 
+def small_case(R):
+    """testsupport::SmallInstance (proj/tests/test_support.hpp:38-75), through
+    every hot-path entry point of the reference."""
+    import ctypes as C
+
+    import golden_util as gu
+    from paper_2409_10876_b200.api import SirenSpec
+
+    si = gu.small_instance()
+    T = C.c_int(0)
+    t0 = C.c_double(0)
+    R.call("small_instance_signals", None, C.byref(T), C.byref(t0))
+    sig = np.zeros((si.ring.n_transducers, T.value))
+    R.call("small_instance_signals", sig.ctypes.data_as(C.c_void_p), C.byref(T), C.byref(t0))
+    sig = sig.astype(np.float32).astype(np.float64)  # both sides consume fp32 values
+    meta = SignalMetaInfo(T.value, 25e-9, t0.value, 1500.0)
+    cfg = si.cfg
+    spec = SirenSpec(cfg.hidden, cfg.sine_layers, cfg.omega0, cfg.out_scale, 1500.0)
+    n_params = spec.param_count()
+    theta0 = R.init_siren(0, spec, n_params)
+    theta2 = R.init_siren(2, spec, n_params)
+    stack = R.das_stack(sig, si.ring, meta, si.grid, 1500.0, cfg.delays, workers=1)
+    Y = R.patch_spectra(stack, cfg.delays, 1500.0, si.grid, cfg.patch_mm, cfg.overlap, 1)
+    step = R.nf_step(sig, si.ring, meta, si.grid, si.mask, cfg, theta2)
+    lay = R.patch_layout(si.grid, cfg.patch_mm, cfg.overlap)
+    H0 = R.transfer_stack(step["w"][0], cfg.delays, lay["P"], si.grid.pitch)
+    tv_val, tv_grad = R.tv_loss(si.grid, step["sos"], si.mask, cfg.lambda_tv)
+    from dataclasses import replace
+
+    jcfg = replace(cfg, epochs=3, steps_per_epoch=2, seed=5)
+    reports, jimg, jsos, jtheta = R.joint_reconstruct(sig, si.ring, meta, si.grid, si.mask, jcfg,
+                                                      n_params)
+    # deconvolve_image under the rendered SOS (deconv.hpp:176-198)
+    dimg = R.deconvolve_image(stack, cfg.delays, 1500.0, si.grid, step["sos"], si.ring, si.mask,
+                              cfg.patch_mm, cfg.overlap, cfg.eps_deconv, cfg.n_angles,
+                              cfg.ray_step, cfg.merge_fwhm, 1)
+    save("small_instance", sig=sig.astype(np.float32), meta=meta_arr(meta), theta0=theta0,
+         theta2=theta2, stack=stack, Y=Y.astype(np.complex64), sos=step["sos"], w=step["w"],
+         dw=step["dw"], loss_patch=step["loss_patch"], data_term=np.array(step["data_term"]),
+         tv_term=np.array(step["tv_term"]), grad_v_masked=step["grad_v_masked"],
+         grad_theta=step["grad_theta"], image=step["image"], H0=H0, tv_value=np.array(tv_val),
+         tv_grad=tv_grad, deconv=dimg, reports=reports, joint_image=jimg, joint_sos=jsos,
+         joint_theta=jtheta)
+
+
+def cfg2_case(R):
+    """BASELINE configs[1] (cfg2, Appendix A): simulated signals, one forward +
+    gradient evaluation at the seed-0 SIREN, and the deconvolved image."""
+    from paper_2409_10876_b200.api import CircularMask, SirenSpec
+
+    w = wl.cfg2()
+    sig = gu_simulate(R, w, seed=0)
+    cfg = wl.train_config(w)
+    spec = SirenSpec(cfg.hidden, cfg.sine_layers, cfg.omega0, cfg.out_scale, w.v0)
+    theta = R.init_siren(0, spec, spec.param_count())
+    step = R.nf_step(sig, w.ring, w.meta, w.grid, w.mask, cfg, theta)
+    g = w.grid
+    crop = GridSpec(32, 32, g.pitch, g.origin_x + 100 * g.pitch, g.origin_y + 60 * g.pitch)
+    das_crop = R.das_stack(sig, w.ring, w.meta, crop, w.v0, cfg.delays)
+    lay = R.patch_layout(g, cfg.patch_mm, cfg.overlap)
+    H24 = R.transfer_stack(step["w"][24], cfg.delays, lay["P"], g.pitch)
+    save("cfg2_step", sig=sig.astype(np.float32), theta=theta, das_crop=das_crop.astype(np.float32),
+         crop=grid_arr(crop), sos=step["sos"].astype(np.float32), w=step["w"], dw=step["dw"],
+         loss_patch=step["loss_patch"], data_term=np.array(step["data_term"]),
+         tv_term=np.array(step["tv_term"]), grad_theta=step["grad_theta"],
+         image=step["image"].astype(np.float32), H24=H24.astype(np.complex64))
+
+
+def gu_simulate(R, w, seed):
+    """simulate_signals (phantom.hpp:282-362) of the Appendix A phantom, through
+    the reference; SOS mask = disc of the image half-diagonal (D5)."""
+    import math
+
+    p, sos = wl.phantom_rasters(w, seed)
+    g = w.grid
+    r_half = math.hypot((g.width - 1) * g.pitch / 2, (g.height - 1) * g.pitch / 2) + g.pitch
+    out = np.zeros((w.ring.n_transducers, w.meta.n_samples))
+    pr = np.ascontiguousarray(p)
+    so = np.ascontiguousarray(sos)
+    import ctypes as C
+
+    R.call("simulate_signals", g.width, g.height, g.pitch, g.origin_x, g.origin_y,
+           pr.ctypes.data_as(C.c_void_p), so.ctypes.data_as(C.c_void_p), 0.0, 0.0, r_half, w.v0,
+           w.ring.n_transducers, w.ring.radius, w.ring.angle_offset, 100e-9, w.meta.dt, w.meta.t0,
+           w.meta.n_samples, 0.05, 0, out.ctypes.data_as(C.c_void_p))
+    return out.astype(np.float32).astype(np.float64)
+
+
 def main():
     R = ref()
     if R is None:
         sys.exit("oracle/_ref/libpact_ref.so missing: make -C oracle ref")
-    das_cases(R)
+    which = sys.argv[1:] or ["das", "small", "cfg2"]
+    if "das" in which:
+        das_cases(R)
+    if "small" in which:
+        small_case(R)
+    if "cfg2" in which:
+        cfg2_case(R)
 
 
 if __name__ == "__main__":
