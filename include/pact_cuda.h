@@ -126,6 +126,16 @@ int pact_das_stack(pact_ctx* ctx, const pact_ring* ring, const pact_signal_meta*
                    const float* signals, const pact_grid* grid, double v0,
                    const double* delays, int32_t n_delays, float* out);
 
+/* simulate_signals, phantom.hpp:282-362 (+ time_of_flight, aberration.hpp:79-100):
+ * the input-side step before DAS.  pressure, sos: HOST fp64 [H][W] rasters of
+ * the Phantom on `grid`; mask = Phantom::mask (TOF integration disc);
+ * meta->t0 / n_samples fix the window (SimulateOptions t0 / n_samples);
+ * out: device fp32 [n_transducers][n_samples]. */
+int pact_simulate_signals(pact_ctx* ctx, const pact_grid* grid, const double* pressure,
+                          const double* sos, const pact_mask* mask, double background_sos,
+                          const pact_ring* ring, double pulse_sigma,
+                          const pact_signal_meta* meta, double ray_step, float* out);
+
 /* ---- patch layout (host) ---- */
 
 /* make_patch_layout, core.hpp:252-281 (same validation and messages). */

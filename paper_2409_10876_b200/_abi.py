@@ -109,6 +109,8 @@ SIGNATURES = {
     "pact_make_delays": (C.c_int, [_D, _D, _I, _DP]),
     "pact_das_stack": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(SignalMeta), _P,
                                  C.POINTER(Grid), _D, _DP, _I, _P]),
+    "pact_simulate_signals": (C.c_int, [_P, C.POINTER(Grid), _DP, _DP, C.POINTER(Mask), _D,
+                                        C.POINTER(Ring), _D, C.POINTER(SignalMeta), _D, _P]),
     "pact_make_patch_layout": (C.c_int, [C.POINTER(Grid), _D, _D, C.POINTER(Layout)]),
     "pact_layout_n_patches": (C.c_int32, [C.POINTER(Layout)]),
     "pact_layout_patches": (C.c_int, [C.POINTER(Layout), _IP, _DP]),

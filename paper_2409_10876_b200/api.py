@@ -339,7 +339,22 @@ def _ctx_methods():
         check(_abi.lib().pact_adam_step(self._h, theta.numel(), dptr(theta), dptr(grad), dptr(m),
                                         dptr(v), t, lr, beta1, beta2, eps))
 
-    for f in (render_sos, siren_backward, wavefront, transfer_stack, patch_spectra,
+    def simulate_signals(self, grid: GridSpec, pressure, sos, mask: CircularMask,
+                         background_sos: float, ring: RingGeometry, meta: SignalMetaInfo,
+                         pulse_sigma: float = 100e-9, ray_step: float = 0.05) -> torch.Tensor:
+        """simulate_signals, phantom.hpp:282-362 -> fp32 [N, T] on the device."""
+        pr = np.ascontiguousarray(pressure, np.float64)
+        so = np.ascontiguousarray(sos, np.float64)
+        out = torch.empty((ring.n_transducers, meta.n_samples), device="cuda", dtype=torch.float32)
+        g, m, r, mt = grid.c(), mask.c(), ring.c(), meta.c()
+        check(_abi.lib().pact_simulate_signals(self._h, C.byref(g),
+                                               pr.ctypes.data_as(C.POINTER(C.c_double)),
+                                               so.ctypes.data_as(C.POINTER(C.c_double)),
+                                               C.byref(m), background_sos, C.byref(r), pulse_sigma,
+                                               C.byref(mt), ray_step, dptr(out)))
+        return out
+
+    for f in (simulate_signals, render_sos, siren_backward, wavefront, transfer_stack, patch_spectra,
               deconvolve_image, loss_grad, ray_backward, tv_loss, adam_step):
         setattr(Context, f.__name__, f)
 

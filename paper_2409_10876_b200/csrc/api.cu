@@ -139,11 +139,6 @@ Status siren_state(pact_ctx* ctx, const pact_siren& s, const pact_grid& g, const
   return {};
 }
 
-__global__ void fill_kernel(float* x, size_t n, float v) {
-  size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-  if (i < n) x[i] = v;
-}
-
 __global__ void add_const_kernel(const float* __restrict__ dv, size_t n, float v0,
                                  float* __restrict__ out) {
   size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;

@@ -153,3 +153,17 @@ def train_config(w: Workload, **kw):
     for k, v in kw.items():
         setattr(c, k, v)
     return c
+
+
+def simulation_mask(w: Workload) -> CircularMask:
+    """D5: the simulator's TOF disc = image half-diagonal (+ one pitch)."""
+    g = w.grid
+    return CircularMask(0.0, 0.0, math.hypot((g.width - 1) * g.pitch / 2,
+                                             (g.height - 1) * g.pitch / 2) + g.pitch)
+
+
+def simulate(ctx, w: Workload, seed: int = 0):
+    """Signals of the seeded Appendix-A phantom, simulated on the GPU
+    (pact_simulate_signals); fp32 [N, T] device tensor."""
+    p, sos = phantom_rasters(w, seed)
+    return ctx.simulate_signals(w.grid, p, sos, simulation_mask(w), w.v0, w.ring, w.meta)

@@ -104,11 +104,32 @@ def test_ray_backward(ctx, G, si):
     assert err <= GRAD_TOL, err
 
 
+def tv_unambiguous(grid, mask, sos, rtol=1e-6):
+    """Masked pixels none of whose TV pairs has |dv| below fp32 resolution
+    (sign() there is a tie in one precision and not the other)."""
+    idx, _ = masked_pixels(grid, mask)
+    W, H = grid.width, grid.height
+    inm = np.zeros(W * H, bool)
+    inm[idx] = True
+    v = sos.ravel()
+    amb = np.zeros(W * H, bool)
+    for p in idx:
+        x, y = p % W, p // W
+        for q, ok in ((p + 1, x + 1 < W), (p + W, y + 1 < H)):
+            if ok and inm[q] and abs(v[q] - v[p]) <= rtol * abs(v[p]):
+                amb[p] = amb[q] = True
+    return ~amb[idx]
+
+
 def test_tv_loss(ctx, G, si):
-    raster = torch.as_tensor(G["sos"].astype(np.float32)).cuda()
-    val, grad = ctx.tv_loss(si.grid, si.mask, raster, si.cfg.lambda_tv)
+    # the raster is passed as v - v0 (fp32 keeps the full relative precision)
+    val, grad = ctx.tv_loss(si.grid, si.mask, _dev(G), si.cfg.lambda_tv)
     assert abs(val - float(G["tv_value"])) <= LOSS_TOL * abs(float(G["tv_value"]))
-    assert rel_l2(grad.double().cpu().numpy(), G["tv_grad"]) <= GRAD_TOL
+    keep = tv_unambiguous(si.grid, si.mask, G["sos"])
+    assert keep.mean() > 0.95
+    # gradients are lambda * (sum of signs): compare the integer sign sums
+    np.testing.assert_array_equal(np.round(grad.double().cpu().numpy()[keep] / si.cfg.lambda_tv),
+                                  np.round(G["tv_grad"][keep] / si.cfg.lambda_tv))
 
 
 def test_siren_backward(ctx, G, si):
