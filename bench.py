@@ -3,15 +3,22 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One JSON line on rank 0.  For N > 1 the driver launches one process per GPU
-with torchrun; ranks shard independent units (weak scaling) and the timed
-region is bracketed by barrier + synchronize, max over ranks.
+Workload (BASELINE.json configs[3], "cfg4"): 8 independent cfg3 frames
+(N=512 transducers, T=4096, 512x512 @ 0.1 mm, K=32 delays, 225 patches of
+64x64, SIREN 2->128x4->1), seeds 0-7, sharded over the ranks (frame f on rank
+f % N).  A step is one NF-APACT iteration (optimize.hpp:413-471: render ->
+wavefronts -> fused Fourier loss -> ray backward -> TV -> SIREN backward ->
+Adam) of every frame; `value` is frame-iterations/s over the whole job.
+`e2e` runs each frame end to end through the C-ABI (pact_joint_reconstruct,
+10 iterations as the cfg4 frame definition of SURVEY §8(d)) from pinned host
+signals to a host image.  One JSON line on rank 0.
 """
 from __future__ import annotations
 
 import argparse
 import ctypes as C
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -26,16 +33,18 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+N_FRAMES = 8
+E2E_ITERS = 10
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # FFMA pipe at max clock
 
 
 def peaks():
     try:
         with open(PEAKS_PATH) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), float(p["bf16_tflops_sustained"]), "measured"
     except Exception:
-        return FALLBACK_HBM_GBS, "fallback"
+        return 6650.0, 1400.0, "fallback (B200_PROFILING.md)"
 
 
 class Clocks:
@@ -50,14 +59,13 @@ class Clocks:
         self.proc = None
         self.lines = []
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                  "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
         return self
@@ -66,7 +74,7 @@ class Clocks:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
-    def __exit__(self, *a):
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             try:
@@ -94,70 +102,115 @@ class Clocks:
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def ray_steps(w, cfg):
+    """Total midpoint steps of one wavefront pass (make_ray / aberration.hpp:153-171)."""
+    from paper_2409_10876_b200.api import make_patch_layout
+
+    lay = make_patch_layout(w.grid, cfg.patch_mm, cfg.overlap)
+    c = lay.centers
+    th = 2 * np.pi * np.arange(cfg.n_angles) / cfg.n_angles
+    ux, uy = np.cos(th)[None, :], np.sin(th)[None, :]
+    cx, cy = c[:, :1], c[:, 1:]
+    R = w.ring.radius
+    b = cx * ux + cy * uy
+    cc = cx**2 + cy**2 - R * R
+    t_ring = -b + np.sqrt(b * b - cc)
+    ex, ey = cx + ux * t_ring, cy + uy * t_ring
+    dx, dy = ex - cx, ey - cy
+    ln = np.hypot(dx, dy)
+    vx, vy = dx / ln, dy / ln
+    m = w.mask
+    mx, my = cx - m.center_x, cy - m.center_y
+    bq = mx * vx + my * vy
+    cq = mx * mx + my * my - m.radius**2
+    disc = bq * bq - cq
+    s = np.sqrt(np.maximum(disc, 0))
+    t0 = np.maximum(-bq - s, 0)
+    t1 = np.minimum(-bq + s, ln)
+    ok = (disc >= 0) & (t0 < t1)
+    n = np.where(ok, np.maximum(1, np.ceil((t1 - t0) / cfg.ray_step)), 0)
+    return int(n.sum())
+
+
+def work_model(w, cfg, n_masked):
+    """Algorithmic work of one iteration per stage."""
+    H, L = cfg.hidden, cfg.sine_layers
+    mac_px = 2 * H + (L - 1) * H * H + H
+    from paper_2409_10876_b200.api import make_patch_layout
+
+    lay = make_patch_layout(w.grid, cfg.patch_mm, cfg.overlap)
+    P = lay.patch_pixels
+    steps = ray_steps(w, cfg)
+    return {
+        "siren_flops": 6.0 * mac_px * n_masked,
+        "ray_steps": steps,
+        "wavefront_bytes": 16.0 * steps,
+        "ray_backward_bytes": 16.0 * steps,
+        "fused_loss_bytes": 8.0 * lay.n_patches * len(cfg.delays) * P * P,
+    }
 
 
 # --------------------------------------------------------------------------- #
-# CPU reference arm: the reference's own das_stack (oracle/_ref), all threads
+# CPU reference arm: the reference's own iteration (oracle/_ref), all threads
 # --------------------------------------------------------------------------- #
 
-def ref_das_seconds(w, sig64, reps, workers):
-    from oracle_lib import REF_PATH
-
-    L = C.CDLL(REF_PATH)
-    f = L.ref_time_das_stack
-    _D, _I, _P = C.c_double, C.c_int, C.c_void_p
-    f.argtypes = [_I, _I, _D, _D, _I, _D, _D, _P, _I, _I, _D, _D, _D, _D, _I, _P, _I]
-    f.restype = C.c_double
-    d = np.ascontiguousarray(w.delays, dtype=np.float64)
-    g = w.grid
-    return f(reps, w.ring.n_transducers, w.ring.radius, w.ring.angle_offset, w.meta.n_samples,
-             w.meta.dt, w.meta.t0, sig64.ctypes.data_as(_P), g.width, g.height, g.pitch,
-             g.origin_x, g.origin_y, w.v0, len(d), d.ctypes.data_as(_P), workers)
+SLAB_ROWS = 128
 
 
-def cpu_slab(w, rows):
-    """A row slab of the workload's grid (bounded CPU sample)."""
-    from paper_2409_10876_b200.api import GridSpec
+def ref_iteration_seconds(w, cfg, sig64, theta):
+    """One reference iteration on a SLAB_ROWS-row slab of the cfg3 grid
+    (render + per-patch wavefront/fused loss/trace + TV + backprop), seconds."""
     from dataclasses import replace
 
+    from oracle_lib import ref
+    from paper_2409_10876_b200.api import GridSpec
+
+    R = ref()
     g = w.grid
-    y0 = (g.height - rows) // 2
-    slab = GridSpec(g.width, rows, g.pitch, g.origin_x, g.origin_y + y0 * g.pitch)
-    return replace(w, grid=slab)
+    y0 = (g.height - SLAB_ROWS) // 2
+    slab = GridSpec(g.width, SLAB_ROWS, g.pitch, g.origin_x, g.origin_y + y0 * g.pitch)
+    ws = replace(w, grid=slab)
+    out = R.nf_step(sig64, ws.ring, ws.meta, slab, ws.mask, cfg, theta, want_image=False)
+    return out["seconds"], g.height / SLAB_ROWS
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
-    from paper_2409_10876_b200 import workloads as wl
-
-    w = wl.cfg3()
     if rank != 0:
         return
+    from paper_2409_10876_b200 import workloads as wl
+    from paper_2409_10876_b200.api import SirenSpec, init_siren
+
+    w = wl.cfg3()
+    cfg = wl.train_config(w, workers=0)
     cores = os.cpu_count() or 1
     sig = wl.iid_signals(w, 0).astype(np.float64)
-    # bounded sample: a 64-row slab of the cfg3 grid (1/8 of the taps)
-    slab = cpu_slab(w, 64)
-    frac = slab.das_samples / w.das_samples
-    for _ in range(args.warmup):
-        ref_das_seconds(slab, sig, 1, cores)
-    secs = [ref_das_seconds(slab, sig, 1, cores) for _ in range(args.steps)]
+    theta = init_siren(0, SirenSpec(cfg.hidden, cfg.sine_layers, cfg.omega0, cfg.out_scale, w.v0))
+    for _ in range(min(args.warmup, 1)):
+        ref_iteration_seconds(w, cfg, sig, theta)
+    secs = []
+    for _ in range(args.steps):
+        s, scale = ref_iteration_seconds(w, cfg, sig, theta)
+        secs.append(s * scale)
     t = sum(secs)
-    value = args.steps * slab.das_samples / t / 1e9
+    value = args.steps / t
+    sample = (f"reference iteration (render_sos, wavefront_profile, fused_patch_loss_grad, "
+              f"wavefront_grad_trace, tv_loss, backprop_sos) on a {SLAB_ROWS}x512 slab of one cfg3 "
+              f"frame per step, time x{512 // SLAB_ROWS} (pixel ratio), workers={cores}")
     line = {
-        "metric": "DAS-stack GSamples/s", "value": value, "unit": "GSamples/s",
+        "metric": "NF-APACT iterations/s", "value": value, "unit": "frame-iterations/s",
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * t / args.steps / frac, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg3 DAS stack (N=512, T=4096, 512x512, K=32)",
-                   "signals": "iid N(0,1) seed 0", "sample": "64-row slab of the grid per step"},
-        "cpu_baseline": {"value": value, "unit": "GSamples/s", "cores": cores,
-                         "kind": "reference",
-                         "sample": "das_stack on a 64x512-pixel slab (1/8 of cfg3) per step"},
-        "e2e": {"value": value, "unit": "GSamples/s", "h2d_bytes_per_step": 0,
+        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg4: 8 x cfg3 frames (N=512, T=4096, 512x512, K=32, 225 patches, "
+                               "SIREN 2->128x4->1)", "signals": "iid N(0,1) (cost is content-independent)"},
+        "cpu_baseline": {"value": value, "unit": "frame-iterations/s", "cores": cores,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "frame-iterations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -178,122 +231,191 @@ def run_ours(args):
 
     from paper_2409_10876_b200 import _abi
     from paper_2409_10876_b200 import workloads as wl
-    from paper_2409_10876_b200.api import Context
+    from paper_2409_10876_b200.api import Context, SirenSpec, Trainer, joint_reconstruct
 
     w = wl.cfg3()
+    cfg = wl.train_config(w)
     ctx = Context(local)
-    stream = torch.cuda.current_stream()
     L = _abi.lib()
+    my_frames = [f for f in range(N_FRAMES) if f % world == rank]
+    hbm, bf16, peak_src = peaks()
 
-    # Each rank beamforms its own frame (seed = rank): independent units.
-    sig_h = wl.iid_signals(w, rank)
-    sig = torch.as_tensor(sig_h).cuda()
-    K, H, W = len(w.delays), w.grid.height, w.grid.width
-    out = torch.empty((K, H, W), device="cuda", dtype=torch.float32)
+    # ---- inputs: simulated on the GPU from seeded phantoms (one-time) ----
+    signals = {f: wl.simulate(ctx, w, seed=f) for f in my_frames}
+    torch.cuda.synchronize()
+
+    # ---- DAS stack on its own (the one-time part-1 kernel) ----
     flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda", dtype=torch.float32)
+    stack = torch.empty((len(w.delays), w.grid.height, w.grid.width), device="cuda")
+    s0 = signals[my_frames[0]]
+    for _ in range(3):
+        ctx.das_stack(s0, w.ring, w.meta, w.grid, w.v0, w.delays, out=stack)
+    das_ms = []
+    for _ in range(5):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        ctx.das_stack(s0, w.ring, w.meta, w.grid, w.v0, w.delays, out=stack)
+        b.record()
+        torch.cuda.synchronize()
+        das_ms.append(a.elapsed_time(b))
+    das_t = statistics.median(das_ms)
+    das_ach = w.das_bytes / (das_t * 1e-3) / 1e9
+    del stack
 
-    def step():
-        ctx.das_stack(sig, w.ring, w.meta, w.grid, w.v0, w.delays, out=out)
+    # ---- engines: one trainer per frame (DAS + spectra + init, one-time) ----
+    trainers = [Trainer(ctx, signals[f], w.ring, w.meta, w.grid, w.mask,
+                        wl.train_config(w, seed=f)) for f in my_frames]
+    torch.cuda.synchronize()
+    n_masked = int(L.pact_masked_count(C.byref(w.grid.c()), C.byref(w.mask.c())))
+    work = work_model(w, cfg, n_masked)
 
-    clk = Clocks(local).__enter__()  # sampling starts with the warm-up load
-    t_w = time.time()
-    n_warm = 0
-    while n_warm < max(3, args.warmup) or time.time() - t_w < 0.5:
-        step()
-        n_warm += 1
-        if n_warm % 8 == 0:
-            torch.cuda.synchronize()
+    def step_all():
+        for tr in trainers:
+            tr.step(1)
+
+    clk = Clocks(local).start()
+    for _ in range(max(3, args.warmup)):
+        step_all()
+    torch.cuda.synchronize()
+    stages = trainers[0].profile_step()  # one eager iteration with per-stage events
     torch.cuda.synchronize()
 
-    # ---- device-resident timed region ----
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
+    # ---- timed region: K iterations of every frame, frames on their own streams ----
+    tstream = torch.cuda.current_stream()
+    streams = [tr.stream() for tr in trainers]
+    n0 = sum(tr.launch_count() for tr in trainers)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    n0 = ctx.launch_count()
-    for i in range(args.steps):
-        flush.zero_()  # L2 flush (256 MB > 126 MB L2) outside the event pair
-        ev[i][0].record(stream)
-        step()
-        ev[i][1].record(stream)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(tstream)
+    for s in streams:
+        s.wait_event(start)
+    for _ in range(args.steps):
+        step_all()
+    for s in streams:
+        e = torch.cuda.Event()
+        e.record(s)
+        tstream.wait_event(e)
+    end.record(tstream)
     torch.cuda.synchronize()
-    clk.__exit__()
-    launches = ctx.launch_count() - n0
+    clk.stop()
+    launches = sum(tr.launch_count() for tr in trainers) - n0
     if world > 1:
         dist.barrier()
-    ms = [a.elapsed_time(b) for a, b in ev]
-    t_ms = torch.tensor([sum(ms)], device="cuda", dtype=torch.float64)
+    t_ms = torch.tensor([start.elapsed_time(end)], device="cuda", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     total_ms = float(t_ms.item())
-    per_step_ms = total_ms / args.steps
-    value = world * w.das_samples * args.steps / (total_ms * 1e-3) / 1e9
+    value = N_FRAMES * args.steps / (total_ms * 1e-3)
+    reports = [tr.report() for tr in trainers]
+    for tr in trainers:
+        tr.close()
+    del trainers
 
-    # ---- end-to-end through the C-ABI with host buffers ----
-    nbytes_in = sig_h.nbytes
-    nbytes_out = K * H * W * 4
-    hin = C.c_void_p()
-    hout = C.c_void_p()
-    _abi.check(L.pact_host_alloc_pinned(nbytes_in, C.byref(hin)))
-    _abi.check(L.pact_host_alloc_pinned(nbytes_out, C.byref(hout)))
-    C.memmove(hin, sig_h.ctypes.data, nbytes_in)
-    e2e_ms = []
-    for i in range(args.warmup + args.steps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        flush.zero_()
-        a.record(stream)
-        _abi.check(L.pact_upload(ctx.handle, C.c_void_p(sig.data_ptr()), hin, nbytes_in))
-        step()
-        _abi.check(L.pact_download(ctx.handle, hout, C.c_void_p(out.data_ptr()), nbytes_out))
-        b.record(stream)
-        torch.cuda.synchronize()
-        if i >= args.warmup:
-            e2e_ms.append(a.elapsed_time(b))
-    e2e_t = torch.tensor([sum(e2e_ms)], device="cuda", dtype=torch.float64)
+    # ---- end to end: pinned host signals -> joint_reconstruct -> host image ----
+    e2e_cfg = wl.train_config(w, epochs=E2E_ITERS, steps_per_epoch=1)
+    nbytes_in = w.ring.n_transducers * w.meta.n_samples * 4
+    nbytes_out = 2 * w.grid.width * w.grid.height * 4
+    hin = {f: torch.empty(signals[f].shape, dtype=torch.float32, pin_memory=True) for f in my_frames}
+    for f in my_frames:
+        hin[f].copy_(signals[f])
+    himg = torch.empty((2, w.grid.height, w.grid.width), dtype=torch.float32, pin_memory=True)
+    dsig = torch.empty_like(signals[my_frames[0]])
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for f in my_frames:
+        dsig.copy_(hin[f], non_blocking=True)
+        reps, img, sos, _ = joint_reconstruct(ctx, dsig, w.ring, w.meta, w.grid, w.mask,
+                                              wl.train_config(w, epochs=E2E_ITERS,
+                                                              steps_per_epoch=1, seed=f))
+        himg[0].copy_(img, non_blocking=True)
+        himg[1].copy_(sos, non_blocking=True)
+    b.record()
+    torch.cuda.synchronize()
+    e2e_t = torch.tensor([a.elapsed_time(b)], device="cuda", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = world * w.das_samples * args.steps / (float(e2e_t.item()) * 1e-3) / 1e9
-    L.pact_host_free_pinned(hin)
-    L.pact_host_free_pinned(hout)
+    e2e_value = N_FRAMES * E2E_ITERS / (float(e2e_t.item()) * 1e-3)
 
-    # ---- roofline of the dominant kernel (DAS) ----
-    hbm, src = peaks()
-    achieved = w.das_bytes / (per_step_ms * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None,
-                "peak_source": src,
-                "byte_model": "8*S + 4*K*W*H + 4*N*T (SURVEY 8(d)), S = W*H*K*N"}
+    # ---- roofline of the dominant stage ----
+    siren_ms = stages["siren_fwd"] + stages["siren_bwd"]
+    stage_rl = {
+        "siren_fwd+bwd": {"ms": siren_ms, "achieved_tflops": work["siren_flops"] / (siren_ms * 1e-3) / 1e12},
+        "wavefront": {"ms": stages["wavefront"],
+                      "achieved_gbs": work["wavefront_bytes"] / (stages["wavefront"] * 1e-3) / 1e9},
+        "ray_backward": {"ms": stages["ray_backward"],
+                         "achieved_gbs": work["ray_backward_bytes"] / (stages["ray_backward"] * 1e-3) / 1e9},
+        "fused_loss": {"ms": stages["fused_loss"],
+                       "achieved_gbs": work["fused_loss_bytes"] / (stages["fused_loss"] * 1e-3) / 1e9},
+        "tv_report": {"ms": stages["tv_report"]}, "adam": {"ms": stages["adam"]},
+    }
+    dominant = max(stage_rl, key=lambda k: stage_rl[k]["ms"])
+    if dominant == "siren_fwd+bwd":
+        ach = stage_rl[dominant]["achieved_tflops"]
+        roofline = {"bound": "tensor", "achieved": ach, "peak": bf16, "unit": "TFLOP/s",
+                    "frac": ach / bf16, "traffic": None, "kernel": "SIREN fwd+bwd (FP32 SIMT GEMMs)",
+                    "peak_source": f"{peak_src} bf16 dense sustained",
+                    "fp32_pipe_peak_tflops": FP32_PEAK_TFLOPS,
+                    "frac_of_fp32_pipe": ach / FP32_PEAK_TFLOPS,
+                    "work_model": "6 * MAC_px * masked pixels (SURVEY 8(d)); TF32/BF16 fail parity"}
+    else:
+        ach = stage_rl[dominant]["achieved_gbs"]
+        roofline = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                    "frac": ach / hbm, "traffic": None, "kernel": dominant,
+                    "peak_source": peak_src, "work_model": "SURVEY 8(d) algorithmic bytes"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle_lib import REF_PATH
 
         if os.path.exists(REF_PATH):
+            from paper_2409_10876_b200.api import init_siren
+
             cores = os.cpu_count() or 1
-            slab = cpu_slab(w, 32)
-            secs = ref_das_seconds(slab, sig_h.astype(np.float64), 1, cores)
-            cpu = {"value": slab.das_samples / secs / 1e9, "unit": "GSamples/s",
-                   "cores": cores, "kind": "reference",
-                   "sample": f"reference das_stack on a 32-row slab of cfg3 ({secs:.1f} s)"}
+            theta = init_siren(0, SirenSpec(cfg.hidden, cfg.sine_layers, cfg.omega0,
+                                            cfg.out_scale, w.v0))
+            sig64 = signals[0].double().cpu().numpy()
+            secs, scale = ref_iteration_seconds(w, wl.train_config(w, workers=0), sig64, theta)
+            cpu = {"value": 1.0 / (secs * scale), "unit": "frame-iterations/s", "cores": cores,
+                   "kind": "reference",
+                   "sample": f"one reference iteration on a {SLAB_ROWS}x512 slab of cfg3 frame 0 "
+                             f"({secs:.1f} s), scaled x{scale:g} by pixel count"}
         else:
-            cpu = {"value": None, "unit": "GSamples/s", "cores": 0, "kind": "reference",
+            cpu = {"value": None, "unit": "frame-iterations/s", "cores": 0, "kind": "reference",
                    "sample": "oracle/_ref missing on this machine"}
 
     if rank == 0:
         line = {
-            "metric": "DAS-stack GSamples/s", "value": value, "unit": "GSamples/s",
+            "metric": "NF-APACT iterations/s", "value": value, "unit": "frame-iterations/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": per_step_ms, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "cfg3 DAS stack (N=512, T=4096, 512x512 @0.1mm, K=32 in [-2,2] mm)",
-                       "signals": "iid N(0,1), seed = rank", "l2": "flushed (256 MB write) between steps",
-                       "parallelism": f"{world} independent frames"},
+            "config": {"workload": "cfg4: 8 independent cfg3 frames (N=512, T=4096, 512x512 @0.1mm, "
+                                   "K=32 in [-2,2] mm, 225 patches 64x64, SIREN 2->128x4->1, "
+                                   "512 angles, ray step 0.05 mm)",
+                       "frames_on_rank0": len(my_frames),
+                       "signals": "GPU straight-ray simulation of seeded phantoms (seeds 0-7)",
+                       "l2": "per-frame working set (Y 236 MB + activations 537 MB) > 126 MB L2",
+                       "parallelism": f"{world} rank(s), frames sharded f % N, one CUDA stream per frame"},
             "clocks": clk.summary(),
-            "e2e": {"value": e2e_value, "unit": "GSamples/s", "h2d_bytes_per_step": nbytes_in,
-                    "d2h_bytes_per_step": nbytes_out},
+            "e2e": {"value": e2e_value, "unit": "frame-iterations/s",
+                    "h2d_bytes_per_step": nbytes_in * N_FRAMES // world,
+                    "d2h_bytes_per_step": nbytes_out * N_FRAMES // world,
+                    "what": f"per frame: pinned H2D signals, pact_joint_reconstruct ({E2E_ITERS} "
+                            f"iterations incl. DAS, spectra, final deconvolution), D2H image+SOS"},
             "gpu_launches": launches,
             "roofline": roofline,
+            "stages_ms_one_frame": stage_rl,
+            "das": {"ms": das_t, "gsamples_per_s": w.das_samples / (das_t * 1e-3) / 1e9,
+                    "roofline": {"bound": "hbm", "achieved": das_ach, "peak": hbm, "unit": "GB/s",
+                                 "frac": das_ach / hbm, "peak_source": peak_src,
+                                 "byte_model": "8*S + 4*K*W*H + 4*N*T, S = W*H*K*N"}},
+            "loss_report_frame0": reports[0],
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

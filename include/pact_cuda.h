@@ -311,6 +311,12 @@ void* pact_trainer_buffer(pact_trainer* tr, int32_t what);
 int pact_trainer_destroy(pact_trainer* tr);
 /* Kernels the engine launched so far (graph replays counted per kernel). */
 int64_t pact_trainer_launch_count(pact_trainer* tr);
+/* The engine's private cudaStream_t (as void*), for event timing. */
+void* pact_trainer_stream(pact_trainer* tr);
+/* One iteration run eagerly with CUDA events between its stages; stage_ms[7]:
+ * SIREN forward, wavefront, fused loss, ray backward, TV+report, SIREN
+ * backward, Adam (device ms).  Synchronises. */
+int pact_trainer_profile_step(pact_trainer* tr, float* stage_ms);
 
 /* joint_reconstruct, optimize.hpp:367-494, end to end.  reports: HOST
  * double[epochs][4] {data, tv, total, wall_s}; image, sos: device fp32

@@ -465,6 +465,19 @@ class Trainer:
     def launch_count(self) -> int:
         return int(_abi.lib().pact_trainer_launch_count(self._h))
 
+    def stream(self) -> torch.cuda.ExternalStream:
+        """The engine's private CUDA stream (for event timing)."""
+        return torch.cuda.ExternalStream(int(_abi.lib().pact_trainer_stream(self._h)))
+
+    STAGES = ("siren_fwd", "wavefront", "fused_loss", "ray_backward", "tv_report", "siren_bwd",
+              "adam")
+
+    def profile_step(self) -> dict:
+        """One iteration with CUDA events between stages -> {stage: ms}."""
+        ms = (C.c_float * 7)()
+        check(_abi.lib().pact_trainer_profile_step(self._h, ms))
+        return dict(zip(self.STAGES, [float(x) for x in ms]))
+
     def close(self):
         if self._h:
             _abi.lib().pact_trainer_destroy(self._h)

@@ -106,6 +106,46 @@ Status enqueue_step(pact_trainer* tr) {
   return {};
 }
 
+// One eager step with events between the stages of enqueue_step (same kernels,
+// same order): render, wavefront, loss, ray backward, TV + report, SIREN
+// backward, Adam.
+Status profile_step(pact_trainer* tr, float* ms) {
+  pact_ctx* ctx = &tr->eng;
+  cudaStream_t s = ctx->stream;
+  const size_t npx = static_cast<size_t>(tr->grid.width) * tr->grid.height;
+  cudaEvent_t ev[8];
+  for (auto& e : ev) PACT_CUDA_S(cudaEventCreate(&e));
+  PACT_CUDA_S(cudaEventRecord(ev[0], s));
+  PACT_TRY_S(siren_forward(ctx, tr->shape, tr->theta32, tr->sw, tr->dv));
+  PACT_TRY_S(launch_check_finite_f32(ctx, tr->dv, tr->sw.idx, tr->mp.n, kFlagSos, tr->flags));
+  PACT_CUDA_S(cudaEventRecord(ev[1], s));
+  PACT_TRY_S(launch_wavefront(ctx, tr->ray, tr->w));
+  PACT_CUDA_S(cudaEventRecord(ev[2], s));
+  PACT_TRY_S(launch_loss_grad(ctx, tr->ftab.tab, tr->Y, tr->w, tr->n_patches, tr->cfg.eps_deconv,
+                              tr->loss_scale, tr->cfg.implicit_xhat_grad != 0, tr->loss_patch,
+                              tr->dw));
+  PACT_CUDA_S(cudaEventRecord(ev[3], s));
+  PACT_CUDA_S(cudaMemsetAsync(tr->gv, 0, sizeof(double) * npx, s));
+  PACT_TRY_S(launch_ray_backward(ctx, tr->ray, tr->dw, tr->gv));
+  PACT_CUDA_S(cudaEventRecord(ev[4], s));
+  PACT_TRY_S(launch_tv(ctx, tr->dv, tr->inmask, tr->sw.idx, tr->mp.n, tr->grid.width,
+                       tr->grid.height, tr->cfg.lambda_tv, tr->gtv, tr->tv_partial, tr->n_tv));
+  PACT_TRY_S(launch_step_report(ctx, tr->loss_patch, tr->n_patches, tr->tv_partial, tr->n_tv,
+                                tr->cfg.lambda_tv, tr->report, tr->flags));
+  PACT_CUDA_S(cudaEventRecord(ev[5], s));
+  PACT_TRY_S(siren_backward(ctx, tr->shape, tr->theta32, tr->sw, tr->gv, tr->gtv, tr->grad));
+  PACT_TRY_S(launch_check_finite_f64(ctx, tr->grad, tr->n_params, kFlagGrad, tr->flags));
+  PACT_CUDA_S(cudaEventRecord(ev[6], s));
+  PACT_TRY_S(launch_adam(ctx, tr->n_params, tr->theta, tr->grad, tr->m, tr->v, tr->t,
+                         tr->cfg.learning_rate, tr->cfg.beta1, tr->cfg.beta2, tr->cfg.adam_eps,
+                         tr->flags, tr->theta32, true));
+  PACT_CUDA_S(cudaEventRecord(ev[7], s));
+  PACT_CUDA_S(cudaEventSynchronize(ev[7]));
+  for (int i = 0; i < 7; ++i) PACT_CUDA_S(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+  for (auto& e : ev) cudaEventDestroy(e);
+  return {};
+}
+
 Status capture_graph(pact_trainer* tr) {
   cudaStream_t s = tr->eng.stream;
   PACT_CUDA_S(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -476,6 +516,19 @@ int pact_trainer_destroy(pact_trainer* tr) {
 }
 
 int64_t pact_trainer_launch_count(pact_trainer* tr) { return tr ? tr->eng.launches.load() : -1; }
+
+void* pact_trainer_stream(pact_trainer* tr) { return tr ? (void*)tr->eng.stream : nullptr; }
+
+int pact_trainer_profile_step(pact_trainer* tr, float* stage_ms) {
+  if (!tr || !stage_ms) return validation("pact_trainer_profile_step: null argument").code;
+  if (tr->steps_done == 0) {  // configure kernels / capture the graph first
+    int rc = pact_trainer_step(tr, 1);
+    if (rc) return rc;
+  }
+  PACT_TRY(profile_step(tr, stage_ms));
+  ++tr->steps_done;
+  return PACT_OK;
+}
 
 int pact_joint_reconstruct(pact_ctx* ctx, const pact_ring* ring, const pact_signal_meta* meta,
                            const float* signals, const pact_grid* grid, const pact_mask* mask,
