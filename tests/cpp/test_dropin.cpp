@@ -1,0 +1,306 @@
+// The drop-in C++ API (paper_2409_10876_b200/include/pact/*.hpp, same names as
+// the reference's proj/include/pact) exercised the way the reference's own
+// Catch2 suites exercise it (proj/tests/test_*.cpp), on the GPU, with the CPU
+// oracle (oracle/pact_oracle.c) as the checker where a comparison is needed.
+// Built and run by tests/test_cpp_dropin.py.
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "pact/beamform.hpp"
+#include "pact/core.hpp"
+#include "pact/deconv.hpp"
+#include "pact/nfield.hpp"
+#include "pact/optimize.hpp"
+#include "pact_oracle.h"
+
+using namespace pact;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(cond)                                                              \
+  do {                                                                           \
+    ++g_checks;                                                                  \
+    if (!(cond)) {                                                               \
+      ++g_fail;                                                                  \
+      std::printf("  FAILED %s:%d: %s\n", __FILE__, __LINE__, #cond);            \
+    }                                                                            \
+  } while (0)
+
+template <typename E, typename F>
+static bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+static double rel_l2(const std::vector<double>& a, const std::vector<double>& b) {
+  double num = 0, den = 0;
+  for (size_t i = 0; i < a.size(); ++i) {
+    num += (a[i] - b[i]) * (a[i] - b[i]);
+    den += b[i] * b[i];
+  }
+  return std::sqrt(num / (den > 0 ? den : 1));
+}
+
+static const RingGeometry kRing{128, 50.0, 0.0};
+
+// One point source at `pos` simulated by the oracle (simulate_signals, phantom.hpp:282-362).
+static SignalSet point_signals(Vec2 pos) {
+  GridSpec g = GridSpec::centered(255, 255, 0.1);
+  std::vector<double> pr(255 * 255, 0.0), sos(255 * 255, 1500.0);
+  Vec2 q = g.pixel(pos);
+  pr[std::lround(q.y) * 255 + std::lround(q.x)] = 1.0;
+  SignalSet s;
+  s.geom = kRing;
+  s.n_samples = 1400;
+  s.dt = 25e-9;
+  s.t0 = 32e-6;
+  s.background_sos = 1500.0;
+  s.data.resize(128 * 1400);
+  orc_simulate_signals(255, 255, 0.1, g.origin.x, g.origin.y, pr.data(), sos.data(), 0, 0, 10.0,
+                       1500.0, 128, 50.0, 0.0, 100e-9, 25e-9, 32e-6, 1400, 0.05, 1,
+                       s.data.data());
+  for (double& v : s.data) v = static_cast<float>(v);
+  return s;
+}
+
+static std::pair<int, int> argmax_abs(const RasterGrid& img) {
+  int bx = 0, by = 0;
+  double best = -1;
+  for (int y = 0; y < img.height; ++y)
+    for (int x = 0; x < img.width; ++x)
+      if (std::abs(img.at(x, y)) > best) {
+        best = std::abs(img.at(x, y));
+        bx = x;
+        by = y;
+      }
+  return {bx, by};
+}
+
+static void test_beamform() {
+  // test_beamform.cpp:55-70
+  SignalSet s = point_signals({0.0, 0.0});
+  GridSpec grid = GridSpec::centered(65, 65, 0.1);
+  auto [bx, by] = argmax_abs(das(s, grid, 1500.0, 0.0));
+  CHECK(bx == 32 && by == 32);
+  RasterGrid ring = das(s, grid, 1500.0, 0.5);
+  auto [rx, ry] = argmax_abs(ring);
+  double r = ring.world(rx, ry).norm();
+  CHECK(r > 0.35 && r < 0.65);
+  // test_beamform.cpp:99-111: stack element == das at that delay (bitwise)
+  GridSpec small = GridSpec::centered(33, 33, 0.1);
+  std::vector<double> d = {-0.4, 0.0, 0.3};
+  DasStack st = das_stack(s, small, 1500.0, d);
+  CHECK(st.n_delays() == 3);
+  for (int j = 0; j < 3; ++j) CHECK(st.images[j].values == das(s, small, 1500.0, d[j]).values);
+  CHECK(throws<ValidationError>([&] { das_stack(s, small, 1500.0, {0.1, 0.1}); }));
+  CHECK(throws<ValidationError>([&] { das_stack(s, small, -1.0, {0.0}); }));
+  // parity with the oracle on random signals (north_star tolerance 1e-4)
+  std::mt19937_64 rng(9);
+  std::normal_distribution<double> nd;
+  for (double& v : s.data) v = static_cast<float>(nd(rng));
+  std::vector<double> want(3 * 33 * 33);
+  orc_das_stack(128, 50.0, 0.0, 1400, 25e-9, 32e-6, s.data.data(), 33, 33, 0.1, small.origin.x,
+                small.origin.y, 1500.0, 3, d.data(), 1, want.data());
+  st = das_stack(s, small, 1500.0, d);
+  std::vector<double> got;
+  for (auto& im : st.images) got.insert(got.end(), im.values.begin(), im.values.end());
+  CHECK(rel_l2(got, want) <= 1e-4);
+}
+
+static void test_nfield() {
+  // test_nfield.cpp:26-32
+  CHECK(init_siren(0).param_count() == 4417);
+  CHECK(init_siren(0, 16, 2).param_count() == 337);
+  CHECK(siren_param_count(2, 64, 2) == 4417);
+  SirenParams p = init_siren(2, 8, 2, 30.0, 60.0, 1500.0);
+  std::vector<double> want(p.theta.size());
+  orc_init_siren(2, 8, 2, 30.0, 60.0, 1500.0, want.data());
+  CHECK(p.theta == want);  // bit-identical initialisation
+  GridSpec grid = GridSpec::centered(64, 64, 0.1);
+  CircularMask mask{{0.0, 0.0}, 2.6};
+  SosField f = render_sos(p, grid, mask);
+  std::vector<double> ref(64 * 64);
+  orc_render_sos(8, 2, 30.0, 60.0, 1500.0, p.theta.data(), 64, 64, 0.1, grid.origin.x,
+                 grid.origin.y, 0, 0, 2.6, ref.data(), nullptr);
+  CHECK(rel_l2(f.raster.values, ref) <= 1e-6);
+  std::vector<double> g(f.masked_indices.size());
+  for (size_t i = 0; i < g.size(); ++i) g[i] = std::sin(0.01 * i);
+  std::vector<double> grad = backprop_sos(p, f, g), gref(p.theta.size());
+  orc_backprop_sos(8, 2, 30.0, 60.0, 1500.0, p.theta.data(), 64, 64, 0.1, grid.origin.x,
+                   grid.origin.y, 0, 0, 2.6, g.data(), gref.data());
+  CHECK(rel_l2(grad, gref) <= 1e-3);
+}
+
+static void test_aberration() {
+  // transfer function identities (test_aberration.cpp:165-191), fp32 margins
+  const int P = 32;
+  WavefrontProfile zero;
+  zero.n_angles = 64;
+  zero.w.assign(64, 0.0);
+  TransferStack t0 = transfer_stack(zero, {0.0}, P, 0.1);
+  double e = 0;
+  for (auto& h : t0.spectra[0]) e = std::max(e, std::abs(h - cplx(1.0)));
+  CHECK(e < 1e-6);
+  TransferStack t1 = transfer_stack(zero, {0.35}, P, 0.1);
+  e = 0;
+  for (int by = 0; by < P; ++by)
+    for (int bx = 0; bx < P; ++bx) {
+      double s = 2 * M_PI / (P * 0.1);
+      double k = std::hypot(s * (bx <= P / 2 ? bx : bx - P), s * (by <= P / 2 ? by : by - P));
+      e = std::max(e, std::abs(t1.spectra[0][by * P + bx] - cplx(std::cos(k * 0.35))));
+    }
+  CHECK(e < 1e-5);
+  WavefrontProfile flat = zero;
+  flat.w.assign(64, 0.21);
+  TransferStack t2 = transfer_stack(flat, {0.21}, P, 0.1);
+  e = 0;
+  for (auto& h : t2.spectra[0]) e = std::max(e, std::abs(h - cplx(1.0)));
+  CHECK(e < 1e-5);
+  // conjugate symmetry, |H| <= 1, DC = 1 (193-214)
+  std::mt19937_64 rng(3);
+  std::uniform_real_distribution<double> u(-0.5, 0.5);
+  WavefrontProfile p = zero;
+  for (double& w : p.w) w = u(rng);
+  TransferStack ts = transfer_stack(p, {-0.3, 0.0, 0.4}, P, 0.1);
+  for (const auto& h : ts.spectra) {
+    double asym = 0, mx = 0;
+    for (int by = 0; by < P; ++by)
+      for (int bx = 0; bx < P; ++bx) {
+        size_t i = by * P + bx, j = ((P - by) % P) * P + (P - bx) % P;
+        asym = std::max(asym, std::abs(h[i] - std::conj(h[j])));
+        mx = std::max(mx, std::abs(h[i]));
+      }
+    CHECK(asym < 1e-6);
+    CHECK(mx <= 1.0 + 1e-6);
+    CHECK(std::abs(h[0] - cplx(1.0)) < 1e-7);
+  }
+  // wavefront at the centre of a 5 mm disc is (1 - v0/v1) r (92-98)
+  GridSpec g = GridSpec::centered(509, 509, 0.05);
+  RasterGrid sos = RasterGrid::constant(g, 1500.0);
+  for (int y = 0; y < g.height; ++y)
+    for (int x = 0; x < g.width; ++x) {
+      int in = 0;
+      for (int sy = 0; sy < 8; ++sy)
+        for (int sx = 0; sx < 8; ++sx) {
+          Vec2 q = g.world(x - 0.5 + (sx + 0.5) / 8, y - 0.5 + (sy + 0.5) / 8);
+          in += q.norm() <= 5.0;
+        }
+      sos.at(x, y) = 1500.0 + 50.0 * in / 64.0;
+    }
+  RingGeometry ring{512, 50.0, 0.0};
+  WavefrontProfile w = wavefront_profile({0, 0}, ring, sos, 1500.0, {{0, 0}, 10.0}, 512, 0.05, false);
+  double want = (1.0 - 1500.0 / 1550.0) * 5.0;
+  double worst = 0;
+  for (double v : w.w) worst = std::max(worst, std::abs(v - want) / want);
+  CHECK(worst < 1e-3);
+  CHECK(throws<ValidationError>(
+      [&] { wavefront_profile({60.0, 0.0}, ring, sos, 1500.0, {{0, 0}, 10.0}, 64, 0.05, false); }));
+  CHECK(throws<ValidationError>(
+      [&] { wavefront_profile({1.0, 2.0}, ring, sos, 1500.0, {{0, 0}, 10.0}, 3, 0.05, false); }));
+}
+
+static void test_optimize() {
+  // Adam (test_optimize.cpp:27-66)
+  std::vector<double> params{1.0, -2.0, 0.5};
+  AdamState st;
+  adam_step(params, {0.0, 0.0, 0.0}, st, 1e-3, 0.9, 0.999, 1e-8);
+  CHECK(st.t == 1 && params == (std::vector<double>{1.0, -2.0, 0.5}));
+  params = {0.0, 0.0};
+  st = AdamState{};
+  adam_step(params, {3.7, -0.002}, st, 1e-3, 0.9, 0.999, 1e-8);
+  CHECK(std::abs(params[0] + 1e-3) < 1e-7 && std::abs(params[1] - 1e-3) < 1e-5);
+  params = {0.0};
+  st = AdamState{};
+  double prev = 0, step = 0;
+  for (int t = 0; t < 200; ++t) {
+    adam_step(params, {0.42}, st, 1e-3, 0.9, 0.999, 1e-8);
+    step = prev - params[0];
+    prev = params[0];
+  }
+  CHECK(std::abs(step - 1e-3) < 1e-6);
+  st = AdamState{};
+  CHECK(throws<NumericalError>([&] { adam_step(params, {NAN}, st, 1e-3, 0.9, 0.999, 1e-8); }));
+  // TV: constant field is zero; a step edge gives lambda h L (97-104)
+  GridSpec g = GridSpec::centered(12, 12, 0.1);
+  SosField f;
+  f.mask = {{0, 0}, 10.0};
+  f.raster = RasterGrid::constant(g, 1500.0);
+  for (int i = 0; i < 144; ++i) {
+    f.masked_indices.push_back(i);
+    f.coords.push_back({0, 0});
+  }
+  TvLossResult tv = tv_loss(f, 2.0);
+  CHECK(tv.value == 0.0);
+  for (int y = 0; y < 12; ++y)
+    for (int x = 0; x < 12; ++x) f.raster.at(x, y) = g.world(x, y).x > 0 ? 7.5 : 0.0;
+  tv = tv_loss(f, 0.3);
+  CHECK(std::abs(tv.value - 0.3 * 7.5 * 12) < 1e-5);
+}
+
+static void test_joint_reconstruct() {
+  // a small joint reconstruction against the oracle's (optimize.hpp:367-494)
+  SignalSet s = point_signals({0.3, -0.2});
+  GridSpec grid = GridSpec::centered(64, 64, 0.1);
+  CircularMask mask{{0.0, 0.0}, 2.6};
+  TrainConfig cfg;
+  cfg.epochs = 2;
+  cfg.steps_per_epoch = 2;
+  cfg.delays = make_delays(-0.4, 0.4, 4);
+  cfg.n_angles = 32;
+  cfg.ray_step = 0.1;
+  cfg.patch_mm = 3.2;
+  cfg.overlap = 0.0;
+  cfg.hidden = 8;
+  cfg.out_scale = 60.0;
+  cfg.lambda_tv = 1e-4;
+  JointResult jr = joint_reconstruct(s, grid, mask, cfg);
+  OrcTrainCfg oc{cfg.epochs, cfg.steps_per_epoch, cfg.learning_rate, cfg.beta1, cfg.beta2,
+                 cfg.adam_eps, cfg.lambda_tv, static_cast<int>(cfg.delays.size()),
+                 cfg.delays.data(), cfg.eps_deconv, cfg.n_angles, cfg.ray_step, cfg.seed,
+                 cfg.hidden, cfg.sine_layers, cfg.omega0, cfg.out_scale, cfg.patch_mm,
+                 cfg.overlap, cfg.merge_fwhm, 1, 1};
+  std::vector<double> reps(4 * cfg.epochs), img(64 * 64), sos(64 * 64), th(jr.params.theta.size());
+  orc_joint_reconstruct(128, 50.0, 0.0, s.n_samples, s.dt, s.t0, 1500.0, s.data.data(), 64, 64,
+                        0.1, grid.origin.x, grid.origin.y, 0, 0, 2.6, &oc, reps.data(),
+                        img.data(), sos.data(), th.data());
+  CHECK(jr.reports.size() == 2u);
+  for (int e = 0; e < cfg.epochs; ++e) {
+    CHECK(std::abs(jr.reports[e].data_term - reps[4 * e]) <= 1e-3 * std::abs(reps[4 * e]));
+    CHECK(std::abs(jr.reports[e].total - (jr.reports[e].data_term + jr.reports[e].tv_term)) <=
+          1e-9 * std::abs(jr.reports[e].total));
+  }
+  CHECK(rel_l2(jr.image.values, img) <= 1e-3);
+  CHECK(rel_l2(jr.params.theta, th) <= 1e-3);
+}
+
+int main() {
+  struct Case {
+    const char* name;
+    std::function<void()> fn;
+  } cases[] = {{"beamform", test_beamform},
+               {"nfield", test_nfield},
+               {"aberration", test_aberration},
+               {"optimize", test_optimize},
+               {"joint_reconstruct", test_joint_reconstruct}};
+  for (auto& c : cases) {
+    int before = g_fail;
+    try {
+      c.fn();
+    } catch (const std::exception& e) {
+      ++g_fail;
+      std::printf("  EXCEPTION %s\n", e.what());
+    }
+    std::printf("[%s] %s\n", g_fail == before ? "ok" : "FAIL", c.name);
+  }
+  std::printf("%d checks, %d failures\n", g_checks, g_fail);
+  return g_fail ? 1 : 0;
+}
