@@ -237,7 +237,7 @@ def run_ours(args):
     cfg = wl.train_config(w)
     ctx = Context(local)
     L = _abi.lib()
-    my_frames = [f for f in range(N_FRAMES) if f % world == rank]
+    my_frames = wl.shard_frames(N_FRAMES, rank, world)
     hbm, bf16, peak_src = peaks()
 
     # ---- inputs: simulated on the GPU from seeded phantoms (one-time) ----

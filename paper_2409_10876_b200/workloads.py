@@ -167,3 +167,9 @@ def simulate(ctx, w: Workload, seed: int = 0):
     (pact_simulate_signals); fp32 [N, T] device tensor."""
     p, sos = phantom_rasters(w, seed)
     return ctx.simulate_signals(w.grid, p, sos, simulation_mask(w), w.v0, w.ring, w.meta)
+
+
+def shard_frames(n_frames: int, rank: int, world: int) -> list[int]:
+    """cfg4 sharding: frame f runs on rank f % world (independent units, no
+    data-path collective)."""
+    return [f for f in range(n_frames) if f % world == rank]
