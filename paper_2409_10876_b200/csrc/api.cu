@@ -325,7 +325,13 @@ int pact_deconvolve_image(pact_ctx* ctx, const float* stack, int32_t K, const do
   ra.dv = sos_dev;
   ra.centers = dc;
   ra.n_rays = n * opt->n_angles;
-  PACT_TRY(launch_wavefront(ctx, ra, w));
+  make_raster_texture(sos_dev, lay->grid.width, lay->grid.height, &ra.tex);
+  Status wst = launch_wavefront(ctx, ra, w);
+  if (ra.tex) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaDestroyTextureObject(ra.tex);
+  }
+  PACT_TRY(wst);
   PACT_TRY(launch_wiener(ctx, c->ftab.tab, Y, w, n, opt->eps, X));
   PACT_TRY(launch_patch_ifft_real(ctx, P, n, X, patches));
   PACT_TRY(launch_merge(ctx, *lay, patches, dwin, image));

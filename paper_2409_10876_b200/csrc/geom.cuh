@@ -118,7 +118,15 @@ struct RayArgs {
   int n_angles;
   int n_rays;
   const double2* centers;  // [n_centers]
+  // Optional pitch-2D texture over dv (0: plain loads).  Interior stencils are
+  // then one tex2Dgather instead of four scattered loads.
+  cudaTextureObject_t tex;
 };
+
+// Creates a point-sampled, clamped pitch-2D texture over a row-major fp32
+// raster; returns false (and leaves *out = 0) when the row pitch does not meet
+// the device's texture pitch alignment.
+bool make_raster_texture(const float* dv, int W, int H, cudaTextureObject_t* out);
 
 // freq_index, fft.hpp:35
 PACT_HD int freq_index(int i, int n) { return i <= n / 2 ? i : i - n; }

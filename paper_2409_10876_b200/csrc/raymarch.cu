@@ -25,12 +25,84 @@ namespace pactgpu {
 
 namespace {
 
-__device__ __forceinline__ float sample_dev(const float* __restrict__ dv, const Stencil& s) {
-  return s.w00 * __ldg(dv + s.i00) + s.w01 * __ldg(dv + s.i01) + s.w10 * __ldg(dv + s.i10) +
-         s.w11 * __ldg(dv + s.i11);
+// The grid border (left/right columns, bottom/top rows) cached in shared
+// memory: every step beyond the grid samples only border pixels (the stencil
+// clamps, aberration.hpp:49-55), which is most steps when the mask is the ring.
+struct Border {
+  float* colL;  // x = 0      [H]
+  float* colR;  // x = W - 1  [H]
+  float* rowB;  // y = 0      [W]
+  float* rowT;  // y = H - 1  [W]
+};
+
+__device__ __forceinline__ Border load_border(const RayArgs& a, float* sm) {
+  const int W = a.W, H = a.H;
+  Border b{sm, sm + H, sm + 2 * H, sm + 2 * H + W};
+  for (int i = threadIdx.x; i < H; i += blockDim.x) {
+    b.colL[i] = __ldg(a.dv + static_cast<size_t>(i) * W);
+    b.colR[i] = __ldg(a.dv + static_cast<size_t>(i) * W + W - 1);
+  }
+  for (int i = threadIdx.x; i < W; i += blockDim.x) {
+    b.rowB[i] = __ldg(a.dv + i);
+    b.rowT[i] = __ldg(a.dv + static_cast<size_t>(H - 1) * W + i);
+  }
+  __syncthreads();
+  return b;
 }
 
+// One midpoint step: the clamped stencil of detail::bilinear_stencil and the
+// four raster values under it, fetched from the cheapest source.
+struct Step {
+  int ix, iy;
+  float w00, w01, w10, w11;
+  float d;      // interpolated deviation
+  bool corner;  // both coordinates clamped: the stencil is a single pixel from here on
+};
+
+template <bool TEX>
+__device__ __forceinline__ Step step_at(const RayArgs& a, const Border& bd, float fxr, float fyr) {
+  const int W = a.W, H = a.H;
+  const float Wm1 = static_cast<float>(W - 1), Hm1 = static_cast<float>(H - 1);
+  const bool xo = !(fxr >= 0.f && fxr <= Wm1), yo = !(fyr >= 0.f && fyr <= Hm1);
+  const float fx = fminf(fmaxf(fxr, 0.f), Wm1), fy = fminf(fmaxf(fyr, 0.f), Hm1);
+  Step s;
+  s.ix = min(static_cast<int>(fx), max(W - 2, 0));
+  s.iy = min(static_cast<int>(fy), max(H - 2, 0));
+  const float ax = fx - s.ix, ay = fy - s.iy;
+  s.w00 = (1.f - ax) * (1.f - ay);
+  s.w01 = ax * (1.f - ay);
+  s.w10 = (1.f - ax) * ay;
+  s.w11 = ax * ay;
+  s.corner = xo && yo;
+  if (xo || yo) {
+    // clamped: weights vanish off the border line (ax or ay is exactly 0 or 1)
+    if (xo && !yo) {
+      const float* col = fx == 0.f ? bd.colL : bd.colR;
+      s.d = (1.f - ay) * col[s.iy] + ay * col[min(s.iy + 1, H - 1)];
+    } else if (yo && !xo) {
+      const float* row = fy == 0.f ? bd.rowB : bd.rowT;
+      s.d = (1.f - ax) * row[s.ix] + ax * row[min(s.ix + 1, W - 1)];
+    } else {
+      const float* col = fx == 0.f ? bd.colL : bd.colR;
+      s.d = col[fy == 0.f ? 0 : H - 1];
+    }
+  } else if (TEX) {
+    // texel (i, j) centre at (i + 0.5, j + 0.5): the gather footprint of
+    // (ix + 1, iy + 1) is exactly {ix, ix+1} x {iy, iy+1}
+    float4 g = tex2Dgather<float4>(a.tex, s.ix + 1.f, s.iy + 1.f, 0);
+    s.d = s.w00 * g.w + s.w01 * g.z + s.w10 * g.x + s.w11 * g.y;
+  } else {
+    const int ix1 = min(s.ix + 1, W - 1), iy1 = min(s.iy + 1, H - 1);
+    s.d = s.w00 * __ldg(a.dv + s.iy * W + s.ix) + s.w01 * __ldg(a.dv + s.iy * W + ix1) +
+          s.w10 * __ldg(a.dv + iy1 * W + s.ix) + s.w11 * __ldg(a.dv + iy1 * W + ix1);
+  }
+  return s;
+}
+
+template <bool TEX>
 __global__ void __launch_bounds__(256) wavefront_kernel(RayArgs a, float* __restrict__ w) {
+  extern __shared__ float s_border[];
+  const Border bd = load_border(a, s_border);
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= a.n_rays) return;
   int patch = r / a.n_angles, ang = r - patch * a.n_angles;
@@ -41,13 +113,16 @@ __global__ void __launch_bounds__(256) wavefront_kernel(RayArgs a, float* __rest
   const double dfx = ray.ux * a.inv_pitch, dfy = ray.uy * a.inv_pitch;
   const float v0 = static_cast<float>(a.v0);
   float acc = 0.f;
-#pragma unroll 4
   for (int i = 0; i < ray.n; ++i) {
     double s = ray.t0 + (i + 0.5) * ray.dl;
-    Stencil st = stencil_at(static_cast<float>(fx0 + s * dfx), static_cast<float>(fy0 + s * dfy),
-                            a.W, a.H);
-    float d = sample_dev(a.dv, st);
-    acc += d / (v0 + d);  // (1 - v0/v), v = v0 + d
+    Step st = step_at<TEX>(a, bd, static_cast<float>(fx0 + s * dfx),
+                           static_cast<float>(fy0 + s * dfy));
+    float term = st.d / (v0 + st.d);  // (1 - v0/v), v = v0 + d
+    if (st.corner) {                  // the ray moves outward: every remaining step is identical
+      acc += static_cast<float>(ray.n - i) * term;
+      break;
+    }
+    acc += term;
   }
   w[r] = static_cast<float>(ray.dl) * acc;
 }
@@ -61,8 +136,11 @@ __device__ __forceinline__ void flush_cell(double* __restrict__ g, int W, int H,
   if (acc[3] != 0.0) atomicAdd(g + iy1 * W + ix1, acc[3]);
 }
 
+template <bool TEX>
 __global__ void __launch_bounds__(256) ray_backward_kernel(RayArgs a, const float* __restrict__ dw,
                                                            double* __restrict__ grad) {
+  extern __shared__ float s_border[];
+  const Border bd = load_border(a, s_border);
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= a.n_rays) return;
   const float gr = dw[r];
@@ -81,33 +159,59 @@ __global__ void __launch_bounds__(256) ray_backward_kernel(RayArgs a, const floa
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int i = 0; i < ray.n; ++i) {
     double s = ray.t0 + (i + 0.5) * ray.dl;
-    float fx = fminf(fmaxf(static_cast<float>(fx0 + s * dfx), 0.f), static_cast<float>(W - 1));
-    float fy = fminf(fmaxf(static_cast<float>(fy0 + s * dfy), 0.f), static_cast<float>(H - 1));
-    int ix = min(static_cast<int>(fx), max(W - 2, 0));
-    int iy = min(static_cast<int>(fy), max(H - 2, 0));
-    float ax = fx - ix, ay = fy - iy;
-    int ix1 = min(ix + 1, W - 1), iy1 = min(iy + 1, H - 1);
-    float w00 = (1.f - ax) * (1.f - ay), w01 = ax * (1.f - ay), w10 = (1.f - ax) * ay,
-          w11 = ax * ay;
-    float d = w00 * __ldg(a.dv + iy * W + ix) + w01 * __ldg(a.dv + iy * W + ix1) +
-              w10 * __ldg(a.dv + iy1 * W + ix) + w11 * __ldg(a.dv + iy1 * W + ix1);
-    float v = v0 + d;
+    Step st = step_at<TEX>(a, bd, static_cast<float>(fx0 + s * dfx),
+                           static_cast<float>(fy0 + s * dfy));
+    float v = v0 + st.d;
     float f = gscale / (v * v);
-    if (ix != cx || iy != cy) {
+    if (st.corner) f *= static_cast<float>(ray.n - i);  // all remaining steps, same pixel
+    if (st.ix != cx || st.iy != cy) {
       if (cx >= 0) flush_cell(grad, W, H, cx, cy, acc);
-      cx = ix;
-      cy = iy;
+      cx = st.ix;
+      cy = st.iy;
       acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
     }
-    acc[0] += f * w00;
-    acc[1] += f * w01;
-    acc[2] += f * w10;
-    acc[3] += f * w11;
+    acc[0] += f * st.w00;
+    acc[1] += f * st.w01;
+    acc[2] += f * st.w10;
+    acc[3] += f * st.w11;
+    if (st.corner) break;
   }
   flush_cell(grad, W, H, cx, cy, acc);
 }
 
 }  // namespace
+
+bool make_raster_texture(const float* dv, int W, int H, cudaTextureObject_t* out) {
+  *out = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  int align = 0;
+  if (cudaDeviceGetAttribute(&align, cudaDevAttrTexturePitchAlignment, dev) != cudaSuccess)
+    return false;
+  const size_t pitch = sizeof(float) * static_cast<size_t>(W);
+  if (W < 2 || H < 2 || align <= 0 || pitch % align != 0 ||
+      reinterpret_cast<uintptr_t>(dv) % align != 0)
+    return false;
+  cudaResourceDesc res{};
+  res.resType = cudaResourceTypePitch2D;
+  res.res.pitch2D.devPtr = const_cast<float*>(dv);
+  res.res.pitch2D.desc = cudaCreateChannelDesc<float>();
+  res.res.pitch2D.width = W;
+  res.res.pitch2D.height = H;
+  res.res.pitch2D.pitchInBytes = pitch;
+  cudaTextureDesc td{};
+  td.addressMode[0] = cudaAddressModeClamp;
+  td.addressMode[1] = cudaAddressModeClamp;
+  td.filterMode = cudaFilterModePoint;
+  td.readMode = cudaReadModeElementType;
+  td.normalizedCoords = 0;
+  if (cudaCreateTextureObject(out, &res, &td, nullptr) != cudaSuccess) {
+    cudaGetLastError();
+    *out = 0;
+    return false;
+  }
+  return true;
+}
 
 Status ray_args(const pact_ring& ring, const pact_grid& grid, double v0, const pact_mask& mask,
                 int n_angles, double step, RayArgs& a) {
@@ -139,17 +243,57 @@ Status validate_centers(const pact_ring& ring, int n, const double* centers) {
   return {};
 }
 
+static size_t border_smem(const RayArgs& a) { return sizeof(float) * 2 * (a.W + a.H); }
+
+template <typename K>
+static Status allow_smem(K kernel, size_t smem) {
+  if (smem > 48 * 1024)
+    PACT_CUDA_S(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+  return {};
+}
+
 Status launch_wavefront(pact_ctx* ctx, const RayArgs& a, float* w) {
   int blocks = div_up(a.n_rays, 256);
-  wavefront_kernel<<<blocks, 256, 0, ctx->stream>>>(a, w);
+  size_t smem = border_smem(a);
+  if (a.tex) {
+    PACT_TRY_S(allow_smem(wavefront_kernel<true>, smem));
+    wavefront_kernel<true><<<blocks, 256, smem, ctx->stream>>>(a, w);
+  } else {
+    PACT_TRY_S(allow_smem(wavefront_kernel<false>, smem));
+    wavefront_kernel<false><<<blocks, 256, smem, ctx->stream>>>(a, w);
+  }
   return after_launch(ctx, "wavefront_kernel");
 }
 
 Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, double* grad) {
   int blocks = div_up(a.n_rays, 256);
-  ray_backward_kernel<<<blocks, 256, 0, ctx->stream>>>(a, dw, grad);
+  size_t smem = border_smem(a);
+  if (a.tex) {
+    PACT_TRY_S(allow_smem(ray_backward_kernel<true>, smem));
+    ray_backward_kernel<true><<<blocks, 256, smem, ctx->stream>>>(a, dw, grad);
+  } else {
+    PACT_TRY_S(allow_smem(ray_backward_kernel<false>, smem));
+    ray_backward_kernel<false><<<blocks, 256, smem, ctx->stream>>>(a, dw, grad);
+  }
   return after_launch(ctx, "ray_backward_kernel");
 }
+
+// Standalone entry points: a texture over the caller's raster for the
+// duration of one (synchronised) launch.
+struct ScopedTexture {
+  cudaTextureObject_t t = 0;
+  pact_ctx* ctx;
+  ScopedTexture(pact_ctx* c, const float* dv, int W, int H) : ctx(c) {
+    make_raster_texture(dv, W, H, &t);
+  }
+  ~ScopedTexture() {
+    if (t) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaDestroyTextureObject(t);
+    }
+  }
+};
 
 }  // namespace pactgpu
 
@@ -172,6 +316,8 @@ extern "C" int pact_wavefront(pact_ctx* ctx, const pact_ring* ring, const pact_g
   a.dv = sos_dev;
   a.centers = static_cast<const double2*>(dc);
   a.n_rays = n_centers * n_angles;
+  ScopedTexture tex(ctx, sos_dev, grid->width, grid->height);
+  a.tex = tex.t;
   PACT_TRY(launch_wavefront(ctx, a, w));
   return PACT_OK;
 }
@@ -192,6 +338,8 @@ extern "C" int pact_ray_backward(pact_ctx* ctx, const pact_ring* ring, const pac
   a.dv = sos_dev;
   a.centers = static_cast<const double2*>(dc);
   a.n_rays = n_centers * n_angles;
+  ScopedTexture tex(ctx, sos_dev, grid->width, grid->height);
+  a.tex = tex.t;
   PACT_TRY(launch_ray_backward(ctx, a, dw, grad_v));
   return PACT_OK;
 }

@@ -363,6 +363,7 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
   tr->ray.dv = tr->dv;
   tr->ray.centers = tr->centers;
   tr->ray.n_rays = tr->n_patches * tr->A;
+  make_raster_texture(tr->dv, grid->width, grid->height, &tr->ray.tex);
   // DAS stack + spectra, once (optimize.hpp:380-392)
   TRY_ST(das_stack_device(e, *ring, *meta, signals, *grid, v0, tr->delays.data(), tr->K,
                           tr->stack));
@@ -505,6 +506,7 @@ int pact_trainer_destroy(pact_trainer* tr) {
   if (tr->eng.stream) cudaStreamSynchronize(tr->eng.stream);
   if (tr->user) tr->user->launches.fetch_add(tr->eng.launches.exchange(0));
   if (tr->graph) cudaGraphExecDestroy(tr->graph);
+  if (tr->ray.tex) cudaDestroyTextureObject(tr->ray.tex);
   siren_work_free(tr->sw);
   fourier_table_free(tr->ftab);
   for (auto& sc : tr->eng.scratch)
