@@ -68,6 +68,7 @@ enum ScratchSlot {
   kScratchGeneric2 = 4,
   kScratchGeneric3 = 5,
   kScratchTables = 6,
+  kScratchNyq = 7,
 };
 
 Status scratch_get(pact_ctx* ctx, int slot, size_t bytes, void** out);

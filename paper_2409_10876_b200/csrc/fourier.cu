@@ -209,47 +209,8 @@ struct BinLoss {
   float wk;    // |k| * scale
 };
 
-// Pass 1 + 2 for one bin whose symmetrised H is h_sym(...) (or its conjugate
-// when `conj_h` — the partner of a Nyquist bin).
-__device__ __forceinline__ BinLoss bin_loss(const FourierTab& t, const float2* __restrict__ Y,
-                                            int b, int hb, int hm, float2 e1b, float2 e2b,
-                                            float2 e1m, float2 e2m, bool conj_h, float eps_m,
-                                            float scale, double& value) {
-  BinLoss L;
-  L.wk = t.kmag[b] * scale;
-  float2 num = make_float2(0.f, 0.f);
-  float den = eps_m;
-  for (int j = 0; j < t.K; ++j) {
-    float2 h = h_sym(t, j, hb, hm, e1b, e2b, e1m, e2m);
-    if (conj_h) h.y = -h.y;
-    float2 y = Y[j * t.P2 + b];
-    float2 c = cmulc(h, y);
-    num.x += c.x;
-    num.y += c.y;
-    den += h.x * h.x + h.y * h.y;
-  }
-  L.den = den;
-  L.x = den > 0.f ? make_float2(num.x / den, num.y / den) : make_float2(0.f, 0.f);
-  float2 G = make_float2(0.f, 0.f);
-  float acc = 0.f;
-  for (int j = 0; j < t.K; ++j) {
-    float2 h = h_sym(t, j, hb, hm, e1b, e2b, e1m, e2m);
-    if (conj_h) h.y = -h.y;
-    float2 y = Y[j * t.P2 + b];
-    float2 hx = cmul(h, L.x);
-    float2 r = make_float2(y.x - hx.x, y.y - hx.y);
-    acc += r.x * r.x + r.y * r.y;
-    float2 c = cmulc(r, h);
-    G.x += c.x;
-    G.y += c.y;
-  }
-  value += static_cast<double>(L.wk) * acc;
-  L.G = G;
-  L.gx = G.x * L.x.x - G.y * L.x.y;
-  return L;
-}
-
-// dL/dH_j at bin b (explicit + implicit terms, optimize.hpp:290-311).
+// dL/dH_j at bin b before symmetrisation (explicit + implicit terms,
+// optimize.hpp:290-311).
 __device__ __forceinline__ float2 bin_grad(const BinLoss& L, float2 h, float2 y, bool implicit) {
   float2 hx = cmul(h, L.x);
   float2 r = make_float2(y.x - hx.x, y.y - hx.y);
@@ -264,9 +225,37 @@ __device__ __forceinline__ float2 bin_grad(const BinLoss& L, float2 h, float2 y,
   return g;
 }
 
-__global__ void __launch_bounds__(512) loss_grad_kernel(FourierTab t, const float2* __restrict__ Y_all,
+// dL/dH -> (G1, G2) through t1 = dp e1 / 2, t2 = conj(dp) e2 / 2 (optimize.hpp:314-317)
+__device__ __forceinline__ void pullback(float2 g, float2 dp, float2 e1, float2 e2, float k,
+                                         float& G1, float& G2) {
+  float2 t1 = cmul(dp, e1), t2 = cmul(conjf2(dp), e2);
+  G1 += 0.5f * k * (g.x * -t1.y + g.y * t1.x);
+  G2 += 0.5f * k * (g.x * t2.y - g.y * t2.x);
+}
+
+// Slot of a Nyquist bin (even P) in the per-patch exchange buffer: the
+// by == P/2 row (P slots), then the bx == P/2 column without that row (P - 1).
+__device__ __forceinline__ int nyq_slot(int b, int P) {
+  const int by = b / P, bx = b - by * P, half = P / 2;
+  if (by == half) return bx;
+  return P + (by < half ? by : by - 1);
+}
+
+__device__ __forceinline__ int nyq_bin(int s, int P) {
+  const int half = P / 2;
+  if (s < P) return half * P + s;
+  int by = s - P;
+  by = by < half ? by : by + 1;
+  return by * P + half;
+}
+
+// KT > 0: the bin's K spectra are held in registers (loads issued together);
+// KT == 0: runtime K, spectra re-read from L1/L2 in each pass.
+template <int KT>
+__global__ void __launch_bounds__(256, 2) loss_grad_kernel(FourierTab t, const float2* __restrict__ Y_all,
                                                         const float* __restrict__ w_all, float eps_m,
                                                         float scale, int implicit,
+                                                        float2* __restrict__ nyq_all,
                                                         double* __restrict__ loss_out,
                                                         float* __restrict__ dw_out) {
   extern __shared__ float smem[];
@@ -275,41 +264,106 @@ __global__ void __launch_bounds__(512) loss_grad_kernel(FourierTab t, const floa
   float* s_g2 = s_g1 + t.P2;       // [P2]
   __shared__ double s_red[32];
   const int patch = blockIdx.x;
+  const int K = t.K, P2 = t.P2;
   for (int a = threadIdx.x; a < t.A; a += blockDim.x) s_w[a] = w_all[patch * t.A + a];
   __syncthreads();
-  const float2* Y = Y_all + static_cast<size_t>(patch) * t.K * t.P2;
+  const float2* Y = Y_all + static_cast<size_t>(patch) * K * P2;
+  float2* nyq = nyq_all + static_cast<size_t>(patch) * (2 * t.P - 1) * K;
+  const bool impl = implicit != 0;
   double value = 0.0;
-  for (int b = threadIdx.x; b < t.P2; b += blockDim.x) {
+  constexpr int KR = KT > 0 ? KT : 1;
+  for (int b = threadIdx.x; b < P2; b += blockDim.x) {
     float G1 = 0.f, G2 = 0.f;
-    if (t.kmag[b] * scale != 0.f) {
+    const int m = t.mirror[b];
+    BinLoss L;
+    L.wk = t.kmag[b] * scale;
+    if (L.wk != 0.f) {
       float2 e1b, e2b, e1m = {}, e2m = {};
       bin_phases(t, s_w, b, e1b, e2b);
-      const int m = t.mirror[b];
       if (m >= 0) bin_phases(t, s_w, m, e1m, e2m);
-      BinLoss Lb = bin_loss(t, Y, b, b, m, e1b, e2b, e1m, e2m, false, eps_m, scale, value);
-      BinLoss Lm;
-      if (m >= 0) {
-        double dummy = 0.0;  // the partner's own thread adds its loss
-        Lm = bin_loss(t, Y, m, b, m, e1b, e2b, e1m, e2m, true, eps_m, scale, dummy);
+      float2 yr[KR];
+      if constexpr (KT > 0) {
+#pragma unroll
+        for (int j = 0; j < KT; ++j)
+          if (j < K) yr[j] = Y[j * P2 + b];
       }
-      const float k = t.kmag[b];
-      for (int j = 0; j < t.K; ++j) {
-        float2 h = h_sym(t, j, b, m, e1b, e2b, e1m, e2m);
-        float2 g = bin_grad(Lb, h, Y[j * t.P2 + b], implicit != 0);
-        if (m >= 0) {  // self-adjoint symmetrisation of dL/dH (optimize.hpp:306-308)
-          float2 gm = bin_grad(Lm, conjf2(h), Y[j * t.P2 + m], implicit != 0);
-          g = make_float2(0.5f * (g.x + gm.x), 0.5f * (g.y - gm.y));
+      auto for_j = [&](auto&& fn) {
+        if constexpr (KT > 0) {
+#pragma unroll
+          for (int j = 0; j < KT; ++j)
+            if (j < K) fn(j, yr[j]);
+        } else {
+          for (int j = 0; j < K; ++j) fn(j, Y[j * P2 + b]);
         }
-        // pullback through t1 = dp e1 / 2, t2 = conj(dp) e2 / 2 (optimize.hpp:314-317)
-        float2 dp = t.dp[j * t.P2 + b];
-        float2 t1 = cmul(dp, e1b), t2 = cmul(conjf2(dp), e2b);
-        G1 += 0.5f * k * (g.x * -t1.y + g.y * t1.x);
-        G2 += 0.5f * k * (g.x * t2.y - g.y * t2.x);
-      }
+      };
+      // pass 1: X-hat
+      float2 num = make_float2(0.f, 0.f);
+      float den = eps_m;
+      for_j([&](int j, float2 y) {
+        float2 h = h_sym(t, j, b, m, e1b, e2b, e1m, e2m);
+        float2 c = cmulc(h, y);
+        num.x += c.x;
+        num.y += c.y;
+        den += h.x * h.x + h.y * h.y;
+      });
+      L.den = den;
+      L.x = den > 0.f ? make_float2(num.x / den, num.y / den) : make_float2(0.f, 0.f);
+      // pass 2: residuals, loss, G
+      float2 G = make_float2(0.f, 0.f);
+      float acc = 0.f;
+      for_j([&](int j, float2 y) {
+        float2 h = h_sym(t, j, b, m, e1b, e2b, e1m, e2m);
+        float2 hx = cmul(h, L.x);
+        float2 r = make_float2(y.x - hx.x, y.y - hx.y);
+        acc += r.x * r.x + r.y * r.y;
+        float2 c = cmulc(r, h);
+        G.x += c.x;
+        G.y += c.y;
+      });
+      value += static_cast<double>(L.wk) * acc;
+      L.G = G;
+      L.gx = G.x * L.x.x - G.y * L.x.y;
+      // pass 3: dL/dH; ordinary bins pull back now, Nyquist bins wait for
+      // their partner's dL/dH (symmetrisation, optimize.hpp:306-308)
+      const float k = t.kmag[b];
+      for_j([&](int j, float2 y) {
+        float2 h = h_sym(t, j, b, m, e1b, e2b, e1m, e2m);
+        float2 g = bin_grad(L, h, y, impl);
+        if (m < 0)
+          pullback(g, t.dp[j * P2 + b], e1b, e2b, k, G1, G2);
+        else
+          nyq[nyq_slot(b, t.P) * K + j] = g;
+      });
+    } else if (m >= 0) {
+      for (int j = 0; j < K; ++j) nyq[nyq_slot(b, t.P) * K + j] = make_float2(0.f, 0.f);
     }
-    s_g1[b] = G1;
-    s_g2[b] = G2;
+    if (m < 0) {
+      s_g1[b] = G1;
+      s_g2[b] = G2;
+    }
   }
+  __syncthreads();
+  // Nyquist bins: g = (dL/dH_b + conj(dL/dH_m)) / 2, then the pullback
+  if (t.P % 2 == 0) {
+    for (int s = threadIdx.x; s < 2 * t.P - 1; s += blockDim.x) {
+      const int b = nyq_bin(s, t.P), m = t.mirror[b];
+      const int sm = nyq_slot(m, t.P);
+      float G1 = 0.f, G2 = 0.f;
+      const float k = t.kmag[b];
+      if (k * scale != 0.f) {
+        float2 e1b, e2b;
+        bin_phases(t, s_w, b, e1b, e2b);
+        for (int j = 0; j < K; ++j) {
+          float2 gb = nyq[s * K + j], gm = nyq[sm * K + j];
+          float2 g = make_float2(0.5f * (gb.x + gm.x), 0.5f * (gb.y - gm.y));
+          pullback(g, t.dp[j * P2 + b], e1b, e2b, k, G1, G2);
+        }
+      }
+      s_g1[b] = G1;
+      s_g2[b] = G2;
+    }
+  }
+  __syncthreads();
   // deterministic block reduction of the patch loss
   for (int o = 16; o > 0; o >>= 1) value += __shfl_xor_sync(0xffffffffu, value, o);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = value;
@@ -373,16 +427,25 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
                         int n_patches, double eps, double scale, bool implicit, double* loss,
                         float* dw) {
   size_t smem = sizeof(float) * (t.A + 2 * t.P2);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    PACT_CUDA_S(cudaFuncSetAttribute(loss_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-    configured = smem;
-  }
-  loss_grad_kernel<<<n_patches, 512, smem, ctx->stream>>>(
-      t, Y, w, static_cast<float>(eps * t.K), static_cast<float>(scale), implicit ? 1 : 0, loss,
-      dw);
-  return after_launch(ctx, "loss_grad_kernel");
+  void* nyq = nullptr;  // Nyquist dL/dH exchange, [patch][2P-1][K]
+  PACT_TRY_S(scratch_get(ctx, kScratchNyq,
+                         sizeof(float2) * static_cast<size_t>(n_patches) * (2 * t.P) * t.K, &nyq));
+  auto launch = [&](auto kernel) -> Status {
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+      PACT_CUDA_S(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+      configured = smem;
+    }
+    kernel<<<n_patches, 256, smem, ctx->stream>>>(t, Y, w, static_cast<float>(eps * t.K),
+                                                  static_cast<float>(scale), implicit ? 1 : 0,
+                                                  static_cast<float2*>(nyq), loss, dw);
+    return after_launch(ctx, "loss_grad_kernel");
+  };
+  if (t.K <= 8) return launch(loss_grad_kernel<8>);
+  if (t.K <= 16) return launch(loss_grad_kernel<16>);
+  if (t.K <= 32) return launch(loss_grad_kernel<32>);
+  return launch(loss_grad_kernel<0>);
 }
 
 Status launch_wiener(pact_ctx* ctx, const FourierTab& t, const float2* Y, const float* w,

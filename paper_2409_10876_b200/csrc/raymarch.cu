@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(256) ray_backward_kernel(RayArgs a, const floa
   const float gscale = static_cast<float>(static_cast<double>(gr) * ray.dl * a.v0);
   const int W = a.W, H = a.H;
   int cx = -1, cy = -1;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  // accumulators of the current cell's pixels (cx + i, cy + j): a{j}{i}
+  double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
   for (int i = 0; i < ray.n; ++i) {
     double s = ray.t0 + (i + 0.5) * ray.dl;
     Step st = step_at<TEX>(a, bd, static_cast<float>(fx0 + s * dfx),
@@ -165,18 +166,43 @@ __global__ void __launch_bounds__(256) ray_backward_kernel(RayArgs a, const floa
     float f = gscale / (v * v);
     if (st.corner) f *= static_cast<float>(ray.n - i);  // all remaining steps, same pixel
     if (st.ix != cx || st.iy != cy) {
-      if (cx >= 0) flush_cell(grad, W, H, cx, cy, acc);
+      if (cx >= 0) {
+        // Move to the new cell: pixels shared with it keep accumulating in
+        // registers, the others are flushed (halves the atomics of a
+        // horizontal/vertical move).
+        const int dx = st.ix - cx, dy = st.iy - cy;
+        double n00 = 0.0, n01 = 0.0, n10 = 0.0, n11 = 0.0;
+        const double old[4] = {a00, a01, a10, a11};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int ox = (q & 1) - dx, oy = (q >> 1) - dy;  // old pixel in the new cell
+          const double val = old[q];
+          if (ox >= 0 && ox <= 1 && oy >= 0 && oy <= 1) {
+            const int t = oy * 2 + ox;
+            n00 += t == 0 ? val : 0.0;
+            n01 += t == 1 ? val : 0.0;
+            n10 += t == 2 ? val : 0.0;
+            n11 += t == 3 ? val : 0.0;
+          } else if (val != 0.0) {
+            atomicAdd(grad + (cy + (q >> 1)) * W + cx + (q & 1), val);
+          }
+        }
+        a00 = n00;
+        a01 = n01;
+        a10 = n10;
+        a11 = n11;
+      }
       cx = st.ix;
       cy = st.iy;
-      acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
     }
-    acc[0] += f * st.w00;
-    acc[1] += f * st.w01;
-    acc[2] += f * st.w10;
-    acc[3] += f * st.w11;
+    a00 += f * st.w00;
+    a01 += f * st.w01;
+    a10 += f * st.w10;
+    a11 += f * st.w11;
     if (st.corner) break;
   }
-  flush_cell(grad, W, H, cx, cy, acc);
+  const double fin[4] = {a00, a01, a10, a11};
+  flush_cell(grad, W, H, cx, cy, fin);
 }
 
 }  // namespace
