@@ -249,19 +249,19 @@ __device__ __forceinline__ int nyq_bin(int s, int P) {
   return by * P + half;
 }
 
-// KT > 0: the bin's K spectra are held in registers (loads issued together);
-// KT == 0: runtime K, spectra re-read from L1/L2 in each pass.
+// Kernel A of the fused loss: one thread per (patch, bin), grid (patch, bin
+// chunk).  Ordinary bins write their pulled-back (G1, G2); Nyquist bins write
+// their unsymmetrised dL/dH_j to the exchange buffer.  KT > 0: the bin's K
+// spectra are held in registers (loads issued together); KT == 0: runtime K.
 template <int KT>
-__global__ void __launch_bounds__(256, 2) loss_grad_kernel(FourierTab t, const float2* __restrict__ Y_all,
+__global__ void __launch_bounds__(256, 2) loss_bins_kernel(FourierTab t, const float2* __restrict__ Y_all,
                                                         const float* __restrict__ w_all, float eps_m,
                                                         float scale, int implicit,
                                                         float2* __restrict__ nyq_all,
-                                                        double* __restrict__ loss_out,
-                                                        float* __restrict__ dw_out) {
+                                                        float2* __restrict__ gbuf,
+                                                        double* __restrict__ loss_part) {
   extern __shared__ float smem[];
-  float* s_w = smem;               // [A]
-  float* s_g1 = smem + t.A;        // [P2]
-  float* s_g2 = s_g1 + t.P2;       // [P2]
+  float* s_w = smem;  // [A]
   __shared__ double s_red[32];
   const int patch = blockIdx.x;
   const int K = t.K, P2 = t.P2;
@@ -272,7 +272,8 @@ __global__ void __launch_bounds__(256, 2) loss_grad_kernel(FourierTab t, const f
   const bool impl = implicit != 0;
   double value = 0.0;
   constexpr int KR = KT > 0 ? KT : 1;
-  for (int b = threadIdx.x; b < P2; b += blockDim.x) {
+  const int b = blockIdx.y * blockDim.x + threadIdx.x;
+  if (b < P2) {
     float G1 = 0.f, G2 = 0.f;
     const int m = t.mirror[b];
     BinLoss L;
@@ -337,34 +338,9 @@ __global__ void __launch_bounds__(256, 2) loss_grad_kernel(FourierTab t, const f
     } else if (m >= 0) {
       for (int j = 0; j < K; ++j) nyq[nyq_slot(b, t.P) * K + j] = make_float2(0.f, 0.f);
     }
-    if (m < 0) {
-      s_g1[b] = G1;
-      s_g2[b] = G2;
-    }
+    if (m < 0) gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G1, G2);
   }
-  __syncthreads();
-  // Nyquist bins: g = (dL/dH_b + conj(dL/dH_m)) / 2, then the pullback
-  if (t.P % 2 == 0) {
-    for (int s = threadIdx.x; s < 2 * t.P - 1; s += blockDim.x) {
-      const int b = nyq_bin(s, t.P), m = t.mirror[b];
-      const int sm = nyq_slot(m, t.P);
-      float G1 = 0.f, G2 = 0.f;
-      const float k = t.kmag[b];
-      if (k * scale != 0.f) {
-        float2 e1b, e2b;
-        bin_phases(t, s_w, b, e1b, e2b);
-        for (int j = 0; j < K; ++j) {
-          float2 gb = nyq[s * K + j], gm = nyq[sm * K + j];
-          float2 g = make_float2(0.5f * (gb.x + gm.x), 0.5f * (gb.y - gm.y));
-          pullback(g, t.dp[j * P2 + b], e1b, e2b, k, G1, G2);
-        }
-      }
-      s_g1[b] = G1;
-      s_g2[b] = G2;
-    }
-  }
-  __syncthreads();
-  // deterministic block reduction of the patch loss
+  // deterministic block reduction of this chunk's loss
   for (int o = 16; o > 0; o >>= 1) value += __shfl_xor_sync(0xffffffffu, value, o);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = value;
   __syncthreads();
@@ -372,16 +348,58 @@ __global__ void __launch_bounds__(256, 2) loss_grad_kernel(FourierTab t, const f
     int nw = blockDim.x >> 5;
     double v = threadIdx.x < nw ? s_red[threadIdx.x] : 0.0;
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) loss_out[patch] = v;
+    if (threadIdx.x == 0) loss_part[patch * gridDim.y + blockIdx.y] = v;
   }
-  // dL/dw gather per angle
+}
+
+// Kernel B: per patch, the Nyquist bins' symmetrised pullback
+// g = (dL/dH_b + conj(dL/dH_m)) / 2, the per-angle gather of dL/dw through the
+// static CSR table, and the fixed-order sum of the chunk losses.
+__global__ void __launch_bounds__(256) loss_finish_kernel(FourierTab t, const float* __restrict__ w_all,
+                                                          float scale,
+                                                          const float2* __restrict__ nyq_all,
+                                                          float2* __restrict__ gbuf,
+                                                          const double* __restrict__ loss_part,
+                                                          int n_chunks, double* __restrict__ loss_out,
+                                                          float* __restrict__ dw_out) {
+  extern __shared__ float s_w[];  // [A]
+  const int patch = blockIdx.x;
+  const int K = t.K, P2 = t.P2;
+  for (int a = threadIdx.x; a < t.A; a += blockDim.x) s_w[a] = w_all[patch * t.A + a];
+  __syncthreads();
+  float2* g = gbuf + static_cast<size_t>(patch) * P2;
+  if (t.P % 2 == 0) {
+    const float2* nyq = nyq_all + static_cast<size_t>(patch) * (2 * t.P - 1) * K;
+    for (int s = threadIdx.x; s < 2 * t.P - 1; s += blockDim.x) {
+      const int b = nyq_bin(s, t.P), sm = nyq_slot(t.mirror[b], t.P);
+      float G1 = 0.f, G2 = 0.f;
+      const float k = t.kmag[b];
+      if (k * scale != 0.f) {
+        float2 e1b, e2b;
+        bin_phases(t, s_w, b, e1b, e2b);
+        for (int j = 0; j < K; ++j) {
+          float2 gb = nyq[s * K + j], gm = nyq[sm * K + j];
+          float2 gs = make_float2(0.5f * (gb.x + gm.x), 0.5f * (gb.y - gm.y));
+          pullback(gs, t.dp[j * P2 + b], e1b, e2b, k, G1, G2);
+        }
+      }
+      g[b] = make_float2(G1, G2);
+    }
+  }
+  __syncthreads();
   for (int a = threadIdx.x; a < t.A; a += blockDim.x) {
     float acc = 0.f;
     for (int e = t.csr_start[a]; e < t.csr_start[a + 1]; ++e) {
       int key = t.csr_key[e];
-      acc += t.csr_wt[e] * ((key & 1) ? s_g2[key >> 1] : s_g1[key >> 1]);
+      float2 v = g[key >> 1];
+      acc += t.csr_wt[e] * ((key & 1) ? v.y : v.x);
     }
     dw_out[patch * t.A + a] = acc;
+  }
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int c = 0; c < n_chunks; ++c) v += loss_part[patch * n_chunks + c];
+    loss_out[patch] = v;
   }
 }
 
@@ -426,26 +444,32 @@ Status launch_transfer_stack(pact_ctx* ctx, const FourierTab& t, const float* w,
 Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, const float* w,
                         int n_patches, double eps, double scale, bool implicit, double* loss,
                         float* dw) {
-  size_t smem = sizeof(float) * (t.A + 2 * t.P2);
-  void* nyq = nullptr;  // Nyquist dL/dH exchange, [patch][2P-1][K]
+  const size_t smem = sizeof(float) * t.A;
+  const int chunks = div_up(t.P2, 256);
+  // scratch: Nyquist dL/dH exchange [patch][2P-1][K] | (G1, G2) [patch][P2] | chunk losses
+  const size_t n_nyq = static_cast<size_t>(n_patches) * (2 * t.P) * t.K;
+  const size_t n_g = static_cast<size_t>(n_patches) * t.P2;
+  void* base = nullptr;
   PACT_TRY_S(scratch_get(ctx, kScratchNyq,
-                         sizeof(float2) * static_cast<size_t>(n_patches) * (2 * t.P) * t.K, &nyq));
-  auto launch = [&](auto kernel) -> Status {
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-      PACT_CUDA_S(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
-      configured = smem;
-    }
-    kernel<<<n_patches, 256, smem, ctx->stream>>>(t, Y, w, static_cast<float>(eps * t.K),
-                                                  static_cast<float>(scale), implicit ? 1 : 0,
-                                                  static_cast<float2*>(nyq), loss, dw);
-    return after_launch(ctx, "loss_grad_kernel");
-  };
-  if (t.K <= 8) return launch(loss_grad_kernel<8>);
-  if (t.K <= 16) return launch(loss_grad_kernel<16>);
-  if (t.K <= 32) return launch(loss_grad_kernel<32>);
-  return launch(loss_grad_kernel<0>);
+                         sizeof(float2) * (n_nyq + n_g) + sizeof(double) * n_patches * chunks + 256,
+                         &base));
+  float2* nyq = static_cast<float2*>(base);
+  float2* gbuf = nyq + n_nyq;
+  double* part = reinterpret_cast<double*>(gbuf + n_g);
+  const float eps_m = static_cast<float>(eps * t.K), sc = static_cast<float>(scale);
+  dim3 grid(n_patches, chunks);
+  if (t.K <= 8)
+    loss_bins_kernel<8><<<grid, 256, smem, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, nyq, gbuf, part);
+  else if (t.K <= 16)
+    loss_bins_kernel<16><<<grid, 256, smem, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, nyq, gbuf, part);
+  else if (t.K <= 32)
+    loss_bins_kernel<32><<<grid, 256, smem, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, nyq, gbuf, part);
+  else
+    loss_bins_kernel<0><<<grid, 256, smem, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, nyq, gbuf, part);
+  PACT_TRY_S(after_launch(ctx, "loss_bins_kernel"));
+  loss_finish_kernel<<<n_patches, 256, smem, ctx->stream>>>(t, w, sc, nyq, gbuf, part, chunks, loss,
+                                                             dw);
+  return after_launch(ctx, "loss_finish_kernel");
 }
 
 Status launch_wiener(pact_ctx* ctx, const FourierTab& t, const float2* Y, const float* w,

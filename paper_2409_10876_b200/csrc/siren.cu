@@ -38,8 +38,18 @@ namespace {
 
 constexpr int BM = 128, BK = 16, NT = 256;
 
-__device__ __forceinline__ float sinw(float a, float w0) { return sinf(w0 * a); }
-__device__ __forceinline__ float dsinw(float a, float w0) { return w0 * cosf(w0 * a); }
+// x mod 2pi into [-pi, pi] (two-constant Cody-Waite), so the MUFU sine/cosine
+// run on their accurate range (abs. error ~4e-7, below the fp32 rounding of
+// the argument w0 * a itself).
+__device__ __forceinline__ float red2pi(float x) {
+  const float k = rintf(x * 0.159154943091895336f);
+  return fmaf(-k, -1.74845553146951720e-07f, fmaf(-k, 6.28318548202514648f, x));
+}
+__device__ __forceinline__ float sinw(float a, float w0) { return __sinf(red2pi(w0 * a)); }
+__device__ __forceinline__ float dsinw(float a, float w0) { return w0 * __cosf(red2pi(w0 * a)); }
+__device__ __forceinline__ void sincosw(float a, float w0, float* s, float* c) {
+  __sincosf(red2pi(w0 * a), s, c);
+}
 
 // ---- tiled GEMM core: acc[8 rows][TN cols] += As[kk][rows] * Bs[kk][cols] ----
 template <int BN>
@@ -77,64 +87,69 @@ __device__ __forceinline__ void mma_tile(const float* __restrict__ As, const flo
   }
 }
 
-// Load R rows x 16 cols of row-major X (leading dim ld) starting at
-// (r0, c0) into smem transposed: S[kk][r].  Rows >= rmax are zero.  TR: sine.
+// Operand tiles are fetched into registers one k-step ahead (load), then
+// transformed and written to the other shared-memory buffer (store) after the
+// current step's FMAs: one barrier per k-step, global latency hidden behind math.
+//
+// TileT: R rows x 16 cols of row-major X (leading dim ld) at (r0, c0), stored
+// transposed S[kk][r].  Rows >= rmax are zero.  SIN: store sin(w0 x).
 template <int R, bool SIN>
-__device__ __forceinline__ void load_T(float* __restrict__ S, const float* __restrict__ X, int ld,
-                                       int r0, int c0, int rmax, float w0) {
-  // R*16 elements, 8 consecutive per thread (R = 128) or 4 (R = 64)
-  constexpr int PER = R * BK / NT;
-  const int t = threadIdx.x;
-  const int r = t / (BK / PER);
-  const int kk0 = (t % (BK / PER)) * PER;
+struct TileT {
+  static constexpr int PER = R * BK / NT;  // 8 (R = 128) or 4 (R = 64)
   float v[PER];
-  if (r0 + r < rmax) {
-    const float* src = X + static_cast<size_t>(r0 + r) * ld + c0 + kk0;
+  __device__ __forceinline__ void load(const float* __restrict__ X, int ld, int r0, int c0,
+                                       int rmax) {
+    const int t = threadIdx.x, r = t / (BK / PER), kk0 = (t % (BK / PER)) * PER;
+    if (r0 + r < rmax) {
+      const float* src = X + static_cast<size_t>(r0 + r) * ld + c0 + kk0;
 #pragma unroll
-    for (int q = 0; q < PER; q += 4) {
-      float4 x = *reinterpret_cast<const float4*>(src + q);
-      v[q] = x.x; v[q + 1] = x.y; v[q + 2] = x.z; v[q + 3] = x.w;
+      for (int q = 0; q < PER; q += 4) {
+        float4 x = *reinterpret_cast<const float4*>(src + q);
+        v[q] = x.x; v[q + 1] = x.y; v[q + 2] = x.z; v[q + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < PER; ++q) v[q] = 0.f;
     }
-    if (SIN) {
-#pragma unroll
-      for (int q = 0; q < PER; ++q) v[q] = sinw(v[q], w0);
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < PER; ++q) v[q] = 0.f;
   }
+  __device__ __forceinline__ void store(float* __restrict__ S, float w0) const {
+    const int t = threadIdx.x, r = t / (BK / PER), kk0 = (t % (BK / PER)) * PER;
 #pragma unroll
-  for (int q = 0; q < PER; ++q) S[(kk0 + q) * R + r] = v[q];
-}
+    for (int q = 0; q < PER; ++q) S[(kk0 + q) * R + r] = SIN ? sinw(v[q], w0) : v[q];
+  }
+};
 
-// Load 16 rows x C cols of row-major X at (r0, c0) directly: S[kk][c].
+// TileD: 16 rows x C cols of row-major X at (r0, c0), stored directly S[kk][c].
 template <int C, bool SIN>
-__device__ __forceinline__ void load_D(float* __restrict__ S, const float* __restrict__ X, int ld,
-                                       int r0, int c0, int rmax, float w0) {
-  constexpr int PER = C * BK / NT;  // 8 or 4
-  const int t = threadIdx.x;
-  const int kk = t / (C / PER);
-  const int cc = (t % (C / PER)) * PER;
+struct TileD {
+  static constexpr int PER = C * BK / NT;  // 8 or 4
   float v[PER];
-  if (r0 + kk < rmax) {
-    const float* src = X + static_cast<size_t>(r0 + kk) * ld + c0 + cc;
+  __device__ __forceinline__ void load(const float* __restrict__ X, int ld, int r0, int c0,
+                                       int rmax) {
+    const int t = threadIdx.x, kk = t / (C / PER), cc = (t % (C / PER)) * PER;
+    if (r0 + kk < rmax) {
+      const float* src = X + static_cast<size_t>(r0 + kk) * ld + c0 + cc;
+#pragma unroll
+      for (int q = 0; q < PER; q += 4) {
+        float4 x = *reinterpret_cast<const float4*>(src + q);
+        v[q] = x.x; v[q + 1] = x.y; v[q + 2] = x.z; v[q + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < PER; ++q) v[q] = 0.f;
+    }
+  }
+  __device__ __forceinline__ void store(float* __restrict__ S, float w0) const {
+    const int t = threadIdx.x, kk = t / (C / PER), cc = (t % (C / PER)) * PER;
 #pragma unroll
     for (int q = 0; q < PER; q += 4) {
-      float4 x = *reinterpret_cast<const float4*>(src + q);
-      v[q] = x.x; v[q + 1] = x.y; v[q + 2] = x.z; v[q + 3] = x.w;
+      float4 o = SIN ? make_float4(sinw(v[q], w0), sinw(v[q + 1], w0), sinw(v[q + 2], w0),
+                                   sinw(v[q + 3], w0))
+                     : make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+      *reinterpret_cast<float4*>(S + kk * C + cc + q) = o;
     }
-    if (SIN) {
-#pragma unroll
-      for (int q = 0; q < PER; ++q) v[q] = sinw(v[q], w0);
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < PER; ++q) v[q] = 0.f;
   }
-#pragma unroll
-  for (int q = 0; q < PER; q += 4)
-    *reinterpret_cast<float4*>(S + kk * C + cc + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
-}
+};
 
 // a_0[m][n] = b_0[n] + W_0[n][0] c_x + W_0[n][1] c_y     (nfield.hpp:117-121, l = 0)
 __global__ void siren_first_kernel(const float2* __restrict__ coords, const float* __restrict__ W0,
@@ -153,16 +168,30 @@ __global__ void __launch_bounds__(NT, 2)
 siren_fwd_kernel(const float* __restrict__ Ain, const float* __restrict__ W,
                  const float* __restrict__ b, int n, int H, float w0, float* __restrict__ Aout) {
   constexpr int TN = TileShape<BN>::TN;
-  __shared__ __align__(16) float As[BK * BM];
-  __shared__ __align__(16) float Bs[BK * BN];
+  __shared__ __align__(16) float As[2][BK * BM];
+  __shared__ __align__(16) float Bs[2][BK * BN];
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
   float acc[8][TN] = {};
-  for (int k0 = 0; k0 < H; k0 += BK) {
-    load_T<BM, true>(As, Ain, H, m0, k0, n, w0);
-    load_T<BN, false>(Bs, W, H, n0, k0, H, w0);  // Bs[kk][n] = W[n0+n][k0+kk]
-    __syncthreads();
-    mma_tile<BN>(As, Bs, acc, ty, tx);
+  TileT<BM, true> ta;    // As[kk][m] = sin(w0 a_{l-1}[m0+m][k0+kk])
+  TileT<BN, false> tb;   // Bs[kk][n] = W[n0+n][k0+kk]
+  ta.load(Ain, H, m0, 0, n);
+  tb.load(W, H, n0, 0, H);
+  ta.store(As[0], w0);
+  tb.store(Bs[0], w0);
+  __syncthreads();
+  const int nk = H / BK;
+  for (int kt = 0; kt < nk; ++kt) {
+    const int cur = kt & 1;
+    if (kt + 1 < nk) {
+      ta.load(Ain, H, m0, (kt + 1) * BK, n);
+      tb.load(W, H, n0, (kt + 1) * BK, H);
+    }
+    mma_tile<BN>(As[cur], Bs[cur], acc, ty, tx);
+    if (kt + 1 < nk) {
+      ta.store(As[cur ^ 1], w0);
+      tb.store(Bs[cur ^ 1], w0);
+    }
     __syncthreads();
   }
 #pragma unroll
@@ -218,7 +247,7 @@ __global__ void siren_top_kernel(const float* __restrict__ A, const float* __res
     g *= out_scale;
     float a = A[static_cast<size_t>(m) * H + k];
     float s, c;
-    sincosf(w0 * a, &s, &c);
+    sincosw(a, w0, &s, &c);
     dA[static_cast<size_t>(m) * H + k] = g * wk * w0 * c;
     gw = fmaf(g, s, gw);
     gb += g;
@@ -248,16 +277,30 @@ siren_dgrad_kernel(const float* __restrict__ dAl, const float* __restrict__ W,
                    const float* __restrict__ Aprev, int n, int H, float w0,
                    float* __restrict__ dAprev) {
   constexpr int TN = TileShape<BN>::TN;
-  __shared__ __align__(16) float As[BK * BM];
-  __shared__ __align__(16) float Bs[BK * BN];
+  __shared__ __align__(16) float As[2][BK * BM];
+  __shared__ __align__(16) float Bs[2][BK * BN];
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
   float acc[8][TN] = {};
-  for (int r0 = 0; r0 < H; r0 += BK) {
-    load_T<BM, false>(As, dAl, H, m0, r0, n, w0);   // As[rr][m] = dA_l[m][r0+rr]
-    load_D<BN, false>(Bs, W, H, r0, n0, H, w0);     // Bs[rr][k] = W[r0+rr][n0+k]
-    __syncthreads();
-    mma_tile<BN>(As, Bs, acc, ty, tx);
+  TileT<BM, false> ta;  // As[rr][m] = dA_l[m0+m][r0+rr]
+  TileD<BN, false> tb;  // Bs[rr][k] = W[r0+rr][n0+k]
+  ta.load(dAl, H, m0, 0, n);
+  tb.load(W, H, 0, n0, H);
+  ta.store(As[0], w0);
+  tb.store(Bs[0], w0);
+  __syncthreads();
+  const int nk = H / BK;
+  for (int kt = 0; kt < nk; ++kt) {
+    const int cur = kt & 1;
+    if (kt + 1 < nk) {
+      ta.load(dAl, H, m0, (kt + 1) * BK, n);
+      tb.load(W, H, (kt + 1) * BK, n0, H);
+    }
+    mma_tile<BN>(As[cur], Bs[cur], acc, ty, tx);
+    if (kt + 1 < nk) {
+      ta.store(As[cur ^ 1], w0);
+      tb.store(Bs[cur ^ 1], w0);
+    }
     __syncthreads();
   }
 #pragma unroll
@@ -286,8 +329,8 @@ __global__ void __launch_bounds__(NT, 2)
 siren_wgrad_kernel(const float* __restrict__ dAl, const float* __restrict__ Aprev, int n, int H,
                    int rows, float w0, float* __restrict__ partial) {
   constexpr int T = BN / 16;  // outputs per thread along each axis (8 or 4)
-  __shared__ __align__(16) float As[BK * BN];
-  __shared__ __align__(16) float Bs[BK * BN];
+  __shared__ __align__(16) float As[2][BK * BN];
+  __shared__ __align__(16) float Bs[2][BK * BN];
   const int chunk = blockIdx.x;
   const int r0 = blockIdx.y * BN, k0 = blockIdx.z * BN;
   const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
@@ -295,18 +338,32 @@ siren_wgrad_kernel(const float* __restrict__ dAl, const float* __restrict__ Apre
   float acc[T][T] = {};
   float bias[T] = {};
   const bool do_bias = (blockIdx.z == 0 && tx == 0);
+  TileD<BN, false> ta;  // As[mm][r] = dA[mb+mm][r0+r]
+  TileD<BN, true> tb;   // Bs[mm][k] = sin(w0 a_{l-1}[mb+mm][k0+k])
+  if (m_begin < m_end) {
+    ta.load(dAl, H, m_begin, r0, m_end);
+    tb.load(Aprev, H, m_begin, k0, m_end);
+    ta.store(As[0], w0);
+    tb.store(Bs[0], w0);
+  }
+  __syncthreads();
+  int cur = 0;
   for (int mb = m_begin; mb < m_end; mb += BK) {
-    load_D<BN, false>(As, dAl, H, mb, r0, m_end, w0);   // As[mm][r] = dA[mb+mm][r0+r]
-    load_D<BN, true>(Bs, Aprev, H, mb, k0, m_end, w0);  // Bs[mm][k] = sin(w0 a_{l-1}[mb+mm][k0+k])
-    __syncthreads();
+    const bool more = mb + BK < m_end;
+    if (more) {
+      ta.load(dAl, H, mb + BK, r0, m_end);
+      tb.load(Aprev, H, mb + BK, k0, m_end);
+    }
+    const float* A_ = As[cur];
+    const float* B_ = Bs[cur];
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
       float a[T], b[T];
 #pragma unroll
       for (int q = 0; q < T; q += 4) {
-        float4 x = *reinterpret_cast<const float4*>(As + kk * BN + ty * T + q);
+        float4 x = *reinterpret_cast<const float4*>(A_ + kk * BN + ty * T + q);
         a[q] = x.x; a[q + 1] = x.y; a[q + 2] = x.z; a[q + 3] = x.w;
-        float4 y = *reinterpret_cast<const float4*>(Bs + kk * BN + (q == 0 ? tx * 4 : 64 + tx * 4));
+        float4 y = *reinterpret_cast<const float4*>(B_ + kk * BN + (q == 0 ? tx * 4 : 64 + tx * 4));
         b[q] = y.x; b[q + 1] = y.y; b[q + 2] = y.z; b[q + 3] = y.w;
       }
 #pragma unroll
@@ -318,7 +375,12 @@ siren_wgrad_kernel(const float* __restrict__ dAl, const float* __restrict__ Apre
         for (int i = 0; i < T; ++i) bias[i] += a[i];
       }
     }
+    if (more) {
+      ta.store(As[cur ^ 1], w0);
+      tb.store(Bs[cur ^ 1], w0);
+    }
     __syncthreads();
+    cur ^= 1;
   }
   // partial layout per chunk: [H rows][H cols] weights then [H] bias
   float* out = partial + static_cast<size_t>(chunk) * (static_cast<size_t>(H) * H + H);
