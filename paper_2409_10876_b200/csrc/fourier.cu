@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(256, 2) loss_bins_kernel(FourierTab t, const f
           for (int j = 0; j < K; ++j) fn(j, Y[j * P2 + b]);
         }
       };
-      // pass 1: X-hat
+      // pass 1: X-hat = num / den
       float2 num = make_float2(0.f, 0.f);
       float den = eps_m;
       for_j([&](int j, float2 y) {
@@ -309,32 +309,27 @@ __global__ void __launch_bounds__(256, 2) loss_bins_kernel(FourierTab t, const f
       });
       L.den = den;
       L.x = den > 0.f ? make_float2(num.x / den, num.y / den) : make_float2(0.f, 0.f);
-      // pass 2: residuals, loss, G
-      float2 G = make_float2(0.f, 0.f);
+      // G = sum_j conj(r_j) h_j = conj(num) - conj(X) sum|h_j|^2 = conj(num) eps M / den
+      // (optimize.hpp:287-294; closed form, no cancellation)
+      L.G = den > 0.f ? make_float2(num.x * (eps_m / den), -num.y * (eps_m / den))
+                      : make_float2(0.f, 0.f);
+      L.gx = L.G.x * L.x.x - L.G.y * L.x.y;
+      // pass 2: residuals (the loss) and dL/dH; ordinary bins pull back now,
+      // Nyquist bins wait for their partner (symmetrisation, optimize.hpp:306-308)
+      const float k = t.kmag[b];
       float acc = 0.f;
       for_j([&](int j, float2 y) {
         float2 h = h_sym(t, j, b, m, e1b, e2b, e1m, e2m);
         float2 hx = cmul(h, L.x);
         float2 r = make_float2(y.x - hx.x, y.y - hx.y);
         acc += r.x * r.x + r.y * r.y;
-        float2 c = cmulc(r, h);
-        G.x += c.x;
-        G.y += c.y;
-      });
-      value += static_cast<double>(L.wk) * acc;
-      L.G = G;
-      L.gx = G.x * L.x.x - G.y * L.x.y;
-      // pass 3: dL/dH; ordinary bins pull back now, Nyquist bins wait for
-      // their partner's dL/dH (symmetrisation, optimize.hpp:306-308)
-      const float k = t.kmag[b];
-      for_j([&](int j, float2 y) {
-        float2 h = h_sym(t, j, b, m, e1b, e2b, e1m, e2m);
         float2 g = bin_grad(L, h, y, impl);
         if (m < 0)
           pullback(g, t.dp[j * P2 + b], e1b, e2b, k, G1, G2);
         else
           nyq[nyq_slot(b, t.P) * K + j] = g;
       });
+      value += static_cast<double>(L.wk) * acc;
     } else if (m >= 0) {
       for (int j = 0; j < K; ++j) nyq[nyq_slot(b, t.P) * K + j] = make_float2(0.f, 0.f);
     }

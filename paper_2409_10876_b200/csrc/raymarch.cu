@@ -99,6 +99,36 @@ __device__ __forceinline__ Step step_at(const RayArgs& a, const Border& bd, floa
   return s;
 }
 
+// Pixel coordinates of the midpoint steps, f_i = f_s + i * df (GridSpec::pixel,
+// core.hpp:75, of p_i = c + u (t0 + (i + 0.5) dl)): the start and increment
+// are formed in fp64 once per ray; per step one FFMA (error ~1e-5 px), and the
+// index from which both coordinates are off the grid (the corner regime).
+struct RayPix {
+  float fxs, fys, dfx, dfy;
+  int i_corner;  // first step index with both coordinates outside (>= n: never)
+};
+
+__device__ __forceinline__ RayPix ray_pixels(const RayArgs& a, double cx, double cy, const Ray& ray) {
+  const double fx0 = (cx - a.ox) * a.inv_pitch, fy0 = (cy - a.oy) * a.inv_pitch;
+  const double sx = ray.ux * a.inv_pitch, sy = ray.uy * a.inv_pitch;
+  const double s0 = ray.t0 + 0.5 * ray.dl;
+  const double fxs = fx0 + s0 * sx, fys = fy0 + s0 * sy;
+  const double dx = ray.dl * sx, dy = ray.dl * sy;
+  auto exit_index = [](double f, double d, double hi) -> double {
+    if (d > 0.0) return floor((hi - f) / d) + 1.0;
+    if (d < 0.0) return floor(-f / d) + 1.0;
+    return 1e30;
+  };
+  double ic = fmax(exit_index(fxs, dx, a.W - 1.0), exit_index(fys, dy, a.H - 1.0));
+  RayPix p;
+  p.fxs = static_cast<float>(fxs);
+  p.fys = static_cast<float>(fys);
+  p.dfx = static_cast<float>(dx);
+  p.dfy = static_cast<float>(dy);
+  p.i_corner = ic > 2e9 ? INT_MAX : static_cast<int>(fmax(ic, 0.0));
+  return p;
+}
+
 template <bool TEX>
 __global__ void __launch_bounds__(256) wavefront_kernel(RayArgs a, float* __restrict__ w) {
   extern __shared__ float s_border[];
@@ -108,17 +138,23 @@ __global__ void __launch_bounds__(256) wavefront_kernel(RayArgs a, float* __rest
   int patch = r / a.n_angles, ang = r - patch * a.n_angles;
   double2 c = a.centers[patch];
   Ray ray = make_ray(c.x, c.y, ang, a.n_angles, a.ring_r, a.mcx, a.mcy, a.mr, a.step);
-  // Pixel coordinates along the ray: f(s) = f0 + s * df  (GridSpec::pixel, core.hpp:75)
-  const double fx0 = (c.x - a.ox) * a.inv_pitch, fy0 = (c.y - a.oy) * a.inv_pitch;
-  const double dfx = ray.ux * a.inv_pitch, dfy = ray.uy * a.inv_pitch;
+  const RayPix rp = ray_pixels(a, c.x, c.y, ray);
   const float v0 = static_cast<float>(a.v0);
   float acc = 0.f;
-  for (int i = 0; i < ray.n; ++i) {
-    double s = ray.t0 + (i + 0.5) * ray.dl;
-    Step st = step_at<TEX>(a, bd, static_cast<float>(fx0 + s * dfx),
-                           static_cast<float>(fy0 + s * dfy));
-    float term = st.d / (v0 + st.d);  // (1 - v0/v), v = v0 + d
-    if (st.corner) {                  // the ray moves outward: every remaining step is identical
+  // steps that cannot be in the corner regime: no early exit, unrolled
+  const int i_main = max(0, min(ray.n, rp.i_corner - 2));
+  int i = 0;
+#pragma unroll 4
+  for (; i < i_main; ++i) {
+    Step st = step_at<TEX>(a, bd, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
+                           fmaf(static_cast<float>(i), rp.dfy, rp.fys));
+    acc += st.d / (v0 + st.d);  // (1 - v0/v), v = v0 + d
+  }
+  for (; i < ray.n; ++i) {
+    Step st = step_at<TEX>(a, bd, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
+                           fmaf(static_cast<float>(i), rp.dfy, rp.fys));
+    float term = st.d / (v0 + st.d);
+    if (st.corner) {  // the ray moves outward: every remaining step is identical
       acc += static_cast<float>(ray.n - i) * term;
       break;
     }
@@ -149,42 +185,42 @@ __global__ void __launch_bounds__(256) ray_backward_kernel(RayArgs a, const floa
   double2 c = a.centers[patch];
   Ray ray = make_ray(c.x, c.y, ang, a.n_angles, a.ring_r, a.mcx, a.mcy, a.mr, a.step);
   if (ray.n == 0) return;
-  const double fx0 = (c.x - a.ox) * a.inv_pitch, fy0 = (c.y - a.oy) * a.inv_pitch;
-  const double dfx = ray.ux * a.inv_pitch, dfy = ray.uy * a.inv_pitch;
+  const RayPix rp = ray_pixels(a, c.x, c.y, ray);
   const float v0 = static_cast<float>(a.v0);
   // f = g * dl * v0 / v^2 per step (aberration.hpp:354-355)
   const float gscale = static_cast<float>(static_cast<double>(gr) * ray.dl * a.v0);
-  const int W = a.W, H = a.H;
+  const int W = a.W;
   int cx = -1, cy = -1;
-  // accumulators of the current cell's pixels (cx + i, cy + j): a{j}{i}
-  double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
+  // accumulators of the current cell's pixels (cx + i, cy + j): a{j}{i}.  A
+  // pixel collects a handful of steps in fp32 before its fp64 flush.
+  float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
   for (int i = 0; i < ray.n; ++i) {
-    double s = ray.t0 + (i + 0.5) * ray.dl;
-    Step st = step_at<TEX>(a, bd, static_cast<float>(fx0 + s * dfx),
-                           static_cast<float>(fy0 + s * dfy));
+    Step st = step_at<TEX>(a, bd, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
+                           fmaf(static_cast<float>(i), rp.dfy, rp.fys));
     float v = v0 + st.d;
     float f = gscale / (v * v);
-    if (st.corner) f *= static_cast<float>(ray.n - i);  // all remaining steps, same pixel
+    const bool corner = st.corner && i >= rp.i_corner - 2;
+    if (corner) f *= static_cast<float>(ray.n - i);  // all remaining steps, same pixel
     if (st.ix != cx || st.iy != cy) {
       if (cx >= 0) {
         // Move to the new cell: pixels shared with it keep accumulating in
         // registers, the others are flushed (halves the atomics of a
         // horizontal/vertical move).
         const int dx = st.ix - cx, dy = st.iy - cy;
-        double n00 = 0.0, n01 = 0.0, n10 = 0.0, n11 = 0.0;
-        const double old[4] = {a00, a01, a10, a11};
+        float n00 = 0.f, n01 = 0.f, n10 = 0.f, n11 = 0.f;
+        const float old[4] = {a00, a01, a10, a11};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int ox = (q & 1) - dx, oy = (q >> 1) - dy;  // old pixel in the new cell
-          const double val = old[q];
+          const float val = old[q];
           if (ox >= 0 && ox <= 1 && oy >= 0 && oy <= 1) {
             const int t = oy * 2 + ox;
-            n00 += t == 0 ? val : 0.0;
-            n01 += t == 1 ? val : 0.0;
-            n10 += t == 2 ? val : 0.0;
-            n11 += t == 3 ? val : 0.0;
-          } else if (val != 0.0) {
-            atomicAdd(grad + (cy + (q >> 1)) * W + cx + (q & 1), val);
+            n00 += t == 0 ? val : 0.f;
+            n01 += t == 1 ? val : 0.f;
+            n10 += t == 2 ? val : 0.f;
+            n11 += t == 3 ? val : 0.f;
+          } else if (val != 0.f) {
+            atomicAdd(grad + (cy + (q >> 1)) * W + cx + (q & 1), static_cast<double>(val));
           }
         }
         a00 = n00;
@@ -195,14 +231,14 @@ __global__ void __launch_bounds__(256) ray_backward_kernel(RayArgs a, const floa
       cx = st.ix;
       cy = st.iy;
     }
-    a00 += f * st.w00;
-    a01 += f * st.w01;
-    a10 += f * st.w10;
-    a11 += f * st.w11;
-    if (st.corner) break;
+    a00 = fmaf(f, st.w00, a00);
+    a01 = fmaf(f, st.w01, a01);
+    a10 = fmaf(f, st.w10, a10);
+    a11 = fmaf(f, st.w11, a11);
+    if (corner) break;
   }
   const double fin[4] = {a00, a01, a10, a11};
-  flush_cell(grad, W, H, cx, cy, fin);
+  flush_cell(grad, W, a.H, cx, cy, fin);
 }
 
 }  // namespace
