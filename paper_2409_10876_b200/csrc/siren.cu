@@ -14,6 +14,7 @@
 // dense layers stay on the FP32 pipe here.  Hidden widths that are not a
 // multiple of 64 (unit-test networks) take a per-pixel path.
 #include <cmath>
+#include <cstdlib>
 #include <random>
 
 #include "siren.cuh"
@@ -523,6 +524,18 @@ __global__ void reduce_rows_kernel(const float* __restrict__ contrib, int n, int
   grad[p] = s;
 }
 
+}  // namespace
+
+bool siren_use_tc(int hidden) {
+  static const bool simt = [] {
+    const char* e = std::getenv("PACT_SIREN_SIMT");
+    return e && e[0] == '1';
+  }();
+  return !simt && siren_tc_supported(hidden);
+}
+
+namespace {
+
 bool tiled(const SirenShape& s) { return s.hidden % 64 == 0 && s.hidden <= 256 && s.in_dim == 2; }
 
 int chunk_rows(int n, int tiles, int num_sms) {
@@ -599,6 +612,10 @@ Status siren_forward(pact_ctx* ctx, const SirenShape& s, const float* theta, Sir
     const float* b = W + static_cast<size_t>(H) * H;
     const float* Ain = w.acts + (l - 1) * stride;
     float* Aout = w.acts + l * stride;
+    if (siren_use_tc(H)) {
+      PACT_TRY_S(tc_forward_layer(ctx, H, Ain, W, b, n, w0, Aout));
+      continue;
+    }
     if (H == 64) {
       siren_fwd_kernel<64><<<dim3(div_up(n, BM), 1), NT, 0, st>>>(Ain, W, b, n, H, w0, Aout);
     } else {
@@ -638,7 +655,9 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
   const int tilesW = (H / 128 > 0 ? H / 128 : 1) * (H / 128 > 0 ? H / 128 : 1);
   const int rows_top = chunk_rows(n, 1, ctx->num_sms);
   const int n_top = div_up(n, rows_top);
-  const int rows_w = chunk_rows(n, tilesW, ctx->num_sms);
+  const bool use_tc = siren_use_tc(H);
+  int rows_w = chunk_rows(n, tilesW, ctx->num_sms);
+  if (use_tc) rows_w = std::max(32, div_up(div_up(n, ctx->num_sms), 32) * 32);
   const int n_w = div_up(n, rows_w);
   size_t need = std::max(static_cast<size_t>(n_top) * (H + 1),
                          static_cast<size_t>(n_w) * (static_cast<size_t>(H) * H + H));
@@ -659,22 +678,26 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
     const float* W = theta + s.offset(l);
     const float* Aprev = w.acts + (l - 1) * stride;
     // weight gradient of layer l
-    if (H == 64)
+    if (use_tc)
+      PACT_TRY_S(tc_wgrad_layer(ctx, H, cur, Aprev, n, rows_w, w0, w.partial, n_w));
+    else if (H == 64)
       siren_wgrad_kernel<64><<<dim3(n_w, 1, 1), NT, 0, st>>>(cur, Aprev, n, H, rows_w, w0, w.partial);
     else
       siren_wgrad_kernel<128><<<dim3(n_w, H / 128, H / 128), NT, 0, st>>>(cur, Aprev, n, H, rows_w,
                                                                          w0, w.partial);
-    PACT_TRY_S(after_launch(ctx, "siren_wgrad_kernel"));
+    if (!use_tc) PACT_TRY_S(after_launch(ctx, "siren_wgrad_kernel"));
     int per = H * H + H;
     reduce_partials_kernel<<<div_up(per, 256), 256, 0, st>>>(w.partial, n_w, per, grad + s.offset(l));
     PACT_TRY_S(after_launch(ctx, "reduce_partials_kernel"));
     // delta to layer l-1
-    if (H == 64)
+    if (use_tc)
+      PACT_TRY_S(tc_dgrad_layer(ctx, H, cur, W, Aprev, n, w0, nxt));
+    else if (H == 64)
       siren_dgrad_kernel<64><<<dim3(div_up(n, BM), 1), NT, 0, st>>>(cur, W, Aprev, n, H, w0, nxt);
     else
       siren_dgrad_kernel<128><<<dim3(div_up(n, BM), H / 128), NT, 0, st>>>(cur, W, Aprev, n, H, w0,
                                                                           nxt);
-    PACT_TRY_S(after_launch(ctx, "siren_dgrad_kernel"));
+    if (!use_tc) PACT_TRY_S(after_launch(ctx, "siren_dgrad_kernel"));
     std::swap(cur, nxt);
   }
   siren_wgrad0_kernel<<<n_top, NT, 0, st>>>(cur, w.coords, n, H, rows_top, w.partial);
