@@ -657,7 +657,7 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
   const int n_top = div_up(n, rows_top);
   const bool use_tc = siren_use_tc(H);
   int rows_w = chunk_rows(n, tilesW, ctx->num_sms);
-  if (use_tc) rows_w = std::max(32, div_up(div_up(n, ctx->num_sms), 32) * 32);
+  if (use_tc) rows_w = tc_wgrad_rows(ctx, n);
   const int n_w = div_up(n, rows_w);
   size_t need = std::max(static_cast<size_t>(n_top) * (H + 1),
                          static_cast<size_t>(n_w) * (static_cast<size_t>(H) * H + H));

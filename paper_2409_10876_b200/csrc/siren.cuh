@@ -63,7 +63,7 @@ Status siren_forward(pact_ctx* ctx, const SirenShape& s, const float* theta, Sir
 Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, SirenWork& w,
                       const double* gv_raster, const float* g_masked, double* grad);
 
-// tcgen05 3xTF32 hidden layers (siren_tc.cu), hidden in {64, 128}.  The
+// tcgen05 3xTF32 hidden layers (siren_tc.cu), hidden == 128.  The
 // SIMT tiles remain for other widths and when PACT_SIREN_SIMT=1.
 bool siren_tc_supported(int hidden);
 bool siren_use_tc(int hidden);
@@ -71,6 +71,7 @@ Status tc_forward_layer(pact_ctx* ctx, int H, const float* Ain, const float* W, 
                         int n, float w0, float* Aout);
 Status tc_dgrad_layer(pact_ctx* ctx, int H, const float* dAl, const float* W, const float* Aprev,
                       int n, float w0, float* dAprev);
+int tc_wgrad_rows(pact_ctx* ctx, int n);  // pixels per weight-gradient partial
 Status tc_wgrad_layer(pact_ctx* ctx, int H, const float* dAl, const float* Aprev, int n, int rows,
                       float w0, float* partial, int n_chunks);
 

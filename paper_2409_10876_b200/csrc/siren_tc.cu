@@ -1,16 +1,25 @@
-// SIREN dense layers on the 5th-generation tensor cores (tcgen05, sm_100a),
-// 3xTF32 split precision (tc.cuh): the hidden-layer GEMMs of nfield.hpp
-// (forward a_l = W_l z + b, backward dA_{l-1} = (dA_l W_l) * w0 cos(w0 a_{l-1}),
-// weight gradient dA_l^T z_{l-1}) for hidden widths 64 and 128.
+// SIREN hidden layers on the 5th-generation tensor cores (tcgen05, sm_100a),
+// 3xTF32 split precision (tc.cuh), hidden width 128 (cfg3, cfg4):
+//   forward   a_l = W_l sin(w0 a_{l-1}) + b_l                  (nfield.hpp:164-180)
+//   backward  dA_{l-1} = (W_l^T dA_l) * w0 cos(w0 a_{l-1})     (nfield.hpp:190-230)
+//   weights   gW_l = sum_m dA_l[m] sin(w0 a_{l-1}[m])^T, gb_l = sum_m dA_l[m]
 //
-// Persistent CTAs (one per SM, 128 threads).  The layer weights are split into
-// TF32 hi/lo planes once per CTA and stay resident in shared memory; the
-// activation operand streams through two 32-wide K-chunk buffers.  The whole
-// CTA stages a chunk (global -> sine / split -> core-matrix layout), one
-// thread issues the 12 MMAs of the chunk (4 k-steps x {hi*hi, hi*lo, lo*hi})
-// into a TMEM accumulator, and the commit of chunk c frees its buffer for
-// chunk c + 2 while the tensor core runs.  Epilogues read TMEM row-per-thread
-// (tcgen05.ld 32x32b) and fuse bias / cosine.
+// Layer kernels (forward / dgrad): persistent, one CTA of 128 threads per SM.
+// The layer matrix is the MMA's A operand and lives in TMEM for the whole
+// kernel (hi and lo TF32 planes, lane = output feature); pixels are the MMA's
+// N.  Each 128-pixel tile of activations arrives by cp.async.bulk (one 512-B
+// row per copy, padded rows so the re-layout is bank-conflict free) one tile
+// ahead of use; the CTA re-lays a 32-wide K-chunk into K-major hi/lo planes
+// (fusing the sine), one thread issues the chunk's 12 MMAs, and the commit
+// frees the chunk buffer.  Two TMEM accumulators alternate so the epilogue of
+// tile i-1 (bias or cosine, coalesced stores: lane = feature) runs while the
+// tensor core works on tile i.
+//
+// Weight gradient: split over pixel ranges (one CTA per SM), accumulator
+// D[r][k] in TMEM with K = pixels.  dA^T enters TMEM directly from registers
+// (tcgen05.st, lane = r), sin(w0 a_{l-1})^T goes through shared-memory planes;
+// both raw tiles (64 pixels) arrive by bulk copies one tile ahead.  Partials
+// are reduced in a fixed order in fp64 by the caller (deterministic).
 #include <cstdint>
 
 #include "siren.cuh"
@@ -19,9 +28,9 @@
 namespace pactgpu {
 namespace {
 
-constexpr int TM = 128;   // pixel rows per tile (MMA M)
+constexpr int H = 128;    // hidden width handled here
+constexpr int TP = 128;   // pixels per layer tile (MMA N)
 constexpr int KC = 32;    // K per staged chunk
-constexpr int NTH = 128;  // threads per CTA
 
 __device__ __forceinline__ float red2pi_tc(float x) {
   const float k = rintf(x * 0.159154943091895336f);
@@ -40,7 +49,13 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-// Store 4 consecutive-K values (k % 4 == 0) of one row into the hi/lo planes.
+__device__ __forceinline__ void sync_tc() {
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+}
+
+// 4 consecutive-K values (k % 4 == 0) of one row into K-major hi/lo planes.
 __device__ __forceinline__ void put4(float* hi, float* lo, int row, int k, int R, float4 v) {
   float4 h, l;
   tc::split_tf32(v.x, h.x, l.x);
@@ -52,281 +67,334 @@ __device__ __forceinline__ void put4(float* hi, float* lo, int row, int k, int R
   *reinterpret_cast<float4*>(lo + o) = l;
 }
 
-// Resident weight planes: B[n][k] (N rows, K = H) from row-major W.
-//   TRANS = false: B[n][k] = W[n][k] (forward: a = z W^T)
-//   TRANS = true : B[n][k] = W[k][n] (backward: dA_{l-1} = dA_l W)
-template <int H, bool TRANS>
-__device__ void load_weights(const float* __restrict__ W, float* wh, float* wl) {
-  for (int e = threadIdx.x; e < H * H / 4; e += NTH) {
-    const int n = e / (H / 4), k = (e % (H / 4)) * 4;
-    float4 v;
-    if (!TRANS) {
-      v = *reinterpret_cast<const float4*>(W + n * H + k);
-    } else {
-      v = make_float4(W[k * H + n], W[(k + 1) * H + n], W[(k + 2) * H + n], W[(k + 3) * H + n]);
-    }
-    put4(wh, wl, n, k, H, v);
-  }
+__device__ __forceinline__ uint32_t lane_base(uint32_t t0, int warp) {
+  return t0 + (static_cast<uint32_t>(32 * warp) << 16);
 }
 
-// Issue the 12 MMAs of one K-chunk: A planes (TM x KC, chunk-local), B planes
-// resident (H x H) at K offset kc0.
-template <int H>
-__device__ __forceinline__ void issue_chunk(uint32_t taddr, const float* ah, const float* al,
-                                            const float* bh, const float* bl, int kc0,
-                                            bool first) {
-  constexpr uint32_t LBO_A = (TM / 8) * 128, LBO_B = (H / 8) * 128;
-  constexpr uint32_t idesc = tc::idesc_tf32(TM, H);
-  const uint32_t a_hi = saddr(ah), a_lo = saddr(al), b_hi = saddr(bh), b_lo = saddr(bl);
-#pragma unroll
-  for (int s = 0; s < KC / 8; ++s) {
-    const uint32_t qa = 2 * s * LBO_A, qb = (kc0 / 4 + 2 * s) * LBO_B;
-    const uint64_t dah = tc::smem_desc(a_hi + qa, LBO_A, 128);
-    const uint64_t dal = tc::smem_desc(a_lo + qa, LBO_A, 128);
-    const uint64_t dbh = tc::smem_desc(b_hi + qb, LBO_B, 128);
-    const uint64_t dbl = tc::smem_desc(b_lo + qb, LBO_B, 128);
-    tc::mma_tf32(taddr, dal, dbh, idesc, (first && s == 0) ? 0u : 1u);
-    tc::mma_tf32(taddr, dah, dbl, idesc, 1u);
-    tc::mma_tf32(taddr, dah, dbh, idesc, 1u);
-  }
-}
+// ---- layer kernels (forward, dgrad) ---------------------------------------
+enum Mode { kForward = 0, kDgrad = 1 };
 
-struct TcShared {
-  uint64_t bar_buf[2];
-  uint64_t bar_acc;
+struct LayerBars {
+  uint64_t raw[2];    // raw tile landed (bulk copies)
+  uint64_t buf[2];    // chunk planes free (MMA commit)
+  uint64_t full[2];   // accumulator ready (MMA commit)
+  uint64_t empty[2];  // accumulator drained (128 epilogue threads)
   uint32_t tslot;
 };
 
-// One persistent GEMM over pixel tiles:  ACC[m][n] = sum_k Aop(m, k) B[n][k]
-// with Aop(m, k) = SIN ? sin(w0 X[m][k]) : X[m][k], then the epilogue
-// EPI(row m, columns c0..c0+31, values).
-template <int H, bool SIN, bool TRANS_W, class Epi>
-__device__ void gemm_tiles(const float* __restrict__ X, const float* __restrict__ W, int n,
-                           float w0, Epi epi) {
-  extern __shared__ __align__(1024) unsigned char smem[];
-  float* wh = reinterpret_cast<float*>(smem);
-  float* wl = wh + H * H;
-  float* ah = wl + H * H;           // [2][TM * KC]
-  float* al = ah + 2 * TM * KC;     // [2][TM * KC]
-  __shared__ TcShared sh;
+// TMEM columns: A_hi [0,128), A_lo [128,256), D0 [256,384), D1 [384,512)
+constexpr uint32_t kColAlo = 128, kColD = 256;
+constexpr int LNTH = 512;  // warps 0-7 stage (thread 0 issues), warps 8-15 drain
+constexpr int LPROD = 256;  // producer threads
+constexpr int WNTH = 256;  // weight gradient: warps 0-3 dA^T, warps 4-7 sine planes
+
+template <int MODE>
+__global__ void __launch_bounds__(LNTH, 1)
+tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l-1} or dA_l)
+                const float* __restrict__ W,      // [H][H] layer matrix, row-major
+                const float* __restrict__ bias,   // forward: [H]
+                const float* __restrict__ Aprev,  // dgrad: a_{l-1} for the cosine
+                int n, float w0, float* __restrict__ Y) {
+  extern __shared__ unsigned char smem_dyn[];
+  // 1024-B alignment: the 128-B swizzle is a function of the address bits
+  float* raw = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) &
+                                        ~static_cast<uintptr_t>(1023));  // [2][TP][H]
+  float* zh = raw + 2 * TP * H;                                         // [2][TP][KC] SW128
+  float* zl = zh + 2 * TP * KC;                                         // [2][TP][KC] SW128
+  float* wst = raw + TP * H;  // prologue only: W staged [H][H + 1] over raw[1] and the planes
+  __shared__ LayerBars sb;
   const int tid = threadIdx.x, warp = tid >> 5;
-  if (warp == 0) tc::tmem_alloc<H>(&sh.tslot);
+  const int row = tid & 127;  // TMEM lane of this thread (warp % 4 quarter)
+  if (warp == 0) tc::tmem_alloc<512>(&sb.tslot);
   if (tid == 0) {
-    tc::mbar_init(&sh.bar_buf[0], 1);
-    tc::mbar_init(&sh.bar_buf[1], 1);
-    tc::mbar_init(&sh.bar_acc, 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&sb.raw[i], 1);
+      tc::mbar_init(&sb.buf[i], 1);
+      tc::mbar_init(&sb.full[i], 1);
+      tc::mbar_init(&sb.empty[i], LNTH - LPROD);
+    }
     fence_mbar_init();
   }
-  load_weights<H, TRANS_W>(W, wh, wl);
-  tc::fence_proxy_async();
-  tc::fence_before_sync();
+  sync_tc();
+  const uint32_t t0 = sb.tslot;
+  const int n_tiles = (n + TP - 1) / TP;
+  const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  // Bulk-load local tile i (rows m0.., contiguous) into raw[i & 1] (thread 0).
+  auto load_tile = [&](int i) {
+    const int m0 = (blockIdx.x + i * gridDim.x) * TP;
+    const uint32_t bytes = static_cast<uint32_t>(min(TP, n - m0)) * H * 4;
+    tc::mbar_expect_tx(&sb.raw[i & 1], bytes);
+    tc::bulk_load(raw + (i & 1) * TP * H, X + static_cast<size_t>(m0) * H, bytes, &sb.raw[i & 1]);
+  };
+  if (tid == 0 && my_tiles > 0) load_tile(0);
+
+  // Layer matrix -> TMEM A (lane = output row).  W is staged through shared
+  // memory with an odd row stride (coalesced loads, conflict-free reads);
+  // warp w writes lane quarter w % 4, plane (w / 8) and K half (w / 4) % 2.
+  // Forward A[r][k] = W[r][k]; dgrad A[k][r] = W[r][k].
+  for (int e = tid; e < H * H / 4; e += LNTH) {
+    const float4 w4 = reinterpret_cast<const float4*>(W)[e];
+    float* d = wst + (e / (H / 4)) * (H + 1) + (e % (H / 4)) * 4;
+    d[0] = w4.x;
+    d[1] = w4.y;
+    d[2] = w4.z;
+    d[3] = w4.w;
+  }
   __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t taddr = sh.tslot;
-  const int n_tiles = (n + TM - 1) / TM;
-  uint32_t g = 0;          // chunks staged so far (buffer = g & 1)
-  uint32_t acc_phase = 0;
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int m0 = tile * TM;
-    const int row = m0 + tid;  // this thread stages and drains row `row`
-    for (int kc0 = 0; kc0 < H; kc0 += KC, ++g) {
-      const int b = g & 1;
-      if (g >= 2) tc::mbar_wait(&sh.bar_buf[b], ((g - 2) >> 1) & 1);
-      float* bh_ = ah + b * TM * KC;
-      float* bl_ = al + b * TM * KC;
-#pragma unroll
-      for (int k = 0; k < KC; k += 4) {
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (row < n) {
-          v = *reinterpret_cast<const float4*>(X + static_cast<size_t>(row) * H + kc0 + k);
-          if (SIN) v = make_float4(sin_w(v.x, w0), sin_w(v.y, w0), sin_w(v.z, w0), sin_w(v.w, w0));
-        }
-        put4(bh_, bl_, tid, k, TM, v);
-      }
-      tc::fence_proxy_async();
-      __syncthreads();
-      if (tid == 0) {
-        tc::fence_after_sync();
-        issue_chunk<H>(taddr, bh_, bl_, wh, wl, kc0, kc0 == 0);
-        tc::mma_commit(&sh.bar_buf[b]);
-      }
-    }
-    if (tid == 0) tc::mma_commit(&sh.bar_acc);
-    tc::mbar_wait(&sh.bar_acc, acc_phase);
-    acc_phase ^= 1;
-    tc::fence_after_sync();
+  {
+    const bool lo_plane = warp >= 8;
+    const uint32_t lb = lane_base(t0, warp & 3) + (lo_plane ? kColAlo : 0);
 #pragma unroll 1
-    for (int c0 = 0; c0 < H; c0 += 32) {
+    for (int k0 = ((warp >> 2) & 1) * (H / 2); k0 < ((warp >> 2) & 1) * (H / 2) + H / 2; k0 += 32) {
       float v[32];
-      tc::tmem_ld32(taddr + (static_cast<uint32_t>(32 * warp) << 16) + c0, v);
-      if (row < n) epi(row, c0, v);
-    }
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-  }
-  __syncthreads();
-  if (warp == 0) tc::tmem_free<H>(taddr);
-}
-
-// a_l[m][:] = W_l sin(w0 a_{l-1}[m][:]) + b_l
-template <int H>
-__global__ void __launch_bounds__(NTH, 1)
-tc_fwd_kernel(const float* __restrict__ Ain, const float* __restrict__ W,
-              const float* __restrict__ bias, int n, float w0, float* __restrict__ Aout) {
-  gemm_tiles<H, true, false>(Ain, W, n, w0, [&](int m, int c0, const float (&v)[32]) {
-    float* o = Aout + static_cast<size_t>(m) * H + c0;
 #pragma unroll
-    for (int i = 0; i < 32; i += 4)
-      *reinterpret_cast<float4*>(o + i) = make_float4(v[i] + bias[c0 + i], v[i + 1] + bias[c0 + i + 1],
-                                                      v[i + 2] + bias[c0 + i + 2],
-                                                      v[i + 3] + bias[c0 + i + 3]);
-  });
-}
-
-// dA_{l-1}[m][k] = (sum_r dA_l[m][r] W_l[r][k]) w0 cos(w0 a_{l-1}[m][k])
-template <int H>
-__global__ void __launch_bounds__(NTH, 1)
-tc_dgrad_kernel(const float* __restrict__ dAl, const float* __restrict__ W,
-                const float* __restrict__ Aprev, int n, float w0, float* __restrict__ dAprev) {
-  gemm_tiles<H, false, true>(dAl, W, n, w0, [&](int m, int c0, const float (&v)[32]) {
-    const float* a = Aprev + static_cast<size_t>(m) * H + c0;
-    float* o = dAprev + static_cast<size_t>(m) * H + c0;
-#pragma unroll
-    for (int i = 0; i < 32; i += 4) {
-      float4 x = *reinterpret_cast<const float4*>(a + i);
-      *reinterpret_cast<float4*>(o + i) =
-          make_float4(v[i] * dsin_w(x.x, w0), v[i + 1] * dsin_w(x.y, w0),
-                      v[i + 2] * dsin_w(x.z, w0), v[i + 3] * dsin_w(x.w, w0));
-    }
-  });
-}
-
-// Split-M weight gradient: partial[chunk][r][k] = sum_{m in chunk} dA_l[m][r] sin(w0 a_{l-1}[m][k]),
-// partial bias[chunk][r] = sum_m dA_l[m][r].  The GEMM's M is r (= H rows of
-// TMEM), its N is k, its K is the pixel chunk.  Thread t owns r = t (H = 128)
-// or r = t % 64 with two pixel halves (H = 64).
-template <int H>
-__global__ void __launch_bounds__(NTH, 1)
-tc_wgrad_kernel(const float* __restrict__ dAl, const float* __restrict__ Aprev, int n, int rows,
-                float w0, float* __restrict__ partial) {
-  extern __shared__ __align__(1024) unsigned char smem[];
-  // A planes: [2][TM=H-padded-to-128 rows r][KC pixels];  B planes: [2][H rows k][KC pixels]
-  float* ah = reinterpret_cast<float*>(smem);
-  float* al = ah + 2 * TM * KC;
-  float* bh = al + 2 * TM * KC;
-  float* bl = bh + 2 * H * KC;
-  __shared__ TcShared sh;
-  __shared__ float s_bias[2][H];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (warp == 0) tc::tmem_alloc<H>(&sh.tslot);
-  if (tid == 0) {
-    tc::mbar_init(&sh.bar_buf[0], 1);
-    tc::mbar_init(&sh.bar_buf[1], 1);
-    tc::mbar_init(&sh.bar_acc, 1);
-    fence_mbar_init();
-  }
-  // zero the A planes once: rows r >= H (H = 64) stay zero
-  for (int e = tid; e < 4 * TM * KC; e += NTH) ah[e] = 0.f;
-  tc::fence_proxy_async();
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t taddr = sh.tslot;
-  constexpr uint32_t LBO_A = (TM / 8) * 128, LBO_B = (H / 8) * 128;
-  constexpr uint32_t idesc = tc::idesc_tf32(TM, H);
-  const int m_begin = blockIdx.x * rows, m_end = min(n, m_begin + rows);
-  // thread -> (r or k index, pixel sub-range) for staging
-  constexpr int GROUPS = NTH / H;      // 1 (H = 128) or 2 (H = 64)
-  const int idx = tid % H, grp = tid / H;
-  float bias_acc = 0.f;
-  uint32_t g = 0;
-  for (int p0 = m_begin; p0 < m_end; p0 += KC, ++g) {
-    const int b = g & 1;
-    if (g >= 2) tc::mbar_wait(&sh.bar_buf[b], ((g - 2) >> 1) & 1);
-    float* ah_ = ah + b * TM * KC;
-    float* al_ = al + b * TM * KC;
-    float* bh_ = bh + b * H * KC;
-    float* bl_ = bl + b * H * KC;
-    // pixels p0 + [grp * KC/GROUPS, (grp+1) * KC/GROUPS), four at a time
-#pragma unroll
-    for (int q = grp * (KC / GROUPS); q < (grp + 1) * (KC / GROUPS); q += 4) {
-      float4 da, z;
-      float* dav = &da.x;
-      float* zv = &z.x;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int m = p0 + q + u;
-        float x = 0.f, y = 0.f;
-        if (m < m_end) {
-          x = dAl[static_cast<size_t>(m) * H + idx];
-          y = sin_w(Aprev[static_cast<size_t>(m) * H + idx], w0);
-        }
-        dav[u] = x;
-        zv[u] = y;
-        bias_acc += x;
+      for (int i = 0; i < 32; ++i) {
+        const float w = MODE == kForward ? wst[row * (H + 1) + k0 + i] : wst[(k0 + i) * (H + 1) + row];
+        float hi, lo;
+        tc::split_tf32(w, hi, lo);
+        v[i] = lo_plane ? lo : hi;
       }
-      put4(ah_, al_, idx, q, TM, da);
-      put4(bh_, bl_, idx, q, H, z);
-    }
-    tc::fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      tc::fence_after_sync();
-      const uint32_t a_hi = saddr(ah_), a_lo = saddr(al_), b_hi = saddr(bh_), b_lo = saddr(bl_);
-#pragma unroll
-      for (int s = 0; s < KC / 8; ++s) {
-        const uint32_t qa = 2 * s * LBO_A, qb = 2 * s * LBO_B;
-        const uint64_t dah = tc::smem_desc(a_hi + qa, LBO_A, 128);
-        const uint64_t dal = tc::smem_desc(a_lo + qa, LBO_A, 128);
-        const uint64_t dbh = tc::smem_desc(b_hi + qb, LBO_B, 128);
-        const uint64_t dbl = tc::smem_desc(b_lo + qb, LBO_B, 128);
-        tc::mma_tf32(taddr, dal, dbh, idesc, (g == 0 && s == 0) ? 0u : 1u);
-        tc::mma_tf32(taddr, dah, dbl, idesc, 1u);
-        tc::mma_tf32(taddr, dah, dbh, idesc, 1u);
-      }
-      tc::mma_commit(&sh.bar_buf[b]);
+      tc::tmem_st32(lb + k0, v);
     }
   }
-  s_bias[grp][idx] = bias_acc;
-  float* out = partial + static_cast<size_t>(blockIdx.x) * (static_cast<size_t>(H) * H + H);
-  if (g > 0) {
-    if (tid == 0) tc::mma_commit(&sh.bar_acc);
-    tc::mbar_wait(&sh.bar_acc, 0);
-    tc::fence_after_sync();
-    // TMEM lane r holds row r of the (r x k) accumulator; rows >= H are padding
-    const int r = 32 * warp + lane;
+  sync_tc();
+
+  if (tid < LPROD) {
+    // ---- producers: re-layout K-chunks, issue MMAs ----
+    constexpr uint32_t idesc = tc::idesc_tf32(H, TP);
+    const int c4 = tid & 7, p0 = tid >> 3;  // 16-B chunk of the K-chunk row, first row
+    uint32_t g = 0;  // chunks staged so far (chunk buffer g & 1)
+    for (int i = 0; i < my_tiles; ++i) {
+      const int m0 = (blockIdx.x + i * gridDim.x) * TP;
+      const int rows = min(TP, n - m0);
+      if (tid == 0 && i + 1 < my_tiles) load_tile(i + 1);
+      tc::mbar_wait(&sb.raw[i & 1], (i >> 1) & 1);
+      const float* rt = raw + (i & 1) * TP * H;
+      const uint32_t dcol = t0 + kColD + (i & 1) * TP;
 #pragma unroll 1
-    for (int c0 = 0; c0 < H; c0 += 32) {
-      float v[32];
-      tc::tmem_ld32(taddr + (static_cast<uint32_t>(32 * warp) << 16) + c0, v);
-      if (r < H) {
+      for (int kc0 = 0; kc0 < H; kc0 += KC, ++g) {
+        const int b = g & 1;
+        if (g >= 2) tc::mbar_wait(&sb.buf[b], ((g - 2) >> 1) & 1);
+        float* bh = zh + b * TP * KC;
+        float* bl = zl + b * TP * KC;
+        // Rows >= `rows` of the raw tile hold stale bytes: load them anyway
+        // (keeps the eight loads independent) and select zero afterwards.
+        // Eight threads read one 128-B row segment and write one swizzled
+        // 128-B plane row: both conflict free.
+        constexpr int PJ = TP / (LPROD / 8);
+        float4 v[PJ];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) out[static_cast<size_t>(r) * H + c0 + i] = v[i];
+        for (int j = 0; j < PJ; ++j)
+          v[j] = *reinterpret_cast<const float4*>(rt + (p0 + (LPROD / 8) * j) * H + kc0 + 4 * c4);
+#pragma unroll
+        for (int j = 0; j < PJ; ++j) {
+          const int p = p0 + (LPROD / 8) * j;
+          float4 z = v[j];
+          if (MODE == kForward)
+            z = make_float4(sin_w(z.x, w0), sin_w(z.y, w0), sin_w(z.z, w0), sin_w(z.w, w0));
+          if (p >= rows) z = make_float4(0.f, 0.f, 0.f, 0.f);
+          float4 h, l;
+          tc::split_tf32(z.x, h.x, l.x);
+          tc::split_tf32(z.y, h.y, l.y);
+          tc::split_tf32(z.z, h.z, l.z);
+          tc::split_tf32(z.w, h.w, l.w);
+          const int o = p * KC + ((c4 ^ (p & 7)) << 2);
+          *reinterpret_cast<float4*>(bh + o) = h;
+          *reinterpret_cast<float4*>(bl + o) = l;
+        }
+        tc::fence_proxy_async();
+        tc::named_sync(1, LPROD);
+        if (tid == 0) {
+          if (kc0 == 0 && i >= 2) tc::mbar_wait(&sb.empty[i & 1], ((i - 2) >> 1) & 1);
+          tc::fence_after_sync();
+          const uint32_t sbh = saddr(bh), sbl = saddr(bl);
+#pragma unroll
+          for (int s = 0; s < KC / 8; ++s) {
+            const uint32_t ka = kc0 + 8 * s;
+            const uint64_t dh = tc::smem_desc_sw128(sbh + 32 * s);
+            const uint64_t dl = tc::smem_desc_sw128(sbl + 32 * s);
+            tc::mma_tf32_ts(dcol, t0 + kColAlo + ka, dh, idesc, (kc0 | s) != 0);
+            tc::mma_tf32_ts(dcol, t0 + ka, dl, idesc, 1u);
+            tc::mma_tf32_ts(dcol, t0 + ka, dh, idesc, 1u);
+          }
+          tc::mma_commit(&sb.buf[b]);
+          if (kc0 + KC == H) tc::mma_commit(&sb.full[i & 1]);
+        }
       }
     }
   } else {
-    for (int e = tid; e < H * H; e += NTH) out[e] = 0.f;
+    // ---- epilogue: lane = output feature, columns = pixels of the tile;
+    // warps 8-11 and 12-15 share the TMEM lane quarters and split the columns ----
+    const float brow = MODE == kForward ? bias[row] : 0.f;
+    const int cb = ((warp - LPROD / 32) >> 2) * (TP / 2);
+    for (int i = 0; i < my_tiles; ++i) {
+      const int m0 = (blockIdx.x + i * gridDim.x) * TP;
+      const int rows = min(TP, n - m0);
+      float av[TP / 2];
+      if (MODE == kDgrad) {
+        // a_{l-1} does not depend on the accumulator: fetch before waiting
+        const float* a = Aprev + static_cast<size_t>(m0) * H + row;
+#pragma unroll
+        for (int j = 0; j < TP / 2; ++j) av[j] = a[min(cb + j, rows - 1) * H];
+      }
+      tc::mbar_wait(&sb.full[i & 1], (i >> 1) & 1);
+      tc::fence_after_sync();
+      const uint32_t d = lane_base(t0, warp & 3) + kColD + (i & 1) * TP;
+      float* y = Y + static_cast<size_t>(m0) * H + row;
+#pragma unroll
+      for (int h = 0; h < TP / 2; h += 32) {
+        float v[32];
+        tc::tmem_ld32(d + cb + h, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int c = cb + h + j;
+          const float out = MODE == kForward ? v[j] + brow : v[j] * dsin_w(av[h + j], w0);
+          if (c < rows) y[c * H] = out;
+        }
+      }
+      tc::fence_before_sync();
+      tc::mbar_arrive(&sb.empty[i & 1]);
+    }
   }
-  __syncthreads();
-  if (tid < H) {
-    float t = 0.f;
-    for (int q = 0; q < GROUPS; ++q) t += s_bias[q][tid];
-    out[static_cast<size_t>(H) * H + tid] = t;
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  if (warp == 0) tc::tmem_free<H>(taddr);
+  sync_tc();
+  if (warp == 0) tc::tmem_free<512>(t0);
 }
 
-template <int H>
-size_t gemm_smem() {
-  return sizeof(float) * (2 * H * H + 4 * TM * KC);
+// ---- weight gradient --------------------------------------------------------
+constexpr int WP = 64;  // pixels per raw tile
+
+struct WgradBars {
+  uint64_t raw[2];
+  uint64_t buf[2];
+  uint64_t acc;
+  uint32_t tslot;
+};
+
+// TMEM: D [0,128); A chunk b: hi [128 + 64b, +32), lo [160 + 64b, +32).
+// Warps 0-3 put dA^T into TMEM (lane r), warps 4-7 build the sine planes.
+__global__ void __launch_bounds__(WNTH, 1)
+tc_wgrad_kernel(const float* __restrict__ dA, const float* __restrict__ Aprev, int n, int rows,
+                float w0, float* __restrict__ partial) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  float* rda = reinterpret_cast<float*>(smem);  // [2][WP][H]
+  float* rap = rda + 2 * WP * H;                // [2][WP][H]
+  float* zh = rap + 2 * WP * H;                 // [2][H * KC]
+  float* zl = zh + 2 * H * KC;                  // [2][H * KC]
+  __shared__ WgradBars sb;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int r = tid & 127;
+  if (warp == 0) tc::tmem_alloc<256>(&sb.tslot);
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&sb.raw[i], 1);
+      tc::mbar_init(&sb.buf[i], 1);
+    }
+    tc::mbar_init(&sb.acc, 1);
+    fence_mbar_init();
+  }
+  sync_tc();
+  const uint32_t t0 = sb.tslot;
+  const int m_begin = blockIdx.x * rows, m_end = min(n, m_begin + rows);
+  const int n_raw = m_end > m_begin ? (m_end - m_begin + WP - 1) / WP : 0;
+
+  auto load_tile = [&](int i) {
+    const int p0 = m_begin + i * WP;
+    const uint32_t bytes = static_cast<uint32_t>(min(WP, m_end - p0)) * H * 4;
+    uint64_t* bar = &sb.raw[i & 1];
+    tc::mbar_expect_tx(bar, 2 * bytes);
+    tc::bulk_load(rda + (i & 1) * WP * H, dA + static_cast<size_t>(p0) * H, bytes, bar);
+    tc::bulk_load(rap + (i & 1) * WP * H, Aprev + static_cast<size_t>(p0) * H, bytes, bar);
+  };
+  if (tid == 0 && n_raw > 0) load_tile(0);
+
+  constexpr uint32_t LBO = (H / 8) * 128;
+  constexpr uint32_t idesc = tc::idesc_tf32(H, H);
+  float bias_acc = 0.f;
+  uint32_t g = 0;
+  for (int i = 0; i < n_raw; ++i) {
+    const int p0 = m_begin + i * WP;
+    const int valid = min(WP, m_end - p0);
+    if (tid == 0 && i + 1 < n_raw) load_tile(i + 1);
+    tc::mbar_wait(&sb.raw[i & 1], (i >> 1) & 1);
+    const float* ta = rda + (i & 1) * WP * H;
+    const float* tz = rap + (i & 1) * WP * H;
+#pragma unroll 1
+    for (int q0 = 0; q0 < WP; q0 += KC, ++g) {
+      const int b = g & 1;
+      if (g >= 2) tc::mbar_wait(&sb.buf[b], ((g - 2) >> 1) & 1);
+      float* bh = zh + b * H * KC;
+      float* bl = zl + b * H * KC;
+      if (warp < 4) {
+        // dA^T chunk -> TMEM (lane r, column = pixel)
+        float hi[32], lo[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) hi[j] = ta[(q0 + j) * H + r];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float x = q0 + j < valid ? hi[j] : 0.f;
+          bias_acc += x;
+          tc::split_tf32(x, hi[j], lo[j]);
+        }
+        const uint32_t lb = lane_base(t0, warp) + 128 + 64 * b;
+        tc::tmem_st32(lb, hi);
+        tc::tmem_st32(lb + 32, lo);
+      } else {
+        // sin(w0 a_{l-1})^T chunk -> planes (row k = r, K = pixel)
+        float a[KC];
+#pragma unroll
+        for (int j = 0; j < KC; ++j) a[j] = tz[(q0 + j) * H + r];
+#pragma unroll
+        for (int j = 0; j < KC; ++j) a[j] = q0 + j < valid ? sin_w(a[j], w0) : 0.f;
+#pragma unroll
+        for (int j = 0; j < KC; j += 4)
+          put4(bh, bl, r, j, H, make_float4(a[j], a[j + 1], a[j + 2], a[j + 3]));
+        tc::fence_proxy_async();
+      }
+      sync_tc();
+      if (tid == 0) {
+        const uint32_t sbh = saddr(bh), sbl = saddr(bl);
+        const uint32_t ah = t0 + 128 + 64 * b, al = ah + 32;
+#pragma unroll
+        for (int s = 0; s < KC / 8; ++s) {
+          const uint64_t dh = tc::smem_desc(sbh + 2 * s * LBO, LBO, 128);
+          const uint64_t dl = tc::smem_desc(sbl + 2 * s * LBO, LBO, 128);
+          tc::mma_tf32_ts(t0, al + 8 * s, dh, idesc, (g | s) != 0);
+          tc::mma_tf32_ts(t0, ah + 8 * s, dl, idesc, 1u);
+          tc::mma_tf32_ts(t0, ah + 8 * s, dh, idesc, 1u);
+        }
+        tc::mma_commit(&sb.buf[b]);
+      }
+    }
+  }
+  float* out = partial + static_cast<size_t>(blockIdx.x) * (static_cast<size_t>(H) * H + H);
+  if (g > 0) {
+    if (tid == 0) tc::mma_commit(&sb.acc);
+    tc::mbar_wait(&sb.acc, 0);
+    tc::fence_after_sync();
+    // warps w and w + 4 share TMEM lanes; each drains half the columns
+    const uint32_t lb = lane_base(t0, warp & 3);
+    const int cbeg = warp < 4 ? 0 : H / 2;
+#pragma unroll 1
+    for (int c0 = cbeg; c0 < cbeg + H / 2; c0 += 32) {
+      float v[32];
+      tc::tmem_ld32(lb + c0, v);
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(out + static_cast<size_t>(r) * H + c0 + j) =
+            make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    }
+  } else {
+    for (int c = (warp < 4 ? 0 : H / 2); c < (warp < 4 ? H / 2 : H); ++c)
+      out[static_cast<size_t>(r) * H + c] = 0.f;
+  }
+  if (warp < 4) out[static_cast<size_t>(H) * H + r] = bias_acc;
+  sync_tc();
+  if (warp == 0) tc::tmem_free<256>(t0);
 }
-template <int H>
-size_t wgrad_smem() {
-  return sizeof(float) * (4 * TM * KC + 4 * H * KC);
-}
+
+constexpr size_t kLayerSmem = sizeof(float) * (2 * TP * H + 4 * TP * KC) + 1024;
+constexpr size_t kWgradSmem = sizeof(float) * (4 * WP * H + 4 * H * KC);
 
 template <class K>
 Status set_smem(K kernel, size_t bytes) {
@@ -335,62 +403,52 @@ Status set_smem(K kernel, size_t bytes) {
   return {};
 }
 
+int layer_grid(pact_ctx* ctx, int n) {
+  return std::max(1, std::min((n + TP - 1) / TP, ctx->num_sms));
+}
+
+Status unsupported_width() {
+  set_error("tcgen05 SIREN layers need hidden == %d", H);
+  return {PACT_E_UNSUPPORTED};
+}
+
 }  // namespace
 
-bool siren_tc_supported(int hidden) { return hidden == 64 || hidden == 128; }
+bool siren_tc_supported(int hidden) { return hidden == H; }
 
-Status tc_forward_layer(pact_ctx* ctx, int H, const float* Ain, const float* W, const float* b,
-                        int n, float w0, float* Aout) {
-  const int tiles = (n + TM - 1) / TM;
-  const int grid = std::max(1, std::min(tiles, ctx->num_sms));
-  if (H == 128) {
-    static bool cfg = false;
-    if (!cfg) PACT_TRY_S(set_smem(tc_fwd_kernel<128>, gemm_smem<128>()));
-    cfg = true;
-    tc_fwd_kernel<128><<<grid, NTH, gemm_smem<128>(), ctx->stream>>>(Ain, W, b, n, w0, Aout);
-  } else {
-    static bool cfg = false;
-    if (!cfg) PACT_TRY_S(set_smem(tc_fwd_kernel<64>, gemm_smem<64>()));
-    cfg = true;
-    tc_fwd_kernel<64><<<grid, NTH, gemm_smem<64>(), ctx->stream>>>(Ain, W, b, n, w0, Aout);
-  }
-  return after_launch(ctx, "tc_fwd_kernel");
+int tc_wgrad_rows(pact_ctx* ctx, int n) {
+  return std::max(WP, div_up(div_up(n, ctx->num_sms), WP) * WP);
 }
 
-Status tc_dgrad_layer(pact_ctx* ctx, int H, const float* dAl, const float* W, const float* Aprev,
-                      int n, float w0, float* dAprev) {
-  const int tiles = (n + TM - 1) / TM;
-  const int grid = std::max(1, std::min(tiles, ctx->num_sms));
-  if (H == 128) {
-    static bool cfg = false;
-    if (!cfg) PACT_TRY_S(set_smem(tc_dgrad_kernel<128>, gemm_smem<128>()));
-    cfg = true;
-    tc_dgrad_kernel<128><<<grid, NTH, gemm_smem<128>(), ctx->stream>>>(dAl, W, Aprev, n, w0, dAprev);
-  } else {
-    static bool cfg = false;
-    if (!cfg) PACT_TRY_S(set_smem(tc_dgrad_kernel<64>, gemm_smem<64>()));
-    cfg = true;
-    tc_dgrad_kernel<64><<<grid, NTH, gemm_smem<64>(), ctx->stream>>>(dAl, W, Aprev, n, w0, dAprev);
-  }
-  return after_launch(ctx, "tc_dgrad_kernel");
+Status tc_forward_layer(pact_ctx* ctx, int hidden, const float* Ain, const float* W,
+                        const float* b, int n, float w0, float* Aout) {
+  if (hidden != H) return unsupported_width();
+  static bool cfg = false;
+  if (!cfg) PACT_TRY_S(set_smem(tc_layer_kernel<kForward>, kLayerSmem));
+  cfg = true;
+  tc_layer_kernel<kForward><<<layer_grid(ctx, n), LNTH, kLayerSmem, ctx->stream>>>(
+      Ain, W, b, nullptr, n, w0, Aout);
+  return after_launch(ctx, "tc_layer_kernel<forward>");
 }
 
-// Returns the number of pixel chunks (partials) written.
-Status tc_wgrad_layer(pact_ctx* ctx, int H, const float* dAl, const float* Aprev, int n, int rows,
-                      float w0, float* partial, int n_chunks) {
-  if (H == 128) {
-    static bool cfg = false;
-    if (!cfg) PACT_TRY_S(set_smem(tc_wgrad_kernel<128>, wgrad_smem<128>()));
-    cfg = true;
-    tc_wgrad_kernel<128><<<n_chunks, NTH, wgrad_smem<128>(), ctx->stream>>>(dAl, Aprev, n, rows, w0,
-                                                                           partial);
-  } else {
-    static bool cfg = false;
-    if (!cfg) PACT_TRY_S(set_smem(tc_wgrad_kernel<64>, wgrad_smem<64>()));
-    cfg = true;
-    tc_wgrad_kernel<64><<<n_chunks, NTH, wgrad_smem<64>(), ctx->stream>>>(dAl, Aprev, n, rows, w0,
-                                                                         partial);
-  }
+Status tc_dgrad_layer(pact_ctx* ctx, int hidden, const float* dAl, const float* W,
+                      const float* Aprev, int n, float w0, float* dAprev) {
+  if (hidden != H) return unsupported_width();
+  static bool cfg = false;
+  if (!cfg) PACT_TRY_S(set_smem(tc_layer_kernel<kDgrad>, kLayerSmem));
+  cfg = true;
+  tc_layer_kernel<kDgrad><<<layer_grid(ctx, n), LNTH, kLayerSmem, ctx->stream>>>(
+      dAl, W, nullptr, Aprev, n, w0, dAprev);
+  return after_launch(ctx, "tc_layer_kernel<dgrad>");
+}
+
+Status tc_wgrad_layer(pact_ctx* ctx, int hidden, const float* dAl, const float* Aprev, int n,
+                      int rows, float w0, float* partial, int n_chunks) {
+  if (hidden != H) return unsupported_width();
+  static bool cfg = false;
+  if (!cfg) PACT_TRY_S(set_smem(tc_wgrad_kernel, kWgradSmem));
+  cfg = true;
+  tc_wgrad_kernel<<<n_chunks, WNTH, kWgradSmem, ctx->stream>>>(dAl, Aprev, n, rows, w0, partial);
   return after_launch(ctx, "tc_wgrad_kernel");
 }
 

@@ -48,6 +48,20 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
+// K-major SWIZZLE_128B: 8-row x 128-B atoms (32 fp32 of K per row), 16-B
+// chunk index XOR (row % 8), atoms 1024-B aligned and stacked at SBO = 1024.
+// byte(row, k) = row*128 + ((k/4) ^ (row%8))*16 + (k%4)*4 within one 32-wide
+// K chunk; K step s of 8 advances the start address by 32*s bytes.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1) << 16;              // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;      // SBO
+  d |= static_cast<uint64_t>(1) << 46;              // version
+  d |= static_cast<uint64_t>(2) << 61;              // SWIZZLE_128B
+  return d;
+}
+
 // Instruction descriptor, kind::tf32, fp32 accumulator, both operands K-major.
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
   return (1u << 4)                                   // c_format = F32
@@ -124,6 +138,16 @@ __device__ __forceinline__ void fence_proxy_async() {
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s) : "memory");
+}
+
+// Named barrier over `nthreads` (a multiple of 32) of the CTA.
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {

@@ -1,4 +1,4 @@
-// Probe 2 of the tcgen05 building blocks: A operand in TMEM (tcgen05.st from
+// Probe 2 (+ SW128 variant) of the tcgen05 building blocks: A operand in TMEM (tcgen05.st from
 // registers, lane = row), B staged with one cp.async.bulk into shared memory
 // and re-laid out into K-major hi/lo planes; 3xTF32 via the TS form of
 // tcgen05.mma.  C[128][N] = A[128][K] . B[N][K]^T against fp64.
@@ -90,6 +90,78 @@ __global__ void probe(const float* A, const float* B, float* C) {
   if (warp == 0) tc::tmem_free<NC>(t0);
 }
 
+// B planes as SWIZZLE_128B K-major chunks of 32 (one 128-B row per n).
+template <int N, int K>
+__global__ void probe_sw(const float* A, const float* B, float* C) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* b_hi = reinterpret_cast<float*>(smem);  // [K/32][N][32]
+  float* b_lo = b_hi + N * K;
+  __shared__ uint64_t bar_mma;
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  constexpr int NC = 2 * K + N <= 256 ? 256 : 512;
+  if (warp == 0) tc::tmem_alloc<NC>(&tslot);
+  if (tid == 0) {
+    tc::mbar_init(&bar_mma, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t t0 = tslot;
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    float hi[32], lo[32];
+    for (int i = 0; i < 32; ++i) tc::split_tf32(A[tid * K + k0 + i], hi[i], lo[i]);
+    const uint32_t lane_base = t0 + (static_cast<uint32_t>(32 * warp) << 16);
+    tc::tmem_st32(lane_base + k0, hi);
+    tc::tmem_st32(lane_base + K + k0, lo);
+  }
+  for (int e = tid; e < N * K / 4; e += 128) {
+    const int n = e / (K / 4), k = (e % (K / 4)) * 4;
+    float4 v = *reinterpret_cast<const float4*>(B + n * K + k);
+    float4 h, l;
+    tc::split_tf32(v.x, h.x, l.x);
+    tc::split_tf32(v.y, h.y, l.y);
+    tc::split_tf32(v.z, h.z, l.z);
+    tc::split_tf32(v.w, h.w, l.w);
+    const int chunk = k / 32, c = (k % 32) / 4;
+    const int o = chunk * N * 32 + n * 32 + ((c ^ (n & 7)) * 4);
+    *reinterpret_cast<float4*>(b_hi + o) = h;
+    *reinterpret_cast<float4*>(b_lo + o) = l;
+  }
+  tc::fence_proxy_async();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  constexpr uint32_t idesc = tc::idesc_tf32(128, N);
+  if (tid == 0) {
+    const uint32_t sh = static_cast<uint32_t>(__cvta_generic_to_shared(b_hi));
+    const uint32_t sl = static_cast<uint32_t>(__cvta_generic_to_shared(b_lo));
+    const uint32_t d = t0 + 2 * K;
+    for (int s = 0; s < K / 8; ++s) {
+      const uint32_t off = (s / 4) * N * 128 + (s % 4) * 32;
+      const uint64_t bh = tc::smem_desc_sw128(sh + off);
+      const uint64_t bl = tc::smem_desc_sw128(sl + off);
+      tc::mma_tf32_ts(d, t0 + K + 8 * s, bh, idesc, s != 0);
+      tc::mma_tf32_ts(d, t0 + 8 * s, bl, idesc, 1);
+      tc::mma_tf32_ts(d, t0 + 8 * s, bh, idesc, 1);
+    }
+    tc::mma_commit(&bar_mma);
+  }
+  tc::mbar_wait(&bar_mma, 0);
+  tc::fence_after_sync();
+  for (int c0 = 0; c0 < N; c0 += 32) {
+    float v[32];
+    tc::tmem_ld32(t0 + 2 * K + (static_cast<uint32_t>(32 * warp) << 16) + c0, v);
+    for (int i = 0; i < 32; ++i) C[tid * N + c0 + i] = v[i];
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<NC>(t0);
+}
+
 template <int N, int K>
 int run() {
   std::mt19937_64 rng(7);
@@ -106,7 +178,15 @@ int run() {
   const size_t smem = 3 * N * K * 4;
   cudaFuncSetAttribute(probe<N, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaMemset(dC, 0, C.size() * 4);
-  probe<N, K><<<1, 128, smem>>>(dA, dB, dC);
+  static int variant = 0;
+  if (variant++ % 2 == 0) {
+    probe<N, K><<<1, 128, smem>>>(dA, dB, dC);
+  } else {
+    const size_t sm2 = 2 * N * K * 4 + 1024;
+    cudaFuncSetAttribute(probe_sw<N, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    probe_sw<N, K><<<1, 128, sm2>>>(dA, dB, dC);
+    printf("[SW128] ");
+  }
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     printf("N=%d K=%d launch error %s\n", N, K, cudaGetErrorString(e));
@@ -136,7 +216,8 @@ int run() {
 }
 
 int main() {
-  int bad = run<128, 128>() + run<64, 64>() + run<128, 32>();
+  int bad = 0;
+  for (int rep = 0; rep < 2; ++rep) bad += run<128, 128>() + run<64, 64>() + run<128, 32>();
   printf(bad ? "PROBE2 FAILED\n" : "PROBE2 OK\n");
   return bad;
 }
