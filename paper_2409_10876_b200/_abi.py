@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpact_cuda.so")
+LIB_PATH = os.environ.get("PACT_LIB") or os.path.join(_HERE, "lib", "libpact_cuda.so")
 
 PACT_OK = 0
 PACT_E_VALIDATION = 2

@@ -153,14 +153,23 @@ struct TileD {
 };
 
 // a_0[m][n] = b_0[n] + W_0[n][0] c_x + W_0[n][1] c_y     (nfield.hpp:117-121, l = 0)
+// One thread per 4 consecutive features of a pixel (float4 store).
 __global__ void siren_first_kernel(const float2* __restrict__ coords, const float* __restrict__ W0,
                                    const float* __restrict__ b0, int n, int H,
                                    float* __restrict__ A0) {
-  size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-  if (i >= static_cast<size_t>(n) * H) return;
-  int m = static_cast<int>(i / H), k = static_cast<int>(i - static_cast<size_t>(m) * H);
-  float2 c = coords[m];
-  A0[i] = fmaf(W0[2 * k + 1], c.y, fmaf(W0[2 * k], c.x, b0[k]));
+  const int q4 = H / 4;
+  const size_t total = static_cast<size_t>(n) * q4;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int m = static_cast<int>(i / q4), k = static_cast<int>(i - static_cast<size_t>(m) * q4) * 4;
+    const float2 c = coords[m];
+    const float4 wa = *reinterpret_cast<const float4*>(W0 + 2 * k);
+    const float4 wb = *reinterpret_cast<const float4*>(W0 + 2 * k + 4);
+    const float4 b = *reinterpret_cast<const float4*>(b0 + k);
+    *reinterpret_cast<float4*>(A0 + i * 4) =
+        make_float4(fmaf(wa.y, c.y, fmaf(wa.x, c.x, b.x)), fmaf(wa.w, c.y, fmaf(wa.z, c.x, b.y)),
+                    fmaf(wb.y, c.y, fmaf(wb.x, c.x, b.z)), fmaf(wb.w, c.y, fmaf(wb.z, c.x, b.w)));
+  }
 }
 
 // a_l = W_l sin(w0 a_{l-1}) + b_l        grid (ceil(n/128), H/BN)
@@ -209,50 +218,83 @@ siren_fwd_kernel(const float* __restrict__ Ain, const float* __restrict__ W,
   }
 }
 
-// dv[idx[m]] = out_scale (b_L + sum_k w_L[k] sin(w0 a_{L-1}[m][k]))   one warp per pixel group
+// dv[idx[m]] = out_scale (b_L + sum_k w_L[k] sin(w0 a_{L-1}[m][k]))
+// Eight threads per pixel (H/8 features each, float4 loads), 3-step shuffle sum.
 __global__ void siren_out_kernel(const float* __restrict__ A, const float* __restrict__ wL,
                                  const float* __restrict__ bL, const int* __restrict__ idx, int n,
                                  int H, float w0, float out_scale, float* __restrict__ dv) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int m0 = warp * 32;
-  for (int q = 0; q < 32; ++q) {
-    int m = m0 + q;
-    if (m >= n) break;
-    const float* row = A + static_cast<size_t>(m) * H;
+  const int sub = threadIdx.x & 7;
+  const int per = H / 8;  // features per thread, multiple of 4 (H % 32 == 0)
+  for (int m = (blockIdx.x * blockDim.x + threadIdx.x) >> 3; m < ((n + 3) & ~3);
+       m += (gridDim.x * blockDim.x) >> 3) {
     float s = 0.f;
-    for (int k = lane; k < H; k += 32) s = fmaf(wL[k], sinw(row[k], w0), s);
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) dv[idx[m]] = out_scale * (bL[0] + s);
+    if (m < n) {
+      const float* row = A + static_cast<size_t>(m) * H + sub * 4;
+      for (int k = 0; k < per; k += 4) {
+        const float4 a = *reinterpret_cast<const float4*>(row + k * 8);
+        const float4 w = *reinterpret_cast<const float4*>(wL + sub * 4 + k * 8);
+        s = fmaf(w.x, sinw(a.x, w0), s);
+        s = fmaf(w.y, sinw(a.y, w0), s);
+        s = fmaf(w.z, sinw(a.z, w0), s);
+        s = fmaf(w.w, sinw(a.w, w0), s);
+      }
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (sub == 0 && m < n) dv[idx[m]] = out_scale * (bL[0] + s);
   }
 }
 
 // Top of the backward: g_m = out_scale (gv[idx m] + gmask[m]);
 //   dA_{L-1}[m][k] = g_m w_L[k] w0 cos(w0 a)      (nfield.hpp:198-200)
 //   partial gW_L[k] += g_m sin(w0 a), gb_L += g_m (nfield.hpp:194-197)
-// grid.x = pixel chunks of `rows` pixels; 256 threads = H columns x (256/H) row lanes.
-__global__ void siren_top_kernel(const float* __restrict__ A, const float* __restrict__ wL,
-                                 const double* __restrict__ gv, const float* __restrict__ gmask,
-                                 const int* __restrict__ idx, int n, int H, int rows, float w0,
-                                 float out_scale, float* __restrict__ dA,
-                                 float* __restrict__ partial) {
+// grid.x = pixel chunks of `rows` pixels; 256 threads = H columns x (256/H)
+// row lanes; pixels in batches of 8 per lane with the loads issued first.
+__global__ void __launch_bounds__(NT)
+siren_top_kernel(const float* __restrict__ A, const float* __restrict__ wL,
+                 const double* __restrict__ gv, const float* __restrict__ gmask,
+                 const int* __restrict__ idx, int n, int H, int rows, float w0, float out_scale,
+                 float* __restrict__ dA, float* __restrict__ partial) {
+  constexpr int U = 8;
+  __shared__ float s_g[NT];
   __shared__ float s_part[NT + 32];
   const int lanes = NT / H;  // H in {64, 128, 256}
   const int k = threadIdx.x % H, rl = threadIdx.x / H;
   const int m_begin = blockIdx.x * rows, m_end = min(n, m_begin + rows);
   float gw = 0.f, gb = 0.f;
   const float wk = wL[k];
-  for (int m = m_begin + rl; m < m_end; m += lanes) {
-    float g = 0.f;
-    if (gv) g += static_cast<float>(gv[idx[m]]);
-    if (gmask) g += gmask[m];
-    g *= out_scale;
-    float a = A[static_cast<size_t>(m) * H + k];
-    float s, c;
-    sincosw(a, w0, &s, &c);
-    dA[static_cast<size_t>(m) * H + k] = g * wk * w0 * c;
-    gw = fmaf(g, s, gw);
-    gb += g;
+  for (int m0 = m_begin; m0 < m_end; m0 += U * lanes) {
+    const int cnt = min(U * lanes, m_end - m0);
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+      const int m = m0 + threadIdx.x;
+      float g = 0.f;
+      if (gv) g += static_cast<float>(gv[idx[m]]);
+      if (gmask) g += gmask[m];
+      s_g[threadIdx.x] = g * out_scale;
+    }
+    __syncthreads();
+    float a[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int q = rl + lanes * j;
+      a[j] = q < cnt ? A[static_cast<size_t>(m0 + q) * H + k] : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int q = rl + lanes * j;
+      if (q < cnt) {
+        const float g = s_g[q];
+        float sn, cs;
+        sincosw(a[j], w0, &sn, &cs);
+        dA[static_cast<size_t>(m0 + q) * H + k] = g * wk * w0 * cs;
+        gw = fmaf(g, sn, gw);
+        gb += g;
+      }
+    }
   }
+  __syncthreads();
   s_part[threadIdx.x] = gw;
   __syncthreads();
   float* out = partial + static_cast<size_t>(blockIdx.x) * (H + 1);
@@ -402,12 +444,22 @@ __global__ void siren_wgrad0_kernel(const float* __restrict__ dA0, const float2*
   const int r = threadIdx.x % H, rl = threadIdx.x / H;
   const int m_begin = blockIdx.x * rows, m_end = min(n, m_begin + rows);
   float gx = 0.f, gy = 0.f, gb = 0.f;
-  for (int m = m_begin + rl; m < m_end; m += lanes) {
-    float d = dA0[static_cast<size_t>(m) * H + r];
-    float2 c = coords[m];
-    gx = fmaf(d, c.x, gx);
-    gy = fmaf(d, c.y, gy);
-    gb += d;
+  constexpr int U = 8;
+  for (int m0 = m_begin + rl; m0 < m_end; m0 += U * lanes) {
+    float d[U];
+    float2 c[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int m = m0 + lanes * j;
+      d[j] = m < m_end ? dA0[static_cast<size_t>(m) * H + r] : 0.f;
+      c[j] = m < m_end ? coords[m] : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      gx = fmaf(d[j], c[j].x, gx);
+      gy = fmaf(d[j], c[j].y, gy);
+      gb += d[j];
+    }
   }
   s_part[threadIdx.x] = gx;
   s_part[NT + threadIdx.x] = gy;
@@ -428,13 +480,31 @@ __global__ void siren_wgrad0_kernel(const float* __restrict__ dA0, const float2*
 }
 
 // grad[off + p] = sum_chunk partial[chunk][p]   (fixed order, fp64)
-__global__ void reduce_partials_kernel(const float* __restrict__ partial, int n_chunks,
-                                       int per_chunk, double* __restrict__ grad) {
-  int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= per_chunk) return;
-  double s = 0.0;
-  for (int c = 0; c < n_chunks; ++c) s += partial[static_cast<size_t>(c) * per_chunk + p];
-  grad[p] = s;
+// Block (32 params) x (32 chunk lanes); lane y sums chunks y, y+32, ... with
+// four independent accumulators, then a fixed-order fold over the lanes.
+__global__ void __launch_bounds__(1024)
+reduce_partials_kernel(const float* __restrict__ partial, int n_chunks, int per_chunk,
+                       double* __restrict__ grad) {
+  __shared__ double s_sum[32][33];
+  const int p = blockIdx.x * 32 + threadIdx.x;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (p < per_chunk) {
+    int c = threadIdx.y;
+    for (; c + 96 < n_chunks; c += 128) {
+      a0 += partial[static_cast<size_t>(c) * per_chunk + p];
+      a1 += partial[static_cast<size_t>(c + 32) * per_chunk + p];
+      a2 += partial[static_cast<size_t>(c + 64) * per_chunk + p];
+      a3 += partial[static_cast<size_t>(c + 96) * per_chunk + p];
+    }
+    for (; c < n_chunks; c += 32) a0 += partial[static_cast<size_t>(c) * per_chunk + p];
+  }
+  s_sum[threadIdx.y][threadIdx.x] = (a0 + a1) + (a2 + a3);
+  __syncthreads();
+  if (threadIdx.y == 0 && p < per_chunk) {
+    double t = 0.0;
+    for (int y = 0; y < 32; ++y) t += s_sum[y][threadIdx.x];
+    grad[p] = t;
+  }
 }
 
 // ---- per-pixel path for small / odd hidden widths (unit-test networks) ----
@@ -603,8 +673,7 @@ Status siren_forward(pact_ctx* ctx, const SirenShape& s, const float* theta, Sir
                                                            dv, stride);
     return after_launch(ctx, "siren_fwd_small_kernel");
   }
-  size_t total = stride;
-  siren_first_kernel<<<static_cast<int>((total + 255) / 256), 256, 0, st>>>(
+  siren_first_kernel<<<ctx->num_sms * 8, 256, 0, st>>>(
       w.coords, theta + s.offset(0), theta + s.offset(0) + 2 * H, n, H, w.acts);
   PACT_TRY_S(after_launch(ctx, "siren_first_kernel"));
   for (int l = 1; l < L; ++l) {
@@ -624,7 +693,7 @@ Status siren_forward(pact_ctx* ctx, const SirenShape& s, const float* theta, Sir
     PACT_TRY_S(after_launch(ctx, "siren_fwd_kernel"));
   }
   const float* wL = theta + s.offset(L);
-  siren_out_kernel<<<div_up(div_up(n, 32), 8), 256, 0, st>>>(w.acts + (L - 1) * stride, wL, wL + H,
+  siren_out_kernel<<<std::min(div_up(n, 32), ctx->num_sms * 8), 256, 0, st>>>(w.acts + (L - 1) * stride, wL, wL + H,
                                                              w.idx, n, H, w0,
                                                              static_cast<float>(s.out_scale), dv);
   return after_launch(ctx, "siren_out_kernel");
@@ -653,7 +722,7 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
   }
   // chunking for the split-M reductions
   const int tilesW = (H / 128 > 0 ? H / 128 : 1) * (H / 128 > 0 ? H / 128 : 1);
-  const int rows_top = chunk_rows(n, 1, ctx->num_sms);
+  const int rows_top = chunk_rows(n, 1, 4 * ctx->num_sms);
   const int n_top = div_up(n, rows_top);
   const bool use_tc = siren_use_tc(H);
   int rows_w = chunk_rows(n, tilesW, ctx->num_sms);
@@ -671,7 +740,7 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
   siren_top_kernel<<<n_top, NT, 0, st>>>(w.acts + (L - 1) * stride, wL, gv, gmask, w.idx, n, H,
                                          rows_top, w0, osc, cur, w.partial);
   PACT_TRY_S(after_launch(ctx, "siren_top_kernel"));
-  reduce_partials_kernel<<<div_up(H + 1, 128), 128, 0, st>>>(w.partial, n_top, H + 1,
+  reduce_partials_kernel<<<div_up(H + 1, 32), dim3(32, 32), 0, st>>>(w.partial, n_top, H + 1,
                                                              grad + s.offset(L));
   PACT_TRY_S(after_launch(ctx, "reduce_partials_kernel"));
   for (int l = L - 1; l >= 1; --l) {
@@ -687,7 +756,7 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
                                                                          w0, w.partial);
     if (!use_tc) PACT_TRY_S(after_launch(ctx, "siren_wgrad_kernel"));
     int per = H * H + H;
-    reduce_partials_kernel<<<div_up(per, 256), 256, 0, st>>>(w.partial, n_w, per, grad + s.offset(l));
+    reduce_partials_kernel<<<div_up(per, 32), dim3(32, 32), 0, st>>>(w.partial, n_w, per, grad + s.offset(l));
     PACT_TRY_S(after_launch(ctx, "reduce_partials_kernel"));
     // delta to layer l-1
     if (use_tc)
@@ -702,7 +771,7 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
   }
   siren_wgrad0_kernel<<<n_top, NT, 0, st>>>(cur, w.coords, n, H, rows_top, w.partial);
   PACT_TRY_S(after_launch(ctx, "siren_wgrad0_kernel"));
-  reduce_partials_kernel<<<div_up(3 * H, 128), 128, 0, st>>>(w.partial, n_top, 3 * H,
+  reduce_partials_kernel<<<div_up(3 * H, 32), dim3(32, 32), 0, st>>>(w.partial, n_top, 3 * H,
                                                              grad + s.offset(0));
   return after_launch(ctx, "reduce_partials_kernel");
 }

@@ -25,6 +25,13 @@
 #include "siren.cuh"
 #include "tc.cuh"
 
+// TC_EXP (experiments only, never set in the product build): 1 = no MMA
+// issue, 2 = no raw reads / sine (zero planes), 3 = no epilogue stores,
+// 4 = 1 + 2 (bulk loads, barriers and epilogue only).
+#ifndef TC_EXP
+#define TC_EXP 0
+#endif
+
 namespace pactgpu {
 namespace {
 
@@ -86,7 +93,7 @@ struct LayerBars {
 constexpr uint32_t kColAlo = 128, kColD = 256;
 constexpr int LNTH = 512;  // warps 0-7 stage (thread 0 issues), warps 8-15 drain
 constexpr int LPROD = 256;  // producer threads
-constexpr int WNTH = 256;  // weight gradient: warps 0-3 dA^T, warps 4-7 sine planes
+constexpr int WNTH = 384;  // weight gradient: warps 0-3 dA^T, warps 4-11 sine planes
 
 template <int MODE>
 __global__ void __launch_bounds__(LNTH, 1)
@@ -186,12 +193,14 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
         float4 v[PJ];
 #pragma unroll
         for (int j = 0; j < PJ; ++j)
-          v[j] = *reinterpret_cast<const float4*>(rt + (p0 + (LPROD / 8) * j) * H + kc0 + 4 * c4);
+          v[j] = (TC_EXP == 2 || TC_EXP == 4) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                             : *reinterpret_cast<const float4*>(rt + (p0 + (LPROD / 8) * j) * H +
+                                                                kc0 + 4 * c4);
 #pragma unroll
         for (int j = 0; j < PJ; ++j) {
           const int p = p0 + (LPROD / 8) * j;
           float4 z = v[j];
-          if (MODE == kForward)
+          if (MODE == kForward && TC_EXP != 2 && TC_EXP != 4)
             z = make_float4(sin_w(z.x, w0), sin_w(z.y, w0), sin_w(z.z, w0), sin_w(z.w, w0));
           if (p >= rows) z = make_float4(0.f, 0.f, 0.f, 0.f);
           float4 h, l;
@@ -210,7 +219,7 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
           tc::fence_after_sync();
           const uint32_t sbh = saddr(bh), sbl = saddr(bl);
 #pragma unroll
-          for (int s = 0; s < KC / 8; ++s) {
+          for (int s = 0; s < (TC_EXP == 1 || TC_EXP == 4 ? 0 : KC / 8); ++s) {
             const uint32_t ka = kc0 + 8 * s;
             const uint64_t dh = tc::smem_desc_sw128(sbh + 32 * s);
             const uint64_t dl = tc::smem_desc_sw128(sbl + 32 * s);
@@ -250,7 +259,7 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
         for (int j = 0; j < 32; ++j) {
           const int c = cb + h + j;
           const float out = MODE == kForward ? v[j] + brow : v[j] * dsin_w(av[h + j], w0);
-          if (c < rows) y[c * H] = out;
+          if (c < rows && (TC_EXP != 3 || out == 12345.f)) y[c * H] = out;
         }
       }
       tc::fence_before_sync();
@@ -340,15 +349,18 @@ tc_wgrad_kernel(const float* __restrict__ dA, const float* __restrict__ Aprev, i
         tc::tmem_st32(lb, hi);
         tc::tmem_st32(lb + 32, lo);
       } else {
-        // sin(w0 a_{l-1})^T chunk -> planes (row k = r, K = pixel)
-        float a[KC];
+        // sin(w0 a_{l-1})^T chunk -> planes (row k = r, K = pixel); warps
+        // 4-7 take pixels [0, 16) of the chunk, warps 8-11 pixels [16, 32)
+        constexpr int HK = KC / 2;
+        const int j0 = warp >= 8 ? HK : 0;
+        float a[HK];
 #pragma unroll
-        for (int j = 0; j < KC; ++j) a[j] = tz[(q0 + j) * H + r];
+        for (int j = 0; j < HK; ++j) a[j] = tz[(q0 + j0 + j) * H + r];
 #pragma unroll
-        for (int j = 0; j < KC; ++j) a[j] = q0 + j < valid ? sin_w(a[j], w0) : 0.f;
+        for (int j = 0; j < HK; ++j) a[j] = q0 + j0 + j < valid ? sin_w(a[j], w0) : 0.f;
 #pragma unroll
-        for (int j = 0; j < KC; j += 4)
-          put4(bh, bl, r, j, H, make_float4(a[j], a[j + 1], a[j + 2], a[j + 3]));
+        for (int j = 0; j < HK; j += 4)
+          put4(bh, bl, r, j0 + j, H, make_float4(a[j], a[j + 1], a[j + 2], a[j + 3]));
         tc::fence_proxy_async();
       }
       sync_tc();
@@ -372,19 +384,21 @@ tc_wgrad_kernel(const float* __restrict__ dA, const float* __restrict__ Aprev, i
     if (tid == 0) tc::mma_commit(&sb.acc);
     tc::mbar_wait(&sb.acc, 0);
     tc::fence_after_sync();
-    // warps w and w + 4 share TMEM lanes; each drains half the columns
+    // warps w and w + 4 (w < 4) share TMEM lanes; each drains half the columns
     const uint32_t lb = lane_base(t0, warp & 3);
     const int cbeg = warp < 4 ? 0 : H / 2;
+    if (warp < 8) {
 #pragma unroll 1
-    for (int c0 = cbeg; c0 < cbeg + H / 2; c0 += 32) {
-      float v[32];
-      tc::tmem_ld32(lb + c0, v);
+      for (int c0 = cbeg; c0 < cbeg + H / 2; c0 += 32) {
+        float v[32];
+        tc::tmem_ld32(lb + c0, v);
 #pragma unroll
-      for (int j = 0; j < 32; j += 4)
-        *reinterpret_cast<float4*>(out + static_cast<size_t>(r) * H + c0 + j) =
-            make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(out + static_cast<size_t>(r) * H + c0 + j) =
+              make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
     }
-  } else {
+  } else if (warp < 8) {
     for (int c = (warp < 4 ? 0 : H / 2); c < (warp < 4 ? H / 2 : H); ++c)
       out[static_cast<size_t>(r) * H + c] = 0.f;
   }
