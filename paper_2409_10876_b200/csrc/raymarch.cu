@@ -129,6 +129,330 @@ __device__ __forceinline__ RayPix ray_pixels(const RayArgs& a, double cx, double
   return p;
 }
 
+// ---- generic per-step marches (any start position; the reference's branch
+// structure step by step) ---------------------------------------------------
+template <bool TEX>
+__device__ float march_forward_generic(const RayArgs& a, const Border& bd, const RayPix& rp,
+                                       int n, float v0) {
+  float acc = 0.f;
+  // steps that cannot be in the corner regime: no early exit, unrolled
+  const int i_main = max(0, min(n, rp.i_corner - 2));
+  int i = 0;
+#pragma unroll 4
+  for (; i < i_main; ++i) {
+    Step st = step_at<TEX>(a, bd, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
+                           fmaf(static_cast<float>(i), rp.dfy, rp.fys));
+    acc += st.d / (v0 + st.d);  // (1 - v0/v), v = v0 + d
+  }
+  for (; i < n; ++i) {
+    Step st = step_at<TEX>(a, bd, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
+                           fmaf(static_cast<float>(i), rp.dfy, rp.fys));
+    float term = st.d / (v0 + st.d);
+    if (st.corner) {  // the ray moves outward: every remaining step is identical
+      acc += static_cast<float>(n - i) * term;
+      break;
+    }
+    acc += term;
+  }
+  return acc;
+}
+
+__device__ __forceinline__ void flush_cell(double* __restrict__ g, int W, int H, int ix, int iy,
+                                           const double acc[4]) {
+  int ix1 = min(ix + 1, W - 1), iy1 = min(iy + 1, H - 1);
+  if (acc[0] != 0.0) atomicAdd(g + iy * W + ix, acc[0]);
+  if (acc[1] != 0.0) atomicAdd(g + iy * W + ix1, acc[1]);
+  if (acc[2] != 0.0) atomicAdd(g + iy1 * W + ix, acc[2]);
+  if (acc[3] != 0.0) atomicAdd(g + iy1 * W + ix1, acc[3]);
+}
+
+// Per-ray accumulators of the current stencil cell's pixels (cx + i, cy + j):
+// a{j}{i}.  A pixel collects a handful of steps in fp32 before its fp64 flush;
+// on a move, pixels shared with the new cell stay in registers (halves the
+// atomics of a horizontal/vertical move).
+struct CellAcc {
+  int cx = -1, cy = -1;
+  float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
+
+  __device__ __forceinline__ void move(double* __restrict__ grad, int W, int ix, int iy) {
+    if (ix == cx && iy == cy) return;
+    if (cx >= 0) {
+      const int dx = ix - cx, dy = iy - cy;
+      float n00 = 0.f, n01 = 0.f, n10 = 0.f, n11 = 0.f;
+      const float old[4] = {a00, a01, a10, a11};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int ox = (q & 1) - dx, oy = (q >> 1) - dy;  // old pixel in the new cell
+        const float val = old[q];
+        if (ox >= 0 && ox <= 1 && oy >= 0 && oy <= 1) {
+          const int t = oy * 2 + ox;
+          n00 += t == 0 ? val : 0.f;
+          n01 += t == 1 ? val : 0.f;
+          n10 += t == 2 ? val : 0.f;
+          n11 += t == 3 ? val : 0.f;
+        } else if (val != 0.f) {
+          atomicAdd(grad + (cy + (q >> 1)) * W + cx + (q & 1), static_cast<double>(val));
+        }
+      }
+      a00 = n00;
+      a01 = n01;
+      a10 = n10;
+      a11 = n11;
+    }
+    cx = ix;
+    cy = iy;
+  }
+  __device__ __forceinline__ void flush(double* __restrict__ grad, int W, int H) {
+    if (cx < 0) return;
+    const double fin[4] = {a00, a01, a10, a11};
+    flush_cell(grad, W, H, cx, cy, fin);
+    cx = cy = -1;
+    a00 = a01 = a10 = a11 = 0.f;
+  }
+};
+
+template <bool TEX>
+__device__ void march_backward_generic(const RayArgs& a, const Border& bd, const RayPix& rp, int n,
+                                       float v0, float gscale, double* __restrict__ grad) {
+  CellAcc c;
+  for (int i = 0; i < n; ++i) {
+    Step st = step_at<TEX>(a, bd, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
+                           fmaf(static_cast<float>(i), rp.dfy, rp.fys));
+    float v = v0 + st.d;
+    float f = gscale / (v * v);
+    const bool corner = st.corner && i >= rp.i_corner - 2;
+    if (corner) f *= static_cast<float>(n - i);  // all remaining steps, same pixel
+    c.move(grad, a.W, st.ix, st.iy);
+    c.a00 = fmaf(f, st.w00, c.a00);
+    c.a01 = fmaf(f, st.w01, c.a01);
+    c.a10 = fmaf(f, st.w10, c.a10);
+    c.a11 = fmaf(f, st.w11, c.a11);
+    if (corner) break;
+  }
+  c.flush(grad, a.W, a.H);
+}
+
+// ---- regime-split marches (texture path, ray starts inside the grid) -------
+// A ray from an interior point moves monotonically away in each coordinate,
+// so its steps fall into three contiguous ranges: interior [0, i_side), one
+// coordinate clamped (a 1-D interpolation along a border line) up to
+// i_corner, and the corner (both clamped: one pixel) for the rest.  Each range
+// is a branch-free loop; the range ends come from the same fp32 position
+// formula the steps use, so the regime of every step matches step_at.
+struct Regimes {
+  int i_side, i_corner;
+  bool x_first;  // x leaves the grid first: the side range runs along a column
+};
+
+__device__ __forceinline__ bool out_at(int i, float fs, float df, float hi) {
+  const float f = fmaf(static_cast<float>(i), df, fs);
+  return !(f >= 0.f && f <= hi);
+}
+
+// First step index in [0, n] whose coordinate is off [0, hi] (n: never).
+__device__ int first_out(float fs, float df, float hi, int n) {
+  double g;
+  if (df > 0.f)
+    g = floor((static_cast<double>(hi) - fs) / df) + 1.0;
+  else if (df < 0.f)
+    g = floor(-static_cast<double>(fs) / df) + 1.0;
+  else
+    g = static_cast<double>(n);
+  int i = static_cast<int>(fmin(fmax(g, 0.0), static_cast<double>(n)));
+  while (i > 0 && out_at(i - 1, fs, df, hi)) --i;
+  while (i < n && !out_at(i, fs, df, hi)) ++i;
+  return i;
+}
+
+__device__ __forceinline__ Regimes regimes(const RayPix& rp, int n, float Wm1, float Hm1) {
+  const int ix = first_out(rp.fxs, rp.dfx, Wm1, n), iy = first_out(rp.fys, rp.dfy, Hm1, n);
+  return {min(ix, iy), max(ix, iy), ix < iy};
+}
+
+__device__ __forceinline__ float interior_d(cudaTextureObject_t tex, float fx, float fy, int W,
+                                            int H, float& ax, float& ay, int& ix, int& iy) {
+  ix = min(static_cast<int>(fx), W - 2);
+  iy = min(static_cast<int>(fy), H - 2);
+  ax = fx - ix;
+  ay = fy - iy;
+  // texel (i, j) centre at (i + 0.5, j + 0.5): the gather footprint of
+  // (ix + 1, iy + 1) is {ix, ix+1} x {iy, iy+1}: w=(ix,iy) z=(ix+1,iy) x=(ix,iy+1) y=(ix+1,iy+1)
+  const float4 g = tex2Dgather<float4>(tex, ix + 1.f, iy + 1.f, 0);
+  const float top = fmaf(ax, g.z - g.w, g.w);
+  const float bot = fmaf(ax, g.y - g.x, g.x);
+  return fmaf(ay, bot - top, top);
+}
+
+__global__ void __launch_bounds__(256) wavefront_split_kernel(RayArgs a, float* __restrict__ w) {
+  extern __shared__ float s_border[];
+  const Border bd = load_border(a, s_border);
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.n_rays) return;
+  int patch = r / a.n_angles, ang = r - patch * a.n_angles;
+  double2 c = a.centers[patch];
+  Ray ray = make_ray(c.x, c.y, ang, a.n_angles, a.ring_r, a.mcx, a.mcy, a.mr, a.step);
+  const RayPix rp = ray_pixels(a, c.x, c.y, ray);
+  const float v0 = static_cast<float>(a.v0);
+  const int W = a.W, H = a.H, n = ray.n;
+  const float Wm1 = static_cast<float>(W - 1), Hm1 = static_cast<float>(H - 1);
+  float acc = 0.f;
+  if (n > 0 && (out_at(0, rp.fxs, rp.dfx, Wm1) || out_at(0, rp.fys, rp.dfy, Hm1))) {
+    acc = march_forward_generic<true>(a, bd, rp, n, v0);
+  } else if (n > 0) {
+    const Regimes rg = regimes(rp, n, Wm1, Hm1);
+#pragma unroll 4
+    for (int i = 0; i < rg.i_side; ++i) {
+      float ax, ay;
+      int ix, iy;
+      const float d = interior_d(a.tex, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
+                                 fmaf(static_cast<float>(i), rp.dfy, rp.fys), W, H, ax, ay, ix, iy);
+      acc += __fdividef(d, v0 + d);
+    }
+    if (rg.x_first) {
+      const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
+#pragma unroll 4
+      for (int i = rg.i_side; i < rg.i_corner; ++i) {
+        const float fy = fmaf(static_cast<float>(i), rp.dfy, rp.fys);
+        const int iy = min(static_cast<int>(fy), H - 2);
+        const float c0 = col[iy];
+        const float d = fmaf(fy - iy, col[iy + 1] - c0, c0);
+        acc += __fdividef(d, v0 + d);
+      }
+    } else {
+      const float* row = rp.dfy > 0.f ? bd.rowT : bd.rowB;
+#pragma unroll 4
+      for (int i = rg.i_side; i < rg.i_corner; ++i) {
+        const float fx = fmaf(static_cast<float>(i), rp.dfx, rp.fxs);
+        const int ix = min(static_cast<int>(fx), W - 2);
+        const float c0 = row[ix];
+        const float d = fmaf(fx - ix, row[ix + 1] - c0, c0);
+        acc += __fdividef(d, v0 + d);
+      }
+    }
+    if (rg.i_corner < n) {
+      const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
+      const float d = col[rp.dfy > 0.f ? H - 1 : 0];
+      acc += static_cast<float>(n - rg.i_corner) * __fdividef(d, v0 + d);
+    }
+  }
+  w[r] = static_cast<float>(ray.dl) * acc;
+}
+
+// 1-D carry along a border line: pixels (line position q, q + 1).
+struct LineAcc {
+  int q = -1;
+  float b0 = 0.f, b1 = 0.f;
+  __device__ __forceinline__ void move(double* __restrict__ grad, int nq, int stride, int base) {
+    if (nq == q) return;
+    if (q >= 0) {
+      if (nq == q + 1) {
+        if (b0 != 0.f) atomicAdd(grad + base + q * stride, static_cast<double>(b0));
+        b0 = b1;
+        b1 = 0.f;
+      } else if (nq == q - 1) {
+        if (b1 != 0.f) atomicAdd(grad + base + (q + 1) * stride, static_cast<double>(b1));
+        b1 = b0;
+        b0 = 0.f;
+      } else {
+        if (b0 != 0.f) atomicAdd(grad + base + q * stride, static_cast<double>(b0));
+        if (b1 != 0.f) atomicAdd(grad + base + (q + 1) * stride, static_cast<double>(b1));
+        b0 = b1 = 0.f;
+      }
+    }
+    q = nq;
+  }
+  __device__ __forceinline__ void flush(double* __restrict__ grad, int stride, int base) {
+    if (q < 0) return;
+    if (b0 != 0.f) atomicAdd(grad + base + q * stride, static_cast<double>(b0));
+    if (b1 != 0.f) atomicAdd(grad + base + (q + 1) * stride, static_cast<double>(b1));
+  }
+};
+
+__global__ void __launch_bounds__(256) ray_backward_split_kernel(RayArgs a, const float* __restrict__ dw,
+                                                                 double* __restrict__ grad) {
+  extern __shared__ float s_border[];
+  const Border bd = load_border(a, s_border);
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.n_rays) return;
+  const float gr = dw[r];
+  if (gr == 0.f) return;  // aberration.hpp:340
+  int patch = r / a.n_angles, ang = r - patch * a.n_angles;
+  double2 c = a.centers[patch];
+  Ray ray = make_ray(c.x, c.y, ang, a.n_angles, a.ring_r, a.mcx, a.mcy, a.mr, a.step);
+  if (ray.n == 0) return;
+  const RayPix rp = ray_pixels(a, c.x, c.y, ray);
+  const float v0 = static_cast<float>(a.v0);
+  // f = g * dl * v0 / v^2 per step (aberration.hpp:354-355)
+  const float gscale = static_cast<float>(static_cast<double>(gr) * ray.dl * a.v0);
+  const int W = a.W, H = a.H, n = ray.n;
+  const float Wm1 = static_cast<float>(W - 1), Hm1 = static_cast<float>(H - 1);
+  if (out_at(0, rp.fxs, rp.dfx, Wm1) || out_at(0, rp.fys, rp.dfy, Hm1)) {
+    march_backward_generic<true>(a, bd, rp, n, v0, gscale, grad);
+    return;
+  }
+  const Regimes rg = regimes(rp, n, Wm1, Hm1);
+  {
+    CellAcc cell;
+    for (int i = 0; i < rg.i_side; ++i) {
+      float ax, ay;
+      int ix, iy;
+      const float d = interior_d(a.tex, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
+                                 fmaf(static_cast<float>(i), rp.dfy, rp.fys), W, H, ax, ay, ix, iy);
+      const float v = v0 + d;
+      const float f = __fdividef(gscale, v * v);
+      cell.move(grad, W, ix, iy);
+      const float fy1 = f * ay, fy0 = f - fy1;  // f (1 - ay), f ay
+      cell.a00 = fmaf(-fy0, ax, cell.a00 + fy0);
+      cell.a01 = fmaf(fy0, ax, cell.a01);
+      cell.a10 = fmaf(-fy1, ax, cell.a10 + fy1);
+      cell.a11 = fmaf(fy1, ax, cell.a11);
+    }
+    cell.flush(grad, W, H);
+  }
+  if (rg.i_side < rg.i_corner) {
+    LineAcc line;
+    if (rg.x_first) {
+      const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
+      const int base = rp.dfx > 0.f ? W - 1 : 0;
+      for (int i = rg.i_side; i < rg.i_corner; ++i) {
+        const float fy = fmaf(static_cast<float>(i), rp.dfy, rp.fys);
+        const int iy = min(static_cast<int>(fy), H - 2);
+        const float ay = fy - iy, c0 = col[iy];
+        const float v = v0 + fmaf(ay, col[iy + 1] - c0, c0);
+        const float f = __fdividef(gscale, v * v);
+        line.move(grad, iy, W, base);
+        const float f1 = f * ay;
+        line.b0 += f - f1;
+        line.b1 += f1;
+      }
+      line.flush(grad, W, base);
+    } else {
+      const float* row = rp.dfy > 0.f ? bd.rowT : bd.rowB;
+      const int base = rp.dfy > 0.f ? (H - 1) * W : 0;
+      for (int i = rg.i_side; i < rg.i_corner; ++i) {
+        const float fx = fmaf(static_cast<float>(i), rp.dfx, rp.fxs);
+        const int ix = min(static_cast<int>(fx), W - 2);
+        const float ax = fx - ix, c0 = row[ix];
+        const float v = v0 + fmaf(ax, row[ix + 1] - c0, c0);
+        const float f = __fdividef(gscale, v * v);
+        line.move(grad, ix, 1, base);
+        const float f1 = f * ax;
+        line.b0 += f - f1;
+        line.b1 += f1;
+      }
+      line.flush(grad, 1, base);
+    }
+  }
+  if (rg.i_corner < n) {
+    const int px = rp.dfx > 0.f ? W - 1 : 0, py = rp.dfy > 0.f ? H - 1 : 0;
+    const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
+    const float v = v0 + col[py];
+    const float f = __fdividef(gscale, v * v) * static_cast<float>(n - rg.i_corner);
+    if (f != 0.f) atomicAdd(grad + py * W + px, static_cast<double>(f));
+  }
+}
+
+// Generic kernels (plain loads, no texture): one per-step march per ray.
 template <bool TEX>
 __global__ void __launch_bounds__(256) wavefront_kernel(RayArgs a, float* __restrict__ w) {
   extern __shared__ float s_border[];
@@ -139,37 +463,8 @@ __global__ void __launch_bounds__(256) wavefront_kernel(RayArgs a, float* __rest
   double2 c = a.centers[patch];
   Ray ray = make_ray(c.x, c.y, ang, a.n_angles, a.ring_r, a.mcx, a.mcy, a.mr, a.step);
   const RayPix rp = ray_pixels(a, c.x, c.y, ray);
-  const float v0 = static_cast<float>(a.v0);
-  float acc = 0.f;
-  // steps that cannot be in the corner regime: no early exit, unrolled
-  const int i_main = max(0, min(ray.n, rp.i_corner - 2));
-  int i = 0;
-#pragma unroll 4
-  for (; i < i_main; ++i) {
-    Step st = step_at<TEX>(a, bd, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
-                           fmaf(static_cast<float>(i), rp.dfy, rp.fys));
-    acc += st.d / (v0 + st.d);  // (1 - v0/v), v = v0 + d
-  }
-  for (; i < ray.n; ++i) {
-    Step st = step_at<TEX>(a, bd, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
-                           fmaf(static_cast<float>(i), rp.dfy, rp.fys));
-    float term = st.d / (v0 + st.d);
-    if (st.corner) {  // the ray moves outward: every remaining step is identical
-      acc += static_cast<float>(ray.n - i) * term;
-      break;
-    }
-    acc += term;
-  }
+  const float acc = march_forward_generic<TEX>(a, bd, rp, ray.n, static_cast<float>(a.v0));
   w[r] = static_cast<float>(ray.dl) * acc;
-}
-
-__device__ __forceinline__ void flush_cell(double* __restrict__ g, int W, int H, int ix, int iy,
-                                           const double acc[4]) {
-  int ix1 = min(ix + 1, W - 1), iy1 = min(iy + 1, H - 1);
-  if (acc[0] != 0.0) atomicAdd(g + iy * W + ix, acc[0]);
-  if (acc[1] != 0.0) atomicAdd(g + iy * W + ix1, acc[1]);
-  if (acc[2] != 0.0) atomicAdd(g + iy1 * W + ix, acc[2]);
-  if (acc[3] != 0.0) atomicAdd(g + iy1 * W + ix1, acc[3]);
 }
 
 template <bool TEX>
@@ -186,59 +481,8 @@ __global__ void __launch_bounds__(256) ray_backward_kernel(RayArgs a, const floa
   Ray ray = make_ray(c.x, c.y, ang, a.n_angles, a.ring_r, a.mcx, a.mcy, a.mr, a.step);
   if (ray.n == 0) return;
   const RayPix rp = ray_pixels(a, c.x, c.y, ray);
-  const float v0 = static_cast<float>(a.v0);
-  // f = g * dl * v0 / v^2 per step (aberration.hpp:354-355)
   const float gscale = static_cast<float>(static_cast<double>(gr) * ray.dl * a.v0);
-  const int W = a.W;
-  int cx = -1, cy = -1;
-  // accumulators of the current cell's pixels (cx + i, cy + j): a{j}{i}.  A
-  // pixel collects a handful of steps in fp32 before its fp64 flush.
-  float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
-  for (int i = 0; i < ray.n; ++i) {
-    Step st = step_at<TEX>(a, bd, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
-                           fmaf(static_cast<float>(i), rp.dfy, rp.fys));
-    float v = v0 + st.d;
-    float f = gscale / (v * v);
-    const bool corner = st.corner && i >= rp.i_corner - 2;
-    if (corner) f *= static_cast<float>(ray.n - i);  // all remaining steps, same pixel
-    if (st.ix != cx || st.iy != cy) {
-      if (cx >= 0) {
-        // Move to the new cell: pixels shared with it keep accumulating in
-        // registers, the others are flushed (halves the atomics of a
-        // horizontal/vertical move).
-        const int dx = st.ix - cx, dy = st.iy - cy;
-        float n00 = 0.f, n01 = 0.f, n10 = 0.f, n11 = 0.f;
-        const float old[4] = {a00, a01, a10, a11};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int ox = (q & 1) - dx, oy = (q >> 1) - dy;  // old pixel in the new cell
-          const float val = old[q];
-          if (ox >= 0 && ox <= 1 && oy >= 0 && oy <= 1) {
-            const int t = oy * 2 + ox;
-            n00 += t == 0 ? val : 0.f;
-            n01 += t == 1 ? val : 0.f;
-            n10 += t == 2 ? val : 0.f;
-            n11 += t == 3 ? val : 0.f;
-          } else if (val != 0.f) {
-            atomicAdd(grad + (cy + (q >> 1)) * W + cx + (q & 1), static_cast<double>(val));
-          }
-        }
-        a00 = n00;
-        a01 = n01;
-        a10 = n10;
-        a11 = n11;
-      }
-      cx = st.ix;
-      cy = st.iy;
-    }
-    a00 = fmaf(f, st.w00, a00);
-    a01 = fmaf(f, st.w01, a01);
-    a10 = fmaf(f, st.w10, a10);
-    a11 = fmaf(f, st.w11, a11);
-    if (corner) break;
-  }
-  const double fin[4] = {a00, a01, a10, a11};
-  flush_cell(grad, W, a.H, cx, cy, fin);
+  march_backward_generic<TEX>(a, bd, rp, ray.n, static_cast<float>(a.v0), gscale, grad);
 }
 
 }  // namespace
@@ -318,27 +562,27 @@ static Status allow_smem(K kernel, size_t smem) {
 Status launch_wavefront(pact_ctx* ctx, const RayArgs& a, float* w) {
   int blocks = div_up(a.n_rays, 256);
   size_t smem = border_smem(a);
-  if (a.tex) {
-    PACT_TRY_S(allow_smem(wavefront_kernel<true>, smem));
-    wavefront_kernel<true><<<blocks, 256, smem, ctx->stream>>>(a, w);
+  if (a.tex) {  // make_raster_texture requires W, H >= 2
+    PACT_TRY_S(allow_smem(wavefront_split_kernel, smem));
+    wavefront_split_kernel<<<blocks, 256, smem, ctx->stream>>>(a, w);
   } else {
     PACT_TRY_S(allow_smem(wavefront_kernel<false>, smem));
     wavefront_kernel<false><<<blocks, 256, smem, ctx->stream>>>(a, w);
   }
-  return after_launch(ctx, "wavefront_kernel");
+  return after_launch(ctx, a.tex ? "wavefront_split_kernel" : "wavefront_kernel");
 }
 
 Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, double* grad) {
   int blocks = div_up(a.n_rays, 256);
   size_t smem = border_smem(a);
   if (a.tex) {
-    PACT_TRY_S(allow_smem(ray_backward_kernel<true>, smem));
-    ray_backward_kernel<true><<<blocks, 256, smem, ctx->stream>>>(a, dw, grad);
+    PACT_TRY_S(allow_smem(ray_backward_split_kernel, smem));
+    ray_backward_split_kernel<<<blocks, 256, smem, ctx->stream>>>(a, dw, grad);
   } else {
     PACT_TRY_S(allow_smem(ray_backward_kernel<false>, smem));
     ray_backward_kernel<false><<<blocks, 256, smem, ctx->stream>>>(a, dw, grad);
   }
-  return after_launch(ctx, "ray_backward_kernel");
+  return after_launch(ctx, a.tex ? "ray_backward_split_kernel" : "ray_backward_kernel");
 }
 
 // Standalone entry points: a texture over the caller's raster for the
