@@ -21,6 +21,12 @@
 #include "common.cuh"
 #include "geom.cuh"
 
+// RAY_EXP (experiments only, never set in the product build): 1 = interior
+// carries without atomics, 2 = interior without carries.
+#ifndef RAY_EXP
+#define RAY_EXP 0
+#endif
+
 namespace pactgpu {
 
 namespace {
@@ -190,7 +196,7 @@ struct CellAcc {
           n01 += t == 1 ? val : 0.f;
           n10 += t == 2 ? val : 0.f;
           n11 += t == 3 ? val : 0.f;
-        } else if (val != 0.f) {
+        } else if (val != 0.f && RAY_EXP == 0) {
           atomicAdd(grad + (cy + (q >> 1)) * W + cx + (q & 1), static_cast<double>(val));
         }
       }
@@ -283,59 +289,95 @@ __device__ __forceinline__ float interior_d(cudaTextureObject_t tex, float fx, f
   return fmaf(ay, bot - top, top);
 }
 
+// Threads per ray in the split kernels: each ray's steps are cut into SEG
+// contiguous segments of about equal cost (an interior step costs ~2 border
+// steps, corner steps are free), one lane each; the lanes of a ray are
+// adjacent in the warp (forward partial sums are shuffled in a fixed order).
+constexpr int SEG = 1;
+
+struct Segment {
+  int lo, hi;
+};
+
+__device__ __forceinline__ Segment segment_of(const Regimes& rg, int n, int seg) {
+  const int side_end = min(rg.i_corner, n);
+  const int cost = 2 * rg.i_side + (side_end - rg.i_side);
+  auto at_cost = [&](int c) {  // first step index whose cumulative cost reaches c
+    return c <= 2 * rg.i_side ? (c + 1) / 2 : min(side_end, rg.i_side + (c - 2 * rg.i_side));
+  };
+  const int lo = seg == 0 ? 0 : at_cost(cost * seg / SEG);
+  const int hi = seg == SEG - 1 ? n : at_cost(cost * (seg + 1) / SEG);
+  return {lo, hi};
+}
+
 __global__ void __launch_bounds__(256) wavefront_split_kernel(RayArgs a, float* __restrict__ w) {
   extern __shared__ float s_border[];
   const Border bd = load_border(a, s_border);
-  int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= a.n_rays) return;
-  int patch = r / a.n_angles, ang = r - patch * a.n_angles;
-  double2 c = a.centers[patch];
-  Ray ray = make_ray(c.x, c.y, ang, a.n_angles, a.ring_r, a.mcx, a.mcy, a.mr, a.step);
-  const RayPix rp = ray_pixels(a, c.x, c.y, ray);
-  const float v0 = static_cast<float>(a.v0);
-  const int W = a.W, H = a.H, n = ray.n;
-  const float Wm1 = static_cast<float>(W - 1), Hm1 = static_cast<float>(H - 1);
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = t / SEG, seg = t % SEG;
   float acc = 0.f;
-  if (n > 0 && (out_at(0, rp.fxs, rp.dfx, Wm1) || out_at(0, rp.fys, rp.dfy, Hm1))) {
-    acc = march_forward_generic<true>(a, bd, rp, n, v0);
-  } else if (n > 0) {
-    const Regimes rg = regimes(rp, n, Wm1, Hm1);
+  double dl = 0.0;
+  if (r < a.n_rays) {
+    int patch = r / a.n_angles, ang = r - patch * a.n_angles;
+    double2 c = a.centers[patch];
+    Ray ray = make_ray(c.x, c.y, ang, a.n_angles, a.ring_r, a.mcx, a.mcy, a.mr, a.step);
+    dl = ray.dl;
+    const RayPix rp = ray_pixels(a, c.x, c.y, ray);
+    const float v0 = static_cast<float>(a.v0);
+    const int W = a.W, H = a.H, n = ray.n;
+    const float Wm1 = static_cast<float>(W - 1), Hm1 = static_cast<float>(H - 1);
+    if (n > 0 && (out_at(0, rp.fxs, rp.dfx, Wm1) || out_at(0, rp.fys, rp.dfy, Hm1))) {
+      if (seg == 0) acc = march_forward_generic<true>(a, bd, rp, n, v0);
+    } else if (n > 0) {
+      const Regimes rg = regimes(rp, n, Wm1, Hm1);
+      const Segment sg = segment_of(rg, n, seg);
+      const int i1 = min(rg.i_side, sg.hi);
 #pragma unroll 4
-    for (int i = 0; i < rg.i_side; ++i) {
-      float ax, ay;
-      int ix, iy;
-      const float d = interior_d(a.tex, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
-                                 fmaf(static_cast<float>(i), rp.dfy, rp.fys), W, H, ax, ay, ix, iy);
-      acc += __fdividef(d, v0 + d);
-    }
-    if (rg.x_first) {
-      const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
-#pragma unroll 4
-      for (int i = rg.i_side; i < rg.i_corner; ++i) {
-        const float fy = fmaf(static_cast<float>(i), rp.dfy, rp.fys);
-        const int iy = min(static_cast<int>(fy), H - 2);
-        const float c0 = col[iy];
-        const float d = fmaf(fy - iy, col[iy + 1] - c0, c0);
+      for (int i = sg.lo; i < i1; ++i) {
+        float ax, ay;
+        int ix, iy;
+        const float d = interior_d(a.tex, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
+                                   fmaf(static_cast<float>(i), rp.dfy, rp.fys), W, H, ax, ay, ix,
+                                   iy);
         acc += __fdividef(d, v0 + d);
       }
-    } else {
-      const float* row = rp.dfy > 0.f ? bd.rowT : bd.rowB;
+      const int s0 = max(rg.i_side, sg.lo), s1 = min(rg.i_corner, sg.hi);
+      if (rg.x_first) {
+        const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
 #pragma unroll 4
-      for (int i = rg.i_side; i < rg.i_corner; ++i) {
-        const float fx = fmaf(static_cast<float>(i), rp.dfx, rp.fxs);
-        const int ix = min(static_cast<int>(fx), W - 2);
-        const float c0 = row[ix];
-        const float d = fmaf(fx - ix, row[ix + 1] - c0, c0);
-        acc += __fdividef(d, v0 + d);
+        for (int i = s0; i < s1; ++i) {
+          const float fy = fmaf(static_cast<float>(i), rp.dfy, rp.fys);
+          const int iy = min(static_cast<int>(fy), H - 2);
+          const float c0 = col[iy];
+          const float d = fmaf(fy - iy, col[iy + 1] - c0, c0);
+          acc += __fdividef(d, v0 + d);
+        }
+      } else {
+        const float* row = rp.dfy > 0.f ? bd.rowT : bd.rowB;
+#pragma unroll 4
+        for (int i = s0; i < s1; ++i) {
+          const float fx = fmaf(static_cast<float>(i), rp.dfx, rp.fxs);
+          const int ix = min(static_cast<int>(fx), W - 2);
+          const float c0 = row[ix];
+          const float d = fmaf(fx - ix, row[ix + 1] - c0, c0);
+          acc += __fdividef(d, v0 + d);
+        }
       }
-    }
-    if (rg.i_corner < n) {
-      const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
-      const float d = col[rp.dfy > 0.f ? H - 1 : 0];
-      acc += static_cast<float>(n - rg.i_corner) * __fdividef(d, v0 + d);
+      const int n_corner = sg.hi - max(rg.i_corner, sg.lo);
+      if (n_corner > 0) {
+        const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
+        const float d = col[rp.dfy > 0.f ? H - 1 : 0];
+        acc += static_cast<float>(n_corner) * __fdividef(d, v0 + d);
+      }
     }
   }
-  w[r] = static_cast<float>(ray.dl) * acc;
+  // fixed-order sum of the ray's segments (lanes r*SEG .. r*SEG + SEG - 1)
+#pragma unroll
+  for (int o = 1; o < SEG; o <<= 1) {
+    const float other = __shfl_down_sync(0xffffffffu, acc, o, SEG);
+    acc += other;
+  }
+  if (r < a.n_rays && seg == 0) w[r] = static_cast<float>(dl) * acc;
 }
 
 // 1-D carry along a border line: pixels (line position q, q + 1).
@@ -372,7 +414,8 @@ __global__ void __launch_bounds__(256) ray_backward_split_kernel(RayArgs a, cons
                                                                  double* __restrict__ grad) {
   extern __shared__ float s_border[];
   const Border bd = load_border(a, s_border);
-  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = t / SEG, seg = t % SEG;
   if (r >= a.n_rays) return;
   const float gr = dw[r];
   if (gr == 0.f) return;  // aberration.hpp:340
@@ -387,34 +430,56 @@ __global__ void __launch_bounds__(256) ray_backward_split_kernel(RayArgs a, cons
   const int W = a.W, H = a.H, n = ray.n;
   const float Wm1 = static_cast<float>(W - 1), Hm1 = static_cast<float>(H - 1);
   if (out_at(0, rp.fxs, rp.dfx, Wm1) || out_at(0, rp.fys, rp.dfy, Hm1)) {
-    march_backward_generic<true>(a, bd, rp, n, v0, gscale, grad);
+    if (seg == 0) march_backward_generic<true>(a, bd, rp, n, v0, gscale, grad);
     return;
   }
   const Regimes rg = regimes(rp, n, Wm1, Hm1);
+  const Segment sg = segment_of(rg, n, seg);
   {
+    // interior: gathers issued four steps at a time, then the carries
     CellAcc cell;
-    for (int i = 0; i < rg.i_side; ++i) {
-      float ax, ay;
-      int ix, iy;
-      const float d = interior_d(a.tex, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
-                                 fmaf(static_cast<float>(i), rp.dfy, rp.fys), W, H, ax, ay, ix, iy);
-      const float v = v0 + d;
-      const float f = __fdividef(gscale, v * v);
-      cell.move(grad, W, ix, iy);
-      const float fy1 = f * ay, fy0 = f - fy1;  // f (1 - ay), f ay
-      cell.a00 = fmaf(-fy0, ax, cell.a00 + fy0);
-      cell.a01 = fmaf(fy0, ax, cell.a01);
-      cell.a10 = fmaf(-fy1, ax, cell.a10 + fy1);
-      cell.a11 = fmaf(fy1, ax, cell.a11);
+    const int i1 = min(rg.i_side, sg.hi);
+    int i = sg.lo;
+    for (; i < i1; i += 4) {
+      float4 g[4];
+      float ax[4], ay[4];
+      int ix[4], iy[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float fx = fmaf(static_cast<float>(min(i + u, i1 - 1)), rp.dfx, rp.fxs);
+        const float fy = fmaf(static_cast<float>(min(i + u, i1 - 1)), rp.dfy, rp.fys);
+        ix[u] = min(static_cast<int>(fx), W - 2);
+        iy[u] = min(static_cast<int>(fy), H - 2);
+        ax[u] = fx - ix[u];
+        ay[u] = fy - iy[u];
+        g[u] = tex2Dgather<float4>(a.tex, ix[u] + 1.f, iy[u] + 1.f, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i + u < i1) {
+          // gather order: w=(ix,iy) z=(ix+1,iy) x=(ix,iy+1) y=(ix+1,iy+1)
+          const float top = fmaf(ax[u], g[u].z - g[u].w, g[u].w);
+          const float bot = fmaf(ax[u], g[u].y - g[u].x, g[u].x);
+          const float v = v0 + fmaf(ay[u], bot - top, top);
+          const float f = __fdividef(gscale, v * v);
+          if (RAY_EXP != 2) cell.move(grad, W, ix[u], iy[u]);
+          const float fy1 = f * ay[u], fy0 = f - fy1;  // f (1 - ay), f ay
+          cell.a00 = fmaf(-fy0, ax[u], cell.a00 + fy0);
+          cell.a01 = fmaf(fy0, ax[u], cell.a01);
+          cell.a10 = fmaf(-fy1, ax[u], cell.a10 + fy1);
+          cell.a11 = fmaf(fy1, ax[u], cell.a11);
+        }
+      }
     }
     cell.flush(grad, W, H);
   }
-  if (rg.i_side < rg.i_corner) {
+  const int s0 = max(rg.i_side, sg.lo), s1 = min(rg.i_corner, sg.hi);
+  if (s0 < s1) {
     LineAcc line;
     if (rg.x_first) {
       const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
       const int base = rp.dfx > 0.f ? W - 1 : 0;
-      for (int i = rg.i_side; i < rg.i_corner; ++i) {
+      for (int i = s0; i < s1; ++i) {
         const float fy = fmaf(static_cast<float>(i), rp.dfy, rp.fys);
         const int iy = min(static_cast<int>(fy), H - 2);
         const float ay = fy - iy, c0 = col[iy];
@@ -429,7 +494,7 @@ __global__ void __launch_bounds__(256) ray_backward_split_kernel(RayArgs a, cons
     } else {
       const float* row = rp.dfy > 0.f ? bd.rowT : bd.rowB;
       const int base = rp.dfy > 0.f ? (H - 1) * W : 0;
-      for (int i = rg.i_side; i < rg.i_corner; ++i) {
+      for (int i = s0; i < s1; ++i) {
         const float fx = fmaf(static_cast<float>(i), rp.dfx, rp.fxs);
         const int ix = min(static_cast<int>(fx), W - 2);
         const float ax = fx - ix, c0 = row[ix];
@@ -443,11 +508,12 @@ __global__ void __launch_bounds__(256) ray_backward_split_kernel(RayArgs a, cons
       line.flush(grad, 1, base);
     }
   }
-  if (rg.i_corner < n) {
+  const int n_corner = sg.hi - max(rg.i_corner, sg.lo);
+  if (n_corner > 0) {
     const int px = rp.dfx > 0.f ? W - 1 : 0, py = rp.dfy > 0.f ? H - 1 : 0;
     const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
     const float v = v0 + col[py];
-    const float f = __fdividef(gscale, v * v) * static_cast<float>(n - rg.i_corner);
+    const float f = __fdividef(gscale, v * v) * static_cast<float>(n_corner);
     if (f != 0.f) atomicAdd(grad + py * W + px, static_cast<double>(f));
   }
 }
@@ -560,7 +626,7 @@ static Status allow_smem(K kernel, size_t smem) {
 }
 
 Status launch_wavefront(pact_ctx* ctx, const RayArgs& a, float* w) {
-  int blocks = div_up(a.n_rays, 256);
+  int blocks = div_up(a.n_rays * (a.tex ? SEG : 1), 256);
   size_t smem = border_smem(a);
   if (a.tex) {  // make_raster_texture requires W, H >= 2
     PACT_TRY_S(allow_smem(wavefront_split_kernel, smem));
@@ -573,7 +639,7 @@ Status launch_wavefront(pact_ctx* ctx, const RayArgs& a, float* w) {
 }
 
 Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, double* grad) {
-  int blocks = div_up(a.n_rays, 256);
+  int blocks = div_up(a.n_rays * (a.tex ? SEG : 1), 256);
   size_t smem = border_smem(a);
   if (a.tex) {
     PACT_TRY_S(allow_smem(ray_backward_split_kernel, smem));
