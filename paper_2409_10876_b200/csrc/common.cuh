@@ -73,6 +73,13 @@ enum ScratchSlot {
 
 Status scratch_get(pact_ctx* ctx, int slot, size_t bytes, void** out);
 
+// Stream-ordered device memory from the device's default pool, whose release
+// threshold is raised on first use: buffers freed by one trainer / entry point
+// are reused by the next without cudaMalloc / cudaFree (which synchronise the
+// device and, for GB-sized arenas, can stall for many milliseconds).
+Status pool_alloc(void** ptr, size_t bytes, cudaStream_t stream);
+void pool_free(void* ptr, cudaStream_t stream);
+
 // After every launch: count it and surface launch-configuration errors.
 inline Status after_launch(pact_ctx* ctx, const char* name) {
   ctx->launches.fetch_add(1, std::memory_order_relaxed);

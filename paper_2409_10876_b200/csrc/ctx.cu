@@ -1,6 +1,7 @@
 // Context, error and memory entry points of include/pact_cuda.h.
 #include <cmath>
 #include <cstring>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -15,18 +16,34 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+Status pool_alloc(void** ptr, size_t bytes, cudaStream_t stream) {
+  static std::once_flag once[64];
+  int dev = 0;
+  PACT_CUDA_S(cudaGetDevice(&dev));
+  std::call_once(once[dev & 63], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  });
+  PACT_CUDA_S(cudaMallocAsync(ptr, bytes ? bytes : 1, stream));
+  return {};
+}
+
+void pool_free(void* ptr, cudaStream_t stream) {
+  if (ptr) cudaFreeAsync(ptr, stream);
+}
+
 Status scratch_get(pact_ctx* ctx, int slot, size_t bytes, void** out) {
   pact_scratch& s = ctx->scratch[slot];
   if (s.bytes < bytes) {
-    if (s.ptr) {
-      // The previous buffer may still be in use by queued work.
-      PACT_CUDA_S(cudaStreamSynchronize(ctx->stream));
-      PACT_CUDA_S(cudaFree(s.ptr));
-      s.ptr = nullptr;
-      s.bytes = 0;
-    }
+    // stream-ordered: queued work on ctx->stream still sees the old buffer
+    pool_free(s.ptr, ctx->stream);
+    s.ptr = nullptr;
+    s.bytes = 0;
     size_t want = bytes < 256 ? 256 : bytes;
-    PACT_CUDA_S(cudaMalloc(&s.ptr, want));
+    PACT_TRY_S(pool_alloc(&s.ptr, want, ctx->stream));
     s.bytes = want;
   }
   *out = s.ptr;
@@ -75,8 +92,8 @@ int pact_ctx_destroy(pact_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->api && ctx->api_free) ctx->api_free(ctx->api);
-  for (auto& s : ctx->scratch)
-    if (s.ptr) cudaFree(s.ptr);
+  for (auto& s : ctx->scratch) pool_free(s.ptr, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return PACT_OK;

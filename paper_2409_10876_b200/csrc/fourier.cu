@@ -22,7 +22,7 @@
 namespace pactgpu {
 
 void fourier_table_free(FourierTable& t) {
-  if (t.dev) cudaFree(t.dev);
+  pool_free(t.dev, t.stream);
   t.dev = nullptr;
   t.bytes = 0;
   t.P = 0;
@@ -112,12 +112,10 @@ Status fourier_table(pact_ctx* ctx, FourierTable& t, int P, double pitch, int A,
   std::memcpy(host.data() + o_start, start.data(), 4 * (A + 1));
   std::memcpy(host.data() + o_key, key.data(), 16 * P2);
   std::memcpy(host.data() + o_wt, wt.data(), 16 * P2);
-  if (t.dev && t.bytes < total) {
-    PACT_CUDA_S(cudaStreamSynchronize(ctx->stream));
-    fourier_table_free(t);
-  }
+  if (t.dev && t.bytes < total) fourier_table_free(t);
   if (!t.dev) {
-    PACT_CUDA_S(cudaMalloc(&t.dev, total));
+    PACT_TRY_S(pool_alloc(&t.dev, total, ctx->stream));
+    t.stream = ctx->stream;
     t.bytes = total;
   }
   PACT_CUDA_S(cudaMemcpyAsync(t.dev, host.data(), total, cudaMemcpyHostToDevice, ctx->stream));

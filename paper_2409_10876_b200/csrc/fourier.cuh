@@ -29,6 +29,7 @@ struct FourierTable {
   std::vector<double> delays;
   void* dev = nullptr;
   size_t bytes = 0;
+  cudaStream_t stream = nullptr;  // pool stream of `dev`
   FourierTab tab;
 };
 

@@ -624,11 +624,13 @@ Status siren_work_alloc(SirenWork& w, const MaskedPixels& mp, const SirenShape& 
   w.hidden = s.hidden;
   w.layers = s.layers;
   size_t nh = static_cast<size_t>(std::max(1, mp.n)) * s.hidden;
-  PACT_CUDA_S(cudaMalloc(&w.idx, sizeof(int) * std::max(1, mp.n)));
-  PACT_CUDA_S(cudaMalloc(&w.coords, sizeof(float2) * std::max(1, mp.n)));
-  PACT_CUDA_S(cudaMalloc(&w.acts, sizeof(float) * nh * s.layers));
-  PACT_CUDA_S(cudaMalloc(&w.dA, sizeof(float) * nh * 2));
-  PACT_CUDA_S(cudaMalloc(&w.dB, sizeof(float) * nh));
+  w.stream = stream;
+  PACT_TRY_S(pool_alloc(reinterpret_cast<void**>(&w.idx), sizeof(int) * std::max(1, mp.n), stream));
+  PACT_TRY_S(pool_alloc(reinterpret_cast<void**>(&w.coords), sizeof(float2) * std::max(1, mp.n),
+                        stream));
+  PACT_TRY_S(pool_alloc(reinterpret_cast<void**>(&w.acts), sizeof(float) * nh * s.layers, stream));
+  PACT_TRY_S(pool_alloc(reinterpret_cast<void**>(&w.dA), sizeof(float) * nh * 2, stream));
+  PACT_TRY_S(pool_alloc(reinterpret_cast<void**>(&w.dB), sizeof(float) * nh, stream));
   if (mp.n > 0) {
     PACT_CUDA_S(cudaMemcpyAsync(w.idx, mp.idx.data(), sizeof(int) * mp.n, cudaMemcpyHostToDevice,
                                 stream));
@@ -640,22 +642,21 @@ Status siren_work_alloc(SirenWork& w, const MaskedPixels& mp, const SirenShape& 
 }
 
 void siren_work_free(SirenWork& w) {
-  if (w.idx) cudaFree(w.idx);
-  if (w.coords) cudaFree(w.coords);
-  if (w.acts) cudaFree(w.acts);
-  if (w.dA) cudaFree(w.dA);
-  if (w.dB) cudaFree(w.dB);
-  if (w.partial) cudaFree(w.partial);
+  pool_free(w.idx, w.stream);
+  pool_free(w.coords, w.stream);
+  pool_free(w.acts, w.stream);
+  pool_free(w.dA, w.stream);
+  pool_free(w.dB, w.stream);
+  pool_free(w.partial, w.stream);
   w = SirenWork{};
 }
 
 static Status ensure_partial(SirenWork& w, size_t floats, cudaStream_t stream) {
   if (w.partial_floats >= floats) return {};
-  if (w.partial) {
-    PACT_CUDA_S(cudaStreamSynchronize(stream));
-    cudaFree(w.partial);
-  }
-  PACT_CUDA_S(cudaMalloc(&w.partial, sizeof(float) * floats));
+  pool_free(w.partial, stream);
+  w.partial = nullptr;
+  PACT_TRY_S(pool_alloc(reinterpret_cast<void**>(&w.partial), sizeof(float) * floats, stream));
+  w.stream = stream;
   w.partial_floats = floats;
   return {};
 }

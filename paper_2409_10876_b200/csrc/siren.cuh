@@ -46,6 +46,7 @@ struct SirenWork {
   float* dB = nullptr;       // [n][hidden]  backward pong
   float* partial = nullptr;  // split-M weight-gradient partials
   size_t partial_floats = 0;
+  cudaStream_t stream = nullptr;  // pool stream of the buffers
 };
 
 Status siren_work_alloc(SirenWork& w, const MaskedPixels& mp, const SirenShape& s,

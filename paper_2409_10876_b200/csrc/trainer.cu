@@ -297,8 +297,8 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
   add(sizeof(double2) * tr->n_patches);                          // centers
   add(sizeof(float) * P2);                                       // window
   bytes += 64 * 256;  // per-carve alignment slack
-  ce = cudaMalloc(&tr->arena, bytes);
-  if (ce != cudaSuccess) return fail(cuda_status(ce, "trainer arena").code);
+  st = pool_alloc(&tr->arena, bytes, tr->eng.stream);
+  if (!st.ok()) return fail(st.code);
   char* p = static_cast<char*>(tr->arena);
   tr->stack = carve<float>(p, tr->K * npx);
   tr->Y = carve<float2>(p, tr->n_patches * tr->K * P2);
@@ -509,9 +509,9 @@ int pact_trainer_destroy(pact_trainer* tr) {
   if (tr->ray.tex) cudaDestroyTextureObject(tr->ray.tex);
   siren_work_free(tr->sw);
   fourier_table_free(tr->ftab);
-  for (auto& sc : tr->eng.scratch)
-    if (sc.ptr) cudaFree(sc.ptr);
-  if (tr->arena) cudaFree(tr->arena);
+  for (auto& sc : tr->eng.scratch) pool_free(sc.ptr, tr->eng.stream);
+  pool_free(tr->arena, tr->eng.stream);
+  if (tr->eng.stream) cudaStreamSynchronize(tr->eng.stream);
   if (tr->eng.own_stream) cudaStreamDestroy(tr->eng.own_stream);
   delete tr;
   return PACT_OK;
