@@ -40,6 +40,13 @@ Status fourier_table(pact_ctx* ctx, FourierTable& t, int P, double pitch, int A,
   std::vector<float2> frac(P2);
   std::vector<int> mirror(P2, -1);
   std::vector<float2> dp(static_cast<size_t>(K) * P2);
+  // evenly spaced delays (make_delays, beamform.hpp:113-120): phase recurrence
+  double dd = K > 1 ? (delays[K - 1] - delays[0]) / (K - 1) : 0.0, dmax = 0.0;
+  for (int j = 0; j < K; ++j) dmax = std::max(dmax, std::fabs(delays[j]));
+  bool uniform = K > 1;
+  for (int j = 0; j < K && uniform; ++j)
+    uniform = std::fabs(delays[j] - (delays[0] + j * dd)) <= 1e-12 * (1.0 + dmax);
+  std::vector<float2> rho(P2);
   // PatchBinTable::make, aberration.hpp:373-401
   auto interp = [&](double theta, int& i0, int& i1, double& f) {
     double pos = std::fmod(theta, tau);
@@ -66,6 +73,7 @@ Status fourier_table(pact_ctx* ctx, FourierTable& t, int P, double pitch, int A,
       frac[b] = make_float2(static_cast<float>(f1), static_cast<float>(f2));
       if (P % 2 == 0 && (bx == half || by == half))
         mirror[b] = ((P - by) % P) * P + (P - bx) % P;
+      rho[b] = make_float2(static_cast<float>(std::cos(-k * dd)), static_cast<float>(std::sin(-k * dd)));
       for (int j = 0; j < K; ++j) {
         // make_delay_phases, optimize.hpp:229: polar(1, -|k| d_j)
         double ph = -k * delays[j];
@@ -102,7 +110,7 @@ Status fourier_table(pact_ctx* ctx, FourierTable& t, int P, double pitch, int A,
   size_t o_kmag = 0, o_idx = al(o_kmag + 4 * P2), o_frac = al(o_idx + 16 * P2),
          o_mirror = al(o_frac + 8 * P2), o_dp = al(o_mirror + 4 * P2),
          o_start = al(o_dp + 8 * static_cast<size_t>(K) * P2), o_key = al(o_start + 4 * (A + 1)),
-         o_wt = al(o_key + 16 * P2), total = al(o_wt + 16 * P2);
+         o_wt = al(o_key + 16 * P2), o_rho = al(o_wt + 16 * P2), total = al(o_rho + 8 * P2);
   std::vector<char> host(total, 0);
   std::memcpy(host.data() + o_kmag, kmag.data(), 4 * P2);
   std::memcpy(host.data() + o_idx, idx.data(), 16 * P2);
@@ -112,6 +120,7 @@ Status fourier_table(pact_ctx* ctx, FourierTable& t, int P, double pitch, int A,
   std::memcpy(host.data() + o_start, start.data(), 4 * (A + 1));
   std::memcpy(host.data() + o_key, key.data(), 16 * P2);
   std::memcpy(host.data() + o_wt, wt.data(), 16 * P2);
+  std::memcpy(host.data() + o_rho, rho.data(), 8 * P2);
   if (t.dev && t.bytes < total) fourier_table_free(t);
   if (!t.dev) {
     PACT_TRY_S(pool_alloc(&t.dev, total, ctx->stream));
@@ -138,6 +147,7 @@ Status fourier_table(pact_ctx* ctx, FourierTable& t, int P, double pitch, int A,
   t.tab.csr_start = reinterpret_cast<const int*>(d + o_start);
   t.tab.csr_key = reinterpret_cast<const int*>(d + o_key);
   t.tab.csr_wt = reinterpret_cast<const float*>(d + o_wt);
+  t.tab.rho = uniform ? reinterpret_cast<const float2*>(d + o_rho) : nullptr;
   return {};
 }
 
@@ -202,6 +212,7 @@ __global__ void transfer_stack_kernel(FourierTab t, const float* __restrict__ w_
 struct BinLoss {
   float2 x;    // X-hat
   float den;   // sum |h|^2 + eps M
+  float inv;   // 1 / den
   float2 G;    // sum conj(r_j) h_j
   float gx;    // Re(G X)
   float wk;    // |k| * scale
@@ -216,9 +227,8 @@ __device__ __forceinline__ float2 bin_grad(const BinLoss& L, float2 h, float2 y,
   float2 g = make_float2(-2.f * L.wk * z.x, 2.f * L.wk * z.y);
   if (implicit && L.den > 0.f) {
     float2 gy = cmul(L.G, y);
-    float inv = 1.f / L.den;
-    g.x += (-2.f * L.wk * gy.x + 4.f * L.wk * L.gx * h.x) * inv;
-    g.y += (-2.f * L.wk * gy.y + 4.f * L.wk * L.gx * h.y) * inv;
+    g.x += (-2.f * L.wk * gy.x + 4.f * L.wk * L.gx * h.x) * L.inv;
+    g.y += (-2.f * L.wk * gy.y + 4.f * L.wk * L.gx * h.y) * L.inv;
   }
   return g;
 }
@@ -247,102 +257,181 @@ __device__ __forceinline__ int nyq_bin(int s, int P) {
   return by * P + half;
 }
 
-// Kernel A of the fused loss: one thread per (patch, bin), grid (patch, bin
-// chunk).  Ordinary bins write their pulled-back (G1, G2); Nyquist bins write
-// their unsymmetrised dL/dH_j to the exchange buffer.  KT > 0: the bin's K
-// spectra are held in registers (loads issued together); KT == 0: runtime K.
-template <int KT>
-__global__ void __launch_bounds__(256, 2) loss_bins_kernel(FourierTab t, const float2* __restrict__ Y_all,
-                                                        const float* __restrict__ w_all, float eps_m,
-                                                        float scale, int implicit,
-                                                        float2* __restrict__ nyq_all,
-                                                        float2* __restrict__ gbuf,
-                                                        double* __restrict__ loss_part) {
-  extern __shared__ float smem[];
-  float* s_w = smem;  // [A]
-  __shared__ double s_red[32];
-  const int patch = blockIdx.x;
+// The per-bin chain of the fused loss (optimize.hpp:275-317) for bin b with
+// its K spectra y(j).  SYM: a Nyquist bin (even P) whose H_j is symmetrised
+// with its conjugate partner m; its unsymmetrised dL/dH_j go to `nyq_out`
+// (the partner's pullback happens in kernel B).  Otherwise (G1, G2) are
+// returned.  Returns the bin's weighted residual energy.
+template <bool SYM, class YF>
+__device__ __forceinline__ double bin_chain(const FourierTab& t, const float* __restrict__ s_w, int b,
+                                            int m, float eps_m, float scale, bool impl, YF y_of,
+                                            float& G1, float& G2, float2* __restrict__ nyq_out) {
   const int K = t.K, P2 = t.P2;
-  for (int a = threadIdx.x; a < t.A; a += blockDim.x) s_w[a] = w_all[patch * t.A + a];
-  __syncthreads();
-  const float2* Y = Y_all + static_cast<size_t>(patch) * K * P2;
-  float2* nyq = nyq_all + static_cast<size_t>(patch) * (2 * t.P - 1) * K;
-  const bool impl = implicit != 0;
-  double value = 0.0;
-  constexpr int KR = KT > 0 ? KT : 1;
-  const int b = blockIdx.y * blockDim.x + threadIdx.x;
-  if (b < P2) {
-    float G1 = 0.f, G2 = 0.f;
-    const int m = t.mirror[b];
-    BinLoss L;
-    L.wk = t.kmag[b] * scale;
-    if (L.wk != 0.f) {
-      float2 e1b, e2b, e1m = {}, e2m = {};
-      bin_phases(t, s_w, b, e1b, e2b);
-      if (m >= 0) bin_phases(t, s_w, m, e1m, e2m);
-      float2 yr[KR];
-      if constexpr (KT > 0) {
-#pragma unroll
-        for (int j = 0; j < KT; ++j)
-          if (j < K) yr[j] = Y[j * P2 + b];
-      }
-      auto for_j = [&](auto&& fn) {
-        if constexpr (KT > 0) {
-#pragma unroll
-          for (int j = 0; j < KT; ++j)
-            if (j < K) fn(j, yr[j]);
-        } else {
-          for (int j = 0; j < K; ++j) fn(j, Y[j * P2 + b]);
-        }
-      };
-      // pass 1: X-hat = num / den
-      float2 num = make_float2(0.f, 0.f);
-      float den = eps_m;
-      for_j([&](int j, float2 y) {
-        float2 h = h_sym(t, j, b, m, e1b, e2b, e1m, e2m);
-        float2 c = cmulc(h, y);
-        num.x += c.x;
-        num.y += c.y;
-        den += h.x * h.x + h.y * h.y;
-      });
-      L.den = den;
-      L.x = den > 0.f ? make_float2(num.x / den, num.y / den) : make_float2(0.f, 0.f);
-      // G = sum_j conj(r_j) h_j = conj(num) - conj(X) sum|h_j|^2 = conj(num) eps M / den
-      // (optimize.hpp:287-294; closed form, no cancellation)
-      L.G = den > 0.f ? make_float2(num.x * (eps_m / den), -num.y * (eps_m / den))
-                      : make_float2(0.f, 0.f);
-      L.gx = L.G.x * L.x.x - L.G.y * L.x.y;
-      // pass 2: residuals (the loss) and dL/dH; ordinary bins pull back now,
-      // Nyquist bins wait for their partner (symmetrisation, optimize.hpp:306-308)
-      const float k = t.kmag[b];
-      float acc = 0.f;
-      for_j([&](int j, float2 y) {
-        float2 h = h_sym(t, j, b, m, e1b, e2b, e1m, e2m);
-        float2 hx = cmul(h, L.x);
-        float2 r = make_float2(y.x - hx.x, y.y - hx.y);
-        acc += r.x * r.x + r.y * r.y;
-        float2 g = bin_grad(L, h, y, impl);
-        if (m < 0)
-          pullback(g, t.dp[j * P2 + b], e1b, e2b, k, G1, G2);
-        else
-          nyq[nyq_slot(b, t.P) * K + j] = g;
-      });
-      value += static_cast<double>(L.wk) * acc;
-    } else if (m >= 0) {
-      for (int j = 0; j < K; ++j) nyq[nyq_slot(b, t.P) * K + j] = make_float2(0.f, 0.f);
-    }
-    if (m < 0) gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G1, G2);
+  G1 = G2 = 0.f;
+  BinLoss L;
+  L.wk = t.kmag[b] * scale;
+  if (L.wk == 0.f) {
+    if (SYM)
+      for (int j = 0; j < K; ++j) nyq_out[j] = make_float2(0.f, 0.f);
+    return 0.0;
   }
-  // deterministic block reduction of this chunk's loss
+  float2 e1b, e2b, e1m = {}, e2m = {};
+  bin_phases(t, s_w, b, e1b, e2b);
+  if (SYM) bin_phases(t, s_w, m, e1m, e2m);
+  // delay phases dp_j at b (and m): the recurrence dp_{j+1} = dp_j rho for
+  // evenly spaced delays, table loads otherwise
+  const bool walk = t.rho != nullptr;
+  const float2 rb = walk ? t.rho[b] : make_float2(1.f, 0.f);
+  const float2 rm = SYM && walk ? t.rho[m] : make_float2(1.f, 0.f);
+  const float2 db0 = t.dp[b], dm0 = SYM ? t.dp[m] : make_float2(1.f, 0.f);
+  auto next = [&](int j, float2& db, float2& dm) {  // phases of delay j + 1
+    if (walk) {
+      db = cmul(db, rb);
+      if (SYM) dm = cmul(dm, rm);
+    } else if (j + 1 < K) {
+      db = t.dp[(j + 1) * P2 + b];
+      if (SYM) dm = t.dp[(j + 1) * P2 + m];
+    }
+  };
+  // h_j = (t1 + t2) / 2, t1 = dp e1, t2 = conj(dp) e2 (optimize.hpp:270-271)
+  auto h_at = [&](float2 db, float2 dm, float2& t1, float2& t2) {
+    t1 = cmul(db, e1b);
+    t2 = cmul(conjf2(db), e2b);
+    float2 hb = make_float2(0.5f * (t1.x + t2.x), 0.5f * (t1.y + t2.y));
+    if (!SYM) return hb;
+    float2 hm = h_of(dm, e1m, e2m);
+    return make_float2(0.5f * (hb.x + hm.x), 0.5f * (hb.y - hm.y));  // (h_b + conj h_m)/2
+  };
+  // pass 1: X-hat = num / den
+  float2 num = make_float2(0.f, 0.f);
+  float den = eps_m;
+  {
+    float2 db = db0, dm = dm0;
+#pragma unroll 4
+    for (int j = 0; j < K; ++j) {
+      float2 t1, t2;
+      const float2 h = h_at(db, dm, t1, t2);
+      const float2 c = cmulc(h, y_of(j));
+      num.x += c.x;
+      num.y += c.y;
+      den += h.x * h.x + h.y * h.y;
+      next(j, db, dm);
+    }
+  }
+  L.den = den;
+  L.inv = den > 0.f ? 1.f / den : 0.f;
+  L.x = make_float2(num.x * L.inv, num.y * L.inv);
+  // G = sum_j conj(r_j) h_j = conj(num) - conj(X) sum|h_j|^2 = conj(num) eps M / den
+  // (optimize.hpp:287-294; closed form, no cancellation)
+  L.G = make_float2(num.x * (eps_m * L.inv), -num.y * (eps_m * L.inv));
+  L.gx = L.G.x * L.x.x - L.G.y * L.x.y;
+  // pass 2: residuals (the loss) and dL/dH, pulled back through t1, t2
+  // (optimize.hpp:296-317)
+  const float hk = 0.5f * t.kmag[b];
+  float acc = 0.f;
+  {
+    float2 db = db0, dm = dm0;
+#pragma unroll 4
+    for (int j = 0; j < K; ++j) {
+      float2 t1, t2;
+      const float2 h = h_at(db, dm, t1, t2);
+      const float2 y = y_of(j);
+      const float2 hx = cmul(h, L.x);
+      const float2 r = make_float2(y.x - hx.x, y.y - hx.y);
+      acc += r.x * r.x + r.y * r.y;
+      const float2 g = bin_grad(L, h, y, impl);
+      if (SYM) {
+        nyq_out[j] = g;
+      } else {
+        G1 += hk * (g.y * t1.x - g.x * t1.y);
+        G2 += hk * (g.x * t2.y - g.y * t2.x);
+      }
+      next(j, db, dm);
+    }
+  }
+  return static_cast<double>(L.wk) * acc;
+}
+
+__device__ __forceinline__ void block_sum_store(double value, double* s_red, double* out) {
   for (int o = 16; o > 0; o >>= 1) value += __shfl_xor_sync(0xffffffffu, value, o);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = value;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    int nw = blockDim.x >> 5;
-    double v = threadIdx.x < nw ? s_red[threadIdx.x] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) loss_part[patch * gridDim.y + blockIdx.y] = v;
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) v += s_red[q];
+    *out = v;
   }
+}
+
+// Kernel A of the fused loss: ordinary bins, one thread per (patch, bin),
+// grid (patch, bin chunk of LB).  The chunk's K spectra are staged in shared
+// memory with coalesced 16-B loads ([j][bin], conflict free), so the passes
+// over the delays are rolled loops.  Nyquist bins are skipped here (their
+// lanes idle) and handled by kernel A'.
+constexpr int LB = 128;
+
+__global__ void __launch_bounds__(LB) loss_bins_kernel(FourierTab t, const float2* __restrict__ Y_all,
+                                                       const float* __restrict__ w_all, float eps_m,
+                                                       float scale, int implicit,
+                                                       float2* __restrict__ gbuf,
+                                                       double* __restrict__ loss_part, int n_parts) {
+  extern __shared__ __align__(16) float smem[];
+  const int K = t.K, P2 = t.P2;
+  float2* s_y = reinterpret_cast<float2*>(smem);  // [K][LB]
+  float* s_w = smem + 2 * K * LB;                 // [A]
+  __shared__ double s_red[LB / 32];
+  const int patch = blockIdx.x, b0 = blockIdx.y * LB;
+  const float2* Y = Y_all + static_cast<size_t>(patch) * K * P2;
+  for (int a = threadIdx.x; a < t.A; a += LB) s_w[a] = w_all[patch * t.A + a];
+  const int nb = min(LB, P2 - b0);
+  if (nb == LB) {
+    for (int e = threadIdx.x; e < K * LB / 2; e += LB) {
+      const int j = e / (LB / 2), q = e - j * (LB / 2);
+      reinterpret_cast<float4*>(s_y)[e] =
+          reinterpret_cast<const float4*>(Y + static_cast<size_t>(j) * P2 + b0)[q];
+    }
+  } else {
+    for (int e = threadIdx.x; e < K * LB; e += LB) {
+      const int j = e / LB, q = e - j * LB;
+      s_y[e] = q < nb ? Y[static_cast<size_t>(j) * P2 + b0 + q] : make_float2(0.f, 0.f);
+    }
+  }
+  __syncthreads();
+  double value = 0.0;
+  const int b = b0 + threadIdx.x;
+  if (b < P2 && t.mirror[b] < 0) {
+    float G1, G2;
+    const float2* yb = s_y + threadIdx.x;
+    value = bin_chain<false>(t, s_w, b, -1, eps_m, scale, implicit != 0,
+                             [&](int j) { return yb[j * LB]; }, G1, G2, nullptr);
+    gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G1, G2);
+  }
+  block_sum_store(value, s_red, loss_part + patch * n_parts + blockIdx.y);
+}
+
+// Kernel A': the Nyquist bins (even P), one thread per exchange slot.
+__global__ void __launch_bounds__(LB) loss_nyquist_kernel(FourierTab t, const float2* __restrict__ Y_all,
+                                                          const float* __restrict__ w_all,
+                                                          float eps_m, float scale, int implicit,
+                                                          float2* __restrict__ nyq_all,
+                                                          double* __restrict__ loss_part,
+                                                          int n_parts, int part0) {
+  extern __shared__ float s_w[];  // [A]
+  __shared__ double s_red[LB / 32];
+  const int patch = blockIdx.x, K = t.K, P2 = t.P2;
+  for (int a = threadIdx.x; a < t.A; a += LB) s_w[a] = w_all[patch * t.A + a];
+  __syncthreads();
+  const float2* Y = Y_all + static_cast<size_t>(patch) * K * P2;
+  const int slot = blockIdx.y * LB + threadIdx.x;
+  double value = 0.0;
+  if (slot < 2 * t.P - 1) {
+    const int b = nyq_bin(slot, t.P);
+    float G1, G2;
+    value = bin_chain<true>(t, s_w, b, t.mirror[b], eps_m, scale, implicit != 0,
+                            [&](int j) { return Y[static_cast<size_t>(j) * P2 + b]; }, G1, G2,
+                            nyq_all + (static_cast<size_t>(patch) * (2 * t.P - 1) + slot) * K);
+  }
+  block_sum_store(value, s_red, loss_part + patch * n_parts + part0 + blockIdx.y);
 }
 
 // Kernel B: per patch, the Nyquist bins' symmetrised pullback
@@ -438,29 +527,35 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
                         int n_patches, double eps, double scale, bool implicit, double* loss,
                         float* dw) {
   const size_t smem = sizeof(float) * t.A;
-  const int chunks = div_up(t.P2, 256);
+  const int chunks = div_up(t.P2, LB);
+  const int nyq_chunks = t.P % 2 == 0 ? div_up(2 * t.P - 1, LB) : 0;
+  const int n_parts = chunks + nyq_chunks;  // per-patch loss partials, summed in order
   // scratch: Nyquist dL/dH exchange [patch][2P-1][K] | (G1, G2) [patch][P2] | chunk losses
   const size_t n_nyq = static_cast<size_t>(n_patches) * (2 * t.P) * t.K;
   const size_t n_g = static_cast<size_t>(n_patches) * t.P2;
   void* base = nullptr;
   PACT_TRY_S(scratch_get(ctx, kScratchNyq,
-                         sizeof(float2) * (n_nyq + n_g) + sizeof(double) * n_patches * chunks + 256,
+                         sizeof(float2) * (n_nyq + n_g) + sizeof(double) * n_patches * n_parts + 256,
                          &base));
   float2* nyq = static_cast<float2*>(base);
   float2* gbuf = nyq + n_nyq;
   double* part = reinterpret_cast<double*>(gbuf + n_g);
   const float eps_m = static_cast<float>(eps * t.K), sc = static_cast<float>(scale);
-  dim3 grid(n_patches, chunks);
-  if (t.K <= 8)
-    loss_bins_kernel<8><<<grid, 256, smem, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, nyq, gbuf, part);
-  else if (t.K <= 16)
-    loss_bins_kernel<16><<<grid, 256, smem, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, nyq, gbuf, part);
-  else if (t.K <= 32)
-    loss_bins_kernel<32><<<grid, 256, smem, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, nyq, gbuf, part);
-  else
-    loss_bins_kernel<0><<<grid, 256, smem, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, nyq, gbuf, part);
+  const size_t smem_bins = sizeof(float2) * t.K * LB + smem;
+  if (smem_bins > 48 * 1024) {
+    if (smem_bins > 200 * 1024) return validation("fused loss: too many delays for one bin chunk");
+    PACT_CUDA_S(cudaFuncSetAttribute(loss_bins_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem_bins)));
+  }
+  loss_bins_kernel<<<dim3(n_patches, chunks), LB, smem_bins, ctx->stream>>>(
+      t, Y, w, eps_m, sc, implicit, gbuf, part, n_parts);
   PACT_TRY_S(after_launch(ctx, "loss_bins_kernel"));
-  loss_finish_kernel<<<n_patches, 256, smem, ctx->stream>>>(t, w, sc, nyq, gbuf, part, chunks, loss,
+  if (nyq_chunks > 0) {
+    loss_nyquist_kernel<<<dim3(n_patches, nyq_chunks), LB, smem, ctx->stream>>>(
+        t, Y, w, eps_m, sc, implicit, nyq, part, n_parts, chunks);
+    PACT_TRY_S(after_launch(ctx, "loss_nyquist_kernel"));
+  }
+  loss_finish_kernel<<<n_patches, 256, smem, ctx->stream>>>(t, w, sc, nyq, gbuf, part, n_parts, loss,
                                                              dw);
   return after_launch(ctx, "loss_finish_kernel");
 }

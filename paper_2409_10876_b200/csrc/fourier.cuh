@@ -17,6 +17,8 @@ struct FourierTab {
   const float2* frac = nullptr;   // [P2] (f1, f2)
   const int* mirror = nullptr;    // [P2] conjugate partner for Nyquist bins, -1 otherwise
   const float2* dp = nullptr;     // [K][P2] exp(-i |k| d_j)
+  const float2* rho = nullptr;    // [P2] exp(-i |k| (d_1 - d_0)) for evenly spaced delays, else null:
+                                  // dp_j = dp_0 rho^j is then walked in registers
   const int* csr_start = nullptr; // [A+1] angle -> contributions
   const int* csr_key = nullptr;   // [4 P2] (bin << 1) | (0: via w1, 1: via w2)
   const float* csr_wt = nullptr;  // [4 P2] interpolation weight
