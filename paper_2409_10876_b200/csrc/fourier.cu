@@ -385,10 +385,19 @@ __global__ void __launch_bounds__(LB) loss_bins_kernel(FourierTab t, const float
   for (int a = threadIdx.x; a < t.A; a += LB) s_w[a] = w_all[patch * t.A + a];
   const int nb = min(LB, P2 - b0);
   if (nb == LB) {
-    for (int e = threadIdx.x; e < K * LB / 2; e += LB) {
-      const int j = e / (LB / 2), q = e - j * (LB / 2);
-      reinterpret_cast<float4*>(s_y)[e] =
-          reinterpret_cast<const float4*>(Y + static_cast<size_t>(j) * P2 + b0)[q];
+    // K * LB / 2 float4 of the chunk, eight loads in flight per thread
+    for (int e0 = threadIdx.x; e0 < K * LB / 2; e0 += 8 * LB) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * LB, j = e / (LB / 2), q = e - j * (LB / 2);
+        v[u] = e < K * LB / 2
+                   ? reinterpret_cast<const float4*>(Y + static_cast<size_t>(j) * P2 + b0)[q]
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (e0 + u * LB < K * LB / 2) reinterpret_cast<float4*>(s_y)[e0 + u * LB] = v[u];
     }
   } else {
     for (int e = threadIdx.x; e < K * LB; e += LB) {
@@ -409,78 +418,100 @@ __global__ void __launch_bounds__(LB) loss_bins_kernel(FourierTab t, const float
   block_sum_store(value, s_red, loss_part + patch * n_parts + blockIdx.y);
 }
 
-// Kernel A': the Nyquist bins (even P), one thread per exchange slot.
-__global__ void __launch_bounds__(LB) loss_nyquist_kernel(FourierTab t, const float2* __restrict__ Y_all,
-                                                          const float* __restrict__ w_all,
-                                                          float eps_m, float scale, int implicit,
-                                                          float2* __restrict__ nyq_all,
-                                                          double* __restrict__ loss_part,
-                                                          int n_parts, int part0) {
-  extern __shared__ float s_w[];  // [A]
-  __shared__ double s_red[LB / 32];
-  const int patch = blockIdx.x, K = t.K, P2 = t.P2;
-  for (int a = threadIdx.x; a < t.A; a += LB) s_w[a] = w_all[patch * t.A + a];
-  __syncthreads();
+// Kernel A': the Nyquist bins (even P), one block per patch, one thread per
+// exchange slot (2P - 1 of them).  Each slot's unsymmetrised dL/dH_j goes to
+// the exchange buffer; after the barrier every slot pulls back the
+// symmetrised g = (dL/dH_b + conj(dL/dH_m)) / 2 (optimize.hpp:306-308).
+__global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const float2* __restrict__ Y_all,
+                                                            const float* __restrict__ w_all,
+                                                            float eps_m, float scale, int implicit,
+                                                            float2* __restrict__ nyq_all,
+                                                            float2* __restrict__ gbuf,
+                                                            double* __restrict__ loss_part,
+                                                            int n_parts, int part0) {
+  extern __shared__ __align__(16) float smem[];
+  __shared__ double s_red[32];
+  const int patch = blockIdx.x, K = t.K, P2 = t.P2, S = 2 * t.P - 1;
+  float* s_w = smem;                                              // [A]
+  float2* s_y = reinterpret_cast<float2*>(smem + ((t.A + 1) & ~1));  // [K][S]
+  float2* s_g = s_y + K * S;                                         // [S][K] exchange
+  for (int a = threadIdx.x; a < t.A; a += blockDim.x) s_w[a] = w_all[patch * t.A + a];
   const float2* Y = Y_all + static_cast<size_t>(patch) * K * P2;
-  const int slot = blockIdx.y * LB + threadIdx.x;
+  // the slots' spectra, eight loads in flight per thread
+  for (int e0 = threadIdx.x; e0 < K * S; e0 += 8 * blockDim.x) {
+    float2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      const int j = e / S, q = e - j * S;
+      v[u] = e < K * S ? Y[static_cast<size_t>(j) * P2 + nyq_bin(q, t.P)] : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (e0 + u * blockDim.x < K * S) s_y[e0 + u * blockDim.x] = v[u];
+  }
+  __syncthreads();
+  const int slot = threadIdx.x;
   double value = 0.0;
-  if (slot < 2 * t.P - 1) {
-    const int b = nyq_bin(slot, t.P);
+  int b = -1;
+  if (slot < S) {
+    b = nyq_bin(slot, t.P);
     float G1, G2;
     value = bin_chain<true>(t, s_w, b, t.mirror[b], eps_m, scale, implicit != 0,
-                            [&](int j) { return Y[static_cast<size_t>(j) * P2 + b]; }, G1, G2,
-                            nyq_all + (static_cast<size_t>(patch) * (2 * t.P - 1) + slot) * K);
+                            [&](int j) { return s_y[j * S + slot]; }, G1, G2,
+                            s_g + static_cast<size_t>(slot) * K);
   }
-  block_sum_store(value, s_red, loss_part + patch * n_parts + part0 + blockIdx.y);
+  block_sum_store(value, s_red, loss_part + patch * n_parts + part0);
+  __syncthreads();  // the exchange buffer of every slot is complete
+  if (slot < S) {
+    const int sm = nyq_slot(t.mirror[b], t.P);
+    float G1 = 0.f, G2 = 0.f;
+    const float k = t.kmag[b];
+    if (k * scale != 0.f) {
+      float2 e1b, e2b;
+      bin_phases(t, s_w, b, e1b, e2b);
+      const bool walk = t.rho != nullptr;
+      const float2 rb = walk ? t.rho[b] : make_float2(1.f, 0.f);
+      float2 db = t.dp[b];
+#pragma unroll 4
+      for (int j = 0; j < K; ++j) {
+        float2 gb = s_g[slot * K + j], gm = s_g[sm * K + j];
+        float2 gs = make_float2(0.5f * (gb.x + gm.x), 0.5f * (gb.y - gm.y));
+        pullback(gs, db, e1b, e2b, k, G1, G2);
+        if (walk)
+          db = cmul(db, rb);
+        else if (j + 1 < K)
+          db = t.dp[(j + 1) * P2 + b];
+      }
+    }
+    gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G1, G2);
+  }
 }
 
-// Kernel B: per patch, the Nyquist bins' symmetrised pullback
-// g = (dL/dH_b + conj(dL/dH_m)) / 2, the per-angle gather of dL/dw through the
-// static CSR table, and the fixed-order sum of the chunk losses.
-__global__ void __launch_bounds__(256) loss_finish_kernel(FourierTab t, const float* __restrict__ w_all,
-                                                          float scale,
-                                                          const float2* __restrict__ nyq_all,
-                                                          float2* __restrict__ gbuf,
+// Kernel B: dL/dw by the per-angle gather through the static CSR table (one
+// warp per angle, fixed-order shuffle sum) and the fixed-order sum of the
+// per-patch loss partials.  grid (patch, ceil(A / 8)), 256 threads.
+__global__ void __launch_bounds__(256) loss_finish_kernel(FourierTab t, const float2* __restrict__ gbuf,
                                                           const double* __restrict__ loss_part,
-                                                          int n_chunks, double* __restrict__ loss_out,
+                                                          int n_parts, double* __restrict__ loss_out,
                                                           float* __restrict__ dw_out) {
-  extern __shared__ float s_w[];  // [A]
-  const int patch = blockIdx.x;
-  const int K = t.K, P2 = t.P2;
-  for (int a = threadIdx.x; a < t.A; a += blockDim.x) s_w[a] = w_all[patch * t.A + a];
-  __syncthreads();
-  float2* g = gbuf + static_cast<size_t>(patch) * P2;
-  if (t.P % 2 == 0) {
-    const float2* nyq = nyq_all + static_cast<size_t>(patch) * (2 * t.P - 1) * K;
-    for (int s = threadIdx.x; s < 2 * t.P - 1; s += blockDim.x) {
-      const int b = nyq_bin(s, t.P), sm = nyq_slot(t.mirror[b], t.P);
-      float G1 = 0.f, G2 = 0.f;
-      const float k = t.kmag[b];
-      if (k * scale != 0.f) {
-        float2 e1b, e2b;
-        bin_phases(t, s_w, b, e1b, e2b);
-        for (int j = 0; j < K; ++j) {
-          float2 gb = nyq[s * K + j], gm = nyq[sm * K + j];
-          float2 gs = make_float2(0.5f * (gb.x + gm.x), 0.5f * (gb.y - gm.y));
-          pullback(gs, t.dp[j * P2 + b], e1b, e2b, k, G1, G2);
-        }
-      }
-      g[b] = make_float2(G1, G2);
-    }
-  }
-  __syncthreads();
-  for (int a = threadIdx.x; a < t.A; a += blockDim.x) {
+  const int patch = blockIdx.x, lane = threadIdx.x & 31;
+  const int a = blockIdx.y * 8 + (threadIdx.x >> 5);
+  const float2* g = gbuf + static_cast<size_t>(patch) * t.P2;
+  if (a < t.A) {
     float acc = 0.f;
-    for (int e = t.csr_start[a]; e < t.csr_start[a + 1]; ++e) {
-      int key = t.csr_key[e];
-      float2 v = g[key >> 1];
+    const int e1 = t.csr_start[a + 1];
+    for (int e = t.csr_start[a] + lane; e < e1; e += 32) {
+      const int key = t.csr_key[e];
+      const float2 v = g[key >> 1];
       acc += t.csr_wt[e] * ((key & 1) ? v.y : v.x);
     }
-    dw_out[patch * t.A + a] = acc;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) dw_out[patch * t.A + a] = acc;
   }
-  if (threadIdx.x == 0) {
+  if (blockIdx.y == 0 && threadIdx.x == 0) {
     double v = 0.0;
-    for (int c = 0; c < n_chunks; ++c) v += loss_part[patch * n_chunks + c];
+    for (int c = 0; c < n_parts; ++c) v += loss_part[patch * n_parts + c];
     loss_out[patch] = v;
   }
 }
@@ -528,7 +559,7 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
                         float* dw) {
   const size_t smem = sizeof(float) * t.A;
   const int chunks = div_up(t.P2, LB);
-  const int nyq_chunks = t.P % 2 == 0 ? div_up(2 * t.P - 1, LB) : 0;
+  const int nyq_chunks = t.P % 2 == 0 ? 1 : 0;
   const int n_parts = chunks + nyq_chunks;  // per-patch loss partials, summed in order
   // scratch: Nyquist dL/dH exchange [patch][2P-1][K] | (G1, G2) [patch][P2] | chunk losses
   const size_t n_nyq = static_cast<size_t>(n_patches) * (2 * t.P) * t.K;
@@ -550,13 +581,22 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
   loss_bins_kernel<<<dim3(n_patches, chunks), LB, smem_bins, ctx->stream>>>(
       t, Y, w, eps_m, sc, implicit, gbuf, part, n_parts);
   PACT_TRY_S(after_launch(ctx, "loss_bins_kernel"));
-  if (nyq_chunks > 0) {
-    loss_nyquist_kernel<<<dim3(n_patches, nyq_chunks), LB, smem, ctx->stream>>>(
-        t, Y, w, eps_m, sc, implicit, nyq, part, n_parts, chunks);
+  if (t.P % 2 == 0) {
+    const int S = 2 * t.P - 1, nt = div_up(S, 32) * 32;
+    if (nt > 1024) return validation("fused loss: patch size too large for the Nyquist kernel");
+    const size_t smem_nyq = sizeof(float) * ((t.A + 1) & ~1) + 2 * sizeof(float2) * t.K * S;
+    if (smem_nyq > 48 * 1024) {
+      if (smem_nyq > 200 * 1024) return validation("fused loss: Nyquist set too large");
+      PACT_CUDA_S(cudaFuncSetAttribute(loss_nyquist_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem_nyq)));
+    }
+    loss_nyquist_kernel<<<n_patches, nt, smem_nyq, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, nyq,
+                                                                   gbuf, part, n_parts, chunks);
     PACT_TRY_S(after_launch(ctx, "loss_nyquist_kernel"));
   }
-  loss_finish_kernel<<<n_patches, 256, smem, ctx->stream>>>(t, w, sc, nyq, gbuf, part, n_parts, loss,
-                                                             dw);
+  loss_finish_kernel<<<dim3(n_patches, div_up(t.A, 8)), 256, 0, ctx->stream>>>(t, gbuf, part, n_parts,
+                                                                               loss, dw);
   return after_launch(ctx, "loss_finish_kernel");
 }
 

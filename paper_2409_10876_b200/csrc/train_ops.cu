@@ -53,15 +53,33 @@ __global__ void tv_kernel(const float* __restrict__ v, const unsigned char* __re
 }
 
 // report[0] = data = sum_patch loss; report[1] = tv = lambda * sum partial;
-// report[2] = total.  Raises flag bits for non-finite terms.  One warp.
-__global__ void step_report_kernel(const double* __restrict__ loss_patch, int n_patches,
-                                   const double* __restrict__ tv_partial, int n_tv, double lambda,
-                                   double* __restrict__ report, unsigned* __restrict__ flags) {
+// report[2] = total.  Raises flag bits for non-finite terms.  One block of
+// 256: strided partial sums, then a fixed-order fold (deterministic).
+__global__ void __launch_bounds__(256) step_report_kernel(const double* __restrict__ loss_patch,
+                                                         int n_patches,
+                                                         const double* __restrict__ tv_partial,
+                                                         int n_tv, double lambda,
+                                                         double* __restrict__ report,
+                                                         unsigned* __restrict__ flags) {
+  __shared__ double s_d[8], s_t[8];
+  double d = 0.0, t = 0.0;
+  for (int i = threadIdx.x; i < n_patches; i += blockDim.x) d += loss_patch[i];
+  for (int i = threadIdx.x; i < n_tv; i += blockDim.x) t += tv_partial[i];
+  for (int o = 16; o > 0; o >>= 1) {
+    d += __shfl_xor_sync(0xffffffffu, d, o);
+    t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_d[threadIdx.x >> 5] = d;
+    s_t[threadIdx.x >> 5] = t;
+  }
+  __syncthreads();
   if (threadIdx.x != 0) return;
-  double data = 0.0;
-  for (int i = 0; i < n_patches; ++i) data += loss_patch[i];
-  double tv = 0.0;
-  for (int i = 0; i < n_tv; ++i) tv += tv_partial[i];
+  double data = 0.0, tv = 0.0;
+  for (int w = 0; w < 8; ++w) {
+    data += s_d[w];
+    tv += s_t[w];
+  }
   tv *= lambda;
   report[0] = data;
   report[1] = tv;
@@ -134,7 +152,7 @@ Status launch_tv(pact_ctx* ctx, const float* v, const unsigned char* inmask, con
 Status launch_step_report(pact_ctx* ctx, const double* loss_patch, int n_patches,
                           const double* tv_partial, int n_tv, double lambda, double* report,
                           unsigned* flags) {
-  step_report_kernel<<<1, 32, 0, ctx->stream>>>(loss_patch, n_patches, tv_partial, n_tv, lambda,
+  step_report_kernel<<<1, 256, 0, ctx->stream>>>(loss_patch, n_patches, tv_partial, n_tv, lambda,
                                                 report, flags);
   return after_launch(ctx, "step_report_kernel");
 }
