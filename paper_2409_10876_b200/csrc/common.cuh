@@ -69,6 +69,7 @@ enum ScratchSlot {
   kScratchGeneric3 = 5,
   kScratchTables = 6,
   kScratchNyq = 7,
+  kScratchRayBorder = 8,
 };
 
 Status scratch_get(pact_ctx* ctx, int slot, size_t bytes, void** out);

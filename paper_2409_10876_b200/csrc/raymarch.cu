@@ -386,7 +386,7 @@ struct LineAcc {
   float b0 = 0.f, b1 = 0.f;
   __device__ __forceinline__ void move(double* __restrict__ grad, int nq, int stride, int base) {
     if (nq == q) return;
-    if (q >= 0) {
+    if (q >= 0 && RAY_EXP != 5) {
       if (nq == q + 1) {
         if (b0 != 0.f) atomicAdd(grad + base + q * stride, static_cast<double>(b0));
         b0 = b1;
@@ -410,8 +410,16 @@ struct LineAcc {
   }
 };
 
+// Border deposits: every ray of every patch that leaves the grid deposits on
+// the same 2(W + H) border pixels (and 4 corners), so global atomics there
+// contend.  They go to one of kBorderReplicas copies of the border (by block)
+// and border_reduce_kernel folds the copies into the raster afterwards in a
+// fixed order.  Replica layout: [R][colL H | colR H | rowB W | rowT W].
+constexpr int kBorderReplicas = 32;
+
 __global__ void __launch_bounds__(256) ray_backward_split_kernel(RayArgs a, const float* __restrict__ dw,
-                                                                 double* __restrict__ grad) {
+                                                                 double* __restrict__ grad,
+                                                                 double* __restrict__ border_rep) {
   extern __shared__ float s_border[];
   const Border bd = load_border(a, s_border);
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -476,36 +484,37 @@ __global__ void __launch_bounds__(256) ray_backward_split_kernel(RayArgs a, cons
   const int s0 = max(rg.i_side, sg.lo), s1 = min(rg.i_corner, sg.hi);
   if (s0 < s1) {
     LineAcc line;
+    double* rep = border_rep + static_cast<size_t>(blockIdx.x % kBorderReplicas) * 2 * (W + H);
     if (rg.x_first) {
       const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
-      const int base = rp.dfx > 0.f ? W - 1 : 0;
+      double* dst = rep + (rp.dfx > 0.f ? H : 0);
       for (int i = s0; i < s1; ++i) {
         const float fy = fmaf(static_cast<float>(i), rp.dfy, rp.fys);
         const int iy = min(static_cast<int>(fy), H - 2);
         const float ay = fy - iy, c0 = col[iy];
         const float v = v0 + fmaf(ay, col[iy + 1] - c0, c0);
         const float f = __fdividef(gscale, v * v);
-        line.move(grad, iy, W, base);
+        line.move(dst, iy, 1, 0);
         const float f1 = f * ay;
         line.b0 += f - f1;
         line.b1 += f1;
       }
-      line.flush(grad, W, base);
+      line.flush(dst, 1, 0);
     } else {
       const float* row = rp.dfy > 0.f ? bd.rowT : bd.rowB;
-      const int base = rp.dfy > 0.f ? (H - 1) * W : 0;
+      double* dst = rep + 2 * H + (rp.dfy > 0.f ? W : 0);
       for (int i = s0; i < s1; ++i) {
         const float fx = fmaf(static_cast<float>(i), rp.dfx, rp.fxs);
         const int ix = min(static_cast<int>(fx), W - 2);
         const float ax = fx - ix, c0 = row[ix];
         const float v = v0 + fmaf(ax, row[ix + 1] - c0, c0);
         const float f = __fdividef(gscale, v * v);
-        line.move(grad, ix, 1, base);
+        line.move(dst, ix, 1, 0);
         const float f1 = f * ax;
         line.b0 += f - f1;
         line.b1 += f1;
       }
-      line.flush(grad, 1, base);
+      line.flush(dst, 1, 0);
     }
   }
   const int n_corner = sg.hi - max(rg.i_corner, sg.lo);
@@ -514,8 +523,37 @@ __global__ void __launch_bounds__(256) ray_backward_split_kernel(RayArgs a, cons
     const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
     const float v = v0 + col[py];
     const float f = __fdividef(gscale, v * v) * static_cast<float>(n_corner);
-    if (f != 0.f) atomicAdd(grad + py * W + px, static_cast<double>(f));
+    double* rep = border_rep + static_cast<size_t>(blockIdx.x % kBorderReplicas) * 2 * (W + H);
+    if (f != 0.f) atomicAdd(rep + (px == 0 ? 0 : H) + py, static_cast<double>(f));
   }
+}
+
+// grad[p] += sum over replicas of the slot(s) of border pixel p (fixed order).
+// One thread per border pixel: left / right columns, then the bottom / top
+// rows without their corners.
+__global__ void border_reduce_kernel(const double* __restrict__ rep, int W, int H,
+                                     double* __restrict__ grad) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_in = max(W - 2, 0);
+  if (i >= 2 * H + 2 * n_in) return;
+  int px, py;
+  if (i < 2 * H) {
+    px = i < H ? 0 : W - 1;
+    py = i < H ? i : i - H;
+  } else {
+    const int k = i - 2 * H;
+    px = 1 + (k < n_in ? k : k - n_in);
+    py = k < n_in ? 0 : H - 1;
+  }
+  const int col = px == 0 ? py : (px == W - 1 ? H + py : -1);
+  const int row = py == 0 ? 2 * H + px : (py == H - 1 ? 2 * H + W + px : -1);
+  const size_t stride = 2 * static_cast<size_t>(W + H);
+  double s = 0.0;
+  for (int r = 0; r < kBorderReplicas; ++r) {
+    if (col >= 0) s += rep[r * stride + col];
+    if (row >= 0) s += rep[r * stride + row];
+  }
+  if (s != 0.0) grad[static_cast<size_t>(py) * W + px] += s;
 }
 
 // Generic kernels (plain loads, no texture): one per-step march per ray.
@@ -642,13 +680,23 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
   int blocks = div_up(a.n_rays * (a.tex ? SEG : 1), 256);
   size_t smem = border_smem(a);
   if (a.tex) {
+    const size_t rep_n = static_cast<size_t>(kBorderReplicas) * 2 * (a.W + a.H);
+    void* rep = nullptr;
+    PACT_TRY_S(scratch_get(ctx, kScratchRayBorder, sizeof(double) * rep_n, &rep));
+    PACT_CUDA_S(cudaMemsetAsync(rep, 0, sizeof(double) * rep_n, ctx->stream));
     PACT_TRY_S(allow_smem(ray_backward_split_kernel, smem));
-    ray_backward_split_kernel<<<blocks, 256, smem, ctx->stream>>>(a, dw, grad);
+    ray_backward_split_kernel<<<blocks, 256, smem, ctx->stream>>>(a, dw, grad,
+                                                                   static_cast<double*>(rep));
+    PACT_TRY_S(after_launch(ctx, "ray_backward_split_kernel"));
+    const int nbp = 2 * a.H + 2 * std::max(a.W - 2, 0);
+    border_reduce_kernel<<<div_up(nbp, 256), 256, 0, ctx->stream>>>(static_cast<double*>(rep), a.W,
+                                                                     a.H, grad);
+    return after_launch(ctx, "border_reduce_kernel");
   } else {
     PACT_TRY_S(allow_smem(ray_backward_kernel<false>, smem));
     ray_backward_kernel<false><<<blocks, 256, smem, ctx->stream>>>(a, dw, grad);
   }
-  return after_launch(ctx, a.tex ? "ray_backward_split_kernel" : "ray_backward_kernel");
+  return after_launch(ctx, "ray_backward_kernel");
 }
 
 // Standalone entry points: a texture over the caller's raster for the
