@@ -101,6 +101,20 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+STAGE_KERNEL = {"ray_backward": "ray_backward_split_kernel", "wavefront": "wavefront_split_kernel",
+                "fused_loss": "loss_bins_kernel"}
+
+
+def load_traffic():
+    """Per-launch DRAM bytes of the hot kernels from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
 def dist_env():
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
             int(os.environ.get("LOCAL_RANK", "0")))
@@ -355,19 +369,31 @@ def run_ours(args):
         "tv_report": {"ms": stages["tv_report"]}, "adam": {"ms": stages["adam"]},
     }
     dominant = max(stage_rl, key=lambda k: stage_rl[k]["ms"])
+    traffic = load_traffic()
     if dominant == "siren_fwd+bwd":
         ach = stage_rl[dominant]["achieved_tflops"]
         roofline = {"bound": "tensor", "achieved": ach, "peak": bf16, "unit": "TFLOP/s",
-                    "frac": ach / bf16, "traffic": None, "kernel": "SIREN fwd+bwd (FP32 SIMT GEMMs)",
+                    "frac": ach / bf16, "traffic": None,
+                    "kernel": "SIREN fwd+bwd (tcgen05 3xTF32 layers + SIMT edge layers)",
                     "peak_source": f"{peak_src} bf16 dense sustained",
-                    "fp32_pipe_peak_tflops": FP32_PEAK_TFLOPS,
-                    "frac_of_fp32_pipe": ach / FP32_PEAK_TFLOPS,
-                    "work_model": "6 * MAC_px * masked pixels (SURVEY 8(d)); TF32/BF16 fail parity"}
+                    "work_model": "6 * MAC_px * masked pixels (SURVEY 8(d))"}
     else:
+        kern = STAGE_KERNEL.get(dominant, dominant)
         ach = stage_rl[dominant]["achieved_gbs"]
         roofline = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                    "frac": ach / hbm, "traffic": None, "kernel": dominant,
-                    "peak_source": peak_src, "work_model": "SURVEY 8(d) algorithmic bytes"}
+                    "frac": ach / hbm, "traffic": traffic.get(kern), "kernel": kern,
+                    "peak_source": peak_src,
+                    "work_model": "SURVEY 8(d) algorithmic bytes (16 B per ray step)",
+                    "traffic_source": traffic.get("_source")}
+    # SURVEY 8(d) iteration roofline: sum_k max(B_k / HBM, F_k / peak_k), SIREN at the FP32 pipe
+    model_ms = 1e3 * (max(work["siren_flops"] / (FP32_PEAK_TFLOPS * 1e12), 0.0)
+                      + (work["wavefront_bytes"] + work["ray_backward_bytes"]
+                         + work["fused_loss_bytes"]) / (hbm * 1e9))
+    iter_ms = sum(v["ms"] for v in stage_rl.values())
+    iteration_roofline = {"model_ms": model_ms, "measured_ms": iter_ms, "frac": model_ms / iter_ms,
+                          "model": "SURVEY 8(d): SIREN F at the FP32 FFMA peak + ray and loss bytes "
+                                   "at measured HBM; measured = sum of stage CUDA-event times of "
+                                   "one frame"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -410,6 +436,7 @@ def run_ours(args):
                             f"iterations incl. DAS, spectra, final deconvolution), D2H image+SOS"},
             "gpu_launches": launches,
             "roofline": roofline,
+            "iteration_roofline": iteration_roofline,
             "stages_ms_one_frame": stage_rl,
             "das": {"ms": das_t, "gsamples_per_s": w.das_samples / (das_t * 1e-3) / 1e9,
                     "roofline": {"bound": "hbm", "achieved": das_ach, "peak": hbm, "unit": "GB/s",
