@@ -208,6 +208,38 @@ struct CellAcc {
     cx = ix;
     cy = iy;
   }
+  // Interior move by at most one cell per axis (a step is <= 1 px): the
+  // remap is a fixed select network and the evictions are predicated atomics
+  // (no loop); larger jumps take the general path.
+  __device__ __forceinline__ void move_unit(double* __restrict__ grad, int W, int ix, int iy) {
+    if (ix == cx && iy == cy) return;
+    const int dx = ix - cx, dy = iy - cy;
+    if (cx < 0 || dx < -1 || dx > 1 || dy < -1 || dy > 1) {
+      move(grad, W, ix, iy);
+      return;
+    }
+    // old slot (i, j) [x i, y j] survives iff (i - dx, j - dy) is in the new cell
+    const bool keep_x0 = dx <= 0, keep_x1 = dx >= 0, keep_y0 = dy <= 0, keep_y1 = dy >= 0;
+    if (RAY_EXP == 0) {
+      double* p = grad + cy * W + cx;
+      if (!(keep_x0 && keep_y0) && a00 != 0.f) atomicAdd(p, static_cast<double>(a00));
+      if (!(keep_x1 && keep_y0) && a01 != 0.f) atomicAdd(p + 1, static_cast<double>(a01));
+      if (!(keep_x0 && keep_y1) && a10 != 0.f) atomicAdd(p + W, static_cast<double>(a10));
+      if (!(keep_x1 && keep_y1) && a11 != 0.f) atomicAdd(p + W + 1, static_cast<double>(a11));
+    }
+    // x shift within each old row j: new x0 <- old (dx == 0 ? x0 : dx == 1 ? x1 : none)
+    const float r00 = dx == 0 ? a00 : (dx == 1 ? a01 : 0.f);
+    const float r01 = dx == 0 ? a01 : (dx == -1 ? a00 : 0.f);
+    const float r10 = dx == 0 ? a10 : (dx == 1 ? a11 : 0.f);
+    const float r11 = dx == 0 ? a11 : (dx == -1 ? a10 : 0.f);
+    // then the y shift
+    a00 = dy == 0 ? r00 : (dy == 1 ? r10 : 0.f);
+    a01 = dy == 0 ? r01 : (dy == 1 ? r11 : 0.f);
+    a10 = dy == 0 ? r10 : (dy == -1 ? r00 : 0.f);
+    a11 = dy == 0 ? r11 : (dy == -1 ? r01 : 0.f);
+    cx = ix;
+    cy = iy;
+  }
   __device__ __forceinline__ void flush(double* __restrict__ grad, int W, int H) {
     if (cx < 0) return;
     const double fin[4] = {a00, a01, a10, a11};
@@ -470,7 +502,7 @@ __global__ void __launch_bounds__(256) ray_backward_split_kernel(RayArgs a, cons
           const float bot = fmaf(ax[u], g[u].y - g[u].x, g[u].x);
           const float v = v0 + fmaf(ay[u], bot - top, top);
           const float f = __fdividef(gscale, v * v);
-          if (RAY_EXP != 2) cell.move(grad, W, ix[u], iy[u]);
+          if (RAY_EXP != 2) cell.move_unit(grad, W, ix[u], iy[u]);
           const float fy1 = f * ay[u], fy0 = f - fy1;  // f (1 - ay), f ay
           cell.a00 = fmaf(-fy0, ax[u], cell.a00 + fy0);
           cell.a01 = fmaf(fy0, ax[u], cell.a01);
