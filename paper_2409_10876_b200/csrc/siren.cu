@@ -683,7 +683,15 @@ Status siren_forward(pact_ctx* ctx, const SirenShape& s, const float* theta, Sir
     const float* Ain = w.acts + (l - 1) * stride;
     float* Aout = w.acts + l * stride;
     if (siren_use_tc(H)) {
-      PACT_TRY_S(tc_forward_layer(ctx, H, Ain, W, b, n, w0, Aout));
+      SirenHead head;
+      if (l == L - 1) {  // the output layer rides on the last layer's epilogue
+        head.w = theta + s.offset(L);
+        head.b = head.w + H;
+        head.idx = w.idx;
+        head.dv = dv;
+        head.scale = static_cast<float>(s.out_scale);
+      }
+      PACT_TRY_S(tc_forward_layer(ctx, H, Ain, W, b, n, w0, Aout, head));
       continue;
     }
     if (H == 64) {
@@ -693,6 +701,7 @@ Status siren_forward(pact_ctx* ctx, const SirenShape& s, const float* theta, Sir
     }
     PACT_TRY_S(after_launch(ctx, "siren_fwd_kernel"));
   }
+  if (L >= 2 && siren_use_tc(H)) return {};  // output layer fused (tc_forward_layer)
   const float* wL = theta + s.offset(L);
   siren_out_kernel<<<std::min(div_up(n, 32), ctx->num_sms * 8), 256, 0, st>>>(w.acts + (L - 1) * stride, wL, wL + H,
                                                              w.idx, n, H, w0,

@@ -68,8 +68,17 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
 // SIMT tiles remain for other widths and when PACT_SIREN_SIMT=1.
 bool siren_tc_supported(int hidden);
 bool siren_use_tc(int hidden);
+// Output layer fused into the last forward layer's epilogue (w == null: not fused):
+// dv[idx[m]] = scale * (b[0] + sum_k w[k] sin(w0 a_{L-1}[m][k])).
+struct SirenHead {
+  const float* w = nullptr;
+  const float* b = nullptr;
+  const int* idx = nullptr;
+  float* dv = nullptr;
+  float scale = 0.f;
+};
 Status tc_forward_layer(pact_ctx* ctx, int H, const float* Ain, const float* W, const float* b,
-                        int n, float w0, float* Aout);
+                        int n, float w0, float* Aout, const SirenHead& head);
 Status tc_dgrad_layer(pact_ctx* ctx, int H, const float* dAl, const float* W, const float* Aprev,
                       int n, float w0, float* dAprev);
 int tc_wgrad_rows(pact_ctx* ctx, int n);  // pixels per weight-gradient partial

@@ -81,6 +81,22 @@ __device__ __forceinline__ uint32_t lane_base(uint32_t t0, int warp) {
 // ---- layer kernels (forward, dgrad) ---------------------------------------
 enum Mode { kForward = 0, kDgrad = 1 };
 
+// Lane j of the warp receives sum over the warp's lanes of z[j] (fixed
+// butterfly order: deterministic).  31 shuffles for 32 sums.
+__device__ __forceinline__ float transpose_reduce32(float (&z)[32], int lane) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < off; ++i) {
+      const float send = up ? z[i] : z[i + off];
+      const float keep = up ? z[i + off] : z[i];
+      z[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return z[0];
+}
+
 struct LayerBars {
   uint64_t raw[2];    // raw tile landed (bulk copies)
   uint64_t buf[2];    // chunk planes free (MMA commit)
@@ -101,7 +117,7 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
                 const float* __restrict__ W,      // [H][H] layer matrix, row-major
                 const float* __restrict__ bias,   // forward: [H]
                 const float* __restrict__ Aprev,  // dgrad: a_{l-1} for the cosine
-                int n, float w0, float* __restrict__ Y) {
+                int n, float w0, float* __restrict__ Y, SirenHead head) {
   extern __shared__ unsigned char smem_dyn[];
   // 1024-B alignment: the 128-B swizzle is a function of the address bits
   float* raw = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) &
@@ -110,6 +126,7 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
   float* zl = zh + 2 * TP * KC;                                         // [2][TP][KC] SW128
   float* wst = raw + TP * H;  // prologue only: W staged [H][H + 1] over raw[1] and the planes
   __shared__ LayerBars sb;
+  __shared__ float s_out[2][4][TP];  // fused output layer: per-quarter partial sums
   const int tid = threadIdx.x, warp = tid >> 5;
   const int row = tid & 127;  // TMEM lane of this thread (warp % 4 quarter)
   if (warp == 0) tc::tmem_alloc<512>(&sb.tslot);
@@ -237,6 +254,8 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
     // warps 8-11 and 12-15 share the TMEM lane quarters and split the columns ----
     const float brow = MODE == kForward ? bias[row] : 0.f;
     const int cb = ((warp - LPROD / 32) >> 2) * (TP / 2);
+    const bool fuse_out = MODE == kForward && head.w != nullptr;
+    const float wrow = fuse_out ? head.w[row] : 0.f;
     for (int i = 0; i < my_tiles; ++i) {
       const int m0 = (blockIdx.x + i * gridDim.x) * TP;
       const int rows = min(TP, n - m0);
@@ -260,10 +279,28 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
           const int c = cb + h + j;
           const float out = MODE == kForward ? v[j] + brow : v[j] * dsin_w(av[h + j], w0);
           if (c < rows && (TC_EXP != 3 || out == 12345.f)) y[c * H] = out;
+          v[j] = out;
+        }
+        if (fuse_out) {
+          // output layer w_L . sin(w0 a_{L-1}) (nfield.hpp:126-130): this warp's
+          // 32 features per pixel, lane j <- pixel cb + h + j
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = wrow * sin_w(v[j], w0);
+          const float part = transpose_reduce32(v, tid & 31);
+          s_out[i & 1][warp & 3][cb + h + (tid & 31)] = part;
         }
       }
       tc::fence_before_sync();
       tc::mbar_arrive(&sb.empty[i & 1]);
+      if (fuse_out) {
+        tc::named_sync(2, LNTH - LPROD);
+        const int c = tid - LPROD;
+        if (c < rows) {
+          const float* so = &s_out[i & 1][0][0];
+          const float s = ((so[c] + so[TP + c]) + so[2 * TP + c]) + so[3 * TP + c];
+          head.dv[head.idx[m0 + c]] = head.scale * (head.b[0] + s);
+        }
+      }
     }
   }
   sync_tc();
@@ -435,13 +472,13 @@ int tc_wgrad_rows(pact_ctx* ctx, int n) {
 }
 
 Status tc_forward_layer(pact_ctx* ctx, int hidden, const float* Ain, const float* W,
-                        const float* b, int n, float w0, float* Aout) {
+                        const float* b, int n, float w0, float* Aout, const SirenHead& head) {
   if (hidden != H) return unsupported_width();
   static bool cfg = false;
   if (!cfg) PACT_TRY_S(set_smem(tc_layer_kernel<kForward>, kLayerSmem));
   cfg = true;
   tc_layer_kernel<kForward><<<layer_grid(ctx, n), LNTH, kLayerSmem, ctx->stream>>>(
-      Ain, W, b, nullptr, n, w0, Aout);
+      Ain, W, b, nullptr, n, w0, Aout, head);
   return after_launch(ctx, "tc_layer_kernel<forward>");
 }
 
@@ -452,7 +489,7 @@ Status tc_dgrad_layer(pact_ctx* ctx, int hidden, const float* dAl, const float* 
   if (!cfg) PACT_TRY_S(set_smem(tc_layer_kernel<kDgrad>, kLayerSmem));
   cfg = true;
   tc_layer_kernel<kDgrad><<<layer_grid(ctx, n), LNTH, kLayerSmem, ctx->stream>>>(
-      dAl, W, nullptr, Aprev, n, w0, dAprev);
+      dAl, W, nullptr, Aprev, n, w0, dAprev, SirenHead{});
   return after_launch(ctx, "tc_layer_kernel<dgrad>");
 }
 
