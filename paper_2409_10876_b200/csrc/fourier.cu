@@ -17,6 +17,9 @@
 #include <cmath>
 #include <cstring>
 
+#include <memory>
+#include <mutex>
+
 #include "fourier.cuh"
 
 namespace pactgpu {
@@ -24,15 +27,24 @@ namespace pactgpu {
 void fourier_table_free(FourierTable& t) {
   pool_free(t.dev, t.stream);
   t.dev = nullptr;
+  t.host.reset();
   t.bytes = 0;
   t.P = 0;
 }
 
-Status fourier_table(pact_ctx* ctx, FourierTable& t, int P, double pitch, int A,
-                     const double* delays, int K) {
-  if (t.dev && t.P == P && t.pitch == pitch && t.A == A && t.K == K &&
-      std::equal(t.delays.begin(), t.delays.end(), delays))
-    return {};
+namespace {
+
+// Host image of the tables for (P, pitch, A, delays): one byte buffer with
+// 16-byte aligned sections.  Cached per process (the tables depend only on
+// the layout and the delays), so repeated reconstructions only upload.
+struct HostFourier {
+  std::vector<char> bytes;
+  size_t o_kmag, o_idx, o_frac, o_mirror, o_dp, o_start, o_key, o_wt, o_rho;
+  bool uniform;
+};
+
+std::shared_ptr<const HostFourier> build_host_fourier(int P, double pitch, int A,
+                                                      const double* delays, int K) {
   const int P2 = P * P;
   const double tau = 2.0 * M_PI;
   std::vector<float> kmag(P2);
@@ -111,7 +123,9 @@ Status fourier_table(pact_ctx* ctx, FourierTable& t, int P, double pitch, int A,
          o_mirror = al(o_frac + 8 * P2), o_dp = al(o_mirror + 4 * P2),
          o_start = al(o_dp + 8 * static_cast<size_t>(K) * P2), o_key = al(o_start + 4 * (A + 1)),
          o_wt = al(o_key + 16 * P2), o_rho = al(o_wt + 16 * P2), total = al(o_rho + 8 * P2);
-  std::vector<char> host(total, 0);
+  auto hf = std::make_shared<HostFourier>();
+  std::vector<char>& host = hf->bytes;
+  host.assign(total, 0);
   std::memcpy(host.data() + o_kmag, kmag.data(), 4 * P2);
   std::memcpy(host.data() + o_idx, idx.data(), 16 * P2);
   std::memcpy(host.data() + o_frac, frac.data(), 8 * P2);
@@ -121,14 +135,63 @@ Status fourier_table(pact_ctx* ctx, FourierTable& t, int P, double pitch, int A,
   std::memcpy(host.data() + o_key, key.data(), 16 * P2);
   std::memcpy(host.data() + o_wt, wt.data(), 16 * P2);
   std::memcpy(host.data() + o_rho, rho.data(), 8 * P2);
+  hf->o_kmag = o_kmag;
+  hf->o_idx = o_idx;
+  hf->o_frac = o_frac;
+  hf->o_mirror = o_mirror;
+  hf->o_dp = o_dp;
+  hf->o_start = o_start;
+  hf->o_key = o_key;
+  hf->o_wt = o_wt;
+  hf->o_rho = o_rho;
+  hf->uniform = uniform;
+  return hf;
+}
+
+std::shared_ptr<const HostFourier> host_fourier(int P, double pitch, int A, const double* delays,
+                                                int K) {
+  struct Entry {
+    int P, A;
+    double pitch;
+    std::vector<double> delays;
+    std::shared_ptr<const HostFourier> hf;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Entry& e : cache)
+      if (e.P == P && e.A == A && e.pitch == pitch && static_cast<int>(e.delays.size()) == K &&
+          std::equal(e.delays.begin(), e.delays.end(), delays))
+        return e.hf;
+  }
+  auto hf = build_host_fourier(P, pitch, A, delays, K);
+  std::lock_guard<std::mutex> lock(mu);
+  if (cache.size() >= 4) cache.erase(cache.begin());
+  cache.push_back({P, A, pitch, std::vector<double>(delays, delays + K), hf});
+  return hf;
+}
+
+}  // namespace
+
+Status fourier_table(pact_ctx* ctx, FourierTable& t, int P, double pitch, int A,
+                     const double* delays, int K) {
+  if (t.dev && t.P == P && t.pitch == pitch && t.A == A && t.K == K &&
+      std::equal(t.delays.begin(), t.delays.end(), delays))
+    return {};
+  const auto hf = host_fourier(P, pitch, A, delays, K);
+  const size_t total = hf->bytes.size();
+  const int P2 = P * P;
   if (t.dev && t.bytes < total) fourier_table_free(t);
   if (!t.dev) {
     PACT_TRY_S(pool_alloc(&t.dev, total, ctx->stream));
     t.stream = ctx->stream;
     t.bytes = total;
   }
-  PACT_CUDA_S(cudaMemcpyAsync(t.dev, host.data(), total, cudaMemcpyHostToDevice, ctx->stream));
-  PACT_CUDA_S(cudaStreamSynchronize(ctx->stream));  // `host` goes out of scope
+  // the cached host image outlives the copy (held by the cache and by `t`)
+  PACT_CUDA_S(cudaMemcpyAsync(t.dev, hf->bytes.data(), total, cudaMemcpyHostToDevice,
+                              ctx->stream));
+  t.host = hf;
   char* d = static_cast<char*>(t.dev);
   t.P = P;
   t.A = A;
@@ -139,15 +202,15 @@ Status fourier_table(pact_ctx* ctx, FourierTable& t, int P, double pitch, int A,
   t.tab.P2 = P2;
   t.tab.A = A;
   t.tab.K = K;
-  t.tab.kmag = reinterpret_cast<const float*>(d + o_kmag);
-  t.tab.idx = reinterpret_cast<const int4*>(d + o_idx);
-  t.tab.frac = reinterpret_cast<const float2*>(d + o_frac);
-  t.tab.mirror = reinterpret_cast<const int*>(d + o_mirror);
-  t.tab.dp = reinterpret_cast<const float2*>(d + o_dp);
-  t.tab.csr_start = reinterpret_cast<const int*>(d + o_start);
-  t.tab.csr_key = reinterpret_cast<const int*>(d + o_key);
-  t.tab.csr_wt = reinterpret_cast<const float*>(d + o_wt);
-  t.tab.rho = uniform ? reinterpret_cast<const float2*>(d + o_rho) : nullptr;
+  t.tab.kmag = reinterpret_cast<const float*>(d + hf->o_kmag);
+  t.tab.idx = reinterpret_cast<const int4*>(d + hf->o_idx);
+  t.tab.frac = reinterpret_cast<const float2*>(d + hf->o_frac);
+  t.tab.mirror = reinterpret_cast<const int*>(d + hf->o_mirror);
+  t.tab.dp = reinterpret_cast<const float2*>(d + hf->o_dp);
+  t.tab.csr_start = reinterpret_cast<const int*>(d + hf->o_start);
+  t.tab.csr_key = reinterpret_cast<const int*>(d + hf->o_key);
+  t.tab.csr_wt = reinterpret_cast<const float*>(d + hf->o_wt);
+  t.tab.rho = hf->uniform ? reinterpret_cast<const float2*>(d + hf->o_rho) : nullptr;
   return {};
 }
 

@@ -4,6 +4,7 @@
 // optimize.hpp:223-232).
 #pragma once
 
+#include <memory>
 #include <vector>
 
 #include "common.cuh"
@@ -32,6 +33,7 @@ struct FourierTable {
   void* dev = nullptr;
   size_t bytes = 0;
   cudaStream_t stream = nullptr;  // pool stream of `dev`
+  std::shared_ptr<const void> host;  // host image being uploaded (kept alive)
   FourierTab tab;
 };
 

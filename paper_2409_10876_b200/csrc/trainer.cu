@@ -21,6 +21,21 @@
 #include "siren.cuh"
 #include "train_ops.cuh"
 
+namespace {
+// PACT_TRACE=1: host-side phase timings of trainer creation on stderr.
+struct HostTrace {
+  bool on = std::getenv("PACT_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pact] %-28s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+}  // namespace
+
 namespace pactgpu {
 Status merge_window(double fwhm, int P, double pitch, std::vector<float>& w);
 Status launch_sos_from_dev(pact_ctx* ctx, const float* dv, size_t n, double v0, float* out);
@@ -227,6 +242,7 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
   const double v0 = meta->background_sos;
   if (!(v0 > 0.0)) return validation("joint_reconstruct: non-positive background SOS").code;
 
+  HostTrace trace;
   auto* tr = new pact_trainer();
   tr->user = ctx;
   tr->eng.device = ctx->device;
@@ -271,7 +287,9 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
   std::vector<float> win;
   st = merge_window(cfg->merge_fwhm, tr->P, grid->pitch, win);
   if (!st.ok()) return fail(st.code);
+  trace.mark("layout + window");
   tr->mp = masked_pixels(*grid, *mask);
+  trace.mark("masked pixels");
 
   // ---- device arena ----
   const size_t npx = static_cast<size_t>(grid->width) * grid->height;
@@ -321,6 +339,7 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
   tr->centers = carve<double2>(p, tr->n_patches);
   tr->win = carve<float>(p, P2);
 
+  trace.mark("arena");
   pact_ctx* e = &tr->eng;
   cudaStream_t s = e->stream;
   // inputs produced on the caller's stream must be visible to the engine
@@ -347,6 +366,7 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
     Status _s = (x);                                     \
     if (!_s.ok()) return fail(_s.code);                  \
   } while (0)
+  trace.mark("init_siren + flags");
   TRY_CU(cudaMemcpyAsync(tr->inmask, flag.data(), npx, cudaMemcpyHostToDevice, s));
   TRY_CU(cudaMemcpyAsync(tr->theta, theta.data(), sizeof(double) * tr->n_params,
                          cudaMemcpyHostToDevice, s));
@@ -364,13 +384,18 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
   tr->ray.centers = tr->centers;
   tr->ray.n_rays = tr->n_patches * tr->A;
   make_raster_texture(tr->dv, grid->width, grid->height, &tr->ray.tex);
+  trace.mark("uploads + texture");
   // DAS stack + spectra, once (optimize.hpp:380-392)
   TRY_ST(das_stack_device(e, *ring, *meta, signals, *grid, v0, tr->delays.data(), tr->K,
                           tr->stack));
   TRY_ST(launch_patch_fft(e, tr->lay, tr->stack, tr->K, tr->Y));
+  trace.mark("DAS + FFT launched");
   TRY_ST(siren_work_alloc(tr->sw, tr->mp, tr->shape, s));
+  trace.mark("siren work");
   TRY_ST(fourier_table(e, tr->ftab, tr->P, grid->pitch, tr->A, tr->delays.data(), tr->K));
+  trace.mark("fourier table");
   TRY_CU(cudaStreamSynchronize(s));
+  trace.mark("final sync");
   *out = tr;
   return PACT_OK;
 #undef TRY_CU
