@@ -326,6 +326,20 @@ __device__ __forceinline__ float interior_d(cudaTextureObject_t tex, float fx, f
 // steps, corner steps are free), one lane each; the lanes of a ray are
 // adjacent in the warp (forward partial sums are shuffled in a fixed order).
 constexpr int SEG = 1;
+// Blocks of the split kernels: one wave, evenly loaded.  All rays are
+// resident at once (115k rays at cfg3 vs 148 x 2048 thread slots), so the
+// kernel time is set by the most loaded SM: ceil(n_rays / SMs) rounded to a
+// warp, one block per SM.  (Measured at cfg3: 256-thread blocks leave 4 blocks
+// on some SMs, 0.855 ms; 800-thread blocks 0.820 ms.)  The wavefront pass is
+// fastest with two whole patches (1024 rays) per block when that still fills
+// most SMs (texture-cache locality: 0.252 vs 0.293 ms).
+constexpr int kRayBlockMax = 1024;
+
+int ray_block(const RayArgs& a, int num_sms, bool wavefront) {
+  if (wavefront && a.n_rays >= kRayBlockMax * (num_sms / 2)) return kRayBlockMax;
+  const int per_sm = div_up(a.n_rays, std::max(1, num_sms));
+  return std::min(kRayBlockMax, std::max(256, div_up(per_sm, 32) * 32));
+}
 
 struct Segment {
   int lo, hi;
@@ -342,7 +356,7 @@ __device__ __forceinline__ Segment segment_of(const Regimes& rg, int n, int seg)
   return {lo, hi};
 }
 
-__global__ void __launch_bounds__(256) wavefront_split_kernel(RayArgs a, float* __restrict__ w) {
+__global__ void __launch_bounds__(kRayBlockMax) wavefront_split_kernel(RayArgs a, float* __restrict__ w) {
   extern __shared__ float s_border[];
   const Border bd = load_border(a, s_border);
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -449,7 +463,7 @@ struct LineAcc {
 // fixed order.  Replica layout: [R][colL H | colR H | rowB W | rowT W].
 constexpr int kBorderReplicas = 32;
 
-__global__ void __launch_bounds__(256) ray_backward_split_kernel(RayArgs a, const float* __restrict__ dw,
+__global__ void __launch_bounds__(kRayBlockMax) ray_backward_split_kernel(RayArgs a, const float* __restrict__ dw,
                                                                  double* __restrict__ grad,
                                                                  double* __restrict__ border_rep) {
   extern __shared__ float s_border[];
@@ -696,11 +710,12 @@ static Status allow_smem(K kernel, size_t smem) {
 }
 
 Status launch_wavefront(pact_ctx* ctx, const RayArgs& a, float* w) {
-  int blocks = div_up(a.n_rays * (a.tex ? SEG : 1), 256);
+  int blocks = div_up(a.n_rays, 256);
   size_t smem = border_smem(a);
   if (a.tex) {  // make_raster_texture requires W, H >= 2
     PACT_TRY_S(allow_smem(wavefront_split_kernel, smem));
-    wavefront_split_kernel<<<blocks, 256, smem, ctx->stream>>>(a, w);
+    const int rb = ray_block(a, ctx->num_sms, true);
+    wavefront_split_kernel<<<div_up(a.n_rays * SEG, rb), rb, smem, ctx->stream>>>(a, w);
   } else {
     PACT_TRY_S(allow_smem(wavefront_kernel<false>, smem));
     wavefront_kernel<false><<<blocks, 256, smem, ctx->stream>>>(a, w);
@@ -709,15 +724,17 @@ Status launch_wavefront(pact_ctx* ctx, const RayArgs& a, float* w) {
 }
 
 Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, double* grad) {
-  int blocks = div_up(a.n_rays * (a.tex ? SEG : 1), 256);
+  int blocks = div_up(a.n_rays, 256);
   size_t smem = border_smem(a);
   if (a.tex) {
+    const int rb = ray_block(a, ctx->num_sms, false);
+    blocks = div_up(a.n_rays * SEG, rb);
     const size_t rep_n = static_cast<size_t>(kBorderReplicas) * 2 * (a.W + a.H);
     void* rep = nullptr;
     PACT_TRY_S(scratch_get(ctx, kScratchRayBorder, sizeof(double) * rep_n, &rep));
     PACT_CUDA_S(cudaMemsetAsync(rep, 0, sizeof(double) * rep_n, ctx->stream));
     PACT_TRY_S(allow_smem(ray_backward_split_kernel, smem));
-    ray_backward_split_kernel<<<blocks, 256, smem, ctx->stream>>>(a, dw, grad,
+    ray_backward_split_kernel<<<blocks, rb, smem, ctx->stream>>>(a, dw, grad,
                                                                    static_cast<double*>(rep));
     PACT_TRY_S(after_launch(ctx, "ray_backward_split_kernel"));
     const int nbp = 2 * a.H + 2 * std::max(a.W - 2, 0);
