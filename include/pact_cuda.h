@@ -126,6 +126,24 @@ int pact_das_stack(pact_ctx* ctx, const pact_ring* ring, const pact_signal_meta*
                    const float* signals, const pact_grid* grid, double v0,
                    const double* delays, int32_t n_delays, float* out);
 
+/* BodyModel, beamform.hpp:44-54: the body disc of the two-speed DAS. */
+typedef struct pact_body {
+  double center_x; /* mm */
+  double center_y; /* mm */
+  double radius;   /* mm */
+  double body_sos; /* m/s, validated to [1300, 1800] */
+} pact_body;
+
+/* dual_sos_das, beamform.hpp:124-150: DAS (K = 1, no delay) whose time of
+ * flight runs at body_sos along the analytic chord through the body disc
+ * (segment_circle_intersection, core.hpp:184-204) and at v0 elsewhere.
+ *   signals : device fp32 [n_transducers][n_samples]
+ *   out     : device fp32 [grid.height][grid.width]
+ * Same validation order and messages as the reference. */
+int pact_dual_sos_das(pact_ctx* ctx, const pact_ring* ring, const pact_signal_meta* meta,
+                      const float* signals, const pact_grid* grid, double v0,
+                      const pact_body* body, float* out);
+
 /* simulate_signals, phantom.hpp:282-362 (+ time_of_flight, aberration.hpp:79-100):
  * the input-side step before DAS.  pressure, sos: HOST fp64 [H][W] rasters of
  * the Phantom on `grid`; mask = Phantom::mask (TOF integration disc);

@@ -141,6 +141,35 @@ int orc_das_stack(int n_tx, double radius, double offset, int T, double dt, doub
   return 0;
 }
 
+/* dual_sos_das, beamform.hpp:124-150 (validation beamform.hpp:126-131): the
+ * time of flight runs at body_sos along the chord through the body disc. */
+int orc_dual_sos_das(int n_tx, double radius, double offset, int T, double dt, double t0,
+                     const double* sig, int W, int H, double pitch, double ox, double oy,
+                     double v0, double bcx, double bcy, double br, double bsos, double* out) {
+  if (n_tx < 3 || !(radius > 0.0) || T < 2 || !(dt > 0.0)) return 2;
+  if (W < 1 || H < 1 || !(pitch > 0.0)) return 2;
+  if (!(br > 0.0) || !(bsos >= 1300.0 && bsos <= 1800.0)) return 2;
+  if (!(v0 > 0.0)) return 2;
+  if (hypot(bcx, bcy) + br >= radius) return 2;
+  double* px = (double*)malloc(sizeof(double) * 2 * n_tx);
+  for (int n = 0; n < n_tx; ++n) ring_pos(n_tx, radius, offset, n, &px[2 * n], &px[2 * n + 1]);
+  for (int iy = 0; iy < H; ++iy)
+    for (int ix = 0; ix < W; ++ix) {
+      double rx = ox + ix * pitch, ry = oy + iy * pitch, acc = 0.0;
+      for (int n = 0; n < n_tx; ++n) {
+        double dist = hypot(rx - px[2 * n], ry - px[2 * n + 1]);
+        double s0, s1;
+        seg_circle(rx, ry, px[2 * n], px[2 * n + 1], bcx, bcy, br, &s0, &s1);
+        double inside = s1 - s0 > 0.0 ? s1 - s0 : 0.0;
+        double t = 1e-3 * ((dist - inside) / v0 + inside / bsos);
+        acc += sig_sample(sig + (size_t)n * T, T, t0, dt, t);
+      }
+      out[(size_t)iy * W + ix] = acc;
+    }
+  free(px);
+  return 0;
+}
+
 /* --------------------------------------------------------------------- SIREN */
 
 /* std::mt19937_64 (the engine init_siren seeds, nfield.hpp:94) */

@@ -39,6 +39,9 @@ typedef struct OrcTrainCfg { /* = RefTrainCfg (TrainConfig, optimize.hpp:48-69) 
 int orc_das_stack(int n_tx, double radius, double offset, int T, double dt, double t0,
                   const double* sig, int W, int H, double pitch, double ox, double oy,
                   double v0, int K, const double* delays, int workers, double* out);
+int orc_dual_sos_das(int n_tx, double radius, double offset, int T, double dt, double t0,
+                     const double* sig, int W, int H, double pitch, double ox, double oy,
+                     double v0, double bcx, double bcy, double br, double bsos, double* out);
 int orc_init_siren(uint64_t seed, int hidden, int layers, double omega0, double out_scale,
                    double v0, double* theta);
 int orc_render_sos(int hidden, int layers, double omega0, double out_scale, double v0,

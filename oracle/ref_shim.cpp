@@ -115,6 +115,21 @@ int ref_das(int n_tx, double radius, double offset, int T, double dt, double t0,
   });
 }
 
+// dual_sos_das, beamform.hpp:124-150
+int ref_dual_sos_das(int n_tx, double radius, double offset, int T, double dt, double t0,
+                     const double* sig, int W, int H, double pitch, double ox, double oy,
+                     double v0, double bcx, double bcy, double br, double bsos, double* out) {
+  return guarded([&] {
+    auto s = signals_of(n_tx, radius, offset, T, dt, t0, v0, sig);
+    pact::BodyModel body;
+    body.center = {bcx, bcy};
+    body.radius = br;
+    body.body_sos = bsos;
+    auto img = pact::dual_sos_das(s, grid_of(W, H, pitch, ox, oy), v0, body, 0);
+    std::memcpy(out, img.values.data(), sizeof(double) * img.values.size());
+  });
+}
+
 // init_siren, nfield.hpp:83-107
 int ref_init_siren(uint64_t seed, int hidden, int layers, double omega0, double out_scale,
                    double v0, double* theta) {

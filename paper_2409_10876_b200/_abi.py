@@ -53,6 +53,11 @@ class Mask(C.Structure):
     _fields_ = [("center_x", C.c_double), ("center_y", C.c_double), ("radius", C.c_double)]
 
 
+class Body(C.Structure):
+    _fields_ = [("center_x", C.c_double), ("center_y", C.c_double), ("radius", C.c_double),
+                ("body_sos", C.c_double)]
+
+
 class Layout(C.Structure):
     _fields_ = [("grid", Grid), ("patch_pixels", C.c_int32), ("stride_pixels", C.c_int32),
                 ("nx", C.c_int32), ("ny", C.c_int32), ("last_x", C.c_int32),
@@ -109,6 +114,8 @@ SIGNATURES = {
     "pact_make_delays": (C.c_int, [_D, _D, _I, _DP]),
     "pact_das_stack": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(SignalMeta), _P,
                                  C.POINTER(Grid), _D, _DP, _I, _P]),
+    "pact_dual_sos_das": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(SignalMeta), _P,
+                                    C.POINTER(Grid), _D, C.POINTER(Body), _P]),
     "pact_simulate_signals": (C.c_int, [_P, C.POINTER(Grid), _DP, _DP, C.POINTER(Mask), _D,
                                         C.POINTER(Ring), _D, C.POINTER(SignalMeta), _D, _P]),
     "pact_make_patch_layout": (C.c_int, [C.POINTER(Grid), _D, _D, C.POINTER(Layout)]),

@@ -77,6 +77,18 @@ class CircularMask:
         return Mask(self.center_x, self.center_y, self.radius)
 
 
+@dataclass(frozen=True)
+class BodyModel:
+    """BodyModel, beamform.hpp:44-54."""
+    center_x: float
+    center_y: float
+    radius: float
+    body_sos: float
+
+    def c(self) -> "_abi.Body":
+        return _abi.Body(self.center_x, self.center_y, self.radius, self.body_sos)
+
+
 def make_delays(lo: float, hi: float, count: int) -> list[float]:
     """make_delays, beamform.hpp:113-120."""
     out = (C.c_double * max(1, count))()
@@ -135,6 +147,18 @@ class Context:
     def das(self, signals, ring, meta, grid, v0, d):
         """das, beamform.hpp:56-75 (the K = 1 stack)."""
         return self.das_stack(signals, ring, meta, grid, v0, [d])[0]
+
+    def dual_sos_das(self, signals: torch.Tensor, ring: RingGeometry, meta: SignalMetaInfo,
+                     grid: GridSpec, v0: float, body: "BodyModel",
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+        """dual_sos_das, beamform.hpp:124-150 -> fp32 [H, W] on the device."""
+        assert signals.is_cuda and signals.dtype == torch.float32 and signals.is_contiguous()
+        if out is None:
+            out = torch.empty((grid.height, grid.width), device=signals.device, dtype=torch.float32)
+        r, m, g, b = ring.c(), meta.c(), grid.c(), body.c()
+        check(_abi.lib().pact_dual_sos_das(self._h, C.byref(r), C.byref(m), dptr(signals),
+                                           C.byref(g), float(v0), C.byref(b), dptr(out)))
+        return out
 
 
 # --------------------------------------------------------------------------- #

@@ -62,6 +62,42 @@ inline RasterGrid das(const SignalSet& signals, const GridSpec& grid, double v0,
   return das_stack(signals, grid, v0, {d}, workers).images[0];
 }
 
+/// BodyModel (beamform.hpp:44-54).
+struct BodyModel {
+  Vec2 center;
+  double radius = 0.0;    // mm
+  double body_sos = 0.0;  // m/s
+
+  void validate() const {
+    if (!(radius > 0.0)) throw ValidationError("body model: radius must be > 0");
+    if (!(body_sos >= 1300.0 && body_sos <= 1800.0))
+      throw ValidationError("body model: SOS outside [1300, 1800] m/s");
+  }
+};
+
+/// dual_sos_das (beamform.hpp:124-150) on the GPU; `workers` is accepted and ignored.
+inline RasterGrid dual_sos_das(const SignalSet& signals, const GridSpec& grid, double v0,
+                               const BodyModel& body, int workers = 0) {
+  (void)workers;
+  signals.validate();
+  grid.validate();
+  body.validate();
+  if (!(v0 > 0.0)) throw ValidationError("dual_sos_das: v0 must be > 0");
+  if (body.center.norm() + body.radius >= signals.geom.radius)
+    throw ValidationError("dual_sos_das: body disc extends outside the transducer ring");
+  cuda::Buffer<float> sig(signals.data.size());
+  cuda::upload_f32(sig, signals.data);
+  cuda::Buffer<float> out(static_cast<size_t>(grid.width) * grid.height);
+  pact_ring r = signals.geom.c();
+  pact_signal_meta m = signals.meta();
+  pact_grid g = grid.c();
+  pact_body b{body.center.x, body.center.y, body.radius, body.body_sos};
+  cuda::check(pact_dual_sos_das(cuda::context(), &r, &m, sig.ptr, &g, v0, &b, out.ptr));
+  RasterGrid img = RasterGrid::zeros(grid);
+  img.values = cuda::download_f64(out);
+  return img;
+}
+
 }  // namespace pact
 
 #endif

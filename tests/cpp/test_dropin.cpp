@@ -114,6 +114,18 @@ static void test_beamform() {
   std::vector<double> got;
   for (auto& im : st.images) got.insert(got.end(), im.values.begin(), im.values.end());
   CHECK(rel_l2(got, want) <= 1e-4);
+  // dual_sos_das (beamform.hpp:124-150): parity with the oracle, the body_sos = v0
+  // degenerate case (test_beamform.cpp:133-141) and the validation messages
+  BodyModel body{{1.0, -0.5}, 6.0, 1580.0};
+  std::vector<double> dwant(33 * 33);
+  orc_dual_sos_das(128, 50.0, 0.0, 1400, 25e-9, 32e-6, s.data.data(), 33, 33, 0.1, small.origin.x,
+                   small.origin.y, 1500.0, body.center.x, body.center.y, body.radius,
+                   body.body_sos, dwant.data());
+  CHECK(rel_l2(dual_sos_das(s, small, 1500.0, body).values, dwant) <= 1e-4);
+  RasterGrid same = dual_sos_das(s, small, 1500.0, BodyModel{{0.0, 0.0}, 8.0, 1500.0});
+  CHECK(rel_l2(same.values, das(s, small, 1500.0, 0.0).values) <= 1e-6);
+  CHECK(throws<ValidationError>([&] { dual_sos_das(s, small, 1500.0, BodyModel{{0, 0}, 0.0, 1500.0}); }));
+  CHECK(throws<ValidationError>([&] { dual_sos_das(s, small, 1500.0, BodyModel{{45, 0}, 8.0, 1500.0}); }));
 }
 
 static void test_nfield() {

@@ -65,6 +65,24 @@ def das_cases(R):
          sig=sig1.astype(np.float32), delays=np.array(w.delays), v0=np.array(w.v0), out=out1)
 
 
+def dual_case(R):
+    """dual_sos_das (beamform.hpp:124-150): a body disc overlapping part of a
+    small grid, a window that clips some taps, i.i.d. signals."""
+    from paper_2409_10876_b200.api import BodyModel
+
+    rng = np.random.default_rng(4321)
+    ring = RingGeometry(48, 30.0, 0.05)
+    meta = SignalMetaInfo(600, 25e-9, 14.0e-6, 1500.0)
+    grid = GridSpec(40, 36, 0.3, -5.85, -5.25)
+    sig = rng.standard_normal((48, 600)).astype(np.float32).astype(np.float64)
+    bodies = [BodyModel(1.0, -0.5, 5.0, 1580.0), BodyModel(-2.0, 1.5, 9.0, 1420.0)]
+    outs = [R.dual_sos_das(sig, ring, meta, grid, 1500.0, b) for b in bodies]
+    save("dual_das", ring=ring_arr(ring), meta=meta_arr(meta), grid=grid_arr(grid),
+         sig=sig.astype(np.float32), v0=np.array(1500.0),
+         bodies=np.array([[b.center_x, b.center_y, b.radius, b.body_sos] for b in bodies]),
+         out=np.stack(outs))
+
+
 def small_case(R):
     """testsupport::SmallInstance (proj/tests/test_support.hpp:38-75), through
     every hot-path entry point of the reference."""
@@ -157,9 +175,11 @@ def main():
     R = ref()
     if R is None:
         sys.exit("oracle/_ref/libpact_ref.so missing: make -C oracle ref")
-    which = sys.argv[1:] or ["das", "small", "cfg2"]
+    which = sys.argv[1:] or ["das", "dual", "small", "cfg2"]
     if "das" in which:
         das_cases(R)
+    if "dual" in which:
+        dual_case(R)
     if "small" in which:
         small_case(R)
     if "cfg2" in which:

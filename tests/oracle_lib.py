@@ -48,6 +48,7 @@ def train_cfg(cfg) -> tuple[TrainCfg, object]:
 
 SIGS = {
     "das_stack": [_I, _D, _D, _I, _D, _D, _P, _I, _I, _D, _D, _D, _D, _I, _P, _I, _P],
+    "dual_sos_das": [_I, _D, _D, _I, _D, _D, _P, _I, _I, _D, _D, _D, _D, _D, _D, _D, _D, _P],
     "init_siren": [C.c_uint64, _I, _I, _D, _D, _D, _P],
     "render_sos": [_I, _I, _D, _D, _D, _P, _I, _I, _D, _D, _D, _D, _D, _D, _P, _P],
     "backprop_sos": [_I, _I, _D, _D, _D, _P, _I, _I, _D, _D, _D, _D, _D, _D, _P, _P],
@@ -118,6 +119,13 @@ class Oracle:
         out = np.zeros((len(d), grid.height, grid.width))
         self.call("das_stack", *_r(ring), meta.n_samples, meta.dt, meta.t0, _p(sig), *_g(grid),
                   v0, len(d), _p(d), workers, _p(out))
+        return out
+
+    def dual_sos_das(self, sig, ring, meta, grid, v0, body):
+        sig = _f64(sig)
+        out = np.zeros((grid.height, grid.width))
+        self.call("dual_sos_das", *_r(ring), meta.n_samples, meta.dt, meta.t0, _p(sig), *_g(grid),
+                  v0, body.center_x, body.center_y, body.radius, body.body_sos, _p(out))
         return out
 
     # -- SIREN ------------------------------------------------------------
