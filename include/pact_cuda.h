@@ -144,6 +144,21 @@ int pact_dual_sos_das(pact_ctx* ctx, const pact_ring* ring, const pact_signal_me
                       const float* signals, const pact_grid* grid, double v0,
                       const pact_body* body, float* out);
 
+/* ---- evaluation metrics (evaluate.hpp:39-114), SURVEY §8(f)-4 ----
+ * test, truth: device fp64 [height][width] rasters of the same geometry (the
+ * shape check of the reference is the caller's: RasterGrid carries it).
+ * Synchronous; the value is written to *out (host).  fp64 sums, fixed order. */
+/* psnr, evaluate.hpp:39-51: +inf for identical images. */
+int pact_psnr(pact_ctx* ctx, const double* test, const double* truth, int32_t width,
+              int32_t height, double data_range, double* out);
+/* ssim, evaluate.hpp:53-96: 11x11 Gaussian window (sigma 1.5), K1 0.01, K2 0.03,
+ * mean over the pixels whose window fits. */
+int pact_ssim(pact_ctx* ctx, const double* test, const double* truth, int32_t width,
+              int32_t height, double data_range, double* out);
+/* sos_rmse_masked, evaluate.hpp:99-114: RMSE over pixels whose centres are in the mask. */
+int pact_sos_rmse_masked(pact_ctx* ctx, const double* test, const double* truth,
+                         const pact_grid* grid, const pact_mask* mask, double* out);
+
 /* simulate_signals, phantom.hpp:282-362 (+ time_of_flight, aberration.hpp:79-100):
  * the input-side step before DAS.  pressure, sos: HOST fp64 [H][W] rasters of
  * the Phantom on `grid`; mask = Phantom::mask (TOF integration disc);

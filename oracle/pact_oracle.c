@@ -170,6 +170,79 @@ int orc_dual_sos_das(int n_tx, double radius, double offset, int T, double dt, d
   return 0;
 }
 
+/* ------------------------------------------------------------------ metrics */
+
+/* psnr, evaluate.hpp:39-51 */
+int orc_psnr(const double* test, const double* truth, int W, int H, double data_range,
+             double* out) {
+  if (!(data_range > 0.0)) return 2;
+  double mse = 0.0;
+  const size_t n = (size_t)W * H;
+  for (size_t i = 0; i < n; ++i) {
+    double d = test[i] - truth[i];
+    mse += d * d;
+  }
+  mse /= (double)n;
+  *out = mse == 0.0 ? INFINITY : 10.0 * log10(data_range * data_range / mse);
+  return 0;
+}
+
+/* ssim, evaluate.hpp:53-96 */
+int orc_ssim(const double* test, const double* truth, int W, int H, double data_range,
+             double* out) {
+  if (!(data_range > 0.0)) return 2;
+  if (W < 11 || H < 11) return 2;
+  double kern[11], ksum = 0.0;
+  for (int i = 0; i < 11; ++i) {
+    double d = i - 5.0;
+    kern[i] = exp(-0.5 * d * d / (1.5 * 1.5));
+    ksum += kern[i];
+  }
+  for (int i = 0; i < 11; ++i) kern[i] /= ksum;
+  const double c1 = (0.01 * data_range) * (0.01 * data_range);
+  const double c2 = (0.03 * data_range) * (0.03 * data_range);
+  double acc = 0.0;
+  long count = 0;
+  for (int iy = 5; iy < H - 5; ++iy)
+    for (int ix = 5; ix < W - 5; ++ix) {
+      double mx = 0, my = 0, mxx = 0, myy = 0, mxy = 0;
+      for (int dy = -5; dy <= 5; ++dy)
+        for (int dx = -5; dx <= 5; ++dx) {
+          double w = kern[dy + 5] * kern[dx + 5];
+          double a = test[(size_t)(iy + dy) * W + ix + dx];
+          double b = truth[(size_t)(iy + dy) * W + ix + dx];
+          mx += w * a;
+          my += w * b;
+          mxx += w * a * a;
+          myy += w * b * b;
+          mxy += w * a * b;
+        }
+      double vx = mxx - mx * mx, vy = myy - my * my, cxy = mxy - mx * my;
+      acc += ((2 * mx * my + c1) * (2 * cxy + c2)) / ((mx * mx + my * my + c1) * (vx + vy + c2));
+      ++count;
+    }
+  *out = acc / count;
+  return 0;
+}
+
+/* sos_rmse_masked, evaluate.hpp:99-114 */
+int orc_sos_rmse_masked(const double* test, const double* truth, int W, int H, double pitch,
+                        double ox, double oy, double mcx, double mcy, double mr, double* out) {
+  double acc = 0.0;
+  long n = 0;
+  for (int iy = 0; iy < H; ++iy)
+    for (int ix = 0; ix < W; ++ix) {
+      double px = ox + ix * pitch, py = oy + iy * pitch;
+      if (!(hypot(px - mcx, py - mcy) <= mr)) continue;
+      double d = test[(size_t)iy * W + ix] - truth[(size_t)iy * W + ix];
+      acc += d * d;
+      ++n;
+    }
+  if (n == 0) return 2;
+  *out = sqrt(acc / n);
+  return 0;
+}
+
 /* --------------------------------------------------------------------- SIREN */
 
 /* std::mt19937_64 (the engine init_siren seeds, nfield.hpp:94) */

@@ -42,6 +42,12 @@ int orc_das_stack(int n_tx, double radius, double offset, int T, double dt, doub
 int orc_dual_sos_das(int n_tx, double radius, double offset, int T, double dt, double t0,
                      const double* sig, int W, int H, double pitch, double ox, double oy,
                      double v0, double bcx, double bcy, double br, double bsos, double* out);
+int orc_psnr(const double* test, const double* truth, int W, int H, double data_range,
+             double* out);
+int orc_ssim(const double* test, const double* truth, int W, int H, double data_range,
+             double* out);
+int orc_sos_rmse_masked(const double* test, const double* truth, int W, int H, double pitch,
+                        double ox, double oy, double mcx, double mcy, double mr, double* out);
 int orc_init_siren(uint64_t seed, int hidden, int layers, double omega0, double out_scale,
                    double v0, double* theta);
 int orc_render_sos(int hidden, int layers, double omega0, double out_scale, double v0,

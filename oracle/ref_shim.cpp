@@ -19,6 +19,7 @@
 #include "pact/aberration.hpp"
 #include "pact/beamform.hpp"
 #include "pact/core.hpp"
+#include "pact/evaluate.hpp"
 #include "pact/deconv.hpp"
 #include "pact/nfield.hpp"
 #include "pact/optimize.hpp"
@@ -127,6 +128,38 @@ int ref_dual_sos_das(int n_tx, double radius, double offset, int T, double dt, d
     body.body_sos = bsos;
     auto img = pact::dual_sos_das(s, grid_of(W, H, pitch, ox, oy), v0, body, 0);
     std::memcpy(out, img.values.data(), sizeof(double) * img.values.size());
+  });
+}
+
+// psnr / ssim / sos_rmse_masked, evaluate.hpp:39-114
+static pact::RasterGrid raster_of(const double* v, int W, int H, double pitch, double ox,
+                                  double oy) {
+  pact::RasterGrid r = pact::RasterGrid::zeros(grid_of(W, H, pitch, ox, oy));
+  std::memcpy(r.values.data(), v, sizeof(double) * r.values.size());
+  return r;
+}
+int ref_psnr(const double* test, const double* truth, int W, int H, double data_range,
+             double* out) {
+  return guarded([&] {
+    *out = pact::psnr(raster_of(test, W, H, 0.1, 0, 0), raster_of(truth, W, H, 0.1, 0, 0),
+                      data_range);
+  });
+}
+int ref_ssim(const double* test, const double* truth, int W, int H, double data_range,
+             double* out) {
+  return guarded([&] {
+    *out = pact::ssim(raster_of(test, W, H, 0.1, 0, 0), raster_of(truth, W, H, 0.1, 0, 0),
+                      data_range);
+  });
+}
+int ref_sos_rmse_masked(const double* test, const double* truth, int W, int H, double pitch,
+                        double ox, double oy, double mcx, double mcy, double mr, double* out) {
+  return guarded([&] {
+    pact::CircularMask m;
+    m.center = {mcx, mcy};
+    m.radius = mr;
+    *out = pact::sos_rmse_masked(raster_of(test, W, H, pitch, ox, oy),
+                                 raster_of(truth, W, H, pitch, ox, oy), m);
   });
 }
 

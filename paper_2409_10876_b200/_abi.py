@@ -114,6 +114,9 @@ SIGNATURES = {
     "pact_make_delays": (C.c_int, [_D, _D, _I, _DP]),
     "pact_das_stack": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(SignalMeta), _P,
                                  C.POINTER(Grid), _D, _DP, _I, _P]),
+    "pact_psnr": (C.c_int, [_P, _P, _P, _I, _I, _D, _DP]),
+    "pact_ssim": (C.c_int, [_P, _P, _P, _I, _I, _D, _DP]),
+    "pact_sos_rmse_masked": (C.c_int, [_P, _P, _P, C.POINTER(Grid), C.POINTER(Mask), _DP]),
     "pact_dual_sos_das": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(SignalMeta), _P,
                                     C.POINTER(Grid), _D, C.POINTER(Body), _P]),
     "pact_simulate_signals": (C.c_int, [_P, C.POINTER(Grid), _DP, _DP, C.POINTER(Mask), _D,

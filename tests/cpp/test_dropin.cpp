@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "pact/beamform.hpp"
+#include "pact/evaluate.hpp"
 #include "pact/core.hpp"
 #include "pact/deconv.hpp"
 #include "pact/nfield.hpp"
@@ -126,6 +127,26 @@ static void test_beamform() {
   CHECK(rel_l2(same.values, das(s, small, 1500.0, 0.0).values) <= 1e-6);
   CHECK(throws<ValidationError>([&] { dual_sos_das(s, small, 1500.0, BodyModel{{0, 0}, 0.0, 1500.0}); }));
   CHECK(throws<ValidationError>([&] { dual_sos_das(s, small, 1500.0, BodyModel{{45, 0}, 8.0, 1500.0}); }));
+}
+
+static void test_evaluate() {
+  // test_evaluate.cpp:38-112 through the GPU metrics
+  GridSpec g = GridSpec::centered(32, 32, 0.1);
+  RasterGrid truth = RasterGrid::zeros(g);
+  std::mt19937_64 rng(1);
+  std::uniform_real_distribution<double> u(0, 1);
+  for (double& v : truth.values) v = u(rng);
+  CHECK(std::isinf(psnr(truth, truth, 1.0)));
+  RasterGrid off = truth;
+  for (double& v : off.values) v += 0.1;
+  CHECK(std::abs(psnr(off, truth, 1.0) - 20.0) < 1e-9);
+  CHECK(std::abs(ssim(truth, truth, 1.0) - 1.0) < 1e-12);
+  CHECK(throws<ValidationError>([&] { psnr(truth, truth, 0.0); }));
+  CHECK(throws<ValidationError>([&] { ssim(RasterGrid::zeros(GridSpec::centered(8, 8, 0.1)),
+                                           RasterGrid::zeros(GridSpec::centered(8, 8, 0.1)), 1.0); }));
+  GridSpec g33 = GridSpec::centered(33, 33, 0.1);
+  CHECK(std::abs(sos_rmse_masked(RasterGrid::constant(g33, 1510.0), RasterGrid::constant(g33, 1500.0),
+                                 CircularMask{{0, 0}, 1.0}) - 10.0) < 1e-12);
 }
 
 static void test_nfield() {
@@ -299,6 +320,7 @@ int main() {
     const char* name;
     std::function<void()> fn;
   } cases[] = {{"beamform", test_beamform},
+               {"evaluate", test_evaluate},
                {"nfield", test_nfield},
                {"aberration", test_aberration},
                {"optimize", test_optimize},

@@ -83,6 +83,29 @@ def dual_case(R):
          out=np.stack(outs))
 
 
+def metrics_case(R):
+    """psnr / ssim / sos_rmse_masked (evaluate.hpp:39-114) on random and
+    structured images (a blob field and its 5-pixel shift, test_evaluate.cpp:83-104)."""
+    from paper_2409_10876_b200.api import CircularMask
+
+    rng = np.random.default_rng(777)
+    a = rng.uniform(0, 1, (36, 40))
+    b = np.clip(a + rng.normal(0, 0.05, a.shape), 0, 1)
+    yy, xx = np.mgrid[0:64, 0:64]
+    img = sum(amp * np.exp(-((xx - cx) ** 2 + (yy - cy) ** 2) / 18.0)
+              for cx, cy, amp in [(20, 22, 1.0), (40, 35, 0.8), (30, 48, 0.6)])
+    shifted = np.zeros_like(img)
+    shifted[:, 5:] = img[:, :-5]
+    grid = GridSpec(33, 29, 0.1, -1.6, -1.4)
+    sos_t = 1500 + 40 * rng.uniform(0, 1, (29, 33))
+    sos_r = 1500 + 40 * rng.uniform(0, 1, (29, 33))
+    mask = CircularMask(0.2, -0.1, 1.2)
+    vals = np.array([R.psnr(b, a, 1.0), R.ssim(b, a, 1.0), R.psnr(shifted, img, 1.0),
+                     R.ssim(shifted, img, 1.0), R.sos_rmse_masked(sos_r, sos_t, grid, mask)])
+    save("metrics", a=a, b=b, img=img, shifted=shifted, grid=grid_arr(grid), sos_t=sos_t,
+         sos_r=sos_r, mask=np.array([mask.center_x, mask.center_y, mask.radius]), vals=vals)
+
+
 def small_case(R):
     """testsupport::SmallInstance (proj/tests/test_support.hpp:38-75), through
     every hot-path entry point of the reference."""
@@ -175,11 +198,13 @@ def main():
     R = ref()
     if R is None:
         sys.exit("oracle/_ref/libpact_ref.so missing: make -C oracle ref")
-    which = sys.argv[1:] or ["das", "dual", "small", "cfg2"]
+    which = sys.argv[1:] or ["das", "dual", "metrics", "small", "cfg2"]
     if "das" in which:
         das_cases(R)
     if "dual" in which:
         dual_case(R)
+    if "metrics" in which:
+        metrics_case(R)
     if "small" in which:
         small_case(R)
     if "cfg2" in which:

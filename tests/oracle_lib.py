@@ -49,6 +49,9 @@ def train_cfg(cfg) -> tuple[TrainCfg, object]:
 SIGS = {
     "das_stack": [_I, _D, _D, _I, _D, _D, _P, _I, _I, _D, _D, _D, _D, _I, _P, _I, _P],
     "dual_sos_das": [_I, _D, _D, _I, _D, _D, _P, _I, _I, _D, _D, _D, _D, _D, _D, _D, _D, _P],
+    "psnr": [_P, _P, _I, _I, _D, _P],
+    "ssim": [_P, _P, _I, _I, _D, _P],
+    "sos_rmse_masked": [_P, _P, _I, _I, _D, _D, _D, _D, _D, _D, _P],
     "init_siren": [C.c_uint64, _I, _I, _D, _D, _D, _P],
     "render_sos": [_I, _I, _D, _D, _D, _P, _I, _I, _D, _D, _D, _D, _D, _D, _P, _P],
     "backprop_sos": [_I, _I, _D, _D, _D, _P, _I, _I, _D, _D, _D, _D, _D, _D, _P, _P],
@@ -127,6 +130,25 @@ class Oracle:
         self.call("dual_sos_das", *_r(ring), meta.n_samples, meta.dt, meta.t0, _p(sig), *_g(grid),
                   v0, body.center_x, body.center_y, body.radius, body.body_sos, _p(out))
         return out
+
+    # -- metrics (evaluate.hpp:39-114) -------------------------------------
+    def psnr(self, test, truth, data_range):
+        a, b = _f64(test), _f64(truth)
+        out = np.zeros(1)
+        self.call("psnr", _p(a), _p(b), a.shape[1], a.shape[0], data_range, _p(out))
+        return float(out[0])
+
+    def ssim(self, test, truth, data_range):
+        a, b = _f64(test), _f64(truth)
+        out = np.zeros(1)
+        self.call("ssim", _p(a), _p(b), a.shape[1], a.shape[0], data_range, _p(out))
+        return float(out[0])
+
+    def sos_rmse_masked(self, test, truth, grid, mask):
+        a, b = _f64(test), _f64(truth)
+        out = np.zeros(1)
+        self.call("sos_rmse_masked", _p(a), _p(b), *_g(grid), *_m(mask), _p(out))
+        return float(out[0])
 
     # -- SIREN ------------------------------------------------------------
     def init_siren(self, seed, spec, n_params):

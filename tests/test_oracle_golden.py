@@ -37,6 +37,15 @@ def test_dual_sos_das_restatement_matches_reference():
     assert rel_l2(plain, z["out"][0]) > 0.1
 
 
+def test_metrics_restatement_matches_reference():
+    z = gu.load("metrics")
+    o = orc()
+    got = [o.psnr(z["b"], z["a"], 1.0), o.ssim(z["b"], z["a"], 1.0),
+           o.psnr(z["shifted"], z["img"], 1.0), o.ssim(z["shifted"], z["img"], 1.0),
+           o.sos_rmse_masked(z["sos_r"], z["sos_t"], gu.grid(z["grid"]), gu.mask(z["mask"]))]
+    np.testing.assert_allclose(got, z["vals"], rtol=1e-12)
+
+
 def test_das_edge_fixture_exercises_both_window_edges():
     z = gu.load("das_edge")
     m = gu.meta(z["meta"])
