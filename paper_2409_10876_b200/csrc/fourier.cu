@@ -491,17 +491,21 @@ __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const 
                                                             float2* __restrict__ nyq_all,
                                                             float2* __restrict__ gbuf,
                                                             double* __restrict__ loss_part,
-                                                            int n_parts, int part0) {
+                                                            int n_parts, int part0, int stage_y,
+                                                            int stage_g) {
   extern __shared__ __align__(16) float smem[];
   __shared__ double s_red[32];
   const int patch = blockIdx.x, K = t.K, P2 = t.P2, S = 2 * t.P - 1;
-  float* s_w = smem;                                              // [A]
-  float2* s_y = reinterpret_cast<float2*>(smem + ((t.A + 1) & ~1));  // [K][S]
-  float2* s_g = s_y + K * S;                                         // [S][K] exchange
+  // shared memory: [A] profile | [K][S] spectra (stage_y) | [S][K] exchange
+  // (stage_g); large K x S (cfg5: P = 128, K = 64) falls back to L2 for either
+  float* s_w = smem;
+  float2* s_y = reinterpret_cast<float2*>(smem + ((t.A + 1) & ~1));
+  float2* s_g = stage_g ? s_y + (stage_y ? K * S : 0)
+                        : nyq_all + static_cast<size_t>(patch) * S * K;
   for (int a = threadIdx.x; a < t.A; a += blockDim.x) s_w[a] = w_all[patch * t.A + a];
   const float2* Y = Y_all + static_cast<size_t>(patch) * K * P2;
   // the slots' spectra, eight loads in flight per thread
-  for (int e0 = threadIdx.x; e0 < K * S; e0 += 8 * blockDim.x) {
+  for (int e0 = threadIdx.x; stage_y && e0 < K * S; e0 += 8 * blockDim.x) {
     float2 v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -521,8 +525,11 @@ __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const 
     b = nyq_bin(slot, t.P);
     float G1, G2;
     value = bin_chain<true>(t, s_w, b, t.mirror[b], eps_m, scale, implicit != 0,
-                            [&](int j) { return s_y[j * S + slot]; }, G1, G2,
-                            s_g + static_cast<size_t>(slot) * K);
+                            [&](int j) {
+                              return stage_y ? s_y[j * S + slot]
+                                             : Y[static_cast<size_t>(j) * P2 + b];
+                            },
+                            G1, G2, s_g + static_cast<size_t>(slot) * K);
   }
   block_sum_store(value, s_red, loss_part + patch * n_parts + part0);
   __syncthreads();  // the exchange buffer of every slot is complete
@@ -647,15 +654,17 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
   if (t.P % 2 == 0) {
     const int S = 2 * t.P - 1, nt = div_up(S, 32) * 32;
     if (nt > 1024) return validation("fused loss: patch size too large for the Nyquist kernel");
-    const size_t smem_nyq = sizeof(float) * ((t.A + 1) & ~1) + 2 * sizeof(float2) * t.K * S;
+    const size_t plane = sizeof(float2) * t.K * S, base = sizeof(float) * ((t.A + 1) & ~1);
+    const int stage_y = base + 2 * plane <= 200 * 1024;
+    const int stage_g = base + (stage_y ? 2 : 1) * plane <= 200 * 1024;
+    const size_t smem_nyq = base + (stage_y + stage_g) * plane;
     if (smem_nyq > 48 * 1024) {
-      if (smem_nyq > 200 * 1024) return validation("fused loss: Nyquist set too large");
       PACT_CUDA_S(cudaFuncSetAttribute(loss_nyquist_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem_nyq)));
     }
-    loss_nyquist_kernel<<<n_patches, nt, smem_nyq, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, nyq,
-                                                                   gbuf, part, n_parts, chunks);
+    loss_nyquist_kernel<<<n_patches, nt, smem_nyq, ctx->stream>>>(
+        t, Y, w, eps_m, sc, implicit, nyq, gbuf, part, n_parts, chunks, stage_y, stage_g);
     PACT_TRY_S(after_launch(ctx, "loss_nyquist_kernel"));
   }
   loss_finish_kernel<<<dim3(n_patches, div_up(t.A, 8)), 256, 0, ctx->stream>>>(t, gbuf, part, n_parts,
