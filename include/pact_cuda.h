@@ -325,6 +325,36 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
 /* Enqueue n_steps full iterations (render -> wavefront -> fused loss ->
  * ray backward -> TV -> SIREN backward -> Adam); asynchronous. */
 int pact_trainer_step(pact_trainer* tr, int32_t n_steps);
+
+/* ---- one frame over several GPUs ----
+ * Rank `rank` of `world` owns the patch rows [ny*rank/world, ny*(rank+1)/world)
+ * (spectra, wavefronts, loss, ray adjoint) and the masked pixels
+ * [n*rank/world, n*(rank+1)/world) of the row-major list (SIREN forward and
+ * backward, TV).  Every rank keeps the full dv and dL/dv rasters and a replica
+ * of theta and Adam.  The iteration then runs as phases with the caller's
+ * collectives in between (buffers: pact_trainer_buffer):
+ *   phase 0  render own pixels into a cleared dv     -> all-reduce dv (2, f32, SUM)
+ *   phase 1  wavefront, loss, ray adjoint, TV, report -> all-reduce dL/dv (5, f64, SUM),
+ *            report (8, f64[3], SUM), flags (9, u32, MAX)
+ *   phase 2  SIREN backward                          -> all-reduce gradient (6, f64, SUM)
+ *   phase 3  finiteness check + Adam (identical on every rank)
+ * and the final image as
+ *   phase 4  render                                  -> all-reduce dv (SUM)
+ *   phase 5  deconvolve own patches into merge accumulators num (10), den (11)
+ *            (f32 rasters)                            -> all-reduce (SUM); image = num/den
+ * world == 1 is the whole frame (phases 0-3 in order == pact_trainer_step). */
+typedef struct pact_partition {
+  int32_t rank;
+  int32_t world;
+} pact_partition;
+int pact_trainer_create_partitioned(pact_ctx* ctx, const pact_ring* ring,
+                                    const pact_signal_meta* meta, const float* signals,
+                                    const pact_grid* grid, const pact_mask* mask,
+                                    const pact_train_config* cfg, const pact_partition* part,
+                                    pact_trainer** out);
+int pact_trainer_phase(pact_trainer* tr, int32_t phase);
+/* info[7] = {patch lo, patch hi, pixel lo, pixel hi, total patches, rank, world} */
+int pact_trainer_local(pact_trainer* tr, int32_t* info);
 /* Last step's LossReport terms {data, tv, total} (host) and the NumericalError
  * check of joint_reconstruct; synchronises.  `epoch` is used in the message. */
 int pact_trainer_report(pact_trainer* tr, int32_t epoch, double* report3);
@@ -339,7 +369,10 @@ int pact_trainer_set_theta(pact_trainer* tr, const double* theta);
 /* Device pointers of the engine's state for inspection:
  * what: 0 stack fp32 [K][H][W], 1 spectra c64 [n][K][P][P], 2 sos_dev fp32 [H][W],
  * 3 wavefronts fp32 [n][A], 4 dw fp32 [n][A], 5 grad_v fp64 [H][W],
- * 6 grad_theta fp64 [P], 7 theta fp64 [P]. */
+ * 6 grad_theta fp64 [P], 7 theta fp64 [P], 8 report fp64 [3] (data, tv, total),
+ * 9 NumericalError flags u32, 10/11 merge accumulators fp32 [H][W] (world > 1),
+ * 12 theta fp32 working copy [P].  Spectra, wavefronts and dw cover the local
+ * patches of a partitioned trainer. */
 void* pact_trainer_buffer(pact_trainer* tr, int32_t what);
 int pact_trainer_destroy(pact_trainer* tr);
 /* Kernels the engine launched so far (graph replays counted per kernel). */

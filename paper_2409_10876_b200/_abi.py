@@ -53,6 +53,10 @@ class Mask(C.Structure):
     _fields_ = [("center_x", C.c_double), ("center_y", C.c_double), ("radius", C.c_double)]
 
 
+class Partition(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32)]
+
+
 class Body(C.Structure):
     _fields_ = [("center_x", C.c_double), ("center_y", C.c_double), ("radius", C.c_double),
                 ("body_sos", C.c_double)]
@@ -148,6 +152,12 @@ SIGNATURES = {
     "pact_trainer_create": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(SignalMeta), _P,
                                       C.POINTER(Grid), C.POINTER(Mask), C.POINTER(TrainConfig),
                                       C.POINTER(_P)]),
+    "pact_trainer_create_partitioned": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(SignalMeta), _P,
+                                                  C.POINTER(Grid), C.POINTER(Mask),
+                                                  C.POINTER(TrainConfig), C.POINTER(Partition),
+                                                  C.POINTER(_P)]),
+    "pact_trainer_phase": (C.c_int, [_P, _I]),
+    "pact_trainer_local": (C.c_int, [_P, C.POINTER(C.c_int32)]),
     "pact_trainer_step": (C.c_int, [_P, _I]),
     "pact_trainer_report": (C.c_int, [_P, _I, _DP]),
     "pact_trainer_run_epoch": (C.c_int, [_P, _I, _DP]),

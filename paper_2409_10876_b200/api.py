@@ -428,20 +428,43 @@ class TrainConfig:
         return cfg, arr
 
 
+_TORCH_TYPESTR = {torch.float32: "<f4", torch.float64: "<f8", torch.int32: "<i4",
+                  torch.complex64: "<c8", torch.uint8: "|u1"}
+
+
+def _device_view(ptr: int, shape, dtype: torch.dtype) -> torch.Tensor:
+    """torch tensor over library-owned device memory (no copy)."""
+    class _Iface:
+        __cuda_array_interface__ = {"shape": tuple(int(s) for s in shape),
+                                    "typestr": _TORCH_TYPESTR[dtype], "data": (int(ptr), False),
+                                    "version": 3, "strides": None}
+    return torch.as_tensor(_Iface(), device="cuda")
+
+
 class Trainer:
     """pact_trainer: joint_reconstruct (optimize.hpp:367-494) split into
     create / step / report / finish so the iteration can be timed."""
 
     def __init__(self, ctx: Context, signals: torch.Tensor, ring: RingGeometry,
-                 meta: SignalMetaInfo, grid: GridSpec, mask: CircularMask, cfg: TrainConfig):
+                 meta: SignalMetaInfo, grid: GridSpec, mask: CircularMask, cfg: TrainConfig,
+                 partition: tuple[int, int] | None = None):
+        """partition = (rank, world): this trainer owns a share of one frame and
+        steps by phases (see pact_trainer_create_partitioned, distributed.py)."""
         self.ctx, self.grid, self.cfg = ctx, grid, cfg
+        self.v0 = meta.background_sos
         self._signals = signals.contiguous()
         c, self._arr = cfg.c()
         r, m, g, mk = ring.c(), meta.c(), grid.c(), mask.c()
         h = C.c_void_p()
-        check(_abi.lib().pact_trainer_create(ctx.handle, C.byref(r), C.byref(m),
-                                             dptr(self._signals), C.byref(g), C.byref(mk),
-                                             C.byref(c), C.byref(h)))
+        if partition is None:
+            check(_abi.lib().pact_trainer_create(ctx.handle, C.byref(r), C.byref(m),
+                                                 dptr(self._signals), C.byref(g), C.byref(mk),
+                                                 C.byref(c), C.byref(h)))
+        else:
+            p = _abi.Partition(int(partition[0]), int(partition[1]))
+            check(_abi.lib().pact_trainer_create_partitioned(
+                ctx.handle, C.byref(r), C.byref(m), dptr(self._signals), C.byref(g), C.byref(mk),
+                C.byref(c), C.byref(p), C.byref(h)))
         self._h = h
         self.n_params = SirenSpec(cfg.hidden, cfg.sine_layers, cfg.omega0, cfg.out_scale,
                                   meta.background_sos).param_count()
@@ -477,11 +500,26 @@ class Trainer:
     def buffer(self, what: int) -> int:
         return int(_abi.lib().pact_trainer_buffer(self._h, what) or 0)
 
+    def phase(self, k: int):
+        """pact_trainer_phase: one phase of the iteration (0-3) or of the final
+        image (4-5); asynchronous on the engine stream."""
+        check(_abi.lib().pact_trainer_phase(self._h, int(k)))
+
+    def local(self) -> dict:
+        """The partition this trainer owns (pact_trainer_local)."""
+        info = (C.c_int32 * 7)()
+        check(_abi.lib().pact_trainer_local(self._h, info))
+        keys = ("patch_lo", "patch_hi", "pixel_lo", "pixel_hi", "n_patches", "rank", "world")
+        return dict(zip(keys, list(info)))
+
+    def view(self, what: int, shape, dtype: torch.dtype) -> torch.Tensor:
+        """A zero-copy torch view of an engine buffer (see pact_trainer_buffer)."""
+        return _device_view(self.buffer(what), shape, dtype)
+
     def read(self, what: int, shape, dtype) -> np.ndarray:
         """Copy an engine buffer (see pact_trainer_buffer) to the host."""
         out = np.zeros(shape, dtype)
-        check(_abi.lib().pact_trainer_step(self._h, 0))
-        torch.cuda.synchronize()
+        self.stream().synchronize()
         check(_abi.lib().pact_download(self.ctx.handle, C.c_void_p(out.ctypes.data),
                                        C.c_void_p(self.buffer(what)), out.nbytes))
         return out

@@ -102,13 +102,13 @@ __device__ __forceinline__ int patch_offset(int i, int n, int stride, int last) 
 
 // Y[patch][j] = FFT2(stack[j][oy:oy+P, ox:ox+P])       grid (n_patches, K)
 __global__ void patch_fft_kernel(LayoutDev L, const float* __restrict__ stack, int K, int logP,
-                                 float2* __restrict__ Y) {
+                                 float2* __restrict__ Y, int p_lo) {
   extern __shared__ float2 sm[];
   const int P = L.P, P2 = P * P;
   float2* buf = sm;
   float2* tw = sm + P2;
   float2* scratch = tw + P;
-  const int patch = blockIdx.x, j = blockIdx.y;
+  const int patch = p_lo + blockIdx.x, j = blockIdx.y;  // Y is indexed from p_lo
   const int px = patch % L.nx, py = patch / L.nx;
   const int ox = patch_offset(px, L.nx, L.stride, L.last_x);
   const int oy = patch_offset(py, L.ny, L.stride, L.last_y);
@@ -120,7 +120,7 @@ __global__ void patch_fft_kernel(LayoutDev L, const float* __restrict__ stack, i
   }
   __syncthreads();
   fft2d(buf, scratch, tw, P, logP);
-  float2* out = Y + (static_cast<size_t>(patch) * K + j) * P2;
+  float2* out = Y + (static_cast<size_t>(blockIdx.x) * K + j) * P2;
   for (int e = threadIdx.x; e < P2; e += blockDim.x) out[e] = buf[e];
 }
 
@@ -144,8 +144,12 @@ __global__ void patch_ifft_real_kernel(int P, int logP, const float2* __restrict
 
 // merge_patches (deconv.hpp:142-164) in gather form: every pixel sums the
 // windowed values of the (<= 3x3) patches covering it in layout order.
+// patches holds the patches [p_lo, p_hi) (indexed from p_lo); with num/den set
+// the kernel writes the accumulators sum w x, sum w of those patches instead
+// of the image (a partitioned merge, reduced across ranks by the caller).
 __global__ void merge_kernel(LayoutDev L, const float* __restrict__ patches,
-                             const float* __restrict__ win, float* __restrict__ img) {
+                             const float* __restrict__ win, float* __restrict__ img, int p_lo,
+                             int p_hi, float* __restrict__ num, float* __restrict__ den) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= L.W * L.H) return;
   int y = i / L.W, x = i - y * L.W;
@@ -171,13 +175,20 @@ __global__ void merge_kernel(LayoutDev L, const float* __restrict__ patches,
         px = L.nx - 1;
       }
       const int ox = patch_offset(px, L.nx, L.stride, L.last_x);
+      const int pi = py * L.nx + px;
+      if (pi < p_lo || pi >= p_hi) continue;
       const int q = (y - oy) * P + (x - ox);
       const float w = win[q];
-      acc += w * patches[static_cast<size_t>(py * L.nx + px) * P * P + q];
+      acc += w * patches[static_cast<size_t>(pi - p_lo) * P * P + q];
       ws += w;
     }
   }
-  img[i] = ws > 0.f ? acc / ws : 0.f;
+  if (num) {
+    num[i] = acc;
+    den[i] = ws;
+  } else {
+    img[i] = ws > 0.f ? acc / ws : 0.f;
+  }
 }
 
 int ilog2_exact(int P) {
@@ -207,7 +218,8 @@ LayoutDev layout_dev(const pact_layout& l) {
 }  // namespace
 
 Status launch_patch_fft(pact_ctx* ctx, const pact_layout& lay, const float* stack, int K,
-                        float2* Y) {
+                        float2* Y, int p_lo, int p_hi) {
+  if (p_hi < 0) p_hi = lay.nx * lay.ny;
   const int P = lay.patch_pixels, logP = ilog2_exact(P);
   size_t smem = fft_smem(P, logP);
   if (smem > 220 * 1024) return validation("extract_patch_spectra: patch too large for the device FFT");
@@ -217,8 +229,9 @@ Status launch_patch_fft(pact_ctx* ctx, const pact_layout& lay, const float* stac
                                      (int)smem));
     configured = smem;
   }
-  dim3 g(lay.nx * lay.ny, K);
-  patch_fft_kernel<<<g, 512, smem, ctx->stream>>>(layout_dev(lay), stack, K, logP, Y);
+  if (p_hi <= p_lo) return {};
+  dim3 g(p_hi - p_lo, K);
+  patch_fft_kernel<<<g, 512, smem, ctx->stream>>>(layout_dev(lay), stack, K, logP, Y, p_lo);
   return after_launch(ctx, "patch_fft_kernel");
 }
 
@@ -238,7 +251,16 @@ Status launch_patch_ifft_real(pact_ctx* ctx, int P, int n_patches, const float2*
 Status launch_merge(pact_ctx* ctx, const pact_layout& lay, const float* patches, const float* win,
                     float* img) {
   int n = lay.grid.width * lay.grid.height;
-  merge_kernel<<<div_up(n, 256), 256, 0, ctx->stream>>>(layout_dev(lay), patches, win, img);
+  merge_kernel<<<div_up(n, 256), 256, 0, ctx->stream>>>(layout_dev(lay), patches, win, img, 0,
+                                                         lay.nx * lay.ny, nullptr, nullptr);
+  return after_launch(ctx, "merge_kernel");
+}
+
+Status launch_merge_partial(pact_ctx* ctx, const pact_layout& lay, const float* patches,
+                            const float* win, int p_lo, int p_hi, float* num, float* den) {
+  int n = lay.grid.width * lay.grid.height;
+  merge_kernel<<<div_up(n, 256), 256, 0, ctx->stream>>>(layout_dev(lay), patches, win, nullptr,
+                                                         p_lo, p_hi, num, den);
   return after_launch(ctx, "merge_kernel");
 }
 

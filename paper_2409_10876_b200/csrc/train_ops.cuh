@@ -29,11 +29,15 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
 Status launch_wiener(pact_ctx* ctx, const FourierTab& t, const float2* Y, const float* w,
                      int n_patches, double eps, float2* X);
 
+// Spectra of the patches [p_lo, p_hi) (p_hi < 0: all), Y indexed from p_lo.
 Status launch_patch_fft(pact_ctx* ctx, const pact_layout& lay, const float* stack, int K,
-                        float2* Y);
+                        float2* Y, int p_lo = 0, int p_hi = -1);
 Status launch_patch_ifft_real(pact_ctx* ctx, int P, int n_patches, const float2* X, float* out);
 Status launch_merge(pact_ctx* ctx, const pact_layout& lay, const float* patches, const float* win,
                     float* img);
+// Merge accumulators (sum w x, sum w) of the patches [p_lo, p_hi) only.
+Status launch_merge_partial(pact_ctx* ctx, const pact_layout& lay, const float* patches,
+                            const float* win, int p_lo, int p_hi, float* num, float* den);
 
 Status launch_tv(pact_ctx* ctx, const float* v, const unsigned char* inmask, const int* idx, int n,
                  int W, int H, double lambda, float* grad, double* partial, int n_blocks);

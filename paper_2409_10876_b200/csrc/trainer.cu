@@ -55,6 +55,12 @@ struct pact_trainer {
   double v0 = 0.0;
   pact_layout lay{};
   int n_patches = 0, P = 0, K = 0, A = 0, n_params = 0;
+  // partition: this rank owns patches [p_lo, p_hi) (whole
+  // patch rows) and masked pixels [m_lo, m_hi) of the row-major list; the
+  // caller all-reduces dv, dL/dv, the report and the gradient between phases
+  int rank = 0, world = 1, p_lo = 0, p_hi = 0, n_local = 0, m_lo = 0, m_hi = 0;
+  float* num = nullptr;  // merge accumulators of the final image (world > 1)
+  float* den = nullptr;
   double loss_scale = 0.0;
   SirenShape shape;
   MaskedPixels mp;
@@ -91,33 +97,55 @@ struct pact_trainer {
 
 namespace {
 
-Status enqueue_step(pact_trainer* tr) {
+// The iteration in four phases; a partitioned trainer (world > 1) runs them
+// one at a time with the caller's all-reduces in between:
+//   0 render    -> all-reduce dv (SUM; each pixel has one owner)
+//   1 rays/loss -> all-reduce dL/dv (SUM), report[0..3) (SUM), flags (MAX)
+//   2 SIREN bwd -> all-reduce the gradient (SUM)
+//   3 Adam (replicated)
+Status enqueue_phase(pact_trainer* tr, int phase) {
   pact_ctx* ctx = &tr->eng;
   const size_t npx = static_cast<size_t>(tr->grid.width) * tr->grid.height;
-  // render_sos (optimize.hpp:413) + finiteness (414-417)
-  PACT_TRY_S(siren_forward(ctx, tr->shape, tr->theta32, tr->sw, tr->dv));
-  PACT_TRY_S(launch_check_finite_f32(ctx, tr->dv, tr->sw.idx, tr->mp.n, kFlagSos, tr->flags));
-  // wavefront_profile for every patch (431-433)
-  PACT_TRY_S(launch_wavefront(ctx, tr->ray, tr->w));
-  // fused_patch_loss_grad (434-436)
-  PACT_TRY_S(launch_loss_grad(ctx, tr->ftab.tab, tr->Y, tr->w, tr->n_patches, tr->cfg.eps_deconv,
-                              tr->loss_scale, tr->cfg.implicit_xhat_grad != 0, tr->loss_patch,
-                              tr->dw));
-  // wavefront_grad_trace into dL/dv (437-438)
-  PACT_CUDA_S(cudaMemsetAsync(tr->gv, 0, sizeof(double) * npx, ctx->stream));
-  PACT_TRY_S(launch_ray_backward(ctx, tr->ray, tr->dw, tr->gv));
-  // tv_loss (448) and the loss report / checks (442-451)
-  PACT_TRY_S(launch_tv(ctx, tr->dv, tr->inmask, tr->sw.idx, tr->mp.n, tr->grid.width,
-                       tr->grid.height, tr->cfg.lambda_tv, tr->gtv, tr->tv_partial, tr->n_tv));
-  PACT_TRY_S(launch_step_report(ctx, tr->loss_patch, tr->n_patches, tr->tv_partial, tr->n_tv,
-                                tr->cfg.lambda_tv, tr->report, tr->flags));
-  // backprop_sos of (dL/dv at masked pixels + TV gradient) (453-461)
-  PACT_TRY_S(siren_backward(ctx, tr->shape, tr->theta32, tr->sw, tr->gv, tr->gtv, tr->grad));
-  PACT_TRY_S(launch_check_finite_f64(ctx, tr->grad, tr->n_params, kFlagGrad, tr->flags));
-  // adam_step (466-467)
-  PACT_TRY_S(launch_adam(ctx, tr->n_params, tr->theta, tr->grad, tr->m, tr->v, tr->t,
+  switch (phase) {
+    case 0:
+      // render_sos (optimize.hpp:413) + finiteness (414-417)
+      if (tr->world > 1)  // foreign pixels stay 0 for the all-reduce
+        PACT_CUDA_S(cudaMemsetAsync(tr->dv, 0, sizeof(float) * npx, ctx->stream));
+      PACT_TRY_S(siren_forward(ctx, tr->shape, tr->theta32, tr->sw, tr->dv));
+      PACT_TRY_S(launch_check_finite_f32(ctx, tr->dv, tr->sw.idx, tr->mp.n, kFlagSos, tr->flags));
+      return {};
+    case 1:
+      // wavefront_profile for every (local) patch (431-433)
+      PACT_TRY_S(launch_wavefront(ctx, tr->ray, tr->w));
+      // fused_patch_loss_grad (434-436)
+      PACT_TRY_S(launch_loss_grad(ctx, tr->ftab.tab, tr->Y, tr->w, tr->n_local,
+                                  tr->cfg.eps_deconv, tr->loss_scale,
+                                  tr->cfg.implicit_xhat_grad != 0, tr->loss_patch, tr->dw));
+      // wavefront_grad_trace into dL/dv (437-438)
+      PACT_CUDA_S(cudaMemsetAsync(tr->gv, 0, sizeof(double) * npx, ctx->stream));
+      PACT_TRY_S(launch_ray_backward(ctx, tr->ray, tr->dw, tr->gv));
+      // tv_loss (448) and the loss report / checks (442-451)
+      PACT_TRY_S(launch_tv(ctx, tr->dv, tr->inmask, tr->sw.idx, tr->mp.n, tr->grid.width,
+                           tr->grid.height, tr->cfg.lambda_tv, tr->gtv, tr->tv_partial, tr->n_tv));
+      PACT_TRY_S(launch_step_report(ctx, tr->loss_patch, tr->n_local, tr->tv_partial, tr->n_tv,
+                                    tr->cfg.lambda_tv, tr->report, tr->flags));
+      return {};
+    case 2:
+      // backprop_sos of (dL/dv at masked pixels + TV gradient) (453-461)
+      return siren_backward(ctx, tr->shape, tr->theta32, tr->sw, tr->gv, tr->gtv, tr->grad);
+    case 3:
+      PACT_TRY_S(launch_check_finite_f64(ctx, tr->grad, tr->n_params, kFlagGrad, tr->flags));
+      // adam_step (466-467)
+      return launch_adam(ctx, tr->n_params, tr->theta, tr->grad, tr->m, tr->v, tr->t,
                          tr->cfg.learning_rate, tr->cfg.beta1, tr->cfg.beta2, tr->cfg.adam_eps,
-                         tr->flags, tr->theta32, true));
+                         tr->flags, tr->theta32, true);
+    default:
+      return validation("pact_trainer_phase: unknown phase");
+  }
+}
+
+Status enqueue_step(pact_trainer* tr) {
+  for (int ph = 0; ph < 4; ++ph) PACT_TRY_S(enqueue_phase(tr, ph));
   return {};
 }
 
@@ -136,7 +164,7 @@ Status profile_step(pact_trainer* tr, float* ms) {
   PACT_CUDA_S(cudaEventRecord(ev[1], s));
   PACT_TRY_S(launch_wavefront(ctx, tr->ray, tr->w));
   PACT_CUDA_S(cudaEventRecord(ev[2], s));
-  PACT_TRY_S(launch_loss_grad(ctx, tr->ftab.tab, tr->Y, tr->w, tr->n_patches, tr->cfg.eps_deconv,
+  PACT_TRY_S(launch_loss_grad(ctx, tr->ftab.tab, tr->Y, tr->w, tr->n_local, tr->cfg.eps_deconv,
                               tr->loss_scale, tr->cfg.implicit_xhat_grad != 0, tr->loss_patch,
                               tr->dw));
   PACT_CUDA_S(cudaEventRecord(ev[3], s));
@@ -145,7 +173,7 @@ Status profile_step(pact_trainer* tr, float* ms) {
   PACT_CUDA_S(cudaEventRecord(ev[4], s));
   PACT_TRY_S(launch_tv(ctx, tr->dv, tr->inmask, tr->sw.idx, tr->mp.n, tr->grid.width,
                        tr->grid.height, tr->cfg.lambda_tv, tr->gtv, tr->tv_partial, tr->n_tv));
-  PACT_TRY_S(launch_step_report(ctx, tr->loss_patch, tr->n_patches, tr->tv_partial, tr->n_tv,
+  PACT_TRY_S(launch_step_report(ctx, tr->loss_patch, tr->n_local, tr->tv_partial, tr->n_tv,
                                 tr->cfg.lambda_tv, tr->report, tr->flags));
   PACT_CUDA_S(cudaEventRecord(ev[5], s));
   PACT_TRY_S(siren_backward(ctx, tr->shape, tr->theta32, tr->sw, tr->gv, tr->gtv, tr->grad));
@@ -223,11 +251,15 @@ int pact_train_config_default(pact_train_config* c) {
   return PACT_OK;
 }
 
-int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_meta* meta,
-                        const float* signals, const pact_grid* grid, const pact_mask* mask,
-                        const pact_train_config* cfg, pact_trainer** out) {
-  if (!ctx || !ring || !meta || !signals || !grid || !mask || !cfg || !out)
+int pact_trainer_create_partitioned(pact_ctx* ctx, const pact_ring* ring,
+                                    const pact_signal_meta* meta, const float* signals,
+                                    const pact_grid* grid, const pact_mask* mask,
+                                    const pact_train_config* cfg, const pact_partition* part,
+                                    pact_trainer** out) {
+  if (!ctx || !ring || !meta || !signals || !grid || !mask || !cfg || !out || !part)
     return validation("pact_trainer_create: null argument").code;
+  if (part->world < 1 || part->rank < 0 || part->rank >= part->world)
+    return validation("pact_trainer_create: invalid partition").code;
   *out = nullptr;
   // TrainConfig::validate (optimize.hpp:71-77), SignalSet::validate, v0 (369-371)
   if (cfg->epochs < 1) return validation("train: epochs must be >= 1").code;
@@ -268,6 +300,12 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
   Status st = make_layout(*grid, cfg->patch_mm, cfg->overlap, tr->lay);
   if (!st.ok()) return fail(st.code);
   tr->n_patches = tr->lay.nx * tr->lay.ny;
+  if (part->world > tr->lay.ny) return fail(validation("partition: more ranks than patch rows").code);
+  tr->rank = part->rank;
+  tr->world = part->world;
+  tr->p_lo = (tr->lay.ny * part->rank / part->world) * tr->lay.nx;
+  tr->p_hi = (tr->lay.ny * (part->rank + 1) / part->world) * tr->lay.nx;
+  tr->n_local = tr->p_hi - tr->p_lo;
   tr->P = tr->lay.patch_pixels;
   tr->K = cfg->n_delays;
   tr->A = cfg->n_angles;
@@ -288,7 +326,17 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
   st = merge_window(cfg->merge_fwhm, tr->P, grid->pitch, win);
   if (!st.ok()) return fail(st.code);
   trace.mark("layout + window");
-  tr->mp = masked_pixels(*grid, *mask);
+  const MaskedPixels mp_all = masked_pixels(*grid, *mask);
+  if (mp_all.n < tr->world) return fail(validation("partition: fewer masked pixels than ranks").code);
+  tr->m_lo = static_cast<int>(static_cast<int64_t>(mp_all.n) * tr->rank / tr->world);
+  tr->m_hi = static_cast<int>(static_cast<int64_t>(mp_all.n) * (tr->rank + 1) / tr->world);
+  if (tr->world == 1) {
+    tr->mp = mp_all;
+  } else {
+    tr->mp.n = tr->m_hi - tr->m_lo;
+    tr->mp.idx.assign(mp_all.idx.begin() + tr->m_lo, mp_all.idx.begin() + tr->m_hi);
+    tr->mp.coords.assign(mp_all.coords.begin() + 2 * tr->m_lo, mp_all.coords.begin() + 2 * tr->m_hi);
+  }
   trace.mark("masked pixels");
 
   // ---- device arena ----
@@ -298,11 +346,11 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
   size_t bytes = 0;
   auto add = [&](size_t b) { bytes += (b + 255) & ~size_t(255); };
   add(sizeof(float) * tr->K * npx);                              // stack
-  add(sizeof(float2) * tr->n_patches * tr->K * P2);              // Y
+  add(sizeof(float2) * tr->n_local * tr->K * P2);                // Y (local patches)
   add(sizeof(float) * npx);                                      // dv
-  add(sizeof(float) * tr->n_patches * tr->A);                    // w
-  add(sizeof(float) * tr->n_patches * tr->A);                    // dw
-  add(sizeof(double) * tr->n_patches);                           // loss_patch
+  add(sizeof(float) * tr->n_local * tr->A);                      // w
+  add(sizeof(float) * tr->n_local * tr->A);                      // dw
+  add(sizeof(double) * tr->n_local);                             // loss_patch
   add(sizeof(double) * npx);                                     // gv
   add(sizeof(float) * std::max(tr->mp.n, 1));                    // gtv
   add(sizeof(double) * tr->n_tv);                                // tv_partial
@@ -312,18 +360,19 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
   add(64);                                                       // flags
   add(sizeof(double) * 4);                                       // report
   add(sizeof(long long));                                        // t
-  add(sizeof(double2) * tr->n_patches);                          // centers
+  add(sizeof(double2) * tr->n_local);                            // centers
   add(sizeof(float) * P2);                                       // window
+  if (tr->world > 1) add(sizeof(float) * 2 * npx);               // num, den
   bytes += 64 * 256;  // per-carve alignment slack
   st = pool_alloc(&tr->arena, bytes, tr->eng.stream);
   if (!st.ok()) return fail(st.code);
   char* p = static_cast<char*>(tr->arena);
   tr->stack = carve<float>(p, tr->K * npx);
-  tr->Y = carve<float2>(p, tr->n_patches * tr->K * P2);
+  tr->Y = carve<float2>(p, tr->n_local * tr->K * P2);
   tr->dv = carve<float>(p, npx);
-  tr->w = carve<float>(p, tr->n_patches * tr->A);
-  tr->dw = carve<float>(p, tr->n_patches * tr->A);
-  tr->loss_patch = carve<double>(p, tr->n_patches);
+  tr->w = carve<float>(p, tr->n_local * tr->A);
+  tr->dw = carve<float>(p, tr->n_local * tr->A);
+  tr->loss_patch = carve<double>(p, tr->n_local);
   tr->gv = carve<double>(p, npx);
   tr->gtv = carve<float>(p, std::max(tr->mp.n, 1));
   tr->tv_partial = carve<double>(p, tr->n_tv);
@@ -336,8 +385,12 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
   tr->flags = carve<unsigned>(p, 16);
   tr->report = carve<double>(p, 4);
   tr->t = carve<long long>(p, 1);
-  tr->centers = carve<double2>(p, tr->n_patches);
+  tr->centers = carve<double2>(p, tr->n_local);
   tr->win = carve<float>(p, P2);
+  if (tr->world > 1) {
+    tr->num = carve<float>(p, npx);
+    tr->den = carve<float>(p, npx);
+  }
 
   trace.mark("arena");
   pact_ctx* e = &tr->eng;
@@ -350,7 +403,7 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
   cudaEventDestroy(ev);
 
   std::vector<unsigned char> flag(npx, 0);
-  for (int i : tr->mp.idx) flag[i] = 1;
+  for (int i : mp_all.idx) flag[i] = 1;
   std::vector<double> theta(tr->n_params);
   pact_siren sp{2, cfg->hidden, cfg->sine_layers, cfg->omega0, cfg->out_scale, v0};
   int rc = pact_init_siren(cfg->seed, &sp, theta.data());
@@ -372,8 +425,8 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
                          cudaMemcpyHostToDevice, s));
   TRY_CU(cudaMemcpyAsync(tr->theta32, theta32.data(), sizeof(float) * tr->n_params,
                          cudaMemcpyHostToDevice, s));
-  TRY_CU(cudaMemcpyAsync(tr->centers, centers.data(), sizeof(double2) * tr->n_patches,
-                         cudaMemcpyHostToDevice, s));
+  TRY_CU(cudaMemcpyAsync(tr->centers, centers.data() + 2 * tr->p_lo,
+                         sizeof(double2) * tr->n_local, cudaMemcpyHostToDevice, s));
   TRY_CU(cudaMemcpyAsync(tr->win, win.data(), sizeof(float) * P2, cudaMemcpyHostToDevice, s));
   TRY_CU(cudaMemsetAsync(tr->m, 0, sizeof(double) * tr->n_params, s));
   TRY_CU(cudaMemsetAsync(tr->v, 0, sizeof(double) * tr->n_params, s));
@@ -382,13 +435,13 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
   TRY_CU(cudaMemsetAsync(tr->dv, 0, sizeof(float) * npx, s));
   tr->ray.dv = tr->dv;
   tr->ray.centers = tr->centers;
-  tr->ray.n_rays = tr->n_patches * tr->A;
+  tr->ray.n_rays = tr->n_local * tr->A;
   make_raster_texture(tr->dv, grid->width, grid->height, &tr->ray.tex);
   trace.mark("uploads + texture");
   // DAS stack + spectra, once (optimize.hpp:380-392)
   TRY_ST(das_stack_device(e, *ring, *meta, signals, *grid, v0, tr->delays.data(), tr->K,
                           tr->stack));
-  TRY_ST(launch_patch_fft(e, tr->lay, tr->stack, tr->K, tr->Y));
+  TRY_ST(launch_patch_fft(e, tr->lay, tr->stack, tr->K, tr->Y, tr->p_lo, tr->p_hi));
   trace.mark("DAS + FFT launched");
   TRY_ST(siren_work_alloc(tr->sw, tr->mp, tr->shape, s));
   trace.mark("siren work");
@@ -402,8 +455,62 @@ int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_
 #undef TRY_ST
 }
 
+int pact_trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_meta* meta,
+                        const float* signals, const pact_grid* grid, const pact_mask* mask,
+                        const pact_train_config* cfg, pact_trainer** out) {
+  const pact_partition whole{0, 1};
+  return pact_trainer_create_partitioned(ctx, ring, meta, signals, grid, mask, cfg, &whole, out);
+}
+
+int pact_trainer_phase(pact_trainer* tr, int32_t phase) {
+  if (!tr) return validation("pact_trainer_phase: null trainer").code;
+  pact_ctx* e = &tr->eng;
+  const size_t npx = static_cast<size_t>(tr->grid.width) * tr->grid.height;
+  const size_t P2 = static_cast<size_t>(tr->P) * tr->P;
+  if (phase >= 0 && phase <= 3) {
+    PACT_TRY(enqueue_phase(tr, phase));
+    if (phase == 3) ++tr->steps_done;
+    return PACT_OK;
+  }
+  if (phase == 4) {  // final render (optimize.hpp:478): local pixels into a cleared dv
+    if (tr->world > 1) PACT_CUDA(cudaMemsetAsync(tr->dv, 0, sizeof(float) * npx, e->stream));
+    PACT_TRY(siren_forward(e, tr->shape, tr->theta32, tr->sw, tr->dv));
+    return PACT_OK;
+  }
+  if (phase == 5) {  // final deconvolution of the local patches -> merge accumulators
+    if (tr->world == 1) return validation("pact_trainer_phase: phase 5 needs a partition").code;
+    PACT_TRY(launch_wavefront(e, tr->ray, tr->w));
+    void* tmp = nullptr;
+    PACT_TRY(scratch_get(e, kScratchGeneric1, sizeof(float2) * tr->n_local * P2 +
+                                                  sizeof(float) * tr->n_local * P2 + 256,
+                         &tmp));
+    float2* X = static_cast<float2*>(tmp);
+    float* patches = reinterpret_cast<float*>(X + tr->n_local * P2);
+    PACT_TRY(launch_wiener(e, tr->ftab.tab, tr->Y, tr->w, tr->n_local, tr->cfg.eps_deconv, X));
+    PACT_TRY(launch_patch_ifft_real(e, tr->P, tr->n_local, X, patches));
+    PACT_TRY(launch_merge_partial(e, tr->lay, patches, tr->win, tr->p_lo, tr->p_hi, tr->num,
+                                  tr->den));
+    return PACT_OK;
+  }
+  return validation("pact_trainer_phase: unknown phase").code;
+}
+
+int pact_trainer_local(pact_trainer* tr, int32_t* info) {
+  if (!tr || !info) return validation("pact_trainer_local: null argument").code;
+  info[0] = tr->p_lo;
+  info[1] = tr->p_hi;
+  info[2] = tr->m_lo;
+  info[3] = tr->m_hi;
+  info[4] = tr->n_patches;
+  info[5] = tr->rank;
+  info[6] = tr->world;
+  return PACT_OK;
+}
+
 int pact_trainer_step(pact_trainer* tr, int32_t n_steps) {
   if (!tr) return validation("pact_trainer_step: null trainer").code;
+  if (tr->world > 1)
+    return validation("pact_trainer_step: a partitioned trainer steps by phases").code;
   for (int i = 0; i < n_steps; ++i) {
     if (tr->graph) {
       PACT_CUDA(cudaGraphLaunch(tr->graph, tr->eng.stream));
@@ -464,6 +571,8 @@ int pact_trainer_run_epoch(pact_trainer* tr, int32_t epoch, double* report4) {
 
 int pact_trainer_finish(pact_trainer* tr, float* image, float* sos) {
   if (!tr) return validation("pact_trainer_finish: null trainer").code;
+  if (tr->world > 1)
+    return validation("pact_trainer_finish: a partitioned trainer finishes by phases 4/5").code;
   pact_ctx* e = &tr->eng;
   const size_t npx = static_cast<size_t>(tr->grid.width) * tr->grid.height;
   const size_t P2 = static_cast<size_t>(tr->P) * tr->P;
@@ -522,6 +631,11 @@ void* pact_trainer_buffer(pact_trainer* tr, int32_t what) {
     case 5: return tr->gv;
     case 6: return tr->grad;
     case 7: return tr->theta;
+    case 8: return tr->report;
+    case 9: return tr->flags;
+    case 10: return tr->num;
+    case 11: return tr->den;
+    case 12: return tr->theta32;
     default: return nullptr;
   }
 }
