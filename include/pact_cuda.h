@@ -392,6 +392,20 @@ int pact_joint_reconstruct(pact_ctx* ctx, const pact_ring* ring, const pact_sign
                            const pact_train_config* cfg, double* reports, float* image,
                            float* sos, double* theta);
 
+/* joint_reconstruct of n_frames independent frames of one geometry (cfg4),
+ * run concurrently on one GPU (one engine stream per frame; every frame's
+ * epoch is enqueued before the reports are read).  Results are identical to
+ * n_frames separate pact_joint_reconstruct calls.
+ *   signals[f]: device fp32 [N][T];  cfgs[f]: per-frame TrainConfig (equal epochs)
+ *   reports: HOST double[n_frames][epochs][4] (wall_s = the batch's epoch time)
+ *   images[f], sos[f]: device fp32 [H][W] (arrays may be NULL)
+ *   thetas: HOST fp64 [n_frames][P] (may be NULL) */
+int pact_joint_reconstruct_batch(pact_ctx* ctx, int32_t n_frames, const pact_ring* ring,
+                                 const pact_signal_meta* meta, const float* const* signals,
+                                 const pact_grid* grid, const pact_mask* mask,
+                                 const pact_train_config* cfgs, double* reports,
+                                 float* const* images, float* const* sos, double* thetas);
+
 #ifdef __cplusplus
 }
 #endif

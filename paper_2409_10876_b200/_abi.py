@@ -169,6 +169,10 @@ SIGNATURES = {
     "pact_trainer_launch_count": (C.c_int64, [_P]),
     "pact_trainer_stream": (_P, [_P]),
     "pact_trainer_profile_step": (C.c_int, [_P, _FP]),
+    "pact_joint_reconstruct_batch": (C.c_int, [_P, _I, C.POINTER(Ring), C.POINTER(SignalMeta),
+                                               C.POINTER(_P), C.POINTER(Grid), C.POINTER(Mask),
+                                               C.POINTER(TrainConfig), _DP, C.POINTER(_P),
+                                               C.POINTER(_P), _DP]),
     "pact_joint_reconstruct": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(SignalMeta), _P,
                                          C.POINTER(Grid), C.POINTER(Mask),
                                          C.POINTER(TrainConfig), _DP, _P, _P, _DP]),

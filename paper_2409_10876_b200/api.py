@@ -569,3 +569,36 @@ def joint_reconstruct(ctx: Context, signals: torch.Tensor, ring: RingGeometry,
                                             dptr(img), dptr(sos),
                                             th.ctypes.data_as(C.POINTER(C.c_double))))
     return reps, img, sos, th
+
+
+def joint_reconstruct_batch(ctx: Context, signals: list, ring: RingGeometry, meta: SignalMetaInfo,
+                            grid: GridSpec, mask: CircularMask, cfgs: list,
+                            images: list | None = None, sos: list | None = None):
+    """pact_joint_reconstruct_batch: joint_reconstruct of several frames of one
+    geometry run concurrently (one engine stream each); identical results to
+    separate joint_reconstruct calls.  -> (reports [n, epochs, 4], images, sos, thetas)."""
+    n = len(signals)
+    assert len(cfgs) == n and n > 0
+    cs = [c.c() for c in cfgs]  # keep each delays array alive
+    carr = (_abi.TrainConfig * n)(*[c for c, _ in cs])
+    sigs = [s.contiguous() for s in signals]
+    sig_p = (C.c_void_p * n)(*[s.data_ptr() for s in sigs])
+    if images is None:
+        images = [torch.empty((grid.height, grid.width), device="cuda", dtype=torch.float32)
+                  for _ in range(n)]
+    if sos is None:
+        sos = [torch.empty((grid.height, grid.width), device="cuda", dtype=torch.float32)
+               for _ in range(n)]
+    img_p = (C.c_void_p * n)(*[t.data_ptr() for t in images])
+    sos_p = (C.c_void_p * n)(*[t.data_ptr() for t in sos])
+    c0 = cfgs[0]
+    P = SirenSpec(c0.hidden, c0.sine_layers, c0.omega0, c0.out_scale,
+                  meta.background_sos).param_count()
+    reps = np.zeros((n, c0.epochs, 4))
+    ths = np.zeros((n, P), np.float64)
+    r, m, g, mk = ring.c(), meta.c(), grid.c(), mask.c()
+    check(_abi.lib().pact_joint_reconstruct_batch(
+        ctx.handle, n, C.byref(r), C.byref(m), sig_p, C.byref(g), C.byref(mk), carr,
+        reps.ctypes.data_as(C.POINTER(C.c_double)), img_p, sos_p,
+        ths.ctypes.data_as(C.POINTER(C.c_double))))
+    return reps, images, sos, ths

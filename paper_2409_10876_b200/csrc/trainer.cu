@@ -691,4 +691,54 @@ int pact_joint_reconstruct(pact_ctx* ctx, const pact_ring* ring, const pact_sign
   return rc;
 }
 
+int pact_joint_reconstruct_batch(pact_ctx* ctx, int32_t n_frames, const pact_ring* ring,
+                                 const pact_signal_meta* meta, const float* const* signals,
+                                 const pact_grid* grid, const pact_mask* mask,
+                                 const pact_train_config* cfgs, double* reports,
+                                 float* const* images, float* const* sos, double* thetas) {
+  if (!ctx || n_frames < 0 || (n_frames > 0 && (!signals || !cfgs)))
+    return validation("pact_joint_reconstruct_batch: null argument").code;
+  std::vector<pact_trainer*> trs(n_frames, nullptr);
+  auto cleanup = [&](int rc) {
+    for (pact_trainer* t : trs) pact_trainer_destroy(t);
+    return rc;
+  };
+  const int epochs = n_frames > 0 ? cfgs[0].epochs : 0;
+  for (int f = 0; f < n_frames; ++f) {
+    if (cfgs[f].epochs != epochs)
+      return cleanup(validation("pact_joint_reconstruct_batch: frames need equal epochs").code);
+    int rc = pact_trainer_create(ctx, ring, meta, signals[f], grid, mask, &cfgs[f], &trs[f]);
+    if (rc) return cleanup(rc);
+  }
+  int n_params = 0;
+  if (n_frames > 0) n_params = trs[0]->n_params;
+  for (int e = 1; e <= epochs; ++e) {
+    auto t0 = std::chrono::steady_clock::now();
+    // every frame's steps are enqueued before any report waits: the frames
+    // run concurrently, one engine stream each
+    for (int f = 0; f < n_frames; ++f) {
+      int rc = pact_trainer_step(trs[f], trs[f]->cfg.steps_per_epoch);
+      if (rc) return cleanup(rc);
+    }
+    for (int f = 0; f < n_frames; ++f) {
+      double rep[3];
+      int rc = pact_trainer_report(trs[f], e, rep);
+      if (rc) return cleanup(rc);
+      if (reports) {
+        double* r = reports + (static_cast<size_t>(f) * epochs + (e - 1)) * 4;
+        r[0] = rep[0];
+        r[1] = rep[1];
+        r[2] = rep[2];
+        r[3] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      }
+    }
+  }
+  for (int f = 0; f < n_frames; ++f) {
+    int rc = pact_trainer_finish(trs[f], images ? images[f] : nullptr, sos ? sos[f] : nullptr);
+    if (!rc && thetas) rc = pact_trainer_get_theta(trs[f], thetas + static_cast<size_t>(f) * n_params);
+    if (rc) return cleanup(rc);
+  }
+  return cleanup(PACT_OK);
+}
+
 }  // extern "C"

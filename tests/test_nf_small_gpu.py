@@ -190,3 +190,17 @@ def test_training_is_deterministic(ctx, G, si):
     assert np.array_equal(a[3], b[3])
     for e in range(3):
         assert a[0][e, 2] == pytest.approx(a[0][e, 0] + a[0][e, 1], rel=1e-12)
+
+
+def test_batched_joint_reconstruct_equals_separate_calls(ctx, G, si):
+    from paper_2409_10876_b200.api import joint_reconstruct_batch
+
+    cfgs = [replace(si.cfg, epochs=2, steps_per_epoch=2, seed=s) for s in (5, 7, 9)]
+    sig = torch.as_tensor(G["sig"]).cuda()
+    reps, imgs, soss, ths = joint_reconstruct_batch(ctx, [sig, sig, sig], si.ring, _meta(G),
+                                                    si.grid, si.mask, cfgs)
+    for f, cfg in enumerate(cfgs):
+        r, img, sos, th = joint_reconstruct(ctx, sig, si.ring, _meta(G), si.grid, si.mask, cfg)
+        assert np.array_equal(reps[f][:, :3], r[:, :3])
+        assert torch.equal(imgs[f], img) and torch.equal(soss[f], sos)
+        assert np.array_equal(ths[f], th)
