@@ -32,6 +32,27 @@
 #define TC_EXP 0
 #endif
 
+#if TC_EXP == 5 || TC_EXP == 6
+// Timeline trace of CTA 0 (experiments only): {tag, tile/chunk, globaltimer ns},
+// one region per tracing role, store-only (no atomics on the traced path).
+__device__ unsigned long long g_trace[3 * 4096];
+__device__ unsigned int g_trace_n;
+__device__ __forceinline__ void trace(int tag, int idx) {
+  if (blockIdx.x != 0) return;
+  static __shared__ unsigned int s_cnt[3];
+  const int role = tag <= 4 ? 0 : tag == 5 ? 1 : 2;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const unsigned k = role * 1365 + (s_cnt[role]++ % 1365);
+  g_trace[3 * k] = tag;
+  g_trace[3 * k + 1] = idx;
+  g_trace[3 * k + 2] = t;
+}
+#define TRACE(tag, idx) trace(tag, idx)
+#else
+#define TRACE(tag, idx)
+#endif
+
 namespace pactgpu {
 namespace {
 
@@ -99,6 +120,7 @@ __device__ __forceinline__ float transpose_reduce32(float (&z)[32], int lane) {
 
 struct LayerBars {
   uint64_t raw[2];    // raw tile landed (bulk copies)
+  uint64_t ready[2];  // chunk planes written (256 producer threads)
   uint64_t buf[2];    // chunk planes free (MMA commit)
   uint64_t full[2];   // accumulator ready (MMA commit)
   uint64_t empty[2];  // accumulator drained (128 epilogue threads)
@@ -107,12 +129,24 @@ struct LayerBars {
 
 // TMEM columns: A_hi [0,128), A_lo [128,256), D0 [256,384), D1 [384,512)
 constexpr uint32_t kColAlo = 128, kColD = 256;
-constexpr int LNTH = 512;  // warps 0-7 stage (thread 0 issues), warps 8-15 drain
+// warps 0-7 stage the chunks, warp 8 issues the MMAs (one elected lane, warp-
+// uniform descriptors), warps 9-16 drain the accumulators
 constexpr int LPROD = 256;  // producer threads
+constexpr int LEPI = 256;   // epilogue threads
+// The forward has a dedicated MMA warp (544 threads, 96 registers); the dgrad,
+// whose cosine epilogue needs the registers, issues from producer thread 0
+// after a per-chunk producer barrier (512 threads, 128 registers).
+template <int MODE>
+struct LayerRoles {
+  static constexpr bool kMmaWarp = MODE == 0;
+  static constexpr int kThreads = LPROD + (kMmaWarp ? 32 : 0) + LEPI;
+  static constexpr int kEpi0 = LPROD + (kMmaWarp ? 32 : 0);  // first epilogue thread
+};
+constexpr int kWarpMma = LPROD / 32;  // 8
 constexpr int WNTH = 384;  // weight gradient: warps 0-3 dA^T, warps 4-11 sine planes
 
 template <int MODE>
-__global__ void __launch_bounds__(LNTH, 1)
+__global__ void __launch_bounds__(LayerRoles<MODE>::kThreads, 1)
 tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l-1} or dA_l)
                 const float* __restrict__ W,      // [H][H] layer matrix, row-major
                 const float* __restrict__ bias,   // forward: [H]
@@ -133,9 +167,10 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&sb.raw[i], 1);
+      tc::mbar_init(&sb.ready[i], LPROD);
       tc::mbar_init(&sb.buf[i], 1);
       tc::mbar_init(&sb.full[i], 1);
-      tc::mbar_init(&sb.empty[i], LNTH - LPROD);
+      tc::mbar_init(&sb.empty[i], LEPI);
     }
     fence_mbar_init();
   }
@@ -157,7 +192,9 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
   // memory with an odd row stride (coalesced loads, conflict-free reads);
   // warp w writes lane quarter w % 4, plane (w / 8) and K half (w / 4) % 2.
   // Forward A[r][k] = W[r][k]; dgrad A[k][r] = W[r][k].
-  for (int e = tid; e < H * H / 4; e += LNTH) {
+  constexpr int NTHR = LayerRoles<MODE>::kThreads, EPI0 = LayerRoles<MODE>::kEpi0;
+  constexpr bool MW = LayerRoles<MODE>::kMmaWarp;
+  for (int e = tid; e < H * H / 4; e += NTHR) {
     const float4 w4 = reinterpret_cast<const float4*>(W)[e];
     float* d = wst + (e / (H / 4)) * (H + 1) + (e % (H / 4)) * 4;
     d[0] = w4.x;
@@ -166,7 +203,7 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
     d[3] = w4.w;
   }
   __syncthreads();
-  {
+  if (warp < 16) {
     const bool lo_plane = warp >= 8;
     const uint32_t lb = lane_base(t0, warp & 3) + (lo_plane ? kColAlo : 0);
 #pragma unroll 1
@@ -185,21 +222,22 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
   sync_tc();
 
   if (tid < LPROD) {
-    // ---- producers: re-layout K-chunks, issue MMAs ----
-    constexpr uint32_t idesc = tc::idesc_tf32(H, TP);
+    // ---- producers: re-layout K-chunks into the chunk planes ----
     const int c4 = tid & 7, p0 = tid >> 3;  // 16-B chunk of the K-chunk row, first row
     uint32_t g = 0;  // chunks staged so far (chunk buffer g & 1)
     for (int i = 0; i < my_tiles; ++i) {
       const int m0 = (blockIdx.x + i * gridDim.x) * TP;
       const int rows = min(TP, n - m0);
       if (tid == 0 && i + 1 < my_tiles) load_tile(i + 1);
+      if (tid == 0) TRACE(1, i);
       tc::mbar_wait(&sb.raw[i & 1], (i >> 1) & 1);
+      if (tid == 0) TRACE(2, i);
       const float* rt = raw + (i & 1) * TP * H;
-      const uint32_t dcol = t0 + kColD + (i & 1) * TP;
 #pragma unroll 1
       for (int kc0 = 0; kc0 < H; kc0 += KC, ++g) {
         const int b = g & 1;
         if (g >= 2) tc::mbar_wait(&sb.buf[b], ((g - 2) >> 1) & 1);
+        if (tid == 0) TRACE(3, g);
         float* bh = zh + b * TP * KC;
         float* bl = zl + b * TP * KC;
         // Rows >= `rows` of the raw tile hold stale bytes: load them anyway
@@ -230,13 +268,52 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
           *reinterpret_cast<float4*>(bl + o) = l;
         }
         tc::fence_proxy_async();
-        tc::named_sync(1, LPROD);
-        if (tid == 0) {
-          if (kc0 == 0 && i >= 2) tc::mbar_wait(&sb.empty[i & 1], ((i - 2) >> 1) & 1);
-          tc::fence_after_sync();
-          const uint32_t sbh = saddr(bh), sbl = saddr(bl);
+        if (MW) {
+          tc::mbar_arrive(&sb.ready[b]);
+          if (tid == 0) TRACE(4, g);
+        } else {
+          tc::named_sync(1, LPROD);
+          if (tid == 0) {
+            constexpr uint32_t idesc = tc::idesc_tf32(H, TP);
+            const uint32_t dcol = t0 + kColD + (i & 1) * TP;
+            if (kc0 == 0 && i >= 2) tc::mbar_wait(&sb.empty[i & 1], ((i - 2) >> 1) & 1);
+            tc::fence_after_sync();
+            const uint32_t sbh = saddr(bh), sbl = saddr(bl);
 #pragma unroll
-          for (int s = 0; s < (TC_EXP == 1 || TC_EXP == 4 ? 0 : KC / 8); ++s) {
+            for (int s = 0; s < KC / 8; ++s) {
+              const uint32_t ka = kc0 + 8 * s;
+              const uint64_t dh = tc::smem_desc_sw128(sbh + 32 * s);
+              const uint64_t dl = tc::smem_desc_sw128(sbl + 32 * s);
+              tc::mma_tf32_ts(dcol, t0 + kColAlo + ka, dh, idesc, (kc0 | s) != 0);
+              tc::mma_tf32_ts(dcol, t0 + ka, dl, idesc, 1u);
+              tc::mma_tf32_ts(dcol, t0 + ka, dh, idesc, 1u);
+            }
+            tc::mma_commit(&sb.buf[b]);
+            if (kc0 + KC == H) tc::mma_commit(&sb.full[i & 1]);
+          }
+        }
+      }
+      // every producer is done reading raw[i & 1] before tile i + 2 is loaded into
+      // it (without the MMA warp the per-chunk barrier already orders this)
+      if (MW) tc::named_sync(1, LPROD);
+    }
+  } else if (MW && warp == kWarpMma) {
+    // ---- the MMA warp: waits for a staged chunk, issues its 12 MMAs ----
+    constexpr uint32_t idesc = tc::idesc_tf32(H, TP);
+    uint32_t g = 0;
+    for (int i = 0; i < my_tiles; ++i) {
+      const uint32_t dcol = t0 + kColD + (i & 1) * TP;
+#pragma unroll 1
+      for (int kc0 = 0; kc0 < H; kc0 += KC, ++g) {
+        const int b = g & 1;
+        tc::mbar_wait(&sb.ready[b], (g >> 1) & 1);
+        if (kc0 == 0 && i >= 2) tc::mbar_wait(&sb.empty[i & 1], ((i - 2) >> 1) & 1);
+        tc::fence_after_sync();
+        if ((tid & 31) == 0) TRACE(5, g);
+        const uint32_t sbh = saddr(zh + b * TP * KC), sbl = saddr(zl + b * TP * KC);
+        if (tc::elect_one()) {
+#pragma unroll
+          for (int s = 0; s < (TC_EXP == 1 || TC_EXP == 4 || TC_EXP == 6 ? 0 : KC / 8); ++s) {
             const uint32_t ka = kc0 + 8 * s;
             const uint64_t dh = tc::smem_desc_sw128(sbh + 32 * s);
             const uint64_t dl = tc::smem_desc_sw128(sbl + 32 * s);
@@ -247,37 +324,52 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
           tc::mma_commit(&sb.buf[b]);
           if (kc0 + KC == H) tc::mma_commit(&sb.full[i & 1]);
         }
+        __syncwarp();
       }
     }
   } else {
     // ---- epilogue: lane = output feature, columns = pixels of the tile;
     // warps 8-11 and 12-15 share the TMEM lane quarters and split the columns ----
     const float brow = MODE == kForward ? bias[row] : 0.f;
-    const int cb = ((warp - LPROD / 32) >> 2) * (TP / 2);
+    const int cb = ((warp - EPI0 / 32) >> 2) * (TP / 2);
     const bool fuse_out = MODE == kForward && head.w != nullptr;
     const float wrow = fuse_out ? head.w[row] : 0.f;
     for (int i = 0; i < my_tiles; ++i) {
       const int m0 = (blockIdx.x + i * gridDim.x) * TP;
       const int rows = min(TP, n - m0);
+      // a_{l-1} for the cosine (dgrad) does not depend on the accumulator: all
+      // 64 columns of this thread are fetched before the wait
       float av[TP / 2];
       if (MODE == kDgrad) {
-        // a_{l-1} does not depend on the accumulator: fetch before waiting
         const float* a = Aprev + static_cast<size_t>(m0) * H + row;
 #pragma unroll
         for (int j = 0; j < TP / 2; ++j) av[j] = a[min(cb + j, rows - 1) * H];
       }
+      if (tid == EPI0) TRACE(6, i);
       tc::mbar_wait(&sb.full[i & 1], (i >> 1) & 1);
+      if (tid == EPI0) TRACE(7, i);
       tc::fence_after_sync();
       const uint32_t d = lane_base(t0, warp & 3) + kColD + (i & 1) * TP;
       float* y = Y + static_cast<size_t>(m0) * H + row;
 #pragma unroll
-      for (int h = 0; h < TP / 2; h += 32) {
+      for (int h = 0; MODE == kDgrad && h < TP / 2; h += 32) {
         float v[32];
         tc::tmem_ld32(d + cb + h, v);
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int c = cb + h + j;
-          const float out = MODE == kForward ? v[j] + brow : v[j] * dsin_w(av[h + j], w0);
+          const float out = v[j] * dsin_w(av[h + j], w0);  // unconditional: predicated store
+          if (c < rows && TC_EXP != 3) y[c * H] = out;
+        }
+      }
+#pragma unroll
+      for (int h = 0; MODE == kForward && h < TP / 2; h += 32) {
+        float v[32];
+        tc::tmem_ld32(d + cb + h, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int c = cb + h + j;
+          const float out = v[j] + brow;
           if (c < rows && (TC_EXP != 3 || out == 12345.f)) y[c * H] = out;
           v[j] = out;
         }
@@ -292,9 +384,10 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
       }
       tc::fence_before_sync();
       tc::mbar_arrive(&sb.empty[i & 1]);
+      if (tid == EPI0) TRACE(8, i);
       if (fuse_out) {
-        tc::named_sync(2, LNTH - LPROD);
-        const int c = tid - LPROD;
+        tc::named_sync(2, LEPI);
+        const int c = tid - EPI0;
         if (c < rows) {
           const float* so = &s_out[i & 1][0][0];
           const float s = ((so[c] + so[TP + c]) + so[2 * TP + c]) + so[3 * TP + c];
@@ -477,7 +570,8 @@ Status tc_forward_layer(pact_ctx* ctx, int hidden, const float* Ain, const float
   static bool cfg = false;
   if (!cfg) PACT_TRY_S(set_smem(tc_layer_kernel<kForward>, kLayerSmem));
   cfg = true;
-  tc_layer_kernel<kForward><<<layer_grid(ctx, n), LNTH, kLayerSmem, ctx->stream>>>(
+  tc_layer_kernel<kForward><<<layer_grid(ctx, n), LayerRoles<kForward>::kThreads, kLayerSmem,
+                              ctx->stream>>>(
       Ain, W, b, nullptr, n, w0, Aout, head);
   return after_launch(ctx, "tc_layer_kernel<forward>");
 }
@@ -488,7 +582,8 @@ Status tc_dgrad_layer(pact_ctx* ctx, int hidden, const float* dAl, const float* 
   static bool cfg = false;
   if (!cfg) PACT_TRY_S(set_smem(tc_layer_kernel<kDgrad>, kLayerSmem));
   cfg = true;
-  tc_layer_kernel<kDgrad><<<layer_grid(ctx, n), LNTH, kLayerSmem, ctx->stream>>>(
+  tc_layer_kernel<kDgrad><<<layer_grid(ctx, n), LayerRoles<kDgrad>::kThreads, kLayerSmem,
+                            ctx->stream>>>(
       dAl, W, nullptr, Aprev, n, w0, dAprev, SirenHead{});
   return after_launch(ctx, "tc_layer_kernel<dgrad>");
 }
@@ -504,3 +599,15 @@ Status tc_wgrad_layer(pact_ctx* ctx, int hidden, const float* dAl, const float* 
 }
 
 }  // namespace pactgpu
+
+#if TC_EXP == 5 || TC_EXP == 6
+extern "C" int pact_debug_trace(unsigned long long* out, int n, int reset) {
+  cudaDeviceSynchronize();
+  if (out) cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 3 * std::min(n, 4095));
+  if (reset) {
+    static unsigned long long zero[3 * 4096];
+    cudaMemcpyToSymbol(g_trace, zero, sizeof(zero));
+  }
+  return 4095;
+}
+#endif
