@@ -143,7 +143,7 @@ struct LayerRoles {
   static constexpr int kEpi0 = LPROD + (kMmaWarp ? 32 : 0);  // first epilogue thread
 };
 constexpr int kWarpMma = LPROD / 32;  // 8
-constexpr int WNTH = 384;  // weight gradient: warps 0-3 dA^T, warps 4-11 sine planes
+constexpr int WNTH = 416;  // weight gradient: warps 0-3 dA^T, 4-11 sine planes, 12 MMA
 
 template <int MODE>
 __global__ void __launch_bounds__(LayerRoles<MODE>::kThreads, 1)
@@ -405,13 +405,16 @@ constexpr int WP = 64;  // pixels per raw tile
 
 struct WgradBars {
   uint64_t raw[2];
-  uint64_t buf[2];
+  uint64_t ready[2];  // chunk staged (384 producer threads)
+  uint64_t buf[2];    // chunk consumed (MMA commit)
   uint64_t acc;
   uint32_t tslot;
 };
 
 // TMEM: D [0,128); A chunk b: hi [128 + 64b, +32), lo [160 + 64b, +32).
-// Warps 0-3 put dA^T into TMEM (lane r), warps 4-7 build the sine planes.
+// Warps 0-3 put dA^T into TMEM (lane r), warps 4-11 build the sine planes,
+// warp 12 issues the MMAs (one elected lane).
+constexpr int WPROD = 384;
 __global__ void __launch_bounds__(WNTH, 1)
 tc_wgrad_kernel(const float* __restrict__ dA, const float* __restrict__ Aprev, int n, int rows,
                 float w0, float* __restrict__ partial) {
@@ -427,6 +430,7 @@ tc_wgrad_kernel(const float* __restrict__ dA, const float* __restrict__ Aprev, i
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&sb.raw[i], 1);
+      tc::mbar_init(&sb.ready[i], WPROD);
       tc::mbar_init(&sb.buf[i], 1);
     }
     tc::mbar_init(&sb.acc, 1);
@@ -436,6 +440,7 @@ tc_wgrad_kernel(const float* __restrict__ dA, const float* __restrict__ Aprev, i
   const uint32_t t0 = sb.tslot;
   const int m_begin = blockIdx.x * rows, m_end = min(n, m_begin + rows);
   const int n_raw = m_end > m_begin ? (m_end - m_begin + WP - 1) / WP : 0;
+  const int n_chunks = n_raw * (WP / KC);
 
   auto load_tile = [&](int i) {
     const int p0 = m_begin + i * WP;
@@ -447,56 +452,74 @@ tc_wgrad_kernel(const float* __restrict__ dA, const float* __restrict__ Aprev, i
   };
   if (tid == 0 && n_raw > 0) load_tile(0);
 
-  constexpr uint32_t LBO = (H / 8) * 128;
-  constexpr uint32_t idesc = tc::idesc_tf32(H, H);
   float bias_acc = 0.f;
-  uint32_t g = 0;
-  for (int i = 0; i < n_raw; ++i) {
-    const int p0 = m_begin + i * WP;
-    const int valid = min(WP, m_end - p0);
-    if (tid == 0 && i + 1 < n_raw) load_tile(i + 1);
-    tc::mbar_wait(&sb.raw[i & 1], (i >> 1) & 1);
-    const float* ta = rda + (i & 1) * WP * H;
-    const float* tz = rap + (i & 1) * WP * H;
+  if (tid < WPROD) {
+    // ---- producers ----
+    uint32_t g = 0;
+    for (int i = 0; i < n_raw; ++i) {
+      const int p0 = m_begin + i * WP;
+      const int valid = min(WP, m_end - p0);
+      if (tid == 0 && i + 1 < n_raw) load_tile(i + 1);
+      tc::mbar_wait(&sb.raw[i & 1], (i >> 1) & 1);
+      const float* ta = rda + (i & 1) * WP * H;
+      const float* tz = rap + (i & 1) * WP * H;
 #pragma unroll 1
-    for (int q0 = 0; q0 < WP; q0 += KC, ++g) {
-      const int b = g & 1;
-      if (g >= 2) tc::mbar_wait(&sb.buf[b], ((g - 2) >> 1) & 1);
-      float* bh = zh + b * H * KC;
-      float* bl = zl + b * H * KC;
-      if (warp < 4) {
-        // dA^T chunk -> TMEM (lane r, column = pixel)
-        float hi[32], lo[32];
+      for (int q0 = 0; q0 < WP; q0 += KC, ++g) {
+        const int b = g & 1;
+        if (g >= 2) tc::mbar_wait(&sb.buf[b], ((g - 2) >> 1) & 1);
+        if (warp < 4) {
+          // dA^T chunk -> TMEM (lane r, column = pixel)
+          float hi[32], lo[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) hi[j] = ta[(q0 + j) * H + r];
+          for (int j = 0; j < 32; ++j) hi[j] = ta[(q0 + j) * H + r];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float x = q0 + j < valid ? hi[j] : 0.f;
-          bias_acc += x;
-          tc::split_tf32(x, hi[j], lo[j]);
+          for (int j = 0; j < 32; ++j) {
+            const float x = q0 + j < valid ? hi[j] : 0.f;
+            bias_acc += x;
+            tc::split_tf32(x, hi[j], lo[j]);
+          }
+          const uint32_t lb = lane_base(t0, warp) + 128 + 64 * b;
+          tc::tmem_st32(lb, hi);
+          tc::tmem_st32(lb + 32, lo);
+          tc::fence_before_sync();
+        } else {
+          // sin(w0 a_{l-1})^T chunk -> planes (row k = r, K = pixel); warps
+          // 4-7 take pixels [0, 16) of the chunk, warps 8-11 pixels [16, 32).
+          // Stale rows past `valid` are read and zeroed after the sine (no
+          // branch around the MUFU).
+          constexpr int HK = KC / 2;
+          const int j0 = warp >= 8 ? HK : 0;
+          float a[HK];
+          float* bh = zh + b * H * KC;
+          float* bl = zl + b * H * KC;
+#pragma unroll
+          for (int j = 0; j < HK; ++j) a[j] = tz[(q0 + j0 + j) * H + r];
+#pragma unroll
+          for (int j = 0; j < HK; ++j) {
+            const float z = sin_w(a[j], w0);
+            a[j] = q0 + j0 + j < valid ? z : 0.f;
+          }
+#pragma unroll
+          for (int j = 0; j < HK; j += 4)
+            put4(bh, bl, r, j0 + j, H, make_float4(a[j], a[j + 1], a[j + 2], a[j + 3]));
+          tc::fence_proxy_async();
         }
-        const uint32_t lb = lane_base(t0, warp) + 128 + 64 * b;
-        tc::tmem_st32(lb, hi);
-        tc::tmem_st32(lb + 32, lo);
-      } else {
-        // sin(w0 a_{l-1})^T chunk -> planes (row k = r, K = pixel); warps
-        // 4-7 take pixels [0, 16) of the chunk, warps 8-11 pixels [16, 32)
-        constexpr int HK = KC / 2;
-        const int j0 = warp >= 8 ? HK : 0;
-        float a[HK];
-#pragma unroll
-        for (int j = 0; j < HK; ++j) a[j] = tz[(q0 + j0 + j) * H + r];
-#pragma unroll
-        for (int j = 0; j < HK; ++j) a[j] = q0 + j0 + j < valid ? sin_w(a[j], w0) : 0.f;
-#pragma unroll
-        for (int j = 0; j < HK; j += 4)
-          put4(bh, bl, r, j0 + j, H, make_float4(a[j], a[j + 1], a[j + 2], a[j + 3]));
-        tc::fence_proxy_async();
+        tc::mbar_arrive(&sb.ready[b]);
       }
-      sync_tc();
-      if (tid == 0) {
-        const uint32_t sbh = saddr(bh), sbl = saddr(bl);
-        const uint32_t ah = t0 + 128 + 64 * b, al = ah + 32;
+      // every producer is done reading raw[i & 1] before tile i + 2 is loaded into it
+      tc::named_sync(1, WPROD);
+    }
+  } else if (warp == WPROD / 32) {
+    // ---- the MMA warp ----
+    constexpr uint32_t LBO = (H / 8) * 128;
+    constexpr uint32_t idesc = tc::idesc_tf32(H, H);
+    for (int g = 0; g < n_chunks; ++g) {
+      const int b = g & 1;
+      tc::mbar_wait(&sb.ready[b], (g >> 1) & 1);
+      tc::fence_after_sync();
+      const uint32_t sbh = saddr(zh + b * H * KC), sbl = saddr(zl + b * H * KC);
+      const uint32_t ah = t0 + 128 + 64 * b, al = ah + 32;
+      if (tc::elect_one()) {
 #pragma unroll
         for (int s = 0; s < KC / 8; ++s) {
           const uint64_t dh = tc::smem_desc(sbh + 2 * s * LBO, LBO, 128);
@@ -506,12 +529,13 @@ tc_wgrad_kernel(const float* __restrict__ dA, const float* __restrict__ Aprev, i
           tc::mma_tf32_ts(t0, ah + 8 * s, dh, idesc, 1u);
         }
         tc::mma_commit(&sb.buf[b]);
+        if (g + 1 == n_chunks) tc::mma_commit(&sb.acc);
       }
+      __syncwarp();
     }
   }
   float* out = partial + static_cast<size_t>(blockIdx.x) * (static_cast<size_t>(H) * H + H);
-  if (g > 0) {
-    if (tid == 0) tc::mma_commit(&sb.acc);
+  if (n_chunks > 0) {
     tc::mbar_wait(&sb.acc, 0);
     tc::fence_after_sync();
     // warps w and w + 4 (w < 4) share TMEM lanes; each drains half the columns
