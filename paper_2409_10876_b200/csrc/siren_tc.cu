@@ -86,10 +86,10 @@ __device__ __forceinline__ void sync_tc() {
 // 4 consecutive-K values (k % 4 == 0) of one row into K-major hi/lo planes.
 __device__ __forceinline__ void put4(float* hi, float* lo, int row, int k, int R, float4 v) {
   float4 h, l;
-  tc::split_tf32(v.x, h.x, l.x);
-  tc::split_tf32(v.y, h.y, l.y);
-  tc::split_tf32(v.z, h.z, l.z);
-  tc::split_tf32(v.w, h.w, l.w);
+  tc::split_tf32_trunc(v.x, h.x, l.x);
+  tc::split_tf32_trunc(v.y, h.y, l.y);
+  tc::split_tf32_trunc(v.z, h.z, l.z);
+  tc::split_tf32_trunc(v.w, h.w, l.w);
   const uint32_t o = tc::kmajor_offset(row, k, R) >> 2;
   *reinterpret_cast<float4*>(hi + o) = h;
   *reinterpret_cast<float4*>(lo + o) = l;
@@ -259,10 +259,10 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
             z = make_float4(sin_w(z.x, w0), sin_w(z.y, w0), sin_w(z.z, w0), sin_w(z.w, w0));
           if (p >= rows) z = make_float4(0.f, 0.f, 0.f, 0.f);
           float4 h, l;
-          tc::split_tf32(z.x, h.x, l.x);
-          tc::split_tf32(z.y, h.y, l.y);
-          tc::split_tf32(z.z, h.z, l.z);
-          tc::split_tf32(z.w, h.w, l.w);
+          tc::split_tf32_trunc(z.x, h.x, l.x);
+          tc::split_tf32_trunc(z.y, h.y, l.y);
+          tc::split_tf32_trunc(z.z, h.z, l.z);
+          tc::split_tf32_trunc(z.w, h.w, l.w);
           const int o = p * KC + ((c4 ^ (p & 7)) << 2);
           *reinterpret_cast<float4*>(bh + o) = h;
           *reinterpret_cast<float4*>(bl + o) = l;
@@ -476,7 +476,7 @@ tc_wgrad_kernel(const float* __restrict__ dA, const float* __restrict__ Aprev, i
           for (int j = 0; j < 32; ++j) {
             const float x = q0 + j < valid ? hi[j] : 0.f;
             bias_acc += x;
-            tc::split_tf32(x, hi[j], lo[j]);
+            tc::split_tf32_trunc(x, hi[j], lo[j]);
           }
           const uint32_t lb = lane_base(t0, warp) + 128 + 64 * b;
           tc::tmem_st32(lb, hi);

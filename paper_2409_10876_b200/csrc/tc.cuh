@@ -27,6 +27,16 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   lo = tf32_round(x - hi);
 }
 
+// Split for operands the MMA reads straight from fp32: kind::tf32 ignores the
+// 13 low mantissa bits, so hi can be x itself (the hardware truncates it) and
+// lo = x - trunc(x) is exact in fp32 (<= 13 significant bits; the hardware
+// truncates it to TF32 in turn).  Representation error <= 2^-21 |x| (the
+// rounded split: 2^-22) for 2 instructions instead of 5.
+__device__ __forceinline__ void split_tf32_trunc(float x, float& hi, float& lo) {
+  hi = x;
+  lo = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
 // ---- K-major, no-swizzle smem tiles --------------------------------------
 // An R x Kc fp32 tile (R rows, Kc along K) is laid out as core matrices of
 // 8 rows x 4 elements (128 B):  byte(row, k) = (k/4)*LBO + (row/8)*128 +
