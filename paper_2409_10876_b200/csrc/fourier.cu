@@ -415,6 +415,78 @@ __device__ __forceinline__ double bin_chain(const FourierTab& t, const float* __
   return static_cast<double>(L.wk) * acc;
 }
 
+// Ordinary (non-Nyquist) bins in closed form.  With e1 = exp(+i|k|w1),
+// e2 = exp(-i|k|w2) and dp_j = exp(-i|k|d_j) (optimize.hpp:261-271),
+//   h_j = (dp_j e1 + conj(dp_j) e2) / 2 = phi c_j,  phi = exp(i|k|(w1 - w2)/2),
+//   c_j = cos(|k|(d_j - wbar)) real, wbar = (w1 + w2) / 2.
+// |phi| = 1 cancels from the Wiener estimate and every residual:
+//   X' = sum_j c_j y_j / (sum_j c_j^2 + eps M),  r_j = y_j - c_j X',
+// so the loss needs only c_j, and (with the implicit X' term,
+// optimize.hpp:290-311)
+//   dL/dc_j = -2 wk [Re(conj(r_j) X') + a Re(conj(X') y_j) - 2 a |X'|^2 c_j],
+//   a = eps M / den,   dc_j/dwbar = |k| sin(|k|(d_j - wbar)),
+// and w1, w2 each receive half of dL/dwbar.  About a third of the complex
+// arithmetic of the general chain; same quantities.
+template <class YF>
+__device__ __forceinline__ double bin_chain_real(const FourierTab& t, const float* __restrict__ s_w,
+                                                 int b, float eps_m, float scale, bool impl,
+                                                 YF y_of, float& G) {
+  const int K = t.K, P2 = t.P2;
+  G = 0.f;
+  const float k = t.kmag[b];
+  const float wk = k * scale;
+  if (wk == 0.f) return 0.0;
+  const int4 ix = t.idx[b];
+  const float2 fr = t.frac[b];
+  const float w1 = (1.f - fr.x) * s_w[ix.x] + fr.x * s_w[ix.y];
+  const float w2 = (1.f - fr.y) * s_w[ix.z] + fr.y * s_w[ix.w];
+  float sn, cs;
+  sincosf(k * (0.5f * (w1 + w2)), &sn, &cs);
+  const float2 ew = make_float2(cs, -sn);  // exp(-i|k| wbar)
+  // z_j = conj(dp_j) exp(-i|k| wbar) = exp(i|k|(d_j - wbar)): c_j = Re z_j, s_j = Im z_j
+  const bool walk = t.rho != nullptr;
+  const float2 rr = walk ? conjf2(t.rho[b]) : make_float2(1.f, 0.f);
+  const float2 z0 = cmul(conjf2(t.dp[b]), ew);
+  auto next = [&](int j, float2& z) {
+    if (walk)
+      z = cmul(z, rr);
+    else if (j + 1 < K)
+      z = cmul(conjf2(t.dp[(j + 1) * P2 + b]), ew);
+  };
+  float2 S = make_float2(0.f, 0.f);
+  float den = eps_m;
+  {
+    float2 z = z0;
+#pragma unroll 4
+    for (int j = 0; j < K; ++j) {
+      const float2 y = y_of(j);
+      S.x = fmaf(z.x, y.x, S.x);
+      S.y = fmaf(z.x, y.y, S.y);
+      den = fmaf(z.x, z.x, den);
+      next(j, z);
+    }
+  }
+  const float inv = den > 0.f ? 1.f / den : 0.f;
+  const float2 X = make_float2(S.x * inv, S.y * inv);
+  const float al = impl && den > 0.f ? eps_m * inv : 0.f;
+  const float be = 2.f * al * (X.x * X.x + X.y * X.y);
+  float acc = 0.f, gs = 0.f;
+  {
+    float2 z = z0;
+#pragma unroll 4
+    for (int j = 0; j < K; ++j) {
+      const float2 y = y_of(j);
+      const float rx = fmaf(-z.x, X.x, y.x), ry = fmaf(-z.x, X.y, y.y);
+      acc = fmaf(rx, rx, fmaf(ry, ry, acc));
+      const float dc = fmaf(rx, X.x, ry * X.y) + al * fmaf(X.x, y.x, X.y * y.y) - be * z.x;
+      gs = fmaf(dc, z.y, gs);
+      next(j, z);
+    }
+  }
+  G = -wk * k * gs;  // = (1/2) dL/dwbar, for w1 and for w2
+  return static_cast<double>(wk) * acc;
+}
+
 __device__ __forceinline__ void block_sum_store(double value, double* s_red, double* out) {
   for (int o = 16; o > 0; o >>= 1) value += __shfl_xor_sync(0xffffffffu, value, o);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = value;
@@ -472,11 +544,11 @@ __global__ void __launch_bounds__(LB) loss_bins_kernel(FourierTab t, const float
   double value = 0.0;
   const int b = b0 + threadIdx.x;
   if (b < P2 && t.mirror[b] < 0) {
-    float G1, G2;
+    float G1;
     const float2* yb = s_y + threadIdx.x;
-    value = bin_chain<false>(t, s_w, b, -1, eps_m, scale, implicit != 0,
-                             [&](int j) { return yb[j * LB]; }, G1, G2, nullptr);
-    gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G1, G2);
+    value = bin_chain_real(t, s_w, b, eps_m, scale, implicit != 0,
+                           [&](int j) { return yb[j * LB]; }, G1);
+    gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G1, G1);
   }
   block_sum_store(value, s_red, loss_part + patch * n_parts + blockIdx.y);
 }
