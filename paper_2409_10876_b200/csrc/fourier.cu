@@ -21,6 +21,7 @@
 #include <mutex>
 
 #include "fourier.cuh"
+#include "tc.cuh"
 
 namespace pactgpu {
 
@@ -505,11 +506,74 @@ __device__ __forceinline__ void block_sum_store(double value, double* s_red, dou
 // lanes idle) and handled by kernel A'.
 constexpr int LB = 128;
 
+// Persistent, two-stage pipelined form (P^2 a multiple of LB): each CTA walks
+// the (patch, bin chunk) work list with stride gridDim.x; while it computes a
+// chunk, the next chunk's K rows of LB spectra (1 KB each) and its patch's
+// wavefront profile arrive by cp.async.bulk into the other stage.  The loss
+// partial of every chunk goes to its fixed slot (deterministic).
 __global__ void __launch_bounds__(LB) loss_bins_kernel(FourierTab t, const float2* __restrict__ Y_all,
                                                        const float* __restrict__ w_all, float eps_m,
                                                        float scale, int implicit,
                                                        float2* __restrict__ gbuf,
-                                                       double* __restrict__ loss_part, int n_parts) {
+                                                       double* __restrict__ loss_part, int n_parts,
+                                                       int n_patches) {
+  extern __shared__ __align__(16) float smem[];
+  const int K = t.K, P2 = t.P2, A = t.A;
+  const int chunks = P2 / LB, total = n_patches * chunks;
+  const int stage_floats = 2 * K * LB + ((A + 3) & ~3);
+  __shared__ double s_red[LB / 32];
+  __shared__ __align__(8) uint64_t bar[2];
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int c, int st) {  // thread 0 arms, threads < K + 1 copy
+    const int patch = c / chunks, b0 = (c - patch * chunks) * LB;
+    float* base = smem + st * stage_floats;
+    if (threadIdx.x == 0)
+      tc::mbar_expect_tx(&bar[st], static_cast<uint32_t>(K * LB * 8 + A * 4));
+    __syncwarp();
+    for (int j = threadIdx.x; j <= K; j += 32) {
+      if (j < K)
+        tc::bulk_load(base + 2 * j * LB, Y_all + (static_cast<size_t>(patch) * K + j) * P2 + b0,
+                      LB * 8, &bar[st]);
+      else
+        tc::bulk_load(base + 2 * K * LB, w_all + static_cast<size_t>(patch) * A, A * 4, &bar[st]);
+    }
+  };
+  int i = 0;
+  if (threadIdx.x < 32 && blockIdx.x < total) issue(blockIdx.x, 0);
+  for (int c = blockIdx.x; c < total; c += gridDim.x, ++i) {
+    const int st = i & 1;
+    if (threadIdx.x < 32 && c + static_cast<int>(gridDim.x) < total) issue(c + gridDim.x, st ^ 1);
+    tc::mbar_wait(&bar[st], (i >> 1) & 1);
+    const float* base = smem + st * stage_floats;
+    const float2* s_y = reinterpret_cast<const float2*>(base);
+    const float* s_w = base + 2 * K * LB;
+    const int patch = c / chunks, cb = c - patch * chunks;
+    const int b = cb * LB + threadIdx.x;
+    double value = 0.0;
+    if (t.mirror[b] < 0) {
+      float G;
+      const float2* yb = s_y + threadIdx.x;
+      value = bin_chain_real(t, s_w, b, eps_m, scale, implicit != 0,
+                             [&](int j) { return yb[j * LB]; }, G);
+      gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G, G);
+    }
+    block_sum_store(value, s_red, loss_part + patch * n_parts + cb);
+    __syncthreads();  // stage st is free for chunk i + 2; s_red is reusable
+  }
+}
+
+// Small patches (P^2 < LB or not a multiple of LB): one CTA per (patch, chunk).
+__global__ void __launch_bounds__(LB) loss_bins_small_kernel(FourierTab t, const float2* __restrict__ Y_all,
+                                                             const float* __restrict__ w_all,
+                                                             float eps_m, float scale, int implicit,
+                                                             float2* __restrict__ gbuf,
+                                                             double* __restrict__ loss_part,
+                                                             int n_parts) {
   extern __shared__ __align__(16) float smem[];
   const int K = t.K, P2 = t.P2;
   float2* s_y = reinterpret_cast<float2*>(smem);  // [K][LB]
@@ -519,36 +583,19 @@ __global__ void __launch_bounds__(LB) loss_bins_kernel(FourierTab t, const float
   const float2* Y = Y_all + static_cast<size_t>(patch) * K * P2;
   for (int a = threadIdx.x; a < t.A; a += LB) s_w[a] = w_all[patch * t.A + a];
   const int nb = min(LB, P2 - b0);
-  if (nb == LB) {
-    // K * LB / 2 float4 of the chunk, eight loads in flight per thread
-    for (int e0 = threadIdx.x; e0 < K * LB / 2; e0 += 8 * LB) {
-      float4 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int e = e0 + u * LB, j = e / (LB / 2), q = e - j * (LB / 2);
-        v[u] = e < K * LB / 2
-                   ? reinterpret_cast<const float4*>(Y + static_cast<size_t>(j) * P2 + b0)[q]
-                   : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (e0 + u * LB < K * LB / 2) reinterpret_cast<float4*>(s_y)[e0 + u * LB] = v[u];
-    }
-  } else {
-    for (int e = threadIdx.x; e < K * LB; e += LB) {
-      const int j = e / LB, q = e - j * LB;
-      s_y[e] = q < nb ? Y[static_cast<size_t>(j) * P2 + b0 + q] : make_float2(0.f, 0.f);
-    }
+  for (int e = threadIdx.x; e < K * LB; e += LB) {
+    const int j = e / LB, q = e - j * LB;
+    s_y[e] = q < nb ? Y[static_cast<size_t>(j) * P2 + b0 + q] : make_float2(0.f, 0.f);
   }
   __syncthreads();
   double value = 0.0;
   const int b = b0 + threadIdx.x;
   if (b < P2 && t.mirror[b] < 0) {
-    float G1;
+    float G;
     const float2* yb = s_y + threadIdx.x;
     value = bin_chain_real(t, s_w, b, eps_m, scale, implicit != 0,
-                           [&](int j) { return yb[j * LB]; }, G1);
-    gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G1, G1);
+                           [&](int j) { return yb[j * LB]; }, G);
+    gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G, G);
   }
   block_sum_store(value, s_red, loss_part + patch * n_parts + blockIdx.y);
 }
@@ -714,14 +761,27 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
   float2* gbuf = nyq + n_nyq;
   double* part = reinterpret_cast<double*>(gbuf + n_g);
   const float eps_m = static_cast<float>(eps * t.K), sc = static_cast<float>(scale);
-  const size_t smem_bins = sizeof(float2) * t.K * LB + smem;
-  if (smem_bins > 48 * 1024) {
-    if (smem_bins > 200 * 1024) return validation("fused loss: too many delays for one bin chunk");
-    PACT_CUDA_S(cudaFuncSetAttribute(loss_bins_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem_bins)));
+  if (t.P2 % LB == 0 && t.K * LB * 8 <= 96 * 1024) {
+    const size_t stage = sizeof(float) * (2 * t.K * LB + ((t.A + 3) & ~3));
+    const size_t smem_bins = 2 * stage;
+    if (smem_bins > 48 * 1024)
+      PACT_CUDA_S(cudaFuncSetAttribute(loss_bins_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem_bins)));
+    const int per_sm = std::max(1, static_cast<int>((227 * 1024 - 4096) / smem_bins));
+    const int grid = std::min(n_patches * chunks, ctx->num_sms * per_sm);
+    loss_bins_kernel<<<grid, LB, smem_bins, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, gbuf,
+                                                            part, n_parts, n_patches);
+  } else {
+    const size_t smem_bins = sizeof(float2) * t.K * LB + smem;
+    if (smem_bins > 48 * 1024) {
+      if (smem_bins > 200 * 1024) return validation("fused loss: too many delays for one bin chunk");
+      PACT_CUDA_S(cudaFuncSetAttribute(loss_bins_small_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem_bins)));
+    }
+    loss_bins_small_kernel<<<dim3(n_patches, chunks), LB, smem_bins, ctx->stream>>>(
+        t, Y, w, eps_m, sc, implicit, gbuf, part, n_parts);
   }
-  loss_bins_kernel<<<dim3(n_patches, chunks), LB, smem_bins, ctx->stream>>>(
-      t, Y, w, eps_m, sc, implicit, gbuf, part, n_parts);
   PACT_TRY_S(after_launch(ctx, "loss_bins_kernel"));
   if (t.P % 2 == 0) {
     const int S = 2 * t.P - 1, nt = div_up(S, 32) * 32;
