@@ -600,10 +600,12 @@ __global__ void __launch_bounds__(LB) loss_bins_small_kernel(FourierTab t, const
   block_sum_store(value, s_red, loss_part + patch * n_parts + blockIdx.y);
 }
 
-// Kernel A': the Nyquist bins (even P), one block per patch, one thread per
+// Kernel A': the Nyquist bins (even P), one block per patch, kTps threads per
 // exchange slot (2P - 1 of them).  Each slot's unsymmetrised dL/dH_j goes to
 // the exchange buffer; after the barrier every slot pulls back the
 // symmetrised g = (dL/dH_b + conj(dL/dH_m)) / 2 (optimize.hpp:306-308).
+constexpr int kTps = 4;
+
 __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const float2* __restrict__ Y_all,
                                                             const float* __restrict__ w_all,
                                                             float eps_m, float scale, int implicit,
@@ -637,44 +639,96 @@ __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const 
       if (e0 + u * blockDim.x < K * S) s_y[e0 + u * blockDim.x] = v[u];
   }
   __syncthreads();
-  const int slot = threadIdx.x;
-  double value = 0.0;
-  int b = -1;
-  if (slot < S) {
-    b = nyq_bin(slot, t.P);
-    float G1, G2;
-    value = bin_chain<true>(t, s_w, b, t.mirror[b], eps_m, scale, implicit != 0,
-                            [&](int j) {
-                              return stage_y ? s_y[j * S + slot]
-                                             : Y[static_cast<size_t>(j) * P2 + b];
-                            },
-                            G1, G2, s_g + static_cast<size_t>(slot) * K);
+  // kTps threads per slot (consecutive lanes), each walking K / kTps delays;
+  // the per-bin sums are combined with a fixed xor-shuffle tree
+  const int slot = threadIdx.x / kTps, q = threadIdx.x % kTps;
+  const bool active = slot < S;
+  const int b = nyq_bin(active ? slot : 0, t.P), m = t.mirror[b];
+  const int j0 = q * K / kTps, j1 = (q + 1) * K / kTps;
+  const float k = t.kmag[b];
+  const bool live = active && k * scale != 0.f;
+  auto y_of = [&](int j) {
+    return stage_y ? s_y[j * S + slot] : Y[static_cast<size_t>(j) * P2 + b];
+  };
+  auto group_sum = [&](float v) {
+#pragma unroll
+    for (int o = 1; o < kTps; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
+  float2 e1b, e2b, e1m, e2m;
+  bin_phases(t, s_w, b, e1b, e2b);
+  bin_phases(t, s_w, m, e1m, e2m);
+  const bool walk = t.rho != nullptr;
+  const float2 rb = walk ? t.rho[b] : make_float2(1.f, 0.f);
+  const float2 rm = walk ? t.rho[m] : make_float2(1.f, 0.f);
+  const float2 db0 = t.dp[j0 * P2 + b], dm0 = t.dp[j0 * P2 + m];
+  auto next = [&](int j, float2& db, float2& dm) {
+    if (walk) {
+      db = cmul(db, rb);
+      dm = cmul(dm, rm);
+    } else if (j + 1 < K) {
+      db = t.dp[(j + 1) * P2 + b];
+      dm = t.dp[(j + 1) * P2 + m];
+    }
+  };
+  auto h_sym = [&](float2 db, float2 dm) {  // (h_b + conj h_m) / 2, conj_symmetrize_nyquist
+    const float2 hb = h_of(db, e1b, e2b), hm = h_of(dm, e1m, e2m);
+    return make_float2(0.5f * (hb.x + hm.x), 0.5f * (hb.y - hm.y));
+  };
+  // pass 1: X-hat = num / den
+  float nx = 0.f, ny = 0.f, dd = 0.f;
+  {
+    float2 db = db0, dm = dm0;
+    for (int j = j0; j < j1; ++j) {
+      const float2 h = h_sym(db, dm);
+      const float2 c = cmulc(h, y_of(j));
+      nx += c.x;
+      ny += c.y;
+      dd += h.x * h.x + h.y * h.y;
+      next(j, db, dm);
+    }
   }
+  BinLoss L;
+  L.wk = k * scale;
+  L.den = eps_m + group_sum(dd);
+  L.inv = L.den > 0.f ? 1.f / L.den : 0.f;
+  const float2 num = make_float2(group_sum(nx), group_sum(ny));
+  L.x = make_float2(num.x * L.inv, num.y * L.inv);
+  L.G = make_float2(num.x * (eps_m * L.inv), -num.y * (eps_m * L.inv));
+  L.gx = L.G.x * L.x.x - L.G.y * L.x.y;
+  // pass 2: residuals and the unsymmetrised dL/dH_j -> exchange
+  float acc = 0.f;
+  {
+    float2 db = db0, dm = dm0;
+    for (int j = j0; j < j1; ++j) {
+      const float2 h = h_sym(db, dm), y = y_of(j);
+      const float2 hx = cmul(h, L.x);
+      const float2 r = make_float2(y.x - hx.x, y.y - hx.y);
+      acc += r.x * r.x + r.y * r.y;
+      const float2 g = bin_grad(L, h, y, implicit != 0);
+      if (active) s_g[static_cast<size_t>(slot) * K + j] = live ? g : make_float2(0.f, 0.f);
+      next(j, db, dm);
+    }
+  }
+  acc = group_sum(acc);
+  const double value = live && q == 0 ? static_cast<double>(L.wk) * acc : 0.0;
   block_sum_store(value, s_red, loss_part + patch * n_parts + part0);
   __syncthreads();  // the exchange buffer of every slot is complete
-  if (slot < S) {
-    const int sm = nyq_slot(t.mirror[b], t.P);
-    float G1 = 0.f, G2 = 0.f;
-    const float k = t.kmag[b];
-    if (k * scale != 0.f) {
-      float2 e1b, e2b;
-      bin_phases(t, s_w, b, e1b, e2b);
-      const bool walk = t.rho != nullptr;
-      const float2 rb = walk ? t.rho[b] : make_float2(1.f, 0.f);
-      float2 db = t.dp[b];
-#pragma unroll 4
-      for (int j = 0; j < K; ++j) {
-        float2 gb = s_g[slot * K + j], gm = s_g[sm * K + j];
-        float2 gs = make_float2(0.5f * (gb.x + gm.x), 0.5f * (gb.y - gm.y));
-        pullback(gs, db, e1b, e2b, k, G1, G2);
-        if (walk)
-          db = cmul(db, rb);
-        else if (j + 1 < K)
-          db = t.dp[(j + 1) * P2 + b];
-      }
+  // symmetrised pullback g = (dL/dH_b + conj(dL/dH_m)) / 2 over this lane's delays
+  float G1 = 0.f, G2 = 0.f;
+  if (live) {
+    const int sm = nyq_slot(m, t.P);
+    float2 db = db0, dm = dm0;
+    for (int j = j0; j < j1; ++j) {
+      const float2 gb = s_g[slot * K + j], gm = s_g[sm * K + j];
+      const float2 gs = make_float2(0.5f * (gb.x + gm.x), 0.5f * (gb.y - gm.y));
+      pullback(gs, db, e1b, e2b, k, G1, G2);
+      next(j, db, dm);
     }
-    gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G1, G2);
   }
+  G1 = group_sum(G1);
+  G2 = group_sum(G2);
+  if (active && q == 0) gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G1, G2);
 }
 
 // Kernel B: dL/dw by the per-angle gather through the static CSR table (one
@@ -784,7 +838,7 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
   }
   PACT_TRY_S(after_launch(ctx, "loss_bins_kernel"));
   if (t.P % 2 == 0) {
-    const int S = 2 * t.P - 1, nt = div_up(S, 32) * 32;
+    const int S = 2 * t.P - 1, nt = div_up(S * kTps, 32) * 32;
     if (nt > 1024) return validation("fused loss: patch size too large for the Nyquist kernel");
     const size_t plane = sizeof(float2) * t.K * S, base = sizeof(float) * ((t.A + 1) & ~1);
     const int stage_y = base + 2 * plane <= 200 * 1024;
