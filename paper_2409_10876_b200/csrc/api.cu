@@ -326,7 +326,8 @@ int pact_deconvolve_image(pact_ctx* ctx, const float* stack, int32_t K, const do
   ra.centers = dc;
   ra.n_rays = n * opt->n_angles;
   make_raster_texture(sos_dev, lay->grid.width, lay->grid.height, &ra.tex);
-  Status wst = launch_wavefront(ctx, ra, w);
+  Status wst = ray_plan_cached(ctx, ra, centers.data(), n);
+  if (wst.ok()) wst = launch_wavefront(ctx, ra, w);
   if (ra.tex) {
     cudaStreamSynchronize(ctx->stream);
     cudaDestroyTextureObject(ra.tex);

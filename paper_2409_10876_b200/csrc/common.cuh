@@ -31,6 +31,12 @@ inline Status validation(const char* msg) {
   return {PACT_E_VALIDATION};
 }
 
+// A broken library invariant (reported as a CUDA-class failure).
+inline Status internal_error(const char* msg) {
+  set_error("internal: %s", msg);
+  return {PACT_E_CUDA};
+}
+
 inline Status cuda_status(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return {};
   set_error("%s: %s", what, cudaGetErrorString(e));
@@ -56,6 +62,9 @@ struct pact_ctx {
   // Per-context caches of the standalone entry points (api.cu).
   void* api = nullptr;
   void (*api_free)(void*) = nullptr;
+  // Ray-plan cache of the standalone ray entry points (raymarch.cu).
+  void* rays = nullptr;
+  void (*rays_free)(void*) = nullptr;
 };
 
 namespace pactgpu {

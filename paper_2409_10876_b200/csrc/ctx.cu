@@ -92,6 +92,7 @@ int pact_ctx_destroy(pact_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->api && ctx->api_free) ctx->api_free(ctx->api);
+  if (ctx->rays && ctx->rays_free) ctx->rays_free(ctx->rays);
   for (auto& s : ctx->scratch) pool_free(s.ptr, ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

@@ -106,6 +106,16 @@ __device__ __forceinline__ Stencil stencil_at(float fx, float fy, int W, int H) 
   return s;
 }
 
+// Per-ray record of a ray plan (raymarch.cu: ray_plan_kernel), computed once
+// per geometry.
+struct RayRec {
+  float fxs, fys, dfx, dfy;  // midpoint pixel coordinates f_i = f_s + i df
+  double dl;                 // step length
+  int n;                     // steps
+  int i_side, i_corner;      // regime boundaries or, generic rays, the fp64 corner index
+  int flags;
+};
+
 // Arguments of the ray-march kernels (raymarch.cu).
 struct RayArgs {
   const float* dv;  // SOS deviation raster v - v0, [H][W]
@@ -121,6 +131,14 @@ struct RayArgs {
   // Optional pitch-2D texture over dv (0: plain loads).  Interior stencils are
   // then one tex2Dgather instead of four scattered loads.
   cudaTextureObject_t tex;
+  // Work plan of the texture path (ray_plan_get, raymarch.cu): per-ray
+  // records, the sorted chunk list, each ray's partial-sum slots and the
+  // owner's forward partials.
+  const RayRec* rec;
+  const int4* items;
+  const int2* ray_slots;
+  float* partial;
+  int n_items;
 };
 
 // Creates a point-sampled, clamped pitch-2D texture over a row-major fp32

@@ -18,14 +18,24 @@
 // clamp onto one border cell for long runs) and flushes with fp64 atomics,
 // skipping zero-weight corners; fp64 accumulation makes the result
 // reproducible to fp32 output precision regardless of atomic order.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
 #include "geom.cuh"
+#include "train_ops.cuh"
 
 // RAY_EXP (experiments only, never set in the product build): 1 = interior
 // carries without atomics, 2 = interior without carries.
 #ifndef RAY_EXP
 #define RAY_EXP 0
 #endif
+#define RAY_NO_INT_ATOM (RAY_EXP == 1 || RAY_EXP == 6)
+#define RAY_NO_LINE_ATOM (RAY_EXP == 5 || RAY_EXP == 6)
 
 namespace pactgpu {
 
@@ -196,7 +206,7 @@ struct CellAcc {
           n01 += t == 1 ? val : 0.f;
           n10 += t == 2 ? val : 0.f;
           n11 += t == 3 ? val : 0.f;
-        } else if (val != 0.f && RAY_EXP == 0) {
+        } else if (val != 0.f && !RAY_NO_INT_ATOM) {
           atomicAdd(grad + (cy + (q >> 1)) * W + cx + (q & 1), static_cast<double>(val));
         }
       }
@@ -220,7 +230,7 @@ struct CellAcc {
     }
     // old slot (i, j) [x i, y j] survives iff (i - dx, j - dy) is in the new cell
     const bool keep_x0 = dx <= 0, keep_x1 = dx >= 0, keep_y0 = dy <= 0, keep_y1 = dy >= 0;
-    if (RAY_EXP == 0) {
+    if (!RAY_NO_INT_ATOM) {
       double* p = grad + cy * W + cx;
       if (!(keep_x0 && keep_y0) && a00 != 0.f) atomicAdd(p, static_cast<double>(a00));
       if (!(keep_x1 && keep_y0) && a01 != 0.f) atomicAdd(p + 1, static_cast<double>(a01));
@@ -307,6 +317,30 @@ __device__ __forceinline__ Regimes regimes(const RayPix& rp, int n, float Wm1, f
   return {min(ix, iy), max(ix, iy), ix < iy};
 }
 
+// The border line a ray runs along once one coordinate has left the grid:
+// the moving coordinate f = fs + i df and its line in the smem border
+// [colL H | colR H | rowB W | rowT W] (offset off, cells 0..qmax).
+struct SideLine {
+  float fs, df;
+  int off, qmax;
+};
+
+__device__ __forceinline__ SideLine side_line(const Regimes& rg, const RayPix& rp, int W, int H) {
+  SideLine s;
+  if (rg.x_first) {
+    s.fs = rp.fys;
+    s.df = rp.dfy;
+    s.off = rp.dfx > 0.f ? H : 0;
+    s.qmax = H - 2;
+  } else {
+    s.fs = rp.fxs;
+    s.df = rp.dfx;
+    s.off = 2 * H + (rp.dfy > 0.f ? W : 0);
+    s.qmax = W - 2;
+  }
+  return s;
+}
+
 __device__ __forceinline__ float interior_d(cudaTextureObject_t tex, float fx, float fy, int W,
                                             int H, float& ax, float& ay, int& ix, int& iy) {
   ix = min(static_cast<int>(fx), W - 2);
@@ -321,118 +355,13 @@ __device__ __forceinline__ float interior_d(cudaTextureObject_t tex, float fx, f
   return fmaf(ay, bot - top, top);
 }
 
-// Threads per ray in the split kernels: each ray's steps are cut into SEG
-// contiguous segments of about equal cost (an interior step costs ~2 border
-// steps, corner steps are free), one lane each; the lanes of a ray are
-// adjacent in the warp (forward partial sums are shuffled in a fixed order).
-constexpr int SEG = 1;
-// Blocks of the split kernels: one wave, evenly loaded.  All rays are
-// resident at once (115k rays at cfg3 vs 148 x 2048 thread slots), so the
-// kernel time is set by the most loaded SM: ceil(n_rays / SMs) rounded to a
-// warp, one block per SM.  (Measured at cfg3: 256-thread blocks leave 4 blocks
-// on some SMs, 0.855 ms; 800-thread blocks 0.820 ms.)  The wavefront pass is
-// fastest with two whole patches (1024 rays) per block when that still fills
-// most SMs (texture-cache locality: 0.252 vs 0.293 ms).
-constexpr int kRayBlockMax = 1024;
-
-int ray_block(const RayArgs& a, int num_sms, bool wavefront) {
-  if (wavefront && a.n_rays >= kRayBlockMax * (num_sms / 2)) return kRayBlockMax;
-  const int per_sm = div_up(a.n_rays, std::max(1, num_sms));
-  return std::min(kRayBlockMax, std::max(256, div_up(per_sm, 32) * 32));
-}
-
-struct Segment {
-  int lo, hi;
-};
-
-__device__ __forceinline__ Segment segment_of(const Regimes& rg, int n, int seg) {
-  const int side_end = min(rg.i_corner, n);
-  const int cost = 2 * rg.i_side + (side_end - rg.i_side);
-  auto at_cost = [&](int c) {  // first step index whose cumulative cost reaches c
-    return c <= 2 * rg.i_side ? (c + 1) / 2 : min(side_end, rg.i_side + (c - 2 * rg.i_side));
-  };
-  const int lo = seg == 0 ? 0 : at_cost(cost * seg / SEG);
-  const int hi = seg == SEG - 1 ? n : at_cost(cost * (seg + 1) / SEG);
-  return {lo, hi};
-}
-
-__global__ void __launch_bounds__(kRayBlockMax) wavefront_split_kernel(RayArgs a, float* __restrict__ w) {
-  extern __shared__ float s_border[];
-  const Border bd = load_border(a, s_border);
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = t / SEG, seg = t % SEG;
-  float acc = 0.f;
-  double dl = 0.0;
-  if (r < a.n_rays) {
-    int patch = r / a.n_angles, ang = r - patch * a.n_angles;
-    double2 c = a.centers[patch];
-    Ray ray = make_ray(c.x, c.y, ang, a.n_angles, a.ring_r, a.mcx, a.mcy, a.mr, a.step);
-    dl = ray.dl;
-    const RayPix rp = ray_pixels(a, c.x, c.y, ray);
-    const float v0 = static_cast<float>(a.v0);
-    const int W = a.W, H = a.H, n = ray.n;
-    const float Wm1 = static_cast<float>(W - 1), Hm1 = static_cast<float>(H - 1);
-    if (n > 0 && (out_at(0, rp.fxs, rp.dfx, Wm1) || out_at(0, rp.fys, rp.dfy, Hm1))) {
-      if (seg == 0) acc = march_forward_generic<true>(a, bd, rp, n, v0);
-    } else if (n > 0) {
-      const Regimes rg = regimes(rp, n, Wm1, Hm1);
-      const Segment sg = segment_of(rg, n, seg);
-      const int i1 = min(rg.i_side, sg.hi);
-#pragma unroll 4
-      for (int i = sg.lo; i < i1; ++i) {
-        float ax, ay;
-        int ix, iy;
-        const float d = interior_d(a.tex, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
-                                   fmaf(static_cast<float>(i), rp.dfy, rp.fys), W, H, ax, ay, ix,
-                                   iy);
-        acc += __fdividef(d, v0 + d);
-      }
-      const int s0 = max(rg.i_side, sg.lo), s1 = min(rg.i_corner, sg.hi);
-      if (rg.x_first) {
-        const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
-#pragma unroll 4
-        for (int i = s0; i < s1; ++i) {
-          const float fy = fmaf(static_cast<float>(i), rp.dfy, rp.fys);
-          const int iy = min(static_cast<int>(fy), H - 2);
-          const float c0 = col[iy];
-          const float d = fmaf(fy - iy, col[iy + 1] - c0, c0);
-          acc += __fdividef(d, v0 + d);
-        }
-      } else {
-        const float* row = rp.dfy > 0.f ? bd.rowT : bd.rowB;
-#pragma unroll 4
-        for (int i = s0; i < s1; ++i) {
-          const float fx = fmaf(static_cast<float>(i), rp.dfx, rp.fxs);
-          const int ix = min(static_cast<int>(fx), W - 2);
-          const float c0 = row[ix];
-          const float d = fmaf(fx - ix, row[ix + 1] - c0, c0);
-          acc += __fdividef(d, v0 + d);
-        }
-      }
-      const int n_corner = sg.hi - max(rg.i_corner, sg.lo);
-      if (n_corner > 0) {
-        const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
-        const float d = col[rp.dfy > 0.f ? H - 1 : 0];
-        acc += static_cast<float>(n_corner) * __fdividef(d, v0 + d);
-      }
-    }
-  }
-  // fixed-order sum of the ray's segments (lanes r*SEG .. r*SEG + SEG - 1)
-#pragma unroll
-  for (int o = 1; o < SEG; o <<= 1) {
-    const float other = __shfl_down_sync(0xffffffffu, acc, o, SEG);
-    acc += other;
-  }
-  if (r < a.n_rays && seg == 0) w[r] = static_cast<float>(dl) * acc;
-}
-
 // 1-D carry along a border line: pixels (line position q, q + 1).
 struct LineAcc {
   int q = -1;
   float b0 = 0.f, b1 = 0.f;
   __device__ __forceinline__ void move(double* __restrict__ grad, int nq, int stride, int base) {
     if (nq == q) return;
-    if (q >= 0 && RAY_EXP != 5) {
+    if (q >= 0 && !RAY_NO_LINE_ATOM) {
       if (nq == q + 1) {
         if (b0 != 0.f) atomicAdd(grad + base + q * stride, static_cast<double>(b0));
         b0 = b1;
@@ -461,116 +390,209 @@ struct LineAcc {
 // contend.  They go to one of kBorderReplicas copies of the border (by block)
 // and border_reduce_kernel folds the copies into the raster afterwards in a
 // fixed order.  Replica layout: [R][colL H | colR H | rowB W | rowT W].
-constexpr int kBorderReplicas = 32;
+#ifndef RAY_REPLICAS
+#define RAY_REPLICAS 32
+#endif
+constexpr int kBorderReplicas = RAY_REPLICAS;
 
-__global__ void __launch_bounds__(kRayBlockMax) ray_backward_split_kernel(RayArgs a, const float* __restrict__ dw,
-                                                                 double* __restrict__ grad,
-                                                                 double* __restrict__ border_rep) {
+// ---- planned marches -------------------------------------------------------
+// The ray geometry (centres, angles, mask, grid) is fixed for a whole
+// reconstruction; only the raster changes.  ray_plan_get therefore computes
+// once per geometry each ray's record (fp64 setup, regime boundaries) and a
+// work list: each ray's interior and border-line step ranges cut into chunks
+// of at most kRayChunk steps, sorted by (regime, length) so that the 32 lanes
+// of a warp run equal trip counts of the same loop.  Block b takes items
+// [256 b, 256 b + 256), longest work first; consecutive items are adjacent
+// rays at the same distance, so an SM's resident warps march one neighbourhood
+// of the raster (texture-cache locality).  (A persistent variant with a work
+// counter measured slower: 0.73 vs 0.53 ms for the cfg3 adjoint, and it
+// starves the concurrent frames' kernels.)  The forward pass writes one
+// partial sum per item and ray_finish_kernel adds each ray's partials in a
+// fixed order; the adjoint flushes its carries per item.
+constexpr int kRecGeneric = 1;  // starts outside the grid: per-step generic march
+constexpr int kRecXFirst = 2;   // x leaves the grid first
+
+enum ItemKind { kItemInterior = 0, kItemSide = 1, kItemGeneric = 2 };
+// item = {ray, lo, hi, slot | kind << 28 | corner << 30}
+__device__ __forceinline__ int item_kind(int w) { return (w >> 28) & 3; }
+__device__ __forceinline__ bool item_corner(int w) { return (w >> 30) & 1; }
+__device__ __forceinline__ int item_slot(int w) { return w & 0x0fffffff; }
+
+__global__ void ray_plan_kernel(RayArgs a, RayRec* __restrict__ rec) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.n_rays) return;
+  const int patch = r / a.n_angles, ang = r - patch * a.n_angles;
+  const double2 c = a.centers[patch];
+  const Ray ray = make_ray(c.x, c.y, ang, a.n_angles, a.ring_r, a.mcx, a.mcy, a.mr, a.step);
+  RayRec o{};
+  o.n = ray.n;
+  o.dl = ray.dl;
+  if (ray.n > 0) {
+    const RayPix rp = ray_pixels(a, c.x, c.y, ray);
+    o.fxs = rp.fxs;
+    o.fys = rp.fys;
+    o.dfx = rp.dfx;
+    o.dfy = rp.dfy;
+    const float Wm1 = static_cast<float>(a.W - 1), Hm1 = static_cast<float>(a.H - 1);
+    if (out_at(0, rp.fxs, rp.dfx, Wm1) || out_at(0, rp.fys, rp.dfy, Hm1)) {
+      o.flags = kRecGeneric;
+      o.i_corner = rp.i_corner;
+    } else {
+      const Regimes rg = regimes(rp, ray.n, Wm1, Hm1);
+      o.i_side = rg.i_side;
+      o.i_corner = rg.i_corner;
+      o.flags = rg.x_first ? kRecXFirst : 0;
+    }
+  }
+  rec[r] = o;
+}
+
+__device__ __forceinline__ RayPix rec_pixels(const RayRec& r) {
+  return {r.fxs, r.fys, r.dfx, r.dfy, r.i_corner};
+}
+
+__device__ __forceinline__ Regimes rec_regimes(const RayRec& r) {
+  return {r.i_side, r.i_corner, (r.flags & kRecXFirst) != 0};
+}
+
+__global__ void __launch_bounds__(256) wavefront_plan_kernel(RayArgs a) {
   extern __shared__ float s_border[];
   const Border bd = load_border(a, s_border);
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = t / SEG, seg = t % SEG;
-  if (r >= a.n_rays) return;
-  const float gr = dw[r];
-  if (gr == 0.f) return;  // aberration.hpp:340
-  int patch = r / a.n_angles, ang = r - patch * a.n_angles;
-  double2 c = a.centers[patch];
-  Ray ray = make_ray(c.x, c.y, ang, a.n_angles, a.ring_r, a.mcx, a.mcy, a.mr, a.step);
-  if (ray.n == 0) return;
-  const RayPix rp = ray_pixels(a, c.x, c.y, ray);
+  const int W = a.W, H = a.H;
   const float v0 = static_cast<float>(a.v0);
-  // f = g * dl * v0 / v^2 per step (aberration.hpp:354-355)
-  const float gscale = static_cast<float>(static_cast<double>(gr) * ray.dl * a.v0);
-  const int W = a.W, H = a.H, n = ray.n;
-  const float Wm1 = static_cast<float>(W - 1), Hm1 = static_cast<float>(H - 1);
-  if (out_at(0, rp.fxs, rp.dfx, Wm1) || out_at(0, rp.fys, rp.dfy, Hm1)) {
-    if (seg == 0) march_backward_generic<true>(a, bd, rp, n, v0, gscale, grad);
-    return;
-  }
-  const Regimes rg = regimes(rp, n, Wm1, Hm1);
-  const Segment sg = segment_of(rg, n, seg);
   {
-    // interior: gathers issued four steps at a time, then the carries
-    CellAcc cell;
-    const int i1 = min(rg.i_side, sg.hi);
-    int i = sg.lo;
-    for (; i < i1; i += 4) {
-      float4 g[4];
-      float ax[4], ay[4];
-      int ix[4], iy[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float fx = fmaf(static_cast<float>(min(i + u, i1 - 1)), rp.dfx, rp.fxs);
-        const float fy = fmaf(static_cast<float>(min(i + u, i1 - 1)), rp.dfy, rp.fys);
-        ix[u] = min(static_cast<int>(fx), W - 2);
-        iy[u] = min(static_cast<int>(fy), H - 2);
-        ax[u] = fx - ix[u];
-        ay[u] = fy - iy[u];
-        g[u] = tex2Dgather<float4>(a.tex, ix[u] + 1.f, iy[u] + 1.f, 0);
+    const int it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (it >= a.n_items) return;
+    const int4 item = a.items[it];
+    const RayRec rr = a.rec[item.x];
+    const int lo = item.y, hi = item.z, kind = item_kind(item.w);
+    float acc = 0.f;
+    if (kind == kItemInterior) {
+#pragma unroll 4
+      for (int i = lo; i < hi; ++i) {
+        float ax, ay;
+        int ix, iy;
+        const float d = interior_d(a.tex, fmaf(static_cast<float>(i), rr.dfx, rr.fxs),
+                                   fmaf(static_cast<float>(i), rr.dfy, rr.fys), W, H, ax, ay, ix,
+                                   iy);
+        acc += __fdividef(d, v0 + d);
       }
+    } else if (kind == kItemSide) {
+      // border line: one loop for both orientations; the line is a slice of
+      // the smem border
+      const SideLine sl = side_line(rec_regimes(rr), rec_pixels(rr), W, H);
+#pragma unroll 4
+      for (int i = lo; i < hi; ++i) {
+        const float f = fmaf(static_cast<float>(i), sl.df, sl.fs);
+        const int q = min(static_cast<int>(f), sl.qmax);
+        const float c0 = s_border[sl.off + q];
+        const float d = fmaf(f - q, s_border[sl.off + q + 1] - c0, c0);
+        acc += __fdividef(d, v0 + d);
+      }
+    } else {
+      acc = march_forward_generic<true>(a, bd, rec_pixels(rr), rr.n, v0);
+    }
+    if (item_corner(item.w)) {  // both coordinates clamped: one pixel to the end
+      const float* col = rr.dfx > 0.f ? bd.colR : bd.colL;
+      const float d = col[rr.dfy > 0.f ? H - 1 : 0];
+      acc += static_cast<float>(rr.n - rr.i_corner) * __fdividef(d, v0 + d);
+    }
+    a.partial[item_slot(item.w)] = acc;
+  }
+}
+
+// w[r] = dl * (sum of the ray's item partials, in item order).
+__global__ void ray_finish_kernel(RayArgs a, float* __restrict__ w) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.n_rays) return;
+  const int2 sl = a.ray_slots[r];
+  float acc = 0.f;
+  for (int k = 0; k < sl.y; ++k) acc += a.partial[sl.x + k];
+  w[r] = static_cast<float>(a.rec[r].dl) * acc;
+}
+
+// (256, 4): at most 64 registers, four blocks per SM (0.53 vs 0.56 ms at 68)
+__global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, const float* __restrict__ dw,
+                                                                  double* __restrict__ grad,
+                                                                  double* __restrict__ border_rep) {
+  extern __shared__ float s_border[];
+  const Border bd = load_border(a, s_border);
+  const int W = a.W, H = a.H;
+  const float v0 = static_cast<float>(a.v0);
+  double* rep = border_rep + static_cast<size_t>(blockIdx.x % kBorderReplicas) * 2 * (W + H);
+  {
+    const int it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (it >= a.n_items) return;
+    const int4 item = a.items[it];
+    const float gr = dw[item.x];
+    if (gr == 0.f) return;  // aberration.hpp:340
+    const RayRec rr = a.rec[item.x];
+    // f = g * dl * v0 / v^2 per step (aberration.hpp:354-355)
+    const float gscale = static_cast<float>(static_cast<double>(gr) * rr.dl * a.v0);
+    const int lo = item.y, hi = item.z, kind = item_kind(item.w);
+    if (kind == kItemInterior) {
+      // gathers issued four steps at a time, then the carries
+      CellAcc cell;
+      for (int i = lo; i < hi; i += 4) {
+        float4 gt[4];
+        float ax[4], ay[4];
+        int ix[4], iy[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (i + u < i1) {
-          // gather order: w=(ix,iy) z=(ix+1,iy) x=(ix,iy+1) y=(ix+1,iy+1)
-          const float top = fmaf(ax[u], g[u].z - g[u].w, g[u].w);
-          const float bot = fmaf(ax[u], g[u].y - g[u].x, g[u].x);
-          const float v = v0 + fmaf(ay[u], bot - top, top);
-          const float f = __fdividef(gscale, v * v);
-          if (RAY_EXP != 2) cell.move_unit(grad, W, ix[u], iy[u]);
-          const float fy1 = f * ay[u], fy0 = f - fy1;  // f (1 - ay), f ay
-          cell.a00 = fmaf(-fy0, ax[u], cell.a00 + fy0);
-          cell.a01 = fmaf(fy0, ax[u], cell.a01);
-          cell.a10 = fmaf(-fy1, ax[u], cell.a10 + fy1);
-          cell.a11 = fmaf(fy1, ax[u], cell.a11);
+        for (int u = 0; u < 4; ++u) {
+          const float k = static_cast<float>(min(i + u, hi - 1));
+          const float fx = fmaf(k, rr.dfx, rr.fxs), fy = fmaf(k, rr.dfy, rr.fys);
+          ix[u] = min(static_cast<int>(fx), W - 2);
+          iy[u] = min(static_cast<int>(fy), H - 2);
+          ax[u] = fx - ix[u];
+          ay[u] = fy - iy[u];
+          gt[u] = tex2Dgather<float4>(a.tex, ix[u] + 1.f, iy[u] + 1.f, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (i + u < hi) {
+            // gather order: w=(ix,iy) z=(ix+1,iy) x=(ix,iy+1) y=(ix+1,iy+1)
+            const float top = fmaf(ax[u], gt[u].z - gt[u].w, gt[u].w);
+            const float bot = fmaf(ax[u], gt[u].y - gt[u].x, gt[u].x);
+            const float v = v0 + fmaf(ay[u], bot - top, top);
+            const float f = __fdividef(gscale, v * v);
+            if (RAY_EXP != 2) cell.move_unit(grad, W, ix[u], iy[u]);
+            const float fy1 = f * ay[u], fy0 = f - fy1;  // f (1 - ay), f ay
+            cell.a00 = fmaf(-fy0, ax[u], cell.a00 + fy0);
+            cell.a01 = fmaf(fy0, ax[u], cell.a01);
+            cell.a10 = fmaf(-fy1, ax[u], cell.a10 + fy1);
+            cell.a11 = fmaf(fy1, ax[u], cell.a11);
+          }
         }
       }
-    }
-    cell.flush(grad, W, H);
-  }
-  const int s0 = max(rg.i_side, sg.lo), s1 = min(rg.i_corner, sg.hi);
-  if (s0 < s1) {
-    LineAcc line;
-    double* rep = border_rep + static_cast<size_t>(blockIdx.x % kBorderReplicas) * 2 * (W + H);
-    if (rg.x_first) {
-      const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
-      double* dst = rep + (rp.dfx > 0.f ? H : 0);
-      for (int i = s0; i < s1; ++i) {
-        const float fy = fmaf(static_cast<float>(i), rp.dfy, rp.fys);
-        const int iy = min(static_cast<int>(fy), H - 2);
-        const float ay = fy - iy, c0 = col[iy];
-        const float v = v0 + fmaf(ay, col[iy + 1] - c0, c0);
-        const float f = __fdividef(gscale, v * v);
-        line.move(dst, iy, 1, 0);
-        const float f1 = f * ay;
-        line.b0 += f - f1;
-        line.b1 += f1;
+      cell.flush(grad, W, H);
+    } else if (kind == kItemSide) {
+      // border line (one loop for both orientations); the replica slice has
+      // the smem border's layout
+      const SideLine sl = side_line(rec_regimes(rr), rec_pixels(rr), W, H);
+      double* dst = rep + sl.off;
+      LineAcc line;
+      for (int i = lo; i < hi; ++i) {
+        const float f = fmaf(static_cast<float>(i), sl.df, sl.fs);
+        const int q = min(static_cast<int>(f), sl.qmax);
+        const float fa = f - q, c0 = s_border[sl.off + q];
+        const float v = v0 + fmaf(fa, s_border[sl.off + q + 1] - c0, c0);
+        const float gv = __fdividef(gscale, v * v);
+        line.move(dst, q, 1, 0);
+        const float g1 = gv * fa;
+        line.b0 += gv - g1;
+        line.b1 += g1;
       }
       line.flush(dst, 1, 0);
     } else {
-      const float* row = rp.dfy > 0.f ? bd.rowT : bd.rowB;
-      double* dst = rep + 2 * H + (rp.dfy > 0.f ? W : 0);
-      for (int i = s0; i < s1; ++i) {
-        const float fx = fmaf(static_cast<float>(i), rp.dfx, rp.fxs);
-        const int ix = min(static_cast<int>(fx), W - 2);
-        const float ax = fx - ix, c0 = row[ix];
-        const float v = v0 + fmaf(ax, row[ix + 1] - c0, c0);
-        const float f = __fdividef(gscale, v * v);
-        line.move(dst, ix, 1, 0);
-        const float f1 = f * ax;
-        line.b0 += f - f1;
-        line.b1 += f1;
-      }
-      line.flush(dst, 1, 0);
+      march_backward_generic<true>(a, bd, rec_pixels(rr), rr.n, v0, gscale, grad);
     }
-  }
-  const int n_corner = sg.hi - max(rg.i_corner, sg.lo);
-  if (n_corner > 0) {
-    const int px = rp.dfx > 0.f ? W - 1 : 0, py = rp.dfy > 0.f ? H - 1 : 0;
-    const float* col = rp.dfx > 0.f ? bd.colR : bd.colL;
-    const float v = v0 + col[py];
-    const float f = __fdividef(gscale, v * v) * static_cast<float>(n_corner);
-    double* rep = border_rep + static_cast<size_t>(blockIdx.x % kBorderReplicas) * 2 * (W + H);
-    if (f != 0.f) atomicAdd(rep + (px == 0 ? 0 : H) + py, static_cast<double>(f));
+    if (item_corner(item.w)) {
+      const int px = rr.dfx > 0.f ? W - 1 : 0, py = rr.dfy > 0.f ? H - 1 : 0;
+      const float* col = rr.dfx > 0.f ? bd.colR : bd.colL;
+      const float v = v0 + col[py];
+      const float f = __fdividef(gscale, v * v) * static_cast<float>(rr.n - rr.i_corner);
+      if (f != 0.f) atomicAdd(rep + (px == 0 ? 0 : H) + py, static_cast<double>(f));
+    }
   }
 }
 
@@ -699,6 +721,221 @@ Status validate_centers(const pact_ring& ring, int n, const double* centers) {
   return {};
 }
 
+// ---- ray plans ---------------------------------------------------------------
+namespace {
+
+constexpr int kRayChunk = 128;  // max steps per work item (PACT_RAY_CHUNK overrides)
+constexpr int kPlanBlock = 256;
+constexpr int kLenBucket = 32;
+
+int ray_chunk() {
+  static const int c = [] {
+    const char* e = std::getenv("PACT_RAY_CHUNK");
+    const int v = e ? std::atoi(e) : 0;
+    return v >= 8 ? v : kRayChunk;
+  }();
+  return c;
+}
+
+}  // namespace
+
+// Immutable part of a plan, shared by every owner of the same geometry.
+struct RayPlanData {
+  void* mem = nullptr;  // rec | items | ray_slots (cudaMalloc)
+  const RayRec* rec = nullptr;
+  const int4* items = nullptr;
+  const int2* ray_slots = nullptr;
+  int n_items = 0;
+  std::vector<double> key;
+  ~RayPlanData() {
+    if (mem) cudaFree(mem);
+  }
+};
+
+namespace {
+
+std::vector<double> plan_key(const RayArgs& a, const double* centers, int n_centers) {
+  std::vector<double> key = {static_cast<double>(a.W), static_cast<double>(a.H), a.ox, a.oy,
+                             a.inv_pitch, a.ring_r, a.mcx, a.mcy, a.mr, a.step,
+                             static_cast<double>(a.n_angles), static_cast<double>(a.n_rays)};
+  key.insert(key.end(), centers, centers + 2 * n_centers);
+  return key;
+}
+
+// Builds the shared plan of a's geometry (a.centers on the device).  Synchronous.
+Status build_plan_data(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanData& p) {
+  const int nr = a.n_rays;
+  void* rec_d = nullptr;
+  PACT_CUDA_S(cudaMalloc(&rec_d, sizeof(RayRec) * nr));
+  p.mem = rec_d;  // freed by ~RayPlanData on any failure below
+  ray_plan_kernel<<<div_up(nr, 256), 256, 0, s>>>(a, static_cast<RayRec*>(rec_d));
+  PACT_TRY_S(after_launch(ctx, "ray_plan_kernel"));
+  std::vector<RayRec> rec(nr);
+  PACT_CUDA_S(cudaMemcpyAsync(rec.data(), rec_d, sizeof(RayRec) * nr, cudaMemcpyDeviceToHost, s));
+  PACT_CUDA_S(cudaStreamSynchronize(s));
+  // work items in ray order (slot = index) with their sort keys
+  const int C = ray_chunk();
+  std::vector<int4> items;
+  std::vector<int> key;
+  std::vector<int2> slots(nr);
+  items.reserve(static_cast<size_t>(nr) * 8);
+  key.reserve(static_cast<size_t>(nr) * 8);
+  int max_bucket = 0, max_chunk = 0;
+  auto push = [&](int r, int lo, int hi, int kind, int chunk) {
+    const int slot = static_cast<int>(items.size());
+    items.push_back(make_int4(r, lo, hi, slot | (kind << 28)));
+    const int bucket = (hi - lo + kLenBucket - 1) / kLenBucket;
+    max_bucket = std::max(max_bucket, bucket);
+    max_chunk = std::max(max_chunk, chunk);
+    key.push_back(kind == kItemGeneric ? 0 : kind == kItemInterior ? 1 : 2);  // rank
+    key.push_back(bucket);
+    key.push_back(chunk);
+  };
+  for (int r = 0; r < nr; ++r) {
+    const RayRec& q = rec[r];
+    const int first = static_cast<int>(items.size());
+    if (q.n > 0) {
+      if (q.flags & kRecGeneric) {
+        push(r, 0, q.n, kItemGeneric, 0);
+      } else {
+        const int side_end = std::min(q.i_corner, q.n);
+        for (int i = 0; i < q.i_side; i += C)
+          push(r, i, std::min(q.i_side, i + C), kItemInterior, i / C);
+        for (int i = q.i_side; i < side_end; i += C)
+          push(r, i, std::min(side_end, i + C), kItemSide, (i - q.i_side) / C);
+        if (q.i_corner < q.n && static_cast<int>(items.size()) > first)
+          items.back().w |= 1 << 30;  // the ray's last item adds the corner run
+      }
+    }
+    slots[r] = make_int2(first, static_cast<int>(items.size()) - first);
+  }
+  const int ni = static_cast<int>(items.size());
+  if (ni >= (1 << 28)) return validation("ray plan: too many work items");
+  // Schedule: longest work first -- generic rays, interior chunks (a gather
+  // and a carry per step), border-line chunks -- lengths in buckets of
+  // kLenBucket steps (at most kLenBucket - 1 idle steps per lane), then by
+  // chunk index, then ray, so a warp holds adjacent angles at the same
+  // distance.  A stable counting sort on (rank, -bucket, chunk) keeps ray order.
+  const int nb = max_bucket + 1, nc = max_chunk + 1;
+  const size_t n_keys = static_cast<size_t>(3) * nb * nc;
+  std::vector<int> start(n_keys + 1, 0);
+  std::vector<int> ck(ni);
+  for (int k = 0; k < ni; ++k) {
+    const int* kk = &key[3 * static_cast<size_t>(k)];
+    ck[k] = (kk[0] * nb + (nb - 1 - kk[1])) * nc + kk[2];
+    ++start[ck[k] + 1];
+  }
+  for (size_t k = 0; k < n_keys; ++k) start[k + 1] += start[k];
+  std::vector<int4> sorted(std::max(ni, 1));
+  for (int k = 0; k < ni; ++k) sorted[start[ck[k]]++] = items[k];
+  // one allocation: rec | items | slots
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t o_items = al(sizeof(RayRec) * nr), o_slots = al(o_items + sizeof(int4) * sorted.size()),
+               total = o_slots + sizeof(int2) * nr;
+  void* mem = nullptr;
+  PACT_CUDA_S(cudaMalloc(&mem, total));
+  char* b = static_cast<char*>(mem);
+  Status st = cuda_status(cudaMemcpyAsync(b, rec_d, sizeof(RayRec) * nr, cudaMemcpyDeviceToDevice,
+                                          s), "ray plan");
+  if (st.ok())
+    st = cuda_status(cudaMemcpyAsync(b + o_items, sorted.data(), sizeof(int4) * sorted.size(),
+                                     cudaMemcpyHostToDevice, s), "ray plan");
+  if (st.ok())
+    st = cuda_status(cudaMemcpyAsync(b + o_slots, slots.data(), sizeof(int2) * nr,
+                                     cudaMemcpyHostToDevice, s), "ray plan");
+  if (st.ok()) st = cuda_status(cudaStreamSynchronize(s), "ray plan");  // host vectors die here
+  cudaFree(rec_d);
+  p.mem = mem;
+  if (!st.ok()) return st;
+  p.rec = reinterpret_cast<const RayRec*>(b);
+  p.items = reinterpret_cast<const int4*>(b + o_items);
+  p.ray_slots = reinterpret_cast<const int2*>(b + o_slots);
+  p.n_items = ni;
+  return {};
+}
+
+// Plans of one context, by geometry (most recent first, a few kept).
+struct RayPlanCache {
+  std::mutex mu;
+  std::vector<std::shared_ptr<RayPlanData>> plans;
+  RayPlan scratch;  // the standalone entry points' partials
+};
+constexpr size_t kPlanCacheSize = 4;
+
+RayPlanCache& plan_cache(pact_ctx* ctx) {
+  static std::mutex init_mu;
+  std::lock_guard<std::mutex> lk(init_mu);
+  if (!ctx->rays) {
+    ctx->rays = new RayPlanCache();
+    ctx->rays_free = [](void* p) {
+      auto* c = static_cast<RayPlanCache*>(p);
+      ray_plan_release(c->scratch, nullptr);
+      delete c;
+    };
+  }
+  return *static_cast<RayPlanCache*>(ctx->rays);
+}
+
+}  // namespace
+
+Status ray_plan_get(pact_ctx* cache_ctx, pact_ctx* ctx, RayArgs& a, const double* centers,
+                    int n_centers, RayPlan& out) {
+  ray_plan_release(out, ctx->stream);
+  a.rec = nullptr;
+  a.items = nullptr;
+  a.ray_slots = nullptr;
+  a.partial = nullptr;
+  a.n_items = 0;
+  if (!a.tex || a.n_rays <= 0) return {};
+  std::vector<double> key = plan_key(a, centers, n_centers);
+  RayPlanCache& c = plan_cache(cache_ctx);
+  std::shared_ptr<RayPlanData> data;
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    for (auto& p : c.plans)
+      if (p->key == key) data = p;
+    if (!data) {
+      auto fresh = std::make_shared<RayPlanData>();
+      PACT_TRY_S(build_plan_data(ctx, ctx->stream, a, *fresh));
+      fresh->key = std::move(key);
+      c.plans.insert(c.plans.begin(), fresh);
+      if (c.plans.size() > kPlanCacheSize) c.plans.pop_back();
+      data = fresh;
+    }
+  }
+  void* part = nullptr;
+  PACT_TRY_S(pool_alloc(&part, sizeof(float) * std::max(data->n_items, 1), ctx->stream));
+  out.data = data;
+  out.partial = static_cast<float*>(part);
+  a.rec = data->rec;
+  a.items = data->items;
+  a.ray_slots = data->ray_slots;
+  a.partial = out.partial;
+  a.n_items = data->n_items;
+  return {};
+}
+
+void ray_plan_release(RayPlan& p, cudaStream_t s) {
+  if (p.partial) pool_free(p.partial, s);
+  p.partial = nullptr;
+  p.data.reset();
+}
+
+Status ray_plan_cached(pact_ctx* ctx, RayArgs& a, const double* centers, int n_centers) {
+  if (!a.tex) return {};
+  RayPlanCache& c = plan_cache(ctx);
+  RayPlan& p = c.scratch;
+  if (p.data && p.data->key == plan_key(a, centers, n_centers)) {
+    a.rec = p.data->rec;
+    a.items = p.data->items;
+    a.ray_slots = p.data->ray_slots;
+    a.partial = p.partial;
+    a.n_items = p.data->n_items;
+    return {};
+  }
+  return ray_plan_get(ctx, ctx, a, centers, n_centers, p);
+}
+
 static size_t border_smem(const RayArgs& a) { return sizeof(float) * 2 * (a.W + a.H); }
 
 template <typename K>
@@ -710,41 +947,42 @@ static Status allow_smem(K kernel, size_t smem) {
 }
 
 Status launch_wavefront(pact_ctx* ctx, const RayArgs& a, float* w) {
-  int blocks = div_up(a.n_rays, 256);
-  size_t smem = border_smem(a);
+  const size_t smem = border_smem(a);
   if (a.tex) {  // make_raster_texture requires W, H >= 2
-    PACT_TRY_S(allow_smem(wavefront_split_kernel, smem));
-    const int rb = ray_block(a, ctx->num_sms, true);
-    wavefront_split_kernel<<<div_up(a.n_rays * SEG, rb), rb, smem, ctx->stream>>>(a, w);
-  } else {
-    PACT_TRY_S(allow_smem(wavefront_kernel<false>, smem));
-    wavefront_kernel<false><<<blocks, 256, smem, ctx->stream>>>(a, w);
+    if (!a.rec) return internal_error("launch_wavefront: ray plan missing");
+    if (a.n_items > 0) {
+      PACT_TRY_S(allow_smem(wavefront_plan_kernel, smem));
+      wavefront_plan_kernel<<<div_up(a.n_items, kPlanBlock), kPlanBlock, smem, ctx->stream>>>(a);
+      PACT_TRY_S(after_launch(ctx, "wavefront_plan_kernel"));
+    }
+    ray_finish_kernel<<<div_up(a.n_rays, 256), 256, 0, ctx->stream>>>(a, w);
+    return after_launch(ctx, "ray_finish_kernel");
   }
-  return after_launch(ctx, a.tex ? "wavefront_split_kernel" : "wavefront_kernel");
+  PACT_TRY_S(allow_smem(wavefront_kernel<false>, smem));
+  wavefront_kernel<false><<<div_up(a.n_rays, 256), 256, smem, ctx->stream>>>(a, w);
+  return after_launch(ctx, "wavefront_kernel");
 }
 
 Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, double* grad) {
-  int blocks = div_up(a.n_rays, 256);
-  size_t smem = border_smem(a);
+  const size_t smem = border_smem(a);
   if (a.tex) {
-    const int rb = ray_block(a, ctx->num_sms, false);
-    blocks = div_up(a.n_rays * SEG, rb);
+    if (!a.rec) return internal_error("launch_ray_backward: ray plan missing");
+    if (a.n_items == 0) return {};
     const size_t rep_n = static_cast<size_t>(kBorderReplicas) * 2 * (a.W + a.H);
     void* rep = nullptr;
     PACT_TRY_S(scratch_get(ctx, kScratchRayBorder, sizeof(double) * rep_n, &rep));
     PACT_CUDA_S(cudaMemsetAsync(rep, 0, sizeof(double) * rep_n, ctx->stream));
-    PACT_TRY_S(allow_smem(ray_backward_split_kernel, smem));
-    ray_backward_split_kernel<<<blocks, rb, smem, ctx->stream>>>(a, dw, grad,
-                                                                   static_cast<double*>(rep));
-    PACT_TRY_S(after_launch(ctx, "ray_backward_split_kernel"));
+    PACT_TRY_S(allow_smem(ray_backward_plan_kernel, smem));
+    ray_backward_plan_kernel<<<div_up(a.n_items, kPlanBlock), kPlanBlock, smem, ctx->stream>>>(
+        a, dw, grad, static_cast<double*>(rep));
+    PACT_TRY_S(after_launch(ctx, "ray_backward_plan_kernel"));
     const int nbp = 2 * a.H + 2 * std::max(a.W - 2, 0);
     border_reduce_kernel<<<div_up(nbp, 256), 256, 0, ctx->stream>>>(static_cast<double*>(rep), a.W,
                                                                      a.H, grad);
     return after_launch(ctx, "border_reduce_kernel");
-  } else {
-    PACT_TRY_S(allow_smem(ray_backward_kernel<false>, smem));
-    ray_backward_kernel<false><<<blocks, 256, smem, ctx->stream>>>(a, dw, grad);
   }
+  PACT_TRY_S(allow_smem(ray_backward_kernel<false>, smem));
+  ray_backward_kernel<false><<<div_up(a.n_rays, 256), 256, smem, ctx->stream>>>(a, dw, grad);
   return after_launch(ctx, "ray_backward_kernel");
 }
 
@@ -787,6 +1025,7 @@ extern "C" int pact_wavefront(pact_ctx* ctx, const pact_ring* ring, const pact_g
   a.n_rays = n_centers * n_angles;
   ScopedTexture tex(ctx, sos_dev, grid->width, grid->height);
   a.tex = tex.t;
+  PACT_TRY(ray_plan_cached(ctx, a, centers, n_centers));
   PACT_TRY(launch_wavefront(ctx, a, w));
   return PACT_OK;
 }
@@ -809,6 +1048,7 @@ extern "C" int pact_ray_backward(pact_ctx* ctx, const pact_ring* ring, const pac
   a.n_rays = n_centers * n_angles;
   ScopedTexture tex(ctx, sos_dev, grid->width, grid->height);
   a.tex = tex.t;
+  PACT_TRY(ray_plan_cached(ctx, a, centers, n_centers));
   PACT_TRY(launch_ray_backward(ctx, a, dw, grad_v));
   return PACT_OK;
 }

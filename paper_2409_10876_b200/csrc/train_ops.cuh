@@ -5,6 +5,8 @@
 #include "common.cuh"
 #include "fourier.cuh"
 
+#include <memory>
+
 namespace pactgpu {
 
 // NumericalError stages, in the order joint_reconstruct checks them.
@@ -18,6 +20,21 @@ struct RayArgs;
 Status ray_args(const pact_ring& ring, const pact_grid& grid, double v0, const pact_mask& mask,
                 int n_angles, double step, RayArgs& a);
 Status validate_centers(const pact_ring& ring, int n, const double* centers);
+// Work plan of the texture-path ray kernels for a fixed geometry (raymarch.cu).
+// The immutable part (records, schedule) is built once per geometry and
+// shared through `cache_ctx`; each owner (trainer, standalone call) holds its
+// own forward partials, allocated on ctx's stream.  ray_plan_get fills the
+// plan fields of `a` (centers: host copy of a.centers); synchronous on a miss.
+struct RayPlanData;
+struct RayPlan {
+  std::shared_ptr<RayPlanData> data;
+  float* partial = nullptr;
+};
+Status ray_plan_get(pact_ctx* cache_ctx, pact_ctx* ctx, RayArgs& a, const double* centers,
+                    int n_centers, RayPlan& out);
+void ray_plan_release(RayPlan& p, cudaStream_t s);
+// The standalone entry points' plan (one per context, rebuilt on a new geometry).
+Status ray_plan_cached(pact_ctx* ctx, RayArgs& a, const double* centers, int n_centers);
 Status launch_wavefront(pact_ctx* ctx, const RayArgs& a, float* w);
 Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, double* grad);
 

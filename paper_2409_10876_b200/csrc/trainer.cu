@@ -67,6 +67,7 @@ struct pact_trainer {
   SirenWork sw;
   FourierTable ftab;
   RayArgs ray{};
+  RayPlan ray_plan;
   int n_tv = 0;
   // device state
   void* arena = nullptr;
@@ -437,7 +438,8 @@ int pact_trainer_create_partitioned(pact_ctx* ctx, const pact_ring* ring,
   tr->ray.centers = tr->centers;
   tr->ray.n_rays = tr->n_local * tr->A;
   make_raster_texture(tr->dv, grid->width, grid->height, &tr->ray.tex);
-  trace.mark("uploads + texture");
+  TRY_ST(ray_plan_get(ctx, e, tr->ray, centers.data() + 2 * tr->p_lo, tr->n_local, tr->ray_plan));
+  trace.mark("uploads + texture + ray plan");
   // DAS stack + spectra, once (optimize.hpp:380-392)
   TRY_ST(das_stack_device(e, *ring, *meta, signals, *grid, v0, tr->delays.data(), tr->K,
                           tr->stack));
@@ -646,6 +648,7 @@ int pact_trainer_destroy(pact_trainer* tr) {
   if (tr->user) tr->user->launches.fetch_add(tr->eng.launches.exchange(0));
   if (tr->graph) cudaGraphExecDestroy(tr->graph);
   if (tr->ray.tex) cudaDestroyTextureObject(tr->ray.tex);
+  ray_plan_release(tr->ray_plan, tr->eng.stream);
   siren_work_free(tr->sw);
   fourier_table_free(tr->ftab);
   for (auto& sc : tr->eng.scratch) pool_free(sc.ptr, tr->eng.stream);
