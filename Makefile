@@ -14,9 +14,9 @@ CU_SRCS := $(wildcard $(PKG)/csrc/*.cu)
 CU_OBJS := $(patsubst $(PKG)/csrc/%.cu,build/obj/%.o,$(CU_SRCS))
 CU_HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/pact_cuda.h
 
-.PHONY: all lib oracle ref clean
+.PHONY: all lib oracle ref pactrec clean
 
-all: lib oracle ref
+all: lib oracle ref pactrec
 
 lib: $(LIBDIR)/libpact_cuda.so
 
@@ -27,6 +27,16 @@ build/obj/%.o: $(PKG)/csrc/%.cu $(CU_HDRS)
 $(LIBDIR)/libpact_cuda.so: $(CU_OBJS)
 	@mkdir -p $(LIBDIR)
 	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJS) -lcudart
+
+# pactrec: the reference's CLI driver over the drop-in headers (host C++)
+PACTREC := $(PKG)/bin/pactrec
+pactrec: $(PACTREC)
+
+$(PACTREC): $(PKG)/tools/pactrec.cpp $(PKG)/tools/cli_args.hpp $(PKG)/tools/json_lite.hpp \
+            $(wildcard $(PKG)/include/pact/*.hpp) include/pact_cuda.h $(LIBDIR)/libpact_cuda.so
+	@mkdir -p $(PKG)/bin
+	$(CXX) -std=c++17 -O2 -Wall -Wextra -pthread -Iinclude -I$(PKG)/include -I$(PKG)/tools -o $@ \
+	  $(PKG)/tools/pactrec.cpp -L$(LIBDIR) -lpact_cuda -Wl,-rpath,'$$ORIGIN/../lib'
 
 oracle:
 	$(MAKE) -C oracle oracle

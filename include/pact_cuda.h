@@ -168,6 +168,22 @@ int pact_simulate_signals(pact_ctx* ctx, const pact_grid* grid, const double* pr
                           const double* sos, const pact_mask* mask, double background_sos,
                           const pact_ring* ring, double pulse_sigma,
                           const pact_signal_meta* meta, double ray_step, float* out);
+/* simulate_signals with SimulateOptions::spreading (amplitude / sqrt(distance),
+ * phantom.hpp:351): spreading != 0 enables it; pact_simulate_signals is the
+ * spreading = 0 case. */
+int pact_simulate_signals_ex(pact_ctx* ctx, const pact_grid* grid, const double* pressure,
+                             const double* sos, const pact_mask* mask, double background_sos,
+                             const pact_ring* ring, double pulse_sigma,
+                             const pact_signal_meta* meta, double ray_step, int32_t spreading,
+                             float* out);
+/* The acquisition window of simulate_signals (phantom.hpp:284-334), host only:
+ * the same validation and messages, t0 = NaN / n_samples = 0 select the
+ * automatic window (floor(tau_min/dt) dt, ceil((tau_max - t0)/dt) + 1); fails
+ * with the reference's "time window too short" when an explicit window misses
+ * the arrivals.  out: {n_samples, dt, t0, background_sos}. */
+int pact_simulate_window(const pact_grid* grid, const double* pressure, const double* sos,
+                         double background_sos, const pact_ring* ring, double pulse_sigma,
+                         double dt, double t0, int32_t n_samples, pact_signal_meta* out);
 
 /* ---- patch layout (host) ---- */
 

@@ -20,6 +20,7 @@
 #include "pact/beamform.hpp"
 #include "pact/core.hpp"
 #include "pact/evaluate.hpp"
+#include "pact/io.hpp"
 #include "pact/deconv.hpp"
 #include "pact/nfield.hpp"
 #include "pact/optimize.hpp"
@@ -622,5 +623,128 @@ double ref_time_das_stack(int reps, int n_tx, double radius, double offset, int 
   }
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
 }
+
+// ---- §8(f)-3: file formats, phantoms, PSFs (the pactrec tool path) --------
+
+// pact::builtin_phantom_spec + generate_phantom (phantom.hpp:145-266) with the
+// spec mask replaced as pactrec does (pactrec.cpp:196-199).
+int ref_generate_phantom(const char* name, int W, int H, double pitch, double bg, double mcx,
+                         double mcy, double mr, uint64_t seed, double* pressure, double* sos) {
+  return guarded([&] {
+    pact::PhantomSpec spec = pact::builtin_phantom_spec(name, bg);
+    spec.mask = {{mcx, mcy}, mr};
+    auto ph = pact::generate_phantom(pact::GridSpec::centered(W, H, pitch), spec, seed);
+    std::memcpy(pressure, ph.pressure.values.data(), sizeof(double) * ph.pressure.values.size());
+    std::memcpy(sos, ph.sos.values.data(), sizeof(double) * ph.sos.values.size());
+  });
+}
+
+// io::read_pgrid (io.hpp:93-112); values may be NULL (header query) or hold cap doubles.
+int ref_read_pgrid(const char* path, int* W, int* H, double* geo /* pitch, ox, oy */,
+                   double* values, size_t cap) {
+  return guarded([&] {
+    auto g = pact::io::read_pgrid(path);
+    *W = g.width;
+    *H = g.height;
+    geo[0] = g.pitch;
+    geo[1] = g.origin.x;
+    geo[2] = g.origin.y;
+    if (values) std::memcpy(values, g.values.data(), sizeof(double) * std::min(cap, g.values.size()));
+  });
+}
+
+int ref_write_pgrid(const char* path, int W, int H, double pitch, double ox, double oy,
+                    const double* values) {
+  return guarded([&] { pact::io::write_pgrid(path, raster_of(grid_of(W, H, pitch, ox, oy), values)); });
+}
+
+// io::read_sigset (io.hpp:129-150): meta = {dt, t0, radius, angle_offset, background_sos}.
+int ref_read_sigset(const char* path, int* n_tx, int* T, double* meta, double* data, size_t cap) {
+  return guarded([&] {
+    auto s = pact::io::read_sigset(path);
+    *n_tx = s.geom.n_transducers;
+    *T = s.n_samples;
+    meta[0] = s.dt;
+    meta[1] = s.t0;
+    meta[2] = s.geom.radius;
+    meta[3] = s.geom.angle_offset;
+    meta[4] = s.background_sos;
+    if (data) std::memcpy(data, s.data.data(), sizeof(double) * std::min(cap, s.data.size()));
+  });
+}
+
+int ref_write_sigset(const char* path, int n_tx, int T, const double* meta, const double* data) {
+  return guarded([&] {
+    pact::SignalSet s;
+    s.geom = {n_tx, meta[2], meta[3]};
+    s.n_samples = T;
+    s.dt = meta[0];
+    s.t0 = meta[1];
+    s.background_sos = meta[4];
+    s.data.assign(data, data + static_cast<size_t>(n_tx) * T);
+    pact::io::write_sigset(path, s);
+  });
+}
+
+// load_sirn / write_sirn (nfield.hpp:235-289): shape = {in_dim, hidden, n_hidden_layers},
+// scal = {omega0, out_scale, v0}; theta may be NULL (header query).
+int ref_load_sirn(const char* path, int* shape, double* scal, double* theta, size_t cap) {
+  return guarded([&] {
+    auto p = pact::load_sirn(path);
+    shape[0] = p.in_dim;
+    shape[1] = p.hidden;
+    shape[2] = p.n_hidden_layers;
+    scal[0] = p.omega0;
+    scal[1] = p.out_scale;
+    scal[2] = p.v0;
+    if (theta) std::memcpy(theta, p.theta.data(), sizeof(double) * std::min(cap, p.theta.size()));
+  });
+}
+
+int ref_write_sirn(const char* path, int hidden, int layers, double omega0, double out_scale,
+                   double v0, const double* theta) {
+  return guarded([&] {
+    auto p = siren_of(hidden, layers, omega0, out_scale, v0, theta);
+    pact::write_sirn(path, p);
+  });
+}
+
+// psf_from_transfer (aberration.hpp:407-445): spectrum as interleaved re, im.
+int ref_psf_from_transfer(int P, double pitch, const double* spectrum, double* psf) {
+  return guarded([&] {
+    std::vector<std::complex<double>> sp(static_cast<size_t>(P) * P);
+    for (size_t i = 0; i < sp.size(); ++i) sp[i] = {spectrum[2 * i], spectrum[2 * i + 1]};
+    auto r = pact::psf_from_transfer(sp, P, pitch);
+    std::memcpy(psf, r.values.data(), sizeof(double) * r.values.size());
+  });
+}
+
+// simulate_signals (phantom.hpp:282-362) with the automatic window and
+// SimulateOptions::spreading, as `pactrec simulate` calls it.  meta = {t0, T}
+// out; out may be NULL (window query) or hold cap doubles.
+int ref_simulate_auto(int W, int H, double pitch, double ox, double oy, const double* pressure,
+                      const double* sos, double mcx, double mcy, double mr, double background_sos,
+                      int n_tx, double radius, double offset, double pulse_sigma, double dt,
+                      int spreading, double ray_step, double* meta, double* out, size_t cap) {
+  return guarded([&] {
+    auto g = grid_of(W, H, pitch, ox, oy);
+    pact::Phantom ph;
+    ph.pressure = raster_of(g, pressure);
+    ph.sos = raster_of(g, sos);
+    ph.mask = {{mcx, mcy}, mr};
+    ph.background_sos = background_sos;
+    pact::SimulateOptions opt;
+    opt.pulse_sigma = pulse_sigma;
+    opt.dt = dt;
+    opt.spreading = spreading != 0;
+    opt.ray_step = ray_step;
+    auto s = pact::simulate_signals(ph, {n_tx, radius, offset}, opt);
+    meta[0] = s.t0;
+    meta[1] = s.n_samples;
+    if (out) std::memcpy(out, s.data.data(), sizeof(double) * std::min(cap, s.data.size()));
+  });
+}
+
+double ref_water_sos(double t) { return pact::water_sos(t); }
 
 }  // extern "C"

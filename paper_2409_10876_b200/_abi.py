@@ -125,6 +125,11 @@ SIGNATURES = {
                                     C.POINTER(Grid), _D, C.POINTER(Body), _P]),
     "pact_simulate_signals": (C.c_int, [_P, C.POINTER(Grid), _DP, _DP, C.POINTER(Mask), _D,
                                         C.POINTER(Ring), _D, C.POINTER(SignalMeta), _D, _P]),
+    "pact_simulate_signals_ex": (C.c_int, [_P, C.POINTER(Grid), _DP, _DP, C.POINTER(Mask), _D,
+                                           C.POINTER(Ring), _D, C.POINTER(SignalMeta), _D,
+                                           C.c_int32, _P]),
+    "pact_simulate_window": (C.c_int, [C.POINTER(Grid), _DP, _DP, _D, C.POINTER(Ring), _D, _D, _D,
+                                       C.c_int32, C.POINTER(SignalMeta)]),
     "pact_make_patch_layout": (C.c_int, [C.POINTER(Grid), _D, _D, C.POINTER(Layout)]),
     "pact_layout_n_patches": (C.c_int32, [C.POINTER(Layout)]),
     "pact_layout_patches": (C.c_int, [C.POINTER(Layout), _IP, _DP]),

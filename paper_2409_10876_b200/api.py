@@ -365,17 +365,20 @@ def _ctx_methods():
 
     def simulate_signals(self, grid: GridSpec, pressure, sos, mask: CircularMask,
                          background_sos: float, ring: RingGeometry, meta: SignalMetaInfo,
-                         pulse_sigma: float = 100e-9, ray_step: float = 0.05) -> torch.Tensor:
-        """simulate_signals, phantom.hpp:282-362 -> fp32 [N, T] on the device."""
+                         pulse_sigma: float = 100e-9, ray_step: float = 0.05,
+                         spreading: bool = False) -> torch.Tensor:
+        """simulate_signals, phantom.hpp:282-362 -> fp32 [N, T] on the device
+        (`spreading`: SimulateOptions::spreading, amplitude / sqrt(distance))."""
         pr = np.ascontiguousarray(pressure, np.float64)
         so = np.ascontiguousarray(sos, np.float64)
         out = torch.empty((ring.n_transducers, meta.n_samples), device="cuda", dtype=torch.float32)
         g, m, r, mt = grid.c(), mask.c(), ring.c(), meta.c()
-        check(_abi.lib().pact_simulate_signals(self._h, C.byref(g),
-                                               pr.ctypes.data_as(C.POINTER(C.c_double)),
-                                               so.ctypes.data_as(C.POINTER(C.c_double)),
-                                               C.byref(m), background_sos, C.byref(r), pulse_sigma,
-                                               C.byref(mt), ray_step, dptr(out)))
+        check(_abi.lib().pact_simulate_signals_ex(self._h, C.byref(g),
+                                                  pr.ctypes.data_as(C.POINTER(C.c_double)),
+                                                  so.ctypes.data_as(C.POINTER(C.c_double)),
+                                                  C.byref(m), background_sos, C.byref(r),
+                                                  pulse_sigma, C.byref(mt), ray_step,
+                                                  1 if spreading else 0, dptr(out)))
         return out
 
     for f in (simulate_signals, render_sos, siren_backward, wavefront, transfer_stack, patch_spectra,
@@ -384,6 +387,21 @@ def _ctx_methods():
 
 
 _ctx_methods()
+
+
+def simulate_window(grid: GridSpec, pressure, sos, background_sos: float, ring: RingGeometry,
+                    pulse_sigma: float = 100e-9, dt: float = 25e-9, t0: float = float("nan"),
+                    n_samples: int = 0) -> SignalMetaInfo:
+    """The acquisition window of simulate_signals (phantom.hpp:284-334), host only:
+    t0 = NaN / n_samples = 0 select the automatic window."""
+    pr = np.ascontiguousarray(pressure, np.float64)
+    so = np.ascontiguousarray(sos, np.float64)
+    g, r, out = grid.c(), ring.c(), _abi.SignalMeta()
+    check(_abi.lib().pact_simulate_window(C.byref(g), pr.ctypes.data_as(C.POINTER(C.c_double)),
+                                          so.ctypes.data_as(C.POINTER(C.c_double)),
+                                          background_sos, C.byref(r), pulse_sigma, dt, t0,
+                                          n_samples, C.byref(out)))
+    return SignalMetaInfo(out.n_samples, out.dt, out.t0, out.background_sos)
 
 
 # --------------------------------------------------------------------------- #

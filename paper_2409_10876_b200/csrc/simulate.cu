@@ -31,6 +31,7 @@ struct SimArgs {
   double dt, t0, sigma;
   double v0;
   bool uniform;
+  bool spreading;  // amplitude / sqrt(distance) (SimulateOptions::spreading)
   const float* dv;  // SOS deviation raster v - v0
   int W, H;
   double ox, oy, inv_pitch;
@@ -83,7 +84,9 @@ __global__ void simulate_kernel(SimArgs a) {
   }
   // pulse, phantom.hpp:347-360
   const double support = 6.0 * a.sigma;
-  const double scale = 2.0 * a.amp[s] / a.sigma;
+  double amp = a.amp[s];
+  if (a.spreading) amp /= sqrt(fmax(dist, 1e-6));
+  const double scale = 2.0 * amp / a.sigma;
   int i0 = static_cast<int>(ceil((tau - support - a.t0) / a.dt));
   int i1 = static_cast<int>(floor((tau + support - a.t0) / a.dt));
   i0 = i0 < 0 ? 0 : i0;
@@ -105,34 +108,38 @@ __global__ void to_f32_kernel(const double* __restrict__ in, size_t n, float* __
 
 using namespace pactgpu;
 
-extern "C" int pact_simulate_signals(pact_ctx* ctx, const pact_grid* grid, const double* pressure,
-                                     const double* sos, const pact_mask* mask,
-                                     double background_sos, const pact_ring* ring,
-                                     double pulse_sigma, const pact_signal_meta* meta,
-                                     double ray_step, float* out) {
-  if (!ctx || !grid || !pressure || !sos || !mask || !ring || !meta || !out)
-    return validation("pact_simulate_signals: null argument").code;
-  // validation order of simulate_signals, phantom.hpp:284-334
-  if (ring->n_transducers < 3) return validation("ring: need at least 3 transducers").code;
-  if (!(ring->radius > 0.0)) return validation("ring: radius must be > 0").code;
-  if (!(pulse_sigma > 0.0)) return validation("simulate: pulse_sigma must be > 0").code;
-  if (!(meta->dt > 0.0)) return validation("simulate: dt must be > 0").code;
-  if (meta->n_samples < 1) return validation("simulate: n_samples must be >= 1").code;
-  const int W = grid->width, H = grid->height;
+namespace pactgpu {
+
+// The host scan of simulate_signals (phantom.hpp:284-334): validation in the
+// reference's order, the pressure-bearing sources, the SOS range and the
+// conservative arrival window [tau_min, tau_max].
+struct SimScan {
   std::vector<double2> src;
   std::vector<double> amp;
+  bool uniform = false;
+  double tau_min = 0.0, tau_max = 0.0;
+};
+
+Status sim_scan(const pact_grid& grid, const double* pressure, const double* sos,
+                double background_sos, const pact_ring& ring, double pulse_sigma, double dt,
+                SimScan& o) {
+  if (ring.n_transducers < 3) return validation("ring: need at least 3 transducers");
+  if (!(ring.radius > 0.0)) return validation("ring: radius must be > 0");
+  if (!(pulse_sigma > 0.0)) return validation("simulate: pulse_sigma must be > 0");
+  if (!(dt > 0.0)) return validation("simulate: dt must be > 0");
+  const int W = grid.width, H = grid.height;
   double max_r = 0.0;
   for (int iy = 0; iy < H; ++iy)
     for (int ix = 0; ix < W; ++ix) {
-      double a = pressure[static_cast<size_t>(iy) * W + ix];
+      const double a = pressure[static_cast<size_t>(iy) * W + ix];
       if (a == 0.0) continue;
-      double px = grid->origin_x + ix * grid->pitch, py = grid->origin_y + iy * grid->pitch;
-      double r = std::hypot(px, py);
-      if (r >= ring->radius)
-        return validation("simulate: pressure-bearing pixel outside the transducer ring").code;
+      const double px = grid.origin_x + ix * grid.pitch, py = grid.origin_y + iy * grid.pitch;
+      const double r = std::hypot(px, py);
+      if (r >= ring.radius)
+        return validation("simulate: pressure-bearing pixel outside the transducer ring");
       max_r = std::max(max_r, r);
-      src.push_back(make_double2(px, py));
-      amp.push_back(a);
+      o.src.push_back(make_double2(px, py));
+      o.amp.push_back(a);
     }
   const size_t npx = static_cast<size_t>(W) * H;
   double vmin = npx ? sos[0] : background_sos, vmax = vmin;
@@ -140,17 +147,78 @@ extern "C" int pact_simulate_signals(pact_ctx* ctx, const pact_grid* grid, const
     vmin = std::min(vmin, sos[i]);
     vmax = std::max(vmax, sos[i]);
   }
-  if (!(vmin > 0.0)) return validation("simulate: non-positive SOS value").code;
-  const bool uniform = (vmin == vmax && vmin == background_sos);
-  const double tau_min = 1e-3 * (ring->radius - max_r) / vmax - 8.0 * pulse_sigma;
-  const double tau_max = 1e-3 * (ring->radius + max_r) / vmin + 8.0 * pulse_sigma;
-  if (!src.empty() &&
-      (meta->t0 > tau_min || meta->t0 + (meta->n_samples - 1) * meta->dt < tau_max)) {
-    std::string m = "simulate: time window too short, need [" + std::to_string(tau_min) + ", " +
-                    std::to_string(tau_max) + "] s";
+  if (!(vmin > 0.0)) return validation("simulate: non-positive SOS value");
+  o.uniform = (vmin == vmax && vmin == background_sos);
+  o.tau_min = 1e-3 * (ring.radius - max_r) / vmax - 8.0 * pulse_sigma;
+  o.tau_max = 1e-3 * (ring.radius + max_r) / vmin + 8.0 * pulse_sigma;
+  return {};
+}
+
+Status sim_check_window(const SimScan& sc, double t0, int n_samples, double dt) {
+  if (!sc.src.empty() && (t0 > sc.tau_min || t0 + (n_samples - 1) * dt < sc.tau_max)) {
+    std::string m = "simulate: time window too short, need [" + std::to_string(sc.tau_min) +
+                    ", " + std::to_string(sc.tau_max) + "] s";
     set_error("%s", m.c_str());
-    return PACT_E_VALIDATION;
+    return {PACT_E_VALIDATION};
   }
+  return {};
+}
+
+}  // namespace pactgpu
+
+extern "C" int pact_simulate_window(const pact_grid* grid, const double* pressure,
+                                    const double* sos, double background_sos,
+                                    const pact_ring* ring, double pulse_sigma, double dt,
+                                    double t0, int32_t n_samples, pact_signal_meta* out) {
+  using namespace pactgpu;
+  if (!grid || !pressure || !sos || !ring || !out)
+    return validation("pact_simulate_window: null argument").code;
+  SimScan sc;
+  PACT_TRY(sim_scan(*grid, pressure, sos, background_sos, *ring, pulse_sigma, dt, sc));
+  pact_signal_meta m{};
+  m.dt = dt;
+  m.background_sos = background_sos;
+  // phantom.hpp:320-331: NaN t0 / n_samples 0 -> the auto window
+  m.t0 = std::isnan(t0) ? std::floor(sc.tau_min / dt) * dt : t0;
+  m.n_samples = n_samples > 0 ? n_samples
+                              : static_cast<int>(std::ceil((sc.tau_max - m.t0) / dt)) + 1;
+  PACT_TRY(sim_check_window(sc, m.t0, m.n_samples, dt));
+  *out = m;
+  return PACT_OK;
+}
+
+extern "C" int pact_simulate_signals(pact_ctx* ctx, const pact_grid* grid, const double* pressure,
+                                     const double* sos, const pact_mask* mask,
+                                     double background_sos, const pact_ring* ring,
+                                     double pulse_sigma, const pact_signal_meta* meta,
+                                     double ray_step, float* out) {
+  return pact_simulate_signals_ex(ctx, grid, pressure, sos, mask, background_sos, ring,
+                                  pulse_sigma, meta, ray_step, 0, out);
+}
+
+extern "C" int pact_simulate_signals_ex(pact_ctx* ctx, const pact_grid* grid,
+                                        const double* pressure, const double* sos,
+                                        const pact_mask* mask, double background_sos,
+                                        const pact_ring* ring, double pulse_sigma,
+                                        const pact_signal_meta* meta, double ray_step,
+                                        int32_t spreading, float* out) {
+  using namespace pactgpu;
+  if (!ctx || !grid || !pressure || !sos || !mask || !ring || !meta || !out)
+    return validation("pact_simulate_signals: null argument").code;
+  if (meta->n_samples < 1) {
+    // the reference's checks before the window come first
+    SimScan sc;
+    PACT_TRY(sim_scan(*grid, pressure, sos, background_sos, *ring, pulse_sigma, meta->dt, sc));
+    return validation("simulate: n_samples must be >= 1").code;
+  }
+  SimScan sc;
+  PACT_TRY(sim_scan(*grid, pressure, sos, background_sos, *ring, pulse_sigma, meta->dt, sc));
+  PACT_TRY(sim_check_window(sc, meta->t0, meta->n_samples, meta->dt));
+  const int W = grid->width, H = grid->height;
+  const size_t npx = static_cast<size_t>(W) * H;
+  const std::vector<double2>& src = sc.src;
+  const std::vector<double>& amp = sc.amp;
+  const bool uniform = sc.uniform;
   const int N = ring->n_transducers, T = meta->n_samples;
   std::vector<float> dvh(npx);
   for (size_t i = 0; i < npx; ++i) dvh[i] = static_cast<float>(sos[i] - background_sos);
@@ -185,6 +253,7 @@ extern "C" int pact_simulate_signals(pact_ctx* ctx, const pact_grid* grid, const
   a.sigma = pulse_sigma;
   a.v0 = background_sos;
   a.uniform = uniform;
+  a.spreading = spreading != 0;
   a.W = W;
   a.H = H;
   a.ox = grid->origin_x;

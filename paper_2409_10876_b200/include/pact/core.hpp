@@ -120,6 +120,17 @@ struct CircularMask {
   pact_mask c() const { return {center.x, center.y, radius}; }
 };
 
+/// water_sos (core.hpp:208-218): fifth-order polynomial in temperature (deg C).
+inline double water_sos(double temperature_celsius) {
+  const double t = temperature_celsius;
+  if (!(t >= 0.0 && t <= 95.0))
+    throw ValidationError("water_sos: temperature " + std::to_string(t) +
+                          " outside valid range [0, 95] C");
+  static constexpr double c[6] = {1.402385e3, 5.038813, -5.799136e-2, 3.287156e-4, -1.398845e-6,
+                                  2.787860e-9};
+  return c[0] + t * (c[1] + t * (c[2] + t * (c[3] + t * (c[4] + t * c[5]))));
+}
+
 struct PatchLayout {
   GridSpec grid;
   double patch_mm = 0.0, overlap = 0.0;

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "pact/core.hpp"
+#include "pact/io.hpp"
 
 namespace pact {
 
@@ -19,6 +20,23 @@ struct SirenParams {
   std::vector<double> theta;  // per layer: W row-major [rows][cols], then b
 
   int n_layers() const { return n_hidden_layers + 1; }
+  /// (rows, cols) of layer l's weight matrix; the bias has `rows` entries.
+  std::pair<int, int> layer_shape(int l) const {
+    return {l == n_hidden_layers ? 1 : hidden, l == 0 ? in_dim : hidden};
+  }
+  size_t layer_offset(int l) const {
+    size_t off = 0;
+    for (int k = 0; k < l; ++k) {
+      const auto [r, c] = layer_shape(k);
+      off += static_cast<size_t>(r) * (c + 1);
+    }
+    return off;
+  }
+  const double* weights(int l) const { return theta.data() + layer_offset(l); }
+  const double* bias(int l) const {
+    const auto [r, c] = layer_shape(l);
+    return theta.data() + layer_offset(l) + static_cast<size_t>(r) * c;
+  }
   pact_siren c() const { return {in_dim, hidden, n_hidden_layers, omega0, out_scale, v0}; }
   size_t param_count() const {
     pact_siren s = c();
@@ -100,6 +118,57 @@ inline std::vector<double> backprop_sos(const SirenParams& p, const SosField& fi
   std::vector<double> grad(p.theta.size());
   out.download(grad.data());
   return grad;
+}
+
+// ---- SIRN checkpoints (nfield.hpp:235-289) ---------------------------------
+// "SIRN", u32 n_layers, per layer u32 rows and u32 cols, f64 omega0,
+// f64 out_scale, f64 v0, then the parameters as f32 in layer order (weights
+// row-major, then bias).
+
+inline void write_sirn(const std::string& path, const SirenParams& p) {
+  io::detail::Encoder e;
+  e.raw("SIRN", 4);
+  e.put<uint32_t>(static_cast<uint32_t>(p.n_layers()));
+  for (int l = 0; l < p.n_layers(); ++l) {
+    const auto [r, c] = p.layer_shape(l);
+    e.put<uint32_t>(static_cast<uint32_t>(r));
+    e.put<uint32_t>(static_cast<uint32_t>(c));
+  }
+  e.put<double>(p.omega0);
+  e.put<double>(p.out_scale);
+  e.put<double>(p.v0);
+  e.put_f32_array(p.theta);
+  e.save(path);
+}
+
+inline SirenParams load_sirn(const std::string& path) {
+  io::detail::Decoder d(path);
+  d.magic("SIRN");
+  const uint32_t n_layers = d.get<uint32_t>("n_layers");
+  if (n_layers < 2 || n_layers > 64) throw ValidationError("SIRN: implausible layer count");
+  std::vector<std::pair<uint32_t, uint32_t>> shape(n_layers);
+  for (auto& sh : shape) {
+    sh.first = d.get<uint32_t>("rows");
+    sh.second = d.get<uint32_t>("cols");
+  }
+  SirenParams p;
+  p.in_dim = static_cast<int>(shape.front().second);
+  p.hidden = static_cast<int>(shape.front().first);
+  p.n_hidden_layers = static_cast<int>(n_layers) - 1;
+  const uint32_t h = static_cast<uint32_t>(p.hidden);
+  for (uint32_t l = 1; l + 1 < n_layers; ++l)
+    if (shape[l].first != h || shape[l].second != h)
+      throw ValidationError("SIRN: inconsistent hidden layer shapes in " + path);
+  if (shape.back().first != 1 || shape.back().second != h)
+    throw ValidationError("SIRN: bad output layer shape in " + path);
+  p.omega0 = d.get<double>("omega0");
+  p.out_scale = d.get<double>("out_scale");
+  p.v0 = d.get<double>("v0");
+  if (!(p.omega0 > 0.0) || !std::isfinite(p.out_scale) || !(p.v0 > 0.0))
+    throw ValidationError("SIRN: bad scalar fields in " + path);
+  p.theta = d.f32_array(p.layer_offset(p.n_layers()), "theta",
+                        "SIRN: non-finite parameter in " + path);
+  return p;
 }
 
 }  // namespace pact
