@@ -35,6 +35,7 @@ import numpy as np  # noqa: E402
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 N_FRAMES = 8
 E2E_ITERS = 10
+E2E_REPS = 3  # timed joint_reconstruct_batch calls (after one untimed call)
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # FFMA pipe at max clock
 
 
@@ -101,7 +102,7 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-STAGE_KERNEL = {"ray_backward": "ray_backward_split_kernel", "wavefront": "wavefront_split_kernel",
+STAGE_KERNEL = {"ray_backward": "ray_backward_plan_kernel", "wavefront": "wavefront_plan_kernel",
                 "fused_loss": "loss_bins_kernel"}
 
 
@@ -343,24 +344,29 @@ def run_ours(args):
     dsig = {f: torch.empty_like(signals[f]) for f in my_frames}
     e2e_cfgs = [wl.train_config(w, epochs=E2E_ITERS, steps_per_epoch=1, seed=f) for f in my_frames]
     del signals
+    def e2e_call():
+        for f in my_frames:
+            dsig[f].copy_(hin[f], non_blocking=True)
+        _, imgs, soss, _ = joint_reconstruct_batch(ctx, [dsig[f] for f in my_frames], w.ring,
+                                                   w.meta, w.grid, w.mask, e2e_cfgs)
+        for i, f in enumerate(my_frames):
+            hout[f][0].copy_(imgs[i], non_blocking=True)
+            hout[f][1].copy_(soss[i], non_blocking=True)
+
+    e2e_call()  # untimed: first-call costs (cuFFT plans, pool growth, module load)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for f in my_frames:
-        dsig[f].copy_(hin[f], non_blocking=True)
-    _, imgs, soss, _ = joint_reconstruct_batch(ctx, [dsig[f] for f in my_frames], w.ring, w.meta,
-                                               w.grid, w.mask, e2e_cfgs)
-    for i, f in enumerate(my_frames):
-        hout[f][0].copy_(imgs[i], non_blocking=True)
-        hout[f][1].copy_(soss[i], non_blocking=True)
+    for _ in range(E2E_REPS):
+        e2e_call()
     b.record()
     torch.cuda.synchronize()
     e2e_t = torch.tensor([a.elapsed_time(b)], device="cuda", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = N_FRAMES * E2E_ITERS / (float(e2e_t.item()) * 1e-3)
+    e2e_value = N_FRAMES * E2E_ITERS * E2E_REPS / (float(e2e_t.item()) * 1e-3)
 
     # ---- per-stage roofline of one frame-iteration ----
     siren_ms = stages["siren_fwd"] + stages["siren_bwd"]
@@ -440,7 +446,8 @@ def run_ours(args):
                     "d2h_bytes_per_step": nbytes_out * N_FRAMES // world,
                     "what": f"all frames of the rank: pinned H2D signals, pact_joint_reconstruct_batch "
                             f"({E2E_ITERS} iterations per frame incl. DAS, spectra, final "
-                            f"deconvolution; frames concurrent), D2H image+SOS"},
+                            f"deconvolution; frames concurrent), D2H image+SOS; {E2E_REPS} timed "
+                            f"calls after one untimed call (bytes are per call)"},
             "gpu_launches": launches,
             "roofline": roofline,
             "iteration_roofline": iteration_roofline,

@@ -252,11 +252,26 @@ int pact_train_config_default(pact_train_config* c) {
   return PACT_OK;
 }
 
+// sync_end: wait for the one-time device work (DAS, spectra) before returning,
+// so the caller may release `signals` (the public entry points); the batch
+// entry point keeps the signals alive and lets the frames' setup overlap.
+static int trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_meta* meta,
+                          const float* signals, const pact_grid* grid, const pact_mask* mask,
+                          const pact_train_config* cfg, const pact_partition* part,
+                          pact_trainer** out, bool sync_end);
+
 int pact_trainer_create_partitioned(pact_ctx* ctx, const pact_ring* ring,
                                     const pact_signal_meta* meta, const float* signals,
                                     const pact_grid* grid, const pact_mask* mask,
                                     const pact_train_config* cfg, const pact_partition* part,
                                     pact_trainer** out) {
+  return trainer_create(ctx, ring, meta, signals, grid, mask, cfg, part, out, true);
+}
+
+static int trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signal_meta* meta,
+                          const float* signals, const pact_grid* grid, const pact_mask* mask,
+                          const pact_train_config* cfg, const pact_partition* part,
+                          pact_trainer** out, bool sync_end) {
   if (!ctx || !ring || !meta || !signals || !grid || !mask || !cfg || !out || !part)
     return validation("pact_trainer_create: null argument").code;
   if (part->world < 1 || part->rank < 0 || part->rank >= part->world)
@@ -440,16 +455,18 @@ int pact_trainer_create_partitioned(pact_ctx* ctx, const pact_ring* ring,
   make_raster_texture(tr->dv, grid->width, grid->height, &tr->ray.tex);
   TRY_ST(ray_plan_get(ctx, e, tr->ray, centers.data() + 2 * tr->p_lo, tr->n_local, tr->ray_plan));
   trace.mark("uploads + texture + ray plan");
+  // pageable uploads first: a pageable cudaMemcpyAsync waits for the stream,
+  // which is still idle here (after the DAS launch it would wait for the DAS)
+  TRY_ST(siren_work_alloc(tr->sw, tr->mp, tr->shape, s));
+  trace.mark("siren work");
+  TRY_ST(fourier_table(e, tr->ftab, tr->P, grid->pitch, tr->A, tr->delays.data(), tr->K));
+  trace.mark("fourier table");
   // DAS stack + spectra, once (optimize.hpp:380-392)
   TRY_ST(das_stack_device(e, *ring, *meta, signals, *grid, v0, tr->delays.data(), tr->K,
                           tr->stack));
   TRY_ST(launch_patch_fft(e, tr->lay, tr->stack, tr->K, tr->Y, tr->p_lo, tr->p_hi));
   trace.mark("DAS + FFT launched");
-  TRY_ST(siren_work_alloc(tr->sw, tr->mp, tr->shape, s));
-  trace.mark("siren work");
-  TRY_ST(fourier_table(e, tr->ftab, tr->P, grid->pitch, tr->A, tr->delays.data(), tr->K));
-  trace.mark("fourier table");
-  TRY_CU(cudaStreamSynchronize(s));
+  if (sync_end) TRY_CU(cudaStreamSynchronize(s));
   trace.mark("final sync");
   *out = tr;
   return PACT_OK;
@@ -710,7 +727,9 @@ int pact_joint_reconstruct_batch(pact_ctx* ctx, int32_t n_frames, const pact_rin
   for (int f = 0; f < n_frames; ++f) {
     if (cfgs[f].epochs != epochs)
       return cleanup(validation("pact_joint_reconstruct_batch: frames need equal epochs").code);
-    int rc = pact_trainer_create(ctx, ring, meta, signals[f], grid, mask, &cfgs[f], &trs[f]);
+    const pact_partition whole{0, 1};
+    int rc = trainer_create(ctx, ring, meta, signals[f], grid, mask, &cfgs[f], &whole, &trs[f],
+                            false);
     if (rc) return cleanup(rc);
   }
   int n_params = 0;

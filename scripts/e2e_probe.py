@@ -26,3 +26,14 @@ for rep in range(3):
     joint_reconstruct(ctx, sig, w.ring, w.meta, w.grid, w.mask, wl.train_config(w, epochs=10, steps_per_epoch=1))
     torch.cuda.synchronize()
     print(f"joint_reconstruct {1e3*(time.perf_counter()-t0):.1f} ms")
+
+# the bench's e2e call: 8 frames through joint_reconstruct_batch (traced)
+from paper_2409_10876_b200.api import joint_reconstruct_batch  # noqa: E402
+sigs = [wl.simulate(ctx, w, seed=f) for f in range(8)]
+cfgs = [wl.train_config(w, epochs=10, steps_per_epoch=1, seed=f) for f in range(8)]
+for rep in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    joint_reconstruct_batch(ctx, sigs, w.ring, w.meta, w.grid, w.mask, cfgs)
+    torch.cuda.synchronize()
+    print(f"batch of 8: {1e3*(time.perf_counter()-t0):.1f} ms")
