@@ -515,13 +515,28 @@ __global__ void siren_wgrad0_kernel(const float* __restrict__ dA0, const float2*
 }
 
 // grad[off + p] = sum_chunk partial[chunk][p]   (fixed order, fp64)
-// Block (32 params) x (32 chunk lanes); lane y sums chunks y, y+32, ... with
-// four independent accumulators, then a fixed-order fold over the lanes.
-__global__ void __launch_bounds__(1024)
-reduce_partials_kernel(const float* __restrict__ partial, int n_chunks, int per_chunk,
-                       double* __restrict__ grad) {
+// All of one backward pass's partial-sum reductions in one launch: segment
+// s sums partial rows [n_chunks][per] of src into dst.  A block is
+// (32 params) x (32 chunk lanes); lane y sums chunks y, y+32, ... with four
+// independent accumulators, then a fixed-order fold over the lanes
+// (deterministic).  Block b belongs to the segment whose cumulative block
+// range holds b.
+constexpr int kMaxSeg = 8;
+struct ReduceSegs {
+  const float* src[kMaxSeg];
+  double* dst[kMaxSeg];
+  int n_chunks[kMaxSeg], per[kMaxSeg], block_end[kMaxSeg];
+  int n;
+};
+
+__global__ void __launch_bounds__(1024) reduce_segments_kernel(ReduceSegs sg) {
   __shared__ double s_sum[32][33];
-  const int p = blockIdx.x * 32 + threadIdx.x;
+  int seg = 0;
+  while (seg + 1 < sg.n && blockIdx.x >= static_cast<unsigned>(sg.block_end[seg])) ++seg;
+  const int b = blockIdx.x - (seg ? sg.block_end[seg - 1] : 0);
+  const float* __restrict__ partial = sg.src[seg];
+  const int per_chunk = sg.per[seg], n_chunks = sg.n_chunks[seg];
+  const int p = b * 32 + threadIdx.x;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   if (p < per_chunk) {
     int c = threadIdx.y;
@@ -538,7 +553,7 @@ reduce_partials_kernel(const float* __restrict__ partial, int n_chunks, int per_
   if (threadIdx.y == 0 && p < per_chunk) {
     double t = 0.0;
     for (int y = 0; y < 32; ++y) t += s_sum[y][threadIdx.x];
-    grad[p] = t;
+    sg.dst[seg][p] = t;
   }
 }
 
@@ -773,36 +788,50 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
   int rows_w = chunk_rows(n, tilesW, ctx->num_sms);
   if (use_tc) rows_w = tc_wgrad_rows(ctx, n);
   const int n_w = div_up(n, rows_w);
-  size_t need = std::max(static_cast<size_t>(n_top) * (H + 1),
-                         static_cast<size_t>(n_w) * (static_cast<size_t>(H) * H + H));
-  need = std::max(need, static_cast<size_t>(n_top) * 3 * H);
-  PACT_TRY_S(ensure_partial(w, need, st));
+  // one partial slice per reduction (top, each hidden layer, layer 0), summed
+  // by a single segmented launch at the end
+  // (slices start on 256-B boundaries: the weight-gradient kernels store vectors)
+  auto al64 = [](size_t x) { return (x + 63) & ~size_t(63); };
+  const size_t per_w = static_cast<size_t>(H) * H + H;
+  const size_t sz_top = al64(static_cast<size_t>(n_top) * (H + 1)),
+               sz_w = al64(static_cast<size_t>(n_w) * per_w), sz_0 = static_cast<size_t>(n_top) * 3 * H;
+  PACT_TRY_S(ensure_partial(w, sz_top + (L - 1) * sz_w + sz_0, st));
+  float* part_top = w.partial;
+  float* part_w = part_top + sz_top;  // layer l at part_w + (l - 1) sz_w
+  float* part_0 = part_w + (L - 1) * sz_w;
+  if (L + 1 > kMaxSeg) return validation("siren: too many layers for the segmented reduction");
+  ReduceSegs segs{};
+  auto add_seg = [&](const float* src, int chunks, int per, double* dst) {
+    const int k = segs.n++;
+    segs.src[k] = src;
+    segs.dst[k] = dst;
+    segs.n_chunks[k] = chunks;
+    segs.per[k] = per;
+    segs.block_end[k] = (k ? segs.block_end[k - 1] : 0) + div_up(per, 32);
+  };
 
   float* cur = w.dA;   // dA_l
   float* nxt = w.dB;   // dA_{l-1}
   // output layer
   const float* wL = theta + s.offset(L);
   siren_top_kernel<<<n_top, NT, 0, st>>>(w.acts + (L - 1) * stride, wL, gv, gmask, w.idx, n, H,
-                                         rows_top, w0, osc, cur, w.partial);
+                                         rows_top, w0, osc, cur, part_top);
   PACT_TRY_S(after_launch(ctx, "siren_top_kernel"));
-  reduce_partials_kernel<<<div_up(H + 1, 32), dim3(32, 32), 0, st>>>(w.partial, n_top, H + 1,
-                                                             grad + s.offset(L));
-  PACT_TRY_S(after_launch(ctx, "reduce_partials_kernel"));
+  add_seg(part_top, n_top, H + 1, grad + s.offset(L));
   for (int l = L - 1; l >= 1; --l) {
     const float* W = theta + s.offset(l);
     const float* Aprev = w.acts + (l - 1) * stride;
+    float* part = part_w + (l - 1) * sz_w;
     // weight gradient of layer l
     if (use_tc)
-      PACT_TRY_S(tc_wgrad_layer(ctx, H, cur, Aprev, n, rows_w, w0, w.partial, n_w));
+      PACT_TRY_S(tc_wgrad_layer(ctx, H, cur, Aprev, n, rows_w, w0, part, n_w));
     else if (H == 64)
-      siren_wgrad_kernel<64><<<dim3(n_w, 1, 1), NT, 0, st>>>(cur, Aprev, n, H, rows_w, w0, w.partial);
+      siren_wgrad_kernel<64><<<dim3(n_w, 1, 1), NT, 0, st>>>(cur, Aprev, n, H, rows_w, w0, part);
     else
       siren_wgrad_kernel<128><<<dim3(n_w, H / 128, H / 128), NT, 0, st>>>(cur, Aprev, n, H, rows_w,
-                                                                         w0, w.partial);
+                                                                         w0, part);
     if (!use_tc) PACT_TRY_S(after_launch(ctx, "siren_wgrad_kernel"));
-    int per = H * H + H;
-    reduce_partials_kernel<<<div_up(per, 32), dim3(32, 32), 0, st>>>(w.partial, n_w, per, grad + s.offset(l));
-    PACT_TRY_S(after_launch(ctx, "reduce_partials_kernel"));
+    add_seg(part, n_w, static_cast<int>(per_w), grad + s.offset(l));
     // delta to layer l-1
     if (use_tc)
       PACT_TRY_S(tc_dgrad_layer(ctx, H, cur, W, Aprev, n, w0, nxt));
@@ -814,11 +843,11 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
     if (!use_tc) PACT_TRY_S(after_launch(ctx, "siren_dgrad_kernel"));
     std::swap(cur, nxt);
   }
-  siren_wgrad0_kernel<<<n_top, NT, 0, st>>>(cur, w.coords, n, H, rows_top, w.partial);
+  siren_wgrad0_kernel<<<n_top, NT, 0, st>>>(cur, w.coords, n, H, rows_top, part_0);
   PACT_TRY_S(after_launch(ctx, "siren_wgrad0_kernel"));
-  reduce_partials_kernel<<<div_up(3 * H, 32), dim3(32, 32), 0, st>>>(w.partial, n_top, 3 * H,
-                                                             grad + s.offset(0));
-  return after_launch(ctx, "reduce_partials_kernel");
+  add_seg(part_0, n_top, 3 * H, grad + s.offset(0));
+  reduce_segments_kernel<<<segs.block_end[segs.n - 1], dim3(32, 32), 0, st>>>(segs);
+  return after_launch(ctx, "reduce_segments_kernel");
 }
 
 }  // namespace pactgpu
