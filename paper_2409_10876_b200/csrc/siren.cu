@@ -284,67 +284,94 @@ __global__ void siren_out_kernel(const float* __restrict__ A, const float* __res
 // Top of the backward: g_m = out_scale (gv[idx m] + gmask[m]);
 //   dA_{L-1}[m][k] = g_m w_L[k] w0 cos(w0 a)      (nfield.hpp:198-200)
 //   partial gW_L[k] += g_m sin(w0 a), gb_L += g_m (nfield.hpp:194-197)
-// grid.x = pixel chunks of `rows` pixels; 256 threads = H columns x (256/H)
-// row lanes; pixels in batches of 8 per lane with the loads issued first.
-__global__ void __launch_bounds__(NT)
+// grid.x = pixel chunks of `rows` pixels.  A row is H/4 threads with one
+// float4 each (coalesced 16-B loads / stores); TOP_RP rows per pass; each
+// thread keeps TOP_U rows in flight and prefetches the next batch into a
+// second register set before computing the current one (the kernel streams
+// 2 x 134 MB at cfg3, so it lives on memory-level parallelism).
+template <int H>
+struct TopShape {
+  static constexpr int TPR = H / 4;             // threads per row
+  static constexpr int RP = 256 / TPR;          // rows per pass
+  static constexpr int NTH = TPR * RP;          // block size
+  static constexpr int U = 4;                   // rows in flight per thread
+};
+
+template <int H>
+__global__ void __launch_bounds__(TopShape<H>::NTH)
 siren_top_kernel(const float* __restrict__ A, const float* __restrict__ wL,
                  const double* __restrict__ gv, const float* __restrict__ gmask,
-                 const int* __restrict__ idx, int n, int H, int rows, float w0, float out_scale,
+                 const int* __restrict__ idx, int n, int rows, float w0, float out_scale,
                  float* __restrict__ dA, float* __restrict__ partial) {
-  constexpr int U = 8;
-  __shared__ float s_g[NT];
-  __shared__ float s_part[NT + 32];
-  const int lanes = NT / H;  // H in {64, 128, 256}
-  const int k = threadIdx.x % H, rl = threadIdx.x / H;
+  using T = TopShape<H>;
+  constexpr int TPR = T::TPR, RP = T::RP, U = T::U;
+  __shared__ float s_part[RP][H + 1];
+  const int c4 = threadIdx.x % TPR, rl = threadIdx.x / TPR;
   const int m_begin = blockIdx.x * rows, m_end = min(n, m_begin + rows);
-  float gw = 0.f, gb = 0.f;
-  const float wk = wL[k];
-  for (int m0 = m_begin; m0 < m_end; m0 += U * lanes) {
-    const int cnt = min(U * lanes, m_end - m0);
-    __syncthreads();
-    if (threadIdx.x < cnt) {
-      const int m = m0 + threadIdx.x;
-      float g = 0.f;
-      if (gv) g += static_cast<float>(gv[idx[m]]);
-      if (gmask) g += gmask[m];
-      s_g[threadIdx.x] = g * out_scale;
-    }
-    __syncthreads();
-    float a[U];
+  const float4 wk = reinterpret_cast<const float4*>(wL)[c4];
+  float4 gw = make_float4(0.f, 0.f, 0.f, 0.f);
+  float gb = 0.f;
+  float4 a0[U], a1[U];
+  float g0[U], g1[U];
+  auto load = [&](int m0, float4 (&av)[U], float (&gvv)[U]) {
 #pragma unroll
-    for (int j = 0; j < U; ++j) {
-      const int q = rl + lanes * j;
-      a[j] = q < cnt ? A[static_cast<size_t>(m0 + q) * H + k] : 0.f;
+    for (int u = 0; u < U; ++u) {
+      const int m = m0 + rl + RP * u;
+      const bool ok = m < m_end;
+      const int mm = ok ? m : m_begin;
+      av[u] = reinterpret_cast<const float4*>(A + static_cast<size_t>(mm) * H)[c4];
+      float gg = 0.f;
+      if (gv) gg += static_cast<float>(gv[idx[mm]]);
+      if (gmask) gg += gmask[mm];
+      gvv[u] = ok ? gg * out_scale : 0.f;
     }
+  };
+  auto body = [&](int m0, const float4 (&av)[U], const float (&gvv)[U]) {
 #pragma unroll
-    for (int j = 0; j < U; ++j) {
-      const int q = rl + lanes * j;
-      if (q < cnt) {
-        const float g = s_g[q];
-        float sn, cs;
-        sincosw(a[j], w0, &sn, &cs);
-        dA[static_cast<size_t>(m0 + q) * H + k] = g * wk * w0 * cs;
-        gw = fmaf(g, sn, gw);
-        gb += g;
-      }
+    for (int u = 0; u < U; ++u) {
+      const int m = m0 + rl + RP * u;
+      const float gg = gvv[u];
+      const float4 x = av[u];
+      float4 sn, cs, d;
+      sincosw(x.x, w0, &sn.x, &cs.x);
+      sincosw(x.y, w0, &sn.y, &cs.y);
+      sincosw(x.z, w0, &sn.z, &cs.z);
+      sincosw(x.w, w0, &sn.w, &cs.w);
+      const float gw0 = gg * w0;
+      d.x = gw0 * wk.x * cs.x;
+      d.y = gw0 * wk.y * cs.y;
+      d.z = gw0 * wk.z * cs.z;
+      d.w = gw0 * wk.w * cs.w;
+      if (m < m_end) reinterpret_cast<float4*>(dA + static_cast<size_t>(m) * H)[c4] = d;
+      gw.x = fmaf(gg, sn.x, gw.x);
+      gw.y = fmaf(gg, sn.y, gw.y);
+      gw.z = fmaf(gg, sn.z, gw.z);
+      gw.w = fmaf(gg, sn.w, gw.w);
+      gb += gg;
     }
+  };
+  // two register sets: the next batch is in flight while one is computed
+  constexpr int STEP = RP * U;
+  if (m_begin < m_end) load(m_begin, a0, g0);
+  for (int m0 = m_begin; m0 < m_end; m0 += 2 * STEP) {
+    if (m0 + STEP < m_end) load(m0 + STEP, a1, g1);
+    body(m0, a0, g0);
+    if (m0 + STEP >= m_end) break;
+    if (m0 + 2 * STEP < m_end) load(m0 + 2 * STEP, a0, g0);
+    body(m0 + STEP, a1, g1);
   }
-  __syncthreads();
-  s_part[threadIdx.x] = gw;
+  // fixed-order sums over the row lanes
+  s_part[rl][4 * c4] = gw.x;
+  s_part[rl][4 * c4 + 1] = gw.y;
+  s_part[rl][4 * c4 + 2] = gw.z;
+  s_part[rl][4 * c4 + 3] = gw.w;
+  if (c4 == 0) s_part[rl][H] = gb;
   __syncthreads();
   float* out = partial + static_cast<size_t>(blockIdx.x) * (H + 1);
-  if (threadIdx.x < H) {
+  for (int k = threadIdx.x; k <= H; k += T::NTH) {
     float t = 0.f;
-    for (int q = 0; q < lanes; ++q) t += s_part[q * H + threadIdx.x];
-    out[threadIdx.x] = t;
-  }
-  __syncthreads();
-  s_part[threadIdx.x] = (k == 0) ? gb : 0.f;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int q = 0; q < lanes; ++q) t += s_part[q * H];
-    out[H] = t;
+    for (int q = 0; q < RP; ++q) t += s_part[q][k];
+    out[k] = t;
   }
 }
 
@@ -814,8 +841,26 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
   float* nxt = w.dB;   // dA_{l-1}
   // output layer
   const float* wL = theta + s.offset(L);
-  siren_top_kernel<<<n_top, NT, 0, st>>>(w.acts + (L - 1) * stride, wL, gv, gmask, w.idx, n, H,
-                                         rows_top, w0, osc, cur, part_top);
+  {
+    const float* aL = w.acts + (L - 1) * stride;
+    switch (H) {
+      case 64:
+        siren_top_kernel<64><<<n_top, TopShape<64>::NTH, 0, st>>>(aL, wL, gv, gmask, w.idx, n,
+                                                                  rows_top, w0, osc, cur, part_top);
+        break;
+      case 128:
+        siren_top_kernel<128><<<n_top, TopShape<128>::NTH, 0, st>>>(aL, wL, gv, gmask, w.idx, n,
+                                                                    rows_top, w0, osc, cur, part_top);
+        break;
+      case 192:
+        siren_top_kernel<192><<<n_top, TopShape<192>::NTH, 0, st>>>(aL, wL, gv, gmask, w.idx, n,
+                                                                    rows_top, w0, osc, cur, part_top);
+        break;
+      default:
+        siren_top_kernel<256><<<n_top, TopShape<256>::NTH, 0, st>>>(aL, wL, gv, gmask, w.idx, n,
+                                                                    rows_top, w0, osc, cur, part_top);
+    }
+  }
   PACT_TRY_S(after_launch(ctx, "siren_top_kernel"));
   add_seg(part_top, n_top, H + 1, grad + s.offset(L));
   for (int l = L - 1; l >= 1; --l) {
