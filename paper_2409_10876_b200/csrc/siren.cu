@@ -499,45 +499,79 @@ siren_wgrad_kernel(const float* __restrict__ dAl, const float* __restrict__ Apre
 }
 
 // Layer-0 gradient partials: gW_0[r][c] += dA_0[m][r] c_m[c], gb_0[r] += dA_0[m][r].
-__global__ void siren_wgrad0_kernel(const float* __restrict__ dA0, const float2* __restrict__ coords,
-                                    int n, int H, int rows, float* __restrict__ partial) {
-  __shared__ float s_part[3 * NT];
-  const int lanes = NT / H;
-  const int r = threadIdx.x % H, rl = threadIdx.x / H;
+// Same streaming shape as siren_top_kernel: float4 rows, two register sets.
+template <int H>
+__global__ void __launch_bounds__(TopShape<H>::NTH)
+siren_wgrad0_kernel(const float* __restrict__ dA0, const float2* __restrict__ coords, int n,
+                    int rows, float* __restrict__ partial) {
+  using T = TopShape<H>;
+  constexpr int TPR = T::TPR, RP = T::RP, U = T::U;
+  __shared__ float s_part[3][RP][H + 1];
+  const int c4 = threadIdx.x % TPR, rl = threadIdx.x / TPR;
   const int m_begin = blockIdx.x * rows, m_end = min(n, m_begin + rows);
-  float gx = 0.f, gy = 0.f, gb = 0.f;
-  constexpr int U = 8;
-  for (int m0 = m_begin + rl; m0 < m_end; m0 += U * lanes) {
-    float d[U];
-    float2 c[U];
+  float4 gx = make_float4(0.f, 0.f, 0.f, 0.f), gy = gx, gb = gx;
+  float4 d0[U], d1[U];
+  float2 c0[U], c1[U];
+  auto load = [&](int m0, float4 (&dv)[U], float2 (&cv)[U]) {
 #pragma unroll
-    for (int j = 0; j < U; ++j) {
-      const int m = m0 + lanes * j;
-      d[j] = m < m_end ? dA0[static_cast<size_t>(m) * H + r] : 0.f;
-      c[j] = m < m_end ? coords[m] : make_float2(0.f, 0.f);
+    for (int u = 0; u < U; ++u) {
+      const int m = m0 + rl + RP * u;
+      const bool ok = m < m_end;
+      const int mm = ok ? m : m_begin;
+      dv[u] = reinterpret_cast<const float4*>(dA0 + static_cast<size_t>(mm) * H)[c4];
+      const float2 c = coords[mm];
+      cv[u] = ok ? c : make_float2(0.f, 0.f);
+      if (!ok) dv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+  };
+  auto body = [&](const float4 (&dv)[U], const float2 (&cv)[U]) {
 #pragma unroll
-    for (int j = 0; j < U; ++j) {
-      gx = fmaf(d[j], c[j].x, gx);
-      gy = fmaf(d[j], c[j].y, gy);
-      gb += d[j];
+    for (int u = 0; u < U; ++u) {
+      const float4 d = dv[u];
+      const float2 c = cv[u];
+      gx.x = fmaf(d.x, c.x, gx.x);
+      gx.y = fmaf(d.y, c.x, gx.y);
+      gx.z = fmaf(d.z, c.x, gx.z);
+      gx.w = fmaf(d.w, c.x, gx.w);
+      gy.x = fmaf(d.x, c.y, gy.x);
+      gy.y = fmaf(d.y, c.y, gy.y);
+      gy.z = fmaf(d.z, c.y, gy.z);
+      gy.w = fmaf(d.w, c.y, gy.w);
+      gb.x += d.x;
+      gb.y += d.y;
+      gb.z += d.z;
+      gb.w += d.w;
     }
+  };
+  constexpr int STEP = RP * U;
+  if (m_begin < m_end) load(m_begin, d0, c0);
+  for (int m0 = m_begin; m0 < m_end; m0 += 2 * STEP) {
+    if (m0 + STEP < m_end) load(m0 + STEP, d1, c1);
+    body(d0, c0);
+    if (m0 + STEP >= m_end) break;
+    if (m0 + 2 * STEP < m_end) load(m0 + 2 * STEP, d0, c0);
+    body(d1, c1);
   }
-  s_part[threadIdx.x] = gx;
-  s_part[NT + threadIdx.x] = gy;
-  s_part[2 * NT + threadIdx.x] = gb;
+  const float4* acc[3] = {&gx, &gy, &gb};
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    s_part[q][rl][4 * c4] = acc[q]->x;
+    s_part[q][rl][4 * c4 + 1] = acc[q]->y;
+    s_part[q][rl][4 * c4 + 2] = acc[q]->z;
+    s_part[q][rl][4 * c4 + 3] = acc[q]->w;
+  }
   __syncthreads();
-  if (threadIdx.x < H) {
+  float* out = partial + static_cast<size_t>(blockIdx.x) * (3 * H);
+  for (int r = threadIdx.x; r < H; r += T::NTH) {
     float tx = 0.f, ty = 0.f, tb = 0.f;
-    for (int q = 0; q < lanes; ++q) {
-      tx += s_part[q * H + threadIdx.x];
-      ty += s_part[NT + q * H + threadIdx.x];
-      tb += s_part[2 * NT + q * H + threadIdx.x];
+    for (int q = 0; q < RP; ++q) {
+      tx += s_part[0][q][r];
+      ty += s_part[1][q][r];
+      tb += s_part[2][q][r];
     }
-    float* out = partial + static_cast<size_t>(blockIdx.x) * (3 * H);
-    out[2 * threadIdx.x] = tx;  // W_0 row-major [r][c]
-    out[2 * threadIdx.x + 1] = ty;
-    out[2 * H + threadIdx.x] = tb;
+    out[2 * r] = tx;  // W_0 row-major [r][c]
+    out[2 * r + 1] = ty;
+    out[2 * H + r] = tb;
   }
 }
 
@@ -888,7 +922,19 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
     if (!use_tc) PACT_TRY_S(after_launch(ctx, "siren_dgrad_kernel"));
     std::swap(cur, nxt);
   }
-  siren_wgrad0_kernel<<<n_top, NT, 0, st>>>(cur, w.coords, n, H, rows_top, part_0);
+  switch (H) {
+    case 64:
+      siren_wgrad0_kernel<64><<<n_top, TopShape<64>::NTH, 0, st>>>(cur, w.coords, n, rows_top, part_0);
+      break;
+    case 128:
+      siren_wgrad0_kernel<128><<<n_top, TopShape<128>::NTH, 0, st>>>(cur, w.coords, n, rows_top, part_0);
+      break;
+    case 192:
+      siren_wgrad0_kernel<192><<<n_top, TopShape<192>::NTH, 0, st>>>(cur, w.coords, n, rows_top, part_0);
+      break;
+    default:
+      siren_wgrad0_kernel<256><<<n_top, TopShape<256>::NTH, 0, st>>>(cur, w.coords, n, rows_top, part_0);
+  }
   PACT_TRY_S(after_launch(ctx, "siren_wgrad0_kernel"));
   add_seg(part_0, n_top, 3 * H, grad + s.offset(0));
   reduce_segments_kernel<<<segs.block_end[segs.n - 1], dim3(32, 32), 0, st>>>(segs);
