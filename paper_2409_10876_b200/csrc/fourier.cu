@@ -428,15 +428,24 @@ __device__ __forceinline__ double bin_chain(const FourierTab& t, const float* __
 //   a = eps M / den,   dc_j/dwbar = |k| sin(|k|(d_j - wbar)),
 // and w1, w2 each receive half of dL/dwbar.  About a third of the complex
 // arithmetic of the general chain; same quantities.
-template <class YF>
+// PAIR: the delays are split between this lane and lane ^ 16 (delays
+// [0, K/2) in lanes 0-15, [K/2, K) in lanes 16-31 of the warp); the pass sums
+// are combined with one fixed xor-16 shuffle, so both lanes end with the
+// bin's values.  Twice the warps per bin chunk, half the dependent chain.
+template <bool PAIR = false, class YF>
 __device__ __forceinline__ double bin_chain_real(const FourierTab& t, const float* __restrict__ s_w,
                                                  int b, float eps_m, float scale, bool impl,
                                                  YF y_of, float& G) {
-  const int K = t.K, P2 = t.P2;
+  const int P2 = t.P2;
+  const int half = PAIR ? (threadIdx.x >> 4) & 1 : 0;
+  const int j0 = PAIR ? half * (t.K / 2) : 0, j1 = PAIR ? (half ? t.K : t.K / 2) : t.K;
+  auto pair_sum = [&](float v) {
+    return PAIR ? v + __shfl_xor_sync(0xffffffffu, v, 16) : v;
+  };
   G = 0.f;
   const float k = t.kmag[b];
   const float wk = k * scale;
-  if (wk == 0.f) return 0.0;
+  if (!PAIR && wk == 0.f) return 0.0;  // (paired lanes stay converged for the shuffles)
   const int4 ix = t.idx[b];
   const float2 fr = t.frac[b];
   const float w1 = (1.f - fr.x) * s_w[ix.x] + fr.x * s_w[ix.y];
@@ -447,19 +456,19 @@ __device__ __forceinline__ double bin_chain_real(const FourierTab& t, const floa
   // z_j = conj(dp_j) exp(-i|k| wbar) = exp(i|k|(d_j - wbar)): c_j = Re z_j, s_j = Im z_j
   const bool walk = t.rho != nullptr;
   const float2 rr = walk ? conjf2(t.rho[b]) : make_float2(1.f, 0.f);
-  const float2 z0 = cmul(conjf2(t.dp[b]), ew);
+  const float2 z0 = cmul(conjf2(t.dp[j0 * P2 + b]), ew);
   auto next = [&](int j, float2& z) {
     if (walk)
       z = cmul(z, rr);
-    else if (j + 1 < K)
+    else if (j + 1 < j1)
       z = cmul(conjf2(t.dp[(j + 1) * P2 + b]), ew);
   };
   float2 S = make_float2(0.f, 0.f);
-  float den = eps_m;
+  float den = 0.f;
   {
     float2 z = z0;
 #pragma unroll 4
-    for (int j = 0; j < K; ++j) {
+    for (int j = j0; j < j1; ++j) {
       const float2 y = y_of(j);
       S.x = fmaf(z.x, y.x, S.x);
       S.y = fmaf(z.x, y.y, S.y);
@@ -467,6 +476,9 @@ __device__ __forceinline__ double bin_chain_real(const FourierTab& t, const floa
       next(j, z);
     }
   }
+  S.x = pair_sum(S.x);
+  S.y = pair_sum(S.y);
+  den = eps_m + pair_sum(den);
   const float inv = den > 0.f ? 1.f / den : 0.f;
   const float2 X = make_float2(S.x * inv, S.y * inv);
   const float al = impl && den > 0.f ? eps_m * inv : 0.f;
@@ -475,7 +487,7 @@ __device__ __forceinline__ double bin_chain_real(const FourierTab& t, const floa
   {
     float2 z = z0;
 #pragma unroll 4
-    for (int j = 0; j < K; ++j) {
+    for (int j = j0; j < j1; ++j) {
       const float2 y = y_of(j);
       const float rx = fmaf(-z.x, X.x, y.x), ry = fmaf(-z.x, X.y, y.y);
       acc = fmaf(rx, rx, fmaf(ry, ry, acc));
@@ -484,6 +496,9 @@ __device__ __forceinline__ double bin_chain_real(const FourierTab& t, const floa
       next(j, z);
     }
   }
+  acc = pair_sum(acc);
+  gs = pair_sum(gs);
+  if (wk == 0.f) return 0.0;
   G = -wk * k * gs;  // = (1/2) dL/dwbar, for w1 and for w2
   return static_cast<double>(wk) * acc;
 }
@@ -511,7 +526,7 @@ constexpr int LB = 128;
 // chunk, the next chunk's K rows of LB spectra (1 KB each) and its patch's
 // wavefront profile arrive by cp.async.bulk into the other stage.  The loss
 // partial of every chunk goes to its fixed slot (deterministic).
-__global__ void __launch_bounds__(LB) loss_bins_kernel(FourierTab t, const float2* __restrict__ Y_all,
+__global__ void __launch_bounds__(2 * LB) loss_bins_kernel(FourierTab t, const float2* __restrict__ Y_all,
                                                        const float* __restrict__ w_all, float eps_m,
                                                        float scale, int implicit,
                                                        float2* __restrict__ gbuf,
@@ -521,8 +536,12 @@ __global__ void __launch_bounds__(LB) loss_bins_kernel(FourierTab t, const float
   const int K = t.K, P2 = t.P2, A = t.A;
   const int chunks = P2 / LB, total = n_patches * chunks;
   const int stage_floats = 2 * K * LB + ((A + 3) & ~3);
-  __shared__ double s_red[LB / 32];
+  __shared__ double s_red[2 * LB / 32];
   __shared__ __align__(8) uint64_t bar[2];
+  // 2 LB threads: warp w, lane l -> bin w * 16 + (l & 15) of the chunk, delay
+  // half l >> 4 (conflict-free 8-B smem rows per half-warp)
+  const int bl = (threadIdx.x >> 5) * 16 + (threadIdx.x & 15);
+  const bool lead = (threadIdx.x & 16) == 0;
   if (threadIdx.x == 0) {
     tc::mbar_init(&bar[0], 1);
     tc::mbar_init(&bar[1], 1);
@@ -553,15 +572,16 @@ __global__ void __launch_bounds__(LB) loss_bins_kernel(FourierTab t, const float
     const float2* s_y = reinterpret_cast<const float2*>(base);
     const float* s_w = base + 2 * K * LB;
     const int patch = c / chunks, cb = c - patch * chunks;
-    const int b = cb * LB + threadIdx.x;
-    double value = 0.0;
-    if (t.mirror[b] < 0) {
-      float G;
-      const float2* yb = s_y + threadIdx.x;
-      value = bin_chain_real(t, s_w, b, eps_m, scale, implicit != 0,
-                             [&](int j) { return yb[j * LB]; }, G);
-      gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G, G);
-    }
+    const int b = cb * LB + bl;
+    // every lane runs the chain (the pair shuffles need the whole warp); the
+    // Nyquist bins' lanes (kernel A') discard their result
+    const bool ordinary = t.mirror[b] < 0;
+    float G;
+    const float2* yb = s_y + bl;
+    double value = bin_chain_real<true>(t, s_w, b, eps_m, scale, implicit != 0,
+                                        [&](int j) { return yb[j * LB]; }, G);
+    if (ordinary && lead) gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G, G);
+    if (!ordinary || !lead) value = 0.0;
     block_sum_store(value, s_red, loss_part + patch * n_parts + cb);
     __syncthreads();  // stage st is free for chunk i + 2; s_red is reusable
   }
@@ -836,8 +856,8 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
                                        static_cast<int>(smem_bins)));
     const int per_sm = std::max(1, static_cast<int>((227 * 1024 - 4096) / smem_bins));
     const int grid = std::min(n_patches * chunks, ctx->num_sms * per_sm);
-    loss_bins_kernel<<<grid, LB, smem_bins, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, gbuf,
-                                                            part, n_parts, n_patches);
+    loss_bins_kernel<<<grid, 2 * LB, smem_bins, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, gbuf,
+                                                                part, n_parts, n_patches);
   } else {
     const size_t smem_bins = sizeof(float2) * t.K * LB + smem;
     if (smem_bins > 48 * 1024) {
