@@ -759,6 +759,7 @@ void siren_work_free(SirenWork& w) {
   pool_free(w.dA, w.stream);
   pool_free(w.dB, w.stream);
   pool_free(w.partial, w.stream);
+  pool_free(w.wplanes, w.stream);
   w = SirenWork{};
 }
 
@@ -785,6 +786,13 @@ Status siren_forward(pact_ctx* ctx, const SirenShape& s, const float* theta, Sir
                                                            dv, stride);
     return after_launch(ctx, "siren_fwd_small_kernel");
   }
+  // hidden width 128 on tcgen05: the whole network in one kernel
+  // (PACT_SIREN_CHAIN=0 selects the per-layer kernels, for comparison)
+  static const bool chain = [] {
+    const char* e = std::getenv("PACT_SIREN_CHAIN");
+    return !(e && e[0] == '0');
+  }();
+  if (chain && H == 128 && L >= 2 && siren_use_tc(H)) return tc_forward_chain(ctx, s, theta, w, dv);
   siren_first_kernel<<<ctx->num_sms * 8, 256, 0, st>>>(
       w.coords, theta + s.offset(0), theta + s.offset(0) + 2 * H, n, H, w.acts);
   PACT_TRY_S(after_launch(ctx, "siren_first_kernel"));

@@ -46,6 +46,8 @@ struct SirenWork {
   float* dB = nullptr;       // [n][hidden]  backward pong
   float* partial = nullptr;  // split-M weight-gradient partials
   size_t partial_floats = 0;
+  float* wplanes = nullptr;  // tcgen05 weight planes of the fused forward (siren_chain.cu)
+  size_t wplanes_floats = 0;
   cudaStream_t stream = nullptr;  // pool stream of the buffers
 };
 
@@ -77,6 +79,10 @@ struct SirenHead {
   float* dv = nullptr;
   float scale = 0.f;
 };
+// The whole forward (first layer, tcgen05 hidden layers, head) in one kernel
+// for hidden width 128 (siren_chain.cu).
+Status tc_forward_chain(pact_ctx* ctx, const SirenShape& s, const float* theta, SirenWork& w,
+                        float* dv);
 Status tc_forward_layer(pact_ctx* ctx, int H, const float* Ain, const float* W, const float* b,
                         int n, float w0, float* Aout, const SirenHead& head);
 Status tc_dgrad_layer(pact_ctx* ctx, int H, const float* dAl, const float* W, const float* Aprev,
