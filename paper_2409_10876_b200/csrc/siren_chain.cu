@@ -238,54 +238,52 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
     const int hN = j >> 1;                    // the accumulator N-half holding its features
     const float w0 = a.w0;
     uint32_t nst = 0;  // store boxes issued by this warp
-    for (int i = 0; i < my_tiles; ++i) {
-      const int m0 = (blockIdx.x + i * gridDim.x) * CT;
-      const int rows = min(CT, a.n - m0);
-      const bool valid = p < rows;
-      float* box = box0;
-      // the next store box (its previous TMA store has read it)
-      auto open_box = [&]() {
-        if (nst >= 1) {
-          if (lane == 0) tc::bulk_wait_read<0>();
-          __syncwarp();
-        }
-      };
-      // 16 features (half hf) of this pixel into the SW128 box row
-      auto put_box = [&](const float (&v)[16], int hf) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int g = 4 * hf + c;
-          *reinterpret_cast<float4*>(box + lane * 32 + ((g ^ (lane & 7)) << 2)) =
-              make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-        }
-      };
-      // the box -> acts[l] rows of the warp's 32 pixels (rows >= n clipped)
-      auto store_box = [&](int l) {
-        tc::fence_proxy_async();
+    float* box = box0;
+    // the store box is free (its previous TMA store has read it)
+    auto open_box = [&]() {
+      if (nst >= 1) {
+        if (lane == 0) tc::bulk_wait_read<0>();
         __syncwarp();
-        if (lane == 0) {
-          tc::tma_store_3d(&tmap_acts, box, kb, m0 + 32 * q, l);
-          tc::bulk_commit();
-        }
-        ++nst;
-      };
-      // sin(w0 v) -> this chunk's A columns (hi, lo) of the next layer
-      auto put_a = [&](const float (&v)[16], int hf) {
-        float hi[16], lo[16];
+      }
+    };
+    // 16 features (half hf) of this pixel into the SW128 box row
+    auto put_box = [&](const float (&v)[16], int hf) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) tc::split_tf32_trunc(valid ? sinw(v[k], w0) : 0.f, hi[k], lo[k]);
-        tc::tmem_st16_nowait(lb + kb + 16 * hf, hi);
-        tc::tmem_st16_nowait(lb + kColAlo + kb + 16 * hf, lo);
-      };
-      auto a_ready = [&]() {
-        tc::tmem_wait_st();
-        tc::fence_before_sync();
-        tc::mbar_arrive(&sb.ardy[j]);
-      };
-      // first layer (CUDA cores): a_0 = W_0 c + b_0
-      const int role = (q == 0 && (j == 0 || j == 3)) ? (j == 0 ? 1 : 2) : -1;
-      if (role > 0) CTRACE(role, 10, i);
-      const float2 c = valid ? a.coords[m0 + p] : make_float2(0.f, 0.f);
+      for (int c = 0; c < 4; ++c) {
+        const int g = 4 * hf + c;
+        *reinterpret_cast<float4*>(box + lane * 32 + ((g ^ (lane & 7)) << 2)) =
+            make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+      }
+    };
+    // the box -> acts[l] rows [r0, r0 + 32) (rows >= n clipped by the tensor bounds)
+    auto store_box = [&](int l, int r0) {
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        tc::tma_store_3d(&tmap_acts, box, kb, r0, l);
+        tc::bulk_commit();
+      }
+      ++nst;
+    };
+    // sin(w0 v) -> this chunk's A columns (hi, lo) of the next layer
+    auto put_a = [&](const float (&v)[16], int hf, bool valid) {
+      float hi[16], lo[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) tc::split_tf32_trunc(valid ? sinw(v[k], w0) : 0.f, hi[k], lo[k]);
+      tc::tmem_st16_nowait(lb + kb + 16 * hf, hi);
+      tc::tmem_st16_nowait(lb + kColAlo + kb + 16 * hf, lo);
+    };
+    auto a_ready = [&]() {
+      tc::tmem_wait_st();
+      tc::fence_before_sync();
+      tc::mbar_arrive(&sb.ardy[j]);
+    };
+    auto tile_m0 = [&](int t) { return (blockIdx.x + t * gridDim.x) * CT; };
+    // first layer of tile t (CUDA cores): a_0 = W_0 c + b_0 -> acts[0], A
+    auto first_layer = [&](int t) {
+      const int m0t = tile_m0(t);
+      const bool vt = p < min(CT, a.n - m0t);
+      const float2 c = vt ? a.coords[m0t + p] : make_float2(0.f, 0.f);
       open_box();
 #pragma unroll 1
       for (int hf = 0; hf < 2; ++hf) {
@@ -296,16 +294,58 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
           v[k] = fmaf(s_w0[2 * f + 1], c.y, fmaf(s_w0[2 * f], c.x, s_b0[f]));
         }
         put_box(v, hf);
-        put_a(v, hf);
+        put_a(v, hf, vt);
       }
-      store_box(0);
+      store_box(0, m0t + 32 * q);
       a_ready();
-      if (role > 0) CTRACE(role, 11, i);
+    };
+    const int role = (q == 0 && (j == 0 || j == 3)) ? (j == 0 ? 1 : 2) : -1;
+    if (my_tiles > 0) first_layer(0);
+    for (int i = 0; i < my_tiles; ++i) {
+      const int m0 = tile_m0(i);
+      const int rows = min(CT, a.n - m0);
+      const bool valid = p < rows;
+      if (role > 0) CTRACE(role, 10, i);
       float hp = 0.f;  // head partial over this chunk's features
       for (int l = 0; l < nl; ++l) {
         const uint32_t lc = static_cast<uint32_t>(i * nl + l), b = lc & 1;
         const bool last = l == nl - 1;
-        tc::mbar_wait(&sb.dfull[b][hN], (lc >> 1) & 1);
+        if (!last) {
+          tc::mbar_wait(&sb.dfull[b][hN], (lc >> 1) & 1);
+        } else if (i + 1 < my_tiles) {
+          // the next tile's first layer, computed (and stored) while the
+          // tensor core finishes this tile's last layer; its A columns go in
+          // as soon as every MMA of that layer is done, so the tensor core
+          // restarts while this tile's last layer and head drain
+          const int m1 = tile_m0(i + 1);
+          const bool v1 = p < min(CT, a.n - m1);
+          const float2 c = v1 ? a.coords[m1 + p] : make_float2(0.f, 0.f);
+          float ahi[32], alo[32];
+          open_box();
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            float v[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const int f = kb + 16 * hf + k;
+              v[k] = fmaf(s_w0[2 * f + 1], c.y, fmaf(s_w0[2 * f], c.x, s_b0[f]));
+            }
+            put_box(v, hf);
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+              tc::split_tf32_trunc(v1 ? sinw(v[k], w0) : 0.f, ahi[16 * hf + k], alo[16 * hf + k]);
+          }
+          store_box(0, m1 + 32 * q);
+          tc::mbar_wait(&sb.dfull[b][1], (lc >> 1) & 1);
+          tc::fence_after_sync();
+          tc::tmem_st32(lb + kb, ahi);
+          tc::tmem_st32(lb + kColAlo + kb, alo);
+          tc::fence_before_sync();
+          tc::mbar_arrive(&sb.ardy[j]);
+          if (role > 0) CTRACE(role, 11, i + 1);
+        } else {
+          tc::mbar_wait(&sb.dfull[b][1], (lc >> 1) & 1);
+        }
         if (role > 0) CTRACE(role, 12, lc);
         tc::fence_after_sync();
         open_box();
@@ -320,13 +360,13 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
 #pragma unroll
             for (int k = 0; k < 16; ++k) hp = fmaf(s_wl[kb + 16 * hf + k], sinw(v[k], w0), hp);
           } else {
-            put_a(v, hf);
+            put_a(v, hf, valid);
           }
         }
         tc::fence_before_sync();
         tc::mbar_arrive(&sb.dfree[b][hN]);  // D_b half read; the next layer's A is in flight
         if (role > 0) CTRACE(role, 13, lc);
-        store_box(l + 1);
+        store_box(l + 1, m0 + 32 * q);
         if (!last) a_ready();
         if (role > 0) CTRACE(role, 14, lc);
       }
