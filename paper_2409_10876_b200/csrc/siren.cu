@@ -849,6 +849,63 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
     reduce_rows_kernel<<<div_up(P, 128), 128, 0, st>>>(w.partial, n, P, grad);
     return after_launch(ctx, "reduce_rows_kernel");
   }
+  if (L + 1 > kMaxSeg) return validation("siren: too many layers for the segmented reduction");
+  auto al64 = [](size_t x) { return (x + 63) & ~size_t(63); };
+  ReduceSegs segs{};
+  auto add_seg = [&](const float* src, int chunks, int per, double* dst) {
+    const int k = segs.n++;
+    segs.src[k] = src;
+    segs.dst[k] = dst;
+    segs.n_chunks[k] = chunks;
+    segs.per[k] = per;
+    segs.block_end[k] = (k ? segs.block_end[k - 1] : 0) + div_up(per, 32);
+  };
+  // hidden width 128 on tcgen05: one fused kernel per hidden layer (data +
+  // weight gradient; the output layer folded into the top one, layer 0 into
+  // the bottom one).  PACT_SIREN_FUSED_BWD=0 selects the per-op kernels.
+  static const bool fused = [] {
+    const char* e = std::getenv("PACT_SIREN_FUSED_BWD");
+    return !(e && e[0] == '0');
+  }();
+  if (fused && H == 128 && L >= 2 && siren_use_tc(H)) {
+    const int grid = tc_bwd_grid(ctx, n);
+    const size_t per_w = static_cast<size_t>(H) * H + H;
+    const size_t sz_w = al64(static_cast<size_t>(grid) * per_w),
+                 sz_top = al64(static_cast<size_t>(grid) * (H + 1)),
+                 sz_0 = static_cast<size_t>(grid) * 3 * H;
+    PACT_TRY_S(ensure_partial(w, sz_top + (L - 1) * sz_w + sz_0, st));
+    float* part_top = w.partial;
+    float* part_w = part_top + sz_top;
+    float* part_0 = part_w + (L - 1) * sz_w;
+    float* cur = w.dA;
+    float* nxt = w.dB;
+    for (int l = L - 1; l >= 1; --l) {
+      const bool top = l == L - 1, bottom = l == 1;
+      TcBwdLayer a;
+      a.X = top ? w.acts + (L - 1) * stride : cur;
+      a.Aprev = w.acts + (l - 1) * stride;
+      a.W = theta + s.offset(l);
+      a.gv = gv;
+      a.gmask = gmask;
+      a.idx = w.idx;
+      a.wL = theta + s.offset(L);
+      a.coords = w.coords;
+      a.out_scale = osc;
+      a.w0 = w0;
+      a.n = n;
+      a.Y = bottom ? nullptr : nxt;
+      a.part_w = part_w + (l - 1) * sz_w;
+      a.part_top = part_top;
+      a.part_0 = part_0;
+      PACT_TRY_S(tc_bwd_layer(ctx, top, bottom, a));
+      add_seg(a.part_w, grid, static_cast<int>(per_w), grad + s.offset(l));
+      std::swap(cur, nxt);
+    }
+    add_seg(part_top, grid, H + 1, grad + s.offset(L));
+    add_seg(part_0, grid, 3 * H, grad + s.offset(0));
+    reduce_segments_kernel<<<segs.block_end[segs.n - 1], dim3(32, 32), 0, st>>>(segs);
+    return after_launch(ctx, "reduce_segments_kernel");
+  }
   // chunking for the split-M reductions
   const int tilesW = (H / 128 > 0 ? H / 128 : 1) * (H / 128 > 0 ? H / 128 : 1);
   const int rows_top = chunk_rows(n, 1, 4 * ctx->num_sms);
@@ -860,7 +917,6 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
   // one partial slice per reduction (top, each hidden layer, layer 0), summed
   // by a single segmented launch at the end
   // (slices start on 256-B boundaries: the weight-gradient kernels store vectors)
-  auto al64 = [](size_t x) { return (x + 63) & ~size_t(63); };
   const size_t per_w = static_cast<size_t>(H) * H + H;
   const size_t sz_top = al64(static_cast<size_t>(n_top) * (H + 1)),
                sz_w = al64(static_cast<size_t>(n_w) * per_w), sz_0 = static_cast<size_t>(n_top) * 3 * H;
@@ -868,16 +924,6 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
   float* part_top = w.partial;
   float* part_w = part_top + sz_top;  // layer l at part_w + (l - 1) sz_w
   float* part_0 = part_w + (L - 1) * sz_w;
-  if (L + 1 > kMaxSeg) return validation("siren: too many layers for the segmented reduction");
-  ReduceSegs segs{};
-  auto add_seg = [&](const float* src, int chunks, int per, double* dst) {
-    const int k = segs.n++;
-    segs.src[k] = src;
-    segs.dst[k] = dst;
-    segs.n_chunks[k] = chunks;
-    segs.per[k] = per;
-    segs.block_end[k] = (k ? segs.block_end[k - 1] : 0) + div_up(per, 32);
-  };
 
   float* cur = w.dA;   // dA_l
   float* nxt = w.dB;   // dA_{l-1}

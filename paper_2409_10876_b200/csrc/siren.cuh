@@ -91,4 +91,26 @@ int tc_wgrad_rows(pact_ctx* ctx, int n);  // pixels per weight-gradient partial
 Status tc_wgrad_layer(pact_ctx* ctx, int H, const float* dAl, const float* Aprev, int n, int rows,
                       float w0, float* partial, int n_chunks);
 
+// Fused backward of one tcgen05 layer (siren_bwd.cu, hidden 128): data and
+// weight gradients from one pass; TOP forms dA_l from a_l and g (output
+// layer), BOTTOM accumulates the layer-0 partials instead of storing dA_0.
+struct TcBwdLayer {
+  const float* X = nullptr;      // dA_l [n][128]; TOP: a_l
+  const float* Aprev = nullptr;  // a_{l-1} [n][128]
+  const float* W = nullptr;      // W_l [128][128]
+  const double* gv = nullptr;    // TOP
+  const float* gmask = nullptr;  // TOP
+  const int* idx = nullptr;      // TOP
+  const float* wL = nullptr;     // TOP
+  const float2* coords = nullptr;  // BOTTOM
+  float out_scale = 0.f, w0 = 0.f;
+  int n = 0;
+  float* Y = nullptr;         // dA_{l-1} (not BOTTOM)
+  float* part_w = nullptr;    // [grid][128 * 128 + 128]
+  float* part_top = nullptr;  // TOP: [grid][129]
+  float* part_0 = nullptr;    // BOTTOM: [grid][384]
+};
+int tc_bwd_grid(pact_ctx* ctx, int n);  // CTAs (= partial rows) of tc_bwd_layer
+Status tc_bwd_layer(pact_ctx* ctx, bool top, bool bottom, const TcBwdLayer& layer);
+
 }  // namespace pactgpu

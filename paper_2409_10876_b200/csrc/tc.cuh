@@ -204,6 +204,17 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_
                "r"(bytes)
                : "memory");
 }
+// TMA tensor load of one box of a 2-D tensor at (c0, c1) into smem (completion
+// on an mbarrier, transaction bytes = the full box; out-of-bounds rows are zero).
+__device__ __forceinline__ void tma_load_2d(void* sdst, const void* tmap, int c0, int c1,
+                                            uint64_t* bar) {
+  uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(sdst));
+  uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(d),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(b)
+      : "memory");
+}
 // TMA tensor store of one smem box to a 3-D tensor at (c0, c1, c2) (bulk group).
 __device__ __forceinline__ void tma_store_3d(const void* tmap, const void* ssrc, int c0, int c1,
                                              int c2) {

@@ -75,6 +75,8 @@ void run() {
 }
 
 int main() {
+  run<16, true>();
+  run<32, true>();
   run<64, true>();
   run<128, true>();
   run<256, true>();
