@@ -58,10 +58,13 @@
 #define BWD_EXP 0
 #endif
 #if BWD_EXP == 5
+#ifndef BWD_TRACE_MODE
+#define BWD_TRACE_MODE 0
+#endif
 __device__ unsigned long long g_btrace[16][512];
 #define BTRACE(cond, tag, idx)                                                      \
   do {                                                                              \
-    if (MODE == 0 && blockIdx.x == 0 && (cond) && (idx) < 512) {                   \
+    if (MODE == BWD_TRACE_MODE && blockIdx.x == 0 && (cond) && (idx) < 512) {      \
       unsigned long long t_;                                                        \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
       g_btrace[tag][idx] = t_;                                                      \
@@ -467,15 +470,18 @@ tc_bwd_kernel(BwdArgs a, const __grid_constant__ CUtensorMap tmap_x) {
         for (int t = 0; t < HP; ++t)
           if (pb + t < rows) y[static_cast<size_t>(t) * BH] = v[t] * cw[t];
       } else {
+        // fp32 sums over the tile's 16 pixels, then one fp64 add per tile
+        float sx = 0.f, sy = 0.f, s1 = 0.f;
 #pragma unroll
         for (int t = 0; t < HP; ++t) {
           const float out = pb + t < rows ? v[t] * cw[t] : 0.f;
-          const float cx = __shfl_sync(0xffffffffu, cme.x, t);
-          const float cy = __shfl_sync(0xffffffffu, cme.y, t);
-          gx = fma(static_cast<double>(out), static_cast<double>(cx), gx);
-          gy = fma(static_cast<double>(out), static_cast<double>(cy), gy);
-          gb += static_cast<double>(out);
+          sx = fmaf(out, __shfl_sync(0xffffffffu, cme.x, t), sx);
+          sy = fmaf(out, __shfl_sync(0xffffffffu, cme.y, t), sy);
+          s1 += out;
         }
+        gx += static_cast<double>(sx);
+        gy += static_cast<double>(sy);
+        gb += static_cast<double>(s1);
       }
     }
     if (BOTTOM) {

@@ -58,3 +58,27 @@ def test_siren_backward_h128(ctx, width, height, layers, seed):
         e = rel_l2(got[blk], want[blk])
         assert e <= 1e-3, (l, e)
         off += rows * cols + rows
+
+
+def test_siren_backward_h128_many_tiles(ctx):
+    """The fused per-layer backward (csrc/siren_bwd.cu) at a size where every
+    CTA runs ~20 32-pixel tiles through all buffer rings (ragged last
+    tile, uneven tiles per CTA), against the oracle's backprop_sos; plus the
+    bias and head blocks exactly as the per-op kernels compute them."""
+    grid, mask, spec, theta = _case(401, 383, 4, 9)
+    idx, _ = masked_pixels(grid, mask)
+    assert len(idx) % 32 != 0 and len(idx) > 148 * 32 * 4
+    rng = np.random.default_rng(109)
+    g = rng.standard_normal(len(idx)).astype(np.float32)
+    got = ctx.siren_backward(spec, torch.as_tensor(theta), grid, mask, torch.as_tensor(g))
+    want = orc().backprop_sos(spec, theta.astype(np.float32).astype(np.float64), grid, mask,
+                              g.astype(np.float64))
+    got = got.cpu().numpy()
+    off = 0
+    for l in range(spec.n_hidden_layers + 1):
+        rows = 1 if l == spec.n_hidden_layers else 128
+        cols = 2 if l == 0 else 128
+        for blk in (slice(off, off + rows * cols), slice(off + rows * cols, off + rows * cols + rows)):
+            e = rel_l2(got[blk], want[blk])
+            assert e <= 1e-4, (l, e)
+        off += rows * cols + rows
