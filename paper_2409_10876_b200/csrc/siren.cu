@@ -707,6 +707,17 @@ __global__ void reduce_rows_kernel(const float* __restrict__ contrib, int n, int
 
 }  // namespace
 
+// The fused per-layer backward (siren_bwd.cu) serves hidden width 128 on
+// tcgen05; PACT_SIREN_FUSED_BWD=0 selects the per-op kernels.  When it runs,
+// the forward skips storing a_0 (the backward recomputes it).
+bool siren_fused_bwd(const SirenShape& s) {
+  static const bool on = [] {
+    const char* e = std::getenv("PACT_SIREN_FUSED_BWD");
+    return !(e && e[0] == '0');
+  }();
+  return on && s.hidden == 128 && s.layers >= 2 && siren_use_tc(s.hidden);
+}
+
 bool siren_use_tc(int hidden) {
   static const bool simt = [] {
     const char* e = std::getenv("PACT_SIREN_SIMT");
@@ -792,7 +803,8 @@ Status siren_forward(pact_ctx* ctx, const SirenShape& s, const float* theta, Sir
     const char* e = std::getenv("PACT_SIREN_CHAIN");
     return !(e && e[0] == '0');
   }();
-  if (chain && H == 128 && L >= 2 && siren_use_tc(H)) return tc_forward_chain(ctx, s, theta, w, dv);
+  if (chain && H == 128 && L >= 2 && siren_use_tc(H))
+    return tc_forward_chain(ctx, s, theta, w, dv, !siren_fused_bwd(s));
   siren_first_kernel<<<ctx->num_sms * 8, 256, 0, st>>>(
       w.coords, theta + s.offset(0), theta + s.offset(0) + 2 * H, n, H, w.acts);
   PACT_TRY_S(after_launch(ctx, "siren_first_kernel"));
@@ -863,11 +875,7 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
   // hidden width 128 on tcgen05: one fused kernel per hidden layer (data +
   // weight gradient; the output layer folded into the top one, layer 0 into
   // the bottom one).  PACT_SIREN_FUSED_BWD=0 selects the per-op kernels.
-  static const bool fused = [] {
-    const char* e = std::getenv("PACT_SIREN_FUSED_BWD");
-    return !(e && e[0] == '0');
-  }();
-  if (fused && H == 128 && L >= 2 && siren_use_tc(H)) {
+  if (siren_fused_bwd(s)) {
     const int grid = tc_bwd_grid(ctx, n);
     const size_t per_w = static_cast<size_t>(H) * H + H;
     const size_t sz_w = al64(static_cast<size_t>(grid) * per_w),
@@ -883,13 +891,15 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
       const bool top = l == L - 1, bottom = l == 1;
       TcBwdLayer a;
       a.X = top ? w.acts + (L - 1) * stride : cur;
-      a.Aprev = w.acts + (l - 1) * stride;
+      a.Aprev = bottom ? nullptr : w.acts + (l - 1) * stride;
       a.W = theta + s.offset(l);
       a.gv = gv;
       a.gmask = gmask;
       a.idx = w.idx;
       a.wL = theta + s.offset(L);
       a.coords = w.coords;
+      a.W0 = theta + s.offset(0);
+      a.b0 = a.W0 + 2 * H;
       a.out_scale = osc;
       a.w0 = w0;
       a.n = n;

@@ -70,6 +70,7 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
 // SIMT tiles remain for other widths and when PACT_SIREN_SIMT=1.
 bool siren_tc_supported(int hidden);
 bool siren_use_tc(int hidden);
+bool siren_fused_bwd(const SirenShape& s);
 // Output layer fused into the last forward layer's epilogue (w == null: not fused):
 // dv[idx[m]] = scale * (b[0] + sum_k w[k] sin(w0 a_{L-1}[m][k])).
 struct SirenHead {
@@ -81,8 +82,9 @@ struct SirenHead {
 };
 // The whole forward (first layer, tcgen05 hidden layers, head) in one kernel
 // for hidden width 128 (siren_chain.cu).
+// store_a0 = false: a_0 is not written (the fused backward recomputes it).
 Status tc_forward_chain(pact_ctx* ctx, const SirenShape& s, const float* theta, SirenWork& w,
-                        float* dv);
+                        float* dv, bool store_a0);
 Status tc_forward_layer(pact_ctx* ctx, int H, const float* Ain, const float* W, const float* b,
                         int n, float w0, float* Aout, const SirenHead& head);
 Status tc_dgrad_layer(pact_ctx* ctx, int H, const float* dAl, const float* W, const float* Aprev,
@@ -103,6 +105,8 @@ struct TcBwdLayer {
   const int* idx = nullptr;      // TOP
   const float* wL = nullptr;     // TOP
   const float2* coords = nullptr;  // BOTTOM
+  const float* W0 = nullptr;       // BOTTOM: layer 0 (a_0 is recomputed, not read)
+  const float* b0 = nullptr;
   float out_scale = 0.f, w0 = 0.f;
   int n = 0;
   float* Y = nullptr;         // dA_{l-1} (not BOTTOM)

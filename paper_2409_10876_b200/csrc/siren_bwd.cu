@@ -10,8 +10,10 @@
 //   the head partials gw_L = sum g s sin(w0 a_l), gb_L = sum g s are kept.
 // BOTTOM (l = 1): dA_0 is not stored; its layer-0 partials
 //   gW_0 = sum dA_0 c^T, gb_0 = sum dA_0 (nfield.hpp:228-232) are accumulated
-//   in the epilogue.
-// So a 4-layer network's backward is 3 launches reading a_0..a_3 once each
+//   in the epilogue.  a_0 = W_0 c + b_0 is recomputed from the pixel
+//   coordinates (two FMAs, the forward's expression) instead of being stored
+//   by the forward and streamed back (-2 x 4 B per pixel and feature).
+// So a 4-layer network's backward is 3 launches reading a_1..a_3 once each
 // plus dA_2, dA_1 (written once, read once) instead of 8 kernels.
 //
 // Per 32-pixel tile (persistent CTAs, tile t = blockIdx + i * grid):
@@ -111,6 +113,8 @@ struct BwdArgs {
   const int* idx;       // TOP: masked pixel -> raster index
   const float* wL;      // TOP: head weights [128]
   const float2* coords; // BOTTOM
+  const float* W0;      // BOTTOM: layer 0 [128][2], b0 [128] (a_0 = W_0 c + b_0)
+  const float* b0;
   float out_scale, w0;
   int n;
   float* Y;         // dA_{l-1} [n][128] (not BOTTOM)
@@ -211,7 +215,7 @@ tc_bwd_kernel(BwdArgs a, const __grid_constant__ CUtensorMap tmap_x) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) tc::tma_load_2d(d + c * BT * 32, &tmap_x, 32 * c, m0, bar);
   };
-  if (tid == 0)
+  if (tid == 0 && !BOTTOM)
     for (int i = 0; i < NR && i < my_tiles; ++i) load_raw(i);
   // W_l -> TMEM as the data gradient's A operand: A[k][j] = W[j][k] (lane k)
   for (int e = tid; e < BH * BH / 4; e += kThr) {
@@ -343,20 +347,38 @@ tc_bwd_kernel(BwdArgs a, const __grid_constant__ CUtensorMap tmap_x) {
   } else if (warp < kDW + kZW) {
     // ---- a_{l-1} producers: thread = feature k, pixels [16 h, 16 h + 16) ----
     const int q = warp & 3, h = (warp - kDW) >> 2, k = 32 * q + lane, pb = HP * h;
+    // BOTTOM: a_0 = W_0 c + b_0 from the coordinates (lane t < 16 holds pixel
+    // pb + t of the tile, one tile ahead)
+    float w0x = 0.f, w0y = 0.f, b0k = 0.f;
+    float2 cnext = make_float2(0.f, 0.f);
+    auto load_c = [&](int i) {
+      return a.coords[min(tile_m0(i) + pb + (lane & (HP - 1)), n - 1)];
+    };
+    if (BOTTOM) {
+      w0x = a.W0[2 * k];
+      w0y = a.W0[2 * k + 1];
+      b0k = a.b0[k];
+      if (my_tiles > 0) cnext = load_c(0);
+    }
     for (int i = 0; i < my_tiles; ++i) {
       const int bz = i % NZ, r = i % NR;
       const int rows = min(BT, n - tile_m0(i));
-      tc::mbar_wait(&sb.rfull[r], (i / NR) & 1);
+      const float2 cc = cnext;
+      if (BOTTOM && i + 1 < my_tiles) cnext = load_c(i + 1);
+      if (!BOTTOM) tc::mbar_wait(&sb.rfull[r], (i / NR) & 1);
       BTRACE(warp == kDW && lane == 0, 5, i);
       const float* ar = raw + r * kRaw + pb * BH + k;
       float zh4[HP], zl4[HP];
 #pragma unroll
       for (int t = 0; t < HP; ++t) {
-        float z = __sinf(red2pi_b(w0 * ar[t * BH]));
+        const float av = BOTTOM ? fmaf(w0y, __shfl_sync(0xffffffffu, cc.y, t),
+                                       fmaf(w0x, __shfl_sync(0xffffffffu, cc.x, t), b0k))
+                                : ar[t * BH];
+        float z = __sinf(red2pi_b(w0 * av));
         if (pb + t >= rows) z = 0.f;
         tc::split_tf32_trunc(z, zh4[t], zl4[t]);
       }
-      tc::mbar_arrive(&sb.rfree[r]);
+      if (!BOTTOM) tc::mbar_arrive(&sb.rfree[r]);
       // z planes (the weight gradient's B: row = k, K = pixel) of buffer bz
       if (i >= NZ) tc::mbar_wait(&sb.wfree[bz], ((i - NZ) / NZ) & 1);
       BTRACE(warp == kDW && lane == 0, 6, i);
@@ -438,21 +460,42 @@ tc_bwd_kernel(BwdArgs a, const __grid_constant__ CUtensorMap tmap_x) {
     const uint32_t lb = t0 + (static_cast<uint32_t>(32 * q) << 16);
     const bool loader = warp == kThr / 32 - 1 && lane == 0;  // issues the loads i + NR, i + ND
     double gx = 0.0, gy = 0.0, gb = 0.0;
+    float w0x = 0.f, w0y = 0.f, b0k = 0.f;
+    float2 cnext = make_float2(0.f, 0.f);
+    auto load_c = [&](int i) {
+      return a.coords[min(tile_m0(i) + pb + (lane & (HP - 1)), n - 1)];
+    };
+    if (BOTTOM) {
+      w0x = a.W0[2 * k];
+      w0y = a.W0[2 * k + 1];
+      b0k = a.b0[k];
+      if (my_tiles > 0) cnext = load_c(0);
+    }
     for (int i = 0; i < my_tiles; ++i) {
       const int b = i & 1, r = i % NR;
       const int m0 = tile_m0(i), rows = min(BT, n - m0);
-      float2 cme = make_float2(0.f, 0.f);
-      if (BOTTOM && lane < HP && pb + lane < rows) cme = a.coords[m0 + pb + lane];
-      // the cosine factor from the raw a_{l-1} tile
-      tc::mbar_wait(&sb.rfull[r], (i / NR) & 1);
-      const float* ar = raw + r * kRaw + pb * BH + k;
+      const float2 cme = cnext;
+      if (BOTTOM && i + 1 < my_tiles) cnext = load_c(i + 1);
       float cw[HP];
+      if (BOTTOM) {
+        // a_0 = W_0 c + b_0 (the forward's expression)
 #pragma unroll
-      for (int t = 0; t < HP; ++t) cw[t] = w0 * __cosf(red2pi_b(w0 * ar[t * BH]));
-      tc::mbar_arrive(&sb.rfree[r]);
-      if (loader && i + NR < my_tiles) {
-        tc::mbar_wait(&sb.rfree[r], (i / NR) & 1);
-        load_raw(i + NR);
+        for (int t = 0; t < HP; ++t) {
+          const float av = fmaf(w0y, __shfl_sync(0xffffffffu, cme.y, t),
+                                fmaf(w0x, __shfl_sync(0xffffffffu, cme.x, t), b0k));
+          cw[t] = w0 * __cosf(red2pi_b(w0 * av));
+        }
+      } else {
+        // the cosine factor from the raw a_{l-1} tile
+        tc::mbar_wait(&sb.rfull[r], (i / NR) & 1);
+        const float* ar = raw + r * kRaw + pb * BH + k;
+#pragma unroll
+        for (int t = 0; t < HP; ++t) cw[t] = w0 * __cosf(red2pi_b(w0 * ar[t * BH]));
+        tc::mbar_arrive(&sb.rfree[r]);
+        if (loader && i + NR < my_tiles) {
+          tc::mbar_wait(&sb.rfree[r], (i / NR) & 1);
+          load_raw(i + NR);
+        }
       }
       __syncwarp();
       tc::mbar_wait(&sb.dfull[b], (i >> 1) & 1);
@@ -569,6 +612,8 @@ Status tc_bwd_layer(pact_ctx* ctx, bool top, bool bottom, const TcBwdLayer& L) {
   a.idx = L.idx;
   a.wL = L.wL;
   a.coords = L.coords;
+  a.W0 = L.W0;
+  a.b0 = L.b0;
   a.out_scale = L.out_scale;
   a.w0 = L.w0;
   a.n = L.n;

@@ -20,8 +20,9 @@
 // half h of the features = K-chunks 2h, 2h+1).  The epilogue of layer l
 // writes layer l+1's A one 32-feature chunk at a time and signals it, so the
 // tensor core starts layer l+1 while the rest of layer l drains.  The
-// pre-activations a_l still go to HBM (row-major [n][128], the backward's
-// input); the per-layer re-read of the separate-kernel forward does not.
+// pre-activations a_1 .. a_{L-1} go to HBM (row-major [n][128], the
+// backward's input; a_0 too unless the fused backward recomputes it from the
+// coordinates); the per-layer re-read of the separate-kernel forward does not.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -83,6 +84,7 @@ struct ChainArgs {
   float scale, w0;
   float* acts;  // [L][n][128]
   float* dv;
+  int store_a0;  // 0: a_0 is not written (the fused backward recomputes it)
 };
 
 __device__ __forceinline__ float red2pi_c(float x) {
@@ -284,7 +286,7 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
       const int m0t = tile_m0(t);
       const bool vt = p < min(CT, a.n - m0t);
       const float2 c = vt ? a.coords[m0t + p] : make_float2(0.f, 0.f);
-      open_box();
+      if (a.store_a0) open_box();
 #pragma unroll 1
       for (int hf = 0; hf < 2; ++hf) {
         float v[16];
@@ -293,10 +295,10 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
           const int f = kb + 16 * hf + k;
           v[k] = fmaf(s_w0[2 * f + 1], c.y, fmaf(s_w0[2 * f], c.x, s_b0[f]));
         }
-        put_box(v, hf);
+        if (a.store_a0) put_box(v, hf);
         put_a(v, hf, vt);
       }
-      store_box(0, m0t + 32 * q);
+      if (a.store_a0) store_box(0, m0t + 32 * q);
       a_ready();
     };
     const int role = (q == 0 && (j == 0 || j == 3)) ? (j == 0 ? 1 : 2) : -1;
@@ -321,7 +323,7 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
           const bool v1 = p < min(CT, a.n - m1);
           const float2 c = v1 ? a.coords[m1 + p] : make_float2(0.f, 0.f);
           float ahi[32], alo[32];
-          open_box();
+          if (a.store_a0) open_box();
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {
             float v[16];
@@ -330,12 +332,12 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
               const int f = kb + 16 * hf + k;
               v[k] = fmaf(s_w0[2 * f + 1], c.y, fmaf(s_w0[2 * f], c.x, s_b0[f]));
             }
-            put_box(v, hf);
+            if (a.store_a0) put_box(v, hf);
 #pragma unroll
             for (int k = 0; k < 16; ++k)
               tc::split_tf32_trunc(v1 ? sinw(v[k], w0) : 0.f, ahi[16 * hf + k], alo[16 * hf + k]);
           }
-          store_box(0, m1 + 32 * q);
+          if (a.store_a0) store_box(0, m1 + 32 * q);
           tc::mbar_wait(&sb.dfull[b][1], (lc >> 1) & 1);
           tc::fence_after_sync();
           tc::tmem_st32(lb + kb, ahi);
@@ -390,7 +392,7 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
 
 // Forward of the whole network for hidden width 128 with >= 1 tcgen05 layer.
 Status tc_forward_chain(pact_ctx* ctx, const SirenShape& s, const float* theta, SirenWork& w,
-                        float* dv) {
+                        float* dv, bool store_a0) {
   const int n = w.n, L = s.layers, nl = L - 1;
   if (s.hidden != CH || nl < 1 || nl > kMaxHidden || s.in_dim != 2)
     return validation("tc_forward_chain: unsupported network shape");
@@ -425,6 +427,7 @@ Status tc_forward_chain(pact_ctx* ctx, const SirenShape& s, const float* theta, 
   a.w0 = static_cast<float>(s.omega0);
   a.acts = w.acts;
   a.dv = dv;
+  a.store_a0 = store_a0 ? 1 : 0;
   // acts as a 3-D tensor [L][n][128] fp32 for the epilogue's TMA stores
   static PFN_cuTensorMapEncodeTiled encode = [] {
     void* fn = nullptr;
