@@ -108,7 +108,7 @@ STAGE_KERNEL = {"ray_backward": "ray_backward_plan_kernel", "wavefront": "wavefr
 
 def load_traffic():
     """Per-launch DRAM bytes of the hot kernels from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    path = os.path.join(ROOT, "profiles", "traffic_r01b.json")
     try:
         with open(path) as f:
             return json.load(f)
