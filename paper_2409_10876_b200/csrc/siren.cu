@@ -578,11 +578,13 @@ siren_wgrad0_kernel(const float* __restrict__ dA0, const float2* __restrict__ co
 // grad[off + p] = sum_chunk partial[chunk][p]   (fixed order, fp64)
 // All of one backward pass's partial-sum reductions in one launch: segment
 // s sums partial rows [n_chunks][per] of src into dst.  A block is
-// (32 params) x (32 chunk lanes); lane y sums chunks y, y+32, ... with four
-// independent accumulators, then a fixed-order fold over the lanes
-// (deterministic).  Block b belongs to the segment whose cumulative block
-// range holds b.
+// (64 params) x (4 chunk groups); group y sums its contiguous quarter of the
+// chunks with four interleaved accumulators (every thread has ~n_chunks / 4
+// independent coalesced loads in flight: one wave of latency, not one per
+// chunk), then a fixed-order fold over the groups (deterministic).  Block b
+// belongs to the segment whose cumulative block range holds b.
 constexpr int kMaxSeg = 8;
+constexpr int kRedP = 64, kRedG = 4;
 struct ReduceSegs {
   const float* src[kMaxSeg];
   double* dst[kMaxSeg];
@@ -590,30 +592,34 @@ struct ReduceSegs {
   int n;
 };
 
-__global__ void __launch_bounds__(1024) reduce_segments_kernel(ReduceSegs sg) {
-  __shared__ double s_sum[32][33];
+__global__ void __launch_bounds__(kRedP * kRedG) reduce_segments_kernel(ReduceSegs sg) {
+  __shared__ double s_sum[kRedG][kRedP];
   int seg = 0;
   while (seg + 1 < sg.n && blockIdx.x >= static_cast<unsigned>(sg.block_end[seg])) ++seg;
   const int b = blockIdx.x - (seg ? sg.block_end[seg - 1] : 0);
   const float* __restrict__ partial = sg.src[seg];
   const int per_chunk = sg.per[seg], n_chunks = sg.n_chunks[seg];
-  const int p = b * 32 + threadIdx.x;
+  const int p = b * kRedP + threadIdx.x;
+  const int q = (n_chunks + kRedG - 1) / kRedG;
+  const int c0 = threadIdx.y * q, c1 = min(n_chunks, c0 + q);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   if (p < per_chunk) {
-    int c = threadIdx.y;
-    for (; c + 96 < n_chunks; c += 128) {
-      a0 += partial[static_cast<size_t>(c) * per_chunk + p];
-      a1 += partial[static_cast<size_t>(c + 32) * per_chunk + p];
-      a2 += partial[static_cast<size_t>(c + 64) * per_chunk + p];
-      a3 += partial[static_cast<size_t>(c + 96) * per_chunk + p];
+    const float* src = partial + p;
+    int c = c0;
+#pragma unroll 4
+    for (; c + 3 < c1; c += 4) {
+      a0 += src[static_cast<size_t>(c) * per_chunk];
+      a1 += src[static_cast<size_t>(c + 1) * per_chunk];
+      a2 += src[static_cast<size_t>(c + 2) * per_chunk];
+      a3 += src[static_cast<size_t>(c + 3) * per_chunk];
     }
-    for (; c < n_chunks; c += 32) a0 += partial[static_cast<size_t>(c) * per_chunk + p];
+    for (; c < c1; ++c) a0 += src[static_cast<size_t>(c) * per_chunk];
   }
   s_sum[threadIdx.y][threadIdx.x] = (a0 + a1) + (a2 + a3);
   __syncthreads();
   if (threadIdx.y == 0 && p < per_chunk) {
     double t = 0.0;
-    for (int y = 0; y < 32; ++y) t += s_sum[y][threadIdx.x];
+    for (int y = 0; y < kRedG; ++y) t += s_sum[y][threadIdx.x];
     sg.dst[seg][p] = t;
   }
 }
@@ -870,7 +876,7 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
     segs.dst[k] = dst;
     segs.n_chunks[k] = chunks;
     segs.per[k] = per;
-    segs.block_end[k] = (k ? segs.block_end[k - 1] : 0) + div_up(per, 32);
+    segs.block_end[k] = (k ? segs.block_end[k - 1] : 0) + div_up(per, kRedP);
   };
   // hidden width 128 on tcgen05: one fused kernel per hidden layer (data +
   // weight gradient; the output layer folded into the top one, layer 0 into
@@ -913,7 +919,7 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
     }
     add_seg(part_top, grid, H + 1, grad + s.offset(L));
     add_seg(part_0, grid, 3 * H, grad + s.offset(0));
-    reduce_segments_kernel<<<segs.block_end[segs.n - 1], dim3(32, 32), 0, st>>>(segs);
+    reduce_segments_kernel<<<segs.block_end[segs.n - 1], dim3(kRedP, kRedG), 0, st>>>(segs);
     return after_launch(ctx, "reduce_segments_kernel");
   }
   // chunking for the split-M reductions
@@ -1001,7 +1007,7 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
   }
   PACT_TRY_S(after_launch(ctx, "siren_wgrad0_kernel"));
   add_seg(part_0, n_top, 3 * H, grad + s.offset(0));
-  reduce_segments_kernel<<<segs.block_end[segs.n - 1], dim3(32, 32), 0, st>>>(segs);
+  reduce_segments_kernel<<<segs.block_end[segs.n - 1], dim3(kRedP, kRedG), 0, st>>>(segs);
   return after_launch(ctx, "reduce_segments_kernel");
 }
 
