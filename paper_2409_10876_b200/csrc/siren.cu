@@ -724,6 +724,16 @@ bool siren_fused_bwd(const SirenShape& s) {
   return on && s.hidden == 128 && s.layers >= 2 && siren_use_tc(s.hidden);
 }
 
+// Hidden width 256 on the streamed tcgen05 GEMMs (siren_wide.cu);
+// PACT_SIREN_SIMT=1 also forces the SIMT tiles here.
+bool siren_use_wide(int hidden) {
+  static const bool simt = [] {
+    const char* e = std::getenv("PACT_SIREN_SIMT");
+    return e && e[0] == '1';
+  }();
+  return !simt && siren_wide_supported(hidden);
+}
+
 bool siren_use_tc(int hidden) {
   static const bool simt = [] {
     const char* e = std::getenv("PACT_SIREN_SIMT");
@@ -773,6 +783,9 @@ void siren_work_free(SirenWork& w) {
   pool_free(w.idx, w.stream);
   pool_free(w.coords, w.stream);
   pool_free(w.acts, w.stream);
+  pool_free(w.wide_planes, w.stream);
+  w.wide_planes = nullptr;
+  w.wide_planes_floats = 0;
   pool_free(w.dA, w.stream);
   pool_free(w.dB, w.stream);
   pool_free(w.partial, w.stream);
@@ -787,6 +800,25 @@ static Status ensure_partial(SirenWork& w, size_t floats, cudaStream_t stream) {
   PACT_TRY_S(pool_alloc(reinterpret_cast<void**>(&w.partial), sizeof(float) * floats, stream));
   w.stream = stream;
   w.partial_floats = floats;
+  return {};
+}
+
+// W (transposed = false) or W^T planes of every hidden layer into w.wide_planes:
+// layer l (1 .. L-1) at (l - 1) * 2 + transposed planes slots.
+static Status wide_planes(pact_ctx* ctx, const SirenShape& s, const float* theta, SirenWork& w,
+                          bool transposed) {
+  const size_t per = tc_wide_plane_floats();
+  const size_t need = per * 2 * static_cast<size_t>(s.layers - 1);
+  if (w.wide_planes_floats < need) {
+    pool_free(w.wide_planes, w.stream ? w.stream : ctx->stream);
+    w.wide_planes = nullptr;
+    w.wide_planes_floats = 0;
+    PACT_TRY_S(pool_alloc(reinterpret_cast<void**>(&w.wide_planes), sizeof(float) * need, ctx->stream));
+    w.wide_planes_floats = need;
+  }
+  for (int l = 1; l < s.layers; ++l)
+    PACT_TRY_S(tc_wide_planes(ctx, theta + s.offset(l), transposed,
+                              w.wide_planes + per * (2 * (l - 1) + (transposed ? 1 : 0))));
   return {};
 }
 
@@ -814,11 +846,19 @@ Status siren_forward(pact_ctx* ctx, const SirenShape& s, const float* theta, Sir
   siren_first_kernel<<<ctx->num_sms * 8, 256, 0, st>>>(
       w.coords, theta + s.offset(0), theta + s.offset(0) + 2 * H, n, H, w.acts);
   PACT_TRY_S(after_launch(ctx, "siren_first_kernel"));
+  const bool wide = siren_use_wide(H);
+  if (wide) PACT_TRY_S(wide_planes(ctx, s, theta, w, false));
   for (int l = 1; l < L; ++l) {
     const float* W = theta + s.offset(l);
     const float* b = W + static_cast<size_t>(H) * H;
     const float* Ain = w.acts + (l - 1) * stride;
     float* Aout = w.acts + l * stride;
+    if (wide) {
+      PACT_TRY_S(tc_wide_forward_layer(ctx, Ain,
+                                       w.wide_planes + tc_wide_plane_floats() * 2 * (l - 1), b, n,
+                                       w0, Aout));
+      continue;
+    }
     if (siren_use_tc(H)) {
       SirenHead head;
       if (l == L - 1) {  // the output layer rides on the last layer's epilogue
@@ -926,9 +966,13 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
   const int tilesW = (H / 128 > 0 ? H / 128 : 1) * (H / 128 > 0 ? H / 128 : 1);
   const int rows_top = chunk_rows(n, 1, 4 * ctx->num_sms);
   const int n_top = div_up(n, rows_top);
-  const bool use_tc = siren_use_tc(H);
+  const bool use_tc = siren_use_tc(H), wide = siren_use_wide(H);
   int rows_w = chunk_rows(n, tilesW, ctx->num_sms);
   if (use_tc) rows_w = tc_wgrad_rows(ctx, n);
+  if (wide) {
+    rows_w = tc_wide_wgrad_rows(ctx, n);
+    PACT_TRY_S(wide_planes(ctx, s, theta, w, true));  // W^T for the data gradients
+  }
   const int n_w = div_up(n, rows_w);
   // one partial slice per reduction (top, each hidden layer, layer 0), summed
   // by a single segmented launch at the end
@@ -974,22 +1018,28 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
     // weight gradient of layer l
     if (use_tc)
       PACT_TRY_S(tc_wgrad_layer(ctx, H, cur, Aprev, n, rows_w, w0, part, n_w));
+    else if (wide)
+      PACT_TRY_S(tc_wide_wgrad_layer(ctx, cur, Aprev, n, rows_w, w0, part, n_w));
     else if (H == 64)
       siren_wgrad_kernel<64><<<dim3(n_w, 1, 1), NT, 0, st>>>(cur, Aprev, n, H, rows_w, w0, part);
     else
       siren_wgrad_kernel<128><<<dim3(n_w, H / 128, H / 128), NT, 0, st>>>(cur, Aprev, n, H, rows_w,
                                                                          w0, part);
-    if (!use_tc) PACT_TRY_S(after_launch(ctx, "siren_wgrad_kernel"));
+    if (!use_tc && !wide) PACT_TRY_S(after_launch(ctx, "siren_wgrad_kernel"));
     add_seg(part, n_w, static_cast<int>(per_w), grad + s.offset(l));
     // delta to layer l-1
     if (use_tc)
       PACT_TRY_S(tc_dgrad_layer(ctx, H, cur, W, Aprev, n, w0, nxt));
+    else if (wide)
+      PACT_TRY_S(tc_wide_dgrad_layer(ctx, cur,
+                                     w.wide_planes + tc_wide_plane_floats() * (2 * (l - 1) + 1),
+                                     Aprev, n, w0, nxt));
     else if (H == 64)
       siren_dgrad_kernel<64><<<dim3(div_up(n, BM), 1), NT, 0, st>>>(cur, W, Aprev, n, H, w0, nxt);
     else
       siren_dgrad_kernel<128><<<dim3(div_up(n, BM), H / 128), NT, 0, st>>>(cur, W, Aprev, n, H, w0,
                                                                           nxt);
-    if (!use_tc) PACT_TRY_S(after_launch(ctx, "siren_dgrad_kernel"));
+    if (!use_tc && !wide) PACT_TRY_S(after_launch(ctx, "siren_dgrad_kernel"));
     std::swap(cur, nxt);
   }
   switch (H) {

@@ -48,6 +48,8 @@ struct SirenWork {
   size_t partial_floats = 0;
   float* wplanes = nullptr;  // tcgen05 weight planes of the fused forward (siren_chain.cu)
   size_t wplanes_floats = 0;
+  float* wide_planes = nullptr;  // width-256 layers: W and W^T planes per hidden layer (siren_wide.cu)
+  size_t wide_planes_floats = 0;
   cudaStream_t stream = nullptr;  // pool stream of the buffers
 };
 
@@ -114,6 +116,19 @@ struct TcBwdLayer {
   float* part_top = nullptr;  // TOP: [grid][129]
   float* part_0 = nullptr;    // BOTTOM: [grid][384]
 };
+// Hidden width 256 (cfg5) on tcgen05 (siren_wide.cu): per-layer streamed
+// GEMMs with both operands in shared memory.
+bool siren_wide_supported(int hidden);
+bool siren_use_wide(int hidden);
+size_t tc_wide_plane_floats();  // floats of one matrix's hi/lo planes
+Status tc_wide_planes(pact_ctx* ctx, const float* W, bool transposed, float* planes);
+Status tc_wide_forward_layer(pact_ctx* ctx, const float* Ain, const float* planes, const float* b,
+                             int n, float w0, float* Aout);
+Status tc_wide_dgrad_layer(pact_ctx* ctx, const float* dAl, const float* planes_t,
+                           const float* Aprev, int n, float w0, float* dAprev);
+int tc_wide_wgrad_rows(pact_ctx* ctx, int n);
+Status tc_wide_wgrad_layer(pact_ctx* ctx, const float* dAl, const float* Aprev, int n, int rows,
+                           float w0, float* partial, int n_chunks);
 int tc_bwd_grid(pact_ctx* ctx, int n);  // CTAs (= partial rows) of tc_bwd_layer
 Status tc_bwd_layer(pact_ctx* ctx, bool top, bool bottom, const TcBwdLayer& layer);
 
