@@ -36,6 +36,7 @@
 #ifndef CHAIN_EXP
 #define CHAIN_EXP 0
 #endif
+// CHAIN_EXP 3: no activation stores (timing only).
 // CHAIN_EXP 2: store-only timeline of CTA 0 (roles: MMA warp, epilogue warps
 // (q 0, chunk 0) and (q 0, chunk 3)) read by pact_debug_chain_trace.
 #if CHAIN_EXP == 2
@@ -259,6 +260,7 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
     };
     // the box -> acts[l] rows [r0, r0 + 32) (rows >= n clipped by the tensor bounds)
     auto store_box = [&](int l, int r0) {
+      if (CHAIN_EXP == 3) return;  // experiment: no activation stores
       tc::fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
