@@ -9,12 +9,14 @@
 //                                                                              (nfield.hpp:190-230)
 //
 // Forward / dgrad (tc_wide_layer_kernel): 128-pixel tiles, N = 256 output
-// features in one MMA, K streamed in 8 chunks of 32 through a 2-stage ring.
-// A stage holds the A chunk (rows = pixel, 32 K; its hi plane is the input
-// tile itself, written by a TMA tensor load in the SW128 layout -- kind::tf32
+// features in one MMA, K streamed in 16 chunks of 16 through a 4-stage ring
+// (SWIZZLE_64B: 64-B rows, so a stage is 48 KB and four fit; the weight
+// chunks come from L2 for every tile, and a deep ring hides that latency).
+// A stage holds the A chunk (rows = pixel, 16 K; its hi plane is the input
+// tile itself, written by a TMA tensor load in the SW64 layout -- kind::tf32
 // ignores the low 13 mantissa bits; producers add the lo plane, and for the
 // forward first replace hi by sin(w0 a)) and the B chunk (precomputed hi/lo
-// planes of W or W^T, 64 KB, one bulk copy from L2).  Two 256-column TMEM
+// planes of W or W^T, 32 KB, one bulk copy).  Two 256-column TMEM
 // accumulators alternate between tiles so the epilogue (bias or cosine,
 // coalesced float4 row stores) of tile i overlaps the MMAs of tile i + 1.
 //
@@ -37,11 +39,12 @@ namespace {
 
 constexpr int WH = 256;               // hidden width
 constexpr int WT = 128;               // pixels per tile (MMA M)
-constexpr int WKC = 32;               // K per chunk
-constexpr int WNK = WH / WKC;         // 8 K-chunks
-constexpr uint32_t kAPlane = WT * WKC;   // floats of one A plane (16 KB)
-constexpr uint32_t kBPlane = WH * WKC;   // floats of one B plane (32 KB)
-constexpr uint32_t kStage = 2 * kAPlane + 2 * kBPlane;  // 96 KB
+constexpr int WKC = 16;               // K per chunk (one 64-B SW64 row)
+constexpr int WNK = WH / WKC;         // 16 K-chunks
+constexpr int WNS = 4;                // ring stages
+constexpr uint32_t kAPlane = WT * WKC;   // floats of one A plane (8 KB)
+constexpr uint32_t kBPlane = WH * WKC;   // floats of one B plane (16 KB)
+constexpr uint32_t kStage = 2 * kAPlane + 2 * kBPlane;  // 48 KB
 constexpr int kWideThreads = 32 * 18;  // loader, MMA, 8 producer warps, 8 epilogue warps
 
 enum : int { kWideFwd = 0, kWideDgrad = 1 };
@@ -55,7 +58,23 @@ __device__ __forceinline__ uint32_t sa(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// Weight planes [chunk c][hi | lo][row r][32] (SW128) of W (row r = output
+// K-major SWIZZLE_64B: 8-row x 64-B atoms (16 fp32 of K per row), 16-B chunk
+// index XOR (row / 2) % 4, atoms stacked at SBO = 512 B; K step s of 8
+// advances the start address by 32 s bytes.
+__device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1) << 16;            // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(512 >> 4) << 32;     // SBO
+  d |= static_cast<uint64_t>(1) << 46;            // version
+  d |= static_cast<uint64_t>(4) << 61;            // SWIZZLE_64B
+  return d;
+}
+__device__ __forceinline__ int sw64(int row, int k) {
+  return row * 16 + ((((k >> 2) ^ ((row >> 1) & 3))) << 2) + (k & 3);
+}
+
+// Weight planes [chunk c][hi | lo][row r][16] (SW64) of W (row r = output
 // feature, K = input feature) or of W^T (row r = input feature, K = output).
 __global__ void wide_planes_kernel(const float* __restrict__ W, int transposed, float* __restrict__ out) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -66,13 +85,13 @@ __global__ void wide_planes_kernel(const float* __restrict__ W, int transposed, 
   float hi, lo;
   tc::split_tf32(v, hi, lo);
   float* pl = out + static_cast<size_t>(c) * 2 * kBPlane;
-  const int o = r * WKC + (((kk >> 2) ^ (r & 7)) << 2) + (kk & 3);
+  const int o = sw64(r, kk);
   pl[o] = hi;
   pl[kBPlane + o] = lo;
 }
 
 struct WideBars {
-  uint64_t full[2], ready[2], empty[2];
+  uint64_t full[WNS], ready[WNS], empty[WNS];
   uint64_t dfull[2], dfree[2];
   uint32_t tslot;
 };
@@ -84,16 +103,18 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in, const float* _
                      float* __restrict__ Y) {
   extern __shared__ unsigned char smem_dyn[];
   float* st = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) &
-                                       ~static_cast<uintptr_t>(1023));  // [2][kStage]
-  float* s_bias = st + 2 * kStage;                                      // [WH]
+                                       ~static_cast<uintptr_t>(1023));  // [WNS][kStage]
+  float* s_bias = st + WNS * kStage;                                    // [WH]
   __shared__ WideBars sb;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) tc::tmem_alloc<512>(&sb.tslot);
   if (tid == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < WNS; ++i) {
       tc::mbar_init(&sb.full[i], 1);
       tc::mbar_init(&sb.ready[i], 256);
       tc::mbar_init(&sb.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&sb.dfull[i], 1);
       tc::mbar_init(&sb.dfree[i], 256);
     }
@@ -111,11 +132,11 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in, const float* _
   auto tile_m0 = [&](int i) { return (blockIdx.x + i * gridDim.x) * WT; };
 
   if (warp == 0) {
-    // ---- loader: A chunk (TMA box 32 x 128, rows >= n zero) + B chunk ----
+    // ---- loader: A chunk (TMA box 16 x 128, rows >= n zero) + B chunk ----
     if (lane == 0) {
       for (int g = 0; g < n_g; ++g) {
-        const int s = g & 1, i = g / WNK, c = g % WNK;
-        if (g >= 2) tc::mbar_wait_sleep(&sb.empty[s], ((g - 2) >> 1) & 1);
+        const int s = g % WNS, i = g / WNK, c = g % WNK;
+        if (g >= WNS) tc::mbar_wait_sleep(&sb.empty[s], ((g - WNS) / WNS) & 1);
         float* stg = st + s * kStage;
         tc::mbar_expect_tx(&sb.full[s], 4 * (kAPlane + 2 * kBPlane));
         tc::tma_load_2d(stg, &tmap_in, WKC * c, tile_m0(i), &sb.full[s]);
@@ -124,11 +145,11 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in, const float* _
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issue: per chunk 4 K-steps x 3 products, M = 128, N = 256 ----
+    // ---- MMA issue: per chunk 2 K-steps x 3 products, M = 128, N = 256 ----
     constexpr uint32_t idesc = tc::idesc_tf32(WT, WH);
     for (int g = 0; g < n_g; ++g) {
-      const int s = g & 1, i = g / WNK, c = g % WNK;
-      tc::mbar_wait(&sb.ready[s], (g >> 1) & 1);
+      const int s = g % WNS, i = g / WNK, c = g % WNK;
+      tc::mbar_wait(&sb.ready[s], (g / WNS) & 1);
       if (c == 0 && i >= 2) tc::mbar_wait(&sb.dfree[i & 1], ((i - 2) >> 1) & 1);
       tc::fence_after_sync();
       if (tc::elect_one()) {
@@ -137,8 +158,8 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in, const float* _
         const uint32_t d = t0 + WH * (i & 1);
 #pragma unroll
         for (int k = 0; k < WKC / 8; ++k) {
-          const uint64_t dah = tc::smem_desc_sw128(ah + 32 * k), dal = tc::smem_desc_sw128(al + 32 * k);
-          const uint64_t dbh = tc::smem_desc_sw128(bh + 32 * k), dbl = tc::smem_desc_sw128(bl + 32 * k);
+          const uint64_t dah = desc_sw64(ah + 32 * k), dal = desc_sw64(al + 32 * k);
+          const uint64_t dbh = desc_sw64(bh + 32 * k), dbl = desc_sw64(bl + 32 * k);
           tc::mma_tf32(d, dal, dbh, idesc, (c | k) != 0);
           tc::mma_tf32(d, dah, dbl, idesc, 1u);
           tc::mma_tf32(d, dah, dbh, idesc, 1u);
@@ -149,16 +170,16 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in, const float* _
       __syncwarp();
     }
   } else if (warp < 10) {
-    // ---- producers: row p = t / 2, granules 4 h .. 4 h + 3 of the 128-B row ----
+    // ---- producers: row p = t / 2, granules 2 h, 2 h + 1 of the 64-B row ----
     const int t = tid - 64, p = t >> 1, h = t & 1;
     for (int g = 0; g < n_g; ++g) {
-      const int s = g & 1;
-      tc::mbar_wait(&sb.full[s], (g >> 1) & 1);
+      const int s = g % WNS;
+      tc::mbar_wait(&sb.full[s], (g / WNS) & 1);
       float* hi = st + s * kStage;
       float* lo = hi + kAPlane;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int o = p * WKC + (((4 * h + j) ^ (p & 7)) << 2);
+      for (int j = 0; j < 2; ++j) {
+        const int o = p * WKC + (((2 * h + j) ^ ((p >> 1) & 3)) << 2);
         float4 x = *reinterpret_cast<const float4*>(hi + o);
         if (MODE == kWideFwd) {
           // sin(w0 a_{l-1}); rows past n arrive as zeros and stay zero
@@ -366,7 +387,7 @@ tc_wide_wgrad_kernel(const float* __restrict__ dA, const float* __restrict__ Apr
   if (warp == 0) tc::tmem_free<512>(t0);
 }
 
-constexpr size_t kWideSmem = 1024 + sizeof(float) * (2 * kStage + WH);
+constexpr size_t kWideSmem = 1024 + sizeof(float) * (WNS * kStage + WH);
 constexpr size_t kWgradSmemW = 1024 + sizeof(float) * (kWSlot + 2 * kRawW);
 
 PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
@@ -398,7 +419,7 @@ Status launch_wide(pact_ctx* ctx, const float* in, const float* planes, const fl
   const cuuint64_t strides[1] = {sizeof(float) * WH};
   const cuuint32_t box[2] = {WKC, WT}, estr[2] = {1, 1};
   if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(in), dims, strides, box,
-             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return internal_error("tc_wide_layer: tensor map encoding failed");
   const int grid = std::max(1, std::min(ctx->num_sms, div_up(n, WT)));
