@@ -174,21 +174,22 @@ def cfg2_case(R):
          image=step["image"].astype(np.float32), H24=H24.astype(np.complex64))
 
 
-def cfg2_h128_case(R):
-    """cfg2's geometry and signals (the cfg2_step fixture) with cfg3's network,
-    SIREN 2 -> 128 x 4 -> 1: one forward + gradient evaluation through the
-    reference, for the fused tcgen05 SIREN kernels inside the training step."""
+def cfg2_wide_case(R, hidden, name):
+    """cfg2's geometry and signals (the cfg2_step fixture) with a wider network,
+    SIREN 2 -> hidden x 4 -> 1 (128: cfg3's, 256: cfg5's): one forward +
+    gradient evaluation through the reference, for the tcgen05 SIREN kernels
+    inside the training step."""
     from dataclasses import replace
 
     from paper_2409_10876_b200.api import SirenSpec
 
-    w = replace(wl.cfg2(), hidden=128, sine_layers=4)
+    w = replace(wl.cfg2(), hidden=hidden, sine_layers=4)
     sig = np.load(os.path.join(HERE, "cfg2_step.npz"))["sig"].astype(np.float64)
     cfg = wl.train_config(w)
     spec = SirenSpec(cfg.hidden, cfg.sine_layers, cfg.omega0, cfg.out_scale, w.v0)
     theta = R.init_siren(0, spec, spec.param_count())
     step = R.nf_step(sig, w.ring, w.meta, w.grid, w.mask, cfg, theta, want_image=False)
-    save("cfg2_h128_step", theta=theta, sos=step["sos"].astype(np.float32), w=step["w"],
+    save(name, theta=theta, sos=step["sos"].astype(np.float32), w=step["w"],
          dw=step["dw"], data_term=np.array(step["data_term"]), tv_term=np.array(step["tv_term"]),
          grad_theta=step["grad_theta"])
 
@@ -217,7 +218,7 @@ def main():
     R = ref()
     if R is None:
         sys.exit("oracle/_ref/libpact_ref.so missing: make -C oracle ref")
-    which = sys.argv[1:] or ["das", "dual", "metrics", "small", "cfg2", "cfg2_h128"]
+    which = sys.argv[1:] or ["das", "dual", "metrics", "small", "cfg2", "cfg2_h128", "cfg2_h256"]
     if "das" in which:
         das_cases(R)
     if "dual" in which:
@@ -229,7 +230,9 @@ def main():
     if "cfg2" in which:
         cfg2_case(R)
     if "cfg2_h128" in which:
-        cfg2_h128_case(R)
+        cfg2_wide_case(R, 128, "cfg2_h128_step")
+    if "cfg2_h256" in which:
+        cfg2_wide_case(R, 256, "cfg2_h256_step")
 
 
 if __name__ == "__main__":

@@ -97,15 +97,18 @@ def test_simulated_signals_match_reference_simulator(ctx, G, W):
     assert err <= 1e-4
 
 
-def test_iteration_h128_network(ctx, G, W):
-    """cfg2's geometry and signals with cfg3's network (SIREN 2 -> 128 x 4 -> 1):
-    the training step runs the fused tcgen05 forward (siren_chain.cu) and the
-    fused per-layer backward (siren_bwd.cu) inside its CUDA graph; reference
-    values from tests/golden/cfg2_h128_step.npz (one nf_step of oracle/_ref)."""
+@pytest.mark.parametrize("hidden,fixture", [(128, "cfg2_h128_step"), (256, "cfg2_h256_step")])
+def test_iteration_wide_network(ctx, G, W, hidden, fixture):
+    """cfg2's geometry and signals with cfg3's network (SIREN 2 -> 128 x 4 -> 1:
+    the fused tcgen05 forward of siren_chain.cu and the fused per-layer
+    backward of siren_bwd.cu) or cfg5's (2 -> 256 x 4 -> 1: the streamed
+    tcgen05 GEMMs of siren_wide.cu) inside the training step's CUDA graph;
+    reference values from tests/golden/<fixture>.npz (one nf_step of
+    oracle/_ref)."""
     from dataclasses import replace
 
-    H = gu.load("cfg2_h128_step")
-    w = replace(W, hidden=128, sine_layers=4)
+    H = gu.load(fixture)
+    w = replace(W, hidden=hidden, sine_layers=4)
     cfg = wl.train_config(w, seed=0, epochs=1, steps_per_epoch=1)
     tr = Trainer(ctx, torch.as_tensor(G["sig"]).cuda(), w.ring, w.meta, w.grid, w.mask, cfg)
     tr.step(1)
@@ -117,6 +120,6 @@ def test_iteration_h128_network(ctx, G, W):
     assert rel_l2(tr.read(4, (n, w.n_angles), np.float32), H["dw"]) <= 1e-3
     g = tr.read(6, (tr.n_params,), np.float64)
     err = rel_l2(g, H["grad_theta"])
-    print("cfg2 / H=128 grad rel L2", err)
+    print(f"cfg2 / H={hidden} grad rel L2", err)
     assert err <= 1e-3
     tr.close()
