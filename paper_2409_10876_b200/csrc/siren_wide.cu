@@ -8,7 +8,9 @@
 //   wgrad    gW_l[o][k] += sum_p dA_l[p][o] sin(w0 a_{l-1}[p][k]),  gb_l[o] += sum_p dA_l[p][o]
 //                                                                              (nfield.hpp:190-230)
 //
-// Forward / dgrad (tc_wide_layer_kernel): 128-pixel tiles, N = 256 output
+// Forward / dgrad (tc_wide_layer_kernel, 2-CTA clusters: the pair streams
+// the same weight chunks, each CTA loads one plane and multicasts it into
+// both, halving the weight traffic from L2): 128-pixel tiles, N = 256 output
 // features in one MMA, K streamed in 16 chunks of 16 through a 4-stage ring
 // (SWIZZLE_64B: 64-B rows, so a stage is 48 KB and four fit; the weight
 // chunks come from L2 for every tile, and a deep ring hides that latency).
@@ -56,6 +58,46 @@ __device__ __forceinline__ float red2pi_w(float x) {
 
 __device__ __forceinline__ uint32_t sa(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---- 2-CTA clusters: the two CTAs of a pair stream the same weight chunks,
+// so each loads one of the chunk's two planes and multicasts it into both
+// (half the L2 traffic for the weights) ----
+constexpr int kPair = 2;
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t n_clusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// bulk copy global -> the same smem offset in every CTA of `mask`, completing
+// on the mbarrier at the same offset in each
+__device__ __forceinline__ void bulk_load_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                             uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
+          sa(dst)),
+      "l"(src), "r"(bytes), "r"(sa(bar)), "h"(mask)
+      : "memory");
+}
+// all prior MMAs of this thread arrive on `bar` in every CTA of `mask`
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   sa(bar)),
+               "h"(mask)
+               : "memory");
 }
 
 // K-major SWIZZLE_64B: 8-row x 64-B atoms (16 fp32 of K per row), 16-B chunk
@@ -112,7 +154,7 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in, const float* _
     for (int i = 0; i < WNS; ++i) {
       tc::mbar_init(&sb.full[i], 1);
       tc::mbar_init(&sb.ready[i], 256);
-      tc::mbar_init(&sb.empty[i], 1);
+      tc::mbar_init(&sb.empty[i], kPair);  // both CTAs' MMAs are done with the stage
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&sb.dfull[i], 1);
@@ -124,12 +166,17 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in, const float* _
     for (int i = tid; i < WH; i += kWideThreads) s_bias[i] = bias[i];
   tc::fence_before_sync();
   __syncthreads();
+  cluster_sync_all();  // the peer's barriers exist before any multicast reaches them
   tc::fence_after_sync();
   const uint32_t t0 = sb.tslot;
-  const int n_tiles = (n + WT - 1) / WT;
-  const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // tiles go to the pair together: pair step i covers tiles 2 (cid + i ncl) + rank
+  // (a tile past the end loads zeros and stores nothing; both CTAs run the
+  // same number of steps, as the shared weight chunks require)
+  const uint32_t rank = cluster_rank(), cid = cluster_id_x(), ncl = n_clusters_x();
+  const int n_tiles = (n + WT - 1) / WT, n_pairs = (n_tiles + 1) / 2;
+  const int my_tiles = static_cast<int>(cid) < n_pairs ? (n_pairs - 1 - static_cast<int>(cid)) / static_cast<int>(ncl) + 1 : 0;
   const int n_g = my_tiles * WNK;  // (tile, K-chunk) steps
-  auto tile_m0 = [&](int i) { return (blockIdx.x + i * gridDim.x) * WT; };
+  auto tile_m0 = [&](int i) { return (2 * (static_cast<int>(cid) + i * static_cast<int>(ncl)) + static_cast<int>(rank)) * WT; };
 
   if (warp == 0) {
     // ---- loader: A chunk (TMA box 16 x 128, rows >= n zero) + B chunk ----
@@ -140,8 +187,10 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in, const float* _
         float* stg = st + s * kStage;
         tc::mbar_expect_tx(&sb.full[s], 4 * (kAPlane + 2 * kBPlane));
         tc::tma_load_2d(stg, &tmap_in, WKC * c, tile_m0(i), &sb.full[s]);
-        tc::bulk_load(stg + 2 * kAPlane, planes + static_cast<size_t>(c) * 2 * kBPlane,
-                      4 * 2 * kBPlane, &sb.full[s]);
+        // this CTA's plane of the weight chunk (rank 0: hi, rank 1: lo), into both
+        bulk_load_mc(stg + 2 * kAPlane + rank * kBPlane,
+                     planes + static_cast<size_t>(c) * 2 * kBPlane + rank * kBPlane, 4 * kBPlane,
+                     &sb.full[s], 0x3);
       }
     }
   } else if (warp == 1) {
@@ -164,7 +213,7 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in, const float* _
           tc::mma_tf32(d, dah, dbl, idesc, 1u);
           tc::mma_tf32(d, dah, dbh, idesc, 1u);
         }
-        tc::mma_commit(&sb.empty[s]);
+        mma_commit_mc(&sb.empty[s], 0x3);  // frees the stage in both CTAs
         if (c == WNK - 1) tc::mma_commit(&sb.dfull[i & 1]);
       }
       __syncwarp();
@@ -239,6 +288,7 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in, const float* _
   }
   tc::fence_before_sync();
   __syncthreads();
+  cluster_sync_all();  // no multicast copy or commit still targets this CTA
   if (warp == 0) tc::tmem_free<512>(t0);
 }
 
@@ -422,9 +472,21 @@ Status launch_wide(pact_ctx* ctx, const float* in, const float* planes, const fl
              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return internal_error("tc_wide_layer: tensor map encoding failed");
-  const int grid = std::max(1, std::min(ctx->num_sms, div_up(n, WT)));
-  tc_wide_layer_kernel<MODE><<<grid, kWideThreads, kWideSmem, ctx->stream>>>(tmap, planes, bias, Aprev,
-                                                                             n, w0, Y);
+  // 2-CTA clusters (the pair shares the weight chunks by multicast)
+  const int pairs = std::max(1, std::min(ctx->num_sms / kPair, div_up(div_up(n, WT), kPair)));
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(kPair * pairs);
+  lc.blockDim = dim3(kWideThreads);
+  lc.dynamicSmemBytes = kWideSmem;
+  lc.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kPair;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  PACT_CUDA_S(cudaLaunchKernelEx(&lc, tc_wide_layer_kernel<MODE>, tmap, planes, bias, Aprev, n, w0, Y));
   return after_launch(ctx, MODE == kWideFwd ? "tc_wide_layer_kernel<forward>"
                                             : "tc_wide_layer_kernel<dgrad>");
 }
