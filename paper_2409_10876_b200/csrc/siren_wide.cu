@@ -36,6 +36,12 @@
 #include "siren.cuh"
 #include "tc.cuh"
 
+// WIDE_EXP (timing experiments only, wrong results): 1 = the layer
+// epilogue neither loads a_{l-1} nor stores its output.
+#ifndef WIDE_EXP
+#define WIDE_EXP 0
+#endif
+
 namespace pactgpu {
 namespace {
 
@@ -140,13 +146,15 @@ struct WideBars {
 
 template <int MODE>
 __global__ void __launch_bounds__(kWideThreads, 1)
-tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in, const float* __restrict__ planes,
+tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in,
+                     const __grid_constant__ CUtensorMap tmap_out, const float* __restrict__ planes,
                      const float* __restrict__ bias, const float* __restrict__ Aprev, int n, float w0,
                      float* __restrict__ Y) {
   extern __shared__ unsigned char smem_dyn[];
   float* st = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) &
                                        ~static_cast<uintptr_t>(1023));  // [WNS][kStage]
   float* s_bias = st + WNS * kStage;                                    // [WH]
+  float* s_box = s_bias + WH;  // [8 epilogue warps][32 x 32] SW128 output boxes (1024-aligned)
   __shared__ WideBars sb;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) tc::tmem_alloc<512>(&sb.tslot);
@@ -247,10 +255,14 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in, const float* _
       tc::mbar_arrive(&sb.ready[s]);
     }
   } else {
-    // ---- epilogue: lane = pixel (quarter warp % 4), half ch of the 256 columns ----
+    // ---- epilogue: lane = pixel (quarter warp % 4), half ch of the 256 columns;
+    // each 32 x 32 output block goes through this warp's SW128 box and one
+    // TMA tensor store (coalesced; rows >= n clipped by the tensor bounds) ----
     const int e = warp - 10, q = warp & 3, ch = e >> 2;
     const int px = 32 * q + lane;
     const uint32_t lb = t0 + (static_cast<uint32_t>(32 * q) << 16);
+    float* box = s_box + e * 32 * 32;
+    uint32_t nst = 0;
     for (int i = 0; i < my_tiles; ++i) {
       const int m = tile_m0(i) + px;
       const bool valid = m < n;
@@ -263,10 +275,16 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in, const float* _
         float4 av[8];
         if (MODE == kWideDgrad) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) av[j] = reinterpret_cast<const float4*>(Aprev + row + col)[j];
+          for (int j = 0; j < 8; ++j)
+            av[j] = WIDE_EXP == 1 ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                  : reinterpret_cast<const float4*>(Aprev + row + col)[j];
         }
         float v[32];
         tc::tmem_ld32(lb + WH * (i & 1) + col, v);
+        if (nst > 0) {  // the box's previous store has read it
+          if (lane == 0) tc::bulk_wait_read<0>();
+          __syncwarp();
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           float4 o;
@@ -279,12 +297,20 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in, const float* _
                             v[4 * j + 2] * (w0 * __cosf(red2pi_w(w0 * av[j].z))),
                             v[4 * j + 3] * (w0 * __cosf(red2pi_w(w0 * av[j].w))));
           }
-          if (valid) reinterpret_cast<float4*>(Y + row + col)[j] = o;
+          *reinterpret_cast<float4*>(box + lane * 32 + ((j ^ (lane & 7)) << 2)) = o;
         }
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0 && WIDE_EXP != 1) {
+          tc::tma_store_2d(&tmap_out, box, col, tile_m0(i) + 32 * q);
+          tc::bulk_commit();
+        }
+        ++nst;
       }
       tc::fence_before_sync();
       tc::mbar_arrive(&sb.dfree[i & 1]);
     }
+    if (lane == 0) tc::bulk_wait_all();  // the stores are complete before exit
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -437,7 +463,7 @@ tc_wide_wgrad_kernel(const float* __restrict__ dA, const float* __restrict__ Apr
   if (warp == 0) tc::tmem_free<512>(t0);
 }
 
-constexpr size_t kWideSmem = 1024 + sizeof(float) * (WNS * kStage + WH);
+constexpr size_t kWideSmem = 1024 + sizeof(float) * (WNS * kStage + WH + 8 * 32 * 32);
 constexpr size_t kWgradSmemW = 1024 + sizeof(float) * (kWSlot + 2 * kRawW);
 
 PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
@@ -472,6 +498,12 @@ Status launch_wide(pact_ctx* ctx, const float* in, const float* planes, const fl
              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return internal_error("tc_wide_layer: tensor map encoding failed");
+  CUtensorMap tmap_out;
+  const cuuint32_t obox[2] = {32, 32};
+  if (encode(&tmap_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Y, dims, strides, obox, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return internal_error("tc_wide_layer: output tensor map encoding failed");
   // 2-CTA clusters (the pair shares the weight chunks by multicast)
   const int pairs = std::max(1, std::min(ctx->num_sms / kPair, div_up(div_up(n, WT), kPair)));
   cudaLaunchConfig_t lc{};
@@ -486,7 +518,8 @@ Status launch_wide(pact_ctx* ctx, const float* in, const float* planes, const fl
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  PACT_CUDA_S(cudaLaunchKernelEx(&lc, tc_wide_layer_kernel<MODE>, tmap, planes, bias, Aprev, n, w0, Y));
+  PACT_CUDA_S(cudaLaunchKernelEx(&lc, tc_wide_layer_kernel<MODE>, tmap, tmap_out, planes, bias, Aprev, n,
+                                 w0, Y));
   return after_launch(ctx, MODE == kWideFwd ? "tc_wide_layer_kernel<forward>"
                                             : "tc_wide_layer_kernel<dgrad>");
 }

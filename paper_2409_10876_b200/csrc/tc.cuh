@@ -215,6 +215,13 @@ __device__ __forceinline__ void tma_load_2d(void* sdst, const void* tmap, int c0
       "l"(tmap), "r"(c0), "r"(c1), "r"(b)
       : "memory");
 }
+// TMA tensor store of one smem box to a 2-D tensor at (c0, c1) (bulk group).
+__device__ __forceinline__ void tma_store_2d(const void* tmap, const void* ssrc, int c0, int c1) {
+  uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(ssrc));
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
 // TMA tensor store of one smem box to a 3-D tensor at (c0, c1, c2) (bulk group).
 __device__ __forceinline__ void tma_store_3d(const void* tmap, const void* ssrc, int c0, int c1,
                                              int c2) {
