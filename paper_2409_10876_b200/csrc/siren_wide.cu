@@ -141,13 +141,15 @@ __global__ void wide_planes_kernel(const float* __restrict__ W, int transposed, 
 struct WideBars {
   uint64_t full[WNS], ready[WNS], empty[WNS];
   uint64_t dfull[2], dfree[2];
+  uint64_t abox[8];  // dgrad: a_{l-1} block landed in epilogue warp e's box
   uint32_t tslot;
 };
 
 template <int MODE>
 __global__ void __launch_bounds__(kWideThreads, 1)
 tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in,
-                     const __grid_constant__ CUtensorMap tmap_out, const float* __restrict__ planes,
+                     const __grid_constant__ CUtensorMap tmap_out,
+                     const __grid_constant__ CUtensorMap tmap_prev, const float* __restrict__ planes,
                      const float* __restrict__ bias, const float* __restrict__ Aprev, int n, float w0,
                      float* __restrict__ Y) {
   extern __shared__ unsigned char smem_dyn[];
@@ -168,6 +170,7 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in,
       tc::mbar_init(&sb.dfull[i], 1);
       tc::mbar_init(&sb.dfree[i], 256);
     }
+    for (int i = 0; i < 8; ++i) tc::mbar_init(&sb.abox[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (MODE == kWideFwd)
@@ -257,52 +260,51 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in,
   } else {
     // ---- epilogue: lane = pixel (quarter warp % 4), half ch of the 256 columns;
     // each 32 x 32 output block goes through this warp's SW128 box and one
-    // TMA tensor store (coalesced; rows >= n clipped by the tensor bounds) ----
+    // TMA tensor store (coalesced; rows >= n clipped by the tensor bounds).
+    // The data gradient first TMA-loads the matching a_{l-1} block into the
+    // box and overwrites it in place with the result ----
     const int e = warp - 10, q = warp & 3, ch = e >> 2;
-    const int px = 32 * q + lane;
     const uint32_t lb = t0 + (static_cast<uint32_t>(32 * q) << 16);
     float* box = s_box + e * 32 * 32;
     uint32_t nst = 0;
     for (int i = 0; i < my_tiles; ++i) {
-      const int m = tile_m0(i) + px;
-      const bool valid = m < n;
-      const size_t row = static_cast<size_t>(valid ? m : 0) * WH;
+      const int r0 = tile_m0(i) + 32 * q;  // this warp's 32 rows
       tc::mbar_wait(&sb.dfull[i & 1], (i >> 1) & 1);
       tc::fence_after_sync();
 #pragma unroll 1
       for (int cc = 0; cc < 4; ++cc) {
         const int col = 128 * ch + 32 * cc;
-        float4 av[8];
-        if (MODE == kWideDgrad) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            av[j] = WIDE_EXP == 1 ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                  : reinterpret_cast<const float4*>(Aprev + row + col)[j];
-        }
-        float v[32];
-        tc::tmem_ld32(lb + WH * (i & 1) + col, v);
         if (nst > 0) {  // the box's previous store has read it
           if (lane == 0) tc::bulk_wait_read<0>();
           __syncwarp();
         }
+        if (MODE == kWideDgrad && lane == 0) {
+          tc::mbar_expect_tx(&sb.abox[e], 32 * 32 * 4);
+          tc::tma_load_2d(box, &tmap_prev, col, r0, &sb.abox[e]);
+        }
+        float v[32];
+        tc::tmem_ld32(lb + WH * (i & 1) + col, v);
+        if (MODE == kWideDgrad) tc::mbar_wait(&sb.abox[e], nst & 1);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
+          float* bp = box + lane * 32 + ((j ^ (lane & 7)) << 2);
           float4 o;
           if (MODE == kWideFwd) {
             o = make_float4(v[4 * j] + s_bias[col + 4 * j], v[4 * j + 1] + s_bias[col + 4 * j + 1],
                             v[4 * j + 2] + s_bias[col + 4 * j + 2], v[4 * j + 3] + s_bias[col + 4 * j + 3]);
           } else {
-            o = make_float4(v[4 * j] * (w0 * __cosf(red2pi_w(w0 * av[j].x))),
-                            v[4 * j + 1] * (w0 * __cosf(red2pi_w(w0 * av[j].y))),
-                            v[4 * j + 2] * (w0 * __cosf(red2pi_w(w0 * av[j].z))),
-                            v[4 * j + 3] * (w0 * __cosf(red2pi_w(w0 * av[j].w))));
+            const float4 av = *reinterpret_cast<const float4*>(bp);
+            o = make_float4(v[4 * j] * (w0 * __cosf(red2pi_w(w0 * av.x))),
+                            v[4 * j + 1] * (w0 * __cosf(red2pi_w(w0 * av.y))),
+                            v[4 * j + 2] * (w0 * __cosf(red2pi_w(w0 * av.z))),
+                            v[4 * j + 3] * (w0 * __cosf(red2pi_w(w0 * av.w))));
           }
-          *reinterpret_cast<float4*>(box + lane * 32 + ((j ^ (lane & 7)) << 2)) = o;
+          *reinterpret_cast<float4*>(bp) = o;
         }
         tc::fence_proxy_async();
         __syncwarp();
         if (lane == 0 && WIDE_EXP != 1) {
-          tc::tma_store_2d(&tmap_out, box, col, tile_m0(i) + 32 * q);
+          tc::tma_store_2d(&tmap_out, box, col, r0);
           tc::bulk_commit();
         }
         ++nst;
@@ -498,12 +500,18 @@ Status launch_wide(pact_ctx* ctx, const float* in, const float* planes, const fl
              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return internal_error("tc_wide_layer: tensor map encoding failed");
-  CUtensorMap tmap_out;
+  CUtensorMap tmap_out, tmap_prev;
   const cuuint32_t obox[2] = {32, 32};
   if (encode(&tmap_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Y, dims, strides, obox, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return internal_error("tc_wide_layer: output tensor map encoding failed");
+  tmap_prev = tmap_out;  // forward: unused
+  if (MODE == kWideDgrad &&
+      encode(&tmap_prev, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(Aprev), dims, strides,
+             obox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return internal_error("tc_wide_layer: a_{l-1} tensor map encoding failed");
   // 2-CTA clusters (the pair shares the weight chunks by multicast)
   const int pairs = std::max(1, std::min(ctx->num_sms / kPair, div_up(div_up(n, WT), kPair)));
   cudaLaunchConfig_t lc{};
@@ -518,8 +526,8 @@ Status launch_wide(pact_ctx* ctx, const float* in, const float* planes, const fl
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  PACT_CUDA_S(cudaLaunchKernelEx(&lc, tc_wide_layer_kernel<MODE>, tmap, tmap_out, planes, bias, Aprev, n,
-                                 w0, Y));
+  PACT_CUDA_S(cudaLaunchKernelEx(&lc, tc_wide_layer_kernel<MODE>, tmap, tmap_out, tmap_prev, planes, bias,
+                                 Aprev, n, w0, Y));
   return after_launch(ctx, MODE == kWideFwd ? "tc_wide_layer_kernel<forward>"
                                             : "tc_wide_layer_kernel<dgrad>");
 }
