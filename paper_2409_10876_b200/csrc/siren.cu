@@ -943,6 +943,7 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
       a.gmask = gmask;
       a.idx = w.idx;
       a.wL = theta + s.offset(L);
+      a.gpx = w.dA;  // free until the middle layer writes dA_{L-2} into it
       a.coords = w.coords;
       a.W0 = theta + s.offset(0);
       a.b0 = a.W0 + 2 * H;

@@ -106,6 +106,7 @@ struct TcBwdLayer {
   const float* gmask = nullptr;  // TOP
   const int* idx = nullptr;      // TOP
   const float* wL = nullptr;     // TOP
+  float* gpx = nullptr;          // TOP: scratch for g s per masked pixel [n]
   const float2* coords = nullptr;  // BOTTOM
   const float* W0 = nullptr;       // BOTTOM: layer 0 (a_0 is recomputed, not read)
   const float* b0 = nullptr;

@@ -112,6 +112,7 @@ struct BwdArgs {
   const float* gmask;   // TOP: per-masked-pixel gradient (may be null)
   const int* idx;       // TOP: masked pixel -> raster index
   const float* wL;      // TOP: head weights [128]
+  const float* gpx;     // TOP: g s per masked pixel [n] (gather_g_kernel)
   const float2* coords; // BOTTOM
   const float* W0;      // BOTTOM: layer 0 [128][2], b0 [128] (a_0 = W_0 c + b_0)
   const float* b0;
@@ -153,6 +154,18 @@ __device__ __forceinline__ uint32_t saddr_b(const void* p) {
 // SW128 K-major float offset of (row, k) in a plane of 128-B rows (32 fp32 of K)
 __device__ __forceinline__ uint32_t sw128(int row, int k) {
   return static_cast<uint32_t>(row * 32 + ((((k >> 2) ^ (row & 7))) << 2) + (k & 3));
+}
+
+// g s per masked pixel (the output layer's input gradient, nfield.hpp:194-197):
+// the gather through the pixel index happens once here, not per tile.
+__global__ void gather_g_kernel(const double* __restrict__ gv, const float* __restrict__ gmask,
+                                const int* __restrict__ idx, int n, float scale, float* __restrict__ out) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  float gg = 0.f;
+  if (gv) gg += static_cast<float>(gv[idx[m]]);
+  if (gmask) gg += gmask[m];
+  out[m] = gg * scale;
 }
 
 template <int MODE>
@@ -265,14 +278,11 @@ tc_bwd_kernel(BwdArgs a, const __grid_constant__ CUtensorMap tmap_x) {
     const int q = warp & 3, h = warp >> 2, j = 32 * q + lane, pb = HP * h;
     const float wlj = TOP ? a.wL[j] : 0.f;
     float bacc = 0.f, hacc = 0.f, gbacc = 0.f;
-    // TOP: lane t < 16 holds g of pixel pb + t of the tile (shuffled when used)
+    // TOP: lane t < 16 holds g s of pixel pb + t of the tile (shuffled when
+    // used), from the compact per-pixel array (one coalesced load)
     auto load_g = [&](int i) {
       const int m = tile_m0(i) + pb + (lane & (HP - 1));
-      const int mm = min(m, n - 1);
-      float gg = 0.f;
-      if (a.gv) gg += static_cast<float>(a.gv[a.idx[mm]]);
-      if (a.gmask) gg += a.gmask[mm];
-      return m < n ? gg * a.out_scale : 0.f;
+      return m < n ? a.gpx[m] : 0.f;
     };
     float gnext = (TOP && my_tiles > 0) ? load_g(0) : 0.f;
     for (int i = 0; i < my_tiles; ++i) {
@@ -306,6 +316,7 @@ tc_bwd_kernel(BwdArgs a, const __grid_constant__ CUtensorMap tmap_x) {
         bacc += v;
         tc::split_tf32_trunc(v, hi[t], lo[t]);
       }
+      BTRACE(tid == 0, 14, i);
       // dA^T into TMEM first (the weight gradient's A: lane = j, column =
       // pixel; the critical path) once the previous weight gradient is done
       if (i >= 1 && BWD_EXP != 1) tc::mbar_wait(&sb.tfree, (i - 1) & 1);
@@ -611,6 +622,13 @@ Status tc_bwd_layer(pact_ctx* ctx, bool top, bool bottom, const TcBwdLayer& L) {
   a.gmask = L.gmask;
   a.idx = L.idx;
   a.wL = L.wL;
+  a.gpx = L.gpx;
+  if (top) {
+    if (!L.gpx) return internal_error("tc_bwd_layer: top layer needs the g scratch");
+    gather_g_kernel<<<div_up(L.n, 256), 256, 0, ctx->stream>>>(L.gv, L.gmask, L.idx, L.n, L.out_scale,
+                                                              L.gpx);
+    PACT_TRY_S(after_launch(ctx, "gather_g_kernel"));
+  }
   a.coords = L.coords;
   a.W0 = L.W0;
   a.b0 = L.b0;

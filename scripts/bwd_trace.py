@@ -32,7 +32,7 @@ L.pact_debug_bwd_trace(buf.ctypes.data, 1)
 ev = buf.reshape(16, 512).astype(np.int64)
 names = {1: "D start", 2: "D gfree", 3: "D tfree", 4: "D tready>", 5: "Z rfull", 6: "Z wfree",
          7: "Z zready>", 8: "M w-ready", 9: "M g-ready", 10: "E dfull", 11: "Z stored", 12: "D loaded",
-         13: "D stored"}
+         13: "D stored", 14: "D computed"}
 K = sorted(names)
 t0 = ev[ev > 0].min()
 n = int((ev[1] > 0).sum())
