@@ -83,10 +83,10 @@ namespace {
 constexpr int BH = 128;                 // hidden width
 constexpr int BT = 32;                  // pixels per tile
 #ifndef BWD_ND
-#define BWD_ND 3
+#define BWD_ND 4
 #endif
 #ifndef BWD_NZ
-#define BWD_NZ 2
+#define BWD_NZ 1
 #endif
 #ifndef BWD_NR
 #define BWD_NR 3
