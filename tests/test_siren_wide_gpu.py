@@ -53,3 +53,25 @@ def test_siren_backward_h256(ctx, width, height, layers, seed):
             e = rel_l2(got[blk], want[blk])
             assert e <= 1e-3, (l, e)
         off += rows * cols + rows
+
+
+@pytest.mark.parametrize("hidden", [128, 256])
+@pytest.mark.parametrize("width,height,layers", [(13, 11, 2), (13, 11, 4), (7, 5, 3)])
+def test_siren_tiny_masks(ctx, hidden, width, height, layers):
+    """Masks smaller than one tile (fewer pixels than a 32- or 128-pixel tile,
+    a single CTA or a single 2-CTA cluster with an empty partner tile): the
+    tensor-core paths still match the oracle and terminate."""
+    grid = GridSpec(width, height, 1e-4, -0.5e-4 * width, -0.5e-4 * height)
+    mask = CircularMask(0.0, 0.0, 0.45e-4 * max(width, height))
+    spec = SirenSpec(hidden, layers, 30.0, 100.0, 1500.0)
+    theta = init_siren(7, spec)
+    idx, _ = masked_pixels(grid, mask)
+    assert 0 < len(idx) < 128
+    _, dev = ctx.render_sos(spec, torch.as_tensor(theta), grid, mask)
+    want = orc().render_sos(spec, theta.astype(np.float32).astype(np.float64), grid, mask)
+    assert rel_l2(dev.double().cpu().numpy(), want - spec.v0) <= 1e-5
+    g = np.random.default_rng(3).standard_normal(len(idx)).astype(np.float32)
+    got = ctx.siren_backward(spec, torch.as_tensor(theta), grid, mask, torch.as_tensor(g)).cpu().numpy()
+    want = orc().backprop_sos(spec, theta.astype(np.float32).astype(np.float64), grid, mask,
+                              g.astype(np.float64))
+    assert rel_l2(got, want) <= 1e-3
