@@ -34,6 +34,15 @@
 #ifndef RAY_EXP
 #define RAY_EXP 0
 #endif
+// steps in flight per thread in the interior loops (texture gathers issued
+// back to back before their results are used)
+#ifndef RAY_FWD_UNROLL
+#define RAY_FWD_UNROLL 8
+#endif
+#ifndef RAY_BWD_BATCH
+#define RAY_BWD_BATCH 4
+#endif
+constexpr int kRayFwdUnroll = RAY_FWD_UNROLL;
 #define RAY_NO_INT_ATOM (RAY_EXP == 1 || RAY_EXP == 6)
 #define RAY_NO_LINE_ATOM (RAY_EXP == 5 || RAY_EXP == 6)
 
@@ -468,7 +477,7 @@ __global__ void __launch_bounds__(256) wavefront_plan_kernel(RayArgs a) {
     const int lo = item.y, hi = item.z, kind = item_kind(item.w);
     float acc = 0.f;
     if (kind == kItemInterior) {
-#pragma unroll 4
+#pragma unroll kRayFwdUnroll
       for (int i = lo; i < hi; ++i) {
         float ax, ay;
         int ix, iy;
@@ -531,14 +540,15 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
     const float gscale = static_cast<float>(static_cast<double>(gr) * rr.dl * a.v0);
     const int lo = item.y, hi = item.z, kind = item_kind(item.w);
     if (kind == kItemInterior) {
-      // gathers issued four steps at a time, then the carries
+      // gathers issued RAY_BWD_BATCH steps at a time, then the carries
       CellAcc cell;
-      for (int i = lo; i < hi; i += 4) {
-        float4 gt[4];
-        float ax[4], ay[4];
-        int ix[4], iy[4];
+      constexpr int NB = RAY_BWD_BATCH;
+      for (int i = lo; i < hi; i += NB) {
+        float4 gt[NB];
+        float ax[NB], ay[NB];
+        int ix[NB], iy[NB];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < NB; ++u) {
           const float k = static_cast<float>(min(i + u, hi - 1));
           const float fx = fmaf(k, rr.dfx, rr.fxs), fy = fmaf(k, rr.dfy, rr.fys);
           ix[u] = min(static_cast<int>(fx), W - 2);
@@ -548,7 +558,7 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
           gt[u] = tex2Dgather<float4>(a.tex, ix[u] + 1.f, iy[u] + 1.f, 0);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < NB; ++u) {
           if (i + u < hi) {
             // gather order: w=(ix,iy) z=(ix+1,iy) x=(ix,iy+1) y=(ix+1,iy+1)
             const float top = fmaf(ax[u], gt[u].z - gt[u].w, gt[u].w);
