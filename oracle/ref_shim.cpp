@@ -609,6 +609,141 @@ int ref_nf_step(int n_tx, double radius, double offset, int T, double dt, double
   });
 }
 
+// ---- CPU-baseline session (bench.py cpu_baseline leg) ---------------------
+// joint_reconstruct's one-time setup (optimize.hpp:374-405: layout, das_stack,
+// the complex<float> spectra cache, bin table, delay phases) done once, then
+// its step body (optimize.hpp:413-467, Adam included) run on demand with
+// per-phase wall-clock timings, so one full iteration can be timed without
+// re-running the setup, and the per-patch work can be re-timed at another
+// worker count.  Every computation is a reference entry point.
+struct RefNfSession {
+  pact::SignalSet s;
+  pact::GridSpec grid;
+  pact::CircularMask mask;
+  pact::TrainConfig cfg;
+  pact::PatchLayout layout;
+  std::vector<std::vector<std::vector<std::complex<float>>>> ycache;
+  pact::PatchBinTable table;
+  std::vector<std::vector<std::complex<double>>> phases;
+  pact::SirenParams params;
+  pact::AdamState adam;
+  double loss_scale = 0.0;
+};
+
+void* ref_nf_session_open(int n_tx, double radius, double offset, int T, double dt, double t0,
+                          double v0, const double* sig, int W, int H, double pitch, double ox,
+                          double oy, double mcx, double mcy, double mr, const RefTrainCfg* c,
+                          double* setup_seconds) {
+  RefNfSession* out = nullptr;
+  int rc = guarded([&] {
+    auto t_start = std::chrono::steady_clock::now();
+    auto* h = new RefNfSession;
+    h->s = signals_of(n_tx, radius, offset, T, dt, t0, v0, sig);
+    h->cfg = train_config_of(c);
+    h->grid = grid_of(W, H, pitch, ox, oy);
+    h->mask = {{mcx, mcy}, mr};
+    h->layout = pact::make_patch_layout(h->grid, h->cfg.patch_mm, h->cfg.overlap);
+    const int P = h->layout.patch_pixels, N = h->layout.n_patches();
+    const size_t M = h->cfg.delays.size();
+    h->loss_scale = 1.0 / (static_cast<double>(N) * M * P * P);
+    auto stack = pact::das_stack(h->s, h->grid, v0, h->cfg.delays, h->cfg.workers);
+    h->ycache.resize(N);
+    pact::parallel_for(N, h->cfg.workers, [&](int i) {
+      pact::PatchSpectra ps = pact::extract_patch_spectra_one(stack, h->layout, i);
+      h->ycache[i].resize(M);
+      for (size_t j = 0; j < M; ++j) {
+        h->ycache[i][j].resize(ps.Y[j].size());
+        for (size_t b = 0; b < ps.Y[j].size(); ++b)
+          h->ycache[i][j][b] = std::complex<float>(ps.Y[j][b]);
+      }
+    });
+    h->params = pact::init_siren(h->cfg.seed, h->cfg.hidden, h->cfg.sine_layers, h->cfg.omega0,
+                                 h->cfg.out_scale, v0);
+    h->table = pact::PatchBinTable::make(P, h->grid.pitch, h->cfg.n_angles);
+    h->phases = pact::detail::make_delay_phases(h->table, h->cfg.delays);
+    if (setup_seconds)
+      *setup_seconds =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    out = h;
+  });
+  return rc == 0 ? out : nullptr;
+}
+
+// One step of optimize.hpp:413-467 with `workers` threads over patches
+// [patch_lo, patch_hi) (0/-1 = all).  with_siren = 0 skips render/TV/backprop/
+// Adam (times only the per-patch loop on the session's last rendered field).
+// t[0..5] = render, per-patch loop, TV, backprop, Adam, total (seconds).
+int ref_nf_session_step(void* hp, int workers, int patch_lo, int patch_hi, int with_siren,
+                        double* t, double* data_term) {
+  return guarded([&] {
+    auto* h = static_cast<RefNfSession*>(hp);
+    using clk = std::chrono::steady_clock;
+    auto sec = [](clk::time_point a, clk::time_point b) {
+      return std::chrono::duration<double>(b - a).count();
+    };
+    static thread_local pact::SosField field;
+    const double v0 = h->s.background_sos;
+    const int N = h->layout.n_patches();
+    const int lo = patch_lo, hi = patch_hi < 0 ? N : std::min(N, patch_hi);
+    auto t0 = clk::now();
+    if (with_siren || field.raster.values.empty()) field = pact::render_sos(h->params, h->grid, h->mask);
+    auto t1 = clk::now();
+    const int nw = pact::resolve_workers(workers);
+    const int span = hi - lo;
+    const int n_chunks = std::max(1, std::min(span, nw * 4));
+    const int chunk_len = (span + n_chunks - 1) / n_chunks;
+    std::vector<double> patch_loss(N, 0.0);
+    std::vector<std::vector<double>> chunk_gv(n_chunks);
+    pact::parallel_for(n_chunks, workers, [&](int ck) {
+      int a = lo + ck * chunk_len, b = std::min(hi, a + chunk_len);
+      if (a >= b) return;
+      auto& gv = chunk_gv[ck];
+      gv.assign(field.raster.values.size(), 0.0);
+      pact::detail::FusedScratch scratch;
+      std::vector<double> dw;
+      for (int i = a; i < b; ++i) {
+        auto prof = pact::wavefront_profile(h->layout.centers[i], h->s.geom, field.raster, v0,
+                                            h->mask, h->cfg.n_angles, h->cfg.ray_step, false);
+        patch_loss[i] = pact::detail::fused_patch_loss_grad(
+            h->ycache[i], prof.w, h->table, h->phases, h->cfg.eps_deconv, h->loss_scale,
+            h->cfg.implicit_xhat_grad, scratch, dw);
+        pact::wavefront_grad_trace(h->layout.centers[i], h->s.geom, field.raster, v0, h->mask,
+                                   h->cfg.n_angles, h->cfg.ray_step, dw, gv);
+      }
+    });
+    double data = 0.0;
+    for (int i = 0; i < N; ++i) data += patch_loss[i];
+    auto t2 = clk::now();
+    auto t3 = t2, t4 = t2, t5 = t2;
+    if (with_siren) {
+      auto tv = pact::tv_loss(field, h->cfg.lambda_tv);
+      t3 = clk::now();
+      std::vector<double> gm(field.masked_indices.size(), 0.0);
+      for (const auto& gv : chunk_gv) {
+        if (gv.empty()) continue;
+        for (size_t i = 0; i < gm.size(); ++i) gm[i] += gv[field.masked_indices[i]];
+      }
+      for (size_t i = 0; i < gm.size(); ++i) gm[i] += tv.grad[i];
+      auto grads = pact::backprop_sos(h->params, field, gm);
+      t4 = clk::now();
+      pact::adam_step(h->params.theta, grads, h->adam, h->cfg.learning_rate, h->cfg.beta1,
+                      h->cfg.beta2, h->cfg.adam_eps);
+      t5 = clk::now();
+    }
+    if (t) {
+      t[0] = sec(t0, t1);
+      t[1] = sec(t1, t2);
+      t[2] = sec(t2, t3);
+      t[3] = sec(t3, t4);
+      t[4] = sec(t4, t5);
+      t[5] = sec(t0, t5);
+    }
+    if (data_term) *data_term = data;
+  });
+}
+
+void ref_nf_session_close(void* h) { delete static_cast<RefNfSession*>(h); }
+
 // Wall-clock of `reps` calls of das_stack (the CPU baseline of bench.py).
 double ref_time_das_stack(int reps, int n_tx, double radius, double offset, int T, double dt,
                           double t0, const double* sig, int W, int H, double pitch, double ox,

@@ -282,6 +282,70 @@ class Oracle:
         out["grad_v_masked"] = out["grad_v_masked"][:nm]
         return out
 
+    # -- CPU-baseline session (ref_shim.cpp ref_nf_session_*) -----------
+    def nf_session(self, sig, ring, meta, grid, mask, cfg):
+        """joint_reconstruct's one-time setup (optimize.hpp:374-405), once;
+        returns (handle, setup seconds).  Close with nf_session_close."""
+        c, arr = train_cfg(cfg)
+        sig = _f64(sig)
+        secs = C.c_double(0)
+        fn = self.lib.ref_nf_session_open
+        fn.restype = C.c_void_p
+        fn.argtypes = [_I, _D, _D, _I, _D, _D, _D, _P, _I, _I, _D, _D, _D, _D, _D, _D,
+                       C.POINTER(TrainCfg), _P]
+        h = fn(*_r(ring), meta.n_samples, meta.dt, meta.t0, meta.background_sos, _p(sig),
+               *_g(grid), *_m(mask), C.byref(c), C.byref(secs))
+        if not h:
+            raise RuntimeError("ref_nf_session_open failed: " + self.last_error())
+        return h, secs.value
+
+    def nf_session_step(self, h, workers, patch_lo=0, patch_hi=-1, with_siren=True):
+        """One step of optimize.hpp:413-467 -> dict of phase seconds + data term."""
+        t = np.zeros(6)
+        data = C.c_double(0)
+        fn = self.lib.ref_nf_session_step
+        fn.argtypes = [_P, _I, _I, _I, _I, _P, _P]
+        fn.restype = C.c_int
+        rc = fn(C.c_void_p(h), workers, patch_lo, patch_hi, 1 if with_siren else 0, _p(t),
+                C.byref(data))
+        if rc != 0:
+            raise RuntimeError("ref_nf_session_step failed: " + self.last_error())
+        keys = ("render", "patches", "tv", "backprop", "adam", "total")
+        out = dict(zip(keys, t.tolist()))
+        out["data_term"] = data.value
+        return out
+
+    def nf_session_close(self, h):
+        fn = self.lib.ref_nf_session_close
+        fn.argtypes = [_P]
+        fn.restype = None
+        fn(C.c_void_p(h))
+
+    def last_error(self) -> str:
+        fn = getattr(self.lib, self.prefix + "last_error", None)
+        if fn is None:
+            return ""
+        fn.restype = C.c_char_p
+        return (fn() or b"").decode()
+
+    def param_count(self, hidden, layers) -> int:
+        fn = self.lib.ref_siren_param_count
+        fn.argtypes = [_I, _I]
+        fn.restype = C.c_long
+        return int(fn(hidden, layers))
+
+    def simulate(self, w, pressure, sos, sim_mask, workers=0, ring=None):
+        """simulate_signals (phantom.hpp:282-362) of rasters on w.grid, with
+        the caller's window (w.meta) -> fp64 [N, T]."""
+        g = w.grid
+        ring = ring or w.ring
+        out = np.zeros((ring.n_transducers, w.meta.n_samples))
+        pr, so = _f64(pressure), _f64(sos)
+        self.call("simulate_signals", g.width, g.height, g.pitch, g.origin_x, g.origin_y, _p(pr),
+                  _p(so), *_m(sim_mask), w.v0, *_r(ring), 100e-9, w.meta.dt, w.meta.t0,
+                  w.meta.n_samples, w.ray_step, workers, _p(out))
+        return out
+
     def joint_reconstruct(self, sig, ring, meta, grid, mask, cfg, n_params):
         c, arr = train_cfg(cfg)
         sig = _f64(sig)
