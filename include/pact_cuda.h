@@ -278,6 +278,84 @@ int pact_loss_grad(pact_ctx* ctx, int32_t n_patches, const float* Y, const float
                    int32_t n_angles, const double* delays, int32_t K, int32_t P, double pitch,
                    double eps, double scale, int32_t implicit, double* loss_per_patch, float* dw);
 
+/* MergeWindow::make, deconv.hpp:124-138 (host): Gaussian window, peak 1 at
+ * the patch centre.  weights : HOST double[P * P]. */
+int pact_merge_window(double fwhm_mm, int32_t P, double pitch, double* weights);
+
+/* merge_patches, deconv.hpp:142-164: weight-normalised overlap-add of the
+ * layout's patch images with the window `window` (HOST double[P * P], e.g.
+ * from pact_merge_window; NULL = MergeWindow::make(fwhm_mm)).
+ *   patches : device fp32 [n_patches][P][P] (layout order);  image : device fp32 [H][W] */
+int pact_merge_patches(pact_ctx* ctx, const pact_layout* layout, const float* patches,
+                       const double* window, double fwhm_mm, float* image);
+
+/* ---- part 3, the composed (non-fused) path: fp64, complex128 operands ----
+ * The reference's differentiable-by-parts API (used by its gradient tests and
+ * by callers that want dL/dH).  Spectra are device complex128
+ * [n_patches][K][P][P] (interleaved re, im), the reference's complex<double>.
+ */
+
+/* multichannel_deconvolve, deconv.hpp:78-96, batched:
+ *   X[p][b] = sum_j conj(H_j) Y_j / (sum_j |H_j|^2 + eps K), 0 where the
+ *   denominator is 0.  X : device complex128 [n_patches][P][P]. */
+int pact_multichannel_deconvolve(pact_ctx* ctx, int32_t n_patches, int32_t K, int32_t P,
+                                 const double* Y, const double* H, double eps, double* X);
+
+/* deconv_jacobian_H, deconv.hpp:100-115: dX(bin)/d(Re H_j(bin)) and
+ * dX(bin)/d(Im H_j(bin)) for each query (patch, j, bin) of the device int32
+ * array `queries` [n_queries][3]; out : device complex128 [n_queries][2]. */
+int pact_deconv_jacobian_H(pact_ctx* ctx, int32_t K, int32_t P, const double* Y, const double* H,
+                           double eps, int32_t n_queries, const int32_t* queries, double* out);
+
+/* patch_data_loss, optimize.hpp:164-211, batched with the caller's `scale`:
+ *   loss_per_patch : device fp64 [n_patches]
+ *   grad_h         : device complex128 [n_patches][K][P][P] (dL/dRe H + i dL/dIm H,
+ *                    explicit term plus, with `implicit`, the term through X-hat) */
+int pact_patch_data_loss(pact_ctx* ctx, int32_t n_patches, int32_t K, int32_t P, double pitch,
+                         const double* Y, const double* H, double eps, double scale,
+                         int32_t implicit, double* loss_per_patch, double* grad_h);
+
+/* data_loss, optimize.hpp:336-353: patch_data_loss of every patch with
+ * scale = 1 / (n_patches K P^2), summed in patch order.  value : HOST fp64
+ * (synchronous); loss_per_patch : device fp64 [n_patches] or NULL. */
+int pact_data_loss(pact_ctx* ctx, int32_t n_patches, int32_t K, int32_t P, double pitch,
+                   const double* Y, const double* H, double eps, int32_t implicit, double* value,
+                   double* loss_per_patch, double* grad_h);
+
+/* transfer_grad_to_wavefront, aberration.hpp:270-313, batched:
+ *   w      : device fp64 [n_patches][n_angles] (the profiles H was made from)
+ *   delays : HOST double[K]
+ *   grad_h : device complex128 [n_patches][K][P][P] (Nyquist-symmetrised inside,
+ *            like the reference; the input is not modified)
+ *   dw     : device fp64 [n_patches][n_angles] (overwritten) */
+int pact_transfer_grad_to_wavefront(pact_ctx* ctx, int32_t n_patches, const double* w,
+                                    int32_t n_angles, const double* delays, int32_t K, int32_t P,
+                                    double pitch, const double* grad_h, double* dw);
+
+/* wavefront_profile(..., with_jacobian = true), aberration.hpp:134-186: the
+ * profiles (fp64) and their sparse Jacobian rows w.r.t. the in-mask SOS pixels,
+ * in CSR form with one row per (patch, angle):
+ *   row_start : device int64 [n_centers * n_angles + 1]
+ *   pixel     : device int32 [n_entries]  (flat row-major grid index)
+ *   dw_dv     : device fp32  [n_entries]  (mm per m/s; the reference stores float)
+ *   w         : device fp64 [n_centers][n_angles] or NULL
+ * Call once with pixel = dw_dv = NULL to size: fills row_start and the HOST
+ * *n_entries (synchronous); call again with buffers of >= *n_entries entries
+ * (`capacity`) to fill them.  Rows list entries by step, then stencil corner
+ * (the reference's order). */
+int pact_wavefront_jacobian(pact_ctx* ctx, const pact_ring* ring, const pact_grid* grid,
+                            const float* sos_dev, double v0, const pact_mask* mask,
+                            int32_t n_centers, const double* centers, int32_t n_angles,
+                            double step, double* w, int64_t* row_start, int32_t* pixel,
+                            float* dw_dv, int64_t capacity, int64_t* n_entries);
+
+/* accumulate_wavefront_grad, aberration.hpp:316-326: grad_v (device fp64
+ * [H][W]) += J^T dw over the CSR rows of pact_wavefront_jacobian;
+ * dw : device fp64 [n_rows]. */
+int pact_accumulate_wavefront_grad(pact_ctx* ctx, int64_t n_rows, const int64_t* row_start,
+                                   const int32_t* pixel, const float* dw_dv, const double* dw,
+                                   double* grad_v);
+
 /* wavefront_grad_trace, aberration.hpp:333-361, batched: grad_v (device fp64
  * [H][W]) += sum over rays of dL/dw * dl * v0 / v^2 * bilinear weight. */
 int pact_ray_backward(pact_ctx* ctx, const pact_ring* ring, const pact_grid* grid,

@@ -609,6 +609,148 @@ int ref_nf_step(int n_tx, double radius, double offset, int T, double dt, double
   });
 }
 
+// ---- composed (non-fused) path: one patch per call ------------------------
+namespace {
+pact::TransferStack tstack_of(int K, int P, double pitch, const double* delays, const double* H) {
+  pact::TransferStack ts;
+  ts.patch_pixels = P;
+  ts.pitch = pitch;
+  ts.delays.assign(delays, delays + K);
+  const size_t P2 = static_cast<size_t>(P) * P;
+  const auto* h = reinterpret_cast<const std::complex<double>*>(H);
+  for (int j = 0; j < K; ++j) ts.spectra.emplace_back(h + j * P2, h + (j + 1) * P2);
+  return ts;
+}
+pact::PatchSpectra spectra_of(int K, int P, const double* Y) {
+  pact::PatchSpectra ps;
+  const size_t P2 = static_cast<size_t>(P) * P;
+  const auto* y = reinterpret_cast<const std::complex<double>*>(Y);
+  for (int j = 0; j < K; ++j) ps.Y.emplace_back(y + j * P2, y + (j + 1) * P2);
+  return ps;
+}
+}  // namespace
+
+// multichannel_deconvolve, deconv.hpp:78-96 (Y, H, X complex128)
+int ref_multichannel_deconvolve(int K, int P, const double* Y, const double* H, double eps,
+                                double* X) {
+  return guarded([&] {
+    std::vector<double> d(K, 0.0);
+    auto x = pact::multichannel_deconvolve(spectra_of(K, P, Y), tstack_of(K, P, 1.0, d.data(), H), eps);
+    std::memcpy(X, x.data(), sizeof(double) * 2 * x.size());
+  });
+}
+
+// deconv_jacobian_H, deconv.hpp:100-115 -> out[4] = (dre.re, dre.im, dim.re, dim.im)
+int ref_deconv_jacobian_H(int K, int P, const double* Y, const double* H, double eps, int j,
+                          int bin, double* out) {
+  return guarded([&] {
+    std::vector<double> d(K, 0.0);
+    auto [a, b] = pact::deconv_jacobian_H(spectra_of(K, P, Y), tstack_of(K, P, 1.0, d.data(), H),
+                                          eps, j, bin);
+    out[0] = a.real();
+    out[1] = a.imag();
+    out[2] = b.real();
+    out[3] = b.imag();
+  });
+}
+
+// patch_data_loss, optimize.hpp:164-211 (complex<double> Y)
+int ref_patch_data_loss(int K, int P, double pitch, const double* Y, const double* H, double eps,
+                        double scale, int implicit, double* loss, double* grad_h) {
+  return guarded([&] {
+    std::vector<double> d(K, 0.0);
+    auto r = pact::patch_data_loss(spectra_of(K, P, Y).Y, tstack_of(K, P, pitch, d.data(), H), eps,
+                                   scale, implicit != 0);
+    *loss = r.value;
+    const size_t P2 = static_cast<size_t>(P) * P;
+    for (int j = 0; j < K; ++j) std::memcpy(grad_h + 2 * j * P2, r.grad_h[j].data(), sizeof(double) * 2 * P2);
+  });
+}
+
+// data_loss, optimize.hpp:336-353 over n patches
+int ref_data_loss(int n, int K, int P, double pitch, const double* Y, const double* H, double eps,
+                  int implicit, double* value, double* grad_h) {
+  return guarded([&] {
+    std::vector<double> d(K, 0.0);
+    const size_t stride = 2 * static_cast<size_t>(K) * P * P;
+    std::vector<pact::PatchSpectra> ys;
+    std::vector<pact::TransferStack> hs;
+    for (int i = 0; i < n; ++i) {
+      ys.push_back(spectra_of(K, P, Y + i * stride));
+      hs.push_back(tstack_of(K, P, pitch, d.data(), H + i * stride));
+    }
+    auto r = pact::data_loss(ys, hs, eps, implicit != 0);
+    *value = r.value;
+    const size_t P2 = static_cast<size_t>(P) * P;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < K; ++j)
+        std::memcpy(grad_h + i * stride + 2 * j * P2, r.grad_h[i][j].data(), sizeof(double) * 2 * P2);
+  });
+}
+
+// transfer_grad_to_wavefront, aberration.hpp:270-313
+int ref_transfer_grad_to_wavefront(int A, const double* w, int K, const double* delays, int P,
+                                   double pitch, const double* grad_h, double* dw) {
+  return guarded([&] {
+    pact::WavefrontProfile prof;
+    prof.center = {0.0, 0.0};
+    prof.n_angles = A;
+    prof.w.assign(w, w + A);
+    std::vector<std::vector<std::complex<double>>> g;
+    const size_t P2 = static_cast<size_t>(P) * P;
+    const auto* gh = reinterpret_cast<const std::complex<double>*>(grad_h);
+    for (int j = 0; j < K; ++j) g.emplace_back(gh + j * P2, gh + (j + 1) * P2);
+    auto out = pact::transfer_grad_to_wavefront(prof, std::vector<double>(delays, delays + K), P,
+                                                pitch, g);
+    std::memcpy(dw, out.data(), sizeof(double) * A);
+  });
+}
+
+// wavefront_profile(with_jacobian = true), aberration.hpp:134-186, one centre:
+// w[A], row lengths counts[A], and (when pixel != null) the rows concatenated.
+// With dw != null also accumulate_wavefront_grad (aberration.hpp:316-326) into grad_v.
+int ref_wavefront_jacobian(double cx, double cy, int n_tx, double radius, double offset, int W,
+                           int H, double pitch, double ox, double oy, const double* sos,
+                           double v0, double mcx, double mcy, double mr, int A, double step,
+                           double* w, long* counts, int* pixel, float* dwdv, long cap,
+                           const double* dw, double* grad_v) {
+  return guarded([&] {
+    auto g = grid_of(W, H, pitch, ox, oy);
+    auto prof = pact::wavefront_profile({cx, cy}, {n_tx, radius, offset}, raster_of(g, sos), v0,
+                                        {{mcx, mcy}, mr}, A, step, true);
+    long pos = 0;
+    for (int a = 0; a < A; ++a) {
+      if (w) w[a] = prof.w[a];
+      if (counts) counts[a] = static_cast<long>(prof.jacobian[a].size());
+      for (const auto& e : prof.jacobian[a]) {
+        if (pixel && pos < cap) {
+          pixel[pos] = e.pixel;
+          dwdv[pos] = e.dw_dv;
+        }
+        ++pos;
+      }
+    }
+    if (dw && grad_v) {
+      std::vector<double> gv(grad_v, grad_v + static_cast<size_t>(W) * H);
+      pact::accumulate_wavefront_grad(prof, std::vector<double>(dw, dw + A), gv);
+      std::memcpy(grad_v, gv.data(), sizeof(double) * gv.size());
+    }
+  });
+}
+
+// merge_patches + MergeWindow::make, deconv.hpp:118-164, on make_patch_layout's layout
+int ref_merge_patches(int W, int H, double pitch, double ox, double oy, double patch_mm,
+                      double overlap, const double* patches, double fwhm, double* image) {
+  return guarded([&] {
+    auto lay = pact::make_patch_layout(grid_of(W, H, pitch, ox, oy), patch_mm, overlap);
+    const size_t P2 = static_cast<size_t>(lay.patch_pixels) * lay.patch_pixels;
+    std::vector<std::vector<double>> ps;
+    for (int i = 0; i < lay.n_patches(); ++i) ps.emplace_back(patches + i * P2, patches + (i + 1) * P2);
+    auto img = pact::merge_patches(ps, lay, pact::MergeWindow::make(fwhm, lay.patch_pixels, pitch));
+    std::memcpy(image, img.values.data(), sizeof(double) * img.values.size());
+  });
+}
+
 // ---- CPU-baseline session (bench.py cpu_baseline leg) ---------------------
 // joint_reconstruct's one-time setup (optimize.hpp:374-405: layout, das_stack,
 // the complex<float> spectra cache, bin table, delay phases) done once, then
@@ -627,6 +769,7 @@ struct RefNfSession {
   std::vector<std::vector<std::complex<double>>> phases;
   pact::SirenParams params;
   pact::AdamState adam;
+  pact::SosField field;  // the last rendered field
   double loss_scale = 0.0;
 };
 
@@ -681,7 +824,7 @@ int ref_nf_session_step(void* hp, int workers, int patch_lo, int patch_hi, int w
     auto sec = [](clk::time_point a, clk::time_point b) {
       return std::chrono::duration<double>(b - a).count();
     };
-    static thread_local pact::SosField field;
+    pact::SosField& field = h->field;
     const double v0 = h->s.background_sos;
     const int N = h->layout.n_patches();
     const int lo = patch_lo, hi = patch_hi < 0 ? N : std::min(N, patch_hi);

@@ -152,6 +152,17 @@ SIGNATURES = {
     "pact_ray_backward": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(Grid), _P, _D,
                                     C.POINTER(Mask), _I, _DP, _I, _D, _P, _P]),
     "pact_tv_loss": (C.c_int, [_P, C.POINTER(Grid), C.POINTER(Mask), _P, _D, _DP, _P]),
+    "pact_merge_window": (C.c_int, [_D, _I, _D, _DP]),
+    "pact_merge_patches": (C.c_int, [_P, C.POINTER(Layout), _P, _DP, _D, _P]),
+    "pact_multichannel_deconvolve": (C.c_int, [_P, _I, _I, _I, _P, _P, _D, _P]),
+    "pact_deconv_jacobian_H": (C.c_int, [_P, _I, _I, _P, _P, _D, _I, _P, _P]),
+    "pact_patch_data_loss": (C.c_int, [_P, _I, _I, _I, _D, _P, _P, _D, _D, _I, _P, _P]),
+    "pact_data_loss": (C.c_int, [_P, _I, _I, _I, _D, _P, _P, _D, _I, _DP, _P, _P]),
+    "pact_transfer_grad_to_wavefront": (C.c_int, [_P, _I, _P, _I, _DP, _I, _I, _D, _P, _P]),
+    "pact_wavefront_jacobian": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(Grid), _P, _D,
+                                          C.POINTER(Mask), _I, _DP, _I, _D, _P, _P, _P, _P,
+                                          C.c_int64, C.POINTER(C.c_int64)]),
+    "pact_accumulate_wavefront_grad": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P]),
     "pact_adam_step": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, C.c_int64, _D, _D, _D, _D]),
     "pact_train_config_default": (C.c_int, [C.POINTER(TrainConfig)]),
     "pact_trainer_create": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(SignalMeta), _P,

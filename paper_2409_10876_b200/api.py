@@ -252,6 +252,18 @@ def _cplx(t: torch.Tensor) -> torch.Tensor:
     return t if t.dtype == torch.complex64 else t.to(torch.complex64)
 
 
+def _need(t, name: str, dtype, numel: int | None = None) -> torch.Tensor:
+    """Argument check before a raw device pointer crosses the C-ABI: CUDA,
+    the expected dtype and (optionally) element count; returns it contiguous."""
+    if not (isinstance(t, torch.Tensor) and t.is_cuda):
+        raise TypeError(f"{name}: CUDA tensor expected")
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: {dtype} expected, got {t.dtype}")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name}: {numel} elements expected, got {t.numel()}")
+    return t.contiguous()
+
+
 def _ctx_methods():
     def render_sos(self, spec: SirenSpec, theta: torch.Tensor, grid: GridSpec,
                    mask: CircularMask):
@@ -280,9 +292,10 @@ def _ctx_methods():
         """wavefront_profile, aberration.hpp:134-186 for every centre -> fp32 [n, A]."""
         cen = np.ascontiguousarray(np.asarray(centers, np.float64).reshape(-1, 2))
         n = cen.shape[0]
+        sos_dev = _need(sos_dev, "sos_dev", torch.float32, grid.width * grid.height)
         w = torch.empty((n, n_angles), device="cuda", dtype=torch.float32)
         r, g, m = ring.c(), grid.c(), mask.c()
-        check(_abi.lib().pact_wavefront(self._h, C.byref(r), C.byref(g), dptr(sos_dev.contiguous()),
+        check(_abi.lib().pact_wavefront(self._h, C.byref(r), C.byref(g), dptr(sos_dev),
                                         v0, C.byref(m), n,
                                         cen.ctypes.data_as(C.POINTER(C.c_double)), n_angles, step,
                                         dptr(w)))
@@ -290,7 +303,7 @@ def _ctx_methods():
 
     def transfer_stack(self, w: torch.Tensor, delays, P: int, pitch: float) -> torch.Tensor:
         """transfer_stack, aberration.hpp:236-265 -> complex64 [n, K, P, P]."""
-        w = w.contiguous()
+        w = _need(w, "w", torch.float32)
         n, A = w.shape
         K = len(delays)
         H = torch.empty((n, K, P, P), device="cuda", dtype=torch.complex64)
@@ -300,6 +313,10 @@ def _ctx_methods():
 
     def patch_spectra(self, layout: PatchLayout, stack: torch.Tensor) -> torch.Tensor:
         """extract_patch_spectra, deconv.hpp:64-74 -> complex64 [n, K, P, P]."""
+        g = layout.raw.grid
+        stack = _need(stack, "stack", torch.float32)
+        if stack.dim() != 3 or stack.shape[1:] != (g.height, g.width):
+            raise ValueError("stack: [K, H, W] on the layout grid expected")
         K = stack.shape[0]
         P = layout.patch_pixels
         Y = torch.empty((layout.n_patches, K, P, P), device="cuda", dtype=torch.complex64)
@@ -313,6 +330,8 @@ def _ctx_methods():
                          opt: DeconvolveOptions) -> torch.Tensor:
         """deconvolve_image, deconv.hpp:176-198 -> fp32 [H, W]."""
         g = layout.raw.grid
+        stack = _need(stack, "stack", torch.float32, len(delays) * g.height * g.width)
+        sos_dev = _need(sos_dev, "sos_dev", torch.float32, g.height * g.width)
         img = torch.empty((g.height, g.width), device="cuda", dtype=torch.float32)
         r, m, lay, o = ring.c(), mask.c(), layout.c(), opt.c()
         check(_abi.lib().pact_deconvolve_image(self._h, dptr(stack.contiguous()), len(delays),
@@ -324,9 +343,9 @@ def _ctx_methods():
     def loss_grad(self, Y: torch.Tensor, w: torch.Tensor, delays, P: int, pitch: float,
                   eps: float, scale: float, implicit: bool = True):
         """fused_patch_loss_grad, optimize.hpp:234-325, batched -> (loss fp64 [n], dw fp32 [n, A])."""
-        Y = _cplx(Y).contiguous()
-        w = w.contiguous()
+        w = _need(w, "w", torch.float32)
         n, A = w.shape
+        Y = _need(_cplx(Y), "Y", torch.complex64, n * len(delays) * P * P)
         loss = torch.empty(n, device="cuda", dtype=torch.float64)
         dw = torch.empty_like(w)
         check(_abi.lib().pact_loss_grad(self._h, n, dptr(Y), dptr(w), A, darr(delays), len(delays),
@@ -341,11 +360,15 @@ def _ctx_methods():
         cen = np.ascontiguousarray(np.asarray(centers, np.float64).reshape(-1, 2))
         if grad_v is None:
             grad_v = torch.zeros((grid.height, grid.width), device="cuda", dtype=torch.float64)
+        _need(grad_v, "grad_v", torch.float64, grid.height * grid.width)
+        assert grad_v.is_contiguous(), "grad_v: contiguous fp64 accumulator expected"
+        sos_dev = _need(sos_dev, "sos_dev", torch.float32, grid.height * grid.width)
+        dw = _need(dw, "dw", torch.float32, cen.shape[0] * n_angles)
         r, g, m = ring.c(), grid.c(), mask.c()
         check(_abi.lib().pact_ray_backward(self._h, C.byref(r), C.byref(g),
-                                           dptr(sos_dev.contiguous()), v0, C.byref(m),
+                                           dptr(sos_dev), v0, C.byref(m),
                                            cen.shape[0], cen.ctypes.data_as(C.POINTER(C.c_double)),
-                                           n_angles, step, dptr(dw.contiguous()), dptr(grad_v)))
+                                           n_angles, step, dptr(dw), dptr(grad_v)))
         return grad_v
 
     def tv_loss(self, grid: GridSpec, mask: CircularMask, raster: torch.Tensor, lam: float):
@@ -360,6 +383,10 @@ def _ctx_methods():
 
     def adam_step(self, theta, grad, m, v, t, lr, beta1, beta2, eps):
         """adam_step, optimize.hpp:87-110 on fp64 device tensors (t after the update)."""
+        n = theta.numel()
+        for name, t in (("theta", theta), ("grad", grad), ("m", m), ("v", v)):
+            _need(t, name, torch.float64, n)
+            assert t.is_contiguous(), f"{name}: contiguous tensor expected"
         check(_abi.lib().pact_adam_step(self._h, theta.numel(), dptr(theta), dptr(grad), dptr(m),
                                         dptr(v), t, lr, beta1, beta2, eps))
 
@@ -381,8 +408,136 @@ def _ctx_methods():
                                                   1 if spreading else 0, dptr(out)))
         return out
 
+    # ---- the composed (non-fused) path, fp64 (composed.cu) ----
+    def _c128(t, name, ndim):
+        assert isinstance(t, torch.Tensor) and t.is_cuda, f"{name}: CUDA tensor expected"
+        assert t.dtype == torch.complex128 and t.dim() == ndim, \
+            f"{name}: complex128 tensor with {ndim} dims expected"
+        return t.contiguous()
+
+    def multichannel_deconvolve(self, Y: torch.Tensor, H: torch.Tensor, eps: float) -> torch.Tensor:
+        """multichannel_deconvolve, deconv.hpp:78-96, batched: complex128
+        [n, K, P, P] x2 -> X complex128 [n, P, P]."""
+        Y, H = _c128(Y, "Y", 4), _c128(H, "H", 4)
+        if Y.shape != H.shape:
+            raise _abi.ValidationError(2, "deconvolve: Y and H channel counts differ")
+        n, K, P, _ = Y.shape
+        X = torch.empty((n, P, P), device="cuda", dtype=torch.complex128)
+        check(_abi.lib().pact_multichannel_deconvolve(self._h, n, K, P, dptr(Y), dptr(H), eps,
+                                                      dptr(X)))
+        return X
+
+    def deconv_jacobian_H(self, Y: torch.Tensor, H: torch.Tensor, eps: float, queries):
+        """deconv_jacobian_H, deconv.hpp:100-115 for queries [(patch, j, bin)]
+        -> complex128 [q, 2] = (dX/dRe H_j, dX/dIm H_j) at the bin."""
+        Y, H = _c128(Y, "Y", 4), _c128(H, "H", 4)
+        n, K, P, _ = Y.shape
+        q = torch.as_tensor(np.asarray(queries, np.int32).reshape(-1, 3)).cuda()
+        out = torch.empty((q.shape[0], 2), device="cuda", dtype=torch.complex128)
+        check(_abi.lib().pact_deconv_jacobian_H(self._h, K, P, dptr(Y), dptr(H), eps, q.shape[0],
+                                                dptr(q), dptr(out)))
+        torch.cuda.current_stream().synchronize()
+        return out
+
+    def patch_data_loss(self, Y: torch.Tensor, H: torch.Tensor, pitch: float, eps: float,
+                        scale: float, implicit: bool = True):
+        """patch_data_loss, optimize.hpp:164-211, batched -> (loss fp64 [n],
+        grad_h complex128 [n, K, P, P])."""
+        Y, H = _c128(Y, "Y", 4), _c128(H, "H", 4)
+        if Y.shape != H.shape:
+            raise _abi.ValidationError(2, "data_loss: Y/H channel mismatch")
+        n, K, P, _ = Y.shape
+        loss = torch.empty(n, device="cuda", dtype=torch.float64)
+        g = torch.empty_like(Y)
+        check(_abi.lib().pact_patch_data_loss(self._h, n, K, P, pitch, dptr(Y), dptr(H), eps, scale,
+                                              1 if implicit else 0, dptr(loss), dptr(g)))
+        return loss, g
+
+    def data_loss(self, Y: torch.Tensor, H: torch.Tensor, pitch: float, eps: float,
+                  implicit: bool = True):
+        """data_loss, optimize.hpp:336-353 -> (value, loss fp64 [n], grad_h)."""
+        Y, H = _c128(Y, "Y", 4), _c128(H, "H", 4)
+        if Y.shape[0] != H.shape[0]:
+            raise _abi.ValidationError(2, "data_loss: patch count mismatch")
+        if Y.shape != H.shape:
+            raise _abi.ValidationError(2, "data_loss: Y/H channel mismatch")
+        n, K, P, _ = Y.shape
+        loss = torch.empty(n, device="cuda", dtype=torch.float64)
+        g = torch.empty_like(Y)
+        val = C.c_double()
+        check(_abi.lib().pact_data_loss(self._h, n, K, P, pitch, dptr(Y), dptr(H), eps,
+                                        1 if implicit else 0, C.byref(val), dptr(loss), dptr(g)))
+        return val.value, loss, g
+
+    def transfer_grad_to_wavefront(self, w: torch.Tensor, delays, P: int, pitch: float,
+                                   grad_h: torch.Tensor) -> torch.Tensor:
+        """transfer_grad_to_wavefront, aberration.hpp:270-313, batched:
+        w fp64 [n, A], grad_h complex128 [n, K, P, P] -> dw fp64 [n, A]."""
+        assert w.is_cuda and w.dtype == torch.float64 and w.dim() == 2, "w: CUDA fp64 [n, A]"
+        g = _c128(grad_h, "grad_h", 4)
+        n, A = w.shape
+        assert g.shape == (n, len(delays), P, P), "grad_h: [n, K, P, P] expected"
+        dw = torch.empty_like(w)
+        check(_abi.lib().pact_transfer_grad_to_wavefront(self._h, n, dptr(w.contiguous()), A,
+                                                         darr(delays), len(delays), P, pitch,
+                                                         dptr(g), dptr(dw)))
+        return dw
+
+    def wavefront_jacobian(self, ring: RingGeometry, grid: GridSpec, sos_dev: torch.Tensor,
+                           v0: float, mask: CircularMask, centers, n_angles: int, step: float):
+        """wavefront_profile(..., with_jacobian=true), aberration.hpp:134-186 ->
+        (w fp64 [n, A], row_start int64 [n A + 1], pixel int32 [nnz], dw_dv fp32 [nnz])."""
+        assert sos_dev.is_cuda and sos_dev.dtype == torch.float32, "sos_dev: CUDA fp32 [H, W]"
+        assert sos_dev.numel() == grid.width * grid.height, "sos_dev: grid-sized raster expected"
+        cen = np.ascontiguousarray(np.asarray(centers, np.float64).reshape(-1, 2))
+        n = cen.shape[0]
+        w = torch.empty((n, n_angles), device="cuda", dtype=torch.float64)
+        rs = torch.empty(n * n_angles + 1, device="cuda", dtype=torch.int64)
+        nnz = C.c_int64()
+        r, g, m = ring.c(), grid.c(), mask.c()
+        cp = cen.ctypes.data_as(C.POINTER(C.c_double))
+        L = _abi.lib()
+        sd = dptr(sos_dev.contiguous())
+        check(L.pact_wavefront_jacobian(self._h, C.byref(r), C.byref(g), sd, v0, C.byref(m), n, cp,
+                                        n_angles, step, None, dptr(rs), None, None, 0,
+                                        C.byref(nnz)))
+        pix = torch.empty(max(nnz.value, 1), device="cuda", dtype=torch.int32)
+        val = torch.empty(max(nnz.value, 1), device="cuda", dtype=torch.float32)
+        check(L.pact_wavefront_jacobian(self._h, C.byref(r), C.byref(g), sd, v0, C.byref(m), n, cp,
+                                        n_angles, step, dptr(w), dptr(rs), dptr(pix), dptr(val),
+                                        pix.numel(), C.byref(nnz)))
+        return w, rs, pix[:nnz.value], val[:nnz.value]
+
+    def accumulate_wavefront_grad(self, row_start: torch.Tensor, pixel: torch.Tensor,
+                                  dw_dv: torch.Tensor, dw: torch.Tensor, grad_v: torch.Tensor):
+        """accumulate_wavefront_grad, aberration.hpp:316-326: grad_v (fp64) += J^T dw."""
+        assert grad_v.is_cuda and grad_v.dtype == torch.float64, "grad_v: CUDA fp64"
+        assert dw.is_cuda and dw.dtype == torch.float64, "dw: CUDA fp64"
+        n_rows = row_start.numel() - 1
+        assert dw.numel() == n_rows, "dw: one value per Jacobian row"
+        check(_abi.lib().pact_accumulate_wavefront_grad(self._h, n_rows, dptr(row_start),
+                                                        dptr(pixel), dptr(dw_dv),
+                                                        dptr(dw.contiguous()), dptr(grad_v)))
+        return grad_v
+
+    def merge_patches(self, layout: PatchLayout, patches: torch.Tensor, fwhm: float) -> torch.Tensor:
+        """merge_patches + MergeWindow, deconv.hpp:118-164: fp32 [n, P, P] -> fp32 [H, W]."""
+        P = layout.patch_pixels
+        if patches.shape != (layout.n_patches, P, P):
+            raise _abi.ValidationError(2, "merge_patches: patch count does not match layout")
+        assert patches.is_cuda and patches.dtype == torch.float32, "patches: CUDA fp32"
+        g = layout.raw.grid
+        img = torch.empty((g.height, g.width), device="cuda", dtype=torch.float32)
+        lay = layout.c()
+        check(_abi.lib().pact_merge_patches(self._h, C.byref(lay), dptr(patches.contiguous()), None,
+                                            fwhm, dptr(img)))
+        return img
+
     for f in (simulate_signals, render_sos, siren_backward, wavefront, transfer_stack, patch_spectra,
-              deconvolve_image, loss_grad, ray_backward, tv_loss, adam_step):
+              deconvolve_image, loss_grad, ray_backward, tv_loss, adam_step,
+              multichannel_deconvolve, deconv_jacobian_H, patch_data_loss, data_loss,
+              transfer_grad_to_wavefront, wavefront_jacobian, accumulate_wavefront_grad,
+              merge_patches):
         setattr(Context, f.__name__, f)
 
 

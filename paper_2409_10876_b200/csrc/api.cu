@@ -340,6 +340,40 @@ int pact_deconvolve_image(pact_ctx* ctx, const float* stack, int32_t K, const do
   return PACT_OK;
 }
 
+int pact_merge_window(double fwhm_mm, int32_t P, double pitch, double* weights) {
+  if (!weights) return validation("pact_merge_window: null argument").code;
+  if (!(fwhm_mm > 0.0)) return validation("merge window: FWHM must be > 0").code;
+  // MergeWindow::make, deconv.hpp:124-138
+  const double sigma_px = fwhm_mm / (2.0 * std::sqrt(2.0 * std::log(2.0))) / pitch;
+  const double c = 0.5 * (P - 1);
+  for (int y = 0; y < P; ++y)
+    for (int x = 0; x < P; ++x) {
+      const double r2 = (x - c) * (x - c) + (y - c) * (y - c);
+      weights[static_cast<size_t>(y) * P + x] = std::exp(-0.5 * r2 / (sigma_px * sigma_px));
+    }
+  return PACT_OK;
+}
+
+int pact_merge_patches(pact_ctx* ctx, const pact_layout* lay, const float* patches,
+                       const double* window, double fwhm, float* image) {
+  if (!ctx || !lay || !patches || !image) return validation("pact_merge_patches: null argument").code;
+  const int P = lay->patch_pixels, P2 = P * P;
+  if (P < 1 || lay->nx < 1 || lay->ny < 1) return validation("merge_patches: empty layout").code;
+  std::vector<float> win;
+  if (window) {
+    win.assign(window, window + P2);
+  } else {
+    PACT_TRY(merge_window(fwhm, P, lay->grid.pitch, win));  // MergeWindow::make, deconv.hpp:124-138
+  }
+  void* dwin = nullptr;
+  PACT_TRY(scratch_get(ctx, kScratchGeneric3, sizeof(float) * P2, &dwin));
+  PACT_CUDA(cudaMemcpyAsync(dwin, win.data(), sizeof(float) * P2, cudaMemcpyHostToDevice,
+                            ctx->stream));
+  PACT_TRY(launch_merge(ctx, *lay, patches, static_cast<const float*>(dwin), image));
+  PACT_CUDA(cudaStreamSynchronize(ctx->stream));  // `win` is released
+  return PACT_OK;
+}
+
 int pact_tv_loss(pact_ctx* ctx, const pact_grid* grid, const pact_mask* mask, const float* raster,
                  double lambda, double* value, float* grad_masked) {
   if (!ctx || !grid || !mask || !raster || !value || !grad_masked)

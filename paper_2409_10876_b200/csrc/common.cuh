@@ -65,6 +65,9 @@ struct pact_ctx {
   // Ray-plan cache of the standalone ray entry points (raymarch.cu).
   void* rays = nullptr;
   void (*rays_free)(void*) = nullptr;
+  // Further per-context caches, one slot per owner (pactgpu::ExtSlot).
+  void* ext[4] = {nullptr, nullptr, nullptr, nullptr};
+  void (*ext_free[4])(void*) = {nullptr, nullptr, nullptr, nullptr};
 };
 
 namespace pactgpu {
@@ -83,12 +86,39 @@ enum ScratchSlot {
 
 Status scratch_get(pact_ctx* ctx, int slot, size_t bytes, void** out);
 
+// Per-context cache slots (pact_ctx::ext): created on first use by their
+// owner, destroyed with the context.  Keeping them per context keeps them
+// per device and per stream (a cache shared across contexts could be
+// rewritten while another context's stream still reads it).
+enum ExtSlot {
+  kExtFourier = 0,   // fourier.cu: the table of pact_transfer_stack / pact_loss_grad
+  kExtComposed = 1,  // composed.cu: fp64 bin tables of the composed-path entry points
+};
+
+template <class T>
+T* ctx_ext(pact_ctx* ctx, int slot) {
+  if (!ctx->ext[slot]) {
+    ctx->ext[slot] = new T();
+    ctx->ext_free[slot] = [](void* p) { delete static_cast<T*>(p); };
+  }
+  return static_cast<T*>(ctx->ext[slot]);
+}
+
 // Stream-ordered device memory from the device's default pool, whose release
 // threshold is raised on first use: buffers freed by one trainer / entry point
 // are reused by the next without cudaMalloc / cudaFree (which synchronise the
 // device and, for GB-sized arenas, can stall for many milliseconds).
 Status pool_alloc(void** ptr, size_t bytes, cudaStream_t stream);
 void pool_free(void* ptr, cudaStream_t stream);
+
+// Opt a kernel in to `bytes` of dynamic shared memory on the CURRENT device.
+// The attribute is per device context, so the bookkeeping is per (device,
+// kernel); thread-safe (ctx.cu).
+Status smem_optin_raw(const void* func, size_t bytes);
+template <class F>
+Status smem_optin(F* func, size_t bytes) {
+  return smem_optin_raw(reinterpret_cast<const void*>(func), bytes);
+}
 
 // After every launch: count it and surface launch-configuration errors.
 inline Status after_launch(pact_ctx* ctx, const char* name) {

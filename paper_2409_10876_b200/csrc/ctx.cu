@@ -1,7 +1,9 @@
 // Context, error and memory entry points of include/pact_cuda.h.
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "common.cuh"
 
@@ -33,6 +35,21 @@ Status pool_alloc(void** ptr, size_t bytes, cudaStream_t stream) {
 
 void pool_free(void* ptr, cudaStream_t stream) {
   if (ptr) cudaFreeAsync(ptr, stream);
+}
+
+Status smem_optin_raw(const void* func, size_t bytes) {
+  if (bytes <= 48 * 1024) return {};
+  int dev = 0;
+  PACT_CUDA_S(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{dev, func}];
+  if (have >= bytes) return {};
+  PACT_CUDA_S(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(bytes)));
+  have = bytes;
+  return {};
 }
 
 Status scratch_get(pact_ctx* ctx, int slot, size_t bytes, void** out) {
@@ -93,6 +110,8 @@ int pact_ctx_destroy(pact_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   if (ctx->api && ctx->api_free) ctx->api_free(ctx->api);
   if (ctx->rays && ctx->rays_free) ctx->rays_free(ctx->rays);
+  for (int i = 0; i < 4; ++i)
+    if (ctx->ext[i] && ctx->ext_free[i]) ctx->ext_free[i](ctx->ext[i]);
   for (auto& s : ctx->scratch) pool_free(s.ptr, ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

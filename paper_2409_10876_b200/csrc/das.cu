@@ -256,13 +256,7 @@ Status launch_block(pact_ctx* ctx, DasArgs a, const double* c, int nsplit, dim3 
     dc.g[j] = static_cast<float>(-(cj - fl));
     dc.m[j] = kMagic - static_cast<float>(fl);
   }
-  static bool configured = false;  // per instantiation
-  if (!configured) {
-    PACT_CUDA_S(cudaFuncSetAttribute(das_stack_kernel<KB>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)kWindowSmem));
-    configured = true;
-  }
+  PACT_TRY_S(smem_optin(das_stack_kernel<KB>, kWindowSmem));
   grid.z = nsplit;
   das_stack_kernel<KB><<<grid, kThreads, smem, ctx->stream>>>(a, dc);
   return after_launch(ctx, "das_stack_kernel");

@@ -223,12 +223,7 @@ Status launch_patch_fft(pact_ctx* ctx, const pact_layout& lay, const float* stac
   const int P = lay.patch_pixels, logP = ilog2_exact(P);
   size_t smem = fft_smem(P, logP);
   if (smem > 220 * 1024) return validation("extract_patch_spectra: patch too large for the device FFT");
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    PACT_CUDA_S(cudaFuncSetAttribute(patch_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-    configured = smem;
-  }
+  PACT_TRY_S(smem_optin(patch_fft_kernel, smem));
   if (p_hi <= p_lo) return {};
   dim3 g(p_hi - p_lo, K);
   patch_fft_kernel<<<g, 512, smem, ctx->stream>>>(layout_dev(lay), stack, K, logP, Y, p_lo);
@@ -238,12 +233,7 @@ Status launch_patch_fft(pact_ctx* ctx, const pact_layout& lay, const float* stac
 Status launch_patch_ifft_real(pact_ctx* ctx, int P, int n_patches, const float2* X, float* out) {
   const int logP = ilog2_exact(P);
   size_t smem = fft_smem(P, logP);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    PACT_CUDA_S(cudaFuncSetAttribute(patch_ifft_real_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
-  }
+  PACT_TRY_S(smem_optin(patch_ifft_real_kernel, smem));
   patch_ifft_real_kernel<<<n_patches, 512, smem, ctx->stream>>>(P, logP, X, out);
   return after_launch(ctx, "patch_ifft_real_kernel");
 }

@@ -904,8 +904,16 @@ Status launch_wiener(pact_ctx* ctx, const FourierTab& t, const float2* Y, const 
 using namespace pactgpu;
 
 namespace {
-FourierTable g_tab_api;  // table cache for the standalone entry points
-}
+// Table cache of the standalone entry points, one per context (it is
+// rewritten in place when P, the pitch, the angles or the delays change, so it
+// must not be shared with another context's stream or device).
+struct ApiFourier {
+  FourierTable tab;
+  ~ApiFourier() { fourier_table_free(tab); }
+};
+
+FourierTable& api_table(pact_ctx* ctx) { return ctx_ext<ApiFourier>(ctx, kExtFourier)->tab; }
+}  // namespace
 
 extern "C" int pact_transfer_stack(pact_ctx* ctx, int32_t n_patches, const float* w,
                                    int32_t n_angles, const double* delays, int32_t K, int32_t P,
@@ -915,8 +923,9 @@ extern "C" int pact_transfer_stack(pact_ctx* ctx, int32_t n_patches, const float
   if (P < 1) return validation("transfer_stack: patch_pixels must be >= 1").code;
   if (!(pitch > 0.0)) return validation("transfer_stack: pitch must be > 0").code;
   if (n_angles < 1 || K < 1 || n_patches < 1) return validation("transfer_stack: empty input").code;
-  PACT_TRY(fourier_table(ctx, g_tab_api, P, pitch, n_angles, delays, K));
-  PACT_TRY(launch_transfer_stack(ctx, g_tab_api.tab, w, n_patches, reinterpret_cast<float2*>(H)));
+  FourierTable& tab = api_table(ctx);
+  PACT_TRY(fourier_table(ctx, tab, P, pitch, n_angles, delays, K));
+  PACT_TRY(launch_transfer_stack(ctx, tab.tab, w, n_patches, reinterpret_cast<float2*>(H)));
   return PACT_OK;
 }
 
@@ -929,8 +938,9 @@ extern "C" int pact_loss_grad(pact_ctx* ctx, int32_t n_patches, const float* Y, 
   if (K < 1) return validation("data_loss: no channels").code;
   if (n_patches < 1) return validation("data_loss: no patches").code;
   if (P < 1 || !(pitch > 0.0) || n_angles < 1) return validation("pact_loss_grad: bad geometry").code;
-  PACT_TRY(fourier_table(ctx, g_tab_api, P, pitch, n_angles, delays, K));
-  PACT_TRY(launch_loss_grad(ctx, g_tab_api.tab, reinterpret_cast<const float2*>(Y), w, n_patches,
+  FourierTable& tab = api_table(ctx);
+  PACT_TRY(fourier_table(ctx, tab, P, pitch, n_angles, delays, K));
+  PACT_TRY(launch_loss_grad(ctx, tab.tab, reinterpret_cast<const float2*>(Y), w, n_patches,
                             eps, scale, implicit != 0, loss_per_patch, dw));
   return PACT_OK;
 }

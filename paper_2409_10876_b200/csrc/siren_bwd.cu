@@ -581,12 +581,7 @@ constexpr size_t kBwdSmem = 1024 + sizeof(float) * (ND * 2 * kDa + NZ * 2 * kZ +
 
 template <int MODE>
 Status launch_bwd(pact_ctx* ctx, const BwdArgs& a, int grid) {
-  static bool cfg = false;
-  if (!cfg) {
-    PACT_CUDA_S(cudaFuncSetAttribute(tc_bwd_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kBwdSmem)));
-    cfg = true;
-  }
+  PACT_TRY_S(smem_optin(tc_bwd_kernel<MODE>, kBwdSmem));
   // X = dA_l (TOP: a_l) as a 2-D tensor [n][128] fp32, 32 x 32 SW128 boxes
   static PFN_cuTensorMapEncodeTiled encode = [] {
     void* fn = nullptr;

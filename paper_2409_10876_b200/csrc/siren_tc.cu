@@ -591,9 +591,7 @@ int tc_wgrad_rows(pact_ctx* ctx, int n) {
 Status tc_forward_layer(pact_ctx* ctx, int hidden, const float* Ain, const float* W,
                         const float* b, int n, float w0, float* Aout, const SirenHead& head) {
   if (hidden != H) return unsupported_width();
-  static bool cfg = false;
-  if (!cfg) PACT_TRY_S(set_smem(tc_layer_kernel<kForward>, kLayerSmem));
-  cfg = true;
+  PACT_TRY_S(smem_optin(tc_layer_kernel<kForward>, kLayerSmem));
   tc_layer_kernel<kForward><<<layer_grid(ctx, n), LayerRoles<kForward>::kThreads, kLayerSmem,
                               ctx->stream>>>(
       Ain, W, b, nullptr, n, w0, Aout, head);
@@ -603,9 +601,7 @@ Status tc_forward_layer(pact_ctx* ctx, int hidden, const float* Ain, const float
 Status tc_dgrad_layer(pact_ctx* ctx, int hidden, const float* dAl, const float* W,
                       const float* Aprev, int n, float w0, float* dAprev) {
   if (hidden != H) return unsupported_width();
-  static bool cfg = false;
-  if (!cfg) PACT_TRY_S(set_smem(tc_layer_kernel<kDgrad>, kLayerSmem));
-  cfg = true;
+  PACT_TRY_S(smem_optin(tc_layer_kernel<kDgrad>, kLayerSmem));
   tc_layer_kernel<kDgrad><<<layer_grid(ctx, n), LayerRoles<kDgrad>::kThreads, kLayerSmem,
                             ctx->stream>>>(
       dAl, W, nullptr, Aprev, n, w0, dAprev, SirenHead{});
@@ -615,9 +611,7 @@ Status tc_dgrad_layer(pact_ctx* ctx, int hidden, const float* dAl, const float* 
 Status tc_wgrad_layer(pact_ctx* ctx, int hidden, const float* dAl, const float* Aprev, int n,
                       int rows, float w0, float* partial, int n_chunks) {
   if (hidden != H) return unsupported_width();
-  static bool cfg = false;
-  if (!cfg) PACT_TRY_S(set_smem(tc_wgrad_kernel, kWgradSmem));
-  cfg = true;
+  PACT_TRY_S(smem_optin(tc_wgrad_kernel, kWgradSmem));
   tc_wgrad_kernel<<<n_chunks, WNTH, kWgradSmem, ctx->stream>>>(dAl, Aprev, n, rows, w0, partial);
   return after_launch(ctx, "tc_wgrad_kernel");
 }

@@ -483,13 +483,7 @@ PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
 template <int MODE>
 Status launch_wide(pact_ctx* ctx, const float* in, const float* planes, const float* bias,
                    const float* Aprev, int n, float w0, float* Y) {
-  static bool cfg = false;
-  if (!cfg) {
-    PACT_CUDA_S(cudaFuncSetAttribute(tc_wide_layer_kernel<MODE>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kWideSmem)));
-    cfg = true;
-  }
+  PACT_TRY_S(smem_optin(tc_wide_layer_kernel<MODE>, kWideSmem));
   auto encode = tensor_map_encoder();
   if (!encode) return internal_error("tc_wide_layer: cuTensorMapEncodeTiled unavailable");
   CUtensorMap tmap;
@@ -561,12 +555,7 @@ int tc_wide_wgrad_rows(pact_ctx* ctx, int n) {
 
 Status tc_wide_wgrad_layer(pact_ctx* ctx, const float* dAl, const float* Aprev, int n, int rows,
                            float w0, float* partial, int n_chunks) {
-  static bool cfg = false;
-  if (!cfg) {
-    PACT_CUDA_S(cudaFuncSetAttribute(tc_wide_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kWgradSmemW)));
-    cfg = true;
-  }
+  PACT_TRY_S(smem_optin(tc_wide_wgrad_kernel, kWgradSmemW));
   tc_wide_wgrad_kernel<<<n_chunks, kWideThreads, kWgradSmemW, ctx->stream>>>(dAl, Aprev, n, rows, w0,
                                                                               partial);
   return after_launch(ctx, "tc_wide_wgrad_kernel");

@@ -727,6 +727,10 @@ int pact_joint_reconstruct_batch(pact_ctx* ctx, int32_t n_frames, const pact_rin
   for (int f = 0; f < n_frames; ++f) {
     if (cfgs[f].epochs != epochs)
       return cleanup(validation("pact_joint_reconstruct_batch: frames need equal epochs").code);
+    // `thetas` is strided by one parameter count: every frame needs the same network
+    if (cfgs[f].hidden != cfgs[0].hidden || cfgs[f].sine_layers != cfgs[0].sine_layers)
+      return cleanup(
+          validation("pact_joint_reconstruct_batch: frames need the same SIREN shape").code);
     const pact_partition whole{0, 1};
     int rc = trainer_create(ctx, ring, meta, signals[f], grid, mask, &cfgs[f], &whole, &trs[f],
                             false);

@@ -61,6 +61,78 @@ struct TrainConfig {
   }
 };
 
+struct PatchLossResult {
+  double value = 0.0;
+  std::vector<std::vector<cplx>> grad_h;  // dL/dRe H + j dL/dIm H, per delay per bin
+};
+
+/// patch_data_loss (optimize.hpp:155-211): |k|-weighted residual loss of one
+/// patch and its gradient w.r.t. H (explicit + optional implicit term through
+/// X-hat), fp64 on the GPU.  YScalar is float (the training cache) or double.
+template <typename YScalar>
+PatchLossResult patch_data_loss(const std::vector<std::vector<std::complex<YScalar>>>& Y,
+                                const TransferStack& H, double eps, double scale,
+                                bool implicit_grad) {
+  const size_t M = Y.size();
+  if (M != H.spectra.size()) throw ValidationError("data_loss: Y/H channel mismatch");
+  if (M == 0) throw ValidationError("data_loss: no channels");
+  const int P = H.patch_pixels;
+  const size_t P2 = static_cast<size_t>(P) * P;
+  std::vector<cplx> y;
+  y.reserve(M * P2);
+  for (const auto& c : Y) {
+    if (c.size() != P2) throw ValidationError("data_loss: Y/H channel mismatch");
+    for (const auto& v : c) y.push_back(cplx(v));
+  }
+  cuda::Buffer<double> dY(2 * M * P2), dH(2 * M * P2), dG(2 * M * P2), loss(1);
+  cuda::check(pact_upload(cuda::context(), dY.ptr, y.data(), sizeof(cplx) * y.size()));
+  detail::upload_c128(dH, H.spectra);
+  cuda::check(pact_patch_data_loss(cuda::context(), 1, static_cast<int>(M), P, H.pitch, dY.ptr,
+                                   dH.ptr, eps, scale, implicit_grad ? 1 : 0, loss.ptr, dG.ptr));
+  PatchLossResult res;
+  loss.download(&res.value);
+  std::vector<cplx> g(M * P2);
+  dG.download(reinterpret_cast<double*>(g.data()));
+  for (size_t j = 0; j < M; ++j) res.grad_h.emplace_back(g.begin() + j * P2, g.begin() + (j + 1) * P2);
+  return res;
+}
+
+struct DataLossResult {
+  double value = 0.0;
+  std::vector<std::vector<std::vector<cplx>>> grad_h;  // per patch, per delay, per bin
+};
+
+/// data_loss (optimize.hpp:329-353): all patches, normalised by N * M * P^2.
+inline DataLossResult data_loss(const std::vector<PatchSpectra>& ys,
+                                const std::vector<TransferStack>& hs, double eps,
+                                bool implicit_grad = true) {
+  if (ys.size() != hs.size()) throw ValidationError("data_loss: patch count mismatch");
+  if (ys.empty()) throw ValidationError("data_loss: no patches");
+  const size_t N = ys.size(), M = ys[0].Y.size();
+  const int P = hs[0].patch_pixels;
+  const size_t P2 = static_cast<size_t>(P) * P, per = 2 * M * P2;
+  for (size_t i = 0; i < N; ++i)
+    if (ys[i].Y.size() != M || hs[i].spectra.size() != M)
+      throw ValidationError("data_loss: Y/H channel mismatch");
+  if (M == 0) throw ValidationError("data_loss: no channels");
+  cuda::Buffer<double> dY(per * N), dH(per * N), dG(per * N);
+  for (size_t i = 0; i < N; ++i) {
+    detail::upload_c128(dY, ys[i].Y, i * per);
+    detail::upload_c128(dH, hs[i].spectra, i * per);
+  }
+  DataLossResult out;
+  cuda::check(pact_data_loss(cuda::context(), static_cast<int>(N), static_cast<int>(M), P,
+                             hs[0].pitch, dY.ptr, dH.ptr, eps, implicit_grad ? 1 : 0, &out.value,
+                             nullptr, dG.ptr));
+  std::vector<cplx> g(N * M * P2);
+  dG.download(reinterpret_cast<double*>(g.data()));
+  out.grad_h.resize(N);
+  for (size_t i = 0; i < N; ++i)
+    for (size_t j = 0; j < M; ++j)
+      out.grad_h[i].emplace_back(g.begin() + (i * M + j) * P2, g.begin() + (i * M + j + 1) * P2);
+  return out;
+}
+
 struct AdamState {
   std::vector<double> m, v;
   long t = 0;

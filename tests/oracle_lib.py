@@ -282,6 +282,96 @@ class Oracle:
         out["grad_v_masked"] = out["grad_v_masked"][:nm]
         return out
 
+    # -- composed (non-fused) path, one patch per call (ref_shim.cpp) -----
+    def _fn(self, name, args, res=C.c_int):
+        fn = getattr(self.lib, self.prefix + name)
+        fn.argtypes = args
+        fn.restype = res
+        return fn
+
+    def _ok(self, name, rc):
+        if rc != 0:
+            raise RuntimeError(f"{self.prefix}{name} failed ({rc}): {self.last_error()}")
+
+    def multichannel_deconvolve(self, Y, H, eps):
+        """Y, H complex128 [K, P, P] -> X complex128 [P, P]."""
+        Y = np.ascontiguousarray(Y, np.complex128)
+        H = np.ascontiguousarray(H, np.complex128)
+        K, P = Y.shape[0], Y.shape[1]
+        X = np.zeros((P, P), np.complex128)
+        self._ok("multichannel_deconvolve", self._fn("multichannel_deconvolve",
+                 [_I, _I, _P, _P, _D, _P])(K, P, _p(Y), _p(H), eps, _p(X)))
+        return X
+
+    def deconv_jacobian_H(self, Y, H, eps, j, b):
+        Y = np.ascontiguousarray(Y, np.complex128)
+        H = np.ascontiguousarray(H, np.complex128)
+        out = np.zeros(4)
+        self._ok("deconv_jacobian_H", self._fn("deconv_jacobian_H",
+                 [_I, _I, _P, _P, _D, _I, _I, _P])(Y.shape[0], Y.shape[1], _p(Y), _p(H), eps, j, b,
+                                                   _p(out)))
+        return complex(out[0], out[1]), complex(out[2], out[3])
+
+    def patch_data_loss(self, Y, H, pitch, eps, scale, implicit=True):
+        Y = np.ascontiguousarray(Y, np.complex128)
+        H = np.ascontiguousarray(H, np.complex128)
+        loss = C.c_double()
+        g = np.zeros_like(Y)
+        self._ok("patch_data_loss", self._fn("patch_data_loss",
+                 [_I, _I, _D, _P, _P, _D, _D, _I, _P, _P])(
+                     Y.shape[0], Y.shape[1], pitch, _p(Y), _p(H), eps, scale, 1 if implicit else 0,
+                     C.byref(loss), _p(g)))
+        return loss.value, g
+
+    def data_loss(self, Y, H, pitch, eps, implicit=True):
+        """Y, H complex128 [n, K, P, P] -> (value, grad_h)."""
+        Y = np.ascontiguousarray(Y, np.complex128)
+        H = np.ascontiguousarray(H, np.complex128)
+        val = C.c_double()
+        g = np.zeros_like(Y)
+        self._ok("data_loss", self._fn("data_loss", [_I, _I, _I, _D, _P, _P, _D, _I, _P, _P])(
+            Y.shape[0], Y.shape[1], Y.shape[2], pitch, _p(Y), _p(H), eps, 1 if implicit else 0,
+            C.byref(val), _p(g)))
+        return val.value, g
+
+    def transfer_grad_to_wavefront(self, w, delays, P, pitch, grad_h):
+        w = _f64(w)
+        d = _f64(delays)
+        g = np.ascontiguousarray(grad_h, np.complex128)
+        dw = np.zeros(len(w))
+        self._ok("transfer_grad_to_wavefront", self._fn("transfer_grad_to_wavefront",
+                 [_I, _P, _I, _P, _I, _D, _P, _P])(len(w), _p(w), len(d), _p(d), P, pitch, _p(g),
+                                                   _p(dw)))
+        return dw
+
+    def wavefront_jacobian(self, center, ring, grid, sos, v0, mask, n_angles, step, dw=None,
+                           grad_v=None):
+        """-> (w [A], counts [A], pixel, dw_dv[, grad_v after J^T dw])."""
+        s = _f64(sos)
+        fn = self._fn("wavefront_jacobian", [_D, _D, _I, _D, _D, _I, _I, _D, _D, _D, _P, _D, _D, _D,
+                                             _D, _I, _D, _P, _P, _P, _P, C.c_long, _P, _P])
+        w = np.zeros(n_angles)
+        counts = np.zeros(n_angles, np.int64)
+        args = (float(center[0]), float(center[1]), *_r(ring), *_g(grid), _p(s), v0, *_m(mask),
+                n_angles, step)
+        self._ok("wavefront_jacobian", fn(*args, _p(w), _p(counts), None, None, 0, None, None))
+        nnz = int(counts.sum())
+        pix = np.zeros(max(nnz, 1), np.int32)
+        val = np.zeros(max(nnz, 1), np.float32)
+        gv = None
+        if dw is not None:
+            gv = np.zeros((grid.height, grid.width)) if grad_v is None else _f64(grad_v).copy()
+        self._ok("wavefront_jacobian", fn(*args, _p(w), _p(counts), _p(pix), _p(val), nnz,
+                                          None if dw is None else _p(_f64(dw)), _p(gv)))
+        return w, counts, pix[:nnz], val[:nnz], gv
+
+    def merge_patches(self, grid, patch_mm, overlap, patches, fwhm):
+        ps = _f64(patches)
+        img = np.zeros((grid.height, grid.width))
+        self._ok("merge_patches", self._fn("merge_patches", [_I, _I, _D, _D, _D, _D, _D, _P, _D, _P])(
+            *_g(grid), patch_mm, overlap, _p(ps), fwhm, _p(img)))
+        return img
+
     # -- CPU-baseline session (ref_shim.cpp ref_nf_session_*) -----------
     def nf_session(self, sig, ring, meta, grid, mask, cfg):
         """joint_reconstruct's one-time setup (optimize.hpp:374-405), once;
