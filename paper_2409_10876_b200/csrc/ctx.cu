@@ -38,7 +38,8 @@ void pool_free(void* ptr, cudaStream_t stream) {
 }
 
 Status smem_optin_raw(const void* func, size_t bytes) {
-  if (bytes <= 48 * 1024) return {};
+  // (no small-size shortcut: a kernel with static shared memory needs the
+  // opt-in even when its dynamic part is <= 48 KB)
   int dev = 0;
   PACT_CUDA_S(cudaGetDevice(&dev));
   static std::mutex mu;

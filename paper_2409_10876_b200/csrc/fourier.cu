@@ -15,6 +15,7 @@
 // table (deterministic; no atomics).  The loss is reduced per patch in fp64.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include <memory>
@@ -587,6 +588,108 @@ __global__ void __launch_bounds__(2 * LB) loss_bins_kernel(FourierTab t, const f
   }
 }
 
+// Register form of kernel A (K = NS * JPL): NS lanes share a bin, each holding
+// JPL of its K spectra in registers, loaded straight from HBM with streaming
+// loads (no shared-memory stage, so occupancy is set by registers only and
+// every warp keeps JPL 128-B loads in flight).  Lane l of a warp: bin
+// l % (32 / NS), delay group l / (32 / NS); a group's lanes read consecutive
+// bins of one delay row (coalesced 128-B lines).  The per-bin chain is
+// bin_chain_real's closed form with the group sums combined by fixed xor
+// shuffles.  Nyquist bins (even P) are not evaluated here: their lanes copy
+// their spectra into the compact exchange layout ynyq [patch][slot][K] so
+// that kernel A' reads them contiguously instead of one sector per bin.
+template <int NS, int JPL>
+__global__ void __launch_bounds__(256, 4) loss_reg_kernel(FourierTab t, const float2* __restrict__ Y_all,
+                                                       const float* __restrict__ w_all, float eps_m,
+                                                       float scale, int implicit,
+                                                       float2* __restrict__ gbuf,
+                                                       float2* __restrict__ ynyq,
+                                                       double* __restrict__ loss_part, int n_parts) {
+  constexpr int BPW = 32 / NS, BPB = 8 * BPW, K = NS * JPL;
+  __shared__ double s_red[8];
+  const int P2 = t.P2, lane = threadIdx.x & 31;
+  const int grp = lane / BPW, bi = lane - grp * BPW;
+  const int chunks = (P2 + BPB - 1) / BPB;
+  const int patch = blockIdx.x / chunks, cb = blockIdx.x - patch * chunks;
+  const int b0 = cb * BPB + (threadIdx.x >> 5) * BPW + bi;
+  const bool valid = b0 < P2;
+  const int b = valid ? b0 : P2 - 1;
+  const int j0 = grp * JPL;
+  const float2* Y = Y_all + (static_cast<size_t>(patch) * K + j0) * P2 + b;
+  float2 y[JPL];
+#pragma unroll
+  for (int u = 0; u < JPL; ++u) y[u] = __ldcs(Y + static_cast<size_t>(u) * P2);
+  auto gsum = [&](float v) {
+#pragma unroll
+    for (int o = BPW; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
+  const int m = t.mirror[b];
+  if (m >= 0 && valid) {  // Nyquist bin: hand its spectra to kernel A'
+    float2* dst = ynyq + (static_cast<size_t>(patch) * (2 * t.P - 1) + nyq_slot(b, t.P)) * K + j0;
+#pragma unroll
+    for (int u = 0; u < JPL; ++u) dst[u] = y[u];
+  }
+  const float k = t.kmag[b];
+  const float wk = k * scale;
+  const float* w = w_all + static_cast<size_t>(patch) * t.A;
+  const int4 ix = t.idx[b];
+  const float2 fr = t.frac[b];
+  const float w1 = (1.f - fr.x) * __ldg(w + ix.x) + fr.x * __ldg(w + ix.y);
+  const float w2 = (1.f - fr.y) * __ldg(w + ix.z) + fr.y * __ldg(w + ix.w);
+  float sn, cs;
+  sincosf(k * (0.5f * (w1 + w2)), &sn, &cs);
+  const float2 ew = make_float2(cs, -sn);  // exp(-i|k| wbar)
+  // z_j = conj(dp_j) exp(-i|k| wbar) = exp(i|k|(d_j - wbar)): c_j = Re z_j, s_j = Im z_j
+  const bool walk = t.rho != nullptr;
+  const float2 rr = walk ? conjf2(t.rho[b]) : make_float2(1.f, 0.f);
+  // the phases are walked twice (pass 1, pass 2) rather than kept: registers
+  // hold the spectra only
+  const float2 z0 = cmul(conjf2(t.dp[j0 * P2 + b]), ew);
+  auto znext = [&](int u, float2 z) {
+    return walk ? cmul(z, rr) : cmul(conjf2(t.dp[(j0 + u + 1) * P2 + b]), ew);
+  };
+  float Sx = 0.f, Sy = 0.f, den = 0.f;
+  {
+    float2 z = z0;
+#pragma unroll
+    for (int u = 0; u < JPL; ++u) {
+      Sx = fmaf(z.x, y[u].x, Sx);
+      Sy = fmaf(z.x, y[u].y, Sy);
+      den = fmaf(z.x, z.x, den);
+      if (u + 1 < JPL) z = znext(u, z);
+    }
+  }
+  Sx = gsum(Sx);
+  Sy = gsum(Sy);
+  den = eps_m + gsum(den);
+  const float inv = den > 0.f ? 1.f / den : 0.f;
+  const float2 X = make_float2(Sx * inv, Sy * inv);
+  const float al = implicit && den > 0.f ? eps_m * inv : 0.f;
+  const float be = 2.f * al * (X.x * X.x + X.y * X.y);
+  float acc = 0.f, gs = 0.f;
+  {
+    float2 z = z0;
+#pragma unroll
+    for (int u = 0; u < JPL; ++u) {
+      const float rx = fmaf(-z.x, X.x, y[u].x), ry = fmaf(-z.x, X.y, y[u].y);
+      acc = fmaf(rx, rx, fmaf(ry, ry, acc));
+      const float dc = fmaf(rx, X.x, ry * X.y) + al * fmaf(X.x, y[u].x, X.y * y[u].y) - be * z.x;
+      gs = fmaf(dc, z.y, gs);
+      if (u + 1 < JPL) z = znext(u, z);
+    }
+  }
+  acc = gsum(acc);
+  gs = gsum(gs);
+  const bool ordinary = valid && m < 0 && wk != 0.f;
+  if (grp == 0 && valid && m < 0) {
+    const float G = ordinary ? -wk * k * gs : 0.f;  // (1/2) dL/dwbar, for w1 and for w2
+    gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G, G);
+  }
+  const double value = ordinary && grp == 0 ? static_cast<double>(wk) * acc : 0.0;
+  block_sum_store(value, s_red, loss_part + patch * n_parts + cb);
+}
+
 // Small patches (P^2 < LB or not a multiple of LB): one CTA per (patch, chunk).
 __global__ void __launch_bounds__(LB) loss_bins_small_kernel(FourierTab t, const float2* __restrict__ Y_all,
                                                              const float* __restrict__ w_all,
@@ -649,6 +752,7 @@ constexpr int kTps = 4;
 __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const float2* __restrict__ Y_all,
                                                             const float* __restrict__ w_all,
                                                             float eps_m, float scale, int implicit,
+                                                            const float2* __restrict__ ynyq,
                                                             float2* __restrict__ nyq_all,
                                                             float2* __restrict__ gbuf,
                                                             double* __restrict__ loss_part,
@@ -666,8 +770,14 @@ __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const 
                         : nyq_all + static_cast<size_t>(patch) * S * K;
   for (int a = threadIdx.x; a < t.A; a += blockDim.x) s_w[a] = w_all[patch * t.A + a];
   const float2* Y = Y_all + static_cast<size_t>(patch) * K * P2;
-  // the slots' spectra, eight loads in flight per thread
-  for (int e0 = threadIdx.x; stage_y && e0 < K * S; e0 += 8 * blockDim.x) {
+  // the slots' spectra: from the compact [slot][K] copy kernel A made, or
+  // (other kernel A forms) gathered from Y, eight loads in flight per thread
+  const float2* Yc = ynyq ? ynyq + static_cast<size_t>(patch) * S * K : nullptr;
+  for (int e = threadIdx.x; Yc && stage_y && e < K * S; e += blockDim.x) {
+    const int q = e / K, j = e - q * K;
+    s_y[j * S + q] = Yc[e];
+  }
+  for (int e0 = threadIdx.x; !Yc && stage_y && e0 < K * S; e0 += 8 * blockDim.x) {
     float2 v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -689,7 +799,8 @@ __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const 
   const float k = t.kmag[b];
   const bool live = active && k * scale != 0.f;
   auto y_of = [&](int j) {
-    return stage_y ? s_y[j * S + slot] : Y[static_cast<size_t>(j) * P2 + b];
+    return stage_y ? s_y[j * S + slot]
+                   : (Yc ? Yc[static_cast<size_t>(slot) * K + j] : Y[static_cast<size_t>(j) * P2 + b]);
   };
   auto group_sum = [&](float v) {
 #pragma unroll
@@ -747,7 +858,7 @@ __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const 
       const float2 r = make_float2(y.x - hx.x, y.y - hx.y);
       acc += r.x * r.x + r.y * r.y;
       const float2 g = bin_grad(L, h, y, implicit != 0);
-      if (active) s_g[static_cast<size_t>(slot) * K + j] = live ? g : make_float2(0.f, 0.f);
+      if (active) s_g[static_cast<size_t>(j) * S + slot] = live ? g : make_float2(0.f, 0.f);
       next(j, db, dm);
     }
   }
@@ -761,7 +872,7 @@ __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const 
     const int sm = nyq_slot(m, t.P);
     float2 db = db0, dm = dm0;
     for (int j = j0; j < j1; ++j) {
-      const float2 gb = s_g[slot * K + j], gm = s_g[sm * K + j];
+      const float2 gb = s_g[j * S + slot], gm = s_g[j * S + sm];
       const float2 gs = make_float2(0.5f * (gb.x + gm.x), 0.5f * (gb.y - gm.y));
       pullback(gs, db, e1b, e2b, k, G1, G2);
       next(j, db, dm);
@@ -830,46 +941,69 @@ Status launch_transfer_stack(pact_ctx* ctx, const FourierTab& t, const float* w,
   return after_launch(ctx, "transfer_stack_kernel");
 }
 
+// Kernel A of the register form for (NS, JPL) with K = NS * JPL, or null.
+using LossRegFn = void (*)(FourierTab, const float2*, const float*, float, float, int, float2*,
+                           float2*, double*, int);
+LossRegFn loss_reg_for(int K, int& ns) {
+  // PACT_LOSS_STAGED=1 selects the shared-memory staged kernel A (comparisons)
+  static const bool staged = [] {
+    const char* e = std::getenv("PACT_LOSS_STAGED");
+    return e && e[0] == '1';
+  }();
+  if (staged) return nullptr;
+  switch (K) {
+    case 4: ns = 1; return loss_reg_kernel<1, 4>;
+    case 8: ns = 1; return loss_reg_kernel<1, 8>;
+    case 16: ns = 1; return loss_reg_kernel<1, 16>;
+    case 32: ns = 2; return loss_reg_kernel<2, 16>;
+    case 64: ns = 4; return loss_reg_kernel<4, 16>;
+    default: return nullptr;
+  }
+}
+
 Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, const float* w,
                         int n_patches, double eps, double scale, bool implicit, double* loss,
                         float* dw) {
   const size_t smem = sizeof(float) * t.A;
-  const int chunks = div_up(t.P2, LB);
+  int ns = 0;
+  const LossRegFn reg = loss_reg_for(t.K, ns);
+  const int bpb = reg ? 8 * 32 / ns : LB;  // bins per kernel-A block
+  const int chunks = div_up(t.P2, bpb);
   const int nyq_chunks = t.P % 2 == 0 ? 1 : 0;
   const int n_parts = chunks + nyq_chunks;  // per-patch loss partials, summed in order
-  // scratch: Nyquist dL/dH exchange [patch][2P-1][K] | (G1, G2) [patch][P2] | chunk losses
+  // scratch: Nyquist dL/dH exchange [patch][2P-1][K] | compact Nyquist spectra
+  // [patch][2P-1][K] | (G1, G2) [patch][P2] | chunk losses
   const size_t n_nyq = static_cast<size_t>(n_patches) * (2 * t.P) * t.K;
   const size_t n_g = static_cast<size_t>(n_patches) * t.P2;
   void* base = nullptr;
   PACT_TRY_S(scratch_get(ctx, kScratchNyq,
-                         sizeof(float2) * (n_nyq + n_g) + sizeof(double) * n_patches * n_parts + 256,
+                         sizeof(float2) * (2 * n_nyq + n_g) + sizeof(double) * n_patches * n_parts +
+                             256,
                          &base));
   float2* nyq = static_cast<float2*>(base);
-  float2* gbuf = nyq + n_nyq;
+  float2* ynyq = nyq + n_nyq;
+  float2* gbuf = ynyq + n_nyq;
   double* part = reinterpret_cast<double*>(gbuf + n_g);
   const float eps_m = static_cast<float>(eps * t.K), sc = static_cast<float>(scale);
-  if (t.P2 % LB == 0 && t.K * LB * 8 <= 96 * 1024) {
+  if (reg) {
+    reg<<<n_patches * chunks, 256, 0, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, gbuf, ynyq,
+                                                     part, n_parts);
+  } else if (t.P2 % LB == 0 && t.K * LB * 8 <= 96 * 1024) {
     const size_t stage = sizeof(float) * (2 * t.K * LB + ((t.A + 3) & ~3));
     const size_t smem_bins = 2 * stage;
-    if (smem_bins > 48 * 1024)
-      PACT_CUDA_S(cudaFuncSetAttribute(loss_bins_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem_bins)));
+    PACT_TRY_S(smem_optin(loss_bins_kernel, smem_bins));
     const int per_sm = std::max(1, static_cast<int>((227 * 1024 - 4096) / smem_bins));
     const int grid = std::min(n_patches * chunks, ctx->num_sms * per_sm);
     loss_bins_kernel<<<grid, 2 * LB, smem_bins, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, gbuf,
                                                                 part, n_parts, n_patches);
   } else {
     const size_t smem_bins = sizeof(float2) * t.K * LB + smem;
-    if (smem_bins > 48 * 1024) {
-      if (smem_bins > 200 * 1024) return validation("fused loss: too many delays for one bin chunk");
-      PACT_CUDA_S(cudaFuncSetAttribute(loss_bins_small_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem_bins)));
-    }
+    if (smem_bins > 200 * 1024) return validation("fused loss: too many delays for one bin chunk");
+    PACT_TRY_S(smem_optin(loss_bins_small_kernel, smem_bins));
     loss_bins_small_kernel<<<dim3(n_patches, chunks), LB, smem_bins, ctx->stream>>>(
         t, Y, w, eps_m, sc, implicit, gbuf, part, n_parts);
   }
-  PACT_TRY_S(after_launch(ctx, "loss_bins_kernel"));
+  PACT_TRY_S(after_launch(ctx, reg ? "loss_reg_kernel" : "loss_bins_kernel"));
   if (t.P % 2 == 0) {
     const int S = 2 * t.P - 1, nt = div_up(S * kTps, 32) * 32;
     if (nt > 1024) return validation("fused loss: patch size too large for the Nyquist kernel");
@@ -877,13 +1011,10 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
     const int stage_y = base + 2 * plane <= 200 * 1024;
     const int stage_g = base + (stage_y ? 2 : 1) * plane <= 200 * 1024;
     const size_t smem_nyq = base + (stage_y + stage_g) * plane;
-    if (smem_nyq > 48 * 1024) {
-      PACT_CUDA_S(cudaFuncSetAttribute(loss_nyquist_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem_nyq)));
-    }
+    PACT_TRY_S(smem_optin(loss_nyquist_kernel, smem_nyq));
     loss_nyquist_kernel<<<n_patches, nt, smem_nyq, ctx->stream>>>(
-        t, Y, w, eps_m, sc, implicit, nyq, gbuf, part, n_parts, chunks, stage_y, stage_g, loss, dw);
+        t, Y, w, eps_m, sc, implicit, reg ? ynyq : nullptr, nyq, gbuf, part, n_parts, chunks,
+        stage_y, stage_g, loss, dw);
     return after_launch(ctx, "loss_nyquist_kernel");
   }
   loss_finish_kernel<<<div_up(n_patches * t.A, 256), 256, 0, ctx->stream>>>(t, gbuf, part, n_parts,
