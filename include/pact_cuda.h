@@ -356,6 +356,15 @@ int pact_accumulate_wavefront_grad(pact_ctx* ctx, int64_t n_rows, const int64_t*
                                    const int32_t* pixel, const float* dw_dv, const double* dw,
                                    double* grad_v);
 
+/* psf_from_transfer, aberration.hpp:407-445, batched (fp64): the real,
+ * centred spatial PSF of each conjugate-symmetric P x P transfer spectrum
+ * (zero lag at pixel (P/2, P/2)), with the reference's symmetry check
+ * (ValidationError) and imaginary-residue check (NumericalError), applied to
+ * the spectra in order; the message carries the reference's text.
+ *   spectra : device complex128 [n][P][P];  psf : device fp64 [n][P][P] */
+int pact_psf_from_transfer(pact_ctx* ctx, int32_t n_spectra, int32_t P, const double* spectra,
+                           double* psf);
+
 /* wavefront_grad_trace, aberration.hpp:333-361, batched: grad_v (device fp64
  * [H][W]) += sum over rays of dL/dw * dl * v0 / v^2 * bilinear weight. */
 int pact_ray_backward(pact_ctx* ctx, const pact_ring* ring, const pact_grid* grid,

@@ -163,6 +163,7 @@ SIGNATURES = {
                                           C.POINTER(Mask), _I, _DP, _I, _D, _P, _P, _P, _P,
                                           C.c_int64, C.POINTER(C.c_int64)]),
     "pact_accumulate_wavefront_grad": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P]),
+    "pact_psf_from_transfer": (C.c_int, [_P, _I, _I, _P, _P]),
     "pact_adam_step": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, C.c_int64, _D, _D, _D, _D]),
     "pact_train_config_default": (C.c_int, [C.POINTER(TrainConfig)]),
     "pact_trainer_create": (C.c_int, [_P, C.POINTER(Ring), C.POINTER(SignalMeta), _P,

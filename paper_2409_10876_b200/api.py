@@ -520,6 +520,16 @@ def _ctx_methods():
                                                         dptr(dw.contiguous()), dptr(grad_v)))
         return grad_v
 
+    def psf_from_transfer(self, spectra: torch.Tensor) -> torch.Tensor:
+        """psf_from_transfer, aberration.hpp:407-445, batched (fp64): complex128
+        [n, P, P] conjugate-symmetric spectra -> centred real PSFs fp64 [n, P, P]
+        (zero lag at (P/2, P/2); the raster origin is -(P/2) pitch)."""
+        S = _c128(spectra, "spectra", 3)
+        n, P, _ = S.shape
+        out = torch.empty((n, P, P), device="cuda", dtype=torch.float64)
+        check(_abi.lib().pact_psf_from_transfer(self._h, n, P, dptr(S), dptr(out)))
+        return out
+
     def merge_patches(self, layout: PatchLayout, patches: torch.Tensor, fwhm: float) -> torch.Tensor:
         """merge_patches + MergeWindow, deconv.hpp:118-164: fp32 [n, P, P] -> fp32 [H, W]."""
         P = layout.patch_pixels
@@ -537,7 +547,7 @@ def _ctx_methods():
               deconvolve_image, loss_grad, ray_backward, tv_loss, adam_step,
               multichannel_deconvolve, deconv_jacobian_H, patch_data_loss, data_loss,
               transfer_grad_to_wavefront, wavefront_jacobian, accumulate_wavefront_grad,
-              merge_patches):
+              merge_patches, psf_from_transfer):
         setattr(Context, f.__name__, f)
 
 

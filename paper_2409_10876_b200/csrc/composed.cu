@@ -432,6 +432,60 @@ __global__ void accumulate_jt64_kernel(int64_t n_rows, const int64_t* __restrict
     atomicAdd(grad_v + pixel[e], g * static_cast<double>(dwdv[e]));
 }
 
+// ---- psf_from_transfer (aberration.hpp:407-445), batched, fp64 ----------
+// Stats per spectrum (atomicMax on the bit patterns of non-negative doubles,
+// which order like unsigned integers): [max |S|, max asymmetry, max |Re|, max |Im|].
+__device__ __forceinline__ void dmax(double* p, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+// pass 1, one thread per (spectrum, bin): symmetry statistics, and the row
+// transform R[y][x] = sum_k S[y][k] e^{+2 pi i k x / P} (fft::inverse_2d
+// transforms rows first, fft.hpp:107-115)
+__global__ void psf_rows64_kernel(const double2* __restrict__ S, int P, double2* __restrict__ R,
+                                  double* __restrict__ stats) {
+  const int P2 = P * P, e = blockIdx.x * blockDim.x + threadIdx.x, n = blockIdx.y;
+  if (e >= P2) return;
+  const int y = e / P, x = e - y * P;
+  const double2* s = S + static_cast<size_t>(n) * P2;
+  const double2 a = s[e], b = s[((P - y) % P) * P + (P - x) % P];
+  dmax(stats + 4 * n, hypot(a.x, a.y));
+  dmax(stats + 4 * n + 1, hypot(a.x - b.x, a.y + b.y));  // |S_i - conj(S_j)|
+  double re = 0.0, im = 0.0;
+  for (int k = 0; k < P; ++k) {
+    double sn, cs;
+    sincospi(2.0 * ((k * x) % P) / P, &sn, &cs);
+    const double2 v = s[y * P + k];
+    re += v.x * cs - v.y * sn;
+    im += v.x * sn + v.y * cs;
+  }
+  R[static_cast<size_t>(n) * P2 + e] = make_double2(re, im);
+}
+
+// pass 2: the column transform, the 1 / P^2 scale, the residue statistics and
+// the centred placement psf[(y + P/2) % P][(x + P/2) % P] = Re
+__global__ void psf_cols64_kernel(const double2* __restrict__ R, int P, double* __restrict__ psf,
+                                  double* __restrict__ stats) {
+  const int P2 = P * P, e = blockIdx.x * blockDim.x + threadIdx.x, n = blockIdx.y;
+  if (e >= P2) return;
+  const int y = e / P, x = e - y * P;
+  const double2* r = R + static_cast<size_t>(n) * P2;
+  double re = 0.0, im = 0.0;
+  for (int k = 0; k < P; ++k) {
+    double sn, cs;
+    sincospi(2.0 * ((k * y) % P) / P, &sn, &cs);
+    const double2 v = r[k * P + x];
+    re += v.x * cs - v.y * sn;
+    im += v.x * sn + v.y * cs;
+  }
+  const double inv = 1.0 / (static_cast<double>(P) * P);
+  re *= inv;
+  im *= inv;
+  dmax(stats + 4 * n + 2, fabs(re));
+  dmax(stats + 4 * n + 3, fabs(im));
+  psf[static_cast<size_t>(n) * P2 + ((y + P / 2) % P) * P + (x + P / 2) % P] = re;
+}
+
 }  // namespace
 }  // namespace pactgpu
 
@@ -604,5 +658,44 @@ extern "C" int pact_accumulate_wavefront_grad(pact_ctx* ctx, int64_t n_rows,
   accumulate_jt64_kernel<<<static_cast<unsigned>((n_rows + 255) / 256), 256, 0, ctx->stream>>>(
       n_rows, row_start, pixel, dw_dv, dw, grad_v);
   PACT_TRY(after_launch(ctx, "accumulate_jt64_kernel"));
+  return PACT_OK;
+}
+
+extern "C" int pact_psf_from_transfer(pact_ctx* ctx, int32_t n_spectra, int32_t P,
+                                      const double* spectra, double* psf) {
+  if (!ctx || !spectra || !psf) return validation("pact_psf_from_transfer: null argument").code;
+  if (P < 1 || n_spectra < 0) return validation("psf_from_transfer: spectrum size mismatch").code;
+  if (n_spectra == 0) return PACT_OK;
+  const int P2 = P * P;
+  void* st = nullptr;
+  void* R = nullptr;
+  PACT_TRY(scratch_get(ctx, kScratchGeneric3, sizeof(double) * 4 * n_spectra, &st));
+  PACT_TRY(scratch_get(ctx, kScratchGeneric2, sizeof(double2) * static_cast<size_t>(n_spectra) * P2,
+                       &R));
+  PACT_CUDA(cudaMemsetAsync(st, 0, sizeof(double) * 4 * n_spectra, ctx->stream));
+  const dim3 g(div_up(P2, 128), n_spectra);
+  psf_rows64_kernel<<<g, 128, 0, ctx->stream>>>(reinterpret_cast<const double2*>(spectra), P,
+                                                static_cast<double2*>(R), static_cast<double*>(st));
+  PACT_TRY(after_launch(ctx, "psf_rows64_kernel"));
+  psf_cols64_kernel<<<g, 128, 0, ctx->stream>>>(static_cast<const double2*>(R), P, psf,
+                                                static_cast<double*>(st));
+  PACT_TRY(after_launch(ctx, "psf_cols64_kernel"));
+  std::vector<double> h(4 * static_cast<size_t>(n_spectra));
+  PACT_CUDA(cudaMemcpyAsync(h.data(), st, sizeof(double) * h.size(), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  PACT_CUDA(cudaStreamSynchronize(ctx->stream));
+  // the reference's checks and messages, spectrum by spectrum in order
+  for (int i = 0; i < n_spectra; ++i) {
+    const double max_mag = h[4 * i], asym = h[4 * i + 1], max_real = h[4 * i + 2],
+                 max_imag = h[4 * i + 3];
+    if (asym > 1e-9 * std::max(1.0, max_mag)) {
+      set_error("psf_from_transfer: spectrum not conjugate-symmetric, max asymmetry %f", asym);
+      return PACT_E_VALIDATION;
+    }
+    if (max_real > 0.0 && max_imag > 1e-9 * max_real) {
+      set_error("psf_from_transfer: imaginary residue %f exceeds 1e-9 of max %f", max_imag, max_real);
+      return PACT_E_NUMERICAL;
+    }
+  }
   return PACT_OK;
 }

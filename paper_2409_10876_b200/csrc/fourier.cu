@@ -723,19 +723,7 @@ __global__ void __launch_bounds__(LB) loss_bins_small_kernel(FourierTab t, const
   block_sum_store(value, s_red, loss_part + patch * n_parts + blockIdx.y);
 }
 
-// dL/dw of one angle by the gather through the static CSR table (fixed entry
-// order) and the fixed-order sum of a patch's loss partials.
-__device__ __forceinline__ float finish_angle(const FourierTab& t, const float2* __restrict__ g, int a) {
-  float acc = 0.f;
-  const int e1 = t.csr_start[a + 1];
-  for (int e = t.csr_start[a]; e < e1; ++e) {
-    const int key = t.csr_key[e];
-    const float2 v = g[key >> 1];
-    acc = fmaf(t.csr_wt[e], (key & 1) ? v.y : v.x, acc);
-  }
-  return acc;
-}
-
+// The fixed-order sum of a patch's loss partials.
 __device__ __forceinline__ double patch_loss(const double* __restrict__ loss_part, int patch,
                                              int n_parts) {
   double v = 0.0;
@@ -757,8 +745,7 @@ __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const 
                                                             float2* __restrict__ gbuf,
                                                             double* __restrict__ loss_part,
                                                             int n_parts, int part0, int stage_y,
-                                                            int stage_g, double* __restrict__ loss_out,
-                                                            float* __restrict__ dw_out) {
+                                                            int stage_g) {
   extern __shared__ __align__(16) float smem[];
   __shared__ double s_red[32];
   const int patch = blockIdx.x, K = t.K, P2 = t.P2, S = 2 * t.P - 1;
@@ -881,26 +868,35 @@ __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const 
   G1 = group_sum(G1);
   G2 = group_sum(G2);
   if (active && q == 0) gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G1, G2);
-  // the patch's finish (loss_finish_kernel's work): every other bin of gbuf was
-  // written by loss_bins_kernel before this launch, the Nyquist bins above
-  __syncthreads();
-  const float2* g = gbuf + static_cast<size_t>(patch) * P2;
-  for (int a = threadIdx.x; a < t.A; a += blockDim.x) dw_out[patch * t.A + a] = finish_angle(t, g, a);
-  if (threadIdx.x == 0) loss_out[patch] = patch_loss(loss_part, patch, n_parts);
 }
 
-// Kernel B (odd P; even P folds it into the Nyquist kernel): dL/dw, one
-// thread per (patch, angle), and the per-patch loss.
-__global__ void __launch_bounds__(256) loss_finish_kernel(FourierTab t, const float2* __restrict__ gbuf,
+// Kernel B: dL/dw of every (patch, angle) by the gather through the static
+// CSR table, one warp per angle: lane l takes entries l, l + 32, ... in order
+// and the lanes' partials are combined by a fixed xor tree (deterministic);
+// the angle-0 warp also sums the patch's loss partials.  Many short warps
+// instead of a thread walking its angle's ~4 P^2 / A dependent loads.
+__global__ void __launch_bounds__(256) loss_gather_kernel(FourierTab t, const float2* __restrict__ gbuf,
                                                           const double* __restrict__ loss_part,
                                                           int n_parts, int n_patches,
                                                           double* __restrict__ loss_out,
                                                           float* __restrict__ dw_out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_patches * t.A) return;
-  const int patch = i / t.A, a = i - patch * t.A;
-  dw_out[i] = finish_angle(t, gbuf + static_cast<size_t>(patch) * t.P2, a);
-  if (a == 0) loss_out[patch] = patch_loss(loss_part, patch, n_parts);
+  const int wid = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (wid >= n_patches * t.A) return;
+  const int patch = wid / t.A, a = wid - patch * t.A;
+  const float2* g = gbuf + static_cast<size_t>(patch) * t.P2;
+  float acc = 0.f;
+  const int e1 = t.csr_start[a + 1];
+  for (int e = t.csr_start[a] + lane; e < e1; e += 32) {
+    const int key = __ldg(t.csr_key + e);
+    const float2 v = g[key >> 1];
+    acc = fmaf(__ldg(t.csr_wt + e), (key & 1) ? v.y : v.x, acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) {
+    dw_out[wid] = acc;
+    if (a == 0) loss_out[patch] = patch_loss(loss_part, patch, n_parts);
+  }
 }
 
 // X = sum_j conj(H_j) Y_j / (sum_j |H_j|^2 + eps M), 0 where den == 0
@@ -1014,12 +1010,12 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
     PACT_TRY_S(smem_optin(loss_nyquist_kernel, smem_nyq));
     loss_nyquist_kernel<<<n_patches, nt, smem_nyq, ctx->stream>>>(
         t, Y, w, eps_m, sc, implicit, reg ? ynyq : nullptr, nyq, gbuf, part, n_parts, chunks,
-        stage_y, stage_g, loss, dw);
-    return after_launch(ctx, "loss_nyquist_kernel");
+        stage_y, stage_g);
+    PACT_TRY_S(after_launch(ctx, "loss_nyquist_kernel"));
   }
-  loss_finish_kernel<<<div_up(n_patches * t.A, 256), 256, 0, ctx->stream>>>(t, gbuf, part, n_parts,
-                                                                            n_patches, loss, dw);
-  return after_launch(ctx, "loss_finish_kernel");
+  loss_gather_kernel<<<div_up(n_patches * t.A, 8), 256, 0, ctx->stream>>>(t, gbuf, part, n_parts,
+                                                                           n_patches, loss, dw);
+  return after_launch(ctx, "loss_gather_kernel");
 }
 
 Status launch_wiener(pact_ctx* ctx, const FourierTab& t, const float2* Y, const float* w,

@@ -205,60 +205,22 @@ inline void wavefront_grad_trace(Vec2 center, const RingGeometry& geom, const Ra
 
 /// psf_from_transfer (aberration.hpp:407-445): the real, centred PSF of one
 /// conjugate-symmetric P x P transfer spectrum (zero lag at pixel (P/2, P/2),
-/// origin chosen so that pixel sits at world (0, 0)).  Host-side (the
-/// `psf dump` tool path): the symmetry check, a separable inverse DFT with an
-/// exact twiddle table (scaled 1 / P^2), the imaginary-residue check and the
+/// origin chosen so that pixel sits at world (0, 0)).  On the GPU in fp64
+/// (pact_psf_from_transfer): the symmetry check, the inverse 2-D DFT (rows,
+/// then columns, scaled 1 / P^2), the imaginary-residue check and the
 /// centring shift, with the reference's thresholds and messages.
 inline RasterGrid psf_from_transfer(const std::vector<cplx>& spectrum, int patch_pixels,
                                     double pitch = 1.0) {
   const int P = patch_pixels;
   if (P < 1 || spectrum.size() != static_cast<size_t>(P) * P)
     throw ValidationError("psf_from_transfer: spectrum size mismatch");
-  double max_mag = 0.0, asym = 0.0;
-  for (const cplx& v : spectrum) max_mag = std::max(max_mag, std::abs(v));
-  for (int by = 0; by < P; ++by)
-    for (int bx = 0; bx < P; ++bx) {
-      const cplx a = spectrum[static_cast<size_t>(by) * P + bx];
-      const cplx b = spectrum[static_cast<size_t>((P - by) % P) * P + (P - bx) % P];
-      asym = std::max(asym, std::abs(a - std::conj(b)));
-    }
-  if (asym > 1e-9 * std::max(1.0, max_mag))
-    throw ValidationError("psf_from_transfer: spectrum not conjugate-symmetric, max asymmetry " +
-                          std::to_string(asym));
-  std::vector<cplx> tw(P);  // e^{+2 pi i k / P}
-  for (int k = 0; k < P; ++k) {
-    const double a = 2.0 * M_PI * k / P;
-    tw[k] = {std::cos(a), std::sin(a)};
-  }
-  // rows, then columns (the reference's inverse_2d order), then 1 / P^2
-  std::vector<cplx> rows(static_cast<size_t>(P) * P), out(static_cast<size_t>(P) * P);
-  for (int y = 0; y < P; ++y)
-    for (int x = 0; x < P; ++x) {
-      cplx acc = 0.0;
-      for (int k = 0; k < P; ++k)
-        acc += spectrum[static_cast<size_t>(y) * P + k] * tw[(static_cast<size_t>(k) * x) % P];
-      rows[static_cast<size_t>(y) * P + x] = acc;
-    }
-  const double inv = 1.0 / (static_cast<double>(P) * P);
-  double max_real = 0.0, max_imag = 0.0;
-  for (int y = 0; y < P; ++y)
-    for (int x = 0; x < P; ++x) {
-      cplx acc = 0.0;
-      for (int k = 0; k < P; ++k)
-        acc += rows[static_cast<size_t>(k) * P + x] * tw[(static_cast<size_t>(k) * y) % P];
-      acc *= inv;
-      out[static_cast<size_t>(y) * P + x] = acc;
-      max_real = std::max(max_real, std::abs(acc.real()));
-      max_imag = std::max(max_imag, std::abs(acc.imag()));
-    }
-  if (max_real > 0.0 && max_imag > 1e-9 * max_real)
-    throw NumericalError("psf_from_transfer: imaginary residue " + std::to_string(max_imag) +
-                         " exceeds 1e-9 of max " + std::to_string(max_real));
+  const size_t P2 = static_cast<size_t>(P) * P;
+  cuda::Buffer<double> s(2 * P2), out(P2);
+  cuda::check(pact_upload(cuda::context(), s.ptr, spectrum.data(), sizeof(cplx) * P2));
+  cuda::check(pact_psf_from_transfer(cuda::context(), 1, P, s.ptr, out.ptr));
   GridSpec gs{P, P, pitch, {-(P / 2) * pitch, -(P / 2) * pitch}};
   RasterGrid psf = RasterGrid::zeros(gs);
-  for (int y = 0; y < P; ++y)
-    for (int x = 0; x < P; ++x)
-      psf.at((x + P / 2) % P, (y + P / 2) % P) = out[static_cast<size_t>(y) * P + x].real();
+  out.download(psf.values.data());
   return psf;
 }
 

@@ -8,8 +8,8 @@ pinned to the reference compiled in oracle/_ref.
 * generate_phantom + builtin specs (phantom.hpp:145-266) through
   `pactrec phantom`: the written rasters equal the reference's fp64 rasters
   rounded to f32, bit for bit (seeded jitter included).
-* psf_from_transfer (aberration.hpp:407-445): values within 1e-12, the same
-  validation / numerical errors.
+* psf_from_transfer (aberration.hpp:407-445, GPU test): values within 1e-12,
+  the same validation / numerical errors.
 * the CLI contract of pactrec.cpp: subcommand tree, flag > PACT_* env >
   --config > default precedence, the resolved_config.ini echo (which loads
   back through --config to the same configuration), exit code 2 for bad
@@ -160,7 +160,8 @@ def test_sirn_errors_match_reference(tmp_path):
 # ---- psf_from_transfer ---------------------------------------------------------
 
 @needs_ref
-@pytest.mark.parametrize("P", [16, 12])
+@pytest.mark.gpu  # psf_from_transfer runs on the device (pact_psf_from_transfer, fp64)
+@pytest.mark.parametrize("P", [16, 12, 64])
 def test_psf_from_transfer_matches_reference(tmp_path, P):
     rng = np.random.default_rng(P)
     psf = rng.standard_normal((P, P))

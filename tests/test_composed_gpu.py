@@ -8,6 +8,7 @@ finite-difference contracts for it, run through the GPU entry points:
   transfer_grad_to_wavefront aberration.hpp:270-313
   wavefront_profile(with_jacobian) + accumulate_wavefront_grad  aberration.hpp:134-186, 316-326
   merge_patches             deconv.hpp:118-164
+  psf_from_transfer         aberration.hpp:407-445
   full_chain_grad == the fused training gradient (test_support.hpp:95-118;
   test_optimize.cpp:306-351), on the reference's SmallInstance
 """
@@ -219,7 +220,7 @@ def test_full_chain_grad_equals_fused(ctx, G, si):
     SIREN / ray / H stages)."""
     cfg = si.cfg
     spec = SirenSpec(cfg.hidden, cfg.sine_layers, cfg.omega0, cfg.out_scale, 1500.0)
-    theta = torch.as_tensor(G["theta0"])
+    theta = torch.as_tensor(G["theta2"])  # the golden step's parameters (init_siren seed 2)
     _, dev = ctx.render_sos(spec, theta, si.grid, si.mask)
     lay = make_patch_layout(si.grid, cfg.patch_mm, cfg.overlap)
     P, n, K = lay.patch_pixels, lay.n_patches, len(cfg.delays)
@@ -244,3 +245,27 @@ def test_full_chain_grad_equals_fused(ctx, G, si):
     err = rel_l2(grad, G["grad_theta"])
     print("composed vs fused grad_theta rel L2", err)
     assert err <= 1e-3
+
+
+def test_psf_from_transfer_vs_reference(ctx, G, si):
+    """Spatial PSFs of the SmallInstance patch-0 transfer stack (reference H,
+    golden) vs the reference's psf_from_transfer; the asymmetric-spectrum
+    ValidationError carries the reference's text."""
+    from cli_helpers import RefIO
+
+    refio = RefIO()
+    H = np.ascontiguousarray(G["H0"])  # [K, P, P] complex128, reference transfer_stack
+    K, P, _ = H.shape
+    psf = ctx.psf_from_transfer(_cu(H)).cpu().numpy()
+    for j in range(K):
+        rc, want = refio.psf_from_transfer(H[j], P, si.grid.pitch)
+        assert rc == 0
+        assert np.abs(psf[j] - want).max() <= 1e-12 * np.abs(want).max()
+    bad = H[:1].copy()
+    bad[0, 1, 2] += 1e-3j
+    rc, msg = refio.psf_from_transfer(bad[0], P, si.grid.pitch)
+    from paper_2409_10876_b200._abi import ValidationError
+
+    with pytest.raises(ValidationError) as e:
+        ctx.psf_from_transfer(_cu(bad))
+    assert rc == 2 and str(e.value).endswith(msg)
