@@ -41,7 +41,7 @@ namespace {
 // the layout and the delays), so repeated reconstructions only upload.
 struct HostFourier {
   std::vector<char> bytes;
-  size_t o_kmag, o_idx, o_frac, o_mirror, o_dp, o_start, o_key, o_wt, o_rho;
+  size_t o_kmag, o_idx, o_frac, o_mirror, o_dp, o_start, o_slot, o_rho;
   bool uniform;
 };
 
@@ -95,36 +95,28 @@ std::shared_ptr<const HostFourier> build_host_fourier(int P, double pitch, int A
             make_float2(static_cast<float>(std::cos(ph)), static_cast<float>(std::sin(ph)));
       }
     }
-  // angle -> (bin, branch, weight): the scatter of fused_patch_loss_grad
-  // (optimize.hpp:318-321) as a gather.
+  // the (bin, branch) pairs sorted by lower interpolation angle: the scatter
+  // of fused_patch_loss_grad (optimize.hpp:318-321) as contiguous segments
   std::vector<int> start(A + 1, 0);
   for (int b = 0; b < P2; ++b) {
     start[idx[b].x + 1]++;
-    start[idx[b].y + 1]++;
     start[idx[b].z + 1]++;
-    start[idx[b].w + 1]++;
   }
   for (int a = 0; a < A; ++a) start[a + 1] += start[a];
-  std::vector<int> key(4 * P2);
-  std::vector<float> wt(4 * P2);
-  std::vector<int> fill(start.begin(), start.end() - 1);
-  for (int b = 0; b < P2; ++b) {
-    double f1 = frac[b].x, f2 = frac[b].y;
-    key[fill[idx[b].x]] = (b << 1);
-    wt[fill[idx[b].x]++] = static_cast<float>(1.0 - f1);
-    key[fill[idx[b].y]] = (b << 1);
-    wt[fill[idx[b].y]++] = static_cast<float>(f1);
-    key[fill[idx[b].z]] = (b << 1) | 1;
-    wt[fill[idx[b].z]++] = static_cast<float>(1.0 - f2);
-    key[fill[idx[b].w]] = (b << 1) | 1;
-    wt[fill[idx[b].w]++] = static_cast<float>(f2);
+  std::vector<int2> slot(P2);
+  {
+    std::vector<int> fill(start.begin(), start.end() - 1);
+    for (int b = 0; b < P2; ++b) {  // ascending bin within an angle
+      slot[b].x = fill[idx[b].x]++;
+      slot[b].y = fill[idx[b].z]++;
+    }
   }
   // one device allocation, 16-byte aligned sections
   auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
   size_t o_kmag = 0, o_idx = al(o_kmag + 4 * P2), o_frac = al(o_idx + 16 * P2),
          o_mirror = al(o_frac + 8 * P2), o_dp = al(o_mirror + 4 * P2),
-         o_start = al(o_dp + 8 * static_cast<size_t>(K) * P2), o_key = al(o_start + 4 * (A + 1)),
-         o_wt = al(o_key + 16 * P2), o_rho = al(o_wt + 16 * P2), total = al(o_rho + 8 * P2);
+         o_start = al(o_dp + 8 * static_cast<size_t>(K) * P2), o_slot = al(o_start + 4 * (A + 1)),
+         o_rho = al(o_slot + 8 * P2), total = al(o_rho + 8 * P2);
   auto hf = std::make_shared<HostFourier>();
   std::vector<char>& host = hf->bytes;
   host.assign(total, 0);
@@ -134,8 +126,7 @@ std::shared_ptr<const HostFourier> build_host_fourier(int P, double pitch, int A
   std::memcpy(host.data() + o_mirror, mirror.data(), 4 * P2);
   std::memcpy(host.data() + o_dp, dp.data(), 8 * dp.size());
   std::memcpy(host.data() + o_start, start.data(), 4 * (A + 1));
-  std::memcpy(host.data() + o_key, key.data(), 16 * P2);
-  std::memcpy(host.data() + o_wt, wt.data(), 16 * P2);
+  std::memcpy(host.data() + o_slot, slot.data(), 8 * P2);
   std::memcpy(host.data() + o_rho, rho.data(), 8 * P2);
   hf->o_kmag = o_kmag;
   hf->o_idx = o_idx;
@@ -143,8 +134,7 @@ std::shared_ptr<const HostFourier> build_host_fourier(int P, double pitch, int A
   hf->o_mirror = o_mirror;
   hf->o_dp = o_dp;
   hf->o_start = o_start;
-  hf->o_key = o_key;
-  hf->o_wt = o_wt;
+  hf->o_slot = o_slot;
   hf->o_rho = o_rho;
   hf->uniform = uniform;
   return hf;
@@ -209,9 +199,8 @@ Status fourier_table(pact_ctx* ctx, FourierTable& t, int P, double pitch, int A,
   t.tab.frac = reinterpret_cast<const float2*>(d + hf->o_frac);
   t.tab.mirror = reinterpret_cast<const int*>(d + hf->o_mirror);
   t.tab.dp = reinterpret_cast<const float2*>(d + hf->o_dp);
-  t.tab.csr_start = reinterpret_cast<const int*>(d + hf->o_start);
-  t.tab.csr_key = reinterpret_cast<const int*>(d + hf->o_key);
-  t.tab.csr_wt = reinterpret_cast<const float*>(d + hf->o_wt);
+  t.tab.sstart = reinterpret_cast<const int*>(d + hf->o_start);
+  t.tab.slot = reinterpret_cast<const int2*>(d + hf->o_slot);
   t.tab.rho = hf->uniform ? reinterpret_cast<const float2*>(d + hf->o_rho) : nullptr;
   return {};
 }
@@ -271,6 +260,16 @@ __global__ void transfer_stack_kernel(FourierTab t, const float* __restrict__ w_
   if (m >= 0) bin_phases(t, s_w, m, e1m, e2m);
   float2* out = H + static_cast<size_t>(patch) * t.K * t.P2 + b;
   for (int j = 0; j < t.K; ++j) out[j * t.P2] = h_sym(t, j, b, m, e1b, e2b, e1m, e2m);
+}
+
+// (dL/dw1, dL/dw2) of bin b -> the interpolation weights' shares at the
+// bin's two sorted slots (FourierTab::slot); u is the patch's [2 P2] block.
+__device__ __forceinline__ void put_g(const FourierTab& t, float2* __restrict__ u, int b, float G1,
+                                      float G2) {
+  const int2 s = t.slot[b];
+  const float2 fr = t.frac[b];
+  u[s.x] = make_float2((1.f - fr.x) * G1, fr.x * G1);
+  u[s.y] = make_float2((1.f - fr.y) * G2, fr.y * G2);
 }
 
 // Per-bin state of the loss chain (optimize.hpp:275-311).
@@ -581,7 +580,7 @@ __global__ void __launch_bounds__(2 * LB) loss_bins_kernel(FourierTab t, const f
     const float2* yb = s_y + bl;
     double value = bin_chain_real<true>(t, s_w, b, eps_m, scale, implicit != 0,
                                         [&](int j) { return yb[j * LB]; }, G);
-    if (ordinary && lead) gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G, G);
+    if (ordinary && lead) put_g(t, gbuf + static_cast<size_t>(patch) * 2 * P2, b, G, G);
     if (!ordinary || !lead) value = 0.0;
     block_sum_store(value, s_red, loss_part + patch * n_parts + cb);
     __syncthreads();  // stage st is free for chunk i + 2; s_red is reusable
@@ -667,6 +666,7 @@ __global__ void __launch_bounds__(256, 4) loss_reg_kernel(FourierTab t, const fl
   const float2 X = make_float2(Sx * inv, Sy * inv);
   const float al = implicit && den > 0.f ? eps_m * inv : 0.f;
   const float be = 2.f * al * (X.x * X.x + X.y * X.y);
+  const float al1 = 1.f + al, xb = X.x * X.x + X.y * X.y + be;
   float acc = 0.f, gs = 0.f;
   {
     float2 z = z0;
@@ -674,7 +674,9 @@ __global__ void __launch_bounds__(256, 4) loss_reg_kernel(FourierTab t, const fl
     for (int u = 0; u < JPL; ++u) {
       const float rx = fmaf(-z.x, X.x, y[u].x), ry = fmaf(-z.x, X.y, y[u].y);
       acc = fmaf(rx, rx, fmaf(ry, ry, acc));
-      const float dc = fmaf(rx, X.x, ry * X.y) + al * fmaf(X.x, y[u].x, X.y * y[u].y) - be * z.x;
+      // dc = Re(conj(r) X) + al Re(conj(X) y) - be c = (1 + al) (X . y) - (|X|^2 + be) c
+      const float q = fmaf(X.x, y[u].x, X.y * y[u].y);
+      const float dc = fmaf(al1, q, -xb * z.x);
       gs = fmaf(dc, z.y, gs);
       if (u + 1 < JPL) z = znext(u, z);
     }
@@ -684,7 +686,7 @@ __global__ void __launch_bounds__(256, 4) loss_reg_kernel(FourierTab t, const fl
   const bool ordinary = valid && m < 0 && wk != 0.f;
   if (grp == 0 && valid && m < 0) {
     const float G = ordinary ? -wk * k * gs : 0.f;  // (1/2) dL/dwbar, for w1 and for w2
-    gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G, G);
+    put_g(t, gbuf + static_cast<size_t>(patch) * 2 * P2, b, G, G);
   }
   const double value = ordinary && grp == 0 ? static_cast<double>(wk) * acc : 0.0;
   block_sum_store(value, s_red, loss_part + patch * n_parts + cb);
@@ -718,7 +720,7 @@ __global__ void __launch_bounds__(LB) loss_bins_small_kernel(FourierTab t, const
     const float2* yb = s_y + threadIdx.x;
     value = bin_chain_real(t, s_w, b, eps_m, scale, implicit != 0,
                            [&](int j) { return yb[j * LB]; }, G);
-    gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G, G);
+    put_g(t, gbuf + static_cast<size_t>(patch) * 2 * P2, b, G, G);
   }
   block_sum_store(value, s_red, loss_part + patch * n_parts + blockIdx.y);
 }
@@ -760,9 +762,21 @@ __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const 
   // the slots' spectra: from the compact [slot][K] copy kernel A made, or
   // (other kernel A forms) gathered from Y, eight loads in flight per thread
   const float2* Yc = ynyq ? ynyq + static_cast<size_t>(patch) * S * K : nullptr;
-  for (int e = threadIdx.x; Yc && stage_y && e < K * S; e += blockDim.x) {
-    const int q = e / K, j = e - q * K;
-    s_y[j * S + q] = Yc[e];
+  for (int e0 = threadIdx.x; Yc && stage_y && e0 < K * S; e0 += 8 * blockDim.x) {
+    float2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      v[u] = e < K * S ? Yc[e] : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < K * S) {
+        const int q = e / K, j = e - q * K;
+        s_y[j * S + q] = v[u];
+      }
+    }
   }
   for (int e0 = threadIdx.x; !Yc && stage_y && e0 < K * S; e0 += 8 * blockDim.x) {
     float2 v[8];
@@ -867,36 +881,31 @@ __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const 
   }
   G1 = group_sum(G1);
   G2 = group_sum(G2);
-  if (active && q == 0) gbuf[static_cast<size_t>(patch) * P2 + b] = make_float2(G1, G2);
+  if (active && q == 0) put_g(t, gbuf + static_cast<size_t>(patch) * 2 * P2, b, G1, G2);
 }
 
-// Kernel B: dL/dw of every (patch, angle) by the gather through the static
-// CSR table, one warp per angle: lane l takes entries l, l + 32, ... in order
-// and the lanes' partials are combined by a fixed xor tree (deterministic);
-// the angle-0 warp also sums the patch's loss partials.  Many short warps
-// instead of a thread walking its angle's ~4 P^2 / A dependent loads.
-__global__ void __launch_bounds__(256) loss_gather_kernel(FourierTab t, const float2* __restrict__ gbuf,
+// Kernel B: dL/dw of every (patch, angle) from the angle-sorted slots
+// (FourierTab::slot): the .x shares of angle a's segment plus the .y shares of
+// angle a - 1's, each a contiguous run summed in order (deterministic); the
+// angle-0 thread also sums the patch's loss partials.
+__global__ void __launch_bounds__(256) loss_finish_kernel(FourierTab t, const float2* __restrict__ u_all,
                                                           const double* __restrict__ loss_part,
                                                           int n_parts, int n_patches,
                                                           double* __restrict__ loss_out,
                                                           float* __restrict__ dw_out) {
-  const int wid = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (wid >= n_patches * t.A) return;
-  const int patch = wid / t.A, a = wid - patch * t.A;
-  const float2* g = gbuf + static_cast<size_t>(patch) * t.P2;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_patches * t.A) return;
+  const int patch = i / t.A, a = i - patch * t.A, am = a == 0 ? t.A - 1 : a - 1;
+  const float2* u = u_all + static_cast<size_t>(patch) * 2 * t.P2;
   float acc = 0.f;
-  const int e1 = t.csr_start[a + 1];
-  for (int e = t.csr_start[a] + lane; e < e1; e += 32) {
-    const int key = __ldg(t.csr_key + e);
-    const float2 v = g[key >> 1];
-    acc = fmaf(__ldg(t.csr_wt + e), (key & 1) ? v.y : v.x, acc);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) {
-    dw_out[wid] = acc;
-    if (a == 0) loss_out[patch] = patch_loss(loss_part, patch, n_parts);
-  }
+  const int s0 = __ldg(t.sstart + a), s1 = __ldg(t.sstart + a + 1);
+#pragma unroll 4
+  for (int s = s0; s < s1; ++s) acc += u[s].x;
+  const int r0 = __ldg(t.sstart + am), r1 = __ldg(t.sstart + am + 1);
+#pragma unroll 4
+  for (int s = r0; s < r1; ++s) acc += u[s].y;
+  dw_out[i] = acc;
+  if (a == 0) loss_out[patch] = patch_loss(loss_part, patch, n_parts);
 }
 
 // X = sum_j conj(H_j) Y_j / (sum_j |H_j|^2 + eps M), 0 where den == 0
@@ -970,7 +979,7 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
   // scratch: Nyquist dL/dH exchange [patch][2P-1][K] | compact Nyquist spectra
   // [patch][2P-1][K] | (G1, G2) [patch][P2] | chunk losses
   const size_t n_nyq = static_cast<size_t>(n_patches) * (2 * t.P) * t.K;
-  const size_t n_g = static_cast<size_t>(n_patches) * t.P2;
+  const size_t n_g = static_cast<size_t>(n_patches) * 2 * t.P2;  // slot shares
   void* base = nullptr;
   PACT_TRY_S(scratch_get(ctx, kScratchNyq,
                          sizeof(float2) * (2 * n_nyq + n_g) + sizeof(double) * n_patches * n_parts +
@@ -1013,9 +1022,9 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
         stage_y, stage_g);
     PACT_TRY_S(after_launch(ctx, "loss_nyquist_kernel"));
   }
-  loss_gather_kernel<<<div_up(n_patches * t.A, 8), 256, 0, ctx->stream>>>(t, gbuf, part, n_parts,
-                                                                           n_patches, loss, dw);
-  return after_launch(ctx, "loss_gather_kernel");
+  loss_finish_kernel<<<div_up(n_patches * t.A, 256), 256, 0, ctx->stream>>>(t, gbuf, part, n_parts,
+                                                                            n_patches, loss, dw);
+  return after_launch(ctx, "loss_finish_kernel");
 }
 
 Status launch_wiener(pact_ctx* ctx, const FourierTab& t, const float2* Y, const float* w,

@@ -20,9 +20,15 @@ struct FourierTab {
   const float2* dp = nullptr;     // [K][P2] exp(-i |k| d_j)
   const float2* rho = nullptr;    // [P2] exp(-i |k| (d_1 - d_0)) for evenly spaced delays, else null:
                                   // dp_j = dp_0 rho^j is then walked in registers
-  const int* csr_start = nullptr; // [A+1] angle -> contributions
-  const int* csr_key = nullptr;   // [4 P2] (bin << 1) | (0: via w1, 1: via w2)
-  const float* csr_wt = nullptr;  // [4 P2] interpolation weight
+  // dL/dw pullback (optimize.hpp:318-321) as a sort: the 2 P2 (bin, branch)
+  // pairs ordered by their lower interpolation angle a0 (then bin, branch);
+  // pair (b, r) sits at slot[b].x (r = 1, angle(k)) / slot[b].y (r = 2,
+  // angle(k) + pi), and angle a owns slots [sstart[a], sstart[a + 1]).  The
+  // loss kernels store ((1 - f) G, f G) of every pair at its slot, so dL/dw[a]
+  // is the .x sum over a's slots plus the .y sum over a - 1's slots:
+  // contiguous reads, fixed order.
+  const int2* slot = nullptr;     // [P2]
+  const int* sstart = nullptr;    // [A + 1]
 };
 
 // Host-built table (fp64 reference formulas, stored fp32) + its device copy.
