@@ -15,9 +15,15 @@
 //
 // The backward pass coalesces consecutive steps that share a stencil cell in
 // registers (a step is 0.05 mm, a pixel 0.05-0.2 mm, and steps beyond the grid
-// clamp onto one border cell for long runs) and flushes with fp64 atomics,
-// skipping zero-weight corners; fp64 accumulation makes the result
-// reproducible to fp32 output precision regardless of atomic order.
+// clamp onto one border cell for long runs) and flushes, skipping zero-weight
+// corners, into 64-bit FIXED-POINT accumulators (integer RED.ADD.64): integer
+// addition is associative, so the result is bitwise identical for any atomic
+// order (deterministic by construction), and the integer reduction is faster
+// than RED.ADD.F64 on B200 (scripts/probes/red_rate.cu).  The quantum 2^-S is
+// set per launch from a deterministic bound on any pixel's total
+// (ray_bound_kernel: max |dL/dw|, max 1/v^2 over the raster, the ray count and
+// the longest possible ray), so no sum can overflow and the resolution is
+// ~1e-10 of the largest single deposit; fix_to_grad_kernel converts to fp64.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -73,6 +79,36 @@ __device__ __forceinline__ Border load_border(const RayArgs& a, float* sm) {
   }
   __syncthreads();
   return b;
+}
+
+// Fixed-point deposit target: int64 multiples of 2^-S (see the header).
+struct Fix {
+  unsigned long long* p;
+  double scale;  // 2^S
+  __device__ __forceinline__ Fix operator+(long long off) const { return {p + off, scale}; }
+  __device__ __forceinline__ void add(float v) const {
+    atomicAdd(p, static_cast<unsigned long long>(__double2ll_rn(static_cast<double>(v) * scale)));
+  }
+};
+
+// Per-launch exponent S from the bound statistics (ray_bound_kernel): every
+// deposit is |g| dl v0 / v^2 * beta <= |g|max * step * v0 * max(1/v^2), and a
+// pixel receives at most n_rays * max_steps of them; S keeps that below 2^62.
+__device__ __forceinline__ int fix_exponent(const unsigned long long* stats, double step, double v0,
+                                            double max_steps_total) {
+  const double gmax = __longlong_as_double(static_cast<long long>(stats[0]));
+  const double ivmax = __longlong_as_double(static_cast<long long>(stats[1]));
+  const double B = gmax * step * v0 * ivmax * max_steps_total;
+  if (!(B > 0.0) || !isfinite(B)) return 0;
+  int e;
+  frexp(B, &e);  // B < 2^e
+  return 62 - e;
+}
+
+// The most deposits any pixel can receive in one launch: every ray's steps
+// (a ray from inside the ring is at most one ring diameter long).
+__host__ __device__ __forceinline__ double max_steps_total(const RayArgs& a) {
+  return static_cast<double>(a.n_rays) * (ceil(2.0 * a.ring_r / a.step) + 1.0);
 }
 
 // One midpoint step: the clamped stencil of detail::bilinear_stencil and the
@@ -182,13 +218,12 @@ __device__ float march_forward_generic(const RayArgs& a, const Border& bd, const
   return acc;
 }
 
-__device__ __forceinline__ void flush_cell(double* __restrict__ g, int W, int H, int ix, int iy,
-                                           const double acc[4]) {
+__device__ __forceinline__ void flush_cell(Fix g, int W, int H, int ix, int iy, const float acc[4]) {
   int ix1 = min(ix + 1, W - 1), iy1 = min(iy + 1, H - 1);
-  if (acc[0] != 0.0) atomicAdd(g + iy * W + ix, acc[0]);
-  if (acc[1] != 0.0) atomicAdd(g + iy * W + ix1, acc[1]);
-  if (acc[2] != 0.0) atomicAdd(g + iy1 * W + ix, acc[2]);
-  if (acc[3] != 0.0) atomicAdd(g + iy1 * W + ix1, acc[3]);
+  if (acc[0] != 0.f) (g + (iy * W + ix)).add(acc[0]);
+  if (acc[1] != 0.f) (g + (iy * W + ix1)).add(acc[1]);
+  if (acc[2] != 0.f) (g + (iy1 * W + ix)).add(acc[2]);
+  if (acc[3] != 0.f) (g + (iy1 * W + ix1)).add(acc[3]);
 }
 
 // Per-ray accumulators of the current stencil cell's pixels (cx + i, cy + j):
@@ -199,7 +234,7 @@ struct CellAcc {
   int cx = -1, cy = -1;
   float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
 
-  __device__ __forceinline__ void move(double* __restrict__ grad, int W, int ix, int iy) {
+  __device__ __forceinline__ void move(Fix grad, int W, int ix, int iy) {
     if (ix == cx && iy == cy) return;
     if (cx >= 0) {
       const int dx = ix - cx, dy = iy - cy;
@@ -216,7 +251,7 @@ struct CellAcc {
           n10 += t == 2 ? val : 0.f;
           n11 += t == 3 ? val : 0.f;
         } else if (val != 0.f && !RAY_NO_INT_ATOM) {
-          atomicAdd(grad + (cy + (q >> 1)) * W + cx + (q & 1), static_cast<double>(val));
+          (grad + ((cy + (q >> 1)) * W + cx + (q & 1))).add(val);
         }
       }
       a00 = n00;
@@ -230,7 +265,7 @@ struct CellAcc {
   // Interior move by at most one cell per axis (a step is <= 1 px): the
   // remap is a fixed select network and the evictions are predicated atomics
   // (no loop); larger jumps take the general path.
-  __device__ __forceinline__ void move_unit(double* __restrict__ grad, int W, int ix, int iy) {
+  __device__ __forceinline__ void move_unit(Fix grad, int W, int ix, int iy) {
     if (ix == cx && iy == cy) return;
     const int dx = ix - cx, dy = iy - cy;
     if (cx < 0 || dx < -1 || dx > 1 || dy < -1 || dy > 1) {
@@ -240,11 +275,11 @@ struct CellAcc {
     // old slot (i, j) [x i, y j] survives iff (i - dx, j - dy) is in the new cell
     const bool keep_x0 = dx <= 0, keep_x1 = dx >= 0, keep_y0 = dy <= 0, keep_y1 = dy >= 0;
     if (!RAY_NO_INT_ATOM) {
-      double* p = grad + cy * W + cx;
-      if (!(keep_x0 && keep_y0) && a00 != 0.f) atomicAdd(p, static_cast<double>(a00));
-      if (!(keep_x1 && keep_y0) && a01 != 0.f) atomicAdd(p + 1, static_cast<double>(a01));
-      if (!(keep_x0 && keep_y1) && a10 != 0.f) atomicAdd(p + W, static_cast<double>(a10));
-      if (!(keep_x1 && keep_y1) && a11 != 0.f) atomicAdd(p + W + 1, static_cast<double>(a11));
+      const Fix p = grad + (cy * W + cx);
+      if (!(keep_x0 && keep_y0) && a00 != 0.f) p.add(a00);
+      if (!(keep_x1 && keep_y0) && a01 != 0.f) (p + 1).add(a01);
+      if (!(keep_x0 && keep_y1) && a10 != 0.f) (p + W).add(a10);
+      if (!(keep_x1 && keep_y1) && a11 != 0.f) (p + (W + 1)).add(a11);
     }
     // x shift within each old row j: new x0 <- old (dx == 0 ? x0 : dx == 1 ? x1 : none)
     const float r00 = dx == 0 ? a00 : (dx == 1 ? a01 : 0.f);
@@ -259,9 +294,9 @@ struct CellAcc {
     cx = ix;
     cy = iy;
   }
-  __device__ __forceinline__ void flush(double* __restrict__ grad, int W, int H) {
+  __device__ __forceinline__ void flush(Fix grad, int W, int H) {
     if (cx < 0) return;
-    const double fin[4] = {a00, a01, a10, a11};
+    const float fin[4] = {a00, a01, a10, a11};
     flush_cell(grad, W, H, cx, cy, fin);
     cx = cy = -1;
     a00 = a01 = a10 = a11 = 0.f;
@@ -270,7 +305,7 @@ struct CellAcc {
 
 template <bool TEX>
 __device__ void march_backward_generic(const RayArgs& a, const Border& bd, const RayPix& rp, int n,
-                                       float v0, float gscale, double* __restrict__ grad) {
+                                       float v0, float gscale, Fix grad) {
   CellAcc c;
   for (int i = 0; i < n; ++i) {
     Step st = step_at<TEX>(a, bd, fmaf(static_cast<float>(i), rp.dfx, rp.fxs),
@@ -368,29 +403,29 @@ __device__ __forceinline__ float interior_d(cudaTextureObject_t tex, float fx, f
 struct LineAcc {
   int q = -1;
   float b0 = 0.f, b1 = 0.f;
-  __device__ __forceinline__ void move(double* __restrict__ grad, int nq, int stride, int base) {
+  __device__ __forceinline__ void move(Fix grad, int nq, int stride, int base) {
     if (nq == q) return;
     if (q >= 0 && !RAY_NO_LINE_ATOM) {
       if (nq == q + 1) {
-        if (b0 != 0.f) atomicAdd(grad + base + q * stride, static_cast<double>(b0));
+        if (b0 != 0.f) (grad + (base + q * stride)).add(b0);
         b0 = b1;
         b1 = 0.f;
       } else if (nq == q - 1) {
-        if (b1 != 0.f) atomicAdd(grad + base + (q + 1) * stride, static_cast<double>(b1));
+        if (b1 != 0.f) (grad + (base + (q + 1) * stride)).add(b1);
         b1 = b0;
         b0 = 0.f;
       } else {
-        if (b0 != 0.f) atomicAdd(grad + base + q * stride, static_cast<double>(b0));
-        if (b1 != 0.f) atomicAdd(grad + base + (q + 1) * stride, static_cast<double>(b1));
+        if (b0 != 0.f) (grad + (base + q * stride)).add(b0);
+        if (b1 != 0.f) (grad + (base + (q + 1) * stride)).add(b1);
         b0 = b1 = 0.f;
       }
     }
     q = nq;
   }
-  __device__ __forceinline__ void flush(double* __restrict__ grad, int stride, int base) {
+  __device__ __forceinline__ void flush(Fix grad, int stride, int base) {
     if (q < 0) return;
-    if (b0 != 0.f) atomicAdd(grad + base + q * stride, static_cast<double>(b0));
-    if (b1 != 0.f) atomicAdd(grad + base + (q + 1) * stride, static_cast<double>(b1));
+    if (b0 != 0.f) (grad + (base + q * stride)).add(b0);
+    if (b1 != 0.f) (grad + (base + (q + 1) * stride)).add(b1);
   }
 };
 
@@ -522,13 +557,16 @@ __global__ void ray_finish_kernel(RayArgs a, float* __restrict__ w) {
 
 // (256, 4): at most 64 registers, four blocks per SM (0.53 vs 0.56 ms at 68)
 __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, const float* __restrict__ dw,
-                                                                  double* __restrict__ grad,
-                                                                  double* __restrict__ border_rep) {
+                                                                  unsigned long long* __restrict__ acc,
+                                                                  unsigned long long* __restrict__ border_rep,
+                                                                  const unsigned long long* __restrict__ stats) {
   extern __shared__ float s_border[];
   const Border bd = load_border(a, s_border);
   const int W = a.W, H = a.H;
   const float v0 = static_cast<float>(a.v0);
-  double* rep = border_rep + static_cast<size_t>(blockIdx.x % kBorderReplicas) * 2 * (W + H);
+  const double scale = ldexp(1.0, fix_exponent(stats, a.step, a.v0, max_steps_total(a)));
+  const Fix grad{acc, scale};
+  const Fix rep{border_rep + static_cast<size_t>(blockIdx.x % kBorderReplicas) * 2 * (W + H), scale};
   {
     const int it = blockIdx.x * blockDim.x + threadIdx.x;
     if (it >= a.n_items) return;
@@ -579,7 +617,7 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
       // border line (one loop for both orientations); the replica slice has
       // the smem border's layout
       const SideLine sl = side_line(rec_regimes(rr), rec_pixels(rr), W, H);
-      double* dst = rep + sl.off;
+      const Fix dst = rep + sl.off;
       LineAcc line;
       for (int i = lo; i < hi; ++i) {
         const float f = fmaf(static_cast<float>(i), sl.df, sl.fs);
@@ -601,37 +639,64 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
       const float* col = rr.dfx > 0.f ? bd.colR : bd.colL;
       const float v = v0 + col[py];
       const float f = __fdividef(gscale, v * v) * static_cast<float>(rr.n - rr.i_corner);
-      if (f != 0.f) atomicAdd(rep + (px == 0 ? 0 : H) + py, static_cast<double>(f));
+      if (f != 0.f) (rep + ((px == 0 ? 0 : H) + py)).add(f);
     }
   }
 }
 
-// grad[p] += sum over replicas of the slot(s) of border pixel p (fixed order).
-// One thread per border pixel: left / right columns, then the bottom / top
-// rows without their corners.
-__global__ void border_reduce_kernel(const double* __restrict__ rep, int W, int H,
-                                     double* __restrict__ grad) {
+// grad[p] += (acc[p] + the replicas' slots of p when p is on the border) 2^-S,
+// one thread per pixel; the accumulators it read are reset to zero for the
+// next launch, so the raster needs no per-launch memset.
+__global__ void fix_to_grad_kernel(unsigned long long* __restrict__ acc,
+                                   unsigned long long* __restrict__ rep, int W, int H,
+                                   const unsigned long long* __restrict__ stats, double step, double v0,
+                                   double max_steps, double* __restrict__ grad) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int n_in = max(W - 2, 0);
-  if (i >= 2 * H + 2 * n_in) return;
-  int px, py;
-  if (i < 2 * H) {
-    px = i < H ? 0 : W - 1;
-    py = i < H ? i : i - H;
-  } else {
-    const int k = i - 2 * H;
-    px = 1 + (k < n_in ? k : k - n_in);
-    py = k < n_in ? 0 : H - 1;
+  const int S = fix_exponent(stats, step, v0, max_steps);
+  if (i >= W * H) return;
+  const int py = i / W, px = i - py * W;
+  long long v = static_cast<long long>(acc[i]);
+  acc[i] = 0ull;
+  if (rep && (px == 0 || px == W - 1 || py == 0 || py == H - 1)) {
+    const int col = px == 0 ? py : (px == W - 1 ? H + py : -1);
+    const int row = py == 0 ? 2 * H + px : (py == H - 1 ? 2 * H + W + px : -1);
+    const size_t stride = 2 * static_cast<size_t>(W + H);
+    for (int r = 0; r < kBorderReplicas; ++r) {
+      if (col >= 0) {
+        v += static_cast<long long>(rep[r * stride + col]);
+        rep[r * stride + col] = 0ull;
+      }
+      if (row >= 0) {
+        v += static_cast<long long>(rep[r * stride + row]);
+        rep[r * stride + row] = 0ull;
+      }
+    }
   }
-  const int col = px == 0 ? py : (px == W - 1 ? H + py : -1);
-  const int row = py == 0 ? 2 * H + px : (py == H - 1 ? 2 * H + W + px : -1);
-  const size_t stride = 2 * static_cast<size_t>(W + H);
-  double s = 0.0;
-  for (int r = 0; r < kBorderReplicas; ++r) {
-    if (col >= 0) s += rep[r * stride + col];
-    if (row >= 0) s += rep[r * stride + row];
+  if (v != 0) grad[i] += ldexp(static_cast<double>(v), -S);
+}
+
+// Bound statistics of one adjoint launch (exact maxima, order-independent):
+// stats[0] = max |dL/dw| over the rays, stats[1] = max 1 / v^2 over the
+// raster (non-negative doubles order like their bit patterns).
+__global__ void ray_bound_kernel(const float* __restrict__ dw, int n_rays,
+                                 const float* __restrict__ dv, int npx, float v0,
+                                 unsigned long long* __restrict__ stats) {
+  double g = 0.0, iv = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rays; i += gridDim.x * blockDim.x)
+    g = fmax(g, fabs(static_cast<double>(dw[i])));
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npx; i += gridDim.x * blockDim.x) {
+    const double v = static_cast<double>(v0) + static_cast<double>(dv[i]);
+    iv = fmax(iv, v > 0.0 ? 1.0 / (v * v) : INFINITY);
   }
-  if (s != 0.0) grad[static_cast<size_t>(py) * W + px] += s;
+  for (int o = 16; o > 0; o >>= 1) {
+    g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+    iv = fmax(iv, __shfl_xor_sync(0xffffffffu, iv, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (g != 0.0 || isnan(g))
+      atomicMax(stats, static_cast<unsigned long long>(__double_as_longlong(isnan(g) ? INFINITY : g)));
+    atomicMax(stats + 1, static_cast<unsigned long long>(__double_as_longlong(isnan(iv) ? INFINITY : iv)));
+  }
 }
 
 // Generic kernels (plain loads, no texture): one per-step march per ray.
@@ -651,9 +716,11 @@ __global__ void __launch_bounds__(256) wavefront_kernel(RayArgs a, float* __rest
 
 template <bool TEX>
 __global__ void __launch_bounds__(256) ray_backward_kernel(RayArgs a, const float* __restrict__ dw,
-                                                           double* __restrict__ grad) {
+                                                           unsigned long long* __restrict__ acc,
+                                                           const unsigned long long* __restrict__ stats) {
   extern __shared__ float s_border[];
   const Border bd = load_border(a, s_border);
+  const Fix grad{acc, ldexp(1.0, fix_exponent(stats, a.step, a.v0, max_steps_total(a)))};
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= a.n_rays) return;
   const float gr = dw[r];
@@ -948,52 +1015,60 @@ Status ray_plan_cached(pact_ctx* ctx, RayArgs& a, const double* centers, int n_c
 
 static size_t border_smem(const RayArgs& a) { return sizeof(float) * 2 * (a.W + a.H); }
 
-template <typename K>
-static Status allow_smem(K kernel, size_t smem) {
-  if (smem > 48 * 1024)
-    PACT_CUDA_S(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
-  return {};
-}
-
 Status launch_wavefront(pact_ctx* ctx, const RayArgs& a, float* w) {
   const size_t smem = border_smem(a);
   if (a.tex) {  // make_raster_texture requires W, H >= 2
     if (!a.rec) return internal_error("launch_wavefront: ray plan missing");
     if (a.n_items > 0) {
-      PACT_TRY_S(allow_smem(wavefront_plan_kernel, smem));
+      PACT_TRY_S(smem_optin(wavefront_plan_kernel, smem));
       wavefront_plan_kernel<<<div_up(a.n_items, kPlanBlock), kPlanBlock, smem, ctx->stream>>>(a);
       PACT_TRY_S(after_launch(ctx, "wavefront_plan_kernel"));
     }
     ray_finish_kernel<<<div_up(a.n_rays, 256), 256, 0, ctx->stream>>>(a, w);
     return after_launch(ctx, "ray_finish_kernel");
   }
-  PACT_TRY_S(allow_smem(wavefront_kernel<false>, smem));
+  PACT_TRY_S(smem_optin(wavefront_kernel<false>, smem));
   wavefront_kernel<false><<<div_up(a.n_rays, 256), 256, smem, ctx->stream>>>(a, w);
   return after_launch(ctx, "wavefront_kernel");
 }
 
 Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, double* grad) {
   const size_t smem = border_smem(a);
+  if (a.n_rays == 0) return {};
+  // fixed-point accumulators: raster [H W] | border replicas | bound statistics,
+  // zero between launches (fix_to_grad_kernel resets what it reads)
+  const size_t npx = static_cast<size_t>(a.W) * a.H;
+  const size_t rep_n = static_cast<size_t>(kBorderReplicas) * 2 * (a.W + a.H);
+  const size_t bytes = sizeof(unsigned long long) * (npx + rep_n + 2);
+  pact_scratch& sc = ctx->scratch[kScratchRayBorder];
+  const void* before = sc.ptr;
+  void* base = nullptr;
+  PACT_TRY_S(scratch_get(ctx, kScratchRayBorder, bytes, &base));
+  if (base != before) PACT_CUDA_S(cudaMemsetAsync(base, 0, sc.bytes, ctx->stream));
+  auto* acc = static_cast<unsigned long long*>(base);
+  auto* rep = acc + npx;
+  auto* stats = rep + rep_n;
+  PACT_CUDA_S(cudaMemsetAsync(stats, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  const int nb = std::max(1, std::min(2 * ctx->num_sms, div_up(static_cast<int>(npx), 256)));
+  ray_bound_kernel<<<nb, 256, 0, ctx->stream>>>(dw, a.n_rays, a.dv, static_cast<int>(npx),
+                                                static_cast<float>(a.v0), stats);
+  PACT_TRY_S(after_launch(ctx, "ray_bound_kernel"));
   if (a.tex) {
     if (!a.rec) return internal_error("launch_ray_backward: ray plan missing");
-    if (a.n_items == 0) return {};
-    const size_t rep_n = static_cast<size_t>(kBorderReplicas) * 2 * (a.W + a.H);
-    void* rep = nullptr;
-    PACT_TRY_S(scratch_get(ctx, kScratchRayBorder, sizeof(double) * rep_n, &rep));
-    PACT_CUDA_S(cudaMemsetAsync(rep, 0, sizeof(double) * rep_n, ctx->stream));
-    PACT_TRY_S(allow_smem(ray_backward_plan_kernel, smem));
-    ray_backward_plan_kernel<<<div_up(a.n_items, kPlanBlock), kPlanBlock, smem, ctx->stream>>>(
-        a, dw, grad, static_cast<double*>(rep));
-    PACT_TRY_S(after_launch(ctx, "ray_backward_plan_kernel"));
-    const int nbp = 2 * a.H + 2 * std::max(a.W - 2, 0);
-    border_reduce_kernel<<<div_up(nbp, 256), 256, 0, ctx->stream>>>(static_cast<double*>(rep), a.W,
-                                                                     a.H, grad);
-    return after_launch(ctx, "border_reduce_kernel");
+    if (a.n_items > 0) {
+      PACT_TRY_S(smem_optin(ray_backward_plan_kernel, smem));
+      ray_backward_plan_kernel<<<div_up(a.n_items, kPlanBlock), kPlanBlock, smem, ctx->stream>>>(
+          a, dw, acc, rep, stats);
+      PACT_TRY_S(after_launch(ctx, "ray_backward_plan_kernel"));
+    }
+  } else {
+    PACT_TRY_S(smem_optin(ray_backward_kernel<false>, smem));
+    ray_backward_kernel<false><<<div_up(a.n_rays, 256), 256, smem, ctx->stream>>>(a, dw, acc, stats);
+    PACT_TRY_S(after_launch(ctx, "ray_backward_kernel"));
   }
-  PACT_TRY_S(allow_smem(ray_backward_kernel<false>, smem));
-  ray_backward_kernel<false><<<div_up(a.n_rays, 256), 256, smem, ctx->stream>>>(a, dw, grad);
-  return after_launch(ctx, "ray_backward_kernel");
+  fix_to_grad_kernel<<<div_up(static_cast<int>(npx), 256), 256, 0, ctx->stream>>>(
+      acc, rep, a.W, a.H, stats, a.step, a.v0, max_steps_total(a), grad);
+  return after_launch(ctx, "fix_to_grad_kernel");
 }
 
 // Standalone entry points: a texture over the caller's raster for the

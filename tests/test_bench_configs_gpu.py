@@ -258,3 +258,24 @@ def test_cfg5_window_covers_lookups(W5):
     t_max = 1e-3 * (w.ring.radius + r_max - min(w.delays)) / w.v0
     assert t_min >= w.meta.t0
     assert t_max <= w.meta.t0 + (w.meta.n_samples - 1) * w.meta.dt
+
+
+def test_cfg3_training_is_bitwise_deterministic(ctx, W3, sig3):
+    """Two engines on the same cfg3 frame and seed give bitwise-identical
+    dL/dv, gradients and parameters after two iterations: the ray adjoint
+    accumulates in 64-bit fixed point (order-independent integer sums) and
+    every other reduction runs in a fixed order."""
+    w = W3
+    cfg = wl.train_config(w, seed=0, epochs=1, steps_per_epoch=2)
+    out = []
+    for _ in range(2):
+        tr = Trainer(ctx, sig3, w.ring, w.meta, w.grid, w.mask, cfg)
+        tr.step(2)
+        out.append((tr.read(5, (w.grid.height, w.grid.width), np.float64),
+                    tr.read(6, (tr.n_params,), np.float64), tr.theta(), tr.report(1)))
+        tr.close()
+    (gv_a, g_a, th_a, r_a), (gv_b, g_b, th_b, r_b) = out
+    assert np.array_equal(gv_a, gv_b)
+    assert np.array_equal(g_a, g_b)
+    assert np.array_equal(th_a, th_b)
+    assert r_a == r_b
