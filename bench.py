@@ -290,6 +290,77 @@ def cpu_baseline_leg(sig64, n_patch_sample=8):
 # our arm
 # --------------------------------------------------------------------------- #
 
+CFG5_WARMUP, CFG5_STEPS = 2, 5
+
+
+def cfg5_line(ctx, rank, world, local):
+    """BASELINE configs[4] (cfg5: one 2048^2 frame, N=1024, T=8192, K=64, 961
+    patches of 128^2, SIREN 2->256x4->1) over the job's ranks: each rank owns
+    1/N of the patch rows (and beamforms only their row band) and 1/N of the
+    pixels; NCCL all-gather / reduce-scatter / all-reduce between the phases
+    (distributed.PartitionedFrame).  ms per full iteration (max over ranks,
+    CUDA events) and the DAS of the rank's row band."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2409_10876_b200 import workloads as wl
+    from paper_2409_10876_b200.api import GridSpec, Trainer
+    from paper_2409_10876_b200.distributed import PartitionedFrame, TorchComm
+
+    w = wl.cfg5()
+    sig = wl.simulate(ctx, w, seed=0)
+    cfg = wl.train_config(w, seed=0)
+    tr = Trainer(ctx, sig, w.ring, w.meta, w.grid, w.mask, cfg,
+                 partition=(rank, world) if world > 1 else None)
+    info = tr.local()
+    frame = PartitionedFrame(tr, TorchComm()) if world > 1 else None
+
+    def step():
+        if frame is None:
+            tr.step(1)
+        else:
+            frame.step(1)
+
+    def timed(fn, reps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / reps], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(CFG5_WARMUP):
+        step()
+    it_ms = timed(step, CFG5_STEPS)
+    data, tv, _ = tr.report(1)
+    tr.close()
+    # DAS of this rank's row band (the stack rows its patches cover)
+    r0, nr = info["stack_row0"], info["stack_rows"]
+    g = w.grid
+    band = GridSpec(g.width, nr, g.pitch, g.origin_x, g.origin_y + r0 * g.pitch)
+    out = torch.empty((len(w.delays), nr, g.width), device="cuda")
+    das = lambda: ctx.das_stack(sig, w.ring, w.meta, band, w.v0, w.delays, out=out)  # noqa: E731
+    das()
+    das_ms = timed(das, 3)
+    taps = len(w.delays) * g.width * g.height * w.ring.n_transducers
+    return {"workload": "cfg5 (BASELINE configs[4]): 2048x2048 @0.05mm, N=1024, T=8192, K=64 "
+                        "in [-3,3] mm, 961 patches 128x128, SIREN 2->256x4->1",
+            "ranks": world, "ms_per_iteration": it_ms, "iterations_per_s": 1e3 / it_ms,
+            "steps": CFG5_STEPS, "warmup": CFG5_WARMUP,
+            "collectives": ("all_gather dv, reduce_scatter dL/dv (overlapping TV), all_reduce "
+                            "report/flags/gradient (NCCL)") if world > 1 else "none (one rank)",
+            "das_band_rows": nr, "das_ms": das_ms,
+            "das_gsamples_per_s": taps * (nr / g.height) * world / (das_ms * 1e-3) / 1e9,
+            "loss_report": {"data_term": data, "tv_term": tv}}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -467,6 +538,11 @@ def run_ours(args):
                                    "bf16 / 6) + ray and loss algorithmic bytes at measured HBM; "
                                    "measured = sum of stage CUDA-event times of one frame"}
 
+    cfg5 = None
+    if not args.no_cfg5:
+        torch.cuda.empty_cache()
+        cfg5 = cfg5_line(ctx, rank, world, local)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_leg(hin[my_frames[0]].double().numpy())
@@ -500,6 +576,7 @@ def run_ours(args):
                                  "frac": das_ach / hbm, "peak_source": peak_src,
                                  "byte_model": "8*S + 4*K*W*H + 4*N*T, S = W*H*K*N"}},
             "loss_report_frame0": reports[0],
+            "cfg5": cfg5,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -532,6 +609,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cfg5", action="store_true")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args.gpus))

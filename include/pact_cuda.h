@@ -433,12 +433,17 @@ int pact_trainer_step(pact_trainer* tr, int32_t n_steps);
  * Rank `rank` of `world` owns the patch rows [ny*rank/world, ny*(rank+1)/world)
  * (spectra, wavefronts, loss, ray adjoint) and the masked pixels
  * [n*rank/world, n*(rank+1)/world) of the row-major list (SIREN forward and
- * backward, TV).  Every rank keeps the full dv and dL/dv rasters and a replica
- * of theta and Adam.  The iteration then runs as phases with the caller's
- * collectives in between (buffers: pact_trainer_buffer):
+ * backward, TV); its DAS stack covers only those patches' grid rows.  Every
+ * rank keeps the full dv and dL/dv rasters and a replica of theta and Adam.
+ * The iteration then runs as phases with the caller's collectives in between
+ * (buffers: pact_trainer_buffer):
  *   phase 0  render own pixels into a cleared dv     -> all-reduce dv (2, f32, SUM)
+ *            (or all-gather, when the pixel shares are equal raster slabs)
  *   phase 1  wavefront, loss, ray adjoint, TV, report -> all-reduce dL/dv (5, f64, SUM),
  *            report (8, f64[3], SUM), flags (9, u32, MAX)
+ *            (phase 1 = phase 6 (wavefront, loss, ray adjoint) then phase 7
+ *            (TV, report): the dL/dv collective — a reduce-scatter to the
+ *            pixel slabs — can run while phase 7 does)
  *   phase 2  SIREN backward                          -> all-reduce gradient (6, f64, SUM)
  *   phase 3  finiteness check + Adam (identical on every rank)
  * and the final image as
@@ -456,7 +461,9 @@ int pact_trainer_create_partitioned(pact_ctx* ctx, const pact_ring* ring,
                                     const pact_train_config* cfg, const pact_partition* part,
                                     pact_trainer** out);
 int pact_trainer_phase(pact_trainer* tr, int32_t phase);
-/* info[7] = {patch lo, patch hi, pixel lo, pixel hi, total patches, rank, world} */
+/* info[9] = {patch lo, patch hi, pixel lo, pixel hi, total patches, rank, world,
+ *            first stack row, stack rows}: the DAS stack holds only the grid
+ * rows [row0, row0 + rows) the local patches cover (the row-tile split). */
 int pact_trainer_local(pact_trainer* tr, int32_t* info);
 /* Last step's LossReport terms {data, tv, total} (host) and the NumericalError
  * check of joint_reconstruct; synchronises.  `epoch` is used in the message. */

@@ -649,6 +649,8 @@ class Trainer:
                 ctx.handle, C.byref(r), C.byref(m), dptr(self._signals), C.byref(g), C.byref(mk),
                 C.byref(c), C.byref(p), C.byref(h)))
         self._h = h
+        self.mask = mask
+        self.n_masked = int(_abi.lib().pact_masked_count(C.byref(g), C.byref(mk)))
         self.n_params = SirenSpec(cfg.hidden, cfg.sine_layers, cfg.omega0, cfg.out_scale,
                                   meta.background_sos).param_count()
 
@@ -684,15 +686,16 @@ class Trainer:
         return int(_abi.lib().pact_trainer_buffer(self._h, what) or 0)
 
     def phase(self, k: int):
-        """pact_trainer_phase: one phase of the iteration (0-3) or of the final
-        image (4-5); asynchronous on the engine stream."""
+        """pact_trainer_phase: one phase of the iteration (0-3; 1 = 6 then 7)
+        or of the final image (4-5); asynchronous on the engine stream."""
         check(_abi.lib().pact_trainer_phase(self._h, int(k)))
 
     def local(self) -> dict:
         """The partition this trainer owns (pact_trainer_local)."""
-        info = (C.c_int32 * 7)()
+        info = (C.c_int32 * 9)()
         check(_abi.lib().pact_trainer_local(self._h, info))
-        keys = ("patch_lo", "patch_hi", "pixel_lo", "pixel_hi", "n_patches", "rank", "world")
+        keys = ("patch_lo", "patch_hi", "pixel_lo", "pixel_hi", "n_patches", "rank", "world",
+                "stack_row0", "stack_rows")
         return dict(zip(keys, list(info)))
 
     def view(self, what: int, shape, dtype: torch.dtype) -> torch.Tensor:

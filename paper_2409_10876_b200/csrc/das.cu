@@ -63,6 +63,7 @@ struct DasArgs {
   int n_tx, n_samples;
   int width, height;
   double ox, oy, pitch;
+  int row0;       // first grid row of the computed band (its rows are 0..height-1 here)
   double k_dist;  // samples per mm of path: 1e-3 / (v0 dt)
   double s_off;   // t0 / dt
   double cmin, cmax;
@@ -112,9 +113,10 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
   const int xe = min(x0 + kTile, a.width) - 1, ye = min(y0 + kTile, a.height) - 1;
 
   const double rx0 = a.ox + x0 * a.pitch, rx1 = a.ox + xe * a.pitch;
-  const double ry0 = a.oy + y0 * a.pitch, ry1 = a.oy + ye * a.pitch;
-  // Pixel world position, GridSpec::world (core.hpp:71).
-  const double wx = a.ox + px * a.pitch, wy = a.oy + py * a.pitch;
+  const double ry0 = a.oy + (y0 + a.row0) * a.pitch, ry1 = a.oy + (ye + a.row0) * a.pitch;
+  // Pixel world position, GridSpec::world (core.hpp:71), in the full grid's
+  // coordinates (a band of rows gives bit-identical values to the full stack).
+  const double wx = a.ox + px * a.pitch, wy = a.oy + (py + a.row0) * a.pitch;
 
   const int n_begin = blockIdx.z * a.tx_per_split;
   const int n_end = min(a.n_tx, n_begin + a.tx_per_split);
@@ -265,8 +267,8 @@ Status launch_block(pact_ctx* ctx, DasArgs a, const double* c, int nsplit, dim3 
 }  // namespace
 
 Status das_stack_device(pact_ctx* ctx, const pact_ring& ring, const pact_signal_meta& meta,
-                        const float* signals, const pact_grid& grid, double v0,
-                        const double* delays, int K, float* out) {
+                        const float* signals, const pact_grid& full_grid, double v0,
+                        const double* delays, int K, float* out, int row0, int rows) {
   // Validation order follows das_stack (beamform.hpp:79-85).
   if (K < 1) return validation("das_stack: need at least one delay");
   for (int j = 1; j < K; ++j)
@@ -276,10 +278,17 @@ Status das_stack_device(pact_ctx* ctx, const pact_ring& ring, const pact_signal_
   if (!(ring.radius > 0.0)) return validation("ring: radius must be > 0");
   if (meta.n_samples < 2) return validation("signals: need at least 2 samples");
   if (!(meta.dt > 0.0)) return validation("signals: dt must be > 0");
-  if (grid.width < 1 || grid.height < 1) return validation("grid: width and height must be >= 1");
-  if (!(grid.pitch > 0.0)) return validation("grid: pitch must be > 0");
+  if (full_grid.width < 1 || full_grid.height < 1)
+    return validation("grid: width and height must be >= 1");
+  if (!(full_grid.pitch > 0.0)) return validation("grid: pitch must be > 0");
   if (!(v0 > 0.0)) return validation("das_stack: v0 must be > 0");
   if (!signals || !out) return validation("das_stack: null buffer");
+  // the band [row0, row0 + rows) of the grid (rows < 0: all of it)
+  if (rows < 0) rows = full_grid.height - row0;
+  if (row0 < 0 || rows < 1 || row0 + rows > full_grid.height)
+    return internal_error("das_stack_device: bad row band");
+  pact_grid grid = full_grid;
+  grid.height = rows;
 
   const int N = ring.n_transducers, T = meta.n_samples;
   // Transducer positions in fp64, RingGeometry::transducer_position (core.hpp:162-165).
@@ -310,6 +319,7 @@ Status das_stack_device(pact_ctx* ctx, const pact_ring& ring, const pact_signal_
   a.height = grid.height;
   a.ox = grid.origin_x;
   a.oy = grid.origin_y;
+  a.row0 = row0;
   a.pitch = grid.pitch;
   a.k_dist = k_dist;
   a.s_off = meta.t0 / meta.dt;
@@ -384,6 +394,6 @@ extern "C" int pact_das_stack(pact_ctx* ctx, const pact_ring* ring, const pact_s
   if (!ctx || !ring || !meta || !grid || (!delays && n_delays > 0))
     return pactgpu::validation("pact_das_stack: null argument").code;
   if (n_delays < 1) return pactgpu::validation("das_stack: need at least one delay").code;
-  return pactgpu::das_stack_device(ctx, *ring, *meta, signals, *grid, v0, delays, n_delays, out)
+  return pactgpu::das_stack_device(ctx, *ring, *meta, signals, *grid, v0, delays, n_delays, out, 0, -1)
       .code;
 }

@@ -10,6 +10,8 @@
 // direct DFT like the reference.  The patch gather is fused into the load
 // (no separate crop pass) and the inverse keeps only the real part.
 #include <cmath>
+#include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -91,6 +93,53 @@ __device__ void make_twiddles(float2* tw, int P, double sign) {
   }
 }
 
+// ---- register-resident radix-4 transforms (P = 64) -------------------------
+// A 64-point DFT held in one thread's registers: three radix-4 DIF stages,
+// fully unrolled, twiddles from a __constant__ table at compile-time indices
+// (uniform reads: FFMA constant-bank operands), output in base-4
+// digit-reversed register order (renamed away by rev4 at compile time).  A
+// 2-D transform is 64 threads: column FFTs straight from the coalesced patch
+// load, a padded shared-memory transpose, row FFTs, and a shared-memory pass
+// so the complex output is stored coalesced.  No per-stage barriers.
+__constant__ float2 c_tw64[64];  // exp(-2 pi i q / 64), fp64-accurate
+
+__host__ __device__ constexpr int rev4_3(int k) {  // reverse 3 base-4 digits
+  return ((k & 3) << 4) | (k & 12) | ((k >> 4) & 3);
+}
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }  // -i a
+
+// forward (e^{-i}) 64-point DFT in place; a[rev4_3(k)] = X[k] afterwards
+__device__ __forceinline__ void fft64_regs(float2 (&a)[64]) {
+#pragma unroll
+  for (int L = 64; L >= 4; L >>= 2) {
+    const int Q = L >> 2, stride = 64 / L;
+#pragma unroll
+    for (int base = 0; base < 64; base += L) {
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        const float2 x0 = a[base + j], x1 = a[base + j + Q], x2 = a[base + j + 2 * Q],
+                     x3 = a[base + j + 3 * Q];
+        const float2 t0 = cadd(x0, x2), t1 = csub(x0, x2), t2 = cadd(x1, x3),
+                     t3 = mul_mi(csub(x1, x3));
+        a[base + j] = cadd(t0, t2);
+        const float2 y1 = cadd(t1, t3), y2 = csub(t0, t2), y3 = csub(t1, t3);
+        if (j == 0) {
+          a[base + j + Q] = y1;
+          a[base + j + 2 * Q] = y2;
+          a[base + j + 3 * Q] = y3;
+        } else {
+          a[base + j + Q] = cm(y1, c_tw64[(stride * j) & 63]);
+          a[base + j + 2 * Q] = cm(y2, c_tw64[(stride * 2 * j) & 63]);
+          a[base + j + 3 * Q] = cm(y3, c_tw64[(stride * 3 * j) & 63]);
+        }
+      }
+    }
+  }
+}
+
 struct LayoutDev {
   int P, nx, ny, stride, last_x, last_y, W, H;
 };
@@ -102,7 +151,7 @@ __device__ __forceinline__ int patch_offset(int i, int n, int stride, int last) 
 
 // Y[patch][j] = FFT2(stack[j][oy:oy+P, ox:ox+P])       grid (n_patches, K)
 __global__ void patch_fft_kernel(LayoutDev L, const float* __restrict__ stack, int K, int logP,
-                                 float2* __restrict__ Y, int p_lo) {
+                                 float2* __restrict__ Y, int p_lo, int row0, int rows) {
   extern __shared__ float2 sm[];
   const int P = L.P, P2 = P * P;
   float2* buf = sm;
@@ -113,15 +162,78 @@ __global__ void patch_fft_kernel(LayoutDev L, const float* __restrict__ stack, i
   const int ox = patch_offset(px, L.nx, L.stride, L.last_x);
   const int oy = patch_offset(py, L.ny, L.stride, L.last_y);
   make_twiddles(tw, P, -1.0);
-  const float* img = stack + static_cast<size_t>(j) * L.W * L.H;
+  const float* img = stack + static_cast<size_t>(j) * L.W * rows;
   for (int e = threadIdx.x; e < P2; e += blockDim.x) {
     int y = e / P, x = e - y * P;
-    buf[e] = make_float2(img[static_cast<size_t>(oy + y) * L.W + ox + x], 0.f);
+    buf[e] = make_float2(img[static_cast<size_t>(oy + y - row0) * L.W + ox + x], 0.f);
   }
   __syncthreads();
   fft2d(buf, scratch, tw, P, logP);
   float2* out = Y + (static_cast<size_t>(blockIdx.x) * K + j) * P2;
   for (int e = threadIdx.x; e < P2; e += blockDim.x) out[e] = buf[e];
+}
+
+// Y[patch][j] = FFT2(stack[j][oy:oy+P, ox:ox+P]) for P = 64, 64 threads per
+// transform (thread c: column c, then row c).                 grid (n_patches, K)
+__global__ void __launch_bounds__(64) patch_fft64_kernel(LayoutDev L, const float* __restrict__ stack,
+                                                         int K, float2* __restrict__ Y, int p_lo,
+                                                         int row0, int rows) {
+  __shared__ float2 s[64][65];
+  const int c = threadIdx.x;
+  const int patch = p_lo + blockIdx.x, j = blockIdx.y;
+  const int px = patch % L.nx, py = patch / L.nx;
+  const int ox = patch_offset(px, L.nx, L.stride, L.last_x);
+  const int oy = patch_offset(py, L.ny, L.stride, L.last_y);
+  const float* img = stack + static_cast<size_t>(j) * L.W * rows +
+                     static_cast<size_t>(oy - row0) * L.W + ox + c;
+  float2 a[64];
+#pragma unroll
+  for (int y = 0; y < 64; ++y) a[y] = make_float2(__ldcs(img + static_cast<size_t>(y) * L.W), 0.f);
+  fft64_regs(a);  // columns: a[rev(ky)] = Z[ky][c]
+#pragma unroll
+  for (int ky = 0; ky < 64; ++ky) s[ky][c] = a[rev4_3(ky)];
+  __syncthreads();
+#pragma unroll
+  for (int kx = 0; kx < 64; ++kx) a[kx] = s[c][kx];  // row ky = c
+  fft64_regs(a);  // rows: a[rev(kx)] = Y[c][kx]
+  __syncthreads();
+#pragma unroll
+  for (int kx = 0; kx < 64; ++kx) s[c][kx] = a[rev4_3(kx)];
+  __syncthreads();
+  float2* out = Y + (static_cast<size_t>(blockIdx.x) * K + j) * 4096 + c;
+#pragma unroll
+  for (int ky = 0; ky < 64; ++ky) __stcs(out + ky * 64, s[ky][c]);
+}
+
+// out[patch] = Re(IFFT2(X[patch])) / 64^2 = Re(FFT2(conj X)) / 64^2 (the
+// reference's inverse_2d, fft.hpp:107-115, real part kept), P = 64.
+__global__ void __launch_bounds__(64) patch_ifft64_real_kernel(const float2* __restrict__ X,
+                                                               float* __restrict__ out) {
+  __shared__ float2 s[64][65];
+  const int c = threadIdx.x;
+  const float2* x = X + static_cast<size_t>(blockIdx.x) * 4096 + c;
+  float2 a[64];
+#pragma unroll
+  for (int y = 0; y < 64; ++y) {
+    const float2 v = x[y * 64];
+    a[y] = make_float2(v.x, -v.y);
+  }
+  fft64_regs(a);
+#pragma unroll
+  for (int ky = 0; ky < 64; ++ky) s[ky][c] = a[rev4_3(ky)];
+  __syncthreads();
+#pragma unroll
+  for (int kx = 0; kx < 64; ++kx) a[kx] = s[c][kx];
+  fft64_regs(a);
+  __syncthreads();
+  float* sr = reinterpret_cast<float*>(&s[0][0]);  // [64][65] real plane
+#pragma unroll
+  for (int kx = 0; kx < 64; ++kx) sr[c * 65 + kx] = a[rev4_3(kx)].x;
+  __syncthreads();
+  float* o = out + static_cast<size_t>(blockIdx.x) * 4096 + c;
+  const float inv = 1.f / 4096.f;
+#pragma unroll
+  for (int y = 0; y < 64; ++y) o[y * 64] = sr[y * 65 + c] * inv;
 }
 
 // out[patch][P2] = Re(IFFT2(X[patch])) / (P*P)           grid (n_patches)
@@ -215,22 +327,61 @@ LayoutDev layout_dev(const pact_layout& l) {
   return d;
 }
 
+// c_tw64 once per device (the constant bank is per device context)
+Status twiddles64() {
+  int dev = 0;
+  PACT_CUDA_S(cudaGetDevice(&dev));
+  static std::once_flag once[64];
+  static cudaError_t err[64];
+  std::call_once(once[dev & 63], [dev] {
+    float2 tw[64];
+    for (int q = 0; q < 64; ++q) {
+      const double ang = -2.0 * M_PI * q / 64.0;
+      tw[q] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+    }
+    err[dev & 63] = cudaMemcpyToSymbol(c_tw64, tw, sizeof(tw));
+  });
+  return cuda_status(err[dev & 63], "cudaMemcpyToSymbol(c_tw64)");
+}
+
+bool fft64_enabled() {
+  static const bool off = [] {  // PACT_FFT_SMEM=1: the shared-memory radix-2 kernels
+    const char* e = std::getenv("PACT_FFT_SMEM");
+    return e && e[0] == '1';
+  }();
+  return !off;
+}
+
 }  // namespace
 
 Status launch_patch_fft(pact_ctx* ctx, const pact_layout& lay, const float* stack, int K,
-                        float2* Y, int p_lo, int p_hi) {
+                        float2* Y, int p_lo, int p_hi, int row0, int stack_rows) {
   if (p_hi < 0) p_hi = lay.nx * lay.ny;
+  if (stack_rows < 0) stack_rows = lay.grid.height - row0;
+  if (lay.patch_pixels == 64 && fft64_enabled()) {
+    PACT_TRY_S(twiddles64());
+    if (p_hi <= p_lo) return {};
+    patch_fft64_kernel<<<dim3(p_hi - p_lo, K), 64, 0, ctx->stream>>>(layout_dev(lay), stack, K, Y,
+                                                                     p_lo, row0, stack_rows);
+    return after_launch(ctx, "patch_fft64_kernel");
+  }
   const int P = lay.patch_pixels, logP = ilog2_exact(P);
   size_t smem = fft_smem(P, logP);
   if (smem > 220 * 1024) return validation("extract_patch_spectra: patch too large for the device FFT");
   PACT_TRY_S(smem_optin(patch_fft_kernel, smem));
   if (p_hi <= p_lo) return {};
   dim3 g(p_hi - p_lo, K);
-  patch_fft_kernel<<<g, 512, smem, ctx->stream>>>(layout_dev(lay), stack, K, logP, Y, p_lo);
+  patch_fft_kernel<<<g, 512, smem, ctx->stream>>>(layout_dev(lay), stack, K, logP, Y, p_lo, row0,
+                                                   stack_rows);
   return after_launch(ctx, "patch_fft_kernel");
 }
 
 Status launch_patch_ifft_real(pact_ctx* ctx, int P, int n_patches, const float2* X, float* out) {
+  if (P == 64 && fft64_enabled()) {
+    PACT_TRY_S(twiddles64());
+    patch_ifft64_real_kernel<<<n_patches, 64, 0, ctx->stream>>>(X, out);
+    return after_launch(ctx, "patch_ifft64_real_kernel");
+  }
   const int logP = ilog2_exact(P);
   size_t smem = fft_smem(P, logP);
   PACT_TRY_S(smem_optin(patch_ifft_real_kernel, smem));

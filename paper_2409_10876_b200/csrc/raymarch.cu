@@ -644,59 +644,88 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
   }
 }
 
-// grad[p] += (acc[p] + the replicas' slots of p when p is on the border) 2^-S,
-// one thread per pixel; the accumulators it read are reset to zero for the
-// next launch, so the raster needs no per-launch memset.
-__global__ void fix_to_grad_kernel(unsigned long long* __restrict__ acc,
-                                   unsigned long long* __restrict__ rep, int W, int H,
-                                   const unsigned long long* __restrict__ stats, double step, double v0,
-                                   double max_steps, double* __restrict__ grad) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int S = fix_exponent(stats, step, v0, max_steps);
-  if (i >= W * H) return;
-  const int py = i / W, px = i - py * W;
-  long long v = static_cast<long long>(acc[i]);
-  acc[i] = 0ull;
-  if (rep && (px == 0 || px == W - 1 || py == 0 || py == H - 1)) {
-    const int col = px == 0 ? py : (px == W - 1 ? H + py : -1);
-    const int row = py == 0 ? 2 * H + px : (py == H - 1 ? 2 * H + W + px : -1);
-    const size_t stride = 2 * static_cast<size_t>(W + H);
-    for (int r = 0; r < kBorderReplicas; ++r) {
-      if (col >= 0) {
-        v += static_cast<long long>(rep[r * stride + col]);
-        rep[r * stride + col] = 0ull;
-      }
-      if (row >= 0) {
-        v += static_cast<long long>(rep[r * stride + row]);
-        rep[r * stride + row] = 0ull;
-      }
-    }
+// Border replicas -> the raster accumulator: one warp per border slot
+// ([colL H | colR H | rowB W | rowT W]), lane r reading replica r (32 loads in
+// flight per warp); the integer sum is exact, so folding it into acc with an
+// integer atomic keeps the result order-independent.  Slots are reset.
+__global__ void border_fold_kernel(unsigned long long* __restrict__ rep, int W, int H,
+                                   unsigned long long* __restrict__ acc) {
+  const int slot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int n_slots = 2 * (W + H);
+  if (slot >= n_slots) return;
+  const size_t stride = static_cast<size_t>(n_slots);
+  unsigned long long v = 0ull;
+  for (int r = lane; r < kBorderReplicas; r += 32) {
+    v += rep[r * stride + slot];
+    rep[r * stride + slot] = 0ull;
   }
-  if (v != 0) grad[i] += ldexp(static_cast<double>(v), -S);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane != 0 || v == 0ull) return;
+  int px, py;
+  if (slot < 2 * H) {
+    px = slot < H ? 0 : W - 1;
+    py = slot < H ? slot : slot - H;
+  } else {
+    const int q = slot - 2 * H;
+    px = q < W ? q : q - W;
+    py = q < W ? 0 : H - 1;
+  }
+  atomicAdd(acc + static_cast<size_t>(py) * W + px, v);
+}
+
+// grad[p] += acc[p] 2^-S, one thread per pixel (four per thread, vectorised);
+// the accumulator is reset for the next launch, so the raster needs no
+// per-launch memset.
+__global__ void fix_to_grad_kernel(unsigned long long* __restrict__ acc, int npx,
+                                   const unsigned long long* __restrict__ stats, double step,
+                                   double v0, double max_steps, double* __restrict__ grad) {
+  const int S = fix_exponent(stats, step, v0, max_steps);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npx) return;
+  const long long v = static_cast<long long>(acc[i]);
+  if (v != 0) {
+    acc[i] = 0ull;
+    grad[i] += ldexp(static_cast<double>(v), -S);
+  }
 }
 
 // Bound statistics of one adjoint launch (exact maxima, order-independent):
 // stats[0] = max |dL/dw| over the rays, stats[1] = max 1 / v^2 over the
-// raster (non-negative doubles order like their bit patterns).
-__global__ void ray_bound_kernel(const float* __restrict__ dw, int n_rays,
-                                 const float* __restrict__ dv, int npx, float v0,
-                                 unsigned long long* __restrict__ stats) {
-  double g = 0.0, iv = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rays; i += gridDim.x * blockDim.x)
-    g = fmax(g, fabs(static_cast<double>(dw[i])));
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npx; i += gridDim.x * blockDim.x) {
-    const double v = static_cast<double>(v0) + static_cast<double>(dv[i]);
-    iv = fmax(iv, v > 0.0 ? 1.0 / (v * v) : INFINITY);
+// raster = 1 / min(v)^2 (non-negative doubles order like their bit patterns).
+__global__ void __launch_bounds__(256) ray_bound_kernel(const float* __restrict__ dw, int n_rays,
+                                                        const float* __restrict__ dv, int npx,
+                                                        float v0,
+                                                        unsigned long long* __restrict__ stats) {
+  __shared__ float s_g[8], s_v[8];
+  float g = 0.f, vmin = INFINITY;
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rays; i += stride) {
+    const float x = fabsf(dw[i]);
+    g = x != x ? INFINITY : fmaxf(g, x);  // NaN -> infinite bound
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npx; i += stride) {
+    const float x = dv[i];
+    vmin = x != x ? -INFINITY : fminf(vmin, x);
   }
   for (int o = 16; o > 0; o >>= 1) {
-    g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
-    iv = fmax(iv, __shfl_xor_sync(0xffffffffu, iv, o));
+    g = fmaxf(g, __shfl_xor_sync(0xffffffffu, g, o));
+    vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
   }
   if ((threadIdx.x & 31) == 0) {
-    if (g != 0.0 || isnan(g))
-      atomicMax(stats, static_cast<unsigned long long>(__double_as_longlong(isnan(g) ? INFINITY : g)));
-    atomicMax(stats + 1, static_cast<unsigned long long>(__double_as_longlong(isnan(iv) ? INFINITY : iv)));
+    s_g[threadIdx.x >> 5] = g;
+    s_v[threadIdx.x >> 5] = vmin;
   }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+    g = fmaxf(g, s_g[w]);
+    vmin = fminf(vmin, s_v[w]);
+  }
+  const double v = static_cast<double>(v0) + static_cast<double>(vmin);
+  const double iv = v > 0.0 ? 1.0 / (v * v) : INFINITY;
+  if (g != 0.f) atomicMax(stats, static_cast<unsigned long long>(__double_as_longlong(static_cast<double>(g))));
+  atomicMax(stats + 1, static_cast<unsigned long long>(__double_as_longlong(iv)));
 }
 
 // Generic kernels (plain loads, no texture): one per-step march per ray.
@@ -1049,7 +1078,7 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
   auto* rep = acc + npx;
   auto* stats = rep + rep_n;
   PACT_CUDA_S(cudaMemsetAsync(stats, 0, 2 * sizeof(unsigned long long), ctx->stream));
-  const int nb = std::max(1, std::min(2 * ctx->num_sms, div_up(static_cast<int>(npx), 256)));
+  const int nb = std::max(1, std::min(ctx->num_sms, div_up(static_cast<int>(npx), 1024)));
   ray_bound_kernel<<<nb, 256, 0, ctx->stream>>>(dw, a.n_rays, a.dv, static_cast<int>(npx),
                                                 static_cast<float>(a.v0), stats);
   PACT_TRY_S(after_launch(ctx, "ray_bound_kernel"));
@@ -1066,8 +1095,13 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
     ray_backward_kernel<false><<<div_up(a.n_rays, 256), 256, smem, ctx->stream>>>(a, dw, acc, stats);
     PACT_TRY_S(after_launch(ctx, "ray_backward_kernel"));
   }
+  if (a.tex) {
+    const int n_slots = 2 * (a.W + a.H);
+    border_fold_kernel<<<div_up(n_slots, 8), 256, 0, ctx->stream>>>(rep, a.W, a.H, acc);
+    PACT_TRY_S(after_launch(ctx, "border_fold_kernel"));
+  }
   fix_to_grad_kernel<<<div_up(static_cast<int>(npx), 256), 256, 0, ctx->stream>>>(
-      acc, rep, a.W, a.H, stats, a.step, a.v0, max_steps_total(a), grad);
+      acc, static_cast<int>(npx), stats, a.step, a.v0, max_steps_total(a), grad);
   return after_launch(ctx, "fix_to_grad_kernel");
 }
 

@@ -47,8 +47,9 @@ Status launch_wiener(pact_ctx* ctx, const FourierTab& t, const float2* Y, const 
                      int n_patches, double eps, float2* X);
 
 // Spectra of the patches [p_lo, p_hi) (p_hi < 0: all), Y indexed from p_lo.
+// stack holds the grid rows [row0, row0 + stack_rows) (stack_rows < 0: H - row0)
 Status launch_patch_fft(pact_ctx* ctx, const pact_layout& lay, const float* stack, int K,
-                        float2* Y, int p_lo = 0, int p_hi = -1);
+                        float2* Y, int p_lo = 0, int p_hi = -1, int row0 = 0, int stack_rows = -1);
 Status launch_patch_ifft_real(pact_ctx* ctx, int P, int n_patches, const float2* X, float* out);
 Status launch_merge(pact_ctx* ctx, const pact_layout& lay, const float* patches, const float* win,
                     float* img);
@@ -69,9 +70,11 @@ Status launch_adam(pact_ctx* ctx, int n, double* theta, const double* grad, doub
                    long long* t, double lr, double b1, double b2, double eps,
                    const unsigned* flags, float* theta32, bool tick);
 
+// das_stack of the rows [row0, row0 + rows) of `grid` (rows < 0: to the
+// bottom) into out [K][rows][W]; values are those of the full-grid stack.
 Status das_stack_device(pact_ctx* ctx, const pact_ring& ring, const pact_signal_meta& meta,
                         const float* signals, const pact_grid& grid, double v0,
-                        const double* delays, int K, float* out);
+                        const double* delays, int K, float* out, int row0 = 0, int rows = -1);
 
 // make_patch_layout (core.hpp:252-281) on the host; centres in fp64.
 Status make_layout(const pact_grid& grid, double patch_mm, double overlap, pact_layout& out);

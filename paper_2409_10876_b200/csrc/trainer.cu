@@ -59,6 +59,7 @@ struct pact_trainer {
   // patch rows) and masked pixels [m_lo, m_hi) of the row-major list; the
   // caller all-reduces dv, dL/dv, the report and the gradient between phases
   int rank = 0, world = 1, p_lo = 0, p_hi = 0, n_local = 0, m_lo = 0, m_hi = 0;
+  int row0 = 0, rows = 0;  // the stack's row band [row0, row0 + rows) of the grid
   float* num = nullptr;  // merge accumulators of the final image (world > 1)
   float* den = nullptr;
   double loss_scale = 0.0;
@@ -102,6 +103,8 @@ namespace {
 // one at a time with the caller's all-reduces in between:
 //   0 render    -> all-reduce dv (SUM; each pixel has one owner)
 //   1 rays/loss -> all-reduce dL/dv (SUM), report[0..3) (SUM), flags (MAX)
+//     (= 6 wavefronts, loss, ray adjoint -> the dL/dv collective can start,
+//      then 7 TV + report, which overlaps it)
 //   2 SIREN bwd -> all-reduce the gradient (SUM)
 //   3 Adam (replicated)
 Status enqueue_phase(pact_trainer* tr, int phase) {
@@ -116,6 +119,9 @@ Status enqueue_phase(pact_trainer* tr, int phase) {
       PACT_TRY_S(launch_check_finite_f32(ctx, tr->dv, tr->sw.idx, tr->mp.n, kFlagSos, tr->flags));
       return {};
     case 1:
+      PACT_TRY_S(enqueue_phase(tr, 6));
+      return enqueue_phase(tr, 7);
+    case 6:
       // wavefront_profile for every (local) patch (431-433)
       PACT_TRY_S(launch_wavefront(ctx, tr->ray, tr->w));
       // fused_patch_loss_grad (434-436)
@@ -125,6 +131,8 @@ Status enqueue_phase(pact_trainer* tr, int phase) {
       // wavefront_grad_trace into dL/dv (437-438)
       PACT_CUDA_S(cudaMemsetAsync(tr->gv, 0, sizeof(double) * npx, ctx->stream));
       PACT_TRY_S(launch_ray_backward(ctx, tr->ray, tr->dw, tr->gv));
+      return {};
+    case 7:
       // tv_loss (448) and the loss report / checks (442-451)
       PACT_TRY_S(launch_tv(ctx, tr->dv, tr->inmask, tr->sw.idx, tr->mp.n, tr->grid.width,
                            tr->grid.height, tr->cfg.lambda_tv, tr->gtv, tr->tv_partial, tr->n_tv));
@@ -322,6 +330,15 @@ static int trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signa
   tr->p_lo = (tr->lay.ny * part->rank / part->world) * tr->lay.nx;
   tr->p_hi = (tr->lay.ny * (part->rank + 1) / part->world) * tr->lay.nx;
   tr->n_local = tr->p_hi - tr->p_lo;
+  // the grid rows the local patches cover: only they are beamformed (SURVEY
+  // §8(e): DAS split by image-row tiles; each DAS pixel is independent,
+  // beamform.hpp:96-108, so the band equals those rows of the full stack)
+  {
+    auto oy = [&](int py) { return py == tr->lay.ny - 1 ? tr->lay.last_y : py * tr->lay.stride_pixels; };
+    const int py_lo = tr->p_lo / tr->lay.nx, py_hi = (tr->p_hi - 1) / tr->lay.nx;
+    tr->row0 = tr->n_local > 0 ? oy(py_lo) : 0;
+    tr->rows = tr->n_local > 0 ? oy(py_hi) + tr->lay.patch_pixels - tr->row0 : 1;
+  }
   tr->P = tr->lay.patch_pixels;
   tr->K = cfg->n_delays;
   tr->A = cfg->n_angles;
@@ -361,7 +378,7 @@ static int trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signa
   tr->n_tv = std::max(1, std::min(div_up(std::max(tr->mp.n, 1), 256), ctx->num_sms * 4));
   size_t bytes = 0;
   auto add = [&](size_t b) { bytes += (b + 255) & ~size_t(255); };
-  add(sizeof(float) * tr->K * npx);                              // stack
+  add(sizeof(float) * tr->K * grid->width * tr->rows);           // stack (the local row band)
   add(sizeof(float2) * tr->n_local * tr->K * P2);                // Y (local patches)
   add(sizeof(float) * npx);                                      // dv
   add(sizeof(float) * tr->n_local * tr->A);                      // w
@@ -383,7 +400,7 @@ static int trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signa
   st = pool_alloc(&tr->arena, bytes, tr->eng.stream);
   if (!st.ok()) return fail(st.code);
   char* p = static_cast<char*>(tr->arena);
-  tr->stack = carve<float>(p, tr->K * npx);
+  tr->stack = carve<float>(p, static_cast<size_t>(tr->K) * grid->width * tr->rows);
   tr->Y = carve<float2>(p, tr->n_local * tr->K * P2);
   tr->dv = carve<float>(p, npx);
   tr->w = carve<float>(p, tr->n_local * tr->A);
@@ -463,8 +480,9 @@ static int trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signa
   trace.mark("fourier table");
   // DAS stack + spectra, once (optimize.hpp:380-392)
   TRY_ST(das_stack_device(e, *ring, *meta, signals, *grid, v0, tr->delays.data(), tr->K,
-                          tr->stack));
-  TRY_ST(launch_patch_fft(e, tr->lay, tr->stack, tr->K, tr->Y, tr->p_lo, tr->p_hi));
+                          tr->stack, tr->row0, tr->rows));
+  TRY_ST(launch_patch_fft(e, tr->lay, tr->stack, tr->K, tr->Y, tr->p_lo, tr->p_hi, tr->row0,
+                          tr->rows));
   trace.mark("DAS + FFT launched");
   if (sync_end) TRY_CU(cudaStreamSynchronize(s));
   trace.mark("final sync");
@@ -486,7 +504,7 @@ int pact_trainer_phase(pact_trainer* tr, int32_t phase) {
   pact_ctx* e = &tr->eng;
   const size_t npx = static_cast<size_t>(tr->grid.width) * tr->grid.height;
   const size_t P2 = static_cast<size_t>(tr->P) * tr->P;
-  if (phase >= 0 && phase <= 3) {
+  if ((phase >= 0 && phase <= 3) || phase == 6 || phase == 7) {
     PACT_TRY(enqueue_phase(tr, phase));
     if (phase == 3) ++tr->steps_done;
     return PACT_OK;
@@ -523,6 +541,8 @@ int pact_trainer_local(pact_trainer* tr, int32_t* info) {
   info[4] = tr->n_patches;
   info[5] = tr->rank;
   info[6] = tr->world;
+  info[7] = tr->row0;
+  info[8] = tr->rows;
   return PACT_OK;
 }
 

@@ -108,7 +108,22 @@ def test_partitioned_frame_matches_single_rank(ctx, world):
     ref.step(steps)
     want_rep, want_th = ref.report(1), ref.theta()
     want_img, want_sos = ref.finish()
+    K, H, W = len(w.delays), w.grid.height, w.grid.width
+    full_stack = ref.read(0, (K, H, W), np.float32)
     ref.close()
+    # the row-tile DAS split: each rank beamforms only the rows
+    # its patch rows cover, and those rows equal the full stack's bit for bit
+    bands = []
+    for r in range(world):
+        t = Trainer(ctx, sig, w.ring, w.meta, w.grid, w.mask, cfg, partition=(r, world))
+        info = t.local()
+        r0, nr = info["stack_row0"], info["stack_rows"]
+        assert 0 < nr < H
+        band = t.read(0, (K, nr, W), np.float32)
+        assert np.array_equal(band, full_stack[:, r0:r0 + nr])
+        bands.append((r0, nr))
+        t.close()
+    assert bands[0][0] == 0 and bands[-1][0] + bands[-1][1] == H
     reps, thetas, img, sos, infos = _emulated(ctx, sig, w, cfg, world, steps)
     # the partition covers everything exactly once
     assert infos[0]["patch_lo"] == 0 and infos[-1]["patch_hi"] == infos[0]["n_patches"]
