@@ -321,15 +321,24 @@ def cfg5_line(ctx, rank, world, local):
         else:
             frame.step(1)
 
-    def timed(fn, reps):
+    def timed(fn, reps, stream=None):
+        # events on the timing stream, joined with the engine's private stream
+        # (where the iteration's last phase runs) on both sides
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        cur = torch.cuda.current_stream()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
+        a.record(cur)
+        if stream is not None:
+            stream.wait_event(a)
         for _ in range(reps):
             fn()
-        b.record()
+        if stream is not None:
+            e = torch.cuda.Event()
+            e.record(stream)
+            cur.wait_event(e)
+        b.record(cur)
         torch.cuda.synchronize()
         t = torch.tensor([a.elapsed_time(b) / reps], device="cuda", dtype=torch.float64)
         if world > 1:
@@ -338,7 +347,7 @@ def cfg5_line(ctx, rank, world, local):
 
     for _ in range(CFG5_WARMUP):
         step()
-    it_ms = timed(step, CFG5_STEPS)
+    it_ms = timed(step, CFG5_STEPS, tr.stream())
     data, tv, _ = tr.report(1)
     tr.close()
     # DAS of this rank's row band (the stack rows its patches cover)

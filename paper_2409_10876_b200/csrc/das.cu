@@ -308,6 +308,8 @@ Status das_stack_device(pact_ctx* ctx, const pact_ring& ring, const pact_signal_
 
   const int tiles_x = div_up(grid.width, kTile), tiles_y = div_up(grid.height, kTile);
   const int tiles = tiles_x * tiles_y;
+  const int full_tiles = tiles_x * div_up(full_grid.height, kTile);
+  (void)tiles;
   const size_t plane = static_cast<size_t>(grid.width) * grid.height;
 
   DasArgs a{};
@@ -346,7 +348,9 @@ Status das_stack_device(pact_ctx* ctx, const pact_ring& ring, const pact_signal_
     a.cap = cap;
     a.chunk = chunk;
     // Split the transducer range so the launch covers >= 2 waves of CTAs.
-    int want = div_up(2 * ctx->num_sms * 2, tiles);
+    // The split (and so the partial-sum order) follows the FULL grid's tile
+    // count, so a row band's pixels are bit-identical to the full stack's.
+    int want = div_up(2 * ctx->num_sms * 2, full_tiles);
     int max_split = div_up(N, chunk);
     int nsplit = std::max(1, std::min(want, max_split));
     int per = div_up(div_up(N, nsplit), chunk) * chunk;

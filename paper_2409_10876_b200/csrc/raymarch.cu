@@ -644,24 +644,27 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
   }
 }
 
-// Border replicas -> the raster accumulator: one warp per border slot
-// ([colL H | colR H | rowB W | rowT W]), lane r reading replica r (32 loads in
-// flight per warp); the integer sum is exact, so folding it into acc with an
-// integer atomic keeps the result order-independent.  Slots are reset.
+// Border replicas -> the raster accumulator: one thread per border slot
+// ([colL H | colR H | rowB W | rowT W]; consecutive threads, consecutive
+// slots), its kBorderReplicas loads issued back to back; the integer sum is
+// exact, so folding it into acc with an integer atomic keeps the result
+// order-independent.  Slots are reset.
 __global__ void border_fold_kernel(unsigned long long* __restrict__ rep, int W, int H,
                                    unsigned long long* __restrict__ acc) {
-  const int slot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
   const int n_slots = 2 * (W + H);
   if (slot >= n_slots) return;
   const size_t stride = static_cast<size_t>(n_slots);
-  unsigned long long v = 0ull;
-  for (int r = lane; r < kBorderReplicas; r += 32) {
-    v += rep[r * stride + slot];
-    rep[r * stride + slot] = 0ull;
-  }
+  unsigned long long part[kBorderReplicas];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if (lane != 0 || v == 0ull) return;
+  for (int r = 0; r < kBorderReplicas; ++r) part[r] = rep[r * stride + slot];
+  unsigned long long v = 0ull;
+#pragma unroll
+  for (int r = 0; r < kBorderReplicas; ++r) {
+    v += part[r];
+    if (part[r]) rep[r * stride + slot] = 0ull;
+  }
+  if (v == 0ull) return;
   int px, py;
   if (slot < 2 * H) {
     px = slot < H ? 0 : W - 1;
@@ -724,8 +727,11 @@ __global__ void __launch_bounds__(256) ray_bound_kernel(const float* __restrict_
   }
   const double v = static_cast<double>(v0) + static_cast<double>(vmin);
   const double iv = v > 0.0 ? 1.0 / (v * v) : INFINITY;
-  if (g != 0.f) atomicMax(stats, static_cast<unsigned long long>(__double_as_longlong(static_cast<double>(g))));
-  atomicMax(stats + 1, static_cast<unsigned long long>(__double_as_longlong(iv)));
+  // the statistics only grow: skip the atomic when they already exceed ours
+  const auto gb = static_cast<unsigned long long>(__double_as_longlong(static_cast<double>(g)));
+  const auto ib = static_cast<unsigned long long>(__double_as_longlong(iv));
+  if (g != 0.f && *reinterpret_cast<volatile unsigned long long*>(stats) < gb) atomicMax(stats, gb);
+  if (*reinterpret_cast<volatile unsigned long long*>(stats + 1) < ib) atomicMax(stats + 1, ib);
 }
 
 // Generic kernels (plain loads, no texture): one per-step march per ray.
@@ -1078,7 +1084,7 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
   auto* rep = acc + npx;
   auto* stats = rep + rep_n;
   PACT_CUDA_S(cudaMemsetAsync(stats, 0, 2 * sizeof(unsigned long long), ctx->stream));
-  const int nb = std::max(1, std::min(ctx->num_sms, div_up(static_cast<int>(npx), 1024)));
+  const int nb = std::max(1, div_up(std::max(static_cast<int>(npx), a.n_rays), 256 * 4));
   ray_bound_kernel<<<nb, 256, 0, ctx->stream>>>(dw, a.n_rays, a.dv, static_cast<int>(npx),
                                                 static_cast<float>(a.v0), stats);
   PACT_TRY_S(after_launch(ctx, "ray_bound_kernel"));
@@ -1097,7 +1103,7 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
   }
   if (a.tex) {
     const int n_slots = 2 * (a.W + a.H);
-    border_fold_kernel<<<div_up(n_slots, 8), 256, 0, ctx->stream>>>(rep, a.W, a.H, acc);
+    border_fold_kernel<<<div_up(n_slots, 128), 128, 0, ctx->stream>>>(rep, a.W, a.H, acc);
     PACT_TRY_S(after_launch(ctx, "border_fold_kernel"));
   }
   fix_to_grad_kernel<<<div_up(static_cast<int>(npx), 256), 256, 0, ctx->stream>>>(
