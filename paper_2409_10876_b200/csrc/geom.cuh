@@ -139,7 +139,6 @@ struct RayArgs {
   const int2* ray_slots;
   float* partial;
   int n_items;
-  int n_items_main;  // items [0, n_items_main) are generic / interior, the rest border-line
 };
 
 // Creates a point-sampled, clamped pitch-2D texture over a row-major fp32

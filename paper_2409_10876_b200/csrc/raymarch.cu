@@ -91,24 +91,6 @@ struct Fix {
   }
 };
 
-// The same fixed-point value accumulated in shared memory, where the only
-// native atomic add is 32-bit: value = hi * 2^32 + lo (lo unsigned), the
-// carry out of the low word propagated to hi — still exact integer sums.
-struct SFix {
-  unsigned* lo;
-  int* hi;
-  double scale;
-  __device__ __forceinline__ SFix operator+(long long off) const { return {lo + off, hi + off, scale}; }
-  __device__ __forceinline__ void add(float v) const {
-    const long long q = __double2ll_rn(static_cast<double>(v) * scale);
-    const unsigned ql = static_cast<unsigned>(q);
-    const int qh = static_cast<int>(q >> 32);
-    const unsigned old = atomicAdd(lo, ql);
-    const int c = old + ql < old ? 1 : 0;  // carry out of the low word
-    if (qh + c) atomicAdd(hi, qh + c);
-  }
-};
-
 // Per-launch exponent S from the bound statistics (ray_bound_kernel): every
 // deposit is |g| dl v0 / v^2 * beta <= |g|max * step * v0 * max(1/v^2), and a
 // pixel receives at most n_rays * max_steps of them; S keeps that below 2^62.
@@ -417,13 +399,11 @@ __device__ __forceinline__ float interior_d(cudaTextureObject_t tex, float fx, f
   return fmaf(ay, bot - top, top);
 }
 
-// 1-D carry along a border line: pixels (line position q, q + 1), flushed
-// into a deposit target T (Fix: global; SFix: the block's shared slots).
-template <class T>
+// 1-D carry along a border line: pixels (line position q, q + 1).
 struct LineAcc {
   int q = -1;
   float b0 = 0.f, b1 = 0.f;
-  __device__ __forceinline__ void move(T grad, int nq, int stride, int base) {
+  __device__ __forceinline__ void move(Fix grad, int nq, int stride, int base) {
     if (nq == q) return;
     if (q >= 0 && !RAY_NO_LINE_ATOM) {
       if (nq == q + 1) {
@@ -442,7 +422,7 @@ struct LineAcc {
     }
     q = nq;
   }
-  __device__ __forceinline__ void flush(T grad, int stride, int base) {
+  __device__ __forceinline__ void flush(Fix grad, int stride, int base) {
     if (q < 0) return;
     if (b0 != 0.f) (grad + (base + q * stride)).add(b0);
     if (b1 != 0.f) (grad + (base + (q + 1) * stride)).add(b1);
@@ -589,7 +569,7 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
   const Fix rep{border_rep + static_cast<size_t>(blockIdx.x % kBorderReplicas) * 2 * (W + H), scale};
   {
     const int it = blockIdx.x * blockDim.x + threadIdx.x;
-    if (it >= a.n_items_main) return;
+    if (it >= a.n_items) return;
     const int4 item = a.items[it];
     const float gr = dw[item.x];
     if (gr == 0.f) return;  // aberration.hpp:340
@@ -633,6 +613,24 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
         }
       }
       cell.flush(grad, W, H);
+    } else if (kind == kItemSide) {
+      // border line (one loop for both orientations); the replica slice has
+      // the smem border's layout
+      const SideLine sl = side_line(rec_regimes(rr), rec_pixels(rr), W, H);
+      const Fix dst = rep + sl.off;
+      LineAcc line;
+      for (int i = lo; i < hi; ++i) {
+        const float f = fmaf(static_cast<float>(i), sl.df, sl.fs);
+        const int q = min(static_cast<int>(f), sl.qmax);
+        const float fa = f - q, c0 = s_border[sl.off + q];
+        const float v = v0 + fmaf(fa, s_border[sl.off + q + 1] - c0, c0);
+        const float gv = __fdividef(gscale, v * v);
+        line.move(dst, q, 1, 0);
+        const float g1 = gv * fa;
+        line.b0 += gv - g1;
+        line.b1 += g1;
+      }
+      line.flush(dst, 1, 0);
     } else {
       march_backward_generic<true>(a, bd, rec_pixels(rr), rr.n, v0, gscale, grad);
     }
@@ -643,63 +641,6 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
       const float f = __fdividef(gscale, v * v) * static_cast<float>(rr.n - rr.i_corner);
       if (f != 0.f) (rep + ((px == 0 ? 0 : H) + py)).add(f);
     }
-  }
-}
-
-// Border-line items (both orientations, one loop): every step beyond the grid
-// lands on the 2(W + H) border pixels, so the block accumulates its deposits
-// in shared fixed-point slots (SFix; the smem border layout) and adds the
-// non-zero slots to its global replica once at the end — one integer RED per
-// touched slot per block instead of one per line move.
-__global__ void __launch_bounds__(256) ray_backward_side_kernel(RayArgs a, const float* __restrict__ dw,
-                                                                unsigned long long* __restrict__ border_rep,
-                                                                const unsigned long long* __restrict__ stats) {
-  extern __shared__ float smem[];
-  const int W = a.W, H = a.H, nb = 2 * (W + H);
-  unsigned* s_lo = reinterpret_cast<unsigned*>(smem + nb);
-  int* s_hi = reinterpret_cast<int*>(s_lo + nb);
-  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
-    s_lo[i] = 0u;
-    s_hi[i] = 0;
-  }
-  const Border bd = load_border(a, smem);  // (synchronises)
-  const float v0 = static_cast<float>(a.v0);
-  const double scale = ldexp(1.0, fix_exponent(stats, a.step, a.v0, max_steps_total(a)));
-  const SFix slots{s_lo, s_hi, scale};
-  const int it = a.n_items_main + blockIdx.x * blockDim.x + threadIdx.x;
-  const int4 item = it < a.n_items ? a.items[it] : make_int4(0, 0, 0, 0);
-  const float gr = it < a.n_items ? dw[item.x] : 0.f;
-  if (gr != 0.f) {  // aberration.hpp:340
-    const RayRec rr = a.rec[item.x];
-    const float gscale = static_cast<float>(static_cast<double>(gr) * rr.dl * a.v0);
-    const SideLine sl = side_line(rec_regimes(rr), rec_pixels(rr), W, H);
-    const SFix dst = slots + sl.off;
-    LineAcc<SFix> line;
-    for (int i = item.y; i < item.z; ++i) {
-      const float f = fmaf(static_cast<float>(i), sl.df, sl.fs);
-      const int q = min(static_cast<int>(f), sl.qmax);
-      const float fa = f - q, c0 = smem[sl.off + q];
-      const float v = v0 + fmaf(fa, smem[sl.off + q + 1] - c0, c0);
-      const float gv = __fdividef(gscale, v * v);
-      line.move(dst, q, 1, 0);
-      const float g1 = gv * fa;
-      line.b0 += gv - g1;
-      line.b1 += g1;
-    }
-    line.flush(dst, 1, 0);
-    if (item_corner(item.w)) {  // both coordinates clamped: one pixel to the end
-      const int py = rr.dfy > 0.f ? H - 1 : 0;
-      const float* col = rr.dfx > 0.f ? bd.colR : bd.colL;
-      const float v = v0 + col[py];
-      const float fc = __fdividef(gscale, v * v) * static_cast<float>(rr.n - rr.i_corner);
-      if (fc != 0.f) (slots + ((rr.dfx > 0.f ? H : 0) + py)).add(fc);
-    }
-  }
-  __syncthreads();
-  unsigned long long* rep = border_rep + static_cast<size_t>(blockIdx.x % kBorderReplicas) * nb;
-  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
-    const long long v = (static_cast<long long>(s_hi[i]) << 32) + static_cast<long long>(s_lo[i]);
-    if (v) atomicAdd(rep + i, static_cast<unsigned long long>(v));
   }
 }
 
@@ -917,7 +858,6 @@ struct RayPlanData {
   const int4* items = nullptr;
   const int2* ray_slots = nullptr;
   int n_items = 0;
-  int n_main = 0;  // generic + interior items (sorted first); the rest are border-line
   std::vector<double> key;
   ~RayPlanData() {
     if (mem) cudaFree(mem);
@@ -1023,8 +963,6 @@ Status build_plan_data(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanD
   p.items = reinterpret_cast<const int4*>(b + o_items);
   p.ray_slots = reinterpret_cast<const int2*>(b + o_slots);
   p.n_items = ni;
-  p.n_main = 0;
-  for (int k = 0; k < ni; ++k) p.n_main += key[3 * static_cast<size_t>(k)] < 2;
   return {};
 }
 
@@ -1060,7 +998,6 @@ Status ray_plan_get(pact_ctx* cache_ctx, pact_ctx* ctx, RayArgs& a, const double
   a.ray_slots = nullptr;
   a.partial = nullptr;
   a.n_items = 0;
-  a.n_items_main = 0;
   if (!a.tex || a.n_rays <= 0) return {};
   std::vector<double> key = plan_key(a, centers, n_centers);
   RayPlanCache& c = plan_cache(cache_ctx);
@@ -1087,7 +1024,6 @@ Status ray_plan_get(pact_ctx* cache_ctx, pact_ctx* ctx, RayArgs& a, const double
   a.ray_slots = data->ray_slots;
   a.partial = out.partial;
   a.n_items = data->n_items;
-  a.n_items_main = data->n_main;
   return {};
 }
 
@@ -1107,7 +1043,6 @@ Status ray_plan_cached(pact_ctx* ctx, RayArgs& a, const double* centers, int n_c
     a.ray_slots = p.data->ray_slots;
     a.partial = p.partial;
     a.n_items = p.data->n_items;
-    a.n_items_main = p.data->n_main;
     return {};
   }
   return ray_plan_get(ctx, ctx, a, centers, n_centers, p);
@@ -1155,18 +1090,11 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
   PACT_TRY_S(after_launch(ctx, "ray_bound_kernel"));
   if (a.tex) {
     if (!a.rec) return internal_error("launch_ray_backward: ray plan missing");
-    if (a.n_items_main > 0) {
+    if (a.n_items > 0) {
       PACT_TRY_S(smem_optin(ray_backward_plan_kernel, smem));
-      ray_backward_plan_kernel<<<div_up(a.n_items_main, kPlanBlock), kPlanBlock, smem,
-                                 ctx->stream>>>(a, dw, acc, rep, stats);
+      ray_backward_plan_kernel<<<div_up(a.n_items, kPlanBlock), kPlanBlock, smem, ctx->stream>>>(
+          a, dw, acc, rep, stats);
       PACT_TRY_S(after_launch(ctx, "ray_backward_plan_kernel"));
-    }
-    if (a.n_items > a.n_items_main) {
-      const size_t smem_side = 3 * smem;  // border values | slot lo | slot hi
-      PACT_TRY_S(smem_optin(ray_backward_side_kernel, smem_side));
-      ray_backward_side_kernel<<<div_up(a.n_items - a.n_items_main, kPlanBlock), kPlanBlock,
-                                 smem_side, ctx->stream>>>(a, dw, rep, stats);
-      PACT_TRY_S(after_launch(ctx, "ray_backward_side_kernel"));
     }
   } else {
     PACT_TRY_S(smem_optin(ray_backward_kernel<false>, smem));
