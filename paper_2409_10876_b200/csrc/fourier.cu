@@ -598,118 +598,98 @@ __global__ void __launch_bounds__(2 * LB) loss_bins_kernel(FourierTab t, const f
 // their spectra into the compact exchange layout ynyq [patch][slot][K] so
 // that kernel A' reads them contiguously instead of one sector per bin.
 template <int NS, int JPL>
-__global__ void __launch_bounds__(256, 2) loss_reg_kernel(FourierTab t, const float2* __restrict__ Y_all,
+__global__ void __launch_bounds__(256, 4) loss_reg_kernel(FourierTab t, const float2* __restrict__ Y_all,
                                                        const float* __restrict__ w_all, float eps_m,
                                                        float scale, int implicit,
                                                        float2* __restrict__ gbuf,
                                                        float2* __restrict__ ynyq,
-                                                       double* __restrict__ loss_part, int n_parts,
-                                                       int n_patches) {
+                                                       double* __restrict__ loss_part, int n_parts) {
   constexpr int BPW = 32 / NS, BPB = 8 * BPW, K = NS * JPL;
   __shared__ double s_red[8];
   const int P2 = t.P2, lane = threadIdx.x & 31;
   const int grp = lane / BPW, bi = lane - grp * BPW;
-  const int chunks = (P2 + BPB - 1) / BPB, total = n_patches * chunks;
+  const int chunks = (P2 + BPB - 1) / BPB;
+  const int patch = blockIdx.x / chunks, cb = blockIdx.x - patch * chunks;
+  const int b0 = cb * BPB + (threadIdx.x >> 5) * BPW + bi;
+  const bool valid = b0 < P2;
+  const int b = valid ? b0 : P2 - 1;
   const int j0 = grp * JPL;
-  auto bin_of = [&](int c, int& patch, int& cb) {
-    patch = c / chunks;
-    cb = c - patch * chunks;
-    return cb * BPB + (threadIdx.x >> 5) * BPW + bi;
-  };
-  // persistent over (patch, chunk) work items with stride gridDim.x: the next
-  // item's spectra are in flight (registers) while this one is computed
-  auto load = [&](int c, float2 (&y)[JPL]) {
-    int patch, cb;
-    const int b = min(bin_of(c, patch, cb), P2 - 1);
-    const float2* Y = Y_all + (static_cast<size_t>(patch) * K + j0) * P2 + b;
+  const float2* Y = Y_all + (static_cast<size_t>(patch) * K + j0) * P2 + b;
+  float2 y[JPL];
 #pragma unroll
-    for (int u = 0; u < JPL; ++u) y[u] = __ldcs(Y + static_cast<size_t>(u) * P2);
-  };
+  for (int u = 0; u < JPL; ++u) y[u] = __ldcs(Y + static_cast<size_t>(u) * P2);
   auto gsum = [&](float v) {
 #pragma unroll
     for (int o = BPW; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
   };
-  float2 y[JPL];
-  if (static_cast<int>(blockIdx.x) < total) load(blockIdx.x, y);
-  for (int c = blockIdx.x; c < total; c += gridDim.x) {
-    float2 yn[JPL];
-    if (c + static_cast<int>(gridDim.x) < total) load(c + gridDim.x, yn);
-    int patch, cb;
-    const int b0 = bin_of(c, patch, cb);
-    const bool valid = b0 < P2;
-    const int b = valid ? b0 : P2 - 1;
-    const int m = t.mirror[b];
-    if (m >= 0 && valid) {  // Nyquist bin: hand its spectra to kernel A'
-      float2* dst = ynyq + (static_cast<size_t>(patch) * (2 * t.P - 1) + nyq_slot(b, t.P)) * K + j0;
+  const int m = t.mirror[b];
+  if (m >= 0 && valid) {  // Nyquist bin: hand its spectra to kernel A'
+    float2* dst = ynyq + (static_cast<size_t>(patch) * (2 * t.P - 1) + nyq_slot(b, t.P)) * K + j0;
 #pragma unroll
-      for (int u = 0; u < JPL; ++u) dst[u] = y[u];
-    }
-    const float k = t.kmag[b];
-    const float wk = k * scale;
-    const float* w = w_all + static_cast<size_t>(patch) * t.A;
-    const int4 ix = t.idx[b];
-    const float2 fr = t.frac[b];
-    const float w1 = (1.f - fr.x) * __ldg(w + ix.x) + fr.x * __ldg(w + ix.y);
-    const float w2 = (1.f - fr.y) * __ldg(w + ix.z) + fr.y * __ldg(w + ix.w);
-    float sn, cs;
-    sincosf(k * (0.5f * (w1 + w2)), &sn, &cs);
-    const float2 ew = make_float2(cs, -sn);  // exp(-i|k| wbar)
-    // z_j = conj(dp_j) exp(-i|k| wbar) = exp(i|k|(d_j - wbar)): c_j = Re z_j, s_j = Im z_j
-    const bool walk = t.rho != nullptr;
-    const float2 rr = walk ? conjf2(t.rho[b]) : make_float2(1.f, 0.f);
-    // the phases are walked twice (pass 1, pass 2) rather than kept: registers
-    // hold the spectra only
-    const float2 z0 = cmul(conjf2(t.dp[j0 * P2 + b]), ew);
-    auto znext = [&](int u, float2 z) {
-      return walk ? cmul(z, rr) : cmul(conjf2(t.dp[(j0 + u + 1) * P2 + b]), ew);
-    };
-    float Sx = 0.f, Sy = 0.f, den = 0.f;
-    {
-      float2 z = z0;
-#pragma unroll
-      for (int u = 0; u < JPL; ++u) {
-        Sx = fmaf(z.x, y[u].x, Sx);
-        Sy = fmaf(z.x, y[u].y, Sy);
-        den = fmaf(z.x, z.x, den);
-        if (u + 1 < JPL) z = znext(u, z);
-      }
-    }
-    Sx = gsum(Sx);
-    Sy = gsum(Sy);
-    den = eps_m + gsum(den);
-    const float inv = den > 0.f ? 1.f / den : 0.f;
-    const float2 X = make_float2(Sx * inv, Sy * inv);
-    const float al = implicit && den > 0.f ? eps_m * inv : 0.f;
-    const float be = 2.f * al * (X.x * X.x + X.y * X.y);
-    const float al1 = 1.f + al, xb = X.x * X.x + X.y * X.y + be;
-    float acc = 0.f, gs = 0.f;
-    {
-      float2 z = z0;
-#pragma unroll
-      for (int u = 0; u < JPL; ++u) {
-        const float rx = fmaf(-z.x, X.x, y[u].x), ry = fmaf(-z.x, X.y, y[u].y);
-        acc = fmaf(rx, rx, fmaf(ry, ry, acc));
-        // dc = Re(conj(r) X) + al Re(conj(X) y) - be c = (1 + al) (X . y) - (|X|^2 + be) c
-        const float q = fmaf(X.x, y[u].x, X.y * y[u].y);
-        const float dc = fmaf(al1, q, -xb * z.x);
-        gs = fmaf(dc, z.y, gs);
-        if (u + 1 < JPL) z = znext(u, z);
-      }
-    }
-    acc = gsum(acc);
-    gs = gsum(gs);
-    const bool ordinary = valid && m < 0 && wk != 0.f;
-    if (grp == 0 && valid && m < 0) {
-      const float G = ordinary ? -wk * k * gs : 0.f;  // (1/2) dL/dwbar, for w1 and for w2
-      put_g(t, gbuf + static_cast<size_t>(patch) * 2 * P2, b, G, G);
-    }
-    const double value = ordinary && grp == 0 ? static_cast<double>(wk) * acc : 0.0;
-    block_sum_store(value, s_red, loss_part + patch * n_parts + cb);
-    __syncthreads();  // s_red is reusable
-#pragma unroll
-    for (int u = 0; u < JPL; ++u) y[u] = yn[u];
+    for (int u = 0; u < JPL; ++u) dst[u] = y[u];
   }
+  const float k = t.kmag[b];
+  const float wk = k * scale;
+  const float* w = w_all + static_cast<size_t>(patch) * t.A;
+  const int4 ix = t.idx[b];
+  const float2 fr = t.frac[b];
+  const float w1 = (1.f - fr.x) * __ldg(w + ix.x) + fr.x * __ldg(w + ix.y);
+  const float w2 = (1.f - fr.y) * __ldg(w + ix.z) + fr.y * __ldg(w + ix.w);
+  float sn, cs;
+  sincosf(k * (0.5f * (w1 + w2)), &sn, &cs);
+  const float2 ew = make_float2(cs, -sn);  // exp(-i|k| wbar)
+  // z_j = conj(dp_j) exp(-i|k| wbar) = exp(i|k|(d_j - wbar)): c_j = Re z_j, s_j = Im z_j
+  const bool walk = t.rho != nullptr;
+  const float2 rr = walk ? conjf2(t.rho[b]) : make_float2(1.f, 0.f);
+  // the phases are walked twice (pass 1, pass 2) rather than kept: registers
+  // hold the spectra only
+  const float2 z0 = cmul(conjf2(t.dp[j0 * P2 + b]), ew);
+  auto znext = [&](int u, float2 z) {
+    return walk ? cmul(z, rr) : cmul(conjf2(t.dp[(j0 + u + 1) * P2 + b]), ew);
+  };
+  float Sx = 0.f, Sy = 0.f, den = 0.f;
+  {
+    float2 z = z0;
+#pragma unroll
+    for (int u = 0; u < JPL; ++u) {
+      Sx = fmaf(z.x, y[u].x, Sx);
+      Sy = fmaf(z.x, y[u].y, Sy);
+      den = fmaf(z.x, z.x, den);
+      if (u + 1 < JPL) z = znext(u, z);
+    }
+  }
+  Sx = gsum(Sx);
+  Sy = gsum(Sy);
+  den = eps_m + gsum(den);
+  const float inv = den > 0.f ? 1.f / den : 0.f;
+  const float2 X = make_float2(Sx * inv, Sy * inv);
+  const float al = implicit && den > 0.f ? eps_m * inv : 0.f;
+  const float be = 2.f * al * (X.x * X.x + X.y * X.y);
+  const float al1 = 1.f + al, xb = X.x * X.x + X.y * X.y + be;
+  float acc = 0.f, gs = 0.f;
+  {
+    float2 z = z0;
+#pragma unroll
+    for (int u = 0; u < JPL; ++u) {
+      const float rx = fmaf(-z.x, X.x, y[u].x), ry = fmaf(-z.x, X.y, y[u].y);
+      acc = fmaf(rx, rx, fmaf(ry, ry, acc));
+      // dc = Re(conj(r) X) + al Re(conj(X) y) - be c = (1 + al) (X . y) - (|X|^2 + be) c
+      const float q = fmaf(X.x, y[u].x, X.y * y[u].y);
+      const float dc = fmaf(al1, q, -xb * z.x);
+      gs = fmaf(dc, z.y, gs);
+      if (u + 1 < JPL) z = znext(u, z);
+    }
+  }
+  acc = gsum(acc);
+  gs = gsum(gs);
+  const bool ordinary = valid && m < 0 && wk != 0.f;
+  if (grp == 0 && valid && m < 0) {
+    const float G = ordinary ? -wk * k * gs : 0.f;  // (1/2) dL/dwbar, for w1 and for w2
+    put_g(t, gbuf + static_cast<size_t>(patch) * 2 * P2, b, G, G);
+  }
+  const double value = ordinary && grp == 0 ? static_cast<double>(wk) * acc : 0.0;
+  block_sum_store(value, s_red, loss_part + patch * n_parts + cb);
 }
 
 // Small patches (P^2 < LB or not a multiple of LB): one CTA per (patch, chunk).
@@ -977,7 +957,7 @@ Status launch_transfer_stack(pact_ctx* ctx, const FourierTab& t, const float* w,
 
 // Kernel A of the register form for (NS, JPL) with K = NS * JPL, or null.
 using LossRegFn = void (*)(FourierTab, const float2*, const float*, float, float, int, float2*,
-                           float2*, double*, int, int);
+                           float2*, double*, int);
 LossRegFn loss_reg_for(int K, int& ns) {
   // PACT_LOSS_STAGED=1 selects the shared-memory staged kernel A (comparisons)
   static const bool staged = [] {
@@ -1020,9 +1000,8 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
   double* part = reinterpret_cast<double*>(gbuf + n_g);
   const float eps_m = static_cast<float>(eps * t.K), sc = static_cast<float>(scale);
   if (reg) {
-    const int grid = std::min(n_patches * chunks, 2 * ctx->num_sms);
-    reg<<<grid, 256, 0, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, gbuf, ynyq, part, n_parts,
-                                       n_patches);
+    reg<<<n_patches * chunks, 256, 0, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, gbuf, ynyq,
+                                                     part, n_parts);
   } else if (t.P2 % LB == 0 && t.K * LB * 8 <= 96 * 1024) {
     const size_t stage = sizeof(float) * (2 * t.K * LB + ((t.A + 3) & ~3));
     const size_t smem_bins = 2 * stage;
