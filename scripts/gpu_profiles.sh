@@ -1,12 +1,23 @@
-# Round profiles: bench launch list + full captures of the hot kernels.
-set -x
+#!/bin/bash
+# Round profiles (profiles/r02_*): GPU tests, the bench line, the bench launch
+# list, full captures of the cfg3 hot kernels, the DAS, and cfg5.  Every ncu
+# command runs after the same command exited 0 without ncu.
+cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/bench_plain.json 2> gpurun_out/bench_plain.err; echo bench_plain=$?
-ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv --log-file gpurun_out/bench_launches.csv \
-    python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/bench_ncu.log 2>&1; echo launches=$?
-python scripts/profile_iter.py --steps 1 > gpurun_out/iter_plain.log 2>&1; echo iter_plain=$?
+timeout 1500 python -m pytest tests -m gpu -q -rA > gpurun_out/p_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/p_pytest.log
+timeout 900 python bench.py > gpurun_out/p_bench.json 2> gpurun_out/p_bench.err; echo "bench rc=$?" >> gpurun_out/p_bench.err
+python bench.py --steps 2 --warmup 3 --no-cpu --no-cfg5 > gpurun_out/p_bench_plain.json 2>&1; echo plain=$?
+ncu --metrics gpu__time_duration.sum --clock-control none -c 8000 --csv --log-file gpurun_out/p_launches.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu --no-cfg5 > gpurun_out/p_launches.log 2>&1; echo launches=$?
+python scripts/profile_iter.py --steps 1 > gpurun_out/p_iter.log 2>&1; echo iter=$?
 ncu --set full --clock-control none --import-source on \
-    -k regex:"ray_backward_plan|wavefront_plan|siren_chain_fwd|tc_bwd|loss_bins|loss_nyquist" -s 0 -c 8 \
-    -o gpurun_out/iter_full python scripts/profile_iter.py --steps 1 > gpurun_out/iter_full.log 2>&1; echo full=$?
+    -k regex:"ray_backward_plan|wavefront_plan|siren_chain_fwd|tc_bwd|loss_reg|loss_nyquist|loss_finish|patch_fft64|fix_to_grad|ray_bound|reduce_segments" -s 0 -c 14 \
+    -o gpurun_out/p_iter_full python scripts/profile_iter.py --steps 1 > gpurun_out/p_iter_full.log 2>&1; echo full=$?
 ncu --set full --clock-control none --import-source on -k regex:das_stack -c 1 \
-    -o gpurun_out/das_full python scripts/profile_iter.py --steps 1 > gpurun_out/das_full.log 2>&1; echo das=$?
+    -o gpurun_out/p_das_full python scripts/profile_iter.py --steps 1 > gpurun_out/p_das_full.log 2>&1; echo das=$?
+timeout 900 python scripts/profile_iter.py --steps 1 --cfg cfg5 > gpurun_out/p_iter_cfg5.log 2>&1; echo cfg5=$?
+ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/p_cfg5_launches.csv \
+    python scripts/profile_iter.py --steps 1 --cfg cfg5 > gpurun_out/p_cfg5_launches.log 2>&1; echo cfg5_launches=$?
+ncu --set full --clock-control none --import-source on \
+    -k regex:"das_stack|tc_wide|siren_top|siren_first|wavefront_plan|ray_backward_plan|loss_reg|loss_nyquist|patch_fft" -c 12 \
+    -o gpurun_out/p_cfg5_full python scripts/profile_iter.py --steps 1 --cfg cfg5 > gpurun_out/p_cfg5_full.log 2>&1; echo cfg5_full=$?
