@@ -594,6 +594,26 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def dry_run(args):
+    """The N-rank launch path without GPU work: every rank joins a gloo group,
+    the ranks agree on the world size, and rank 0 prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.tensor([rank], dtype=torch.int64)
+        dist.all_reduce(t)
+        assert int(t.item()) == world * (world - 1) // 2
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "requested": args.gpus,
+                          "impl": args.impl}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def free_port() -> int:
     import socket
 
@@ -619,13 +639,17 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cfg5", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check only: join the ranks over gloo and print one line")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args.gpus))
     _, world, _ = dist_env()
     if world != args.gpus:
         sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
-    if args.impl == "reference":
+    if args.dry_run:
+        dry_run(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)
