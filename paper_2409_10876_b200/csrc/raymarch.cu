@@ -82,12 +82,14 @@ __device__ __forceinline__ Border load_border(const RayArgs& a, float* sm) {
 }
 
 // Fixed-point deposit target: int64 multiples of 2^-S (see the header).
+// v * 2^S is exact in fp32 (a power-of-two scale; |v| 2^S < 2^62 by the
+// bound), so one FMUL + F2I.S64 gives the same integer as an fp64 product.
 struct Fix {
   unsigned long long* p;
-  double scale;  // 2^S
+  float scale;  // 2^S
   __device__ __forceinline__ Fix operator+(long long off) const { return {p + off, scale}; }
   __device__ __forceinline__ void add(float v) const {
-    atomicAdd(p, static_cast<unsigned long long>(__double2ll_rn(static_cast<double>(v) * scale)));
+    atomicAdd(p, static_cast<unsigned long long>(__float2ll_rn(v * scale)));
   }
 };
 
@@ -102,7 +104,7 @@ __device__ __forceinline__ int fix_exponent(const unsigned long long* stats, dou
   if (!(B > 0.0) || !isfinite(B)) return 0;
   int e;
   frexp(B, &e);  // B < 2^e
-  return 62 - e;
+  return min(max(62 - e, -126), 127);  // 2^S is a normal fp32 number
 }
 
 // The most deposits any pixel can receive in one launch: every ray's steps
@@ -367,6 +369,8 @@ __device__ __forceinline__ Regimes regimes(const RayPix& rp, int n, float Wm1, f
 struct SideLine {
   float fs, df;
   int off, qmax;
+  bool col;  // the line is a column (x clamped) / a row (y clamped)
+  float t;   // the clamped texture coordinate: 0 (first line) or W / H (last line)
 };
 
 __device__ __forceinline__ SideLine side_line(const Regimes& rg, const RayPix& rp, int W, int H) {
@@ -376,13 +380,29 @@ __device__ __forceinline__ SideLine side_line(const Regimes& rg, const RayPix& r
     s.df = rp.dfy;
     s.off = rp.dfx > 0.f ? H : 0;
     s.qmax = H - 2;
+    s.col = true;
+    s.t = rp.dfx > 0.f ? static_cast<float>(W) : 0.f;
   } else {
     s.fs = rp.fxs;
     s.df = rp.dfx;
     s.off = 2 * H + (rp.dfy > 0.f ? W : 0);
     s.qmax = W - 2;
+    s.col = false;
+    s.t = rp.dfy > 0.f ? static_cast<float>(H) : 0.f;
   }
   return s;
+}
+
+// The two border-line values at line positions q, q + 1 by ONE texture
+// gather at the clamped coordinate: the 2x2 footprint collapses onto the
+// line (x = 0 or W clamps both columns to the border one), so the lanes'
+// scattered line positions cost no shared-memory bank conflicts.  Same
+// values as the border cache, so the same arithmetic follows.
+__device__ __forceinline__ float2 line_pair(cudaTextureObject_t tex, const SideLine& s, int q) {
+  const float qc = static_cast<float>(q) + 1.f;
+  const float4 g = tex2Dgather<float4>(tex, s.col ? s.t : qc, s.col ? qc : s.t, 0);
+  // gather order: w=(x0,y0) z=(x1,y0) x=(x0,y1) y=(x1,y1)
+  return make_float2(g.w, s.col ? g.x : g.z);
 }
 
 __device__ __forceinline__ float interior_d(cudaTextureObject_t tex, float fx, float fy, int W,
@@ -529,8 +549,8 @@ __global__ void __launch_bounds__(256) wavefront_plan_kernel(RayArgs a) {
       for (int i = lo; i < hi; ++i) {
         const float f = fmaf(static_cast<float>(i), sl.df, sl.fs);
         const int q = min(static_cast<int>(f), sl.qmax);
-        const float c0 = s_border[sl.off + q];
-        const float d = fmaf(f - q, s_border[sl.off + q + 1] - c0, c0);
+        const float2 c = line_pair(a.tex, sl, q);
+        const float d = fmaf(f - q, c.y - c.x, c.x);
         acc += __fdividef(d, v0 + d);
       }
     } else {
@@ -564,7 +584,7 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
   const Border bd = load_border(a, s_border);
   const int W = a.W, H = a.H;
   const float v0 = static_cast<float>(a.v0);
-  const double scale = ldexp(1.0, fix_exponent(stats, a.step, a.v0, max_steps_total(a)));
+  const float scale = ldexpf(1.f, fix_exponent(stats, a.step, a.v0, max_steps_total(a)));
   const Fix grad{acc, scale};
   const Fix rep{border_rep + static_cast<size_t>(blockIdx.x % kBorderReplicas) * 2 * (W + H), scale};
   {
@@ -622,8 +642,9 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
       for (int i = lo; i < hi; ++i) {
         const float f = fmaf(static_cast<float>(i), sl.df, sl.fs);
         const int q = min(static_cast<int>(f), sl.qmax);
-        const float fa = f - q, c0 = s_border[sl.off + q];
-        const float v = v0 + fmaf(fa, s_border[sl.off + q + 1] - c0, c0);
+        const float2 c = line_pair(a.tex, sl, q);
+        const float fa = f - q;
+        const float v = v0 + fmaf(fa, c.y - c.x, c.x);
         const float gv = __fdividef(gscale, v * v);
         line.move(dst, q, 1, 0);
         const float g1 = gv * fa;
@@ -755,7 +776,7 @@ __global__ void __launch_bounds__(256) ray_backward_kernel(RayArgs a, const floa
                                                            const unsigned long long* __restrict__ stats) {
   extern __shared__ float s_border[];
   const Border bd = load_border(a, s_border);
-  const Fix grad{acc, ldexp(1.0, fix_exponent(stats, a.step, a.v0, max_steps_total(a)))};
+  const Fix grad{acc, ldexpf(1.f, fix_exponent(stats, a.step, a.v0, max_steps_total(a)))};
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= a.n_rays) return;
   const float gr = dw[r];

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Summarise ncu captures for profiles/.
 
-    python scripts/ncu_summary.py full <report.ncu-rep>      # --set full capture
+    python scripts/ncu_summary.py full <report.ncu-rep | raw.csv[.gz]>  # --set full capture
     python scripts/ncu_summary.py launches <launches.csv>     # gpu__time_duration list
 """
 import csv
@@ -35,8 +35,15 @@ KEYS = [
 
 
 def full(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if path.endswith(".csv.gz") or path.endswith(".csv"):  # exported on the box (--page raw --csv)
+        import gzip
+
+        op = gzip.open if path.endswith(".gz") else open
+        with op(path, "rt") as f:
+            raw = f.read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     for r in rows[2:]:
@@ -51,7 +58,9 @@ def full(path):
 
 
 def launches(path):
-    text = open(path).read()
+    import gzip
+
+    text = (gzip.open(path, "rt") if path.endswith(".gz") else open(path)).read()
     start = text.find('"ID"')
     rows = list(csv.DictReader(io.StringIO(text[start:])))
     tot = defaultdict(float)
