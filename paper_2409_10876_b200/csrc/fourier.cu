@@ -614,6 +614,14 @@ __global__ void __launch_bounds__(256, 4) loss_reg_kernel(FourierTab t, const fl
   const bool valid = b0 < P2;
   const int b = valid ? b0 : P2 - 1;
   const int j0 = grp * JPL;
+  // the bin's table entries and wavefront samples first (a dependent
+  // idx -> w chain of L2 hits), so they are back before the spectra from HBM
+  const int m = t.mirror[b];
+  const float k = t.kmag[b];
+  const int4 ix = t.idx[b];
+  const float2 fr = t.frac[b];
+  const float* w = w_all + static_cast<size_t>(patch) * t.A;
+  const float wa = __ldg(w + ix.x), wb = __ldg(w + ix.y), wc = __ldg(w + ix.z), wd = __ldg(w + ix.w);
   const float2* Y = Y_all + (static_cast<size_t>(patch) * K + j0) * P2 + b;
   float2 y[JPL];
 #pragma unroll
@@ -623,19 +631,14 @@ __global__ void __launch_bounds__(256, 4) loss_reg_kernel(FourierTab t, const fl
     for (int o = BPW; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
   };
-  const int m = t.mirror[b];
   if (m >= 0 && valid) {  // Nyquist bin: hand its spectra to kernel A'
     float2* dst = ynyq + (static_cast<size_t>(patch) * (2 * t.P - 1) + nyq_slot(b, t.P)) * K + j0;
 #pragma unroll
     for (int u = 0; u < JPL; ++u) dst[u] = y[u];
   }
-  const float k = t.kmag[b];
   const float wk = k * scale;
-  const float* w = w_all + static_cast<size_t>(patch) * t.A;
-  const int4 ix = t.idx[b];
-  const float2 fr = t.frac[b];
-  const float w1 = (1.f - fr.x) * __ldg(w + ix.x) + fr.x * __ldg(w + ix.y);
-  const float w2 = (1.f - fr.y) * __ldg(w + ix.z) + fr.y * __ldg(w + ix.w);
+  const float w1 = (1.f - fr.x) * wa + fr.x * wb;
+  const float w2 = (1.f - fr.y) * wc + fr.y * wd;
   float sn, cs;
   sincosf(k * (0.5f * (w1 + w2)), &sn, &cs);
   const float2 ew = make_float2(cs, -sn);  // exp(-i|k| wbar)

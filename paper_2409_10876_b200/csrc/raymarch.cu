@@ -369,8 +369,6 @@ __device__ __forceinline__ Regimes regimes(const RayPix& rp, int n, float Wm1, f
 struct SideLine {
   float fs, df;
   int off, qmax;
-  bool col;  // the line is a column (x clamped) / a row (y clamped)
-  float t;   // the clamped texture coordinate: 0 (first line) or W / H (last line)
 };
 
 __device__ __forceinline__ SideLine side_line(const Regimes& rg, const RayPix& rp, int W, int H) {
@@ -380,30 +378,15 @@ __device__ __forceinline__ SideLine side_line(const Regimes& rg, const RayPix& r
     s.df = rp.dfy;
     s.off = rp.dfx > 0.f ? H : 0;
     s.qmax = H - 2;
-    s.col = true;
-    s.t = rp.dfx > 0.f ? static_cast<float>(W) : 0.f;
   } else {
     s.fs = rp.fxs;
     s.df = rp.dfx;
     s.off = 2 * H + (rp.dfy > 0.f ? W : 0);
     s.qmax = W - 2;
-    s.col = false;
-    s.t = rp.dfy > 0.f ? static_cast<float>(H) : 0.f;
   }
   return s;
 }
 
-// The two border-line values at line positions q, q + 1 by ONE texture
-// gather at the clamped coordinate: the 2x2 footprint collapses onto the
-// line (x = 0 or W clamps both columns to the border one), so the lanes'
-// scattered line positions cost no shared-memory bank conflicts.  Same
-// values as the border cache, so the same arithmetic follows.
-__device__ __forceinline__ float2 line_pair(cudaTextureObject_t tex, const SideLine& s, int q) {
-  const float qc = static_cast<float>(q) + 1.f;
-  const float4 g = tex2Dgather<float4>(tex, s.col ? s.t : qc, s.col ? qc : s.t, 0);
-  // gather order: w=(x0,y0) z=(x1,y0) x=(x0,y1) y=(x1,y1)
-  return make_float2(g.w, s.col ? g.x : g.z);
-}
 
 __device__ __forceinline__ float interior_d(cudaTextureObject_t tex, float fx, float fy, int W,
                                             int H, float& ax, float& ay, int& ix, int& iy) {
@@ -549,8 +532,8 @@ __global__ void __launch_bounds__(256) wavefront_plan_kernel(RayArgs a) {
       for (int i = lo; i < hi; ++i) {
         const float f = fmaf(static_cast<float>(i), sl.df, sl.fs);
         const int q = min(static_cast<int>(f), sl.qmax);
-        const float2 c = line_pair(a.tex, sl, q);
-        const float d = fmaf(f - q, c.y - c.x, c.x);
+        const float c0 = s_border[sl.off + q];
+        const float d = fmaf(f - q, s_border[sl.off + q + 1] - c0, c0);
         acc += __fdividef(d, v0 + d);
       }
     } else {
@@ -642,9 +625,8 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
       for (int i = lo; i < hi; ++i) {
         const float f = fmaf(static_cast<float>(i), sl.df, sl.fs);
         const int q = min(static_cast<int>(f), sl.qmax);
-        const float2 c = line_pair(a.tex, sl, q);
-        const float fa = f - q;
-        const float v = v0 + fmaf(fa, c.y - c.x, c.x);
+        const float fa = f - q, c0 = s_border[sl.off + q];
+        const float v = v0 + fmaf(fa, s_border[sl.off + q + 1] - c0, c0);
         const float gv = __fdividef(gscale, v * v);
         line.move(dst, q, 1, 0);
         const float g1 = gv * fa;
