@@ -103,17 +103,32 @@ class Clocks:
 
 
 STAGE_KERNEL = {"ray_backward": "ray_backward_plan_kernel", "wavefront": "wavefront_plan_kernel",
-                "fused_loss": "loss_bins_kernel"}
+                "fused_loss": "loss_reg_kernel<2, 16>"}
 
 
 def load_traffic():
     """Per-launch DRAM bytes of the hot kernels from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "traffic_r01b.json")
+    path = os.path.join(ROOT, "profiles", "traffic_r02.json")
     try:
         with open(path) as f:
             return json.load(f)
     except OSError:
         return {}
+
+
+def das_physical(traffic):
+    """Issue / LSU / shared-memory utilisation of das_stack_kernel<32> at cfg3
+    from the committed ncu capture (profiles/traffic_r02.json)."""
+    d = traffic.get("_das_cfg3")
+    if not d:
+        return None
+    wf = d["l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum"]
+    return {"issue_active_pct": d["smsp__issue_active.avg.pct_of_peak_sustained_active"],
+            "lsu_pipe_pct": d["sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"],
+            "fma_pipe_pct": d["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"],
+            "smem_ld_wavefronts": wf,
+            "smem_bank_conflict_frac": d["l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum"] / wf,
+            "source": "ncu --set full, das_stack_kernel<32> at cfg3 (profiles/r02_das_ncu_raw.csv.gz)"}
 
 
 def dist_env():
@@ -583,7 +598,10 @@ def run_ours(args):
             "das": {"ms": das_t, "gsamples_per_s": w.das_samples / (das_t * 1e-3) / 1e9,
                     "roofline": {"bound": "hbm", "achieved": das_ach, "peak": hbm, "unit": "GB/s",
                                  "frac": das_ach / hbm, "peak_source": peak_src,
-                                 "byte_model": "8*S + 4*K*W*H + 4*N*T, S = W*H*K*N"}},
+                                 "byte_model": "8*S + 4*K*W*H + 4*N*T, S = W*H*K*N"},
+                    # the physically binding limits: taps are served from
+                    # shared memory, so issue slots and the LSU pipe bound the kernel
+                    "physical": das_physical(traffic)},
             "loss_report_frame0": reports[0],
             "cfg5": cfg5,
             "cpu_baseline": cpu,
