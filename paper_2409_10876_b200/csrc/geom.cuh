@@ -139,12 +139,6 @@ struct RayArgs {
   const int2* ray_slots;
   float* partial;
   int n_items;
-  // The adjoint's interior steps re-cut by image tile (ray_plan_get): segment
-  // (ray, lo, hi, tile) lists grouped into blocks of one tile each, so a block
-  // accumulates its deposits in shared memory and flushes the tile once.
-  const int4* tseg;    // [n_tseg]
-  const int2* tblock;  // [n_tblocks]: (first segment, segment count)
-  int n_tblocks;       // 0: the interior adjoint runs in the item kernel
 };
 
 // Creates a point-sampled, clamped pitch-2D texture over a row-major fp32

@@ -580,9 +580,7 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
     // f = g * dl * v0 / v^2 per step (aberration.hpp:354-355)
     const float gscale = static_cast<float>(static_cast<double>(gr) * rr.dl * a.v0);
     const int lo = item.y, hi = item.z, kind = item_kind(item.w);
-    if (kind == kItemInterior && a.n_tblocks > 0) {
-      // interior steps: ray_backward_tile_kernel (only the corner run, below)
-    } else if (kind == kItemInterior) {
+    if (kind == kItemInterior) {
       // gathers issued RAY_BWD_BATCH steps at a time, then the carries
       CellAcc cell;
       constexpr int NB = RAY_BWD_BATCH;
@@ -645,146 +643,6 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
       const float v = v0 + col[py];
       const float f = __fdividef(gscale, v * v) * static_cast<float>(rr.n - rr.i_corner);
       if (f != 0.f) (rep + ((px == 0 ? 0 : H) + py)).add(f);
-    }
-  }
-}
-
-// ---- tiled interior adjoint ------------------------------------------------
-// Tile of kRayTile x kRayTile stencil cells; its deposits touch the
-// (kRayTile + 1)^2 pixels [x0, x0 + kRayTile] x [y0, y0 + kRayTile].
-constexpr int kRayTile = 32, kTileW = kRayTile + 1, kTileSlots = kTileW * kTileW;
-
-// Shared fixed-point slots of a tile window: 64-bit value = hi * 2^32 + lo
-// (lo unsigned), the carry out of the low word propagated to hi — exact
-// integer sums with the native 32-bit shared atomics.
-struct TileTgt {
-  unsigned* lo;
-  int* hi;
-  float scale;
-  int x0, y0;
-  __device__ __forceinline__ void add(int x, int y, float v) const {
-    const int s = (y - y0) * kTileW + (x - x0);
-    const long long q = __float2ll_rn(v * scale);
-    const unsigned ql = static_cast<unsigned>(q);
-    const int qh = static_cast<int>(q >> 32);
-    const unsigned old = atomicAdd(lo + s, ql);
-    const int c = old + ql < old ? 1 : 0;  // carry out of the low word
-    if (qh + c) atomicAdd(hi + s, qh + c);
-  }
-};
-
-// CellAcc's carry with deposits addressed by pixel (x, y) into a target T.
-template <class T>
-struct CellAccT {
-  int cx = -1, cy = -1;
-  float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
-
-  __device__ __forceinline__ void move(const T& t, int ix, int iy) {
-    if (ix == cx && iy == cy) return;
-    const int dx = ix - cx, dy = iy - cy;
-    if (cx >= 0 && (dx < -1 || dx > 1 || dy < -1 || dy > 1)) {  // a jump: flush everything
-      flush(t);
-    } else if (cx >= 0) {
-      const bool keep_x0 = dx <= 0, keep_x1 = dx >= 0, keep_y0 = dy <= 0, keep_y1 = dy >= 0;
-      if (!(keep_x0 && keep_y0) && a00 != 0.f) t.add(cx, cy, a00);
-      if (!(keep_x1 && keep_y0) && a01 != 0.f) t.add(cx + 1, cy, a01);
-      if (!(keep_x0 && keep_y1) && a10 != 0.f) t.add(cx, cy + 1, a10);
-      if (!(keep_x1 && keep_y1) && a11 != 0.f) t.add(cx + 1, cy + 1, a11);
-      const float r00 = dx == 0 ? a00 : (dx == 1 ? a01 : 0.f);
-      const float r01 = dx == 0 ? a01 : (dx == -1 ? a00 : 0.f);
-      const float r10 = dx == 0 ? a10 : (dx == 1 ? a11 : 0.f);
-      const float r11 = dx == 0 ? a11 : (dx == -1 ? a10 : 0.f);
-      a00 = dy == 0 ? r00 : (dy == 1 ? r10 : 0.f);
-      a01 = dy == 0 ? r01 : (dy == 1 ? r11 : 0.f);
-      a10 = dy == 0 ? r10 : (dy == -1 ? r00 : 0.f);
-      a11 = dy == 0 ? r11 : (dy == -1 ? r01 : 0.f);
-    }
-    cx = ix;
-    cy = iy;
-  }
-  __device__ __forceinline__ void flush(const T& t) {
-    if (cx < 0) return;
-    if (a00 != 0.f) t.add(cx, cy, a00);
-    if (a01 != 0.f) t.add(cx + 1, cy, a01);
-    if (a10 != 0.f) t.add(cx, cy + 1, a10);
-    if (a11 != 0.f) t.add(cx + 1, cy + 1, a11);
-    cx = cy = -1;
-    a00 = a01 = a10 = a11 = 0.f;
-  }
-};
-
-// One block per (tile, up to 256 segments): every step of every segment has
-// its stencil cell inside the tile (the plan computed the cells with the same
-// fp32 formula), so all deposits land in the block's shared window; the
-// window is added to the raster accumulator once at the end (one integer RED
-// per touched pixel per block instead of about one per step).  The tile's
-// raster neighbourhood is also what the block's texture gathers read.
-__global__ void __launch_bounds__(256) ray_backward_tile_kernel(RayArgs a, const float* __restrict__ dw,
-                                                                unsigned long long* __restrict__ acc,
-                                                                const unsigned long long* __restrict__ stats) {
-  __shared__ unsigned s_lo[kTileSlots];
-  __shared__ int s_hi[kTileSlots];
-  const int W = a.W, H = a.H;
-  const int2 blk = a.tblock[blockIdx.x];
-  const int tile = a.tseg[blk.x].w;
-  const int ntx = (W - 1 + kRayTile - 1) / kRayTile;
-  const int x0 = (tile % ntx) * kRayTile, y0 = (tile / ntx) * kRayTile;
-  for (int i = threadIdx.x; i < kTileSlots; i += blockDim.x) {
-    s_lo[i] = 0u;
-    s_hi[i] = 0;
-  }
-  __syncthreads();
-  const float v0 = static_cast<float>(a.v0);
-  const float scale = ldexpf(1.f, fix_exponent(stats, a.step, a.v0, max_steps_total(a)));
-  const TileTgt tgt{s_lo, s_hi, scale, x0, y0};
-  if (static_cast<int>(threadIdx.x) < blk.y) {
-    const int4 sg = a.tseg[blk.x + threadIdx.x];
-    const float gr = dw[sg.x];
-    if (gr != 0.f) {  // aberration.hpp:340
-      const RayRec rr = a.rec[sg.x];
-      const float gscale = static_cast<float>(static_cast<double>(gr) * rr.dl * a.v0);
-      CellAccT<TileTgt> cell;
-      constexpr int NB = RAY_BWD_BATCH;
-      for (int i = sg.y; i < sg.z; i += NB) {
-        float4 gt[NB];
-        float ax[NB], ay[NB];
-        int ix[NB], iy[NB];
-#pragma unroll
-        for (int u = 0; u < NB; ++u) {
-          const float k = static_cast<float>(min(i + u, sg.z - 1));
-          const float fx = fmaf(k, rr.dfx, rr.fxs), fy = fmaf(k, rr.dfy, rr.fys);
-          ix[u] = min(static_cast<int>(fx), W - 2);
-          iy[u] = min(static_cast<int>(fy), H - 2);
-          ax[u] = fx - ix[u];
-          ay[u] = fy - iy[u];
-          gt[u] = tex2Dgather<float4>(a.tex, ix[u] + 1.f, iy[u] + 1.f, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < NB; ++u) {
-          if (i + u < sg.z) {
-            // gather order: w=(ix,iy) z=(ix+1,iy) x=(ix,iy+1) y=(ix+1,iy+1)
-            const float top = fmaf(ax[u], gt[u].z - gt[u].w, gt[u].w);
-            const float bot = fmaf(ax[u], gt[u].y - gt[u].x, gt[u].x);
-            const float v = v0 + fmaf(ay[u], bot - top, top);
-            const float f = __fdividef(gscale, v * v);
-            cell.move(tgt, ix[u], iy[u]);
-            const float fy1 = f * ay[u], fy0 = f - fy1;  // f (1 - ay), f ay
-            cell.a00 = fmaf(-fy0, ax[u], cell.a00 + fy0);
-            cell.a01 = fmaf(fy0, ax[u], cell.a01);
-            cell.a10 = fmaf(-fy1, ax[u], cell.a10 + fy1);
-            cell.a11 = fmaf(fy1, ax[u], cell.a11);
-          }
-        }
-      }
-      cell.flush(tgt);
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kTileSlots; i += blockDim.x) {
-    const long long v = (static_cast<long long>(s_hi[i]) << 32) + static_cast<long long>(s_lo[i]);
-    if (v) {
-      const int x = x0 + i % kTileW, y = y0 + i / kTileW;
-      atomicAdd(acc + static_cast<size_t>(y) * W + x, static_cast<unsigned long long>(v));
     }
   }
 }
@@ -985,14 +843,6 @@ constexpr int kRayChunk = 128;  // max steps per work item (PACT_RAY_CHUNK overr
 constexpr int kPlanBlock = 256;
 constexpr int kLenBucket = 32;
 
-bool ray_tiles_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PACT_RAY_TILES");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 int ray_chunk() {
   static const int c = [] {
     const char* e = std::getenv("PACT_RAY_CHUNK");
@@ -1011,9 +861,6 @@ struct RayPlanData {
   const int4* items = nullptr;
   const int2* ray_slots = nullptr;
   int n_items = 0;
-  const int4* tseg = nullptr;
-  const int2* tblock = nullptr;
-  int n_tblocks = 0;
   std::vector<double> key;
   ~RayPlanData() {
     if (mem) cudaFree(mem);
@@ -1096,56 +943,10 @@ Status build_plan_data(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanD
   for (size_t k = 0; k < n_keys; ++k) start[k + 1] += start[k];
   std::vector<int4> sorted(std::max(ni, 1));
   for (int k = 0; k < ni; ++k) sorted[start[ck[k]]++] = items[k];
-  // The adjoint's interior steps re-cut by image tile: a ray's interior range
-  // [0, i_side) split where the tile of its stencil cell changes, with the
-  // cells computed by the kernels' own fp32 formula (fmaf(i, df, fs),
-  // monotone in i per axis, so each change point is a binary search).  The
-  // segments are grouped by tile (ray order within a tile) into blocks of at
-  // most kPlanBlock.  PACT_RAY_TILES=0 keeps the interior in the item kernel.
-  std::vector<int4> tseg;
-  std::vector<int2> tblock;
-  if (ray_tiles_enabled()) {
-    const int W = a.W, H = a.H;
-    const int ntx = (W - 1 + kRayTile - 1) / kRayTile, nty = (H - 1 + kRayTile - 1) / kRayTile;
-    auto cell = [](int i, float df, float fs, int lim) {
-      return std::min(static_cast<int>(std::fmaf(static_cast<float>(i), df, fs)), lim);
-    };
-    std::vector<std::vector<int4>> per_tile(static_cast<size_t>(ntx) * nty);
-    for (int r = 0; r < nr; ++r) {
-      const RayRec& q = rec[r];
-      if (q.n <= 0 || (q.flags & kRecGeneric) || q.i_side <= 0) continue;
-      int i = 0;
-      while (i < q.i_side) {
-        const int tx = cell(i, q.dfx, q.fxs, W - 2) / kRayTile;
-        const int ty = cell(i, q.dfy, q.fys, H - 2) / kRayTile;
-        // first j > i (<= i_side) whose tile differs, per axis
-        auto change = [&](float df, float fs, int lim, int t0) {
-          int lo = i + 1, hi = q.i_side;  // answer in [lo, hi]
-          while (lo < hi) {
-            const int mid = lo + (hi - lo) / 2;
-            if (cell(mid, df, fs, lim) / kRayTile != t0) hi = mid;
-            else lo = mid + 1;
-          }
-          return lo;
-        };
-        const int j = std::min(change(q.dfx, q.fxs, W - 2, tx), change(q.dfy, q.fys, H - 2, ty));
-        per_tile[static_cast<size_t>(ty) * ntx + tx].push_back(make_int4(r, i, j, ty * ntx + tx));
-        i = j;
-      }
-    }
-    for (auto& v : per_tile)
-      for (size_t k = 0; k < v.size(); k += kPlanBlock) {
-        tblock.push_back(make_int2(static_cast<int>(tseg.size()),
-                                   static_cast<int>(std::min<size_t>(kPlanBlock, v.size() - k))));
-        tseg.insert(tseg.end(), v.begin() + k, v.begin() + std::min(v.size(), k + kPlanBlock));
-      }
-  }
-  // one allocation: rec | items | slots | tile segments | tile blocks
+  // one allocation: rec | items | slots
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t o_items = al(sizeof(RayRec) * nr), o_slots = al(o_items + sizeof(int4) * sorted.size()),
-               o_tseg = al(o_slots + sizeof(int2) * nr),
-               o_tblk = al(o_tseg + sizeof(int4) * std::max<size_t>(tseg.size(), 1)),
-               total = o_tblk + sizeof(int2) * std::max<size_t>(tblock.size(), 1);
+               total = o_slots + sizeof(int2) * nr;
   void* mem = nullptr;
   PACT_CUDA_S(cudaMalloc(&mem, total));
   char* b = static_cast<char*>(mem);
@@ -1157,12 +958,6 @@ Status build_plan_data(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanD
   if (st.ok())
     st = cuda_status(cudaMemcpyAsync(b + o_slots, slots.data(), sizeof(int2) * nr,
                                      cudaMemcpyHostToDevice, s), "ray plan");
-  if (st.ok() && !tseg.empty())
-    st = cuda_status(cudaMemcpyAsync(b + o_tseg, tseg.data(), sizeof(int4) * tseg.size(),
-                                     cudaMemcpyHostToDevice, s), "ray plan");
-  if (st.ok() && !tblock.empty())
-    st = cuda_status(cudaMemcpyAsync(b + o_tblk, tblock.data(), sizeof(int2) * tblock.size(),
-                                     cudaMemcpyHostToDevice, s), "ray plan");
   if (st.ok()) st = cuda_status(cudaStreamSynchronize(s), "ray plan");  // host vectors die here
   cudaFree(rec_d);
   p.mem = mem;
@@ -1171,9 +966,6 @@ Status build_plan_data(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanD
   p.items = reinterpret_cast<const int4*>(b + o_items);
   p.ray_slots = reinterpret_cast<const int2*>(b + o_slots);
   p.n_items = ni;
-  p.tseg = reinterpret_cast<const int4*>(b + o_tseg);
-  p.tblock = reinterpret_cast<const int2*>(b + o_tblk);
-  p.n_tblocks = static_cast<int>(tblock.size());
   return {};
 }
 
@@ -1209,9 +1001,6 @@ Status ray_plan_get(pact_ctx* cache_ctx, pact_ctx* ctx, RayArgs& a, const double
   a.ray_slots = nullptr;
   a.partial = nullptr;
   a.n_items = 0;
-  a.tseg = nullptr;
-  a.tblock = nullptr;
-  a.n_tblocks = 0;
   if (!a.tex || a.n_rays <= 0) return {};
   std::vector<double> key = plan_key(a, centers, n_centers);
   RayPlanCache& c = plan_cache(cache_ctx);
@@ -1238,9 +1027,6 @@ Status ray_plan_get(pact_ctx* cache_ctx, pact_ctx* ctx, RayArgs& a, const double
   a.ray_slots = data->ray_slots;
   a.partial = out.partial;
   a.n_items = data->n_items;
-  a.tseg = data->tseg;
-  a.tblock = data->tblock;
-  a.n_tblocks = data->n_tblocks;
   return {};
 }
 
@@ -1260,9 +1046,6 @@ Status ray_plan_cached(pact_ctx* ctx, RayArgs& a, const double* centers, int n_c
     a.ray_slots = p.data->ray_slots;
     a.partial = p.partial;
     a.n_items = p.data->n_items;
-    a.tseg = p.data->tseg;
-    a.tblock = p.data->tblock;
-    a.n_tblocks = p.data->n_tblocks;
     return {};
   }
   return ray_plan_get(ctx, ctx, a, centers, n_centers, p);
@@ -1310,10 +1093,6 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
   PACT_TRY_S(after_launch(ctx, "ray_bound_kernel"));
   if (a.tex) {
     if (!a.rec) return internal_error("launch_ray_backward: ray plan missing");
-    if (a.n_tblocks > 0) {
-      ray_backward_tile_kernel<<<a.n_tblocks, kPlanBlock, 0, ctx->stream>>>(a, dw, acc, stats);
-      PACT_TRY_S(after_launch(ctx, "ray_backward_tile_kernel"));
-    }
     if (a.n_items > 0) {
       PACT_TRY_S(smem_optin(ray_backward_plan_kernel, smem));
       ray_backward_plan_kernel<<<div_up(a.n_items, kPlanBlock), kPlanBlock, smem, ctx->stream>>>(
