@@ -35,18 +35,16 @@ constexpr int kTile = 16;
 constexpr int kThreads = kTile * kTile;
 constexpr uint32_t kMagicIndexBias = 0x4B400000u;  // bits(2^23) + 2^22
 constexpr float kMagic = 12582912.0f;                // 1.5 * 2^23
-// Shared-memory window: sample plane X then difference plane D at a fixed
-// offset, so the D load is the X address plus an LDS immediate.
-constexpr int kPlaneFloats = 6144;
-constexpr int kPlaneBytes = kPlaneFloats * 4;
-constexpr size_t kWindowSmem = 2 * kPlaneBytes;
+// Shared-memory window: interleaved (x[i], x[i+1] - x[i]) entries, so a tap
+// is ONE 64-bit shared load (LDS.64) and one FFMA.
+constexpr int kPlaneFloats = 6144;  // entries per window
+constexpr size_t kWindowSmem = 8 * kPlaneFloats;
 
-// (x[i], x[i+1] - x[i]) from the two planes: two conflict-free LDS.32 when the
-// warp's samples span < 32 words.
+// (x[i], x[i+1] - x[i]) of window entry i: one LDS.64.  A half-warp's
+// samples span < 16 entries (8 x 2 pixels), so the load is conflict-free.
 __device__ __forceinline__ float2 lds_xd(uint32_t addr) {
   float2 v;
-  asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+24576];"
-               : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
   return v;
 }
 
@@ -71,8 +69,8 @@ struct DasArgs {
   int cap;        // staged entries per transducer
   int chunk;      // transducers per staging round
   int tx_per_split;
-  // 4 * (bits(2^23) + 2^22): runtime value so ptxas keeps one LEA per tap
-  uint32_t bias4;
+  // 8 * (bits(2^23) + 2^22): runtime value so ptxas keeps one LEA per tap
+  uint32_t bias8;
   float* out;     // [split][K_block][H][W]
   size_t split_stride;
   size_t plane;   // H*W
@@ -100,7 +98,7 @@ __device__ __forceinline__ double rect_max_dist(double px, double py, double x0,
 template <int KB>
 __global__ void __launch_bounds__(kThreads, (KB <= 32 ? 3 : 2))
 das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
-  extern __shared__ float s_win[];  // X plane [chunk][cap], D plane at +kPlaneBytes
+  extern __shared__ float2 s_win[];  // [chunk][cap] (x, dx) entries
   __shared__ int s_lo[128];
 
   const int tid = threadIdx.x;
@@ -156,8 +154,7 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
         if (idx < T) v0 = __ldg(row + idx);
         if (idx + 1 < T) v1 = __ldg(row + idx + 1);
       }
-      s_win[e] = v0;
-      s_win[e + kPlaneFloats] = v1 - v0;
+      s_win[e] = make_float2(v0, v1 - v0);
     }
     __syncthreads();
 
@@ -175,7 +172,7 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
         const f32x2 fb2 = pack2(fb, fb);
         // byte address of tap j: 8*bits(t_j) + cbase (uint32 wrap-around)
         const uint32_t cbase =
-            smem_base + 4u * static_cast<uint32_t>(ib - lo + nl * a.cap) - a.bias4;
+            smem_base + 8u * static_cast<uint32_t>(ib - lo + nl * a.cap) - a.bias8;
         const bool fast = (sb - a.cmax >= 0.0) && (sb - a.cmin <= static_cast<double>(T - 1));
         if (fast) {
 #pragma unroll
@@ -187,8 +184,8 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
             float t0, t1, f0, f1;
             unpack2(t2, t0, t1);
             unpack2(f2, f0, f1);
-            float2 v0 = lds_xd(mad_u32(__float_as_uint(t0), 4u, cbase));
-            float2 v1 = lds_xd(mad_u32(__float_as_uint(t1), 4u, cbase));
+            float2 v0 = lds_xd(mad_u32(__float_as_uint(t0), 8u, cbase));
+            float2 v1 = lds_xd(mad_u32(__float_as_uint(t1), 8u, cbase));
             acc[j / 2] = add2(acc[j / 2], pack2(fmaf(f0, v0.y, v0.x), fmaf(f1, v1.y, v1.x)));
           }
         } else {
@@ -211,7 +208,7 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
               bool valid = (i >= 0) && (i < T - 1 || (i == T - 1 && f[h] == 0.f));
               val[h] = 0.f;
               if (valid) {
-                float2 v = lds_xd(mad_u32(__float_as_uint(t[h]), 4u, cbase));
+                float2 v = lds_xd(mad_u32(__float_as_uint(t[h]), 8u, cbase));
                 val[h] = fmaf(f[h], v.y, v.x);
               }
             }
@@ -326,7 +323,7 @@ Status das_stack_device(pact_ctx* ctx, const pact_ring& ring, const pact_signal_
   a.k_dist = k_dist;
   a.s_off = meta.t0 / meta.dt;
   a.plane = plane;
-  a.bias4 = 4u * kMagicIndexBias;
+  a.bias8 = 8u * kMagicIndexBias;
 
   const double diag = std::hypot((double)(kTile - 1), (double)(kTile - 1)) * grid.pitch;
 
