@@ -40,8 +40,8 @@ constexpr float kMagic = 12582912.0f;                // 1.5 * 2^23
 constexpr int kPlaneFloats = 6144;  // entries per window
 constexpr size_t kWindowSmem = 8 * kPlaneFloats;
 
-// (x[i], x[i+1] - x[i]) of window entry i: one LDS.64.  A half-warp's
-// samples span < 16 entries (8 x 2 pixels), so the load is conflict-free.
+// (x[i], x[i+1] - x[i]) of window entry i: one LDS.64 (a half-warp per
+// shared-memory wavefront; see the pixel mapping in das_stack_kernel).
 __device__ __forceinline__ float2 lds_xd(uint32_t addr) {
   float2 v;
   asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
@@ -103,8 +103,11 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int lx = (warp & 1) * 8 + (lane & 7);
-  const int ly = (warp >> 1) * 4 + (lane >> 3);
+  // warp = 8 x 4 pixels as two 4 x 4 half-warps: a 64-bit shared load is
+  // served per half-warp, and a 4 x 4 block's samples of one transducer span
+  // < 16 window entries at pitch <= 0.1 mm (conflict-free LDS.64)
+  const int lx = (warp & 1) * 8 + (lane >> 4) * 4 + (lane & 3);
+  const int ly = (warp >> 1) * 4 + ((lane >> 2) & 3);
   const int x0 = blockIdx.x * kTile, y0 = blockIdx.y * kTile;
   const int px = x0 + lx, py = y0 + ly;
   const bool active = px < a.width && py < a.height;
