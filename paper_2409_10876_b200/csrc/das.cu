@@ -146,9 +146,10 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
     __syncthreads();
     // Stage the windows: contiguous per transducer, coalesced, zero outside [0, T-1].
     const int total = cnt * a.cap;
+    // (nl, off) of entry e = nl * cap + off, advanced incrementally (no
+    // integer division per staged entry)
+    int nl = tid / a.cap, off = tid - nl * a.cap;
     for (int e = tid; e < total; e += kThreads) {
-      int nl = e / a.cap;
-      int off = e - nl * a.cap;
       int lo = s_lo[nl];
       float v0 = 0.f, v1 = 0.f;
       if (lo != INT_MIN) {
@@ -158,6 +159,11 @@ das_stack_kernel(DasArgs a, DelayConsts<KB> dc) {
         if (idx + 1 < T) v1 = __ldg(row + idx + 1);
       }
       s_win[e] = make_float2(v0, v1 - v0);
+      off += kThreads;
+      while (off >= a.cap) {
+        off -= a.cap;
+        ++nl;
+      }
     }
     __syncthreads();
 
