@@ -584,7 +584,7 @@ siren_wgrad0_kernel(const float* __restrict__ dA0, const float2* __restrict__ co
 // chunk), then a fixed-order fold over the groups (deterministic).  Block b
 // belongs to the segment whose cumulative block range holds b.
 constexpr int kMaxSeg = 8;
-constexpr int kRedP = 32, kRedG = 8;  // params per block, chunk groups per param
+constexpr int kRedP = 64, kRedG = 4;
 struct ReduceSegs {
   const float* src[kMaxSeg];
   double* dst[kMaxSeg];
