@@ -139,6 +139,16 @@ struct RayArgs {
   const int2* ray_slots;
   float* partial;
   int n_items;
+  // Cell-gather plan of the interior adjoint (raymarch.cu; null: interior
+  // items go through the per-ray kernel): per stencil cell (W-1 x H-1,
+  // row-major) the range [cell_start[c], cell_start[c+1]) of cell_ent, each
+  // entry ray << cell_sb | step, one per interior step whose stencil is the
+  // cell.  The items are sorted
+  // generic | interior | side, so the adjoint skips [n_gen, n_gen + n_int).
+  const unsigned* cell_start;
+  const unsigned* cell_ent;
+  int cell_sb;
+  int n_gen_items, n_int_items;
 };
 
 // Creates a point-sampled, clamped pitch-2D texture over a row-major fp32

@@ -31,6 +31,8 @@
 #include <mutex>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "common.cuh"
 #include "geom.cuh"
 #include "train_ops.cuh"
@@ -559,10 +561,13 @@ __global__ void ray_finish_kernel(RayArgs a, float* __restrict__ w) {
 }
 
 // (256, 4): at most 64 registers, four blocks per SM (0.53 vs 0.56 ms at 68)
+// Items [skip_lo, skip_lo + skip_n) (the interior items, when the cell gather
+// takes them) are not run: thread t takes item t, or t + skip_n past skip_lo.
 __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, const float* __restrict__ dw,
                                                                   unsigned long long* __restrict__ acc,
                                                                   unsigned long long* __restrict__ border_rep,
-                                                                  const unsigned long long* __restrict__ stats) {
+                                                                  const unsigned long long* __restrict__ stats,
+                                                                  int skip_lo, int skip_n) {
   extern __shared__ float s_border[];
   const Border bd = load_border(a, s_border);
   const int W = a.W, H = a.H;
@@ -571,7 +576,8 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
   const Fix grad{acc, scale};
   const Fix rep{border_rep + static_cast<size_t>(blockIdx.x % kBorderReplicas) * 2 * (W + H), scale};
   {
-    const int it = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int it = t < skip_lo ? t : t + skip_n;
     if (it >= a.n_items) return;
     const int4 item = a.items[it];
     const float gr = dw[item.x];
@@ -680,35 +686,54 @@ __global__ void border_fold_kernel(unsigned long long* __restrict__ rep, int W, 
   atomicAdd(acc + static_cast<size_t>(py) * W + px, v);
 }
 
-// grad[p] += acc[p] 2^-S, one thread per pixel (four per thread, vectorised);
-// the accumulator is reset for the next launch, so the raster needs no
-// per-launch memset.
-__global__ void fix_to_grad_kernel(unsigned long long* __restrict__ acc, int npx,
+// grad[p] += (acc[p] + the pixel's four cell-gather corners) 2^-S, one thread
+// per pixel (exact integer sums); the accumulator is reset for the next
+// launch, so the raster needs no per-launch memset.
+__global__ void fix_to_grad_kernel(unsigned long long* __restrict__ acc, int W, int H,
                                    const unsigned long long* __restrict__ stats, double step,
-                                   double v0, double max_steps, double* __restrict__ grad) {
+                                   double v0, double max_steps,
+                                   const unsigned long long* __restrict__ cells,
+                                   double* __restrict__ grad) {
   const int S = fix_exponent(stats, step, v0, max_steps);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= npx) return;
-  const long long v = static_cast<long long>(acc[i]);
-  if (v != 0) {
-    acc[i] = 0ull;
-    grad[i] += ldexp(static_cast<double>(v), -S);
+  if (i >= W * H) return;
+  unsigned long long v = acc[i];
+  if (v != 0ull) acc[i] = 0ull;
+  if (cells) {  // cell (x, y) holds corners [(x,y), (x+1,y), (x,y+1), (x+1,y+1)]
+    const int y = i / W, x = i - y * W, Wc = W - 1, Hc = H - 1;
+    if (x < Wc && y < Hc) v += cells[4 * (y * Wc + x) + 0];
+    if (x > 0 && y < Hc) v += cells[4 * (y * Wc + x - 1) + 1];
+    if (x < Wc && y > 0) v += cells[4 * ((y - 1) * Wc + x) + 2];
+    if (x > 0 && y > 0) v += cells[4 * ((y - 1) * Wc + x - 1) + 3];
   }
+  if (v != 0ull) grad[i] += ldexp(static_cast<double>(static_cast<long long>(v)), -S);
 }
 
 // Bound statistics of one adjoint launch (exact maxima, order-independent):
 // stats[0] = max |dL/dw| over the rays, stats[1] = max 1 / v^2 over the
 // raster = 1 / min(v)^2 (non-negative doubles order like their bit patterns).
+// With a cell plan it also writes each ray's 32-byte record for the cell
+// gather: its pixel-coordinate line (fxs, fys, dfx, dfy) and deposit scale
+// g = dL/dw[r] dl v0 (aberration.hpp:354-355; 0 for rays the reference skips,
+// aberration.hpp:340).
 __global__ void __launch_bounds__(256) ray_bound_kernel(const float* __restrict__ dw, int n_rays,
                                                         const float* __restrict__ dv, int npx,
-                                                        float v0,
+                                                        float v0, const RayRec* __restrict__ rec,
+                                                        double v0d, float* __restrict__ gsc,
                                                         unsigned long long* __restrict__ stats) {
   __shared__ float s_g[8], s_v[8];
   float g = 0.f, vmin = INFINITY;
   const int stride = gridDim.x * blockDim.x;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rays; i += stride) {
-    const float x = fabsf(dw[i]);
+    const float d = dw[i], x = fabsf(d);
     g = x != x ? INFINITY : fmaxf(g, x);  // NaN -> infinite bound
+    if (gsc) {  // cell-gather ray record: (fxs, fys, dfx, dfy | g, -, -, -)
+      const RayRec q = rec[i];
+      float4* o = reinterpret_cast<float4*>(gsc) + 2 * static_cast<size_t>(i);
+      o[0] = make_float4(q.fxs, q.fys, q.dfx, q.dfy);
+      o[1] = make_float4(d == 0.f ? 0.f : static_cast<float>(static_cast<double>(d) * q.dl * v0d), 0.f,
+                         0.f, 0.f);
+    }
   }
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npx; i += stride) {
     const float x = dv[i];
@@ -735,6 +760,129 @@ __global__ void __launch_bounds__(256) ray_bound_kernel(const float* __restrict_
   const auto ib = static_cast<unsigned long long>(__double_as_longlong(iv));
   if (g != 0.f && *reinterpret_cast<volatile unsigned long long*>(stats) < gb) atomicMax(stats, gb);
   if (*reinterpret_cast<volatile unsigned long long*>(stats + 1) < ib) atomicMax(stats + 1, ib);
+}
+
+// ---- cell-gather adjoint of the interior steps -------------------------------
+// The interior adjoint as a gather.  The plan (build_cell_plan) lists, per
+// stencil cell, every interior step (ray, step index) whose stencil is that
+// cell, sorted by (ray, step); half a warp per cell walks its list with the
+// cell's four raster values in registers, so a step is pure arithmetic -- no
+// texture gather, no carry, no atomic -- on exactly the positions, stencil
+// values and weights of the per-ray march.  Each lane sums its steps (about a
+// dozen per cell) in fp32, converts the sums once to the 64-bit fixed-point
+// quantum of fix_exponent, and the half-warp adds the integers; the cell's
+// four corner sums go to `cells`, and fix_to_grad_kernel adds each pixel's
+// four corners (integer sums again), so the result is deterministic by
+// construction.
+constexpr int kCellBatch = 4;  // list entries per lane whose loads are in flight together
+
+__device__ __forceinline__ int cell_of(float fx, float fy, int W, int H) {
+  return min(static_cast<int>(fy), H - 2) * (W - 1) + min(static_cast<int>(fx), W - 2);
+}
+
+// Interior steps of ray r (the cell plan's entries): keys[off[r] + i] =
+// cell << 32 | r << sb | i for every interior step i.
+__global__ void cell_steps_kernel(const RayRec* __restrict__ rec, int n_rays, int W, int H, int sb,
+                                  const unsigned long long* __restrict__ off,
+                                  unsigned long long* __restrict__ keys) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rays) return;
+  const RayRec q = rec[r];
+  const int n_int = q.n > 0 && !(q.flags & kRecGeneric) ? q.i_side : 0;
+  unsigned long long* out = keys + off[r];
+  const unsigned long long rr = static_cast<unsigned long long>(r) << sb;
+  for (int i = 0; i < n_int; ++i) {
+    const int c = cell_of(fmaf(static_cast<float>(i), q.dfx, q.fxs),
+                          fmaf(static_cast<float>(i), q.dfy, q.fys), W, H);
+    out[i] = (static_cast<unsigned long long>(c) << 32) | rr | static_cast<unsigned>(i);
+  }
+}
+
+// Sorted keys (cell << 32 | entry) -> entries and the per-cell ranges.
+__global__ void cell_bounds_kernel(const unsigned long long* __restrict__ keys, unsigned n,
+                                   int n_cells, unsigned* __restrict__ start,
+                                   unsigned* __restrict__ ent) {
+  const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const unsigned long long key = keys[k];
+  const int c = static_cast<int>(key >> 32);
+  ent[k] = static_cast<unsigned>(key);
+  const int prev = k == 0 ? -1 : static_cast<int>(keys[k - 1] >> 32);
+  for (int q = prev + 1; q <= c; ++q) start[q] = k;
+  if (k == n - 1)
+    for (int q = c + 1; q <= n_cells; ++q) start[q] = n;
+}
+
+constexpr int LPC = 16;  // lanes per cell
+
+__device__ __forceinline__ long long cell_sum(long long v) {
+#pragma unroll
+  for (int o = LPC / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Half a warp per stencil cell (16 consecutive cells of a row per block);
+// lane l of the half takes the cell's entries l, l + 16, ... (coalesced).
+__global__ void __launch_bounds__(256) cell_gather_kernel(RayArgs a, const float4* __restrict__ rays,
+                                                          const unsigned long long* __restrict__ stats,
+                                                          unsigned long long* __restrict__ cells) {
+  const int lane = threadIdx.x & 31, l16 = lane % LPC;
+  const int W = a.W, H = a.H, Wc = W - 1, n_cells = Wc * (H - 1);
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) / LPC;
+  const bool live = c < n_cells;  // dead halves still join the shuffles
+  const int cc = live ? c : n_cells - 1;
+  const int cy = cc / Wc, cx = cc - cy * Wc;
+  const float q00 = __ldg(a.dv + cy * W + cx), q01 = __ldg(a.dv + cy * W + cx + 1);
+  const float q10 = __ldg(a.dv + (cy + 1) * W + cx), q11 = __ldg(a.dv + (cy + 1) * W + cx + 1);
+  const float dtop = q01 - q00, dbot = q11 - q10;
+  const float v0 = static_cast<float>(a.v0), fcx = static_cast<float>(cx), fcy = static_cast<float>(cy);
+  const int sb = a.cell_sb;
+  const unsigned smask = (1u << sb) - 1u;
+  float r00 = 0.f, r01 = 0.f, r10 = 0.f, r11 = 0.f;
+  const unsigned e0 = live ? a.cell_start[cc] : 0u, e1 = live ? a.cell_start[cc + 1] : 0u;
+  for (unsigned e = e0 + l16; e < e1; e += LPC * kCellBatch) {
+    unsigned en[kCellBatch];
+    float g[kCellBatch];
+    float4 geo[kCellBatch];
+#pragma unroll
+    for (int u = 0; u < kCellBatch; ++u) en[u] = __ldg(a.cell_ent + min(e + LPC * u, e1 - 1));
+#pragma unroll
+    for (int u = 0; u < kCellBatch; ++u) {
+      const float4* rr = rays + 2 * (en[u] >> sb);
+      geo[u] = __ldg(rr);
+      g[u] = e + LPC * u < e1 ? __ldg(reinterpret_cast<const float*>(rr + 1)) : 0.f;  // 0: skipped rays
+    }
+#pragma unroll
+    for (int u = 0; u < kCellBatch; ++u) {
+      // the per-ray march's interior_d / deposit arithmetic, operand for operand
+      const float fi = static_cast<float>(en[u] & smask);
+      const float ax = fmaf(fi, geo[u].z, geo[u].x) - fcx, ay = fmaf(fi, geo[u].w, geo[u].y) - fcy;
+      const float top = fmaf(ax, dtop, q00), bot = fmaf(ax, dbot, q10);
+      const float v = v0 + fmaf(ay, bot - top, top);
+      const float f = g[u] != 0.f ? g[u] * rcp_approx(v * v) : 0.f;
+      const float fy1 = f * ay, fy0 = f - fy1;  // f (1 - ay), f ay
+      r00 = fmaf(-fy0, ax, r00 + fy0);
+      r01 = fmaf(fy0, ax, r01);
+      r10 = fmaf(-fy1, ax, r10 + fy1);
+      r11 = fmaf(fy1, ax, r11);
+    }
+  }
+  const float scale = ldexpf(1.f, fix_exponent(stats, a.step, a.v0, max_steps_total(a)));
+  const long long s00 = cell_sum(__float2ll_rn(r00 * scale)), s01 = cell_sum(__float2ll_rn(r01 * scale));
+  const long long s10 = cell_sum(__float2ll_rn(r10 * scale)), s11 = cell_sum(__float2ll_rn(r11 * scale));
+  if (live && l16 == 0) {
+    unsigned long long* o = cells + 4 * static_cast<size_t>(c);
+    o[0] = static_cast<unsigned long long>(s00);
+    o[1] = static_cast<unsigned long long>(s01);
+    o[2] = static_cast<unsigned long long>(s10);
+    o[3] = static_cast<unsigned long long>(s11);
+  }
 }
 
 // Generic kernels (plain loads, no texture): one per-step march per ray.
@@ -861,9 +1009,16 @@ struct RayPlanData {
   const int4* items = nullptr;
   const int2* ray_slots = nullptr;
   int n_items = 0;
+  int n_gen = 0, n_int = 0;  // items are sorted generic | interior | side
+  // cell-gather plan of the interior adjoint (null: none, see build_cell_plan)
+  void* cell_mem = nullptr;
+  const unsigned* cell_start = nullptr;
+  const unsigned* cell_ent = nullptr;
+  int cell_sb = 0;
   std::vector<double> key;
   ~RayPlanData() {
     if (mem) cudaFree(mem);
+    if (cell_mem) cudaFree(cell_mem);
   }
 };
 
@@ -875,6 +1030,82 @@ std::vector<double> plan_key(const RayArgs& a, const double* centers, int n_cent
                              static_cast<double>(a.n_angles), static_cast<double>(a.n_rays)};
   key.insert(key.end(), centers, centers + 2 * n_centers);
   return key;
+}
+
+bool cells_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PACT_RAY_CELLS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+int bits_for(unsigned long long v) {  // bits to hold 0..v
+  int b = 0;
+  while (b < 64 && (v >> b) != 0ull) ++b;
+  return std::max(b, 1);
+}
+
+// The cell-gather plan (see cell_gather_kernel): every interior step of every
+// ray, keyed (cell, ray, step), radix-sorted once per geometry.  Skipped
+// (interior items stay on the per-ray kernel) when an entry does not fit 32
+// bits or PACT_RAY_CELLS=0.  Synchronous.
+Status build_cell_plan(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanData& p) {
+  if (!cells_enabled() || p.n_int == 0 || a.W < 2 || a.H < 2) return {};
+  const int nr = a.n_rays;
+  std::vector<unsigned long long> ho(nr + 1, 0);
+  int max_side = 0;
+  {
+    std::vector<RayRec> rec(nr);
+    PACT_CUDA_S(cudaMemcpyAsync(rec.data(), p.rec, sizeof(RayRec) * nr, cudaMemcpyDeviceToHost, s));
+    PACT_CUDA_S(cudaStreamSynchronize(s));
+    for (int r = 0; r < nr; ++r) {
+      const RayRec& q = rec[r];
+      const int n_int = q.n > 0 && !(q.flags & kRecGeneric) ? q.i_side : 0;
+      max_side = std::max(max_side, n_int);
+      ho[r + 1] = ho[r] + static_cast<unsigned long long>(n_int);
+    }
+  }
+  const int rb = bits_for(static_cast<unsigned long long>(nr - 1));
+  const int sb = bits_for(static_cast<unsigned long long>(std::max(max_side - 1, 0)));
+  const unsigned long long total = ho[nr];
+  const int n_cells = (a.W - 1) * (a.H - 1);
+  if (rb + sb > 32 || total == 0 || total >= (1ull << 31)) return {};
+  const unsigned n = static_cast<unsigned>(total);
+  auto hold = [](void* q) { return std::unique_ptr<void, void (*)(void*)>(q, [](void* x) { cudaFree(x); }); };
+  // the plan's own memory: start [n_cells + 1] | ent [n]
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t o_ent = al(sizeof(unsigned) * (n_cells + 1)), bytes = o_ent + sizeof(unsigned) * n;
+  void* mem = nullptr;
+  PACT_CUDA_S(cudaMalloc(&mem, bytes));
+  auto hold_mem = hold(mem);
+  char* b = static_cast<char*>(mem);
+  auto* start = reinterpret_cast<unsigned*>(b);
+  auto* ent = reinterpret_cast<unsigned*>(b + o_ent);
+  // scratch: offsets, keys (x2 for the sort), cub temp
+  const int end_bit = 32 + bits_for(static_cast<unsigned long long>(n_cells - 1));
+  size_t temp = 0;
+  unsigned long long* null_keys = nullptr;
+  PACT_CUDA_S(cub::DeviceRadixSort::SortKeys(nullptr, temp, null_keys, null_keys, n, 0, end_bit, s));
+  const size_t o_keys = al(sizeof(unsigned long long) * nr), o_tmp = al(o_keys + 16ull * n);
+  void* scratch = nullptr;
+  PACT_CUDA_S(cudaMalloc(&scratch, o_tmp + std::max<size_t>(temp, 16)));
+  auto hold_scratch = hold(scratch);
+  auto* off = static_cast<unsigned long long*>(scratch);
+  auto* keys = reinterpret_cast<unsigned long long*>(static_cast<char*>(scratch) + o_keys);
+  void* tmp = static_cast<char*>(scratch) + o_tmp;
+  PACT_CUDA_S(cudaMemcpyAsync(off, ho.data(), sizeof(unsigned long long) * nr, cudaMemcpyHostToDevice, s));
+  cell_steps_kernel<<<div_up(nr, 256), 256, 0, s>>>(p.rec, nr, a.W, a.H, sb, off, keys);
+  PACT_TRY_S(after_launch(ctx, "cell_steps_kernel"));
+  PACT_CUDA_S(cub::DeviceRadixSort::SortKeys(tmp, temp, keys, keys + n, n, 0, end_bit, s));
+  cell_bounds_kernel<<<div_up(static_cast<int>(n), 256), 256, 0, s>>>(keys + n, n, n_cells, start, ent);
+  PACT_TRY_S(after_launch(ctx, "cell_bounds_kernel"));
+  PACT_CUDA_S(cudaStreamSynchronize(s));  // the host offsets and the scratch die here
+  p.cell_mem = hold_mem.release();
+  p.cell_start = start;
+  p.cell_ent = ent;
+  p.cell_sb = sb;
+  return {};
 }
 
 // Builds the shared plan of a's geometry (a.centers on the device).  Synchronous.
@@ -918,8 +1149,13 @@ Status build_plan_data(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanD
           push(r, i, std::min(q.i_side, i + C), kItemInterior, i / C);
         for (int i = q.i_side; i < side_end; i += C)
           push(r, i, std::min(side_end, i + C), kItemSide, (i - q.i_side) / C);
-        if (q.i_corner < q.n && static_cast<int>(items.size()) > first)
-          items.back().w |= 1 << 30;  // the ray's last item adds the corner run
+        if (q.i_corner < q.n && static_cast<int>(items.size()) > first) {
+          // the ray's last item adds the corner run; an empty border-line item
+          // carries it when the ray has none (the adjoint's interior items may
+          // run in the cell gather, which has no corner logic)
+          if (((items.back().w >> 28) & 3) == kItemInterior) push(r, side_end, side_end, kItemSide, 0);
+          items.back().w |= 1 << 30;
+        }
       }
     }
     slots[r] = make_int2(first, static_cast<int>(items.size()) - first);
@@ -941,6 +1177,9 @@ Status build_plan_data(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanD
     ++start[ck[k] + 1];
   }
   for (size_t k = 0; k < n_keys; ++k) start[k + 1] += start[k];
+  const size_t per_rank = static_cast<size_t>(nb) * nc;
+  p.n_gen = start[per_rank];
+  p.n_int = start[2 * per_rank] - start[per_rank];
   std::vector<int4> sorted(std::max(ni, 1));
   for (int k = 0; k < ni; ++k) sorted[start[ck[k]]++] = items[k];
   // one allocation: rec | items | slots
@@ -966,7 +1205,7 @@ Status build_plan_data(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanD
   p.items = reinterpret_cast<const int4*>(b + o_items);
   p.ray_slots = reinterpret_cast<const int2*>(b + o_slots);
   p.n_items = ni;
-  return {};
+  return build_cell_plan(ctx, s, a, p);
 }
 
 // Plans of one context, by geometry (most recent first, a few kept).
@@ -993,9 +1232,19 @@ RayPlanCache& plan_cache(pact_ctx* ctx) {
 
 }  // namespace
 
+static void set_cell_args(RayArgs& a, const RayPlanData& d) {
+  a.cell_start = d.cell_start;
+  a.cell_ent = d.cell_ent;
+  a.cell_sb = d.cell_sb;
+  a.n_gen_items = d.n_gen;
+  a.n_int_items = d.n_int;
+}
+
 Status ray_plan_get(pact_ctx* cache_ctx, pact_ctx* ctx, RayArgs& a, const double* centers,
                     int n_centers, RayPlan& out) {
   ray_plan_release(out, ctx->stream);
+  a.cell_start = nullptr;
+  a.cell_ent = nullptr;
   a.rec = nullptr;
   a.items = nullptr;
   a.ray_slots = nullptr;
@@ -1027,6 +1276,7 @@ Status ray_plan_get(pact_ctx* cache_ctx, pact_ctx* ctx, RayArgs& a, const double
   a.ray_slots = data->ray_slots;
   a.partial = out.partial;
   a.n_items = data->n_items;
+  set_cell_args(a, *data);
   return {};
 }
 
@@ -1046,6 +1296,7 @@ Status ray_plan_cached(pact_ctx* ctx, RayArgs& a, const double* centers, int n_c
     a.ray_slots = p.data->ray_slots;
     a.partial = p.partial;
     a.n_items = p.data->n_items;
+    set_cell_args(a, *p.data);
     return {};
   }
   return ray_plan_get(ctx, ctx, a, centers, n_centers, p);
@@ -1074,10 +1325,16 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
   const size_t smem = border_smem(a);
   if (a.n_rays == 0) return {};
   // fixed-point accumulators: raster [H W] | border replicas | bound statistics,
-  // zero between launches (fix_to_grad_kernel resets what it reads)
+  // zero between launches (fix_to_grad_kernel resets what it reads); with a
+  // cell plan also the per-ray deposit scales and the cell corner sums
   const size_t npx = static_cast<size_t>(a.W) * a.H;
   const size_t rep_n = static_cast<size_t>(kBorderReplicas) * 2 * (a.W + a.H);
-  const size_t bytes = sizeof(unsigned long long) * (npx + rep_n + 2);
+  const bool cells = a.tex && a.rec && a.cell_start;
+  const size_t n_cells = cells ? static_cast<size_t>(a.W - 1) * (a.H - 1) : 0;
+  const size_t fix_bytes = sizeof(unsigned long long) * (npx + rep_n + 2);
+  const size_t gsc_off = (fix_bytes + 255) & ~size_t(255);
+  const size_t cell_off = (gsc_off + 32 * static_cast<size_t>(cells ? a.n_rays : 0) + 255) & ~size_t(255);
+  const size_t bytes = cell_off + 4 * sizeof(unsigned long long) * n_cells;
   pact_scratch& sc = ctx->scratch[kScratchRayBorder];
   const void* before = sc.ptr;
   void* base = nullptr;
@@ -1086,18 +1343,29 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
   auto* acc = static_cast<unsigned long long*>(base);
   auto* rep = acc + npx;
   auto* stats = rep + rep_n;
+  float* gsc = cells ? reinterpret_cast<float*>(static_cast<char*>(base) + gsc_off) : nullptr;
+  auto* cell_sums = cells ? reinterpret_cast<unsigned long long*>(static_cast<char*>(base) + cell_off) : nullptr;
   PACT_CUDA_S(cudaMemsetAsync(stats, 0, 2 * sizeof(unsigned long long), ctx->stream));
   const int nb = std::max(1, div_up(std::max(static_cast<int>(npx), a.n_rays), 256 * 4));
   ray_bound_kernel<<<nb, 256, 0, ctx->stream>>>(dw, a.n_rays, a.dv, static_cast<int>(npx),
-                                                static_cast<float>(a.v0), stats);
+                                                static_cast<float>(a.v0), a.rec, a.v0, gsc, stats);
   PACT_TRY_S(after_launch(ctx, "ray_bound_kernel"));
   if (a.tex) {
     if (!a.rec) return internal_error("launch_ray_backward: ray plan missing");
-    if (a.n_items > 0) {
+    // the interior items go to the cell gather when there is a cell plan
+    const int skip_lo = cells ? a.n_gen_items : a.n_items, skip_n = cells ? a.n_int_items : 0;
+    const int n_run = a.n_items - skip_n;
+    if (n_run > 0) {
       PACT_TRY_S(smem_optin(ray_backward_plan_kernel, smem));
-      ray_backward_plan_kernel<<<div_up(a.n_items, kPlanBlock), kPlanBlock, smem, ctx->stream>>>(
-          a, dw, acc, rep, stats);
+      ray_backward_plan_kernel<<<div_up(n_run, kPlanBlock), kPlanBlock, smem, ctx->stream>>>(
+          a, dw, acc, rep, stats, skip_lo, skip_n);
       PACT_TRY_S(after_launch(ctx, "ray_backward_plan_kernel"));
+    }
+    if (cells) {
+      const int grid = div_up(static_cast<int>(n_cells), 256 / LPC);
+      cell_gather_kernel<<<grid, 256, 0, ctx->stream>>>(a, reinterpret_cast<const float4*>(gsc), stats,
+                                                        cell_sums);
+      PACT_TRY_S(after_launch(ctx, "cell_gather_kernel"));
     }
   } else {
     PACT_TRY_S(smem_optin(ray_backward_kernel<false>, smem));
@@ -1110,7 +1378,7 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
     PACT_TRY_S(after_launch(ctx, "border_fold_kernel"));
   }
   fix_to_grad_kernel<<<div_up(static_cast<int>(npx), 256), 256, 0, ctx->stream>>>(
-      acc, static_cast<int>(npx), stats, a.step, a.v0, max_steps_total(a), grad);
+      acc, a.W, a.H, stats, a.step, a.v0, max_steps_total(a), cell_sums, grad);
   return after_launch(ctx, "fix_to_grad_kernel");
 }
 
