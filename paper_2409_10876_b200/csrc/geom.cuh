@@ -140,14 +140,19 @@ struct RayArgs {
   float* partial;
   int n_items;
   // Cell-gather plan of the interior adjoint (raymarch.cu; null: interior
-  // items go through the per-ray kernel): per stencil cell (W-1 x H-1,
-  // row-major) the range [cell_start[c], cell_start[c+1]) of cell_ent, each
-  // entry ray << cell_sb | step, one per interior step whose stencil is the
-  // cell.  The items are sorted
+  // items go through the per-ray kernel).  Stencil cells (W-1 x H-1) are
+  // grouped in tiles of cell_t x cell_t, numbered tile-major (tile, then
+  // row-major inside the tile, padded); cell c's interior steps are
+  // cell_ent[cell_start[c] .. cell_start[c+1]), each local ray << cell_sb |
+  // step, where local ray j of tile t is tile_rays[tile_start[t] + j].
+  // cell_geo[r] = (fxs, fys, dfx, dfy) of ray r.  The items are sorted
   // generic | interior | side, so the adjoint skips [n_gen, n_gen + n_int).
   const unsigned* cell_start;
   const unsigned* cell_ent;
-  int cell_sb;
+  const unsigned* tile_start;
+  const unsigned* tile_rays;
+  const float4* cell_geo;
+  int cell_sb, cell_t, tile_max;
   int n_gen_items, n_int_items;
 };
 

@@ -712,10 +712,9 @@ __global__ void fix_to_grad_kernel(unsigned long long* __restrict__ acc, int W, 
 // Bound statistics of one adjoint launch (exact maxima, order-independent):
 // stats[0] = max |dL/dw| over the rays, stats[1] = max 1 / v^2 over the
 // raster = 1 / min(v)^2 (non-negative doubles order like their bit patterns).
-// With a cell plan it also writes each ray's 32-byte record for the cell
-// gather: its pixel-coordinate line (fxs, fys, dfx, dfy) and deposit scale
-// g = dL/dw[r] dl v0 (aberration.hpp:354-355; 0 for rays the reference skips,
-// aberration.hpp:340).
+// With a cell plan it also writes each ray's deposit scale
+// gsc[r] = dL/dw[r] dl v0 (aberration.hpp:354-355; 0 for rays the reference
+// skips, aberration.hpp:340).
 __global__ void __launch_bounds__(256) ray_bound_kernel(const float* __restrict__ dw, int n_rays,
                                                         const float* __restrict__ dv, int npx,
                                                         float v0, const RayRec* __restrict__ rec,
@@ -727,13 +726,7 @@ __global__ void __launch_bounds__(256) ray_bound_kernel(const float* __restrict_
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rays; i += stride) {
     const float d = dw[i], x = fabsf(d);
     g = x != x ? INFINITY : fmaxf(g, x);  // NaN -> infinite bound
-    if (gsc) {  // cell-gather ray record: (fxs, fys, dfx, dfy | g, -, -, -)
-      const RayRec q = rec[i];
-      float4* o = reinterpret_cast<float4*>(gsc) + 2 * static_cast<size_t>(i);
-      o[0] = make_float4(q.fxs, q.fys, q.dfx, q.dfy);
-      o[1] = make_float4(d == 0.f ? 0.f : static_cast<float>(static_cast<double>(d) * q.dl * v0d), 0.f,
-                         0.f, 0.f);
-    }
+    if (gsc) gsc[i] = d == 0.f ? 0.f : static_cast<float>(static_cast<double>(d) * rec[i].dl * v0d);
   }
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npx; i += stride) {
     const float x = dv[i];
@@ -765,57 +758,104 @@ __global__ void __launch_bounds__(256) ray_bound_kernel(const float* __restrict_
 // ---- cell-gather adjoint of the interior steps -------------------------------
 // The interior adjoint as a gather.  The plan (build_cell_plan) lists, per
 // stencil cell, every interior step (ray, step index) whose stencil is that
-// cell, sorted by (ray, step); half a warp per cell walks its list with the
-// cell's four raster values in registers, so a step is pure arithmetic -- no
-// texture gather, no carry, no atomic -- on exactly the positions, stencil
-// values and weights of the per-ray march.  Each lane sums its steps (about a
-// dozen per cell) in fp32, converts the sums once to the 64-bit fixed-point
-// quantum of fix_exponent, and the half-warp adds the integers; the cell's
-// four corner sums go to `cells`, and fix_to_grad_kernel adds each pixel's
-// four corners (integer sums again), so the result is deterministic by
-// construction.
+// cell, sorted by (ray, step).  One block per tile of cell_t x cell_t cells
+// first stages the line and deposit scale of every ray crossing the tile in
+// shared memory; then half a warp per cell walks the cell's list with the
+// cell's four raster values in registers, so a step is arithmetic on shared
+// operands -- no texture gather, no carry, no atomic -- on exactly the
+// positions, stencil values and weights of the per-ray march.  A cell's lanes
+// sum their steps in fp32 and combine them by a fixed shuffle tree; the four
+// corner sums go to `cells` in the 64-bit fixed-point quantum of fix_exponent,
+// and fix_to_grad_kernel adds each pixel's four corners as integers, so the
+// result is deterministic by construction.
 constexpr int kCellBatch = 4;  // list entries per lane whose loads are in flight together
+constexpr int LPC = 8;         // lanes per cell
 
-__device__ __forceinline__ int cell_of(float fx, float fy, int W, int H) {
-  return min(static_cast<int>(fy), H - 2) * (W - 1) + min(static_cast<int>(fx), W - 2);
+struct CellTiles {  // tile-major cell numbering
+  int T, tx, Wc, Hc;
+  __host__ __device__ __forceinline__ int cell(int cx, int cy) const {
+    return ((cy / T) * tx + cx / T) * T * T + (cy % T) * T + cx % T;
+  }
+  __host__ __device__ __forceinline__ int tile(int cx, int cy) const { return (cy / T) * tx + cx / T; }
+};
+
+__device__ __forceinline__ void cell_xy(const RayRec& q, int i, int W, int H, int& cx, int& cy) {
+  cx = min(static_cast<int>(fmaf(static_cast<float>(i), q.dfx, q.fxs)), W - 2);
+  cy = min(static_cast<int>(fmaf(static_cast<float>(i), q.dfy, q.fys)), H - 2);
 }
 
-// Interior steps of ray r (the cell plan's entries): keys[off[r] + i] =
-// cell << 32 | r << sb | i for every interior step i.
+__device__ __forceinline__ int interior_steps(const RayRec& q) {
+  return q.n > 0 && !(q.flags & kRecGeneric) ? q.i_side : 0;
+}
+
+// Pass A (per ray): its interior steps' keys cell << 32 | r << sb | i at
+// keys[off[r] ..], the (tile, ray) pairs of the tiles it crosses (a straight
+// line crosses a convex tile once) at tkeys[toff[r] ..] or, with tkeys null,
+// their count in tcnt[r]; and the ray's line in geo.
 __global__ void cell_steps_kernel(const RayRec* __restrict__ rec, int n_rays, int W, int H, int sb,
-                                  const unsigned long long* __restrict__ off,
-                                  unsigned long long* __restrict__ keys) {
+                                  CellTiles ct, const unsigned long long* __restrict__ off,
+                                  unsigned long long* __restrict__ keys,
+                                  const unsigned long long* __restrict__ toff,
+                                  unsigned long long* __restrict__ tkeys, unsigned* __restrict__ tcnt,
+                                  float4* __restrict__ geo) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n_rays) return;
   const RayRec q = rec[r];
-  const int n_int = q.n > 0 && !(q.flags & kRecGeneric) ? q.i_side : 0;
-  unsigned long long* out = keys + off[r];
-  const unsigned long long rr = static_cast<unsigned long long>(r) << sb;
+  if (geo) geo[r] = make_float4(q.fxs, q.fys, q.dfx, q.dfy);
+  const int n_int = interior_steps(q);
+  int prev = -1;
+  unsigned nt = 0;
   for (int i = 0; i < n_int; ++i) {
-    const int c = cell_of(fmaf(static_cast<float>(i), q.dfx, q.fxs),
-                          fmaf(static_cast<float>(i), q.dfy, q.fys), W, H);
-    out[i] = (static_cast<unsigned long long>(c) << 32) | rr | static_cast<unsigned>(i);
+    int cx, cy;
+    cell_xy(q, i, W, H, cx, cy);
+    if (keys)
+      keys[off[r] + i] = (static_cast<unsigned long long>(ct.cell(cx, cy)) << 32) |
+                         (static_cast<unsigned long long>(r) << sb) | static_cast<unsigned>(i);
+    const int t = ct.tile(cx, cy);
+    if (t != prev) {
+      if (tkeys) tkeys[toff[r] + nt] = (static_cast<unsigned long long>(t) << 32) | static_cast<unsigned>(r);
+      ++nt;
+      prev = t;
+    }
   }
+  if (tcnt) tcnt[r] = nt;
 }
 
-// Sorted keys (cell << 32 | entry) -> entries and the per-cell ranges.
-__global__ void cell_bounds_kernel(const unsigned long long* __restrict__ keys, unsigned n,
-                                   int n_cells, unsigned* __restrict__ start,
-                                   unsigned* __restrict__ ent) {
+// Sorted keys (group << 32 | value) -> values and the per-group ranges
+// start[0 .. n_groups].
+__global__ void group_bounds_kernel(const unsigned long long* __restrict__ keys, unsigned n,
+                                    int n_groups, unsigned* __restrict__ start,
+                                    unsigned* __restrict__ val) {
   const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const unsigned long long key = keys[k];
   const int c = static_cast<int>(key >> 32);
-  ent[k] = static_cast<unsigned>(key);
+  if (val) val[k] = static_cast<unsigned>(key);
   const int prev = k == 0 ? -1 : static_cast<int>(keys[k - 1] >> 32);
   for (int q = prev + 1; q <= c; ++q) start[q] = k;
   if (k == n - 1)
-    for (int q = c + 1; q <= n_cells; ++q) start[q] = n;
+    for (int q = c + 1; q <= n_groups; ++q) start[q] = n;
 }
 
-constexpr int LPC = 16;  // lanes per cell
+// Pass B (per entry): the ray id -> its index in the tile's sorted ray list.
+__global__ void cell_localize_kernel(const unsigned long long* __restrict__ keys, unsigned n, int sb,
+                                     int T, const unsigned* __restrict__ tile_start,
+                                     const unsigned* __restrict__ tile_rays,
+                                     unsigned* __restrict__ ent) {
+  const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const unsigned long long key = keys[k];
+  const int t = static_cast<int>(key >> 32) / (T * T);
+  const unsigned e = static_cast<unsigned>(key), r = e >> sb;
+  unsigned lo = tile_start[t], hi = tile_start[t + 1];
+  while (lo < hi) {  // lower bound (r is present)
+    const unsigned mid = (lo + hi) >> 1;
+    if (tile_rays[mid] < r) lo = mid + 1; else hi = mid;
+  }
+  ent[k] = ((lo - tile_start[t]) << sb) | (e & ((1u << sb) - 1u));
+}
 
-__device__ __forceinline__ long long cell_sum(long long v) {
+__device__ __forceinline__ float cell_sum(float v) {  // fixed xor tree over the cell's lanes
 #pragma unroll
   for (int o = LPC / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
@@ -827,61 +867,87 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return y;
 }
 
-// Half a warp per stencil cell (16 consecutive cells of a row per block);
-// lane l of the half takes the cell's entries l, l + 16, ... (coalesced).
-__global__ void __launch_bounds__(256) cell_gather_kernel(RayArgs a, const float4* __restrict__ rays,
+// One block (kCellThreads) per tile of T x T cells; dynamic smem: tile_max ray
+// lines (float4) + deposit scales (float).
+constexpr int kCellThreads = 512;
+
+template <int T>
+__global__ void __launch_bounds__(kCellThreads, 3) cell_gather_kernel(RayArgs a, const float* __restrict__ gsc,
                                                           const unsigned long long* __restrict__ stats,
                                                           unsigned long long* __restrict__ cells) {
-  const int lane = threadIdx.x & 31, l16 = lane % LPC;
-  const int W = a.W, H = a.H, Wc = W - 1, n_cells = Wc * (H - 1);
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) / LPC;
-  const bool live = c < n_cells;  // dead halves still join the shuffles
-  const int cc = live ? c : n_cells - 1;
-  const int cy = cc / Wc, cx = cc - cy * Wc;
-  const float q00 = __ldg(a.dv + cy * W + cx), q01 = __ldg(a.dv + cy * W + cx + 1);
-  const float q10 = __ldg(a.dv + (cy + 1) * W + cx), q11 = __ldg(a.dv + (cy + 1) * W + cx + 1);
-  const float dtop = q01 - q00, dbot = q11 - q10;
-  const float v0 = static_cast<float>(a.v0), fcx = static_cast<float>(cx), fcy = static_cast<float>(cy);
+  extern __shared__ float4 s_geo[];
+  float* s_g = reinterpret_cast<float*>(s_geo + a.tile_max);
+  const int W = a.W, H = a.H, Wc = W - 1, Hc = H - 1;
+  const int tile = blockIdx.x, tx = (Wc + T - 1) / T;
+  const int tile_x0 = (tile % tx) * T, tile_y0 = (tile / tx) * T;
+  const unsigned r0 = a.tile_start[tile], nr = a.tile_start[tile + 1] - r0;
+  for (unsigned j = threadIdx.x; j < nr; j += blockDim.x) {
+    const unsigned r = __ldg(a.tile_rays + r0 + j);
+    s_geo[j] = __ldg(a.cell_geo + r);
+    s_g[j] = __ldg(gsc + r);
+  }
+  __syncthreads();
+  const float scale = ldexpf(1.f, fix_exponent(stats, a.step, a.v0, max_steps_total(a)));
+  const float v0 = static_cast<float>(a.v0);
   const int sb = a.cell_sb;
   const unsigned smask = (1u << sb) - 1u;
-  float r00 = 0.f, r01 = 0.f, r10 = 0.f, r11 = 0.f;
-  const unsigned e0 = live ? a.cell_start[cc] : 0u, e1 = live ? a.cell_start[cc + 1] : 0u;
-  for (unsigned e = e0 + l16; e < e1; e += LPC * kCellBatch) {
-    unsigned en[kCellBatch];
-    float g[kCellBatch];
-    float4 geo[kCellBatch];
-#pragma unroll
-    for (int u = 0; u < kCellBatch; ++u) en[u] = __ldg(a.cell_ent + min(e + LPC * u, e1 - 1));
+  const int lane = threadIdx.x & 31, l16 = lane % LPC, half = threadIdx.x / LPC;
+  const int halves = blockDim.x / LPC;
+  for (int lc = half; lc < T * T; lc += halves) {  // uniform per half-warp; rounds uniform per warp
+    const int cx = tile_x0 + lc % T, cy = tile_y0 + lc / T;
+    const bool live = cx < Wc && cy < Hc;
+    const int ccx = min(cx, Wc - 1), ccy = min(cy, Hc - 1);
+    const float q00 = __ldg(a.dv + ccy * W + ccx), q01 = __ldg(a.dv + ccy * W + ccx + 1);
+    const float q10 = __ldg(a.dv + (ccy + 1) * W + ccx), q11 = __ldg(a.dv + (ccy + 1) * W + ccx + 1);
+    const float dtop = q01 - q00, dbot = q11 - q10;
+    const float fcx = static_cast<float>(ccx), fcy = static_cast<float>(ccy);
+    const int c = tile * T * T + lc;
+    const unsigned e0 = live ? a.cell_start[c] : 0u, e1 = live ? a.cell_start[c + 1] : 0u;
+    float r00 = 0.f, r01 = 0.f, r10 = 0.f, r11 = 0.f;
+    // software pipeline: the next batch of entries loads while this one runs
+    unsigned nx[kCellBatch];
 #pragma unroll
     for (int u = 0; u < kCellBatch; ++u) {
-      const float4* rr = rays + 2 * (en[u] >> sb);
-      geo[u] = __ldg(rr);
-      g[u] = e + LPC * u < e1 ? __ldg(reinterpret_cast<const float*>(rr + 1)) : 0.f;  // 0: skipped rays
+      const unsigned q = e0 + l16 + LPC * u;
+      nx[u] = q < e1 ? __ldg(a.cell_ent + q) : 0u;
     }
+    for (unsigned e = e0 + l16; e < e1; e += LPC * kCellBatch) {
+      unsigned en[kCellBatch];
 #pragma unroll
-    for (int u = 0; u < kCellBatch; ++u) {
-      // the per-ray march's interior_d / deposit arithmetic, operand for operand
-      const float fi = static_cast<float>(en[u] & smask);
-      const float ax = fmaf(fi, geo[u].z, geo[u].x) - fcx, ay = fmaf(fi, geo[u].w, geo[u].y) - fcy;
-      const float top = fmaf(ax, dtop, q00), bot = fmaf(ax, dbot, q10);
-      const float v = v0 + fmaf(ay, bot - top, top);
-      const float f = g[u] != 0.f ? g[u] * rcp_approx(v * v) : 0.f;
-      const float fy1 = f * ay, fy0 = f - fy1;  // f (1 - ay), f ay
-      r00 = fmaf(-fy0, ax, r00 + fy0);
-      r01 = fmaf(fy0, ax, r01);
-      r10 = fmaf(-fy1, ax, r10 + fy1);
-      r11 = fmaf(fy1, ax, r11);
+      for (int u = 0; u < kCellBatch; ++u) {
+        en[u] = nx[u];
+        const unsigned q = e + LPC * (kCellBatch + u);
+        nx[u] = q < e1 ? __ldg(a.cell_ent + q) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kCellBatch; ++u) {
+        // the per-ray march's interior_d / deposit arithmetic, operand for operand
+        const unsigned j = en[u] >> sb;
+        const float4 geo = s_geo[j];
+        const float g = e + LPC * u < e1 ? s_g[j] : 0.f;  // 0: rays the reference skips (aberration.hpp:340)
+        const float fi = static_cast<float>(en[u] & smask);
+        const float ax = fmaf(fi, geo.z, geo.x) - fcx, ay = fmaf(fi, geo.w, geo.y) - fcy;
+        const float top = fmaf(ax, dtop, q00), bot = fmaf(ax, dbot, q10);
+        const float v = v0 + fmaf(ay, bot - top, top);
+        const float f = g != 0.f ? g * rcp_approx(v * v) : 0.f;
+        const float fy1 = f * ay, fy0 = f - fy1;  // f (1 - ay), f ay
+        r00 = fmaf(-fy0, ax, r00 + fy0);
+        r01 = fmaf(fy0, ax, r01);
+        r10 = fmaf(-fy1, ax, r10 + fy1);
+        r11 = fmaf(fy1, ax, r11);
+      }
     }
-  }
-  const float scale = ldexpf(1.f, fix_exponent(stats, a.step, a.v0, max_steps_total(a)));
-  const long long s00 = cell_sum(__float2ll_rn(r00 * scale)), s01 = cell_sum(__float2ll_rn(r01 * scale));
-  const long long s10 = cell_sum(__float2ll_rn(r10 * scale)), s11 = cell_sum(__float2ll_rn(r11 * scale));
-  if (live && l16 == 0) {
-    unsigned long long* o = cells + 4 * static_cast<size_t>(c);
-    o[0] = static_cast<unsigned long long>(s00);
-    o[1] = static_cast<unsigned long long>(s01);
-    o[2] = static_cast<unsigned long long>(s10);
-    o[3] = static_cast<unsigned long long>(s11);
+    r00 = cell_sum(r00);
+    r01 = cell_sum(r01);
+    r10 = cell_sum(r10);
+    r11 = cell_sum(r11);
+    if (live && l16 == 0) {
+      unsigned long long* o = cells + 4 * static_cast<size_t>(cy * Wc + cx);
+      o[0] = static_cast<unsigned long long>(__float2ll_rn(r00 * scale));
+      o[1] = static_cast<unsigned long long>(__float2ll_rn(r01 * scale));
+      o[2] = static_cast<unsigned long long>(__float2ll_rn(r10 * scale));
+      o[3] = static_cast<unsigned long long>(__float2ll_rn(r11 * scale));
+    }
   }
 }
 
@@ -1012,13 +1078,18 @@ struct RayPlanData {
   int n_gen = 0, n_int = 0;  // items are sorted generic | interior | side
   // cell-gather plan of the interior adjoint (null: none, see build_cell_plan)
   void* cell_mem = nullptr;
+  void* tile_mem = nullptr;
   const unsigned* cell_start = nullptr;
   const unsigned* cell_ent = nullptr;
-  int cell_sb = 0;
+  const unsigned* tile_start = nullptr;
+  const unsigned* tile_rays = nullptr;
+  const float4* cell_geo = nullptr;
+  int cell_sb = 0, cell_t = 0, tile_max = 0, n_tiles = 0;
   std::vector<double> key;
   ~RayPlanData() {
     if (mem) cudaFree(mem);
     if (cell_mem) cudaFree(cell_mem);
+    if (tile_mem) cudaFree(tile_mem);
   }
 };
 
@@ -1046,13 +1117,18 @@ int bits_for(unsigned long long v) {  // bits to hold 0..v
   return std::max(b, 1);
 }
 
-// The cell-gather plan (see cell_gather_kernel): every interior step of every
-// ray, keyed (cell, ray, step), radix-sorted once per geometry.  Skipped
-// (interior items stay on the per-ray kernel) when an entry does not fit 32
-// bits or PACT_RAY_CELLS=0.  Synchronous.
+// The cell-gather plan (see cell_gather_kernel), built once per geometry:
+// every interior step of every ray keyed (cell, ray, step) and radix-sorted;
+// per tile, the sorted list of rays crossing it; each entry's ray replaced by
+// its index in its tile's list.  The tile edge is 16 cells, or 8 when a
+// tile's ray table would not fit in shared memory.  Skipped (the interior
+// items stay on the per-ray kernel) when an entry does not fit 32 bits or
+// PACT_RAY_CELLS=0.  Synchronous.
+constexpr size_t kCellSmemMax = 160 * 1024;
+
 Status build_cell_plan(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanData& p) {
   if (!cells_enabled() || p.n_int == 0 || a.W < 2 || a.H < 2) return {};
-  const int nr = a.n_rays;
+  const int nr = a.n_rays, Wc = a.W - 1, Hc = a.H - 1;
   std::vector<unsigned long long> ho(nr + 1, 0);
   int max_side = 0;
   {
@@ -1066,45 +1142,121 @@ Status build_cell_plan(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanD
       ho[r + 1] = ho[r] + static_cast<unsigned long long>(n_int);
     }
   }
-  const int rb = bits_for(static_cast<unsigned long long>(nr - 1));
   const int sb = bits_for(static_cast<unsigned long long>(std::max(max_side - 1, 0)));
   const unsigned long long total = ho[nr];
-  const int n_cells = (a.W - 1) * (a.H - 1);
-  if (rb + sb > 32 || total == 0 || total >= (1ull << 31)) return {};
+  if (total == 0 || total >= (1ull << 31) || sb > 20) return {};
   const unsigned n = static_cast<unsigned>(total);
-  auto hold = [](void* q) { return std::unique_ptr<void, void (*)(void*)>(q, [](void* x) { cudaFree(x); }); };
-  // the plan's own memory: start [n_cells + 1] | ent [n]
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const size_t o_ent = al(sizeof(unsigned) * (n_cells + 1)), bytes = o_ent + sizeof(unsigned) * n;
+  auto hold = [](void* q) { return std::unique_ptr<void, void (*)(void*)>(q, [](void* x) { cudaFree(x); }); };
+  unsigned long long* null_keys = nullptr;
+  // per-ray counts and offsets
+  void* small = nullptr;
+  PACT_CUDA_S(cudaMalloc(&small, al(sizeof(unsigned long long) * (nr + 1)) * 2 + al(sizeof(unsigned) * nr)));
+  auto hold_small = hold(small);
+  auto* off = static_cast<unsigned long long*>(small);
+  auto* toff = reinterpret_cast<unsigned long long*>(static_cast<char*>(small) + al(sizeof(unsigned long long) * (nr + 1)));
+  auto* tcnt = reinterpret_cast<unsigned*>(static_cast<char*>(small) + 2 * al(sizeof(unsigned long long) * (nr + 1)));
+  PACT_CUDA_S(cudaMemcpyAsync(off, ho.data(), sizeof(unsigned long long) * nr, cudaMemcpyHostToDevice, s));
+  // 1. the tile size and the per-tile ray lists
+  int T = 0, tile_max = 0, n_tiles = 0;
+  CellTiles ct{};
+  void* tmem = nullptr;  // tile_start [n_tiles + 1] | tile_rays [nt]
+  for (int cand : {16, 8}) {
+    ct = CellTiles{cand, (Wc + cand - 1) / cand, Wc, Hc};
+    const int nti = ct.tx * ((Hc + cand - 1) / cand);
+    cell_steps_kernel<<<div_up(nr, 256), 256, 0, s>>>(p.rec, nr, a.W, a.H, sb, ct, nullptr, nullptr,
+                                                      nullptr, nullptr, tcnt, nullptr);
+    PACT_TRY_S(after_launch(ctx, "cell_steps_kernel"));
+    std::vector<unsigned> hc(nr);
+    PACT_CUDA_S(cudaMemcpyAsync(hc.data(), tcnt, sizeof(unsigned) * nr, cudaMemcpyDeviceToHost, s));
+    PACT_CUDA_S(cudaStreamSynchronize(s));
+    std::vector<unsigned long long> hto(nr);
+    unsigned long long tt = 0;
+    for (int r = 0; r < nr; ++r) {
+      hto[r] = tt;
+      tt += hc[r];
+    }
+    if (tt == 0 || tt >= (1ull << 31)) return {};
+    const unsigned ntc = static_cast<unsigned>(tt);
+    PACT_CUDA_S(cudaMemcpyAsync(toff, hto.data(), sizeof(unsigned long long) * nr, cudaMemcpyHostToDevice, s));
+    size_t ttemp = 0;
+    const int tend = 32 + bits_for(static_cast<unsigned long long>(nti - 1));
+    PACT_CUDA_S(cub::DeviceRadixSort::SortKeys(nullptr, ttemp, null_keys, null_keys, ntc, 0, tend, s));
+    void* tscratch = nullptr;
+    PACT_CUDA_S(cudaMalloc(&tscratch, al(16ull * ntc) + std::max<size_t>(ttemp, 16)));
+    auto hold_ts = hold(tscratch);
+    auto* tkeys = static_cast<unsigned long long*>(tscratch);
+    cell_steps_kernel<<<div_up(nr, 256), 256, 0, s>>>(p.rec, nr, a.W, a.H, sb, ct, nullptr, nullptr,
+                                                      toff, tkeys, nullptr, nullptr);
+    PACT_TRY_S(after_launch(ctx, "cell_steps_kernel"));
+    PACT_CUDA_S(cub::DeviceRadixSort::SortKeys(static_cast<char*>(tscratch) + al(16ull * ntc), ttemp,
+                                               tkeys, tkeys + ntc, ntc, 0, tend, s));
+    void* tm = nullptr;
+    const size_t o_rays = al(sizeof(unsigned) * (nti + 1));
+    PACT_CUDA_S(cudaMalloc(&tm, o_rays + sizeof(unsigned) * ntc));
+    auto hold_tm = hold(tm);
+    auto* ts = static_cast<unsigned*>(tm);
+    group_bounds_kernel<<<div_up(static_cast<int>(ntc), 256), 256, 0, s>>>(
+        tkeys + ntc, ntc, nti, ts, reinterpret_cast<unsigned*>(static_cast<char*>(tm) + o_rays));
+    PACT_TRY_S(after_launch(ctx, "group_bounds_kernel"));
+    std::vector<unsigned> hts(nti + 1);
+    PACT_CUDA_S(cudaMemcpyAsync(hts.data(), ts, sizeof(unsigned) * (nti + 1), cudaMemcpyDeviceToHost, s));
+    PACT_CUDA_S(cudaStreamSynchronize(s));
+    int mx = 0;
+    for (int t = 0; t < nti; ++t) mx = std::max(mx, static_cast<int>(hts[t + 1] - hts[t]));
+    if (static_cast<size_t>(mx) * (sizeof(float4) + sizeof(float)) <= kCellSmemMax &&
+        bits_for(static_cast<unsigned long long>(std::max(mx - 1, 0))) + sb <= 32) {
+      T = cand;
+      tile_max = std::max(mx, 1);
+      n_tiles = nti;
+      tmem = hold_tm.release();
+      break;
+    }
+  }
+  if (!T) return {};
+  auto hold_tmem = hold(tmem);
+  // 2. the step entries, sorted by (tile-major cell, ray, step), then localised
+  const int n_cells = n_tiles * T * T;
+  const size_t o_ent = al(sizeof(unsigned) * (n_cells + 1)), o_geo = al(o_ent + sizeof(unsigned) * n),
+               bytes = o_geo + sizeof(float4) * nr;
   void* mem = nullptr;
   PACT_CUDA_S(cudaMalloc(&mem, bytes));
   auto hold_mem = hold(mem);
   char* b = static_cast<char*>(mem);
   auto* start = reinterpret_cast<unsigned*>(b);
   auto* ent = reinterpret_cast<unsigned*>(b + o_ent);
-  // scratch: offsets, keys (x2 for the sort), cub temp
+  auto* geo = reinterpret_cast<float4*>(b + o_geo);
   const int end_bit = 32 + bits_for(static_cast<unsigned long long>(n_cells - 1));
   size_t temp = 0;
-  unsigned long long* null_keys = nullptr;
   PACT_CUDA_S(cub::DeviceRadixSort::SortKeys(nullptr, temp, null_keys, null_keys, n, 0, end_bit, s));
-  const size_t o_keys = al(sizeof(unsigned long long) * nr), o_tmp = al(o_keys + 16ull * n);
   void* scratch = nullptr;
-  PACT_CUDA_S(cudaMalloc(&scratch, o_tmp + std::max<size_t>(temp, 16)));
+  PACT_CUDA_S(cudaMalloc(&scratch, al(16ull * n) + std::max<size_t>(temp, 16)));
   auto hold_scratch = hold(scratch);
-  auto* off = static_cast<unsigned long long*>(scratch);
-  auto* keys = reinterpret_cast<unsigned long long*>(static_cast<char*>(scratch) + o_keys);
-  void* tmp = static_cast<char*>(scratch) + o_tmp;
-  PACT_CUDA_S(cudaMemcpyAsync(off, ho.data(), sizeof(unsigned long long) * nr, cudaMemcpyHostToDevice, s));
-  cell_steps_kernel<<<div_up(nr, 256), 256, 0, s>>>(p.rec, nr, a.W, a.H, sb, off, keys);
+  auto* keys = static_cast<unsigned long long*>(scratch);
+  cell_steps_kernel<<<div_up(nr, 256), 256, 0, s>>>(p.rec, nr, a.W, a.H, sb, ct, off, keys, nullptr,
+                                                    nullptr, nullptr, geo);
   PACT_TRY_S(after_launch(ctx, "cell_steps_kernel"));
-  PACT_CUDA_S(cub::DeviceRadixSort::SortKeys(tmp, temp, keys, keys + n, n, 0, end_bit, s));
-  cell_bounds_kernel<<<div_up(static_cast<int>(n), 256), 256, 0, s>>>(keys + n, n, n_cells, start, ent);
-  PACT_TRY_S(after_launch(ctx, "cell_bounds_kernel"));
+  PACT_CUDA_S(cub::DeviceRadixSort::SortKeys(static_cast<char*>(scratch) + al(16ull * n), temp, keys,
+                                             keys + n, n, 0, end_bit, s));
+  group_bounds_kernel<<<div_up(static_cast<int>(n), 256), 256, 0, s>>>(keys + n, n, n_cells, start, nullptr);
+  PACT_TRY_S(after_launch(ctx, "group_bounds_kernel"));
+  auto* tstart = static_cast<unsigned*>(tmem);
+  auto* trays = reinterpret_cast<unsigned*>(static_cast<char*>(tmem) + al(sizeof(unsigned) * (n_tiles + 1)));
+  cell_localize_kernel<<<div_up(static_cast<int>(n), 256), 256, 0, s>>>(keys + n, n, sb, T, tstart,
+                                                                       trays, ent);
+  PACT_TRY_S(after_launch(ctx, "cell_localize_kernel"));
   PACT_CUDA_S(cudaStreamSynchronize(s));  // the host offsets and the scratch die here
   p.cell_mem = hold_mem.release();
+  p.tile_mem = hold_tmem.release();
   p.cell_start = start;
   p.cell_ent = ent;
+  p.cell_geo = geo;
+  p.tile_start = tstart;
+  p.tile_rays = trays;
   p.cell_sb = sb;
+  p.cell_t = T;
+  p.tile_max = tile_max;
+  p.n_tiles = n_tiles;
   return {};
 }
 
@@ -1236,6 +1388,11 @@ static void set_cell_args(RayArgs& a, const RayPlanData& d) {
   a.cell_start = d.cell_start;
   a.cell_ent = d.cell_ent;
   a.cell_sb = d.cell_sb;
+  a.tile_start = d.tile_start;
+  a.tile_rays = d.tile_rays;
+  a.cell_geo = d.cell_geo;
+  a.cell_t = d.cell_t;
+  a.tile_max = d.tile_max;
   a.n_gen_items = d.n_gen;
   a.n_int_items = d.n_int;
 }
@@ -1333,7 +1490,7 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
   const size_t n_cells = cells ? static_cast<size_t>(a.W - 1) * (a.H - 1) : 0;
   const size_t fix_bytes = sizeof(unsigned long long) * (npx + rep_n + 2);
   const size_t gsc_off = (fix_bytes + 255) & ~size_t(255);
-  const size_t cell_off = (gsc_off + 32 * static_cast<size_t>(cells ? a.n_rays : 0) + 255) & ~size_t(255);
+  const size_t cell_off = (gsc_off + sizeof(float) * (cells ? a.n_rays : 0) + 255) & ~size_t(255);
   const size_t bytes = cell_off + 4 * sizeof(unsigned long long) * n_cells;
   pact_scratch& sc = ctx->scratch[kScratchRayBorder];
   const void* before = sc.ptr;
@@ -1362,9 +1519,15 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
       PACT_TRY_S(after_launch(ctx, "ray_backward_plan_kernel"));
     }
     if (cells) {
-      const int grid = div_up(static_cast<int>(n_cells), 256 / LPC);
-      cell_gather_kernel<<<grid, 256, 0, ctx->stream>>>(a, reinterpret_cast<const float4*>(gsc), stats,
-                                                        cell_sums);
+      const int T = a.cell_t, n_tiles = ((a.W - 1 + T - 1) / T) * ((a.H - 1 + T - 1) / T);
+      const size_t cs = static_cast<size_t>(a.tile_max) * (sizeof(float4) + sizeof(float));
+      if (T == 16) {
+        PACT_TRY_S(smem_optin(cell_gather_kernel<16>, cs));
+        cell_gather_kernel<16><<<n_tiles, kCellThreads, cs, ctx->stream>>>(a, gsc, stats, cell_sums);
+      } else {
+        PACT_TRY_S(smem_optin(cell_gather_kernel<8>, cs));
+        cell_gather_kernel<8><<<n_tiles, kCellThreads, cs, ctx->stream>>>(a, gsc, stats, cell_sums);
+      }
       PACT_TRY_S(after_launch(ctx, "cell_gather_kernel"));
     }
   } else {
