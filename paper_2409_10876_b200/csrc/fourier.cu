@@ -42,6 +42,7 @@ namespace {
 struct HostFourier {
   std::vector<char> bytes;
   size_t o_kmag, o_idx, o_frac, o_mirror, o_dp, o_start, o_slot, o_rho;
+  int fin_span = 0;
   bool uniform;
 };
 
@@ -103,6 +104,9 @@ std::shared_ptr<const HostFourier> build_host_fourier(int P, double pitch, int A
     start[idx[b].z + 1]++;
   }
   for (int a = 0; a < A; ++a) start[a + 1] += start[a];
+  int fin_span = 0;
+  for (int a0 = 0; a0 < A; a0 += kFinishAngles)
+    fin_span = std::max(fin_span, start[std::min(a0 + kFinishAngles, A)] - start[a0 > 0 ? a0 - 1 : 0]);
   std::vector<int2> slot(P2);
   {
     std::vector<int> fill(start.begin(), start.end() - 1);
@@ -137,6 +141,7 @@ std::shared_ptr<const HostFourier> build_host_fourier(int P, double pitch, int A
   hf->o_slot = o_slot;
   hf->o_rho = o_rho;
   hf->uniform = uniform;
+  hf->fin_span = fin_span;
   return hf;
 }
 
@@ -202,6 +207,7 @@ Status fourier_table(pact_ctx* ctx, FourierTable& t, int P, double pitch, int A,
   t.tab.sstart = reinterpret_cast<const int*>(d + hf->o_start);
   t.tab.slot = reinterpret_cast<const int2*>(d + hf->o_slot);
   t.tab.rho = hf->uniform ? reinterpret_cast<const float2*>(d + hf->o_rho) : nullptr;
+  t.tab.fin_span = hf->fin_span;
   return {};
 }
 
@@ -594,25 +600,160 @@ __global__ void __launch_bounds__(2 * LB) loss_bins_kernel(FourierTab t, const f
 // l % (32 / NS), delay group l / (32 / NS); a group's lanes read consecutive
 // bins of one delay row (coalesced 128-B lines).  The per-bin chain is
 // bin_chain_real's closed form with the group sums combined by fixed xor
-// shuffles.  Nyquist bins (even P) are not evaluated here: their lanes copy
-// their spectra into the compact exchange layout ynyq [patch][slot][K] so
-// that kernel A' reads them contiguously instead of one sector per bin.
+// shuffles.  Nyquist bins' lanes idle; for even P the Nyquist pairs run in
+// the blocks past the ordinary chunks (nyq_pairs).
+//
+// Even P: half spectrum.  The patch stack is real, so Y(-k) = conj(Y(k)); with
+// H(-k) = conj(H(k)) (transfer_stack, aberration.hpp:236-265) the bin -k has
+// the same c_j, conj(X'), conj(r_j), the same loss term and the same (1/2)
+// dL/dwbar as k, at the same two wavefront stencils (angle(k) and
+// angle(k) + pi swap).  Kernel A therefore reads only rows 0 .. P/2 of each
+// spectrum: every ordinary bin k there (row 0: 0 < bx < P/2) counts twice in
+// the loss and writes its shares to its own and to -k's slots; the Nyquist
+// pairs run in the blocks past the ordinary chunks (nyq_pairs).  Half of Y's
+// HBM traffic.
+//
+// Nyquist bins (even P) come in conjugate pairs (b, m = -b) -- the Nyquist
+// row and column, three of them self-paired -- and the reference symmetrises
+// H over each pair (conj_symmetrize_nyquist, aberration.hpp:203-218) and the
+// pullback of dL/dH alike (optimize.hpp:306-308).  With Y(m) = conj(Y(b)) the
+// pair's unsymmetrised gradients are g and conj(g), so the symmetrised
+// gradient is g at b and conj(g) at m (Re g for a self-paired bin): one unit
+// of NS lanes evaluates the pair -- no exchange, no second kernel.
+template <int NS, int JPL>
+__device__ __forceinline__ void nyq_pairs(const FourierTab& t, const float2* __restrict__ Y_all,
+                                          const float* __restrict__ w_all, float eps_m, float scale,
+                                          bool impl, float2* __restrict__ gbuf, double* s_red,
+                                          double* __restrict__ loss_out, int patch, int u0) {
+  constexpr int K = NS * JPL;
+  const int P = t.P, P2 = t.P2, hp = P / 2;
+  const int unit = u0 + static_cast<int>(threadIdx.x) / NS, q = threadIdx.x % NS;
+  const bool valid = unit <= P;  // P + 1 pairs
+  const int uu = valid ? unit : 0;
+  int b, m;
+  if (uu <= hp) {  // Nyquist row: (P/2, bx) with (P/2, P - bx)
+    b = hp * P + uu;
+    m = hp * P + (P - uu) % P;
+  } else {  // Nyquist column: (by, P/2) with (P - by, P/2), by < P/2
+    const int by = uu - hp - 1;
+    b = by * P + hp;
+    m = ((P - by) % P) * P + hp;
+  }
+  const bool self = b == m;
+  const float* w = w_all + static_cast<size_t>(patch) * t.A;
+  float2 e1b, e2b, e1m, e2m;
+  bin_phases(t, w, b, e1b, e2b);
+  bin_phases(t, w, m, e1m, e2m);
+  const float k = t.kmag[b];
+  const int j0 = q * JPL;
+  const bool walk = t.rho != nullptr;
+  const float2 rb = walk ? t.rho[b] : make_float2(1.f, 0.f);
+  const float2 rm = walk ? t.rho[m] : make_float2(1.f, 0.f);
+  const float2 db0 = t.dp[j0 * P2 + b], dm0 = t.dp[j0 * P2 + m];
+  auto next = [&](int j, float2& db, float2& dm) {
+    if (walk) {
+      db = cmul(db, rb);
+      dm = cmul(dm, rm);
+    } else if (j + 1 < K) {
+      db = t.dp[(j + 1) * P2 + b];
+      dm = t.dp[(j + 1) * P2 + m];
+    }
+  };
+  auto h_sym = [&](float2 db, float2 dm) {  // (h_b + conj h_m) / 2
+    const float2 hb = h_of(db, e1b, e2b), hm = h_of(dm, e1m, e2m);
+    return make_float2(0.5f * (hb.x + hm.x), 0.5f * (hb.y - hm.y));
+  };
+  auto usum = [&](float v) {  // the unit's NS consecutive lanes
+#pragma unroll
+    for (int o = 1; o < NS; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
+  // (the spectra are read in both passes, not held: registers stay with the
+  // ordinary chunks' budget)
+  const float2* Y = Y_all + (static_cast<size_t>(patch) * K + j0) * P2 + b;
+  float nx = 0.f, ny = 0.f, dd = 0.f;
+  {
+    float2 db = db0, dm = dm0;
+#pragma unroll 4
+    for (int u = 0; u < JPL; ++u) {
+      const float2 h = h_sym(db, dm);
+      const float2 c = cmulc(h, __ldg(Y + static_cast<size_t>(u) * P2));
+      nx += c.x;
+      ny += c.y;
+      dd += h.x * h.x + h.y * h.y;
+      next(j0 + u, db, dm);
+    }
+  }
+  BinLoss L;
+  L.wk = k * scale;
+  L.den = eps_m + usum(dd);
+  L.inv = L.den > 0.f ? 1.f / L.den : 0.f;
+  const float2 num = make_float2(usum(nx), usum(ny));
+  L.x = make_float2(num.x * L.inv, num.y * L.inv);
+  L.G = make_float2(num.x * (eps_m * L.inv), -num.y * (eps_m * L.inv));
+  L.gx = L.G.x * L.x.x - L.G.y * L.x.y;
+  float acc = 0.f, G1b = 0.f, G2b = 0.f, G1m = 0.f, G2m = 0.f;
+  {
+    float2 db = db0, dm = dm0;
+#pragma unroll 4
+    for (int u = 0; u < JPL; ++u) {
+      const float2 h = h_sym(db, dm), y = __ldg(Y + static_cast<size_t>(u) * P2);
+      const float2 hx = cmul(h, L.x);
+      const float2 r = make_float2(y.x - hx.x, y.y - hx.y);
+      acc += r.x * r.x + r.y * r.y;
+      const float2 g = bin_grad(L, h, y, impl);
+      pullback(g, db, e1b, e2b, k, G1b, G2b);
+      pullback(conjf2(g), dm, e1m, e2m, k, G1m, G2m);
+      next(j0 + u, db, dm);
+    }
+  }
+  acc = usum(acc);
+  G1b = usum(G1b);
+  G2b = usum(G2b);
+  G1m = usum(G1m);
+  G2m = usum(G2m);
+  const bool live = valid && L.wk != 0.f;
+  if (self) {  // symmetrised gradient Re g: (pullback(g) + pullback(conj g)) / 2
+    G1b = 0.5f * (G1b + G1m);
+    G2b = 0.5f * (G2b + G2m);
+  }
+  if (valid && q == 0) {
+    float2* ub = gbuf + static_cast<size_t>(patch) * 2 * P2;
+    put_g(t, ub, b, live ? G1b : 0.f, live ? G2b : 0.f);
+    if (!self) put_g(t, ub, m, live ? G1m : 0.f, live ? G2m : 0.f);
+  }
+  const double value = live && q == 0 ? (self ? 1.0 : 2.0) * static_cast<double>(L.wk) * acc : 0.0;
+  block_sum_store(value, s_red, loss_out);
+}
+
 template <int NS, int JPL>
 __global__ void __launch_bounds__(256, 4) loss_reg_kernel(FourierTab t, const float2* __restrict__ Y_all,
                                                        const float* __restrict__ w_all, float eps_m,
                                                        float scale, int implicit,
                                                        float2* __restrict__ gbuf,
-                                                       float2* __restrict__ ynyq,
-                                                       double* __restrict__ loss_part, int n_parts) {
+                                                       double* __restrict__ loss_part, int n_parts,
+                                                       int n_patches) {
   constexpr int BPW = 32 / NS, BPB = 8 * BPW, K = NS * JPL;
   __shared__ double s_red[8];
-  const int P2 = t.P2, lane = threadIdx.x & 31;
+  const int P2 = t.P2, P = t.P, lane = threadIdx.x & 31;
+  const bool half = (P & 1) == 0;
+  const int n_bins = half ? (P / 2 + 1) * P : P2;  // bins this kernel reads
   const int grp = lane / BPW, bi = lane - grp * BPW;
-  const int chunks = (P2 + BPB - 1) / BPB;
-  const int patch = blockIdx.x / chunks, cb = blockIdx.x - patch * chunks;
+  const int chunks = (n_bins + BPB - 1) / BPB;
+  // the Nyquist pair blocks first (their chains are the longest), then the chunks
+  constexpr int UPB = 256 / NS;
+  const int nb = half ? (P + 1 + UPB - 1) / UPB : 0;
+  if (static_cast<int>(blockIdx.x) < n_patches * nb) {
+    const int patch = blockIdx.x / nb, part = blockIdx.x - patch * nb;
+    nyq_pairs<NS, JPL>(t, Y_all, w_all, eps_m, scale, implicit != 0, gbuf, s_red,
+                       loss_part + patch * n_parts + chunks + part, patch, part * UPB);
+    return;
+  }
+  const int blk = blockIdx.x - n_patches * nb;
+  const int patch = blk / chunks, cb = blk - patch * chunks;
   const int b0 = cb * BPB + (threadIdx.x >> 5) * BPW + bi;
-  const bool valid = b0 < P2;
-  const int b = valid ? b0 : P2 - 1;
+  const bool valid = b0 < n_bins;
+  const int b = valid ? b0 : n_bins - 1;
   const int j0 = grp * JPL;
   // the bin's table entries and wavefront samples first (a dependent
   // idx -> w chain of L2 hits), so they are back before the spectra from HBM
@@ -631,11 +772,6 @@ __global__ void __launch_bounds__(256, 4) loss_reg_kernel(FourierTab t, const fl
     for (int o = BPW; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
   };
-  if (m >= 0 && valid) {  // Nyquist bin: hand its spectra to kernel A'
-    float2* dst = ynyq + (static_cast<size_t>(patch) * (2 * t.P - 1) + nyq_slot(b, t.P)) * K + j0;
-#pragma unroll
-    for (int u = 0; u < JPL; ++u) dst[u] = y[u];
-  }
   const float wk = k * scale;
   const float w1 = (1.f - fr.x) * wa + fr.x * wb;
   const float w2 = (1.f - fr.y) * wc + fr.y * wd;
@@ -686,12 +822,17 @@ __global__ void __launch_bounds__(256, 4) loss_reg_kernel(FourierTab t, const fl
   }
   acc = gsum(acc);
   gs = gsum(gs);
-  const bool ordinary = valid && m < 0 && wk != 0.f;
-  if (grp == 0 && valid && m < 0) {
+  // half spectrum: row 0 keeps 0 < bx < P/2; the partner -k of every kept bin
+  const int by = b / P, bx = b - by * P;
+  const bool kept = valid && m < 0 && !(half && by == 0 && bx > P / 2);
+  const bool ordinary = kept && wk != 0.f;
+  if (grp == 0 && kept) {
     const float G = ordinary ? -wk * k * gs : 0.f;  // (1/2) dL/dwbar, for w1 and for w2
-    put_g(t, gbuf + static_cast<size_t>(patch) * 2 * P2, b, G, G);
+    float2* u = gbuf + static_cast<size_t>(patch) * 2 * P2;
+    put_g(t, u, b, G, G);
+    if (half) put_g(t, u, ((P - by) % P) * P + (P - bx) % P, G, G);
   }
-  const double value = ordinary && grp == 0 ? static_cast<double>(wk) * acc : 0.0;
+  const double value = ordinary && grp == 0 ? (half ? 2.0 : 1.0) * static_cast<double>(wk) * acc : 0.0;
   block_sum_store(value, s_red, loss_part + patch * n_parts + cb);
 }
 
@@ -764,14 +905,30 @@ __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const 
   const float2* Y = Y_all + static_cast<size_t>(patch) * K * P2;
   // the slots' spectra: from the compact [slot][K] copy kernel A made, or
   // (other kernel A forms) gathered from Y, eight loads in flight per thread
+  // (kernel A's half-spectrum form copies the Nyquist bins of rows 0 .. P/2:
+  // a column slot below the Nyquist row, by > P/2, reads conj of its
+  // partner's, by' = P - by: Y(-k) = conj(Y(k)) for the real patch stack)
   const float2* Yc = ynyq ? ynyq + static_cast<size_t>(patch) * S * K : nullptr;
+  const int half = t.P / 2;
+  auto yc = [&](int slot, int j) {
+    if (slot >= t.P + half) {  // column bin by = slot - P + 1 > P/2
+      const float2 v = Yc[static_cast<size_t>(t.P + t.P - (slot - t.P + 1)) * K + j];
+      return make_float2(v.x, -v.y);
+    }
+    return Yc[static_cast<size_t>(slot) * K + j];
+  };
   const int kshift = (K & (K - 1)) == 0 ? __ffs(K) - 1 : -1;  // e / K as a shift
   for (int e0 = threadIdx.x; Yc && stage_y && e0 < K * S; e0 += 8 * blockDim.x) {
     float2 v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int e = e0 + u * blockDim.x;
-      v[u] = e < K * S ? Yc[e] : make_float2(0.f, 0.f);
+      if (e < K * S) {
+        const int q = kshift >= 0 ? e >> kshift : e / K;
+        v[u] = yc(q, e - q * K);
+      } else {
+        v[u] = make_float2(0.f, 0.f);
+      }
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -804,8 +961,7 @@ __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const 
   const float k = t.kmag[b];
   const bool live = active && k * scale != 0.f;
   auto y_of = [&](int j) {
-    return stage_y ? s_y[j * S + slot]
-                   : (Yc ? Yc[static_cast<size_t>(slot) * K + j] : Y[static_cast<size_t>(j) * P2 + b]);
+    return stage_y ? s_y[j * S + slot] : (Yc ? yc(slot, j) : Y[static_cast<size_t>(j) * P2 + b]);
   };
   auto group_sum = [&](float v) {
 #pragma unroll
@@ -891,32 +1047,50 @@ __global__ void __launch_bounds__(1024) loss_nyquist_kernel(FourierTab t, const 
 // Kernel B: dL/dw of every (patch, angle) from the angle-sorted slots
 // (FourierTab::slot): the .x shares of angle a's segment plus the .y shares of
 // angle a - 1's, each a contiguous run summed in order (deterministic); the
-// angle-0 thread also sums the patch's loss partials.
-__global__ void __launch_bounds__(256) loss_finish_kernel(FourierTab t, const float2* __restrict__ u_all,
-                                                          const double* __restrict__ loss_part,
-                                                          int n_parts, int n_patches,
-                                                          double* __restrict__ loss_out,
-                                                          float* __restrict__ dw_out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_patches * t.A) return;
-  const int patch = i / t.A, a = i - patch * t.A, am = a == 0 ? t.A - 1 : a - 1;
+// angle-0 thread also sums the patch's loss partials.  A block takes
+// kFinishAngles angles of one patch and first stages their slot span in
+// shared memory with coalesced loads (the runs are ~2 P^2 / A slots each).
+__global__ void __launch_bounds__(kFinishAngles) loss_finish_kernel(
+    FourierTab t, const float2* __restrict__ u_all, const double* __restrict__ loss_part, int n_parts,
+    int n_patches, double* __restrict__ loss_out, float* __restrict__ dw_out) {
+  extern __shared__ float2 s_u[];
+  const int A = t.A, groups = (A + kFinishAngles - 1) / kFinishAngles;
+  const int patch = blockIdx.x / groups, a0 = (blockIdx.x - patch * groups) * kFinishAngles;
+  const int a1 = min(a0 + kFinishAngles, A);
+  const int lo = __ldg(t.sstart + (a0 > 0 ? a0 - 1 : 0)), hi = __ldg(t.sstart + a1);
   const float2* u = u_all + static_cast<size_t>(patch) * 2 * t.P2;
+  for (int s0 = lo + threadIdx.x; s0 < hi; s0 += 4 * kFinishAngles) {
+    float2 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int s = s0 + q * kFinishAngles;
+      v[q] = s < hi ? __ldcs(u + s) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (s0 + q * kFinishAngles < hi) s_u[s0 + q * kFinishAngles - lo] = v[q];
+  }
+  __syncthreads();
+  const int a = a0 + threadIdx.x;
+  if (a >= A) return;
+  const int am = a == 0 ? A - 1 : a - 1;
   // eight partial sums (element s - start goes to partial (s - start) % 8),
-  // combined in a fixed tree: eight loads in flight, deterministic
+  // combined in a fixed tree
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   const int s0 = __ldg(t.sstart + a), s1 = __ldg(t.sstart + a + 1);
   for (int s = s0; s < s1; s += 8) {
 #pragma unroll
     for (int q = 0; q < 8; ++q)
-      if (s + q < s1) acc[q] += u[s + q].x;
+      if (s + q < s1) acc[q] += s_u[s + q - lo].x;
   }
   const int r0 = __ldg(t.sstart + am), r1 = __ldg(t.sstart + am + 1);
   for (int s = r0; s < r1; s += 8) {
 #pragma unroll
     for (int q = 0; q < 8; ++q)
-      if (s + q < r1) acc[q] += u[s + q].y;
+      if (s + q < r1) acc[q] += a == 0 ? u[s + q].y : s_u[s + q - lo].y;  // angle A - 1 wraps
   }
-  dw_out[i] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  dw_out[static_cast<size_t>(patch) * A + a] =
+      ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
   if (a == 0) loss_out[patch] = patch_loss(loss_part, patch, n_parts);
 }
 
@@ -960,7 +1134,7 @@ Status launch_transfer_stack(pact_ctx* ctx, const FourierTab& t, const float* w,
 
 // Kernel A of the register form for (NS, JPL) with K = NS * JPL, or null.
 using LossRegFn = void (*)(FourierTab, const float2*, const float*, float, float, int, float2*,
-                           float2*, double*, int);
+                           double*, int, int);
 LossRegFn loss_reg_for(int K, int& ns) {
   // PACT_LOSS_STAGED=1 selects the shared-memory staged kernel A (comparisons)
   static const bool staged = [] {
@@ -985,8 +1159,11 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
   int ns = 0;
   const LossRegFn reg = loss_reg_for(t.K, ns);
   const int bpb = reg ? 8 * 32 / ns : LB;  // bins per kernel-A block
-  const int chunks = div_up(t.P2, bpb);
-  const int nyq_chunks = t.P % 2 == 0 ? 1 : 0;
+  // the register form reads rows 0 .. P/2 only for even P (half spectrum)
+  const bool even = t.P % 2 == 0;
+  const int chunks = div_up(reg && even ? (t.P / 2 + 1) * t.P : t.P2, bpb);
+  // Nyquist: the register form's pair blocks (256 / ns units each), else kernel A'
+  const int nyq_chunks = !even ? 0 : reg ? div_up(t.P + 1, 256 / ns) : 1;
   const int n_parts = chunks + nyq_chunks;  // per-patch loss partials, summed in order
   // scratch: Nyquist dL/dH exchange [patch][2P-1][K] | compact Nyquist spectra
   // [patch][2P-1][K] | (G1, G2) [patch][P2] | chunk losses
@@ -1003,8 +1180,8 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
   double* part = reinterpret_cast<double*>(gbuf + n_g);
   const float eps_m = static_cast<float>(eps * t.K), sc = static_cast<float>(scale);
   if (reg) {
-    reg<<<n_patches * chunks, 256, 0, ctx->stream>>>(t, Y, w, eps_m, sc, implicit, gbuf, ynyq,
-                                                     part, n_parts);
+    reg<<<n_patches * (chunks + (even ? nyq_chunks : 0)), 256, 0, ctx->stream>>>(
+        t, Y, w, eps_m, sc, implicit, gbuf, part, n_parts, n_patches);
   } else if (t.P2 % LB == 0 && t.K * LB * 8 <= 96 * 1024) {
     const size_t stage = sizeof(float) * (2 * t.K * LB + ((t.A + 3) & ~3));
     const size_t smem_bins = 2 * stage;
@@ -1021,7 +1198,7 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
         t, Y, w, eps_m, sc, implicit, gbuf, part, n_parts);
   }
   PACT_TRY_S(after_launch(ctx, reg ? "loss_reg_kernel" : "loss_bins_kernel"));
-  if (t.P % 2 == 0) {
+  if (even && !reg) {
     const int S = 2 * t.P - 1, nt = div_up(S * kTps, 32) * 32;
     if (nt > 1024) return validation("fused loss: patch size too large for the Nyquist kernel");
     const size_t plane = sizeof(float2) * t.K * S, base = sizeof(float) * ((t.A + 1) & ~1);
@@ -1030,12 +1207,13 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
     const size_t smem_nyq = base + (stage_y + stage_g) * plane;
     PACT_TRY_S(smem_optin(loss_nyquist_kernel, smem_nyq));
     loss_nyquist_kernel<<<n_patches, nt, smem_nyq, ctx->stream>>>(
-        t, Y, w, eps_m, sc, implicit, reg ? ynyq : nullptr, nyq, gbuf, part, n_parts, chunks,
-        stage_y, stage_g);
+        t, Y, w, eps_m, sc, implicit, nullptr, nyq, gbuf, part, n_parts, chunks, stage_y, stage_g);
     PACT_TRY_S(after_launch(ctx, "loss_nyquist_kernel"));
   }
-  loss_finish_kernel<<<div_up(n_patches * t.A, 256), 256, 0, ctx->stream>>>(t, gbuf, part, n_parts,
-                                                                            n_patches, loss, dw);
+  const size_t fin_smem = sizeof(float2) * std::max(t.fin_span, 1);
+  PACT_TRY_S(smem_optin(loss_finish_kernel, fin_smem));
+  loss_finish_kernel<<<n_patches * div_up(t.A, kFinishAngles), kFinishAngles, fin_smem, ctx->stream>>>(
+      t, gbuf, part, n_parts, n_patches, loss, dw);
   return after_launch(ctx, "loss_finish_kernel");
 }
 

@@ -29,7 +29,11 @@ struct FourierTab {
   // contiguous reads, fixed order.
   const int2* slot = nullptr;     // [P2]
   const int* sstart = nullptr;    // [A + 1]
+  // most slots any group of kFinishAngles angles reads (their .x slots and the
+  // .y slots of the angle before the group): the finish kernel's smem stage
+  int fin_span = 0;
 };
+constexpr int kFinishAngles = 128;
 
 // Host-built table (fp64 reference formulas, stored fp32) + its device copy.
 struct FourierTable {
