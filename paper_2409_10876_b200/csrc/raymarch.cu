@@ -83,6 +83,15 @@ __device__ __forceinline__ Border load_border(const RayArgs& a, float* sm) {
   return b;
 }
 
+// a / b as __fdividef(a, b) computes it for a normal b (the ray integrands'
+// denominators are SOS values or their squares): one MUFU.RCP and a multiply,
+// without __fdividef's guard for |b| > 2^126.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Fixed-point deposit target: int64 multiples of 2^-S (see the header).
 // v * 2^S is exact in fp32 (a power-of-two scale; |v| 2^S < 2^62 by the
 // bound), so one FMUL + F2I.S64 gives the same integer as an fp64 product.
@@ -524,7 +533,7 @@ __global__ void __launch_bounds__(256) wavefront_plan_kernel(RayArgs a) {
         const float d = interior_d(a.tex, fmaf(static_cast<float>(i), rr.dfx, rr.fxs),
                                    fmaf(static_cast<float>(i), rr.dfy, rr.fys), W, H, ax, ay, ix,
                                    iy);
-        acc += __fdividef(d, v0 + d);
+        acc += d * rcp_approx(v0 + d);
       }
     } else if (kind == kItemSide) {
       // border line: one loop for both orientations; the line is a slice of
@@ -536,7 +545,7 @@ __global__ void __launch_bounds__(256) wavefront_plan_kernel(RayArgs a) {
         const int q = min(static_cast<int>(f), sl.qmax);
         const float c0 = s_border[sl.off + q];
         const float d = fmaf(f - q, s_border[sl.off + q + 1] - c0, c0);
-        acc += __fdividef(d, v0 + d);
+        acc += d * rcp_approx(v0 + d);
       }
     } else {
       acc = march_forward_generic<true>(a, bd, rec_pixels(rr), rr.n, v0);
@@ -627,18 +636,43 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
       // the smem border's layout
       const SideLine sl = side_line(rec_regimes(rr), rec_pixels(rr), W, H);
       const Fix dst = rep + sl.off;
+      // The carry of LineAcc without its branches: a step moves the cell by
+      // at most one (|df| <= 1 px per step; larger jumps take LineAcc::move),
+      // so the eviction is a select and one predicated atomic.
       LineAcc line;
+      line.q = min(static_cast<int>(fmaf(static_cast<float>(lo), sl.df, sl.fs)), sl.qmax);
+      float b0 = 0.f, b1 = 0.f;
+      int lq = line.q;
       for (int i = lo; i < hi; ++i) {
         const float f = fmaf(static_cast<float>(i), sl.df, sl.fs);
         const int q = min(static_cast<int>(f), sl.qmax);
         const float fa = f - q, c0 = s_border[sl.off + q];
         const float v = v0 + fmaf(fa, s_border[sl.off + q + 1] - c0, c0);
-        const float gv = __fdividef(gscale, v * v);
-        line.move(dst, q, 1, 0);
+        const float gv = gscale * rcp_approx(v * v);
+        const int dq = q - lq;
+        if (dq > 1 || dq < -1) {  // rare: the general move
+          line.q = lq;
+          line.b0 = b0;
+          line.b1 = b1;
+          line.move(dst, q, 1, 0);
+          b0 = line.b0;
+          b1 = line.b1;
+        } else {
+          const bool up = dq == 1, dn = dq == -1;
+          const float ev = up ? b0 : (dn ? b1 : 0.f);
+          if (ev != 0.f && !RAY_NO_LINE_ATOM) (dst + (up ? lq : lq + 1)).add(ev);
+          const float n0 = up ? b1 : (dn ? 0.f : b0), n1 = up ? 0.f : (dn ? b0 : b1);
+          b0 = n0;
+          b1 = n1;
+        }
+        lq = q;
         const float g1 = gv * fa;
-        line.b0 += gv - g1;
-        line.b1 += g1;
+        b0 += gv - g1;
+        b1 += g1;
       }
+      line.q = lq;
+      line.b0 = b0;
+      line.b1 = b1;
       line.flush(dst, 1, 0);
     } else {
       march_backward_generic<true>(a, bd, rec_pixels(rr), rr.n, v0, gscale, grad);
@@ -859,12 +893,6 @@ __device__ __forceinline__ float cell_sum(float v) {  // fixed xor tree over the
 #pragma unroll
   for (int o = LPC / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
-}
-
-__device__ __forceinline__ float rcp_approx(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
 }
 
 // One block (kCellThreads) per tile of T x T cells; dynamic smem: tile_max ray
