@@ -4,10 +4,10 @@
 // the reference conventions (fft.hpp:86-115): forward e^{-i}, unscaled;
 // inverse e^{+i}, scaled by 1/(w h); rows first, then columns.
 //
-// One CTA per transform; the P x P complex tile lives in shared memory
-// (32 KB at P = 64, 128 KB at P = 128).  Power-of-two P uses an in-place
-// radix-2 Cooley-Tukey with fp64-accurate fp32 twiddles; other sizes use the
-// direct DFT like the reference.  The patch gather is fused into the load
+// P = 64 and P = 128 run register-resident radix-4 transforms (below); other
+// sizes one CTA per transform with the P x P complex tile in shared memory:
+// power-of-two P an in-place radix-2 Cooley-Tukey with fp64-accurate fp32
+// twiddles, other sizes the direct DFT like the reference.  The patch gather is fused into the load
 // (no separate crop pass) and the inverse keeps only the real part.
 #include <cmath>
 #include <cstdlib>
@@ -236,6 +236,101 @@ __global__ void __launch_bounds__(64) patch_ifft64_real_kernel(const float2* __r
   for (int y = 0; y < 64; ++y) o[y * 64] = sr[y * 65 + c] * inv;
 }
 
+// ---- P = 128: two threads per 128-point line (radix-2 over the 64-point
+// register DFT) ------------------------------------------------------------
+// X[k] = E[k] + w^k O[k], X[k + 64] = E[k] - w^k O[k] with E, O the 64-point
+// DFTs of the even / odd samples (w = exp(-2 pi i / 128)).  Thread (line,
+// h) transforms the samples of parity h in registers (fft64_regs), takes its
+// partner's result (lane ^ 16) by shuffles and keeps output half h.  A 2-D
+// transform is 256 threads (warp w: lines 16 w .. 16 w + 15): columns
+// straight from the coalesced load, a padded shared-memory transpose, rows,
+// and a shared-memory pass for coalesced stores.  132 KB of shared memory
+// (the [128][129] tile), one transform per CTA.
+__constant__ float2 c_tw128[64];  // exp(-2 pi i q / 128), q < 64
+
+// a[] holds this thread's 64-point DFT (digit-reversed order); on return
+// a[k] (natural order, k < 64) = X[k + 64 h] of the 128-point line.
+__device__ __forceinline__ void combine128(float2 (&a)[64], int h) {
+  float2 o[64];
+#pragma unroll
+  for (int k = 0; k < 64; ++k) {
+    const float2 own = a[rev4_3(k)];
+    const float2 other = make_float2(__shfl_xor_sync(0xffffffffu, own.x, 16),
+                                     __shfl_xor_sync(0xffffffffu, own.y, 16));
+    const float2 e = h ? other : own, od = h ? own : other;
+    const float2 t = cm(od, c_tw128[k]);
+    o[k] = h ? csub(e, t) : cadd(e, t);
+  }
+#pragma unroll
+  for (int k = 0; k < 64; ++k) a[k] = o[k];
+}
+
+constexpr int kP128Pad = 129;
+
+// FWD: Y[patch][j] = FFT2(stack[j][oy:oy+128, ox:ox+128])    grid (n_patches, K)
+// !FWD: out[patch] = Re(IFFT2(X[patch])) / 128^2 = Re(FFT2(conj X)) / 128^2
+template <bool FWD>
+__global__ void __launch_bounds__(256) patch_fft128_kernel(LayoutDev L, const float* __restrict__ stack,
+                                                           int K, float2* __restrict__ Y, int p_lo,
+                                                           int row0, int rows,
+                                                           const float2* __restrict__ X,
+                                                           float* __restrict__ out) {
+  extern __shared__ float2 s128[];  // [128][kP128Pad]
+  const int lane = threadIdx.x & 31, h = lane >> 4;
+  const int line = (threadIdx.x >> 5) * 16 + (lane & 15);
+  float2 a[64];
+  if (FWD) {
+    const int patch = p_lo + blockIdx.x, j = blockIdx.y;
+    const int px = patch % L.nx, py = patch / L.nx;
+    const int ox = patch_offset(px, L.nx, L.stride, L.last_x);
+    const int oy = patch_offset(py, L.ny, L.stride, L.last_y);
+    const float* img = stack + static_cast<size_t>(j) * L.W * rows +
+                       static_cast<size_t>(oy - row0 + h) * L.W + ox + line;
+#pragma unroll
+    for (int y = 0; y < 64; ++y) a[y] = make_float2(__ldcs(img + static_cast<size_t>(2 * y) * L.W), 0.f);
+  } else {
+    const float2* x = X + static_cast<size_t>(blockIdx.x) * 16384 + h * 128 + line;
+#pragma unroll
+    for (int y = 0; y < 64; ++y) {
+      const float2 v = x[y * 256];
+      a[y] = make_float2(v.x, -v.y);
+    }
+  }
+  fft64_regs(a);
+  combine128(a, h);  // column `line`: a[k] = Z[k + 64 h][line]
+#pragma unroll
+  for (int k = 0; k < 64; ++k) s128[(k + 64 * h) * kP128Pad + line] = a[k];
+  __syncthreads();
+#pragma unroll
+  for (int x = 0; x < 64; ++x) a[x] = s128[line * kP128Pad + 2 * x + h];  // row `line`, parity h
+  fft64_regs(a);
+  combine128(a, h);  // row `line`: a[k] = Y[line][k + 64 h]
+  __syncthreads();
+  if (FWD) {
+#pragma unroll
+    for (int k = 0; k < 64; ++k) s128[line * kP128Pad + k + 64 * h] = a[k];
+    __syncthreads();
+    float2* o = Y + (static_cast<size_t>(blockIdx.x) * K + blockIdx.y) * 16384;
+#pragma unroll 8
+    for (int q = 0; q < 64; ++q) {
+      const int e = q * 256 + threadIdx.x;
+      __stcs(o + e, s128[(e >> 7) * kP128Pad + (e & 127)]);
+    }
+  } else {
+    float* sr = reinterpret_cast<float*>(s128);  // [128][kP128Pad] real plane
+#pragma unroll
+    for (int k = 0; k < 64; ++k) sr[line * kP128Pad + k + 64 * h] = a[k].x;
+    __syncthreads();
+    float* o = out + static_cast<size_t>(blockIdx.x) * 16384;
+    const float inv = 1.f / 16384.f;
+#pragma unroll 8
+    for (int q = 0; q < 64; ++q) {
+      const int e = q * 256 + threadIdx.x;
+      o[e] = sr[(e >> 7) * kP128Pad + (e & 127)] * inv;
+    }
+  }
+}
+
 // out[patch][P2] = Re(IFFT2(X[patch])) / (P*P)           grid (n_patches)
 __global__ void patch_ifft_real_kernel(int P, int logP, const float2* __restrict__ X,
                                        float* __restrict__ out) {
@@ -327,22 +422,26 @@ LayoutDev layout_dev(const pact_layout& l) {
   return d;
 }
 
-// c_tw64 once per device (the constant bank is per device context)
+// c_tw64 / c_tw128 once per device (the constant bank is per device context)
 Status twiddles64() {
   int dev = 0;
   PACT_CUDA_S(cudaGetDevice(&dev));
   static std::once_flag once[64];
   static cudaError_t err[64];
   std::call_once(once[dev & 63], [dev] {
-    float2 tw[64];
+    float2 tw[64], tw2[64];
     for (int q = 0; q < 64; ++q) {
-      const double ang = -2.0 * M_PI * q / 64.0;
+      const double ang = -2.0 * M_PI * q / 64.0, ang2 = -2.0 * M_PI * q / 128.0;
       tw[q] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+      tw2[q] = make_float2(static_cast<float>(std::cos(ang2)), static_cast<float>(std::sin(ang2)));
     }
     err[dev & 63] = cudaMemcpyToSymbol(c_tw64, tw, sizeof(tw));
+    if (err[dev & 63] == cudaSuccess) err[dev & 63] = cudaMemcpyToSymbol(c_tw128, tw2, sizeof(tw2));
   });
   return cuda_status(err[dev & 63], "cudaMemcpyToSymbol(c_tw64)");
 }
+
+constexpr size_t kSmem128 = sizeof(float2) * 128 * kP128Pad;
 
 bool fft64_enabled() {
   static const bool off = [] {  // PACT_FFT_SMEM=1: the shared-memory radix-2 kernels
@@ -365,6 +464,14 @@ Status launch_patch_fft(pact_ctx* ctx, const pact_layout& lay, const float* stac
                                                                      p_lo, row0, stack_rows);
     return after_launch(ctx, "patch_fft64_kernel");
   }
+  if (lay.patch_pixels == 128 && fft64_enabled()) {
+    PACT_TRY_S(twiddles64());
+    PACT_TRY_S(smem_optin(patch_fft128_kernel<true>, kSmem128));
+    if (p_hi <= p_lo) return {};
+    patch_fft128_kernel<true><<<dim3(p_hi - p_lo, K), 256, kSmem128, ctx->stream>>>(
+        layout_dev(lay), stack, K, Y, p_lo, row0, stack_rows, nullptr, nullptr);
+    return after_launch(ctx, "patch_fft128_kernel");
+  }
   const int P = lay.patch_pixels, logP = ilog2_exact(P);
   size_t smem = fft_smem(P, logP);
   if (smem > 220 * 1024) return validation("extract_patch_spectra: patch too large for the device FFT");
@@ -381,6 +488,13 @@ Status launch_patch_ifft_real(pact_ctx* ctx, int P, int n_patches, const float2*
     PACT_TRY_S(twiddles64());
     patch_ifft64_real_kernel<<<n_patches, 64, 0, ctx->stream>>>(X, out);
     return after_launch(ctx, "patch_ifft64_real_kernel");
+  }
+  if (P == 128 && fft64_enabled()) {
+    PACT_TRY_S(twiddles64());
+    PACT_TRY_S(smem_optin(patch_fft128_kernel<false>, kSmem128));
+    patch_fft128_kernel<false><<<n_patches, 256, kSmem128, ctx->stream>>>(LayoutDev{}, nullptr, 0,
+                                                                          nullptr, 0, 0, 0, X, out);
+    return after_launch(ctx, "patch_fft128_kernel");
   }
   const int logP = ilog2_exact(P);
   size_t smem = fft_smem(P, logP);

@@ -242,11 +242,21 @@ def test_cfg5_subgrid_width256_step(ctx, R, W5, sig5):
     tr.step(1)
     theta = R.init_siren(0, _spec(w), tr.n_params)
     st = R.nf_step(sig5.double().cpu().numpy(), w.ring, w.meta, w.grid, w.mask,
-                   wl.train_config(w, seed=0, workers=0), theta, want_image=False)
+                   wl.train_config(w, seed=0, workers=0), theta, want_image=True)
     lay = make_patch_layout(w.grid, w.patch_mm, w.overlap)
     assert (lay.patch_pixels, lay.n_patches) == (128, 9)
     _check_step(tr, st, lay.n_patches, w.n_angles, "cfg5 sub-grid step")
     tr.close()
+    # the P = 128 final deconvolution (forward and inverse patch FFTs,
+    # deconv.hpp:176-198) under theta_0
+    stack = ctx.das_stack(sig5, w.ring, w.meta, w.grid, w.v0, w.delays)
+    _, dev = ctx.render_sos(_spec(w), torch.as_tensor(theta), w.grid, w.mask)
+    img = ctx.deconvolve_image(stack, w.delays, w.v0, dev, w.ring, w.mask, lay,
+                               DeconvolveOptions(w.eps_deconv, w.n_angles, w.ray_step,
+                                                 w.merge_fwhm))
+    img_err = rel_l2(img.double().cpu().numpy(), st["image"])
+    print(f"cfg5 sub-grid image (P=128) rel L2 {img_err:.2e}")
+    assert img_err <= 1e-3
 
 
 def test_cfg5_window_covers_lookups(W5):
