@@ -27,6 +27,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "siren.cuh"
 #include "tc.cuh"
@@ -111,11 +112,29 @@ struct LayerOffsets {
   long long off[kMaxHidden];  // theta offset of hidden tcgen05 layer l (network layer l + 1)
 };
 
+// F16: the planes hold fp16 hi / lo of W * 2^kF16Shift (|W| ~ 1e-2 for a
+// SIREN: the scaled weights sit in fp16's normal range), 64 features per
+// 128-B row: [l][j < 2][hi | lo][n][kk] with 16-B granule kk/8 XOR n % 8.
+constexpr float kF16Scale = 256.f;
+
+template <bool F16>
 __global__ void chain_wplanes_kernel(const float* __restrict__ theta, LayerOffsets lo_, int nl,
                                      float* __restrict__ out) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nl * CH * CH) return;
   const int l = e / (CH * CH), r = (e / CH) % CH, k = e % CH;
+  if (F16) {
+    if (k & 1) return;  // one thread per feature pair
+    const int j = k / 64, kk = k % 64;
+    const float* w = theta + lo_.off[l] + static_cast<size_t>(r) * CH + k;
+    uint32_t hi, lo;
+    tc::split_f16x2(kF16Scale * w[0], kF16Scale * w[1], hi, lo);
+    uint32_t* pl = reinterpret_cast<uint32_t*>(out + static_cast<size_t>(l * 2 + j) * 2 * kPlaneFloats);
+    const int o = r * 32 + ((((kk >> 3) ^ (r & 7))) << 2) + ((kk & 7) >> 1);  // 32-bit words
+    pl[o] = hi;
+    pl[kPlaneFloats + o] = lo;
+    return;
+  }
   const int j = k / CKC, kk = k % CKC;
   float hi, lo;
   tc::split_tf32(theta[lo_.off[l] + static_cast<size_t>(r) * CH + k], hi, lo);
@@ -125,8 +144,16 @@ __global__ void chain_wplanes_kernel(const float* __restrict__ theta, LayerOffse
   pl[kPlaneFloats + o] = lo;
 }
 
+// F16: the MMAs run kind::f16 on split-fp16 operands (tc::split_f16x2): K-chunks
+// of 64 features (two per layer), A packed two features per TMEM column (hi
+// [0, 64), lo [64, 128)), weights scaled by kF16Scale (undone in the
+// epilogue, an exact power of two).
+template <bool F16>
 __global__ void __launch_bounds__(kThreads, 1)
 siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_acts) {
+  constexpr int KCH = F16 ? 2 : NCH;                 // K-chunks (weight stages) per layer
+  constexpr uint32_t kAlo = F16 ? 64u : kColAlo;     // TMEM column of A lo
+  constexpr float kDs = F16 ? 1.f / kF16Scale : 1.f;  // accumulator scale
   extern __shared__ unsigned char smem_dyn[];
   float* wring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) &
                                           ~static_cast<uintptr_t>(1023));  // [WS][2][128][32]
@@ -144,11 +171,11 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) tc::tmem_alloc<512>(&sb.tslot);
   if (tid == 0) {
-    for (int i = 0; i < WS; ++i) {
+    for (int i = 0; i < KCH; ++i) {
       tc::mbar_init(&sb.wfull[i], 1);
       tc::mbar_init(&sb.wempty[i], 1);
     }
-    for (int j = 0; j < NCH; ++j) tc::mbar_init(&sb.ardy[j], CT);  // the 4 warps of chunk j
+    for (int j = 0; j < KCH; ++j) tc::mbar_init(&sb.ardy[j], CT * (NCH / KCH));  // its epilogue warps
     for (int b = 0; b < 2; ++b)
       for (int nh = 0; nh < 2; ++nh) {
         tc::mbar_init(&sb.dfull[b][nh], 1);
@@ -178,7 +205,7 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
       uint32_t u = 0;  // layer uses
       for (int i = 0; i < my_tiles; ++i)
         for (int l = 0; l < nl; ++l, ++u)
-          for (int j = 0; j < NCH; ++j) {
+          for (int j = 0; j < KCH; ++j) {
             if (u > 0) tc::mbar_wait_sleep(&sb.wempty[j], (u - 1) & 1);
             if (CHAIN_EXP == 1 && u > 0) {
               tc::mbar_arrive(&sb.wfull[j]);
@@ -186,7 +213,7 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
             }
             tc::mbar_expect_tx(&sb.wfull[j], kChunkBytes);
             tc::bulk_load(wring + j * 2 * kPlaneFloats,
-                          a.wplanes + static_cast<size_t>(l * NCH + j) * 2 * kPlaneFloats,
+                          a.wplanes + static_cast<size_t>(l * KCH + j) * 2 * kPlaneFloats,
                           kChunkBytes, &sb.wfull[j]);
           }
     }
@@ -194,7 +221,7 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
     // ---- MMA issue: layer l of tile i in two N-halves (64 output features
     // each), so the epilogue drains half 0 while the tensor core computes
     // half 1, and half 0 of the next layer starts on the first A chunks ----
-    constexpr uint32_t idesc = tc::idesc_tf32(CT, CH / 2);
+    constexpr uint32_t idesc = F16 ? tc::idesc_f16(CT, CH / 2) : tc::idesc_tf32(CT, CH / 2);
     for (int i = 0; i < my_tiles; ++i)
       for (int l = 0; l < nl; ++l) {
         const uint32_t lc = static_cast<uint32_t>(i * nl + l), b = lc & 1;
@@ -202,7 +229,7 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
           const uint32_t dcol = t0 + kColD + b * CH + nh * (CH / 2);
           if (lc >= 2) tc::mbar_wait_sleep(&sb.dfree[b][nh], ((lc - 2) >> 1) & 1);
           CTRACE(0, 1, lc * 2 + nh);
-          for (int j = 0; j < NCH; ++j) {
+          for (int j = 0; j < KCH; ++j) {
             if (nh == 0) {
               tc::mbar_wait_sleep(&sb.ardy[j], lc & 1);
               CTRACE(0, 2, lc * 4 + j);
@@ -215,16 +242,24 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
                            sl = sh + kPlaneFloats * 4;
             if (tc::elect_one()) {
 #pragma unroll
-              for (int s = 0; s < CKC / 8; ++s) {
-                const uint32_t ka = j * CKC + 8 * s;
+              // four K steps per 128-B row: 8 tf32 or 16 fp16 features, 8 TMEM
+              // columns and 32 B of the row each
+              for (int s = 0; s < 4; ++s) {
+                const uint32_t ka = j * 32 + 8 * s;
                 const uint64_t dh = tc::smem_desc_sw128(sh + 32 * s);
                 const uint64_t dl = tc::smem_desc_sw128(sl + 32 * s);
-                tc::mma_tf32_ts(dcol, t0 + kColAlo + ka, dh, idesc, (j | s) != 0);
-                tc::mma_tf32_ts(dcol, t0 + ka, dl, idesc, 1u);
-                tc::mma_tf32_ts(dcol, t0 + ka, dh, idesc, 1u);
+                if (F16) {
+                  tc::mma_f16_ts(dcol, t0 + kAlo + ka, dh, idesc, (j | s) != 0);
+                  tc::mma_f16_ts(dcol, t0 + ka, dl, idesc, 1u);
+                  tc::mma_f16_ts(dcol, t0 + ka, dh, idesc, 1u);
+                } else {
+                  tc::mma_tf32_ts(dcol, t0 + kAlo + ka, dh, idesc, (j | s) != 0);
+                  tc::mma_tf32_ts(dcol, t0 + ka, dl, idesc, 1u);
+                  tc::mma_tf32_ts(dcol, t0 + ka, dh, idesc, 1u);
+                }
               }
               if (nh == 1) tc::mma_commit(&sb.wempty[j]);
-              if (j == NCH - 1) tc::mma_commit(&sb.dfull[b][nh]);
+              if (j == KCH - 1) tc::mma_commit(&sb.dfull[b][nh]);
             }
             __syncwarp();
           }
@@ -271,16 +306,27 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
     };
     // sin(w0 v) -> this chunk's A columns (hi, lo) of the next layer
     auto put_a = [&](const float (&v)[16], int hf, bool valid) {
-      float hi[16], lo[16];
+      if (F16) {
+        uint32_t hi[8], lo[8];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) tc::split_tf32_trunc(valid ? sinw(v[k], w0) : 0.f, hi[k], lo[k]);
-      tc::tmem_st16_nowait(lb + kb + 16 * hf, hi);
-      tc::tmem_st16_nowait(lb + kColAlo + kb + 16 * hf, lo);
+        for (int k = 0; k < 8; ++k)
+          tc::split_f16x2(valid ? sinw(v[2 * k], w0) : 0.f, valid ? sinw(v[2 * k + 1], w0) : 0.f, hi[k],
+                          lo[k]);
+        tc::tmem_st8u_nowait(lb + (kb + 16 * hf) / 2, hi);
+        tc::tmem_st8u_nowait(lb + kAlo + (kb + 16 * hf) / 2, lo);
+      } else {
+        float hi[16], lo[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) tc::split_tf32_trunc(valid ? sinw(v[k], w0) : 0.f, hi[k], lo[k]);
+        tc::tmem_st16_nowait(lb + kb + 16 * hf, hi);
+        tc::tmem_st16_nowait(lb + kAlo + kb + 16 * hf, lo);
+      }
     };
+    const int jr = F16 ? j >> 1 : j;  // the K-chunk this warp's features belong to
     auto a_ready = [&]() {
       tc::tmem_wait_st();
       tc::fence_before_sync();
-      tc::mbar_arrive(&sb.ardy[j]);
+      tc::mbar_arrive(&sb.ardy[jr]);
     };
     auto tile_m0 = [&](int t) { return (blockIdx.x + t * gridDim.x) * CT; };
     // first layer of tile t (CUDA cores): a_0 = W_0 c + b_0 -> acts[0], A
@@ -335,17 +381,31 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
               v[k] = fmaf(s_w0[2 * f + 1], c.y, fmaf(s_w0[2 * f], c.x, s_b0[f]));
             }
             if (a.store_a0) put_box(v, hf);
+            if (F16) {
+              uint32_t* h = reinterpret_cast<uint32_t*>(ahi) + 8 * hf;
+              uint32_t* o = reinterpret_cast<uint32_t*>(alo) + 8 * hf;
 #pragma unroll
-            for (int k = 0; k < 16; ++k)
-              tc::split_tf32_trunc(v1 ? sinw(v[k], w0) : 0.f, ahi[16 * hf + k], alo[16 * hf + k]);
+              for (int k = 0; k < 8; ++k)
+                tc::split_f16x2(v1 ? sinw(v[2 * k], w0) : 0.f, v1 ? sinw(v[2 * k + 1], w0) : 0.f, h[k], o[k]);
+            } else {
+#pragma unroll
+              for (int k = 0; k < 16; ++k)
+                tc::split_tf32_trunc(v1 ? sinw(v[k], w0) : 0.f, ahi[16 * hf + k], alo[16 * hf + k]);
+            }
           }
           if (a.store_a0) store_box(0, m1 + 32 * q);
           tc::mbar_wait(&sb.dfull[b][1], (lc >> 1) & 1);
           tc::fence_after_sync();
-          tc::tmem_st32(lb + kb, ahi);
-          tc::tmem_st32(lb + kColAlo + kb, alo);
+          if (F16) {
+            tc::tmem_st16u_nowait(lb + kb / 2, reinterpret_cast<const uint32_t(&)[16]>(ahi));
+            tc::tmem_st16u_nowait(lb + kAlo + kb / 2, reinterpret_cast<const uint32_t(&)[16]>(alo));
+            tc::tmem_wait_st();
+          } else {
+            tc::tmem_st32(lb + kb, ahi);
+            tc::tmem_st32(lb + kAlo + kb, alo);
+          }
           tc::fence_before_sync();
-          tc::mbar_arrive(&sb.ardy[j]);
+          tc::mbar_arrive(&sb.ardy[jr]);
           if (role > 0) CTRACE(role, 11, i + 1);
         } else {
           tc::mbar_wait(&sb.dfull[b][1], (lc >> 1) & 1);
@@ -358,7 +418,7 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
           float v[16];
           tc::tmem_ld16(lb + kColD + b * CH + kb + 16 * hf, v);
 #pragma unroll
-          for (int k = 0; k < 16; ++k) v[k] += s_bias[l * CH + kb + 16 * hf + k];
+          for (int k = 0; k < 16; ++k) v[k] = fmaf(v[k], kDs, s_bias[l * CH + kb + 16 * hf + k]);
           put_box(v, hf);
           if (last) {
 #pragma unroll
@@ -392,6 +452,15 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
 
 }  // namespace
 
+// PACT_SIREN_F16=0 keeps the 3xTF32 MMAs (comparisons); default split fp16.
+static bool chain_f16() {
+  static const bool on = [] {
+    const char* e = std::getenv("PACT_SIREN_F16");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // Forward of the whole network for hidden width 128 with >= 1 tcgen05 layer.
 Status tc_forward_chain(pact_ctx* ctx, const SirenShape& s, const float* theta, SirenWork& w,
                         float* dv, bool store_a0) {
@@ -412,7 +481,11 @@ Status tc_forward_chain(pact_ctx* ctx, const SirenShape& s, const float* theta, 
   // layer offsets into theta travel in the launch arguments (graph-capturable)
   LayerOffsets lo{};
   for (int l = 0; l < nl; ++l) lo.off[l] = static_cast<long long>(s.offset(l + 1));
-  chain_wplanes_kernel<<<div_up(nl * CH * CH, 256), 256, 0, st>>>(theta, lo, nl, w.wplanes);
+  const bool f16 = chain_f16();
+  if (f16)
+    chain_wplanes_kernel<true><<<div_up(nl * CH * CH, 256), 256, 0, st>>>(theta, lo, nl, w.wplanes);
+  else
+    chain_wplanes_kernel<false><<<div_up(nl * CH * CH, 256), 256, 0, st>>>(theta, lo, nl, w.wplanes);
   PACT_TRY_S(after_launch(ctx, "chain_wplanes_kernel"));
   ChainArgs a{};
   a.coords = w.coords;
@@ -451,11 +524,16 @@ Status tc_forward_chain(pact_ctx* ctx, const SirenShape& s, const float* theta, 
     return internal_error("tc_forward_chain: tensor map encoding failed");
   const size_t smem = 1024 + sizeof(float) * (WS * 2 * kPlaneFloats + kEpiWarps * kBoxBytes / 4 +
                                                2 * CH + CH + CH + kMaxHidden * CH + NCH * CT);
-  PACT_CUDA_S(cudaFuncSetAttribute(siren_chain_fwd_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
   const int grid = std::min(ctx->num_sms, div_up(n, CT));
-  siren_chain_fwd_kernel<<<grid, kThreads, smem, st>>>(a, tmap);
+  if (f16) {
+    PACT_CUDA_S(cudaFuncSetAttribute(siren_chain_fwd_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    siren_chain_fwd_kernel<true><<<grid, kThreads, smem, st>>>(a, tmap);
+  } else {
+    PACT_CUDA_S(cudaFuncSetAttribute(siren_chain_fwd_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    siren_chain_fwd_kernel<false><<<grid, kThreads, smem, st>>>(a, tmap);
+  }
   return after_launch(ctx, "siren_chain_fwd_kernel");
 }
 
