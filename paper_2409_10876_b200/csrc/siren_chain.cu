@@ -450,6 +450,253 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
   if (warp == 0) tc::tmem_free<512>(t0);
 }
 
+// ---- split-fp16 forward with two tiles in flight ------------------------------
+// With fp16 operands a tile's A (hi + lo, two features per column) takes 128
+// TMEM columns, so two tiles fit beside one accumulator each:
+//   TMEM  slot t = 0, 1: A hi [128 t, 128 t + 64), lo [128 t + 64, 128 t + 128),
+//         D [256 + 128 t, 256 + 128 t + 128).
+// The tensor core alternates the slots layer by layer -- (tile a, l), (tile
+// b, l), (tile a, l + 1), ... -- so one tile's epilogue (TMEM -> sin ->
+// next-layer A, activation stores) runs while the tensor core computes the
+// other tile's layer, instead of the single-tile MMA -> epilogue -> MMA
+// hand-off.  Roles, weight ring, stores and the head are those of
+// siren_chain_fwd_kernel (F16); a group is the CTA's tiles 2g, 2g + 1.
+struct PairBars {
+  uint64_t wfull[2], wempty[2];  // weight stage j: K-chunk j (64 features) of the current layer
+  uint64_t ardy[2][2];           // [slot][K-chunk] A written (256 threads)
+  uint64_t dfull[2][2], dfree[2][2];  // [slot][N-half]: ready (MMA commit) / drained (256 threads)
+  uint32_t tslot;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+siren_chain_pair_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_acts) {
+  constexpr float kDs = 1.f / kF16Scale;
+  extern __shared__ unsigned char smem_dyn[];
+  float* wring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) &
+                                          ~static_cast<uintptr_t>(1023));  // [2][2][128][64 fp16]
+  float* s_tr = wring + WS * 2 * kPlaneFloats;  // [16 warps] SW128 store boxes (1024-aligned)
+  float* s_w0 = s_tr + kEpiWarps * kBoxBytes / 4;                          // [128][2]
+  float* s_b0 = s_w0 + 2 * CH;                                             // [128]
+  float* s_wl = s_b0 + CH;                                                 // [128]
+  float* s_bias = s_wl + CH;                                               // [nl][128]
+  float* s_head = s_bias + kMaxHidden * CH;                                // [2 slots][4][128]
+  __shared__ PairBars sb;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) tc::tmem_alloc<512>(&sb.tslot);
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&sb.wfull[i], 1);
+      tc::mbar_init(&sb.wempty[i], 1);
+    }
+    for (int t = 0; t < 2; ++t)
+      for (int h = 0; h < 2; ++h) {
+        tc::mbar_init(&sb.ardy[t][h], 2 * CT);
+        tc::mbar_init(&sb.dfull[t][h], 1);
+        tc::mbar_init(&sb.dfree[t][h], 32 * kEpiWarps / 2);
+      }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < 2 * CH; i += kThreads) s_w0[i] = a.W0[i];
+  for (int i = tid; i < CH; i += kThreads) {
+    s_b0[i] = a.b0[i];
+    s_wl[i] = a.wL[i];
+  }
+  for (int l = 0; l < a.nl; ++l)
+    for (int i = tid; i < CH; i += kThreads) s_bias[l * CH + i] = a.bias[l][i];
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t t0 = sb.tslot;
+  const int n_tiles = (a.n + CT - 1) / CT;
+  const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int n_groups = (my_tiles + 1) / 2;
+  const int nl = a.nl;
+  auto group_tiles = [&](int g) { return min(2, my_tiles - 2 * g); };
+
+  if (warp == 0) {
+    // ---- weights: chunk j of (group, layer) into stage j once both slots'
+    // MMAs of the previous (group, layer) are done with it ----
+    if (lane == 0) {
+      uint32_t u = 0;
+      for (int g = 0; g < n_groups; ++g)
+        for (int l = 0; l < nl; ++l, ++u)
+          for (int j = 0; j < 2; ++j) {
+            if (u > 0) tc::mbar_wait_sleep(&sb.wempty[j], (u - 1) & 1);
+            tc::mbar_expect_tx(&sb.wfull[j], kChunkBytes);
+            tc::bulk_load(wring + j * 2 * kPlaneFloats,
+                          a.wplanes + static_cast<size_t>(l * 2 + j) * 2 * kPlaneFloats, kChunkBytes,
+                          &sb.wfull[j]);
+          }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = tc::idesc_f16(CT, CH / 2);
+    for (int g = 0; g < n_groups; ++g) {
+      const int nt = group_tiles(g);
+      for (int l = 0; l < nl; ++l) {
+        const uint32_t u = static_cast<uint32_t>(g * nl + l);  // use of every slot buffer
+        for (int t = 0; t < nt; ++t)
+          for (int nh = 0; nh < 2; ++nh) {
+            const uint32_t dcol = t0 + 256 + 128 * t + nh * (CH / 2), acol = t0 + 128 * t;
+            if (u >= 1) tc::mbar_wait_sleep(&sb.dfree[t][nh], (u - 1) & 1);
+            for (int j = 0; j < 2; ++j) {
+              if (nh == 0) {
+                tc::mbar_wait_sleep(&sb.ardy[t][j], u & 1);
+                tc::mbar_wait_sleep(&sb.wfull[j], u & 1);
+              }
+              tc::fence_after_sync();
+              const uint32_t sh = saddr(wring + j * 2 * kPlaneFloats) + nh * (CH / 2) * 128,
+                             sl = sh + kPlaneFloats * 4;
+              if (tc::elect_one()) {
+#pragma unroll
+                for (int s = 0; s < 4; ++s) {
+                  const uint32_t ka = j * 32 + 8 * s;
+                  const uint64_t dh = tc::smem_desc_sw128(sh + 32 * s);
+                  const uint64_t dl = tc::smem_desc_sw128(sl + 32 * s);
+                  tc::mma_f16_ts(dcol, acol + 64 + ka, dh, idesc, (j | s) != 0);
+                  tc::mma_f16_ts(dcol, acol + ka, dl, idesc, 1u);
+                  tc::mma_f16_ts(dcol, acol + ka, dh, idesc, 1u);
+                }
+                if (t == nt - 1 && nh == 1) tc::mma_commit(&sb.wempty[j]);
+                if (j == 1) tc::mma_commit(&sb.dfull[t][nh]);
+              }
+              __syncwarp();
+            }
+          }
+      }
+    }
+  } else if (warp >= kEpi0 / 32) {
+    // ---- epilogue: 16 warps, warp = (TMEM lane quarter q, feature chunk j of
+    // 32); pixel = lane ----
+    const int q = warp & 3, ew = warp - kEpi0 / 32, j = ew >> 2;
+    const int p = 32 * q + lane, kb = CKC * j;
+    const uint32_t lb = t0 + (static_cast<uint32_t>(32 * q) << 16);
+    float* box = s_tr + ew * kBoxBytes / 4;
+    const int hN = j >> 1, jr = j >> 1;  // the accumulator N-half = the next layer's K-chunk
+    const float w0 = a.w0;
+    uint32_t nst = 0;
+    auto open_box = [&]() {
+      if (nst >= 1) {
+        if (lane == 0) tc::bulk_wait_read<0>();
+        __syncwarp();
+      }
+    };
+    auto put_box = [&](const float (&v)[16], int hf) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int gq = 4 * hf + c;
+        *reinterpret_cast<float4*>(box + lane * 32 + ((gq ^ (lane & 7)) << 2)) =
+            make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+      }
+    };
+    auto store_box = [&](int l, int r0) {
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        tc::tma_store_3d(&tmap_acts, box, kb, r0, l);
+        tc::bulk_commit();
+      }
+      ++nst;
+    };
+    auto put_a = [&](int t, const float (&v)[16], int hf, bool valid) {
+      uint32_t hi[8], lo[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        tc::split_f16x2(valid ? sinw(v[2 * k], w0) : 0.f, valid ? sinw(v[2 * k + 1], w0) : 0.f, hi[k],
+                        lo[k]);
+      tc::tmem_st8u_nowait(lb + 128 * t + (kb + 16 * hf) / 2, hi);
+      tc::tmem_st8u_nowait(lb + 128 * t + 64 + (kb + 16 * hf) / 2, lo);
+    };
+    auto a_ready = [&](int t) {
+      tc::tmem_wait_st();
+      tc::fence_before_sync();
+      tc::mbar_arrive(&sb.ardy[t][jr]);
+    };
+    auto tile_m0 = [&](int i) { return (blockIdx.x + i * gridDim.x) * CT; };
+    // first layer of tile i (CUDA cores): a_0 = W_0 c + b_0 -> acts[0], A of slot t
+    auto first_layer = [&](int i, int t) {
+      const int m0t = tile_m0(i);
+      const bool vt = p < min(CT, a.n - m0t);
+      const float2 c = vt ? a.coords[m0t + p] : make_float2(0.f, 0.f);
+      if (a.store_a0) open_box();
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {
+        float v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int f = kb + 16 * hf + k;
+          v[k] = fmaf(s_w0[2 * f + 1], c.y, fmaf(s_w0[2 * f], c.x, s_b0[f]));
+        }
+        if (a.store_a0) put_box(v, hf);
+        put_a(t, v, hf, vt);
+      }
+      if (a.store_a0) store_box(0, m0t + 32 * q);
+      a_ready(t);
+    };
+    if (n_groups > 0)
+      for (int t = 0; t < group_tiles(0); ++t) first_layer(t, t);
+    float hp[2] = {0.f, 0.f};  // head partials of the slots
+    for (int g = 0; g < n_groups; ++g) {
+      const int nt = group_tiles(g);
+      for (int l = 0; l < nl; ++l) {
+        const uint32_t u = static_cast<uint32_t>(g * nl + l);
+        const bool last = l == nl - 1;
+        for (int t = 0; t < nt; ++t) {
+          const int i = 2 * g + t, m0 = tile_m0(i);
+          const bool valid = p < min(CT, a.n - m0);
+          if (!last) {
+            tc::mbar_wait(&sb.dfull[t][hN], u & 1);
+          } else {
+            // every MMA of this slot's last layer is done (both halves): its A
+            // columns take the next group's tile of this slot (first layer)
+            tc::mbar_wait(&sb.dfull[t][1], u & 1);
+            if (g + 1 < n_groups && t < group_tiles(g + 1)) {
+              tc::fence_after_sync();
+              first_layer(i + 2, t);
+            }
+          }
+          tc::fence_after_sync();
+          open_box();
+          if (l == 0) hp[t] = 0.f;
+#pragma unroll 1
+          for (int hf = 0; hf < 2; ++hf) {
+            float v[16];
+            tc::tmem_ld16(lb + 256 + 128 * t + kb + 16 * hf, v);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] = fmaf(v[k], kDs, s_bias[l * CH + kb + 16 * hf + k]);
+            put_box(v, hf);
+            if (last) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) hp[t] = fmaf(s_wl[kb + 16 * hf + k], sinw(v[k], w0), hp[t]);
+            } else {
+              put_a(t, v, hf, valid);
+            }
+          }
+          tc::fence_before_sync();
+          tc::mbar_arrive(&sb.dfree[t][hN]);
+          store_box(l + 1, m0 + 32 * q);
+          if (!last) a_ready(t);
+        }
+      }
+      // output heads of the group's tiles: the four chunks of a pixel in a fixed order
+      for (int t = 0; t < nt; ++t) s_head[(t * NCH + j) * CT + p] = hp[t];
+      tc::named_sync(1, 32 * kEpiWarps);
+      if (j < nt) {
+        const int t = j, m0 = tile_m0(2 * g + t);
+        if (p < min(CT, a.n - m0)) {
+          const float* h = s_head + t * NCH * CT;
+          a.dv[a.idx[m0 + p]] =
+              a.scale * (a.bL[0] + (((h[p] + h[CT + p]) + h[2 * CT + p]) + h[3 * CT + p]));
+        }
+      }
+      tc::named_sync(1, 32 * kEpiWarps);
+    }
+    if (lane == 0) tc::bulk_wait_all();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<512>(t0);
+}
+
 }  // namespace
 
 // PACT_SIREN_F16=0 keeps the 3xTF32 MMAs (comparisons); default split fp16.
@@ -526,9 +773,10 @@ Status tc_forward_chain(pact_ctx* ctx, const SirenShape& s, const float* theta, 
                                                2 * CH + CH + CH + kMaxHidden * CH + NCH * CT);
   const int grid = std::min(ctx->num_sms, div_up(n, CT));
   if (f16) {
-    PACT_CUDA_S(cudaFuncSetAttribute(siren_chain_fwd_kernel<true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    siren_chain_fwd_kernel<true><<<grid, kThreads, smem, st>>>(a, tmap);
+    const size_t smem2 = smem + sizeof(float) * NCH * CT;  // s_head of the second slot
+    PACT_CUDA_S(cudaFuncSetAttribute(siren_chain_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem2)));
+    siren_chain_pair_kernel<<<grid, kThreads, smem2, st>>>(a, tmap);
   } else {
     PACT_CUDA_S(cudaFuncSetAttribute(siren_chain_fwd_kernel<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
