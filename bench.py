@@ -539,29 +539,36 @@ def run_ours(args):
     sr["fp32_pipe_peak_tflops"] = FP32_PEAK_TFLOPS  # the SIMT path's ceiling, for reference
     # The roofline line is for the dominant kernel.  Since the ray adjoint
     # became a gather (round 2) the SIREN is the largest stage; its forward is
-    # ONE persistent tcgen05 kernel (siren_chain_fwd_kernel: every layer of
-    # every pixel tile), so the line is that kernel against the 3xTF32 tensor
-    # rate.  The ray stages are L1/texture-served (their 16 B/step model
-    # exceeds HBM) and are reported per stage.
+    # ONE persistent tcgen05 kernel (siren_chain_pair_kernel: every layer of
+    # every pixel tile, two tiles in flight), so the line is that kernel
+    # against its tensor ceiling: split-fp16 operands, three kind::f16 MMAs per
+    # fp32-accurate product at the dense 16-bit rate (= the measured bf16
+    # rate), i.e. a third of it.  The ray stages are L1/texture-served (their
+    # 16 B/step model exceeds HBM) and are reported per stage.
+    f16x3 = bf16 / 3.0
     fwd_flops = work["siren_flops"] / 3.0  # 2 FLOP per MAC, forward only
     fwd_ach = fwd_flops / (stages["siren_fwd"] * 1e-3) / 1e12
-    roofline = {"bound": "tensor", "achieved": fwd_ach, "peak": tf32x3, "unit": "TFLOP/s",
-                "frac": fwd_ach / tf32x3, "traffic": traffic.get("siren_chain_fwd_kernel"),
-                "kernel": "siren_chain_fwd_kernel",
-                "peak_source": f"measured dense bf16 {bf16:.1f} TFLOP/s / 6 (3xTF32: three TF32 "
-                               f"MMAs per fp32-accurate product, TF32 at half the bf16 rate)",
+    roofline = {"bound": "tensor", "achieved": fwd_ach, "peak": f16x3, "unit": "TFLOP/s",
+                "frac": fwd_ach / f16x3, "traffic": traffic.get("siren_chain_pair_kernel"),
+                "kernel": "siren_chain_pair_kernel",
+                "peak_source": f"measured dense bf16 {bf16:.1f} TFLOP/s / 3 (split fp16: three "
+                               f"kind::f16 MMAs per fp32-accurate product at the dense 16-bit rate)",
                 "work_model": "SURVEY 8(d): 2 FLOP per MAC of the 2->128x4->1 network per masked "
                               "pixel (fp32-equivalent FLOPs)",
                 "traffic_source": traffic.get("_source")}
     # SURVEY 8(d) iteration roofline: sum_k max(B_k / HBM, F_k / peak_k), SIREN at 3xTF32
-    model_ms = 1e3 * (max(work["siren_flops"] / (tf32x3 * 1e12), 0.0)
+    # the loss reads half of Y since round 2b (the real stack's Hermitian
+    # spectrum): its model bytes stay the full read, like SURVEY 8(d)
+    model_ms = 1e3 * (fwd_flops / (f16x3 * 1e12) + (work["siren_flops"] - fwd_flops) / (tf32x3 * 1e12)
                       + (work["wavefront_bytes"] + work["ray_backward_bytes"]
                          + work["fused_loss_bytes"]) / (hbm * 1e9))
     iter_ms = sum(v["ms"] for v in stage_rl.values())
     iteration_roofline = {"model_ms": model_ms, "measured_ms": iter_ms, "frac": model_ms / iter_ms,
-                          "model": "SURVEY 8(d): SIREN F at the 3xTF32 tensor rate (measured dense "
-                                   "bf16 / 6) + ray and loss algorithmic bytes at measured HBM; "
-                                   "measured = sum of stage CUDA-event times of one frame"}
+                          "model": "SURVEY 8(d): SIREN forward F at the split-fp16 tensor rate "
+                                   "(measured dense bf16 / 3), backward F at the 3xTF32 rate "
+                                   "(bf16 / 6), ray and loss algorithmic bytes at measured HBM; "
+                                   "measured = sum of stage CUDA-event times of one frame. frac > 1: "
+                                   "the ray stages are L1/texture-served, below their HBM byte model"}
 
     cfg5 = None
     if not args.no_cfg5:
