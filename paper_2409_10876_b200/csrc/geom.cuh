@@ -154,6 +154,16 @@ struct RayArgs {
   const float4* cell_geo;
   int cell_sb, cell_t, tile_max;
   int n_gen_items, n_int_items;
+  // Border-line (side) plan of the adjoint (raymarch.cu; null: side items per
+  // ray): every run of a ray's border-line steps in one border cell (<= 255
+  // steps), as side_ent[k] = slot << 48 | (255 - steps) << 40 | ray << 20 |
+  // first step << 8, sorted by (slot, steps desc, ray); slot = the border
+  // cell's index in the [colL H | colR H | rowB W | rowT W] layout;
+  // side_start[slot] its range; side_geo[r] = (fs, df) of ray r's border line.
+  // The adjoint skips the side items [n_gen + n_int, n_items).
+  const unsigned long long* side_ent;
+  const unsigned* side_start;
+  const float2* side_geo;
 };
 
 // Creates a point-sampled, clamped pitch-2D texture over a row-major fp32

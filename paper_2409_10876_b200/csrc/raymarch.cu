@@ -692,7 +692,11 @@ __global__ void __launch_bounds__(256, 4) ray_backward_plan_kernel(RayArgs a, co
 // slots), its kBorderReplicas loads issued back to back; the integer sum is
 // exact, so folding it into acc with an integer atomic keeps the result
 // order-independent.  Slots are reset.
+// With a side plan the border cells' sums (side_gather_kernel<true>) join in:
+// slot s takes the lower pixel sum of cell s and the upper of cell s - 1 (same
+// line).
 __global__ void border_fold_kernel(unsigned long long* __restrict__ rep, int W, int H,
+                                   const unsigned long long* __restrict__ side_cells,
                                    unsigned long long* __restrict__ acc) {
   const int slot = blockIdx.x * blockDim.x + threadIdx.x;
   const int n_slots = 2 * (W + H);
@@ -706,6 +710,12 @@ __global__ void border_fold_kernel(unsigned long long* __restrict__ rep, int W, 
   for (int r = 0; r < kBorderReplicas; ++r) {
     v += part[r];
     if (part[r]) rep[r * stride + slot] = 0ull;
+  }
+  if (side_cells) {
+    const int len = slot < 2 * H ? H : W;
+    const int pos = slot < H ? slot : slot < 2 * H ? slot - H : slot < 2 * H + W ? slot - 2 * H : slot - 2 * H - W;
+    if (pos <= len - 2) v += side_cells[2 * slot];
+    if (pos >= 1) v += side_cells[2 * (slot - 1) + 1];
   }
   if (v == 0ull) return;
   int px, py;
@@ -855,17 +865,17 @@ __global__ void cell_steps_kernel(const RayRec* __restrict__ rec, int n_rays, in
   if (tcnt) tcnt[r] = nt;
 }
 
-// Sorted keys (group << 32 | value) -> values and the per-group ranges
-// start[0 .. n_groups].
+// Sorted keys (group << shift | value) -> the per-group ranges
+// start[0 .. n_groups] and (shift 32, val non-null) the 32-bit values.
 __global__ void group_bounds_kernel(const unsigned long long* __restrict__ keys, unsigned n,
-                                    int n_groups, unsigned* __restrict__ start,
+                                    int n_groups, int shift, unsigned* __restrict__ start,
                                     unsigned* __restrict__ val) {
   const unsigned k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const unsigned long long key = keys[k];
-  const int c = static_cast<int>(key >> 32);
+  const int c = static_cast<int>(key >> shift);
   if (val) val[k] = static_cast<unsigned>(key);
-  const int prev = k == 0 ? -1 : static_cast<int>(keys[k - 1] >> 32);
+  const int prev = k == 0 ? -1 : static_cast<int>(keys[k - 1] >> shift);
   for (int q = prev + 1; q <= c; ++q) start[q] = k;
   if (k == n - 1)
     for (int q = c + 1; q <= n_groups; ++q) start[q] = n;
@@ -977,6 +987,150 @@ __global__ void __launch_bounds__(kCellThreads, 3) cell_gather_kernel(RayArgs a,
       o[3] = static_cast<unsigned long long>(__float2ll_rn(r11 * scale));
     }
   }
+}
+
+// ---- border-line (side) steps as a gather --------------------------------------
+// Once one coordinate has left the grid the stencil clamps onto a border line,
+// so a ray's side steps are a 1-D march along that line: runs of steps in
+// one border cell (two raster values).  The plan lists every run under its
+// border cell, sorted by length (so a warp's lanes run near-equal loops);
+// one block per border cell holds the cell's two values in registers and
+// walks its runs: the per-ray adjoint's step arithmetic operand for operand,
+// without the smem border cache, the carry or the atomics; each run's two
+// pixel sums are converted to the fixed-point quantum once and reduced per
+// cell as integers.  (The forward keeps its per-ray border-line items: with
+// no carry they cost about the same per step, and a ray's sum stays whole.)
+constexpr int kSideThreads = 256;
+constexpr int kSideMaxRun = 255;
+
+__device__ __forceinline__ int side_range(const RayRec& q, int& i1) {
+  const bool ok = q.n > 0 && !(q.flags & kRecGeneric);
+  i1 = ok ? min(q.i_corner, q.n) : 0;
+  return ok ? q.i_side : 0;
+}
+
+// Runs of ray r's side steps: count (pass 0, keys null) or the keys at
+// keys[off[r] ..] (pass 1); and the ray's border line.
+__global__ void side_runs_kernel(const RayRec* __restrict__ rec, int n_rays, int W, int H,
+                                 const unsigned long long* __restrict__ off,
+                                 unsigned long long* __restrict__ keys, unsigned* __restrict__ cnt,
+                                 float2* __restrict__ geo) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rays) return;
+  const RayRec q = rec[r];
+  int i1;
+  const int i0 = side_range(q, i1);
+  const SideLine sl = side_line(rec_regimes(q), rec_pixels(q), W, H);
+  if (geo) geo[r] = make_float2(sl.fs, sl.df);
+  unsigned m = 0;
+  int prev = -1, first = i0;
+  auto emit = [&](int slot, int a0, int a1) {
+    for (int b = a0; b < a1; b += kSideMaxRun) {  // long runs in pieces of <= 255 steps
+      const int c = min(kSideMaxRun, a1 - b);
+      if (keys)
+        keys[off[r] + m] = (static_cast<unsigned long long>(slot) << 48) |
+                           (static_cast<unsigned long long>(kSideMaxRun - c) << 40) |
+                           (static_cast<unsigned long long>(r) << 20) |
+                           (static_cast<unsigned long long>(b) << 8);
+      ++m;
+    }
+  };
+  for (int i = i0; i < i1; ++i) {
+    const int slot = sl.off + min(static_cast<int>(fmaf(static_cast<float>(i), sl.df, sl.fs)), sl.qmax);
+    if (slot != prev) {
+      if (prev >= 0) emit(prev, first, i);
+      prev = slot;
+      first = i;
+    }
+  }
+  if (prev >= 0) emit(prev, first, i1);
+  if (cnt) cnt[r] = m;
+}
+
+// Raster index of border slot s ([colL H | colR H | rowB W | rowT W]).
+__device__ __forceinline__ int border_pixel(int s, int W, int H) {
+  if (s < 2 * H) return (s < H ? s : s - H) * W + (s < H ? 0 : W - 1);
+  const int q = s - 2 * H;
+  return (q < W ? 0 : H - 1) * W + (q < W ? q : q - W);
+}
+
+// One block per border cell (slot): cell_out[slot] = the cell's two pixel
+// sums (lower, upper) in the fixed-point quantum.
+__global__ void __launch_bounds__(kSideThreads) side_gather_kernel(RayArgs a, const float* __restrict__ gsc,
+                                                                   const unsigned long long* __restrict__ stats,
+                                                                   unsigned long long* __restrict__ cell_out) {
+  const int slot = blockIdx.x, W = a.W, H = a.H;
+  const unsigned e0 = a.side_start[slot], e1 = a.side_start[slot + 1];
+  if (e0 == e1) {  // (empty cell: zeros, so the fold reads no stale value)
+    if (threadIdx.x == 0) cell_out[2 * slot] = cell_out[2 * slot + 1] = 0ull;
+    return;
+  }
+  const int q = slot < 2 * H ? (slot < H ? slot : slot - H) : (slot - 2 * H < W ? slot - 2 * H : slot - 2 * H - W);
+  const float c0 = __ldg(a.dv + border_pixel(slot, W, H)), c1 = __ldg(a.dv + border_pixel(slot + 1, W, H));
+  const float dc = c1 - c0, fq = static_cast<float>(q), v0 = static_cast<float>(a.v0);
+  const float scale = ldexpf(1.f, fix_exponent(stats, a.step, a.v0, max_steps_total(a)));
+  long long s0 = 0, s1 = 0;
+  for (unsigned k = e0 + threadIdx.x; k < e1; k += kSideThreads) {
+    const unsigned long long e = __ldg(a.side_ent + k);
+    const int r = static_cast<int>((e >> 20) & 0xfffffu), i0 = static_cast<int>((e >> 8) & 0xfffu);
+    const int cnt = kSideMaxRun - static_cast<int>((e >> 40) & 0xffu);
+    const float g = __ldg(gsc + r);
+    if (g == 0.f) continue;  // aberration.hpp:340
+    const float2 geo = __ldg(a.side_geo + r);
+    // the per-ray border-line march's arithmetic (ray_backward_plan_kernel)
+    float b0 = 0.f, b1 = 0.f;
+    for (int i = i0; i < i0 + cnt; ++i) {
+      const float fa = fmaf(static_cast<float>(i), geo.y, geo.x) - fq;
+      const float v = v0 + fmaf(fa, dc, c0);
+      const float gv = g * rcp_approx(v * v);
+      const float g1 = gv * fa;
+      b0 += gv - g1;
+      b1 += g1;
+    }
+    s0 += __float2ll_rn(b0 * scale);
+    s1 += __float2ll_rn(b1 * scale);
+  }
+  // integer block sums: exact, so the order does not matter
+  __shared__ long long r0[kSideThreads / 32], r1[kSideThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    r0[threadIdx.x >> 5] = s0;
+    r1[threadIdx.x >> 5] = s1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t0 = 0, t1 = 0;
+    for (int w = 0; w < kSideThreads / 32; ++w) {
+      t0 += r0[w];
+      t1 += r1[w];
+    }
+    cell_out[2 * slot] = static_cast<unsigned long long>(t0);
+    cell_out[2 * slot + 1] = static_cast<unsigned long long>(t1);
+  }
+}
+
+// The corner runs of the adjoint (both coordinates clamped: every remaining
+// step on one corner pixel), one thread per ray, into the border replicas.
+__global__ void corner_adjoint_kernel(RayArgs a, const float* __restrict__ gsc,
+                                      const unsigned long long* __restrict__ stats,
+                                      unsigned long long* __restrict__ border_rep) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.n_rays) return;
+  const RayRec rr = a.rec[r];
+  if (rr.n <= 0 || (rr.flags & kRecGeneric) || rr.i_corner >= rr.n) return;
+  const float g = gsc[r];
+  if (g == 0.f) return;
+  const int W = a.W, H = a.H;
+  const int px = rr.dfx > 0.f ? W - 1 : 0, py = rr.dfy > 0.f ? H - 1 : 0;
+  const float v = static_cast<float>(a.v0) + __ldg(a.dv + py * W + px);
+  const float f = __fdividef(g, v * v) * static_cast<float>(rr.n - rr.i_corner);
+  if (f == 0.f) return;
+  const float scale = ldexpf(1.f, fix_exponent(stats, a.step, a.v0, max_steps_total(a)));
+  unsigned long long* rep = border_rep + static_cast<size_t>(r % kBorderReplicas) * 2 * (W + H);
+  atomicAdd(rep + (px == 0 ? 0 : H) + py, static_cast<unsigned long long>(__float2ll_rn(f * scale)));
 }
 
 // Generic kernels (plain loads, no texture): one per-step march per ray.
@@ -1113,11 +1267,18 @@ struct RayPlanData {
   const unsigned* tile_rays = nullptr;
   const float4* cell_geo = nullptr;
   int cell_sb = 0, cell_t = 0, tile_max = 0, n_tiles = 0;
+  // border-line (side) plan (null: none, see build_side_plan)
+  void* side_mem = nullptr;
+  const unsigned long long* side_ent = nullptr;
+  const unsigned* side_start = nullptr;
+  const float2* side_geo = nullptr;
+  unsigned n_side = 0;
   std::vector<double> key;
   ~RayPlanData() {
     if (mem) cudaFree(mem);
     if (cell_mem) cudaFree(cell_mem);
     if (tile_mem) cudaFree(tile_mem);
+    if (side_mem) cudaFree(side_mem);
   }
 };
 
@@ -1225,7 +1386,7 @@ Status build_cell_plan(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanD
     auto hold_tm = hold(tm);
     auto* ts = static_cast<unsigned*>(tm);
     group_bounds_kernel<<<div_up(static_cast<int>(ntc), 256), 256, 0, s>>>(
-        tkeys + ntc, ntc, nti, ts, reinterpret_cast<unsigned*>(static_cast<char*>(tm) + o_rays));
+        tkeys + ntc, ntc, nti, 32, ts, reinterpret_cast<unsigned*>(static_cast<char*>(tm) + o_rays));
     PACT_TRY_S(after_launch(ctx, "group_bounds_kernel"));
     std::vector<unsigned> hts(nti + 1);
     PACT_CUDA_S(cudaMemcpyAsync(hts.data(), ts, sizeof(unsigned) * (nti + 1), cudaMemcpyDeviceToHost, s));
@@ -1266,7 +1427,8 @@ Status build_cell_plan(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanD
   PACT_TRY_S(after_launch(ctx, "cell_steps_kernel"));
   PACT_CUDA_S(cub::DeviceRadixSort::SortKeys(static_cast<char*>(scratch) + al(16ull * n), temp, keys,
                                              keys + n, n, 0, end_bit, s));
-  group_bounds_kernel<<<div_up(static_cast<int>(n), 256), 256, 0, s>>>(keys + n, n, n_cells, start, nullptr);
+  group_bounds_kernel<<<div_up(static_cast<int>(n), 256), 256, 0, s>>>(keys + n, n, n_cells, 32, start,
+                                                                       nullptr);
   PACT_TRY_S(after_launch(ctx, "group_bounds_kernel"));
   auto* tstart = static_cast<unsigned*>(tmem);
   auto* trays = reinterpret_cast<unsigned*>(static_cast<char*>(tmem) + al(sizeof(unsigned) * (n_tiles + 1)));
@@ -1285,6 +1447,82 @@ Status build_cell_plan(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanD
   p.cell_t = T;
   p.tile_max = tile_max;
   p.n_tiles = n_tiles;
+  return {};
+}
+
+bool side_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PACT_RAY_SIDE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// The side plan (see side_gather_kernel): every run of every ray's border-line
+// steps, keyed (slot, length, ray, first step) and radix-sorted.  Skipped
+// (the adjoint's side items stay per ray) when a field does not fit or
+// PACT_RAY_SIDE=0.  Synchronous.
+Status build_side_plan(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanData& p) {
+  const int nr = a.n_rays, n_slots = 2 * (a.W + a.H);
+  if (!side_enabled() || a.W < 2 || a.H < 2 || nr > (1 << 20) || n_slots >= (1 << 16)) return {};
+  {
+    std::vector<RayRec> rec(nr);
+    PACT_CUDA_S(cudaMemcpyAsync(rec.data(), p.rec, sizeof(RayRec) * nr, cudaMemcpyDeviceToHost, s));
+    PACT_CUDA_S(cudaStreamSynchronize(s));
+    for (const RayRec& q : rec)
+      if (q.n > 0 && !(q.flags & kRecGeneric) && std::min(q.i_corner, q.n) > 4096) return {};
+  }
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  auto hold = [](void* q) { return std::unique_ptr<void, void (*)(void*)>(q, [](void* x) { cudaFree(x); }); };
+  void* small = nullptr;
+  PACT_CUDA_S(cudaMalloc(&small, al(sizeof(unsigned long long) * (nr + 1)) + al(sizeof(unsigned) * nr)));
+  auto hold_small = hold(small);
+  auto* off = static_cast<unsigned long long*>(small);
+  auto* cnt = reinterpret_cast<unsigned*>(static_cast<char*>(small) + al(sizeof(unsigned long long) * (nr + 1)));
+  side_runs_kernel<<<div_up(nr, 256), 256, 0, s>>>(p.rec, nr, a.W, a.H, nullptr, nullptr, cnt, nullptr);
+  PACT_TRY_S(after_launch(ctx, "side_runs_kernel"));
+  std::vector<unsigned> hc(nr);
+  PACT_CUDA_S(cudaMemcpyAsync(hc.data(), cnt, sizeof(unsigned) * nr, cudaMemcpyDeviceToHost, s));
+  PACT_CUDA_S(cudaStreamSynchronize(s));
+  std::vector<unsigned long long> ho(nr);
+  unsigned long long total = 0;
+  for (int r = 0; r < nr; ++r) {
+    ho[r] = total;
+    total += hc[r];
+  }
+  if (total == 0 || total >= (1ull << 31)) return {};
+  const unsigned n = static_cast<unsigned>(total);
+  PACT_CUDA_S(cudaMemcpyAsync(off, ho.data(), sizeof(unsigned long long) * nr, cudaMemcpyHostToDevice, s));
+  // the plan's memory: ent [n] | start [n_slots + 1] | geo [nr]
+  const size_t o_start = al(sizeof(unsigned long long) * n), o_geo = al(o_start + sizeof(unsigned) * (n_slots + 1)),
+               bytes = o_geo + sizeof(float2) * nr;
+  void* mem = nullptr;
+  PACT_CUDA_S(cudaMalloc(&mem, bytes));
+  auto hold_mem = hold(mem);
+  char* b = static_cast<char*>(mem);
+  auto* ent = reinterpret_cast<unsigned long long*>(b);
+  auto* start = reinterpret_cast<unsigned*>(b + o_start);
+  auto* geo = reinterpret_cast<float2*>(b + o_geo);
+  unsigned long long* nk = nullptr;
+  const int end_bit = 48 + bits_for(static_cast<unsigned long long>(n_slots - 1));
+  size_t temp = 0;
+  PACT_CUDA_S(cub::DeviceRadixSort::SortKeys(nullptr, temp, nk, nk, n, 0, end_bit, s));
+  void* scratch = nullptr;
+  PACT_CUDA_S(cudaMalloc(&scratch, al(8ull * n) + std::max<size_t>(temp, 16)));
+  auto hold_scratch = hold(scratch);
+  auto* keys = static_cast<unsigned long long*>(scratch);
+  side_runs_kernel<<<div_up(nr, 256), 256, 0, s>>>(p.rec, nr, a.W, a.H, off, keys, nullptr, geo);
+  PACT_TRY_S(after_launch(ctx, "side_runs_kernel"));
+  PACT_CUDA_S(cub::DeviceRadixSort::SortKeys(static_cast<char*>(scratch) + al(8ull * n), temp, keys, ent, n, 0,
+                                             end_bit, s));
+  group_bounds_kernel<<<div_up(static_cast<int>(n), 256), 256, 0, s>>>(ent, n, n_slots, 48, start, nullptr);
+  PACT_TRY_S(after_launch(ctx, "group_bounds_kernel"));
+  PACT_CUDA_S(cudaStreamSynchronize(s));
+  p.side_mem = hold_mem.release();
+  p.side_ent = ent;
+  p.side_start = start;
+  p.side_geo = geo;
+  p.n_side = n;
   return {};
 }
 
@@ -1385,7 +1623,8 @@ Status build_plan_data(pact_ctx* ctx, cudaStream_t s, const RayArgs& a, RayPlanD
   p.items = reinterpret_cast<const int4*>(b + o_items);
   p.ray_slots = reinterpret_cast<const int2*>(b + o_slots);
   p.n_items = ni;
-  return build_cell_plan(ctx, s, a, p);
+  PACT_TRY_S(build_cell_plan(ctx, s, a, p));
+  return build_side_plan(ctx, s, a, p);
 }
 
 // Plans of one context, by geometry (most recent first, a few kept).
@@ -1413,6 +1652,9 @@ RayPlanCache& plan_cache(pact_ctx* ctx) {
 }  // namespace
 
 static void set_cell_args(RayArgs& a, const RayPlanData& d) {
+  a.side_ent = d.side_ent;
+  a.side_start = d.side_start;
+  a.side_geo = d.side_geo;
   a.cell_start = d.cell_start;
   a.cell_ent = d.cell_ent;
   a.cell_sb = d.cell_sb;
@@ -1430,6 +1672,7 @@ Status ray_plan_get(pact_ctx* cache_ctx, pact_ctx* ctx, RayArgs& a, const double
   ray_plan_release(out, ctx->stream);
   a.cell_start = nullptr;
   a.cell_ent = nullptr;
+  a.side_ent = nullptr;
   a.rec = nullptr;
   a.items = nullptr;
   a.ray_slots = nullptr;
@@ -1493,6 +1736,8 @@ Status launch_wavefront(pact_ctx* ctx, const RayArgs& a, float* w) {
   const size_t smem = border_smem(a);
   if (a.tex) {  // make_raster_texture requires W, H >= 2
     if (!a.rec) return internal_error("launch_wavefront: ray plan missing");
+    // (the forward keeps its border-line items: without a carry they are as
+    // cheap per step as the side gather, and a ray's sum stays in one place)
     if (a.n_items > 0) {
       PACT_TRY_S(smem_optin(wavefront_plan_kernel, smem));
       wavefront_plan_kernel<<<div_up(a.n_items, kPlanBlock), kPlanBlock, smem, ctx->stream>>>(a);
@@ -1511,15 +1756,20 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
   if (a.n_rays == 0) return {};
   // fixed-point accumulators: raster [H W] | border replicas | bound statistics,
   // zero between launches (fix_to_grad_kernel resets what it reads); with a
-  // cell plan also the per-ray deposit scales and the cell corner sums
+  // cell / side plan also the per-ray deposit scales, the cell corner sums
+  // and the border cells' sums
   const size_t npx = static_cast<size_t>(a.W) * a.H;
-  const size_t rep_n = static_cast<size_t>(kBorderReplicas) * 2 * (a.W + a.H);
+  const int n_slots = 2 * (a.W + a.H);
+  const size_t rep_n = static_cast<size_t>(kBorderReplicas) * n_slots;
   const bool cells = a.tex && a.rec && a.cell_start;
+  const bool side = a.tex && a.rec && a.side_ent;
   const size_t n_cells = cells ? static_cast<size_t>(a.W - 1) * (a.H - 1) : 0;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t fix_bytes = sizeof(unsigned long long) * (npx + rep_n + 2);
-  const size_t gsc_off = (fix_bytes + 255) & ~size_t(255);
-  const size_t cell_off = (gsc_off + sizeof(float) * (cells ? a.n_rays : 0) + 255) & ~size_t(255);
-  const size_t bytes = cell_off + 4 * sizeof(unsigned long long) * n_cells;
+  const size_t gsc_off = al(fix_bytes);
+  const size_t cell_off = al(gsc_off + sizeof(float) * (cells || side ? a.n_rays : 0));
+  const size_t side_off = al(cell_off + 4 * sizeof(unsigned long long) * n_cells);
+  const size_t bytes = side_off + 2 * sizeof(unsigned long long) * (side ? n_slots : 0);
   pact_scratch& sc = ctx->scratch[kScratchRayBorder];
   const void* before = sc.ptr;
   void* base = nullptr;
@@ -1528,8 +1778,10 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
   auto* acc = static_cast<unsigned long long*>(base);
   auto* rep = acc + npx;
   auto* stats = rep + rep_n;
-  float* gsc = cells ? reinterpret_cast<float*>(static_cast<char*>(base) + gsc_off) : nullptr;
-  auto* cell_sums = cells ? reinterpret_cast<unsigned long long*>(static_cast<char*>(base) + cell_off) : nullptr;
+  char* cb = static_cast<char*>(base);
+  float* gsc = cells || side ? reinterpret_cast<float*>(cb + gsc_off) : nullptr;
+  auto* cell_sums = cells ? reinterpret_cast<unsigned long long*>(cb + cell_off) : nullptr;
+  auto* side_cells = side ? reinterpret_cast<unsigned long long*>(cb + side_off) : nullptr;
   PACT_CUDA_S(cudaMemsetAsync(stats, 0, 2 * sizeof(unsigned long long), ctx->stream));
   const int nb = std::max(1, div_up(std::max(static_cast<int>(npx), a.n_rays), 256 * 4));
   ray_bound_kernel<<<nb, 256, 0, ctx->stream>>>(dw, a.n_rays, a.dv, static_cast<int>(npx),
@@ -1537,8 +1789,11 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
   PACT_TRY_S(after_launch(ctx, "ray_bound_kernel"));
   if (a.tex) {
     if (!a.rec) return internal_error("launch_ray_backward: ray plan missing");
-    // the interior items go to the cell gather when there is a cell plan
-    const int skip_lo = cells ? a.n_gen_items : a.n_items, skip_n = cells ? a.n_int_items : 0;
+    // the interior items go to the cell gather, the side items to the side
+    // gather, when there are such plans (items: generic | interior | side)
+    const int lo = cells ? a.n_gen_items : a.n_gen_items + a.n_int_items;
+    const int hi = side ? a.n_items : a.n_gen_items + a.n_int_items;
+    const int skip_lo = cells || side ? lo : a.n_items, skip_n = cells || side ? std::max(0, hi - lo) : 0;
     const int n_run = a.n_items - skip_n;
     if (n_run > 0) {
       PACT_TRY_S(smem_optin(ray_backward_plan_kernel, smem));
@@ -1558,14 +1813,19 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
       }
       PACT_TRY_S(after_launch(ctx, "cell_gather_kernel"));
     }
+    if (side) {
+      side_gather_kernel<<<n_slots, kSideThreads, 0, ctx->stream>>>(a, gsc, stats, side_cells);
+      PACT_TRY_S(after_launch(ctx, "side_gather_kernel"));
+      corner_adjoint_kernel<<<div_up(a.n_rays, 256), 256, 0, ctx->stream>>>(a, gsc, stats, rep);
+      PACT_TRY_S(after_launch(ctx, "corner_adjoint_kernel"));
+    }
   } else {
     PACT_TRY_S(smem_optin(ray_backward_kernel<false>, smem));
     ray_backward_kernel<false><<<div_up(a.n_rays, 256), 256, smem, ctx->stream>>>(a, dw, acc, stats);
     PACT_TRY_S(after_launch(ctx, "ray_backward_kernel"));
   }
   if (a.tex) {
-    const int n_slots = 2 * (a.W + a.H);
-    border_fold_kernel<<<div_up(n_slots, 128), 128, 0, ctx->stream>>>(rep, a.W, a.H, acc);
+    border_fold_kernel<<<div_up(n_slots, 128), 128, 0, ctx->stream>>>(rep, a.W, a.H, side_cells, acc);
     PACT_TRY_S(after_launch(ctx, "border_fold_kernel"));
   }
   fix_to_grad_kernel<<<div_up(static_cast<int>(npx), 256), 256, 0, ctx->stream>>>(

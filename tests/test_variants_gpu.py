@@ -4,6 +4,8 @@ one cfg3 iteration (the benchmarked frame), each variant in its own process
 
   * the interior ray adjoint as a cell gather vs the per-ray kernel
     (PACT_RAY_CELLS=0): dL/dv, the gradient and dL/dw;
+  * the adjoint's border-line steps as a per-border-cell gather vs the
+    per-ray items (PACT_RAY_SIDE=0): dL/dv and the gradient;
   * the SIREN forward on split-fp16 MMAs with two tiles in flight vs 3xTF32
     (PACT_SIREN_F16=0): the wavefronts, dL/dv and the gradient.
 
@@ -44,6 +46,12 @@ def test_cell_gather_and_f16_chain_vs_replaced_variants(tmp_path):
     prod = _step(tmp_path, "product", {})
     cells_off = _step(tmp_path, "cells_off", {"PACT_RAY_CELLS": "0"})
     tf32 = _step(tmp_path, "tf32", {"PACT_SIREN_F16": "0"})
+    side_off = _step(tmp_path, "side_off", {"PACT_RAY_SIDE": "0"})
+    # side gather vs per-ray border-line items: same forward, adjoint to fixed-point rounding
+    assert np.array_equal(prod["w"], side_off["w"])
+    e_gv, e_g = _rel(prod["gv"], side_off["gv"]), _rel(prod["grad"], side_off["grad"])
+    print(f"side gather vs per-ray: dL/dv {e_gv:.2e} grad {e_g:.2e}")
+    assert e_gv <= 1e-6 and e_g <= 1e-6  # (a run's fp32 pixel sums group steps differently)
     # cell gather vs per-ray adjoint: same forward, adjoint to fixed-point rounding
     assert np.array_equal(prod["w"], cells_off["w"])
     e_gv, e_g = _rel(prod["gv"], cells_off["gv"]), _rel(prod["grad"], cells_off["grad"])
