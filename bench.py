@@ -104,7 +104,7 @@ class Clocks:
 
 def load_traffic():
     """Per-launch DRAM bytes of the hot kernels from the committed ncu capture."""
-    for name in ("traffic_r02c.json", "traffic_r02.json"):  # the latest committed capture
+    for name in ("traffic_r02d.json", "traffic_r02c.json", "traffic_r02.json"):  # the latest committed capture
         try:
             with open(os.path.join(ROOT, "profiles", name)) as f:
                 return json.load(f)

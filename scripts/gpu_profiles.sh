@@ -19,9 +19,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 8000 --csv --log-fi
     python bench.py --steps 2 --warmup 3 --no-cpu --no-cfg5 > gpurun_out/p_launches.log 2>&1; echo launches=$?
 python scripts/profile_iter.py --steps 1 > gpurun_out/p_iter.log 2>&1; echo iter=$?
 ncu --set full --clock-control none --import-source on \
-    -k regex:"ray_backward_plan|cell_gather|wavefront_plan|siren_chain_fwd|tc_bwd|loss_reg|loss_finish|patch_fft64|fix_to_grad|ray_bound|reduce_segments" -s 0 -c 14 \
+    -k regex:"ray_backward_plan|cell_gather|side_gather|wavefront_plan|siren_chain|tc_bwd|loss_reg|loss_finish|patch_fft64|fix_to_grad|ray_bound|reduce_segments" -s 0 -c 15 \
     -o gpurun_out/p_iter_full python scripts/profile_iter.py --steps 1 > gpurun_out/p_iter_full.log 2>&1; echo full=$?
-for k in ray_backward_plan cell_gather wavefront_plan loss_reg siren_chain_fwd patch_fft64; do
+for k in ray_backward_plan cell_gather side_gather wavefront_plan loss_reg siren_chain_pair patch_fft64; do
   python scripts/src_hot.py gpurun_out/p_iter_full.ncu-rep $k 30 > gpurun_out/p_hot_$k.txt 2>&1
 done
 export_rep p_iter_full
@@ -32,7 +32,7 @@ timeout 900 python scripts/profile_iter.py --steps 1 --cfg cfg5 > gpurun_out/p_i
 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/p_cfg5_launches.csv \
     python scripts/profile_iter.py --steps 1 --cfg cfg5 > gpurun_out/p_cfg5_launches.log 2>&1; echo cfg5_launches=$?
 ncu --set full --clock-control none --import-source on \
-    -k regex:"das_stack|tc_wide|siren_top|siren_first|wavefront_plan|ray_backward_plan|cell_gather|loss_reg|patch_fft" -c 12 \
+    -k regex:"das_stack|tc_wide|siren_top|siren_first|wavefront_plan|cell_gather|side_gather|loss_reg|patch_fft" -c 12 \
     -o gpurun_out/p_cfg5_full python scripts/profile_iter.py --steps 1 --cfg cfg5 > gpurun_out/p_cfg5_full.log 2>&1; echo cfg5_full=$?
 export_rep p_cfg5_full
 python scripts/traffic_json.py gpurun_out/p_traffic.json gpurun_out/p_iter_full_raw.csv.gz \
