@@ -468,6 +468,28 @@ int pact_trainer_local(pact_trainer* tr, int32_t* info);
 /* Last step's LossReport terms {data, tv, total} (host) and the NumericalError
  * check of joint_reconstruct; synchronises.  `epoch` is used in the message. */
 int pact_trainer_report(pact_trainer* tr, int32_t epoch, double* report3);
+
+/* ---- the multi-GPU frame over NCCL, without a host framework ----
+ * (the context owns the NCCL communicator; §8(e): the phase
+ * orchestration above.)  libnccl.so.2 is loaded at run time.
+ * Rank 0 makes a unique id and hands it to every rank out of band; each rank
+ * attaches it to the context that created its partitioned trainer. */
+#define PACT_NCCL_ID_BYTES 128
+int pact_nccl_unique_id(unsigned char* id /* [PACT_NCCL_ID_BYTES] */);
+int pact_ctx_attach_nccl(pact_ctx* ctx, const unsigned char* id, int32_t rank, int32_t world);
+/* n_steps iterations of a partitioned trainer (rank and world must match the
+ * communicator of the trainer's context): the phases 0, 6, 7, 2, 3 with the
+ * all-gather of dv (equal raster slabs; else all-reduce), the reduce-scatter
+ * of dL/dv (else all-reduce) overlapping phase 7, the all-reduces of the
+ * report, flags and gradient -- on the engine stream and a communication
+ * stream ordered by events; asynchronous.  world == 1 is pact_trainer_step
+ * by phases. */
+int pact_trainer_step_nccl(pact_trainer* tr, int32_t n_steps);
+/* The final image and SOS (optimize.hpp:478-486) of the whole frame on every
+ * rank: phases 4 (+ dv exchange) and 5 (+ all-reduce of the merge
+ * accumulators), image = num / den; device fp32 [H][W] each, on the caller's
+ * context stream. */
+int pact_trainer_finish_nccl(pact_trainer* tr, float* image, float* sos);
 /* One reported epoch (steps_per_epoch steps): report4 = {data, tv, total, wall_s}. */
 int pact_trainer_run_epoch(pact_trainer* tr, int32_t epoch, double* report4);
 /* Final render + deconvolution (optimize.hpp:478-486): device fp32 [H][W]

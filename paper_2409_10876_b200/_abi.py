@@ -174,6 +174,10 @@ SIGNATURES = {
                                                   C.POINTER(TrainConfig), C.POINTER(Partition),
                                                   C.POINTER(_P)]),
     "pact_trainer_phase": (C.c_int, [_P, _I]),
+    "pact_nccl_unique_id": (C.c_int, [_P]),
+    "pact_ctx_attach_nccl": (C.c_int, [_P, _P, _I, _I]),
+    "pact_trainer_step_nccl": (C.c_int, [_P, _I]),
+    "pact_trainer_finish_nccl": (C.c_int, [_P, _P, _P]),
     "pact_trainer_local": (C.c_int, [_P, C.POINTER(C.c_int32)]),
     "pact_trainer_step": (C.c_int, [_P, _I]),
     "pact_trainer_report": (C.c_int, [_P, _I, _DP]),

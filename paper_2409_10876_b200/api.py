@@ -130,6 +130,20 @@ class Context:
     def launch_count(self) -> int:
         return int(_abi.lib().pact_ctx_launch_count(self._h))
 
+    # ---- multi-GPU frame over NCCL (pact_ctx owns the communicator) -------
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        """pact_nccl_unique_id: rank 0 makes it, every rank attaches it."""
+        buf = (C.c_ubyte * 128)()
+        check(_abi.lib().pact_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def attach_nccl(self, uid: bytes, rank: int, world: int):
+        """pact_ctx_attach_nccl: ncclCommInitRank on this context's device."""
+        assert len(uid) == 128
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        check(_abi.lib().pact_ctx_attach_nccl(self._h, buf, int(rank), int(world)))
+
     # ---- part 1 -----------------------------------------------------------
     def das_stack(self, signals: torch.Tensor, ring: RingGeometry, meta: SignalMetaInfo,
                   grid: GridSpec, v0: float, delays, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -689,6 +703,19 @@ class Trainer:
         """pact_trainer_phase: one phase of the iteration (0-3; 1 = 6 then 7)
         or of the final image (4-5); asynchronous on the engine stream."""
         check(_abi.lib().pact_trainer_phase(self._h, int(k)))
+
+    def step_nccl(self, n: int = 1):
+        """pact_trainer_step_nccl: n iterations of a partitioned trainer with the
+        collectives over the NCCL communicator attached to its context
+        (Context.attach_nccl); no host framework involved."""
+        check(_abi.lib().pact_trainer_step_nccl(self._h, int(n)))
+
+    def finish_nccl(self):
+        """pact_trainer_finish_nccl: the whole frame's image and SOS on every rank."""
+        img = torch.empty((self.grid.height, self.grid.width), device="cuda", dtype=torch.float32)
+        sos = torch.empty_like(img)
+        check(_abi.lib().pact_trainer_finish_nccl(self._h, dptr(img), dptr(sos)))
+        return img, sos
 
     def local(self) -> dict:
         """The partition this trainer owns (pact_trainer_local)."""

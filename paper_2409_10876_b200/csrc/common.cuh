@@ -93,6 +93,7 @@ Status scratch_get(pact_ctx* ctx, int slot, size_t bytes, void** out);
 enum ExtSlot {
   kExtFourier = 0,   // fourier.cu: the table of pact_transfer_stack / pact_loss_grad
   kExtComposed = 1,  // composed.cu: fp64 bin tables of the composed-path entry points
+  kExtNccl = 2,      // nccl.cu: the NCCL communicator of the multi-GPU frame
 };
 
 template <class T>

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "geom.cuh"
+#include "nccl_api.cuh"
 #include "siren.cuh"
 #include "train_ops.cuh"
 
@@ -95,6 +96,9 @@ struct pact_trainer {
   cudaGraphExec_t graph = nullptr;
   int64_t graph_kernels = 0;
   int steps_done = 0;
+  // pact_trainer_step_nccl: the collectives' stream and its two ordering events
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_eng = nullptr, ev_comm = nullptr;
 };
 
 namespace {
@@ -222,6 +226,72 @@ T* carve(char*& p, size_t count) {
   T* r = reinterpret_cast<T*>(p);
   p += (sizeof(T) * count + 255) & ~size_t(255);
   return r;
+}
+
+// ---- the partitioned frame over NCCL (pact_trainer_step_nccl) ------------------
+struct NcclRun {
+  pact_trainer* tr;
+  const NcclApi* api;
+  NcclComm c;
+  bool slab;      // equal raster slabs: all-gather / reduce-scatter
+  size_t npx, lo;  // raster pixels, this rank's slab start
+  // the communication stream waits for the engine's work so far, or the reverse
+  Status comm_after_engine() {
+    PACT_CUDA_S(cudaEventRecord(tr->ev_eng, tr->eng.stream));
+    PACT_CUDA_S(cudaStreamWaitEvent(tr->comm_stream, tr->ev_eng, 0));
+    return {};
+  }
+  Status engine_after_comm() {
+    PACT_CUDA_S(cudaEventRecord(tr->ev_comm, tr->comm_stream));
+    PACT_CUDA_S(cudaStreamWaitEvent(tr->eng.stream, tr->ev_comm, 0));
+    return {};
+  }
+  Status all_reduce(void* buf, size_t n, ncclDataType_t t, ncclRedOp_t op, const char* what) {
+    return nccl_status(api->all_reduce(buf, buf, n, t, op, c.comm, tr->comm_stream), what);
+  }
+  // dv (f32): the rank's slab to everyone, or the all-reduce of the zeroed rasters
+  Status share_dv() {
+    if (!slab) return all_reduce(tr->dv, npx, ncclFloat32, ncclSum, "all-reduce dv");
+    const size_t cnt = npx / c.world;
+    return nccl_status(api->all_gather(tr->dv + lo, tr->dv, cnt, ncclFloat32, c.comm, tr->comm_stream),
+                       "all-gather dv");
+  }
+  // dL/dv (f64) to the slab owners (in place), or everywhere
+  Status reduce_gv() {
+    if (!slab) return all_reduce(tr->gv, npx, ncclFloat64, ncclSum, "all-reduce dL/dv");
+    const size_t cnt = npx / c.world;
+    return nccl_status(api->reduce_scatter(tr->gv, tr->gv + lo, cnt, ncclFloat64, ncclSum, c.comm,
+                                           tr->comm_stream),
+                       "reduce-scatter dL/dv");
+  }
+};
+
+Status nccl_run(pact_trainer* tr, NcclRun& r) {
+  r.tr = tr;
+  r.api = nccl_api();
+  if (!r.api) return internal_error("the NCCL path needs libnccl.so.2");
+  r.c = ctx_nccl(tr->user);
+  if (!r.c.comm) return validation("pact_trainer_step_nccl: no NCCL communicator attached to the context");
+  if (r.c.world != tr->world || r.c.rank != tr->rank)
+    return validation("pact_trainer_step_nccl: the communicator's rank / world differ from the trainer's");
+  if (!tr->comm_stream) {
+    PACT_CUDA_S(cudaStreamCreateWithFlags(&tr->comm_stream, cudaStreamNonBlocking));
+    PACT_CUDA_S(cudaEventCreateWithFlags(&tr->ev_eng, cudaEventDisableTiming));
+    PACT_CUDA_S(cudaEventCreateWithFlags(&tr->ev_comm, cudaEventDisableTiming));
+  }
+  r.npx = static_cast<size_t>(tr->grid.width) * tr->grid.height;
+  const size_t W = static_cast<size_t>(tr->world);
+  r.slab = static_cast<size_t>(tr->mp.n) == r.npx && r.npx % W == 0 &&
+           static_cast<size_t>(tr->m_lo) == tr->rank * r.npx / W &&
+           static_cast<size_t>(tr->m_hi) == (tr->rank + 1) * r.npx / W;
+  r.lo = r.slab ? static_cast<size_t>(tr->m_lo) : 0;
+  return {};
+}
+
+__global__ void merge_divide_kernel(const float* __restrict__ num, const float* __restrict__ den,
+                                    int n, float* __restrict__ img) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) img[i] = den[i] > 0.f ? num[i] / den[i] : 0.f;  // merge_patches (deconv.hpp:158-163)
 }
 
 }  // namespace
@@ -684,6 +754,12 @@ int pact_trainer_destroy(pact_trainer* tr) {
   if (tr->eng.stream) cudaStreamSynchronize(tr->eng.stream);
   if (tr->user) tr->user->launches.fetch_add(tr->eng.launches.exchange(0));
   if (tr->graph) cudaGraphExecDestroy(tr->graph);
+  if (tr->comm_stream) {
+    cudaStreamSynchronize(tr->comm_stream);
+    cudaStreamDestroy(tr->comm_stream);
+  }
+  if (tr->ev_eng) cudaEventDestroy(tr->ev_eng);
+  if (tr->ev_comm) cudaEventDestroy(tr->ev_comm);
   if (tr->ray.tex) cudaDestroyTextureObject(tr->ray.tex);
   ray_plan_release(tr->ray_plan, tr->eng.stream);
   siren_work_free(tr->sw);
@@ -693,6 +769,64 @@ int pact_trainer_destroy(pact_trainer* tr) {
   if (tr->eng.stream) cudaStreamSynchronize(tr->eng.stream);
   if (tr->eng.own_stream) cudaStreamDestroy(tr->eng.own_stream);
   delete tr;
+  return PACT_OK;
+}
+
+int pact_trainer_step_nccl(pact_trainer* tr, int32_t n_steps) {
+  if (!tr) return validation("pact_trainer_step_nccl: null trainer").code;
+  NcclRun r;
+  PACT_TRY(nccl_run(tr, r));
+  for (int i = 0; i < n_steps; ++i) {
+    PACT_TRY(enqueue_phase(tr, 0));  // render own pixels -> dv
+    PACT_TRY(r.comm_after_engine());
+    PACT_TRY(r.share_dv());
+    PACT_TRY(r.engine_after_comm());
+    PACT_TRY(enqueue_phase(tr, 6));  // wavefronts, loss, ray adjoint -> dL/dv
+    PACT_TRY(r.comm_after_engine());
+    PACT_TRY(r.reduce_gv());         // ... while the engine runs TV + the report
+    PACT_TRY(enqueue_phase(tr, 7));
+    PACT_TRY(r.comm_after_engine());
+    PACT_TRY(r.all_reduce(tr->report, 3, ncclFloat64, ncclSum, "all-reduce report"));
+    PACT_TRY(r.all_reduce(tr->flags, 1, ncclUint32, ncclMax, "all-reduce flags"));
+    PACT_TRY(r.engine_after_comm());
+    PACT_TRY(enqueue_phase(tr, 2));  // SIREN backward of own pixels -> gradient
+    PACT_TRY(r.comm_after_engine());
+    PACT_TRY(r.all_reduce(tr->grad, static_cast<size_t>(tr->n_params), ncclFloat64, ncclSum,
+                          "all-reduce gradient"));
+    PACT_TRY(r.engine_after_comm());
+    PACT_TRY(enqueue_phase(tr, 3));  // Adam, replicated: theta stays identical on every rank
+    ++tr->steps_done;
+  }
+  return PACT_OK;
+}
+
+int pact_trainer_finish_nccl(pact_trainer* tr, float* image, float* sos) {
+  if (!tr) return validation("pact_trainer_finish_nccl: null trainer").code;
+  if (tr->world == 1) return pact_trainer_finish(tr, image, sos);
+  NcclRun r;
+  PACT_TRY(nccl_run(tr, r));
+  pact_ctx* e = &tr->eng;
+  if (int rc = pact_trainer_phase(tr, 4)) return rc;  // final render of own pixels
+  PACT_TRY(r.comm_after_engine());
+  PACT_TRY(r.share_dv());
+  PACT_TRY(r.engine_after_comm());
+  if (image) {
+    if (int rc = pact_trainer_phase(tr, 5)) return rc;  // own patches -> merge accumulators
+    PACT_TRY(r.comm_after_engine());
+    PACT_TRY(r.all_reduce(tr->num, r.npx, ncclFloat32, ncclSum, "all-reduce merge numerator"));
+    PACT_TRY(r.all_reduce(tr->den, r.npx, ncclFloat32, ncclSum, "all-reduce merge weights"));
+    PACT_TRY(r.engine_after_comm());
+    merge_divide_kernel<<<div_up(static_cast<int>(r.npx), 256), 256, 0, e->stream>>>(
+        tr->num, tr->den, static_cast<int>(r.npx), image);
+    PACT_TRY(after_launch(e, "merge_divide_kernel"));
+  }
+  if (sos) PACT_TRY(launch_sos_from_dev(e, tr->dv, r.npx, tr->v0, sos));
+  cudaEvent_t ev;
+  cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  cudaEventRecord(ev, e->stream);
+  cudaStreamWaitEvent(tr->user->stream, ev, 0);
+  cudaEventDestroy(ev);
+  tr->user->launches.fetch_add(e->launches.exchange(0));
   return PACT_OK;
 }
 

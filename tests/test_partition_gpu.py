@@ -137,3 +137,33 @@ def test_partitioned_frame_matches_single_rank(ctx, world):
     assert rel_l2(thetas[0], want_th) <= 1e-6
     assert rel_l2(sos.double().cpu().numpy() - w.v0, want_sos.double().cpu().numpy() - w.v0) <= 1e-5
     assert rel_l2(img.double().cpu().numpy(), want_img.double().cpu().numpy()) <= 1e-5
+
+
+def test_world1_nccl_step_equals_fused_step(ctx):
+    """The library's own NCCL orchestration (pact_ctx_attach_nccl +
+    pact_trainer_step_nccl / finish_nccl, no host framework) on a one-rank
+    communicator: bitwise the fused (graph) step and the single-GPU finish.
+    More ranks need more GPUs (ranks whose kernels wait on one another must
+    not share a GPU); the orchestration is the same code for any world."""
+    from paper_2409_10876_b200.api import Context
+
+    G = gu.load("small_instance")
+    si = gu.small_instance()
+    cfg = replace(si.cfg, seed=3, use_cuda_graph=True)
+    sig = torch.as_tensor(G["sig"]).cuda()
+    meta = gu.meta(G["meta"])
+    c1 = Context(0)
+    c1.attach_nccl(Context.nccl_unique_id(), 0, 1)
+    a = Trainer(ctx, sig, si.ring, meta, si.grid, si.mask, cfg)
+    b = Trainer(c1, sig, si.ring, meta, si.grid, si.mask, cfg, partition=(0, 1))
+    a.step(3)
+    b.step_nccl(3)
+    assert a.report(1) == b.report(1)
+    assert np.array_equal(a.theta(), b.theta())
+    ia, sa = a.finish()
+    ib, sb = b.finish_nccl()
+    torch.cuda.synchronize()
+    assert torch.equal(ia, ib) and torch.equal(sa, sb)
+    a.close()
+    b.close()
+    c1.close()
