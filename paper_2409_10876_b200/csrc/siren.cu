@@ -74,13 +74,8 @@ namespace {
 
 constexpr int BM = 128, BK = 16, NT = 256;
 
-// x mod 2pi into [-pi, pi] (two-constant Cody-Waite), so the MUFU sine/cosine
-// run on their accurate range (abs. error ~4e-7, below the fp32 rounding of
-// the argument w0 * a itself).
-__device__ __forceinline__ float red2pi(float x) {
-  const float k = rintf(x * 0.159154943091895336f);
-  return fmaf(-k, -1.74845553146951720e-07f, fmaf(-k, 6.28318548202514648f, x));
-}
+// the argument reduction of every SIREN kernel (siren.cuh)
+__device__ __forceinline__ float red2pi(float x) { return sine_reduce(x); }
 __device__ __forceinline__ float sinw(float a, float w0) { return __sinf(red2pi(w0 * a)); }
 __device__ __forceinline__ float dsinw(float a, float w0) { return w0 * __cosf(red2pi(w0 * a)); }
 __device__ __forceinline__ void sincosw(float a, float w0, float* s, float* c) {

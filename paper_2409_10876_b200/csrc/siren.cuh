@@ -8,6 +8,20 @@
 
 namespace pactgpu {
 
+// x mod 2pi into [-pi, pi] (two-constant Cody-Waite), so the MUFU sine/cosine
+// run on their accurate range (abs. error ~4e-7, below the fp32 rounding of
+// the argument w0 * a itself).  k = round(x / 2pi) comes from the 1.5 * 2^23
+// shifter on the FMA pipe (one FFMA + one FADD, exact for |x| < 2pi * 2^22)
+// rather than FMUL + FRND: FRND issues on the same quarter-rate unit as the
+// MUFU sine itself.  Every SIREN kernel (forward and backward) uses this one
+// definition, so a_l -> sin(w0 a_l) is the same function everywhere.
+#ifdef __CUDACC__
+__device__ __forceinline__ float sine_reduce(float x) {
+  const float k = __fadd_rn(__fmaf_rn(x, 0.159154943091895336f, 12582912.f), -12582912.f);
+  return fmaf(-k, -1.74845553146951720e-07f, fmaf(-k, 6.28318548202514648f, x));
+}
+#endif
+
 struct SirenShape {
   int in_dim = 2;
   int hidden = 64;

@@ -139,10 +139,7 @@ struct BwdBars {
   uint32_t tslot;
 };
 
-__device__ __forceinline__ float red2pi_b(float x) {
-  const float k = rintf(x * 0.159154943091895336f);
-  return fmaf(-k, -1.74845553146951720e-07f, fmaf(-k, 6.28318548202514648f, x));
-}
+__device__ __forceinline__ float red2pi_b(float x) { return sine_reduce(x); }
 __device__ __forceinline__ void sincos_w(float a, float w0, float* s, float* c) {
   __sincosf(red2pi_b(w0 * a), s, c);
 }
@@ -175,8 +172,7 @@ tc_bwd_kernel(BwdArgs a, const __grid_constant__ CUtensorMap tmap_x) {
   extern __shared__ unsigned char smem_dyn[];
   // pda[x]: dA hi [4 chunks][BT][32] | dA lo;  pz[z]: z hi [BH][BT] | z lo  (SW128)
   // raw[r]: a_{l-1} tile [BT][BH] (contiguous rows)
-  float* pda = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) &
-                                        ~static_cast<uintptr_t>(1023));
+  float* pda = tc::smem_align1024<float>(smem_dyn);
   float* pz = pda + ND * 2 * kDa;
   float* raw = pz + NZ * 2 * kZ;
   float* red = raw + NR * kRaw;  // [2][BH] bias, [2][BH] head, [2] gb, pad; then [3][BH] fp64

@@ -89,10 +89,7 @@ struct ChainArgs {
   int store_a0;  // 0: a_0 is not written (the fused backward recomputes it)
 };
 
-__device__ __forceinline__ float red2pi_c(float x) {
-  const float k = rintf(x * 0.159154943091895336f);
-  return fmaf(-k, -1.74845553146951720e-07f, fmaf(-k, 6.28318548202514648f, x));
-}
+__device__ __forceinline__ float red2pi_c(float x) { return sine_reduce(x); }
 __device__ __forceinline__ float sinw(float a, float w0) { return __sinf(red2pi_c(w0 * a)); }
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
@@ -155,8 +152,7 @@ siren_chain_fwd_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_act
   constexpr uint32_t kAlo = F16 ? 64u : kColAlo;     // TMEM column of A lo
   constexpr float kDs = F16 ? 1.f / kF16Scale : 1.f;  // accumulator scale
   extern __shared__ unsigned char smem_dyn[];
-  float* wring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) &
-                                          ~static_cast<uintptr_t>(1023));  // [WS][2][128][32]
+  float* wring = tc::smem_align1024<float>(smem_dyn);  // [WS][2][128][32]
   float* s_tr = wring + WS * 2 * kPlaneFloats;  // [16 warps] SW128 store boxes (1024-aligned)
   float* s_w0 = s_tr + kEpiWarps * kBoxBytes / 4;                          // [128][2]
   float* s_b0 = s_w0 + 2 * CH;                                             // [128]
@@ -472,8 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 siren_chain_pair_kernel(ChainArgs a, const __grid_constant__ CUtensorMap tmap_acts) {
   constexpr float kDs = 1.f / kF16Scale;
   extern __shared__ unsigned char smem_dyn[];
-  float* wring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) &
-                                          ~static_cast<uintptr_t>(1023));  // [2][2][128][64 fp16]
+  float* wring = tc::smem_align1024<float>(smem_dyn);  // [2][2][128][64 fp16]
   float* s_tr = wring + WS * 2 * kPlaneFloats;  // [16 warps] SW128 store boxes (1024-aligned)
   float* s_w0 = s_tr + kEpiWarps * kBoxBytes / 4;                          // [128][2]
   float* s_b0 = s_w0 + 2 * CH;                                             // [128]

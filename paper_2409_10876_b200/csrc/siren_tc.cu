@@ -60,10 +60,7 @@ constexpr int H = 128;    // hidden width handled here
 constexpr int TP = 128;   // pixels per layer tile (MMA N)
 constexpr int KC = 32;    // K per staged chunk
 
-__device__ __forceinline__ float red2pi_tc(float x) {
-  const float k = rintf(x * 0.159154943091895336f);
-  return fmaf(-k, -1.74845553146951720e-07f, fmaf(-k, 6.28318548202514648f, x));
-}
+__device__ __forceinline__ float red2pi_tc(float x) { return sine_reduce(x); }
 __device__ __forceinline__ float sin_w(float a, float w0) { return __sinf(red2pi_tc(w0 * a)); }
 __device__ __forceinline__ float dsin_w(float a, float w0) {
   return w0 * __cosf(red2pi_tc(w0 * a));
@@ -154,8 +151,7 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
                 int n, float w0, float* __restrict__ Y, SirenHead head) {
   extern __shared__ unsigned char smem_dyn[];
   // 1024-B alignment: the 128-B swizzle is a function of the address bits
-  float* raw = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) &
-                                        ~static_cast<uintptr_t>(1023));  // [2][TP][H]
+  float* raw = tc::smem_align1024<float>(smem_dyn);  // [2][TP][H]
   float* zh = raw + 2 * TP * H;                                         // [2][TP][KC] SW128
   float* zl = zh + 2 * TP * KC;                                         // [2][TP][KC] SW128
   float* wst = raw + TP * H;  // prologue only: W staged [H][H + 1] over raw[1] and the planes

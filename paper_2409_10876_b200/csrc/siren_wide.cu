@@ -57,10 +57,7 @@ constexpr int kWideThreads = 32 * 18;  // loader, MMA, 8 producer warps, 8 epilo
 
 enum : int { kWideFwd = 0, kWideDgrad = 1 };
 
-__device__ __forceinline__ float red2pi_w(float x) {
-  const float k = rintf(x * 0.159154943091895336f);
-  return fmaf(-k, -1.74845553146951720e-07f, fmaf(-k, 6.28318548202514648f, x));
-}
+__device__ __forceinline__ float red2pi_w(float x) { return sine_reduce(x); }
 
 __device__ __forceinline__ uint32_t sa(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -153,8 +150,7 @@ tc_wide_layer_kernel(const __grid_constant__ CUtensorMap tmap_in,
                      const float* __restrict__ bias, const float* __restrict__ Aprev, int n, float w0,
                      float* __restrict__ Y) {
   extern __shared__ unsigned char smem_dyn[];
-  float* st = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) &
-                                       ~static_cast<uintptr_t>(1023));  // [WNS][kStage]
+  float* st = tc::smem_align1024<float>(smem_dyn);  // [WNS][kStage]
   float* s_bias = st + WNS * kStage;                                    // [WH]
   float* s_box = s_bias + WH;  // [8 epilogue warps][32 x 32] SW128 output boxes (1024-aligned)
   __shared__ WideBars sb;
@@ -337,8 +333,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
 tc_wide_wgrad_kernel(const float* __restrict__ dA, const float* __restrict__ Aprev, int n, int rows,
                      float w0, float* __restrict__ partial) {
   extern __shared__ unsigned char smem_dyn[];
-  float* pl = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) &
-                                       ~static_cast<uintptr_t>(1023));  // [kWSlot]
+  float* pl = tc::smem_align1024<float>(smem_dyn);  // [kWSlot]
   float* raw = pl + kWSlot;                                             // dA [WP][WH] | a [WP][WH]
   __shared__ WgBars sb;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

@@ -166,6 +166,16 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+// 1024-B aligned start inside the dynamic shared window, formed by pointer
+// arithmetic on the __shared__ array itself: a uintptr_t round trip hides the
+// address space from the compiler and every access through the result
+// becomes a generic LD/ST instead of LDS/STS.
+template <class T>
+__device__ __forceinline__ T* smem_align1024(unsigned char* base) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(base));
+  return reinterpret_cast<T*>(base + ((1024u - (s & 1023u)) & 1023u));
+}
+
 // ---- TMEM ----------------------------------------------------------------
 // Called by one full warp; writes the TMEM base address to *slot (smem).
 template <int NCOLS>
