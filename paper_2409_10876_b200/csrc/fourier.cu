@@ -557,6 +557,7 @@ __global__ void __launch_bounds__(2 * LB) loss_bins_kernel(FourierTab t, const f
   auto issue = [&](int c, int st) {  // thread 0 arms, threads < K + 1 copy
     const int patch = c / chunks, b0 = (c - patch * chunks) * LB;
     float* base = smem + st * stage_floats;
+    tc::fence_proxy_async();  // the stage's generic reads (before the barrier) vs the async refill
     if (threadIdx.x == 0)
       tc::mbar_expect_tx(&bar[st], static_cast<uint32_t>(K * LB * 8 + A * 4));
     __syncwarp();

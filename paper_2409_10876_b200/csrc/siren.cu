@@ -922,10 +922,14 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
     const size_t sz_w = al64(static_cast<size_t>(grid) * per_w),
                  sz_top = al64(static_cast<size_t>(grid) * (H + 1)),
                  sz_0 = static_cast<size_t>(grid) * 3 * H;
-    PACT_TRY_S(ensure_partial(w, sz_top + (L - 1) * sz_w + sz_0, st));
+    const bool f16 = tc_bwd_f16();
+    PACT_TRY_S(ensure_partial(w, sz_top + (L - 1) * sz_w + sz_0 + kMaxSeg, st));
     float* part_top = w.partial;
     float* part_w = part_top + sz_top;
     float* part_0 = part_w + (L - 1) * sz_w;
+    // split fp16: the per-layer maxima that set the dA scales (siren_bwd16.cu)
+    unsigned* mx = reinterpret_cast<unsigned*>(part_0 + sz_0);
+    if (f16) PACT_CUDA_S(cudaMemsetAsync(mx, 0, sizeof(unsigned) * L, st));
     float* cur = w.dA;
     float* nxt = w.dB;
     for (int l = L - 1; l >= 1; --l) {
@@ -949,7 +953,10 @@ Status siren_backward(pact_ctx* ctx, const SirenShape& s, const float* theta, Si
       a.part_w = part_w + (l - 1) * sz_w;
       a.part_top = part_top;
       a.part_0 = part_0;
-      PACT_TRY_S(tc_bwd_layer(ctx, top, bottom, a));
+      if (f16)
+        PACT_TRY_S(tc_bwd16_layer(ctx, top, bottom, a, mx + (L - 1 - l), mx + (L - l)));
+      else
+        PACT_TRY_S(tc_bwd_layer(ctx, top, bottom, a));
       add_seg(a.part_w, grid, static_cast<int>(per_w), grad + s.offset(l));
       std::swap(cur, nxt);
     }

@@ -146,5 +146,12 @@ Status tc_wide_wgrad_layer(pact_ctx* ctx, const float* dAl, const float* Aprev, 
                            float w0, float* partial, int n_chunks);
 int tc_bwd_grid(pact_ctx* ctx, int n);  // CTAs (= partial rows) of tc_bwd_layer
 Status tc_bwd_layer(pact_ctx* ctx, bool top, bool bottom, const TcBwdLayer& layer);
+// The same layer on split-fp16 kind::f16 MMAs (siren_bwd16.cu; the default,
+// PACT_SIREN_BWD_F16=0 selects tc_bwd_layer).  mx_in: bits of max|dA_l| (TOP:
+// written here, max|g s|); mx_out: bits of max|dA_{l-1}| (atomicMax).  Both
+// zeroed by the caller before the top layer.
+bool tc_bwd_f16();
+Status tc_bwd16_layer(pact_ctx* ctx, bool top, bool bottom, const TcBwdLayer& layer, unsigned* mx_in,
+                      unsigned* mx_out);
 
 }  // namespace pactgpu

@@ -501,6 +501,7 @@ tc_bwd_kernel(BwdArgs a, const __grid_constant__ CUtensorMap tmap_x) {
         tc::mbar_arrive(&sb.rfree[r]);
         if (loader && i + NR < my_tiles) {
           tc::mbar_wait(&sb.rfree[r], (i / NR) & 1);
+          tc::fence_proxy_async();  // generic reads of the slot before the refill
           load_raw(i + NR);
         }
       }

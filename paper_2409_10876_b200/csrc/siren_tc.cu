@@ -179,6 +179,7 @@ tc_layer_kernel(const float* __restrict__ X,      // [n][H] MMA input rows (a_{l
   auto load_tile = [&](int i) {
     const int m0 = (blockIdx.x + i * gridDim.x) * TP;
     const uint32_t bytes = static_cast<uint32_t>(min(TP, n - m0)) * H * 4;
+    tc::fence_proxy_async();  // the buffer's generic reads before the async refill
     tc::mbar_expect_tx(&sb.raw[i & 1], bytes);
     tc::bulk_load(raw + (i & 1) * TP * H, X + static_cast<size_t>(m0) * H, bytes, &sb.raw[i & 1]);
   };
@@ -442,6 +443,7 @@ tc_wgrad_kernel(const float* __restrict__ dA, const float* __restrict__ Aprev, i
     const int p0 = m_begin + i * WP;
     const uint32_t bytes = static_cast<uint32_t>(min(WP, m_end - p0)) * H * 4;
     uint64_t* bar = &sb.raw[i & 1];
+    tc::fence_proxy_async();  // the buffer's generic reads before the async refill
     tc::mbar_expect_tx(bar, 2 * bytes);
     tc::bulk_load(rda + (i & 1) * WP * H, dA + static_cast<size_t>(p0) * H, bytes, bar);
     tc::bulk_load(rap + (i & 1) * WP * H, Aprev + static_cast<size_t>(p0) * H, bytes, bar);

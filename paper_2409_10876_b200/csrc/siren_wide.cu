@@ -355,6 +355,7 @@ tc_wide_wgrad_kernel(const float* __restrict__ dA, const float* __restrict__ Apr
   auto load = [&](int i) {
     const int p0 = m_begin + i * WP;
     const uint32_t bytes = static_cast<uint32_t>(min(WP, m_end - p0)) * WH * 4;
+    tc::fence_proxy_async();  // the producers' generic reads before the async refill
     tc::mbar_expect_tx(&sb.rfull, 2 * bytes);
     tc::bulk_load(raw, dA + static_cast<size_t>(p0) * WH, bytes, &sb.rfull);
     tc::bulk_load(raw + kRawW, Aprev + static_cast<size_t>(p0) * WH, bytes, &sb.rfull);

@@ -7,7 +7,9 @@ one cfg3 iteration (the benchmarked frame), each variant in its own process
   * the adjoint's border-line steps as a per-border-cell gather vs the
     per-ray items (PACT_RAY_SIDE=0): dL/dv and the gradient;
   * the SIREN forward on split-fp16 MMAs with two tiles in flight vs 3xTF32
-    (PACT_SIREN_F16=0): the wavefronts, dL/dv and the gradient.
+    (PACT_SIREN_F16=0): the wavefronts, dL/dv and the gradient;
+  * the SIREN backward on split-fp16 MMAs (power-of-two operand scales) vs
+    3xTF32 (PACT_SIREN_BWD_F16=0): the gradient (the forward is identical).
 
 Both products are fp32-accurate: the cell gather sums the same deposits in
 another order (fixed point per cell corner), split fp16 carries the same 22
@@ -61,3 +63,9 @@ def test_cell_gather_and_f16_chain_vs_replaced_variants(tmp_path):
     e_w, e_gv2, e_g2 = (_rel(prod[k], tf32[k]) for k in ("w", "gv", "grad"))
     print(f"split fp16 vs 3xTF32 forward: w {e_w:.2e} dL/dv {e_gv2:.2e} grad {e_g2:.2e}")
     assert e_w <= 1e-5 and e_gv2 <= 1e-5 and e_g2 <= 1e-5
+    # split-fp16 backward vs 3xTF32 backward: same forward and adjoint
+    bwd32 = _step(tmp_path, "bwd_tf32", {"PACT_SIREN_BWD_F16": "0"})
+    assert np.array_equal(prod["w"], bwd32["w"]) and np.array_equal(prod["gv"], bwd32["gv"])
+    e_g3 = _rel(prod["grad"], bwd32["grad"])
+    print(f"split fp16 vs 3xTF32 backward: grad {e_g3:.2e}")
+    assert e_g3 <= 1e-5
