@@ -38,9 +38,10 @@
 // refilled as soon as the producers have read it, and the MMAs of a tile
 // issue in order (wgrad(i), dgrad(i)).
 // Roles: warps 0-7 own dA (thread = pixel and 8 features), warps 8-15 own
-// a_{l-1} (thread = feature k, 16 pixels), warp 16 issues the MMAs, warps
-// 17-24 drain D_g (thread = feature k: coalesced stores of dA_{l-1}) and
-// issue the raw a_{l-1} loads.  Partials are per CTA, reduced in fixed
+// a_{l-1} (thread = feature k, 16 pixels: z = sin(w0 a) and the epilogue's
+// factor w0 cos(w0 a) from one argument reduction; they issue the raw a_{l-1}
+// loads), warp 16 issues the MMAs, warps 17-24 drain D_g (thread = feature
+// k: coalesced stores of dA_{l-1}).  Partials are per CTA, reduced in fixed
 // orders here and in fp64 by the caller (deterministic).
 #include <cstdint>
 #include <cstdlib>
@@ -89,10 +90,14 @@ constexpr int HP = BT / 2;
 #ifndef BWD16_NR
 #define BWD16_NR 3
 #endif
-constexpr int NX = BWD16_NX, ND = BWD16_ND, NZ = BWD16_NZ, NR = BWD16_NR;
+#ifndef BWD16_NC
+#define BWD16_NC 2
+#endif
+constexpr int NX = BWD16_NX, ND = BWD16_ND, NZ = BWD16_NZ, NR = BWD16_NR, NC = BWD16_NC;
 constexpr uint32_t kRaw = BT * BH;          // floats of a raw tile (16 KB)
 constexpr uint32_t kPlane = BT * BH;        // 32-bit words of one dA buffer: hi 2 x 4 KB | lo 2 x 4 KB
 constexpr uint32_t kZPlane = BH * 32;       // 32-bit words of one z buffer (16 KB)
+constexpr uint32_t kCw = BT * BH;           // floats of one cosine-factor buffer (16 KB)
 constexpr int kDW = 8, kZW = 8, kEpiW = 8;  // warps per role
 constexpr int kMmaWarp = kDW + kZW;         // 16
 constexpr int kThr = 32 * (kDW + kZW + 1 + kEpiW);  // 800
@@ -121,7 +126,8 @@ struct Bwd16Args {
 
 struct Bwd16Bars {
   uint64_t xfull[NX], xfree[NX];  // raw dA_l slot landed / read (dA producers)
-  uint64_t rfull[NR], rfree[NR];  // raw a_{l-1} slot landed / read (z producers + epilogue)
+  uint64_t rfull[NR], rfree[NR];  // raw a_{l-1} slot landed / read (z producers)
+  uint64_t cready[NC], cfree[NC]; // cosine factors written (z producers) / read (epilogue)
   uint64_t zready[NZ], zfree[NZ]; // z planes written / weight-gradient MMAs done with them
   uint64_t gready[ND], pfree[ND]; // dA planes written / data-gradient MMAs done with them
   uint64_t dfull[2], dfree[2];    // D_g[b] ready (commit) / drained (epilogue)
@@ -196,7 +202,8 @@ __global__ void __launch_bounds__(kThr, 1) tc_bwd16_kernel(Bwd16Args a) {
   uint32_t* pz = pda + ND * kPlane;                          // [NZ][128 rows][hi 16 | lo 16 words]
   float* xr = reinterpret_cast<float*>(pz + NZ * kZPlane);   // [NX][BT][BH]
   float* raw = xr + NX * kRaw;                               // [NR][BT][BH]
-  float* red = raw + NR * kRaw;  // [8][BH] bias, [8][BH] head, [8] gb, pad; then [3][BH] fp64
+  float* pc = raw + NR * kRaw;   // [NC][2 h][BH k][16 t] w0 cos(w0 a_{l-1}) (16-B chunks swizzled)
+  float* red = pc + NC * kCw;    // [8][BH] bias, [8][BH] head, [8] gb, pad; then [3][BH] fp64
   float* wst = reinterpret_cast<float*>(pda);  // prologue: W staged [BH][BH + 1] over planes + xr
   __shared__ Bwd16Bars sb;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -208,7 +215,11 @@ __global__ void __launch_bounds__(kThr, 1) tc_bwd16_kernel(Bwd16Args a) {
     }
     for (int i = 0; i < NR; ++i) {
       tc::mbar_init(&sb.rfull[i], 1);
-      tc::mbar_init(&sb.rfree[i], 32 * (kZW + kEpiW));
+      tc::mbar_init(&sb.rfree[i], 32 * kZW);
+    }
+    for (int i = 0; i < NC; ++i) {
+      tc::mbar_init(&sb.cready[i], 32 * kZW);
+      tc::mbar_init(&sb.cfree[i], 32 * kEpiW);
     }
     for (int i = 0; i < NZ; ++i) {
       tc::mbar_init(&sb.zready[i], 32 * kZW);
@@ -442,18 +453,28 @@ __global__ void __launch_bounds__(kThr, 1) tc_bwd16_kernel(Bwd16Args a) {
       if (!BOTTOM) tc::mbar_wait(&sb.rfull[r], (i / NR) & 1);
       BTRACE(warp == kDW && lane == 0, 5, i);
       const float* ar = raw + r * kRaw + pb * BH + k;
-      float z[HP];
+      float z[HP], cw[HP];
 #pragma unroll
       for (int t = 0; t < HP; ++t) {
         const float av = BOTTOM ? fmaf(w0y, __shfl_sync(0xffffffffu, cc.y, t),
                                        fmaf(w0x, __shfl_sync(0xffffffffu, cc.x, t), b0k))
                                 : ar[t * BH];
-        // computed for every row, then selected: a conditional evaluation
-        // becomes one branch per pixel and serialises the loads and the sines
-        const float zt = __sinf(sine_reduce(w0 * av));
-        z[t] = pb + t < rows ? zt : 0.f;
+        // z = sin(w0 a) for the weight gradient and the epilogue's factor
+        // w0 cos(w0 a) from one argument reduction; computed for every row,
+        // then selected (a conditional evaluation becomes a branch per pixel)
+        float sz, cz;
+        __sincosf(sine_reduce(w0 * av), &sz, &cz);
+        z[t] = pb + t < rows ? sz : 0.f;
+        cw[t] = w0 * cz;
       }
-      if (!BOTTOM) tc::mbar_arrive(&sb.rfree[r]);
+      if (!BOTTOM) {
+        tc::mbar_arrive(&sb.rfree[r]);
+        if (tid == 32 * kDW && i + NR < my_tiles) {  // the raw loader
+          tc::mbar_wait(&sb.rfree[r], (i / NR) & 1);
+          tc::fence_proxy_async();  // generic reads of the slot before the refill
+          load_raw(i + NR);
+        }
+      }
       uint32_t hw[HP / 2], lw[HP / 2];
 #pragma unroll
       for (int u = 0; u < HP / 2; ++u) tc::split_f16x2(z[2 * u], z[2 * u + 1], hw[u], lw[u]);
@@ -471,6 +492,16 @@ __global__ void __launch_bounds__(kThr, 1) tc_bwd16_kernel(Bwd16Args a) {
       tc::fence_proxy_async();
       tc::mbar_arrive(&sb.zready[bz]);
       BTRACE(warp == kDW && lane == 0, 7, i);
+      // cosine factors -> buffer i % NC, row (h, k) of 16 floats, 16-B chunk c
+      // at c ^ (k / 2 % 4): 8 consecutive lanes cover all banks
+      const int cs = i % NC;
+      if (i >= NC) tc::mbar_wait(&sb.cfree[cs], ((i - NC) / NC) & 1);
+      float* cr = pc + cs * kCw + (h * BH + k) * 16;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<float4*>(cr + ((c ^ ((k >> 1) & 3)) << 2)) =
+            make_float4(cw[4 * c], cw[4 * c + 1], cw[4 * c + 2], cw[4 * c + 3]);
+      tc::mbar_arrive(&sb.cready[cs]);
     }
   } else if (warp == kMmaWarp) {
     // ---- MMA issue, in tile order: wgrad(i) then dgrad(i) ----
@@ -530,44 +561,31 @@ __global__ void __launch_bounds__(kThr, 1) tc_bwd16_kernel(Bwd16Args a) {
     const int e = warp - kMmaWarp - 1;
     const int q = warp & 3, h = e >> 2, k = 32 * q + lane, pb = HP * h;
     const uint32_t lb = t0 + (static_cast<uint32_t>(32 * q) << 16);
-    const bool loader = warp == kThr / 32 - 1 && lane == 0;  // issues the loads i + NR
     const float ds = 1.f / (sw * sd);                         // D_g scale (exact)
     double gx = 0.0, gy = 0.0, gb = 0.0;
-    float w0x = 0.f, w0y = 0.f, b0k = 0.f, ymax = 0.f;
-    float2 cnext = make_float2(0.f, 0.f);
+    float ymax = 0.f;
+    float2 cnext = make_float2(0.f, 0.f);  // BOTTOM: the pixel coordinates (layer-0 gradient)
     auto load_c = [&](int i) { return a.coords[min(tile_m0(i) + pb + (lane & (HP - 1)), n - 1)]; };
-    if (BOTTOM) {
-      w0x = a.W0[2 * k];
-      w0y = a.W0[2 * k + 1];
-      b0k = a.b0[k];
-      if (my_tiles > 0) cnext = load_c(0);
-    }
+    if (BOTTOM && my_tiles > 0) cnext = load_c(0);
     for (int i = 0; i < my_tiles; ++i) {
-      const int b = i & 1, r = i % NR;
+      const int b = i & 1;
       const int m0 = tile_m0(i), rows = min(BT, n - m0);
       const float2 cme = cnext;
       if (BOTTOM && i + 1 < my_tiles) cnext = load_c(i + 1);
+      // the cosine factors of this thread's (feature, pixels) from the z producers
       float cw[HP];
-      if (BOTTOM) {
+      const int cs = i % NC;
+      tc::mbar_wait(&sb.cready[cs], (i / NC) & 1);
+      const float* cr = pc + cs * kCw + (h * BH + k) * 16;
 #pragma unroll
-        for (int t = 0; t < HP; ++t) {
-          const float av = fmaf(w0y, __shfl_sync(0xffffffffu, cme.y, t),
-                                fmaf(w0x, __shfl_sync(0xffffffffu, cme.x, t), b0k));
-          cw[t] = w0 * __cosf(sine_reduce(w0 * av));
-        }
-      } else {
-        tc::mbar_wait(&sb.rfull[r], (i / NR) & 1);
-        const float* ar = raw + r * kRaw + pb * BH + k;
-#pragma unroll
-        for (int t = 0; t < HP; ++t) cw[t] = w0 * __cosf(sine_reduce(w0 * ar[t * BH]));
-        tc::mbar_arrive(&sb.rfree[r]);
-        if (loader && i + NR < my_tiles) {
-          tc::mbar_wait(&sb.rfree[r], (i / NR) & 1);
-          tc::fence_proxy_async();  // generic reads of the slot before the refill
-          load_raw(i + NR);
-        }
+      for (int c = 0; c < 4; ++c) {
+        const float4 f = *reinterpret_cast<const float4*>(cr + ((c ^ ((k >> 1) & 3)) << 2));
+        cw[4 * c] = f.x;
+        cw[4 * c + 1] = f.y;
+        cw[4 * c + 2] = f.z;
+        cw[4 * c + 3] = f.w;
       }
-      __syncwarp();
+      tc::mbar_arrive(&sb.cfree[cs]);
       tc::mbar_wait(&sb.dfull[b], (i >> 1) & 1);
       BTRACE(warp == kMmaWarp + 1 && lane == 0, 10, i);
       tc::fence_after_sync();
@@ -641,7 +659,7 @@ __global__ void __launch_bounds__(kThr, 1) tc_bwd16_kernel(Bwd16Args a) {
 }
 
 constexpr size_t kBwd16Smem =
-    1024 + sizeof(float) * (ND * kPlane + NZ * kZPlane + (NX + NR) * kRaw + 22 * BH + 16);
+    1024 + sizeof(float) * (ND * kPlane + NZ * kZPlane + (NX + NR) * kRaw + NC * kCw + 22 * BH + 16);
 static_assert(kBwd16Smem <= 227 * 1024, "tc_bwd16_kernel: shared memory budget");
 // W is staged [BH][BH + 1] over the planes and the raw dA_l slots (filled after it)
 static_assert(ND * kPlane + NZ * kZPlane + NX * kRaw >= BH * (BH + 1), "tc_bwd16_kernel: W staging");

@@ -32,13 +32,18 @@ tr.step(1)
 torch.cuda.synchronize()
 fn(buf.ctypes.data, 0)
 t0 = buf[buf > 0].min()
-names = {1: "dA xfull", 12: "dA hi-ld", 14: "dA comp", 3: "dA tfree", 4: "dA tready", 13: "dA lo-st",
-         2: "dA gready", 5: "z rfull", 6: "z wfree", 11: "z stored", 7: "z zready", 8: "mma w-issue",
-         9: "mma g-issue", 10: "epi dfull"}
+F16 = os.environ.get("BWD16", "1") == "1"
+if F16:  # siren_bwd16.cu tags
+    names = {1: "dA xfull", 12: "dA read", 14: "dA split", 13: "dA pfree", 2: "dA gready", 5: "z rfull",
+             6: "z zfree", 7: "z zready", 8: "mma w-issue", 9: "mma g-issue", 10: "epi dfull"}
+else:
+    names = {1: "dA xfull", 12: "dA hi-ld", 14: "dA comp", 3: "dA tfree", 4: "dA tready", 13: "dA lo-st",
+             2: "dA gready", 5: "z rfull", 6: "z wfree", 11: "z stored", 7: "z zready", 8: "mma w-issue",
+             9: "mma g-issue", 10: "epi dfull"}
 ntile = int((buf[1] > 0).sum())
 print("tiles", ntile)
 rel = np.where(buf > 0, (buf.astype(np.int64) - int(t0)), -1)
-order = [1, 12, 14, 3, 4, 13, 2, 5, 6, 11, 7, 8, 9, 10]
+order = [1, 12, 14, 13, 2, 5, 6, 7, 8, 9, 10] if F16 else [1, 12, 14, 3, 4, 13, 2, 5, 6, 11, 7, 8, 9, 10]
 print("tile " + " ".join(f"{names[t]:>11s}" for t in order))
 for i in list(range(0, 8)) + list(range(20, 26)) + list(range(ntile - 3, ntile)):
     print(f"{i:4d} " + " ".join(f"{rel[t, i]:11d}" for t in order))
@@ -46,10 +51,14 @@ for i in list(range(0, 8)) + list(range(20, 26)) + list(range(ntile - 3, ntile))
 lo, hi = 10, ntile - 5
 per = (rel[1, hi] - rel[1, lo]) / (hi - lo)
 print("period ns/tile", per)
-for a, b in [(1, 12), (12, 14), (14, 3), (3, 4), (4, 13), (13, 2), (5, 6), (6, 11), (11, 7), (4, 8), (7, 8), (8, 9), (9, 10)]:
+pairs = ([(1, 12), (12, 14), (14, 13), (13, 2), (5, 6), (6, 7), (2, 8), (7, 8), (8, 9), (9, 10)] if F16 else
+         [(1, 12), (12, 14), (14, 3), (3, 4), (4, 13), (13, 2), (5, 6), (6, 11), (11, 7), (4, 8), (7, 8), (8, 9), (9, 10)])
+for a, b in pairs:
     print(f"{names[a]:>11s} -> {names[b]:>11s}: {np.mean(rel[b, lo:hi] - rel[a, lo:hi]):8.1f} ns")
-# cross-tile: tfree wait of tile i vs mma w-issue of tile i-1
-print("w-issue(i-1) -> tfree(i):", np.mean(rel[3, lo + 1:hi] - rel[8, lo:hi - 1]))
-print("w-issue(i-1) -> wfree(i):", np.mean(rel[6, lo + 1:hi] - rel[8, lo:hi - 1]))
+# cross-tile gaps
+print("gready(i-1) -> xfull(i):", np.mean(rel[1, lo + 1:hi] - rel[2, lo:hi - 1]))
+print("zready(i-1) -> rfull(i):", np.mean(rel[5, lo + 1:hi] - rel[7, lo:hi - 1]))
+print("g-issue(i-1) -> w-issue(i):", np.mean(rel[8, lo + 1:hi] - rel[9, lo:hi - 1]))
+print("dfull(i-1) -> dfull(i):", np.mean(rel[10, lo + 1:hi] - rel[10, lo:hi - 1]))
 tr.close()
 ctx.close()
