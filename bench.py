@@ -529,13 +529,17 @@ def run_ours(args):
     }
     traffic = load_traffic()
     sr = stage_rl["siren_fwd+bwd"]
-    # the SIREN GEMMs run on the tensor cores in 3xTF32 (three TF32 MMAs per
-    # fp32-accurate product): the ceiling is a third of the dense TF32 rate,
-    # half the measured dense bf16 rate
+    # the width-128 SIREN GEMMs (forward chain and fused backward) run on the
+    # tensor cores with split-fp16 operands (three kind::f16 MMAs per
+    # fp32-accurate product): the ceiling is a third of the dense 16-bit rate
+    # (= the measured bf16 rate); 3xTF32 (the PACT_SIREN_F16=0 /
+    # PACT_SIREN_BWD_F16=0 variants, and cfg5's width-256 layers) is half that
+    f16x3 = bf16 / 3.0
     tf32x3 = bf16 / 2.0 / 3.0
     sr["bf16_dense_peak_tflops"] = bf16
+    sr["tensor_split_f16_peak_tflops"] = f16x3
+    sr["frac_of_split_f16_tensor"] = sr["achieved_tflops"] / f16x3
     sr["tensor_3xtf32_peak_tflops"] = tf32x3
-    sr["frac_of_3xtf32_tensor"] = sr["achieved_tflops"] / tf32x3
     sr["fp32_pipe_peak_tflops"] = FP32_PEAK_TFLOPS  # the SIMT path's ceiling, for reference
     # The roofline line is for the dominant kernel.  Since the ray adjoint
     # became a gather (round 2) the SIREN is the largest stage; its forward is
@@ -545,7 +549,6 @@ def run_ours(args):
     # fp32-accurate product at the dense 16-bit rate (= the measured bf16
     # rate), i.e. a third of it.  The ray stages are L1/texture-served (their
     # 16 B/step model exceeds HBM) and are reported per stage.
-    f16x3 = bf16 / 3.0
     fwd_flops = work["siren_flops"] / 3.0  # 2 FLOP per MAC, forward only
     fwd_ach = fwd_flops / (stages["siren_fwd"] * 1e-3) / 1e12
     roofline = {"bound": "tensor", "achieved": fwd_ach, "peak": f16x3, "unit": "TFLOP/s",
@@ -556,17 +559,17 @@ def run_ours(args):
                 "work_model": "SURVEY 8(d): 2 FLOP per MAC of the 2->128x4->1 network per masked "
                               "pixel (fp32-equivalent FLOPs)",
                 "traffic_source": traffic.get("_source")}
-    # SURVEY 8(d) iteration roofline: sum_k max(B_k / HBM, F_k / peak_k), SIREN at 3xTF32
+    # SURVEY 8(d) iteration roofline: sum_k max(B_k / HBM, F_k / peak_k), SIREN at split fp16
     # the loss reads half of Y since round 2b (the real stack's Hermitian
     # spectrum): its model bytes stay the full read, like SURVEY 8(d)
-    model_ms = 1e3 * (fwd_flops / (f16x3 * 1e12) + (work["siren_flops"] - fwd_flops) / (tf32x3 * 1e12)
+    model_ms = 1e3 * (work["siren_flops"] / (f16x3 * 1e12)
                       + (work["wavefront_bytes"] + work["ray_backward_bytes"]
                          + work["fused_loss_bytes"]) / (hbm * 1e9))
     iter_ms = sum(v["ms"] for v in stage_rl.values())
     iteration_roofline = {"model_ms": model_ms, "measured_ms": iter_ms, "frac": model_ms / iter_ms,
-                          "model": "SURVEY 8(d): SIREN forward F at the split-fp16 tensor rate "
-                                   "(measured dense bf16 / 3), backward F at the 3xTF32 rate "
-                                   "(bf16 / 6), ray and loss algorithmic bytes at measured HBM; "
+                          "model": "SURVEY 8(d): SIREN forward and backward F at the split-fp16 "
+                                   "tensor rate (measured dense bf16 / 3), ray and loss "
+                                   "algorithmic bytes at measured HBM; "
                                    "measured = sum of stage CUDA-event times of one frame. frac > 1: "
                                    "the ray stages are L1/texture-served, below their HBM byte model"}
 
