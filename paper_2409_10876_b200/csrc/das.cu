@@ -356,11 +356,26 @@ Status das_stack_device(pact_ctx* ctx, const pact_ring& ring, const pact_signal_
     // Split the transducer range so the launch covers >= 2 waves of CTAs.
     // The split (and so the partial-sum order) follows the FULL grid's tile
     // count, so a row band's pixels are bit-identical to the full stack's.
-    int want = div_up(2 * ctx->num_sms * 2, full_tiles);
-    int max_split = div_up(N, chunk);
-    int nsplit = std::max(1, std::min(want, max_split));
-    int per = div_up(div_up(N, nsplit), chunk) * chunk;
-    nsplit = div_up(N, per);
+    // Among the splits from there up, take the first whose CTA count fills
+    // its last wave of resident CTAs (>= 95 %; else the fullest): cfg3's 1024
+    // tiles are 2.3 waves of 3 x 148 CTAs unsplit, 6.9 waves split in three.
+    const int want = div_up(2 * ctx->num_sms * 2, full_tiles);
+    const int max_split = div_up(N, chunk);
+    const double slots = static_cast<double>(ctx->num_sms) * (KBsel <= 32 ? 3 : 2);
+    int nsplit = 1, per = N;
+    double best = -1.0;
+    for (int s = std::max(1, std::min(want, max_split)); s <= std::min(want + 5, max_split); ++s) {
+      int p = div_up(div_up(N, s), chunk) * chunk;
+      int ns = div_up(N, p);
+      double waves = static_cast<double>(full_tiles) * ns / slots;
+      double fill = waves / std::ceil(waves);
+      if (fill > best + 1e-9) {
+        best = fill;
+        nsplit = ns;
+        per = p;
+      }
+      if (fill >= 0.95) break;
+    }
     a.tx_per_split = per;
     float* dst = out + static_cast<size_t>(jb) * plane;
     void* part = nullptr;
