@@ -519,6 +519,7 @@ __device__ __forceinline__ Regimes rec_regimes(const RayRec& r) {
   return {r.i_side, r.i_corner, (r.flags & kRecXFirst) != 0};
 }
 
+template <bool kSeries>
 __global__ void __launch_bounds__(256, WF_MINB) wavefront_plan_kernel(RayArgs a) {
   extern __shared__ float s_border[];
   const Border bd = load_border(a, s_border);
@@ -545,13 +546,50 @@ __global__ void __launch_bounds__(256, WF_MINB) wavefront_plan_kernel(RayArgs a)
       // border line: one loop for both orientations; the line is a slice of
       // the smem border
       const SideLine sl = side_line(rec_regimes(rr), rec_pixels(rr), W, H);
+      if (kSeries) {
+        // Run by run: inside one border cell d is linear in the step index,
+        // d_i = dm + beta k about the run's centre, v_i = vm (1 + u k), and
+        //   sum_i d_i / v_i = (dm n - v0 (u^2 S2 + u^4 S4)) / vm,  S2 = sum k^2, S4 = sum k^4
+        // (odd power sums vanish; |u k| <= |c1 - c0| / (2 vm); u^6 dropped:
+        // < 1e-6 of the sum while |u| n <= 0.2, else the steps are summed).
+        // A step on a cell boundary may count for either cell: d is continuous.
+        const float adf = fabsf(sl.df);
+        const float rdf = adf > 0.f ? rcp_approx(adf) : 0.f;
+        int i = lo;
+        while (i < hi) {
+          const float f = fmaf(static_cast<float>(i), sl.df, sl.fs);
+          const int q = min(static_cast<int>(f), sl.qmax);
+          const float fa = f - q;
+          const float room = sl.df > 0.f ? 1.f - fa : fa;  // to the cell's far boundary
+          // steps left in the cell, >= 1 (the conversion saturates; NaN -> 0)
+          const int n = adf > 0.f ? min(static_cast<int>(fmaxf(room, 0.f) * rdf), hi - i - 1) + 1 : hi - i;
+          const float nf = static_cast<float>(n);
+          const float c0 = s_border[sl.off + q], dc = s_border[sl.off + q + 1] - c0;
+          const float dm = fmaf(fmaf(0.5f * (nf - 1.f), sl.df, fa), dc, c0);
+          const float rv = rcp_approx(v0 + dm);
+          const float u = dc * sl.df * rv;
+          if (fabsf(u) * nf <= 0.2f) {
+            const float n2 = nf * nf, u2 = u * u;
+            const float S2 = nf * (n2 - 1.f) * (1.f / 12.f);
+            const float S4 = S2 * fmaf(3.f, n2, -7.f) * (1.f / 20.f);
+            acc = fmaf(rv, fmaf(dm, nf, -v0 * u2 * fmaf(u2, S4, S2)), acc);
+          } else {
+            for (int j = i; j < i + n; ++j) {
+              const float d = fmaf(fmaf(static_cast<float>(j), sl.df, sl.fs) - q, dc, c0);
+              acc += d * rcp_approx(v0 + d);
+            }
+          }
+          i += n;
+        }
+      } else {
 #pragma unroll 4
-      for (int i = lo; i < hi; ++i) {
-        const float f = fmaf(static_cast<float>(i), sl.df, sl.fs);
-        const int q = min(static_cast<int>(f), sl.qmax);
-        const float c0 = s_border[sl.off + q];
-        const float d = fmaf(f - q, s_border[sl.off + q + 1] - c0, c0);
-        acc += d * rcp_approx(v0 + d);
+        for (int i = lo; i < hi; ++i) {
+          const float f = fmaf(static_cast<float>(i), sl.df, sl.fs);
+          const int q = min(static_cast<int>(f), sl.qmax);
+          const float c0 = s_border[sl.off + q];
+          const float d = fmaf(f - q, s_border[sl.off + q + 1] - c0, c0);
+          acc += d * rcp_approx(v0 + d);
+        }
       }
     } else {
       acc = march_forward_generic<true>(a, bd, rec_pixels(rr), rr.n, v0);
@@ -1008,6 +1046,7 @@ __global__ void __launch_bounds__(kCellThreads, CELL_MINB) cell_gather_kernel(Ra
 // no carry they cost about the same per step, and a ray's sum stays whole.)
 constexpr int kSideThreads = 256;
 constexpr int kSideMaxRun = 255;
+constexpr int kSideBatch = 4;  // runs per thread whose loads are in flight together
 
 __device__ __forceinline__ int side_range(const RayRec& q, int& i1) {
   const bool ok = q.n > 0 && !(q.flags & kRecGeneric);
@@ -1062,6 +1101,7 @@ __device__ __forceinline__ int border_pixel(int s, int W, int H) {
 
 // One block per border cell (slot): cell_out[slot] = the cell's two pixel
 // sums (lower, upper) in the fixed-point quantum.
+template <bool kSideSeries>
 __global__ void __launch_bounds__(kSideThreads) side_gather_kernel(RayArgs a, const float* __restrict__ gsc,
                                                                    const unsigned long long* __restrict__ stats,
                                                                    unsigned long long* __restrict__ cell_out) {
@@ -1076,25 +1116,70 @@ __global__ void __launch_bounds__(kSideThreads) side_gather_kernel(RayArgs a, co
   const float dc = c1 - c0, fq = static_cast<float>(q), v0 = static_cast<float>(a.v0);
   const float scale = ldexpf(1.f, fix_exponent(stats, a.step, a.v0, max_steps_total(a)));
   long long s0 = 0, s1 = 0;
-  for (unsigned k = e0 + threadIdx.x; k < e1; k += kSideThreads) {
-    const unsigned long long e = __ldg(a.side_ent + k);
-    const int r = static_cast<int>((e >> 20) & 0xfffffu), i0 = static_cast<int>((e >> 8) & 0xfffu);
-    const int cnt = kSideMaxRun - static_cast<int>((e >> 40) & 0xffu);
-    const float g = __ldg(gsc + r);
-    if (g == 0.f) continue;  // aberration.hpp:340
-    const float2 geo = __ldg(a.side_geo + r);
-    // the per-ray border-line march's arithmetic (ray_backward_plan_kernel)
-    float b0 = 0.f, b1 = 0.f;
-    for (int i = i0; i < i0 + cnt; ++i) {
-      const float fa = fmaf(static_cast<float>(i), geo.y, geo.x) - fq;
-      const float v = v0 + fmaf(fa, dc, c0);
-      const float gv = g * rcp_approx(v * v);
-      const float g1 = gv * fa;
-      b0 += gv - g1;
-      b1 += g1;
+  // kSideBatch runs per thread in flight: the entries, then the rays' scales
+  // and lines (scattered L2 gathers), then the arithmetic
+  for (unsigned k = e0 + threadIdx.x; k < e1; k += kSideThreads * kSideBatch) {
+    unsigned long long ent[kSideBatch];
+    float gs[kSideBatch];
+    float2 geos[kSideBatch];
+#pragma unroll
+    for (int t = 0; t < kSideBatch; ++t) {
+      const unsigned kk = k + t * kSideThreads;
+      ent[t] = kk < e1 ? __ldg(a.side_ent + kk) : 0ull;
     }
-    s0 += __float2ll_rn(b0 * scale);
-    s1 += __float2ll_rn(b1 * scale);
+#pragma unroll
+    for (int t = 0; t < kSideBatch; ++t) {
+      const unsigned kk = k + t * kSideThreads;
+      const int r = static_cast<int>((ent[t] >> 20) & 0xfffffu);
+      gs[t] = kk < e1 ? __ldg(gsc + r) : 0.f;
+      geos[t] = __ldg(a.side_geo + r);
+    }
+#pragma unroll
+    for (int t = 0; t < kSideBatch; ++t) {
+      const unsigned long long e = ent[t];
+      const int i0 = static_cast<int>((e >> 8) & 0xfffu);
+      const int cnt = kSideMaxRun - static_cast<int>((e >> 40) & 0xffu);
+      const float g = gs[t];
+      if (g == 0.f) continue;  // aberration.hpp:340
+      const float2 geo = geos[t];
+      float b0 = 0.f, b1 = 0.f;
+      // Inside one border cell v is linear in the step index: v_i = vm (1 + u k),
+      // k = i - (the run's centre), so the run's two deposits
+      //   sum_i g / v_i^2 (1 - fa_i),  sum_i g / v_i^2 fa_i        (fa_i = fam + k geo.y)
+      // are power series in u k with the odd power sums gone by symmetry:
+      //   sum 1/v_i^2 = (n + 3 u^2 S2 + 5 u^4 S4) / vm^2,  S2 = sum k^2, S4 = sum k^4
+      //   sum k/v_i^2 = -(2 u S2 + 4 u^3 S4) / vm^2
+      // |u k| <= |c1 - c0| / (2 vm) (a run stays in its cell), so the u^6 term
+      // dropped is < 1e-6 of the sum while |u| n <= 0.2; beyond that (a field
+      // with a > 20 % jump between border neighbours) the steps are summed.
+      const float nf = static_cast<float>(cnt);
+      const float ic = static_cast<float>(i0) + 0.5f * (nf - 1.f);
+      const float fam = fmaf(ic, geo.y, geo.x - fq);
+      const float rv = rcp_approx(v0 + fmaf(fam, dc, c0));
+      const float u = dc * geo.y * rv;
+      if (kSideSeries && fabsf(u) * nf <= 0.2f) {
+        const float n2 = nf * nf, u2 = u * u;
+        const float S2 = nf * (n2 - 1.f) * (1.f / 12.f);
+        const float S4 = S2 * fmaf(3.f, n2, -7.f) * (1.f / 20.f);
+        const float T0 = fmaf(u2, fmaf(5.f * u2, S4, 3.f * S2), nf);
+        const float T1 = -u * fmaf(4.f * u2, S4, 2.f * S2);
+        const float gr = g * rv * rv;
+        b1 = gr * fmaf(geo.y, T1, fam * T0);
+        b0 = fmaf(gr, T0, -b1);
+      } else {
+        // the per-ray border-line march's arithmetic (ray_backward_plan_kernel)
+        for (int i = i0; i < i0 + cnt; ++i) {
+          const float fa = fmaf(static_cast<float>(i), geo.y, geo.x) - fq;
+          const float v = v0 + fmaf(fa, dc, c0);
+          const float gv = g * rcp_approx(v * v);
+          const float g1 = gv * fa;
+          b0 += gv - g1;
+          b1 += g1;
+        }
+      }
+      s0 += __float2ll_rn(b0 * scale);
+      s1 += __float2ll_rn(b1 * scale);
+    }
   }
   // integer block sums: exact, so the order does not matter
   __shared__ long long r0[kSideThreads / 32], r1[kSideThreads / 32];
@@ -1464,6 +1549,16 @@ bool side_enabled() {
   return on;
 }
 
+// PACT_SIDE_SERIES=0: the border cells' runs summed step by step (the A/B
+// reference of the closed-form run sums in side_gather_kernel).
+bool side_series_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PACT_SIDE_SERIES");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // The side plan (see side_gather_kernel): every run of every ray's border-line
 // steps, keyed (slot, length, ray, first step) and radix-sorted.  Skipped
 // (the adjoint's side items stay per ray) when a field does not fit or
@@ -1745,8 +1840,13 @@ Status launch_wavefront(pact_ctx* ctx, const RayArgs& a, float* w) {
     // (the forward keeps its border-line items: without a carry they are as
     // cheap per step as the side gather, and a ray's sum stays in one place)
     if (a.n_items > 0) {
-      PACT_TRY_S(smem_optin(wavefront_plan_kernel, smem));
-      wavefront_plan_kernel<<<div_up(a.n_items, kPlanBlock), kPlanBlock, smem, ctx->stream>>>(a);
+      if (side_series_enabled()) {
+        PACT_TRY_S(smem_optin(wavefront_plan_kernel<true>, smem));
+        wavefront_plan_kernel<true><<<div_up(a.n_items, kPlanBlock), kPlanBlock, smem, ctx->stream>>>(a);
+      } else {
+        PACT_TRY_S(smem_optin(wavefront_plan_kernel<false>, smem));
+        wavefront_plan_kernel<false><<<div_up(a.n_items, kPlanBlock), kPlanBlock, smem, ctx->stream>>>(a);
+      }
       PACT_TRY_S(after_launch(ctx, "wavefront_plan_kernel"));
     }
     ray_finish_kernel<<<div_up(a.n_rays, 256), 256, 0, ctx->stream>>>(a, w);
@@ -1820,7 +1920,10 @@ Status launch_ray_backward(pact_ctx* ctx, const RayArgs& a, const float* dw, dou
       PACT_TRY_S(after_launch(ctx, "cell_gather_kernel"));
     }
     if (side) {
-      side_gather_kernel<<<n_slots, kSideThreads, 0, ctx->stream>>>(a, gsc, stats, side_cells);
+      if (side_series_enabled())
+        side_gather_kernel<true><<<n_slots, kSideThreads, 0, ctx->stream>>>(a, gsc, stats, side_cells);
+      else
+        side_gather_kernel<false><<<n_slots, kSideThreads, 0, ctx->stream>>>(a, gsc, stats, side_cells);
       PACT_TRY_S(after_launch(ctx, "side_gather_kernel"));
       corner_adjoint_kernel<<<div_up(a.n_rays, 256), 256, 0, ctx->stream>>>(a, gsc, stats, rep);
       PACT_TRY_S(after_launch(ctx, "corner_adjoint_kernel"));

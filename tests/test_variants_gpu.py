@@ -69,3 +69,8 @@ def test_cell_gather_and_f16_chain_vs_replaced_variants(tmp_path):
     e_g3 = _rel(prod["grad"], bwd32["grad"])
     print(f"split fp16 vs 3xTF32 backward: grad {e_g3:.2e}")
     assert e_g3 <= 1e-5
+    # closed-form run sums vs step sums in the border-cell gather
+    steps = _step(tmp_path, "side_steps", {"PACT_SIDE_SERIES": "0"})
+    e_w4, e_gv4, e_g4 = (_rel(prod[k], steps[k]) for k in ("w", "gv", "grad"))
+    print(f"run series vs step sums: w {e_w4:.2e} dL/dv {e_gv4:.2e} grad {e_g4:.2e}")
+    assert e_w4 <= 1e-6 and e_gv4 <= 1e-5 and e_g4 <= 1e-5
