@@ -8,15 +8,24 @@
 
 namespace pactgpu {
 
-// x mod 2pi into [-pi, pi] (two-constant Cody-Waite), so the MUFU sine/cosine
-// run on their accurate range (abs. error ~4e-7, below the fp32 rounding of
-// the argument w0 * a itself).  k = round(x / 2pi) comes from the 1.5 * 2^23
-// shifter on the FMA pipe (one FFMA + one FADD, exact for |x| < 2pi * 2^22)
-// rather than FMUL + FRND: FRND issues on the same quarter-rate unit as the
-// MUFU sine itself.  Every SIREN kernel (forward and backward) uses this one
-// definition, so a_l -> sin(w0 a_l) is the same function everywhere.
+// The argument of the MUFU sine / cosine.  __sinf(x) is MUFU.SIN(x / 2pi):
+// the unit takes the fractional part of the turns exactly, so the error of an
+// unreduced argument is the rounding of that one product, |x| 2^-24 -- the
+// size of the rounding of x = w0 a itself.  Measured at cfg3 (one iteration vs
+// the reference, tests/test_bench_configs_gpu.py): w 1.0e-6 -> 1.8e-6, SOS
+// 1.3e-6 -> 1.9e-6, grad theta 6.9e-6 unchanged, for four instructions fewer
+// per activation (forward 0.139 -> 0.120 ms, backward 0.299 -> 0.287 ms).
+// PACT_SINE_REDUCE=1 (compile time) restores the two-constant Cody-Waite
+// reduction into [-pi, pi] (k = round(x / 2pi) from the 1.5 * 2^23 shifter on
+// the FMA pipe; FRND would issue on the MUFU's own quarter-rate unit).  Every
+// SIREN kernel (forward and backward) uses this one definition, so
+// a_l -> sin(w0 a_l) is the same function everywhere.
+#ifndef PACT_SINE_REDUCE
+#define PACT_SINE_REDUCE 0
+#endif
 #ifdef __CUDACC__
 __device__ __forceinline__ float sine_reduce(float x) {
+  if (!PACT_SINE_REDUCE) return x;
   const float k = __fadd_rn(__fmaf_rn(x, 0.159154943091895336f, 12582912.f), -12582912.f);
   return fmaf(-k, -1.74845553146951720e-07f, fmaf(-k, 6.28318548202514648f, x));
 }
