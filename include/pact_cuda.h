@@ -528,9 +528,14 @@ int pact_joint_reconstruct(pact_ctx* ctx, const pact_ring* ring, const pact_sign
  * run concurrently on one GPU (one engine stream per frame; every frame's
  * epoch is enqueued before the reports are read).  Results are identical to
  * n_frames separate pact_joint_reconstruct calls.
- *   signals[f]: device fp32 [N][T];  cfgs[f]: per-frame TrainConfig (equal epochs)
+ *   signals[f]: fp32 [N][T], device or HOST memory;  cfgs[f]: per-frame TrainConfig (equal epochs)
  *   reports: HOST double[n_frames][epochs][4] (wall_s = the batch's epoch time)
- *   images[f], sos[f]: device fp32 [H][W] (arrays may be NULL)
+ *   images[f], sos[f]: fp32 [H][W], device or HOST memory (arrays may be NULL)
+ * Host signals / outputs (here, in pact_joint_reconstruct and in
+ * pact_trainer_create / pact_trainer_finish) are staged by the engine on the
+ * frame's own stream: pinned host memory keeps the copies asynchronous and
+ * lets them overlap the other frames' compute; host outputs are complete
+ * once the context stream is synchronised.
  *   thetas: HOST fp64 [n_frames][P] (may be NULL) */
 int pact_joint_reconstruct_batch(pact_ctx* ctx, int32_t n_frames, const pact_ring* ring,
                                  const pact_signal_meta* meta, const float* const* signals,

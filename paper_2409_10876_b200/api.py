@@ -789,12 +789,22 @@ def joint_reconstruct_batch(ctx: Context, signals: list, ring: RingGeometry, met
                             images: list | None = None, sos: list | None = None):
     """pact_joint_reconstruct_batch: joint_reconstruct of several frames of one
     geometry run concurrently (one engine stream each); identical results to
-    separate joint_reconstruct calls.  -> (reports [n, epochs, 4], images, sos, thetas)."""
+    separate joint_reconstruct calls.  `signals`, `images` and `sos` may be CUDA or
+    host tensors (pinned host memory keeps the library's per-frame copies
+    asynchronous; synchronise before reading host outputs).
+    -> (reports [n, epochs, 4], images, sos, thetas)."""
     n = len(signals)
     assert len(cfgs) == n and n > 0
     cs = [c.c() for c in cfgs]  # keep each delays array alive
     carr = (_abi.TrainConfig * n)(*[c for c, _ in cs])
+    # CUDA tensors, or host tensors (pinned: asynchronous) staged by the library
     sigs = [s.contiguous() for s in signals]
+    for s in sigs:
+        assert s.dtype == torch.float32 and s.numel() == ring.n_transducers * meta.n_samples, \
+            "signals: fp32 [N, T] expected"
+    for t in (images or []) + (sos or []):
+        assert t.dtype == torch.float32 and t.is_contiguous() and \
+            t.numel() == grid.width * grid.height, "images / sos: contiguous fp32 [H, W] expected"
     sig_p = (C.c_void_p * n)(*[s.data_ptr() for s in sigs])
     if images is None:
         images = [torch.empty((grid.height, grid.width), device="cuda", dtype=torch.float32)

@@ -109,6 +109,9 @@ T* ctx_ext(pact_ctx* ctx, int slot) {
 // threshold is raised on first use: buffers freed by one trainer / entry point
 // are reused by the next without cudaMalloc / cudaFree (which synchronise the
 // device and, for GB-sized arenas, can stall for many milliseconds).
+// True for host memory (pinned or pageable): the engine entry points stage
+// such inputs / outputs themselves.  NULL and device / managed pointers: false.
+bool is_host_pointer(const void* p);
 Status pool_alloc(void** ptr, size_t bytes, cudaStream_t stream);
 void pool_free(void* ptr, cudaStream_t stream);
 

@@ -37,6 +37,16 @@ void pool_free(void* ptr, cudaStream_t stream) {
   if (ptr) cudaFreeAsync(ptr, stream);
 }
 
+bool is_host_pointer(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, p) != cudaSuccess) {
+    cudaGetLastError();  // (not a CUDA pointer on old drivers: treat as pageable host)
+    return true;
+  }
+  return pa.type == cudaMemoryTypeHost || pa.type == cudaMemoryTypeUnregistered;
+}
+
 Status smem_optin_raw(const void* func, size_t bytes) {
   // (no small-size shortcut: a kernel with static shared memory needs the
   // opt-in even when its dynamic part is <= 48 KB)

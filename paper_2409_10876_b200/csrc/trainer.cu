@@ -549,8 +549,26 @@ static int trainer_create(pact_ctx* ctx, const pact_ring* ring, const pact_signa
   TRY_ST(fourier_table(e, tr->ftab, tr->P, grid->pitch, tr->A, tr->delays.data(), tr->K));
   trace.mark("fourier table");
   // DAS stack + spectra, once (optimize.hpp:380-392)
-  TRY_ST(das_stack_device(e, *ring, *meta, signals, *grid, v0, tr->delays.data(), tr->K,
-                          tr->stack, tr->row0, tr->rows));
+  // host signals (pinned: asynchronous) are uploaded on the engine's own
+  // stream, so a batch's frames overlap their copies with each other's compute
+  const float* dsig = signals;
+  void* staged = nullptr;
+  if (is_host_pointer(signals)) {
+    const size_t nb = sizeof(float) * static_cast<size_t>(ring->n_transducers) * meta->n_samples;
+    TRY_ST(pool_alloc(&staged, nb, s));
+    cudaError_t ce2 = cudaMemcpyAsync(staged, signals, nb, cudaMemcpyHostToDevice, s);
+    if (ce2 != cudaSuccess) {
+      pool_free(staged, s);
+      return fail(cuda_status(ce2, "signals H2D").code);
+    }
+    dsig = static_cast<const float*>(staged);
+  }
+  {
+    Status sd = das_stack_device(e, *ring, *meta, dsig, *grid, v0, tr->delays.data(), tr->K,
+                                 tr->stack, tr->row0, tr->rows);
+    if (staged) pool_free(staged, s);
+    if (sd.code) return fail(sd.code);
+  }
   TRY_ST(launch_patch_fft(e, tr->lay, tr->stack, tr->K, tr->Y, tr->p_lo, tr->p_hi, tr->row0,
                           tr->rows));
   trace.mark("DAS + FFT launched");
@@ -694,12 +712,29 @@ int pact_trainer_finish(pact_trainer* tr, float* image, float* sos) {
                        &tmp));
   float2* X = static_cast<float2*>(tmp);
   float* patches = reinterpret_cast<float*>(X + tr->n_patches * P2);
+  // host outputs (pinned: asynchronous) are written through a pooled device
+  // buffer and copied back on the engine stream
+  auto emit = [&](float* dst, auto&& produce) -> int {
+    if (!is_host_pointer(dst)) return produce(dst);
+    void* dev = nullptr;
+    PACT_TRY(pool_alloc(&dev, sizeof(float) * npx, e->stream));
+    int rc = produce(static_cast<float*>(dev));
+    if (!rc && cudaMemcpyAsync(dst, dev, sizeof(float) * npx, cudaMemcpyDeviceToHost,
+                               e->stream) != cudaSuccess)
+      rc = cuda_status(cudaGetLastError(), "output D2H").code;  // (message set)
+    pool_free(dev, e->stream);
+    return rc;
+  };
   if (image) {
     PACT_TRY(launch_wiener(e, tr->ftab.tab, tr->Y, tr->w, tr->n_patches, tr->cfg.eps_deconv, X));
     PACT_TRY(launch_patch_ifft_real(e, tr->P, tr->n_patches, X, patches));
-    PACT_TRY(launch_merge(e, tr->lay, patches, tr->win, image));
+    int rc = emit(image, [&](float* d) { return launch_merge(e, tr->lay, patches, tr->win, d).code; });
+    if (rc) return rc;
   }
-  if (sos) PACT_TRY(launch_sos_from_dev(e, tr->dv, npx, tr->v0, sos));
+  if (sos) {
+    int rc = emit(sos, [&](float* d) { return launch_sos_from_dev(e, tr->dv, npx, tr->v0, d).code; });
+    if (rc) return rc;
+  }
   // outputs visible on the caller's stream
   cudaEvent_t ev;
   cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
@@ -913,9 +948,14 @@ int pact_joint_reconstruct_batch(pact_ctx* ctx, int32_t n_frames, const pact_rin
       }
     }
   }
+  // every frame's final render + deconvolution is enqueued before any theta
+  // read waits on a frame
   for (int f = 0; f < n_frames; ++f) {
     int rc = pact_trainer_finish(trs[f], images ? images[f] : nullptr, sos ? sos[f] : nullptr);
-    if (!rc && thetas) rc = pact_trainer_get_theta(trs[f], thetas + static_cast<size_t>(f) * n_params);
+    if (rc) return cleanup(rc);
+  }
+  for (int f = 0; thetas && f < n_frames; ++f) {
+    int rc = pact_trainer_get_theta(trs[f], thetas + static_cast<size_t>(f) * n_params);
     if (rc) return cleanup(rc);
   }
   return cleanup(PACT_OK);

@@ -204,3 +204,29 @@ def test_batched_joint_reconstruct_equals_separate_calls(ctx, G, si):
         assert np.array_equal(reps[f][:, :3], r[:, :3])
         assert torch.equal(imgs[f], img) and torch.equal(soss[f], sos)
         assert np.array_equal(ths[f], th)
+
+
+def test_batched_joint_reconstruct_with_host_buffers(ctx, G, si):
+    """Pinned host signals and outputs (staged by the engine on each frame's
+    stream) give the results of the device-buffer call bitwise."""
+    from paper_2409_10876_b200.api import joint_reconstruct_batch
+
+    cfgs = [replace(si.cfg, epochs=2, steps_per_epoch=1, seed=s) for s in (5, 7)]
+    sig = torch.as_tensor(G["sig"])
+    dev = joint_reconstruct_batch(ctx, [sig.cuda(), sig.cuda()], si.ring, _meta(G), si.grid, si.mask,
+                                  cfgs)
+    hsig = [sig.clone().pin_memory() for _ in cfgs]
+    himg = [torch.zeros((si.grid.height, si.grid.width), dtype=torch.float32).pin_memory()
+            for _ in cfgs]
+    hsos = [torch.zeros_like(t).pin_memory() for t in himg]
+    reps, _, _, ths = joint_reconstruct_batch(ctx, hsig, si.ring, _meta(G), si.grid, si.mask, cfgs,
+                                              images=himg, sos=hsos)
+    torch.cuda.synchronize()
+    assert np.array_equal(reps[:, :, :3], dev[0][:, :, :3]) and np.array_equal(ths, dev[3])
+    for f in range(len(cfgs)):
+        assert torch.equal(himg[f], dev[1][f].cpu()) and torch.equal(hsos[f], dev[2][f].cpu())
+    # pageable host signals work too (a synchronous staged copy)
+    r2 = joint_reconstruct_batch(ctx, [sig.clone(), sig.clone()], si.ring, _meta(G), si.grid,
+                                 si.mask, cfgs)
+    assert torch.equal(r2[1][0], dev[1][0]) and np.array_equal(r2[3], dev[3])
+
