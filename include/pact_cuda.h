@@ -525,8 +525,9 @@ int pact_joint_reconstruct(pact_ctx* ctx, const pact_ring* ring, const pact_sign
                            float* sos, double* theta);
 
 /* joint_reconstruct of n_frames independent frames of one geometry (cfg4),
- * run concurrently on one GPU (one engine stream per frame; every frame's
- * epoch is enqueued before the reports are read).  Results are identical to
+ * run concurrently on one GPU (one engine stream per frame; a frame's first
+ * epoch is enqueued when it is created and each next epoch as soon as its
+ * report is read, so no frame waits for another).  Results are identical to
  * n_frames separate pact_joint_reconstruct calls.
  *   signals[f]: fp32 [N][T], device or HOST memory;  cfgs[f]: per-frame TrainConfig (equal epochs)
  *   reports: HOST double[n_frames][epochs][4] (wall_s = the batch's epoch time)

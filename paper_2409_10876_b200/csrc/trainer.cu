@@ -923,21 +923,25 @@ int pact_joint_reconstruct_batch(pact_ctx* ctx, int32_t n_frames, const pact_rin
     const pact_partition whole{0, 1};
     int rc = trainer_create(ctx, ring, meta, signals[f], grid, mask, &cfgs[f], &whole, &trs[f],
                             false);
+    // the frame's first epoch is enqueued at once: its iterations run while
+    // the host prepares the next frames
+    if (!rc) rc = pact_trainer_step(trs[f], trs[f]->cfg.steps_per_epoch);
     if (rc) return cleanup(rc);
   }
   int n_params = 0;
   if (n_frames > 0) n_params = trs[0]->n_params;
+  auto t0 = std::chrono::steady_clock::now();
   for (int e = 1; e <= epochs; ++e) {
-    auto t0 = std::chrono::steady_clock::now();
-    // every frame's steps are enqueued before any report waits: the frames
-    // run concurrently, one engine stream each
-    for (int f = 0; f < n_frames; ++f) {
-      int rc = pact_trainer_step(trs[f], trs[f]->cfg.steps_per_epoch);
-      if (rc) return cleanup(rc);
-    }
+    // a frame's next epoch (after the last: its final render + deconvolution)
+    // is enqueued as soon as its report is read, so the other frames' streams
+    // keep the GPU busy across the host round trip
     for (int f = 0; f < n_frames; ++f) {
       double rep[3];
       int rc = pact_trainer_report(trs[f], e, rep);
+      if (!rc)
+        rc = e < epochs ? pact_trainer_step(trs[f], trs[f]->cfg.steps_per_epoch)
+                        : pact_trainer_finish(trs[f], images ? images[f] : nullptr,
+                                              sos ? sos[f] : nullptr);
       if (rc) return cleanup(rc);
       if (reports) {
         double* r = reports + (static_cast<size_t>(f) * epochs + (e - 1)) * 4;
@@ -947,13 +951,10 @@ int pact_joint_reconstruct_batch(pact_ctx* ctx, int32_t n_frames, const pact_rin
         r[3] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       }
     }
+    t0 = std::chrono::steady_clock::now();
   }
-  // every frame's final render + deconvolution is enqueued before any theta
-  // read waits on a frame
-  for (int f = 0; f < n_frames; ++f) {
-    int rc = pact_trainer_finish(trs[f], images ? images[f] : nullptr, sos ? sos[f] : nullptr);
-    if (rc) return cleanup(rc);
-  }
+  // every frame's final render + deconvolution was enqueued with its last
+  // report, before any theta read waits on a frame
   for (int f = 0; thetas && f < n_frames; ++f) {
     int rc = pact_trainer_get_theta(trs[f], thetas + static_cast<size_t>(f) * n_params);
     if (rc) return cleanup(rc);
