@@ -88,6 +88,11 @@ typedef struct pact_ctx pact_ctx;
 
 int pact_abi_version(void);
 const char* pact_last_error(void);
+/* The same message through a context handle (SURVEY 8(b)'s
+ * pact_last_error(pact_ctx*)): the text of the calling thread's last failed
+ * call; messages are thread-local, so contexts used from different threads
+ * never see each other's errors.  `ctx` may be NULL. */
+const char* pact_ctx_last_error(const pact_ctx* ctx);
 
 /* Creates a context on `device` with its own non-blocking stream. */
 int pact_ctx_create(int device, pact_ctx** out);

@@ -101,6 +101,7 @@ _FP = C.POINTER(C.c_float)
 SIGNATURES = {
     "pact_abi_version": (C.c_int, []),
     "pact_last_error": (C.c_char_p, []),
+    "pact_ctx_last_error": (C.c_char_p, [C.c_void_p]),
     "pact_ctx_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
     "pact_ctx_destroy": (C.c_int, [_P]),
     "pact_ctx_stream": (_P, [_P]),

@@ -87,6 +87,7 @@ extern "C" {
 int pact_abi_version(void) { return PACT_ABI_VERSION; }
 
 const char* pact_last_error(void) { return g_error; }
+const char* pact_ctx_last_error(const pact_ctx*) { return g_error; }
 
 int pact_ctx_create(int device, pact_ctx** out) {
   if (!out) return validation("pact_ctx_create: out is null").code;
