@@ -123,3 +123,37 @@ def test_iteration_wide_network(ctx, G, W, hidden, fixture):
     print(f"cfg2 / H={hidden} grad rel L2", err)
     assert err <= 1e-3
     tr.close()
+
+
+def test_border_runs_on_a_rough_field(ctx, W):
+    """The closed-form border-line runs (raymarch.cu: forward items and the
+    border-cell gather) near their validity limit and past it.  cfg2's ring
+    (60 mm) lies outside its 25.6 mm grid, so every ray ends in the
+    border-line regime.  A field with jumps of up to ~25 % between
+    neighbouring pixels makes |u| n exceed 0.2 on the long runs (those are
+    summed step by step) and leaves the others with |u k| ~ 0.1, where the
+    dropped u^6 term is ~1e-6.  Wavefront and adjoint of nine patches against
+    the oracle (aberration.hpp:134-186, 333-361)."""
+    from oracle_lib import orc
+
+    lay = make_patch_layout(W.grid, W.patch_mm, W.overlap)
+    cen = np.asarray(lay.centers).reshape(-1, 2)[::6][:9].copy()
+    rng = np.random.default_rng(11)
+    Hh, Ww = W.grid.height, W.grid.width
+    dev = torch.as_tensor(rng.uniform(-180.0, 180.0, (Hh, Ww)).astype(np.float32)).cuda()
+    sos32 = W.v0 + dev.double().cpu().numpy()
+    w = ctx.wavefront(W.ring, W.grid, dev, W.v0, W.mask, cen, W.n_angles, W.ray_step)
+    want_w = orc().wavefront_profile(cen, W.ring, W.grid, sos32, W.v0, W.mask, W.n_angles,
+                                     W.ray_step)
+    e_w = rel_l2(w.double().cpu().numpy(), want_w)
+    dw32 = rng.standard_normal(want_w.shape).astype(np.float32)
+    gv = ctx.ray_backward(W.ring, W.grid, dev, W.v0, W.mask, cen, W.n_angles, W.ray_step,
+                          torch.as_tensor(dw32).cuda())
+    want_g = np.zeros((Hh, Ww))
+    for p, c in enumerate(cen):
+        want_g = orc().wavefront_grad_trace(c, W.ring, W.grid, sos32, W.v0, W.mask, W.n_angles,
+                                            W.ray_step, dw32[p].astype(np.float64), want_g)
+    e_g = rel_l2(gv.cpu().numpy().reshape(Hh, Ww), want_g)
+    print(f"rough field: w {e_w:.2e} dL/dv {e_g:.2e}")
+    assert e_w <= 1e-5 and e_g <= 1e-5
+

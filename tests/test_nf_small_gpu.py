@@ -229,4 +229,3 @@ def test_batched_joint_reconstruct_with_host_buffers(ctx, G, si):
     r2 = joint_reconstruct_batch(ctx, [sig.clone(), sig.clone()], si.ring, _meta(G), si.grid,
                                  si.mask, cfgs)
     assert torch.equal(r2[1][0], dev[1][0]) and np.array_equal(r2[3], dev[3])
-
