@@ -1097,6 +1097,11 @@ __global__ void __launch_bounds__(kFinishAngles) loss_finish_kernel(
 
 // X = sum_j conj(H_j) Y_j / (sum_j |H_j|^2 + eps M), 0 where den == 0
 // (multichannel_deconvolve, deconv.hpp:78-96), H from the wavefront profile.
+// HALF: the patch stack is real, so Y(-k) = conj Y(k), H(-k) = conj H(k) (as in
+// the fused loss) and the estimate X is Hermitian: only the bins of rows
+// 0 .. P/2 are evaluated (half of Y's traffic) and rows 1 .. P/2 - 1 also
+// store conj X at -k (rows 0 and P/2 hold their own mirrors).
+template <bool HALF>
 __global__ void wiener_kernel(FourierTab t, const float2* __restrict__ Y_all,
                               const float* __restrict__ w_all, float eps_m,
                               float2* __restrict__ X_all) {
@@ -1105,7 +1110,7 @@ __global__ void wiener_kernel(FourierTab t, const float2* __restrict__ Y_all,
   for (int a = threadIdx.x; a < t.A; a += blockDim.x) s_w[a] = w_all[patch * t.A + a];
   __syncthreads();
   int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= t.P2) return;
+  if (b >= (HALF ? (t.P / 2 + 1) * t.P : t.P2)) return;
   float2 e1b, e2b, e1m = {}, e2m = {};
   bin_phases(t, s_w, b, e1b, e2b);
   int m = t.mirror[b];
@@ -1113,15 +1118,21 @@ __global__ void wiener_kernel(FourierTab t, const float2* __restrict__ Y_all,
   const float2* Y = Y_all + static_cast<size_t>(patch) * t.K * t.P2;
   float2 num = make_float2(0.f, 0.f);
   float den = eps_m;
+#pragma unroll 4
   for (int j = 0; j < t.K; ++j) {
     float2 h = h_sym(t, j, b, m, e1b, e2b, e1m, e2m);
-    float2 c = cmulc(h, Y[j * t.P2 + b]);
+    float2 c = cmulc(h, __ldcs(Y + static_cast<size_t>(j) * t.P2 + b));
     num.x += c.x;
     num.y += c.y;
     den += h.x * h.x + h.y * h.y;
   }
-  X_all[static_cast<size_t>(patch) * t.P2 + b] =
-      den > 0.f ? make_float2(num.x / den, num.y / den) : make_float2(0.f, 0.f);
+  const float2 x = den > 0.f ? make_float2(num.x / den, num.y / den) : make_float2(0.f, 0.f);
+  float2* X = X_all + static_cast<size_t>(patch) * t.P2;
+  X[b] = x;
+  if (HALF) {
+    const int by = b / t.P, bx = b - by * t.P;
+    if (by >= 1 && by < t.P / 2) X[(t.P - by) * t.P + (t.P - bx) % t.P] = make_float2(x.x, -x.y);
+  }
 }
 
 }  // namespace
@@ -1220,9 +1231,19 @@ Status launch_loss_grad(pact_ctx* ctx, const FourierTab& t, const float2* Y, con
 
 Status launch_wiener(pact_ctx* ctx, const FourierTab& t, const float2* Y, const float* w,
                      int n_patches, double eps, float2* X) {
-  dim3 g(div_up(t.P2, 256), n_patches);
-  wiener_kernel<<<g, 256, t.A * sizeof(float), ctx->stream>>>(t, Y, w,
-                                                              static_cast<float>(eps * t.K), X);
+  // PACT_WIENER_FULL=1: every bin evaluated (the A/B reference of the half spectrum)
+  static const bool full = [] {
+    const char* e = std::getenv("PACT_WIENER_FULL");
+    return e && e[0] == '1';
+  }();
+  const float eps_m = static_cast<float>(eps * t.K);
+  if (!full && t.P % 2 == 0) {
+    dim3 g(div_up((t.P / 2 + 1) * t.P, 256), n_patches);
+    wiener_kernel<true><<<g, 256, t.A * sizeof(float), ctx->stream>>>(t, Y, w, eps_m, X);
+  } else {
+    dim3 g(div_up(t.P2, 256), n_patches);
+    wiener_kernel<false><<<g, 256, t.A * sizeof(float), ctx->stream>>>(t, Y, w, eps_m, X);
+  }
   return after_launch(ctx, "wiener_kernel");
 }
 
