@@ -985,13 +985,17 @@ __global__ void __launch_bounds__(kCellThreads, CELL_MINB) cell_gather_kernel(Ra
     const float fcx = static_cast<float>(ccx), fcy = static_cast<float>(ccy);
     const int c = tile * T * T + lc;
     const unsigned e0 = live ? a.cell_start[c] : 0u, e1 = live ? a.cell_start[c + 1] : 0u;
-    float r00 = 0.f, r01 = 0.f, r10 = 0.f, r11 = 0.f;
-    // software pipeline: the next batch of entries loads while this one runs
+    // the four moments of the cell's deposits f = g / v^2 (the corner sums
+    // follow from them after the loop: five instructions per step, not eight)
+    float F = 0.f, Fx = 0.f, Fy = 0.f, Fxy = 0.f;
+    // software pipeline: the next batch of entries loads while this one runs.
+    // Lanes past the list re-read its last entry with g = 0: every lane
+    // evaluates a real step of this cell (v > 0), so f needs no guard.
     unsigned nx[kCellBatch];
 #pragma unroll
     for (int u = 0; u < kCellBatch; ++u) {
       const unsigned q = e0 + l16 + LPC * u;
-      nx[u] = q < e1 ? __ldg(a.cell_ent + q) : 0u;
+      nx[u] = e1 > e0 ? __ldg(a.cell_ent + min(q, e1 - 1u)) : 0u;
     }
     for (unsigned e = e0 + l16; e < e1; e += LPC * kCellBatch) {
       unsigned en[kCellBatch];
@@ -999,30 +1003,32 @@ __global__ void __launch_bounds__(kCellThreads, CELL_MINB) cell_gather_kernel(Ra
       for (int u = 0; u < kCellBatch; ++u) {
         en[u] = nx[u];
         const unsigned q = e + LPC * (kCellBatch + u);
-        nx[u] = q < e1 ? __ldg(a.cell_ent + q) : 0u;
+        nx[u] = __ldg(a.cell_ent + min(q, e1 - 1u));
       }
 #pragma unroll
       for (int u = 0; u < kCellBatch; ++u) {
-        // the per-ray march's interior_d / deposit arithmetic, operand for operand
+        // the per-ray march's interior_d arithmetic, operand for operand
         const unsigned j = en[u] >> sb;
         const float4 geo = s_geo[j];
-        const float g = e + LPC * u < e1 ? s_g[j] : 0.f;  // 0: rays the reference skips (aberration.hpp:340)
+        const float g = e + LPC * u < e1 ? s_g[j] : 0.f;  // (0 too for rays the reference skips, aberration.hpp:340)
         const float fi = static_cast<float>(en[u] & smask);
         const float ax = fmaf(fi, geo.z, geo.x) - fcx, ay = fmaf(fi, geo.w, geo.y) - fcy;
         const float top = fmaf(ax, dtop, q00), bot = fmaf(ax, dbot, q10);
         const float v = v0 + fmaf(ay, bot - top, top);
-        const float f = g != 0.f ? g * rcp_approx(v * v) : 0.f;
-        const float fy1 = f * ay, fy0 = f - fy1;  // f (1 - ay), f ay
-        r00 = fmaf(-fy0, ax, r00 + fy0);
-        r01 = fmaf(fy0, ax, r01);
-        r10 = fmaf(-fy1, ax, r10 + fy1);
-        r11 = fmaf(fy1, ax, r11);
+        const float f = g * rcp_approx(v * v);
+        const float fy = f * ay;
+        F += f;
+        Fy += fy;
+        Fx = fmaf(f, ax, Fx);
+        Fxy = fmaf(fy, ax, Fxy);
       }
     }
-    r00 = cell_sum(r00);
-    r01 = cell_sum(r01);
-    r10 = cell_sum(r10);
-    r11 = cell_sum(r11);
+    F = cell_sum(F);
+    Fx = cell_sum(Fx);
+    Fy = cell_sum(Fy);
+    Fxy = cell_sum(Fxy);
+    // corner sums: sum f (1-ax)(1-ay), f ax (1-ay), f (1-ax) ay, f ax ay
+    const float r11 = Fxy, r10 = Fy - Fxy, r01 = Fx - Fxy, r00 = (F - Fy) - r01;
     if (live && l16 == 0) {
       unsigned long long* o = cells + 4 * static_cast<size_t>(cy * Wc + cx);
       o[0] = static_cast<unsigned long long>(__float2ll_rn(r00 * scale));

@@ -58,7 +58,7 @@ def test_cell_gather_and_f16_chain_vs_replaced_variants(tmp_path):
     assert np.array_equal(prod["w"], cells_off["w"])
     e_gv, e_g = _rel(prod["gv"], cells_off["gv"]), _rel(prod["grad"], cells_off["grad"])
     print(f"cell gather vs per-ray: dL/dv {e_gv:.2e} grad {e_g:.2e}")
-    assert e_gv <= 1e-7 and e_g <= 1e-6
+    assert e_gv <= 1e-6 and e_g <= 1e-6  # (corner sums from the cell's four fp32 moments)
     # split-fp16 chain vs 3xTF32 chain
     e_w, e_gv2, e_g2 = (_rel(prod[k], tf32[k]) for k in ("w", "gv", "grad"))
     print(f"split fp16 vs 3xTF32 forward: w {e_w:.2e} dL/dv {e_gv2:.2e} grad {e_g2:.2e}")
