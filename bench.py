@@ -576,7 +576,10 @@ def run_ours(args):
     cfg5 = None
     if not args.no_cfg5:
         torch.cuda.empty_cache()
-        cfg5 = cfg5_line(ctx, rank, world, local)
+        try:
+            cfg5 = cfg5_line(ctx, rank, world, local)
+        except Exception as e:  # the headline numbers above stand without the cfg5 extra
+            cfg5 = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
