@@ -104,7 +104,7 @@ class Clocks:
 
 def load_traffic():
     """Per-launch DRAM bytes of the hot kernels from the committed ncu capture."""
-    for name in ("traffic_r02f.json", "traffic_r02e.json", "traffic_r02d.json", "traffic_r02.json"):  # the latest committed capture
+    for name in ("traffic_r02g.json", "traffic_r02f.json", "traffic_r02e.json", "traffic_r02d.json", "traffic_r02.json"):  # the latest committed capture
         try:
             with open(os.path.join(ROOT, "profiles", name)) as f:
                 return json.load(f)
@@ -115,7 +115,7 @@ def load_traffic():
 
 def das_physical(traffic):
     """Issue / LSU / shared-memory utilisation of das_stack_kernel<32> at cfg3
-    from the committed ncu capture (profiles/traffic_r02f.json)."""
+    from the committed ncu capture (profiles/traffic_r02g.json)."""
     d = traffic.get("_das_cfg3")
     if not d:
         return None
@@ -125,7 +125,7 @@ def das_physical(traffic):
             "fma_pipe_pct": d["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"],
             "smem_ld_wavefronts": wf,
             "smem_bank_conflict_frac": d["l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum"] / wf,
-            "source": "ncu --set full, das_stack_kernel<32> at cfg3 (profiles/r02f_das_ncu_raw.csv.gz)"}
+            "source": "ncu --set full, das_stack_kernel<32> at cfg3 (profiles/r02g_das_ncu_raw.csv.gz)"}
 
 
 def dist_env():
