@@ -383,6 +383,9 @@ def cfg5_line(ctx, rank, world, local):
 
 
 def run_ours(args):
+    # a stuck run leaves the Python stacks on stderr (every 10 minutes)
+    import faulthandler
+    faulthandler.dump_traceback_later(600, repeat=True)
     import torch
     import torch.distributed as dist
 
